@@ -1,0 +1,566 @@
+/*
+ * evoke_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU oracle for the n x 73 vertex-orbit
+ * matrix of EVOKE (arXiv 1911.10616).  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this code.
+ * It shares no code, header, table or generator with the CUDA path.
+ *
+ * What it computes:
+ *   - P:139-142 (Sec. 1.1 "Problem Description"): for every vertex v and every
+ *     orbit theta, the number of times v occurs in a copy of theta; "we ask for
+ *     induced counts".
+ *   - P:366-388 (Def. "auto"): orbits = classes of the automorphism relation.
+ *   - P:400-404 ("Induced vs non-induced"): an induced copy is a vertex subset
+ *     with all its edges and non-edges.  So DIM(v,theta) = #{ U : v in U,
+ *     G[U] isomorphic to H(theta), v mapped into the orbit theta }.
+ *   - P:419-422 (Def. "unlabeled-match"): non-induced DM(v,theta) = number of
+ *     distinct (not-necessarily-induced) copies (U,F), F subset of E(G[U]),
+ *     with (U,F) isomorphic to H and v mapped into theta.  Only the tiny-graph
+ *     brute force below computes DM (used to pin the catalog to the paper's
+ *     equations and to Fig. 11).
+ *
+ * The orbit numbering (Fig. 2) is not in the text (the figure is
+ * an empty TikZ macro).  The catalog below is the reading given in DESIGN.md
+ * ("R1"), pinned by tests against the paper's printed equations (Lemma
+ * 4vertexorbit P:704-751, Thm B.1, Fig. 11) and the
+ * textual anchors P:129-146.
+ *
+ * Enumeration: ESU (exclusive-subgraph extension; each connected induced
+ * vertex set of size 2..5 produced exactly once, minimum vertex = root) and an
+ * all-subsets brute force used to pin ESU.  Counts are accumulated in wrapping
+ * uint64 (reading R20: counts are exact modulo 2^64).
+ *
+ * parity unpinned: none of the functions here -- see tests/test_oracle_*.py.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <stdio.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define NORB 73
+#define NPAT 30
+
+/* ------------------------------------------------------------------------- */
+/* Pattern catalog H0..H29 (Fig. 2 reading, R1).                    */
+/* Each pattern: k vertices, edge list, and the orbit id of every vertex.     */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int k;
+  int ne;
+  int e[10][2];
+  int orb[5];
+} pattern_t;
+
+static const pattern_t CATALOG[NPAT] = {
+  /* H0  edge                     */ {2, 1, {{0,1}}, {0,0}},
+  /* H1  path P3 (1 end, 2 mid)   */ {3, 2, {{0,1},{1,2}}, {1,2,1}},
+  /* H2  triangle                 */ {3, 3, {{0,1},{0,2},{1,2}}, {3,3,3}},
+  /* H3  path P4 (4 end, 5 mid)   */ {4, 3, {{0,1},{1,2},{2,3}}, {4,5,5,4}},
+  /* H4  claw (6 leaf, 7 centre)  */ {4, 3, {{0,1},{0,2},{0,3}}, {7,6,6,6}},
+  /* H5  4-cycle                  */ {4, 4, {{0,1},{1,2},{2,3},{3,0}}, {8,8,8,8}},
+  /* H6  paw: tail 9, tri deg2 10, centre 11 */
+  {4, 4, {{0,1},{0,2},{1,2},{0,3}}, {11,10,10,9}},
+  /* H7  diamond: off-chord 12, chord 13 */
+  {4, 5, {{0,1},{0,2},{0,3},{1,2},{1,3}}, {13,13,12,12}},
+  /* H8  K4                       */ {4, 6, {{0,1},{0,2},{0,3},{1,2},{1,3},{2,3}}, {14,14,14,14}},
+  /* H9  path P5: 15 end, 16 next, 17 centre */
+  {5, 4, {{0,1},{1,2},{2,3},{3,4}}, {15,16,17,16,15}},
+  /* H10 chair: 18 long-arm end, 19 short leaves, 20 long-arm middle, 21 centre */
+  {5, 4, {{0,1},{0,2},{0,3},{3,4}}, {21,19,19,20,18}},
+  /* H11 star K1,4: 22 leaf, 23 centre */
+  {5, 4, {{0,1},{0,2},{0,3},{0,4}}, {23,22,22,22,22}},
+  /* H12 bull: 24 pendants, 25 apex, 26 pendant-bearing triangle vertices */
+  {5, 5, {{0,1},{0,2},{1,2},{1,3},{2,4}}, {25,26,26,24,24}},
+  /* H13 triangle + 2-path: 27 end, 28 path middle, 29 tri deg2, 30 attach */
+  {5, 5, {{0,1},{0,2},{1,2},{2,3},{3,4}}, {29,29,30,28,27}},
+  /* H14 cricket: 31 pendants, 32 tri deg2, 33 centre */
+  {5, 5, {{0,1},{0,2},{1,2},{0,3},{0,4}}, {33,32,32,31,31}},
+  /* H15 5-cycle                  */ {5, 5, {{0,1},{1,2},{2,3},{3,4},{4,0}}, {34,34,34,34,34}},
+  /* H16 banner (C4 + pendant): 35 pendant, 36 opposite, 37 adjacent, 38 attach */
+  {5, 5, {{0,1},{1,2},{2,3},{3,0},{0,4}}, {38,37,36,37,35}},
+  /* H17 diamond + pendant on chord vertex: 39 pendant, 40 off-chord, 41 chord, 42 attach */
+  {5, 6, {{0,1},{0,2},{0,3},{1,2},{1,3},{0,4}}, {42,41,40,40,39}},
+  /* H18 bowtie: 43 wings, 44 centre */
+  {5, 6, {{0,1},{0,2},{1,2},{0,3},{0,4},{3,4}}, {44,43,43,43,43}},
+  /* H19 diamond + pendant on off-chord vertex: 45 pendant, 46 free off-chord, 47 attach, 48 chord */
+  {5, 6, {{0,1},{0,2},{0,3},{1,2},{1,3},{2,4}}, {48,48,47,46,45}},
+  /* H20 K2,3: 49 degree-2 side, 50 degree-3 side */
+  {5, 6, {{0,2},{0,3},{0,4},{1,2},{1,3},{1,4}}, {50,50,49,49,49}},
+  /* H21 house: 51 floor, 52 roof, 53 eaves */
+  {5, 6, {{0,1},{1,2},{2,3},{3,0},{4,0},{4,1}}, {53,53,51,51,52}},
+  /* H22 book K1,1,3: 54 pages, 55 spine */
+  {5, 7, {{0,1},{0,2},{0,3},{0,4},{1,2},{1,3},{1,4}}, {55,55,54,54,54}},
+  /* H23 K4 + pendant: 56 pendant, 57 free K4 vertices, 58 attach */
+  {5, 7, {{0,1},{0,2},{0,3},{1,2},{1,3},{2,3},{0,4}}, {58,57,57,57,56}},
+  /* H24 gem (P4 + hub): 59 path ends, 60 path middles, 61 hub */
+  {5, 7, {{0,1},{1,2},{2,3},{4,0},{4,1},{4,2},{4,3}}, {59,60,60,59,61}},
+  /* H25 K2,3 + edge in the 3-side: 62 degree 2, 63 non-adjacent deg 3, 64 adjacent deg 3 */
+  {5, 7, {{0,2},{0,3},{0,4},{1,2},{1,3},{1,4},{2,3}}, {63,63,64,64,62}},
+  /* H26 K4 + degree-2 vertex: 65 degree 2, 66 degree 3, 67 degree 4 */
+  {5, 8, {{0,1},{0,2},{0,3},{1,2},{1,3},{2,3},{4,0},{4,1}}, {67,67,66,66,65}},
+  /* H27 wheel W4: 68 rim, 69 hub */
+  {5, 8, {{0,1},{1,2},{2,3},{3,0},{4,0},{4,1},{4,2},{4,3}}, {68,68,68,68,69}},
+  /* H28 K5 minus edge (3,4): 70 degree 3, 71 degree 4 */
+  {5, 9, {{0,1},{0,2},{0,3},{0,4},{1,2},{1,3},{1,4},{2,3},{2,4}}, {71,71,71,70,70}},
+  /* H29 K5                       */
+  {5, 10, {{0,1},{0,2},{0,3},{0,4},{1,2},{1,3},{1,4},{2,3},{2,4},{3,4}}, {72,72,72,72,72}},
+};
+
+/* bit index of position pair (i,j), i<j: pairs ordered (0,1),(0,2),(1,2),(0,3),... */
+static inline int pair_bit(int i, int j) {
+  if (i > j) { int t = i; i = j; j = t; }
+  return j * (j - 1) / 2 + i;
+}
+
+/* Lookup tables: for k = 2..5 and every mask over the C(k,2) position pairs,
+ * orbit id per position (or -1 if the mask is not a connected spanning graph). */
+static signed char TABLE2[1 << 1][2];
+static signed char TABLE3[1 << 3][3];
+static signed char TABLE4[1 << 6][4];
+static signed char TABLE5[1 << 10][5];
+static int g_tables_ready = 0;
+
+static signed char *table_row(int k, int mask) {
+  switch (k) {
+    case 2: return TABLE2[mask];
+    case 3: return TABLE3[mask];
+    case 4: return TABLE4[mask];
+    default: return TABLE5[mask];
+  }
+}
+
+static int mask_connected(int k, int mask) {
+  int seen = 1, frontier = 1;
+  while (frontier) {
+    int nf = 0;
+    for (int a = 0; a < k; a++) {
+      if (!(frontier >> a & 1)) continue;
+      for (int b = 0; b < k; b++) {
+        if (a == b) continue;
+        if ((mask >> pair_bit(a, b) & 1) && !(seen >> b & 1)) { seen |= 1 << b; nf |= 1 << b; }
+      }
+    }
+    frontier = nf;
+  }
+  return seen == (1 << k) - 1;
+}
+
+static int popcount_i(int x) { int c = 0; while (x) { c += x & 1; x >>= 1; } return c; }
+
+/* next permutation (lexicographic) of p[0..k-1]; returns 0 after the last */
+static int next_perm(int *p, int k) {
+  int i = k - 2;
+  while (i >= 0 && p[i] > p[i + 1]) i--;
+  if (i < 0) return 0;
+  int j = k - 1;
+  while (p[j] < p[i]) j--;
+  int t = p[i]; p[i] = p[j]; p[j] = t;
+  for (int a = i + 1, b = k - 1; a < b; a++, b--) { t = p[a]; p[a] = p[b]; p[b] = t; }
+  return 1;
+}
+
+static int pattern_mask(const pattern_t *P, const int *perm) {
+  /* mask obtained by placing pattern vertex a at position perm[a] */
+  int m = 0;
+  for (int e = 0; e < P->ne; e++) m |= 1 << pair_bit(perm[P->e[e][0]], perm[P->e[e][1]]);
+  return m;
+}
+
+static void build_tables(void) {
+  if (g_tables_ready) return;
+  for (int k = 2; k <= 5; k++) {
+    int npairs = k * (k - 1) / 2;
+    for (int mask = 0; mask < (1 << npairs); mask++) {
+      signed char *row = table_row(k, mask);
+      for (int i = 0; i < k; i++) row[i] = -1;
+      if (!mask_connected(k, mask)) continue;
+      for (int p = 0; p < NPAT && row[0] < 0; p++) {
+        const pattern_t *P = &CATALOG[p];
+        if (P->k != k || P->ne != popcount_i(mask)) continue;
+        int perm[5] = {0, 1, 2, 3, 4};
+        do {
+          if (pattern_mask(P, perm) == mask) {
+            for (int a = 0; a < k; a++) row[perm[a]] = (signed char)P->orb[a];
+            break;
+          }
+        } while (next_perm(perm, k));
+      }
+    }
+  }
+  g_tables_ready = 1;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Catalog self-description (used by tests to pin the catalog).              */
+/* ------------------------------------------------------------------------- */
+int oracle_num_patterns(void) { return NPAT; }
+
+/* Writes k, ne, edges (2*ne ints), orbit per vertex (k ints). */
+int oracle_pattern(int p, int *k, int *ne, int *edges, int *orb) {
+  if (p < 0 || p >= NPAT) return -1;
+  const pattern_t *P = &CATALOG[p];
+  *k = P->k; *ne = P->ne;
+  for (int e = 0; e < P->ne; e++) { edges[2 * e] = P->e[e][0]; edges[2 * e + 1] = P->e[e][1]; }
+  for (int a = 0; a < P->k; a++) orb[a] = P->orb[a];
+  return 0;
+}
+
+/* Automorphism classes by exhaustive permutation (Def. "auto").
+ * cls[a] = smallest vertex b such that some automorphism maps a to b. */
+int oracle_automorphism_classes(int p, int *cls, int *num_aut) {
+  if (p < 0 || p >= NPAT) return -1;
+  const pattern_t *P = &CATALOG[p];
+  int k = P->k, ident[5] = {0, 1, 2, 3, 4};
+  int base = pattern_mask(P, ident);
+  for (int a = 0; a < k; a++) cls[a] = a;
+  int perm[5] = {0, 1, 2, 3, 4}, cnt = 0;
+  do {
+    if (pattern_mask(P, perm) == base) {
+      cnt++;
+      for (int a = 0; a < k; a++) if (perm[a] < cls[a]) cls[a] = perm[a];
+    }
+  } while (next_perm(perm, k));
+  *num_aut = cnt;
+  return 0;
+}
+
+/* classify a mask over k positions: writes orbit per position, returns 0 if
+ * connected spanning, -1 otherwise */
+int oracle_classify(int k, int mask, int *orb) {
+  build_tables();
+  if (k < 2 || k > 5) return -1;
+  signed char *row = table_row(k, mask);
+  if (row[0] < 0) return -1;
+  for (int i = 0; i < k; i++) orb[i] = row[i];
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Graph: cleaned simple undirected graph in sorted adjacency form.          */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n;
+  int64_t *rp;   /* n+1 */
+  int32_t *adj;  /* rp[n] */
+} graph_t;
+
+static int cmp_u64(const void *a, const void *b) {
+  uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return x < y ? -1 : x > y;
+}
+
+/* Input cleaning ("removed directions ... omitted duplicates and self
+ * loops"); ids are kept (row v = vertex v). Returns 0 or -1 on bad input. */
+static int graph_build(graph_t *g, int64_t n, int64_t m, const int32_t *edges) {
+  g->n = n; g->rp = NULL; g->adj = NULL;
+  uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(2 * m + 1));
+  if (!keys) return -1;
+  int64_t cnt = 0;
+  for (int64_t e = 0; e < m; e++) {
+    int64_t a = edges[2 * e], b = edges[2 * e + 1];
+    if (a < 0 || b < 0 || a >= n || b >= n) { free(keys); return -1; }
+    if (a == b) continue;
+    keys[cnt++] = ((uint64_t)a << 32) | (uint64_t)b;
+    keys[cnt++] = ((uint64_t)b << 32) | (uint64_t)a;
+  }
+  qsort(keys, (size_t)cnt, sizeof(uint64_t), cmp_u64);
+  int64_t u = 0;
+  for (int64_t i = 0; i < cnt; i++)
+    if (i == 0 || keys[i] != keys[i - 1]) keys[u++] = keys[i];
+  g->rp = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  g->adj = (int32_t *)malloc(sizeof(int32_t) * (size_t)(u + 1));
+  for (int64_t i = 0; i < u; i++) g->rp[(keys[i] >> 32) + 1]++;
+  for (int64_t v = 0; v < n; v++) g->rp[v + 1] += g->rp[v];
+  for (int64_t i = 0; i < u; i++) g->adj[i] = (int32_t)(keys[i] & 0xffffffffu);
+  free(keys);
+  return 0;
+}
+
+static void graph_free(graph_t *g) { free(g->rp); free(g->adj); }
+
+static int has_edge(const graph_t *g, int a, int b) {
+  int64_t lo = g->rp[a], hi = g->rp[a + 1];
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (g->adj[mid] < b) lo = mid + 1; else hi = mid;
+  }
+  return lo < g->rp[a + 1] && g->adj[lo] == b;
+}
+
+/* adjacency mask of the ordered vertex list S[0..k-1] */
+static int subset_mask(const graph_t *g, const int *S, int k) {
+  int m = 0;
+  for (int j = 1; j < k; j++)
+    for (int i = 0; i < j; i++)
+      if (has_edge(g, S[i], S[j])) m |= 1 << pair_bit(i, j);
+  return m;
+}
+
+/* credit every position of the induced subgraph S */
+static void credit(const graph_t *g, const int *S, int k, uint64_t *out) {
+  int mask = subset_mask(g, S, k);
+  signed char *row = table_row(k, mask);
+  for (int i = 0; i < k; i++) out[(int64_t)S[i] * NORB + row[i]] += 1u;
+}
+
+/* ------------------------------------------------------------------------- */
+/* ESU: every connected induced subgraph on 2..5 vertices exactly once.       */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  const graph_t *g;
+  uint64_t *out;       /* n*73 accumulator, or NULL (rooted mode)  */
+  uint64_t *row;       /* rooted mode: 73 accumulator for S[0]     */
+  int root_filter;     /* 1: only extend with ids > root            */
+  uint64_t work, cap;  /* rooted mode: number of sets, cap (0 = none) */
+  int aborted;
+} esu_ctx;
+
+static int in_set(const int *S, int k, int x) {
+  for (int i = 0; i < k; i++) if (S[i] == x) return 1;
+  return 0;
+}
+
+static int adjacent_to_set(const graph_t *g, const int *S, int k, int x) {
+  for (int i = 0; i < k; i++) if (has_edge(g, S[i], x)) return 1;
+  return 0;
+}
+
+static void esu_extend(esu_ctx *c, int *S, int k, int *ext, int next) {
+  if (c->aborted) return;
+  if (k >= 2) {
+    if (c->out) credit(c->g, S, k, c->out);
+    else {
+      int mask = subset_mask(c->g, S, k);
+      c->row[table_row(k, mask)[0]] += 1u;
+      c->work++;
+      if (c->cap && c->work >= c->cap) { c->aborted = 1; return; }
+    }
+  }
+  if (k == 5) return;
+  const graph_t *g = c->g;
+  int root = S[0];
+  /* Wernicke's ESU: pick w from the extension set; the new extension set is
+   * the rest of the old one plus the exclusive neighbours of w. */
+  while (next > 0) {
+    int w = ext[--next];
+    int ext2[4096];
+    int n2 = 0;
+    for (int i = 0; i < next; i++) ext2[n2++] = ext[i];
+    S[k] = w;
+    for (int64_t p = g->rp[w]; p < g->rp[w + 1]; p++) {
+      int u = g->adj[p];
+      if (c->root_filter && u <= root) continue;
+      if (in_set(S, k + 1, u)) continue;
+      if (adjacent_to_set(g, S, k, u)) continue;  /* u in N(S) => not exclusive */
+      if (in_set(ext2, n2, u)) continue;
+      if (n2 >= 4096) { c->aborted = 2; return; }
+      ext2[n2++] = u;
+    }
+    esu_extend(c, S, k + 1, ext2, n2);
+    if (c->aborted) return;
+  }
+}
+
+/* Induced orbit counts of all vertices by ESU over all roots.
+ * Returns 0, -1 (bad input), -2 (extension set overflow). */
+int oracle_orbits_esu(int64_t n, int64_t m, const int32_t *edges, uint64_t *out, int threads) {
+  build_tables();
+  graph_t g;
+  if (graph_build(&g, n, m, edges)) return -1;
+  memset(out, 0, sizeof(uint64_t) * (size_t)n * NORB);
+  int status = 0;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+#pragma omp parallel
+  {
+    uint64_t *acc = (uint64_t *)calloc((size_t)n * NORB, sizeof(uint64_t));
+    esu_ctx c = {&g, acc, NULL, 1, 0, 0, 0};
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t r = 0; r < n; r++) {
+      int S[5];
+      int ext[4096];
+      int ne = 0;
+      S[0] = (int)r;
+      for (int64_t p = g.rp[r]; p < g.rp[r + 1]; p++)
+        if (g.adj[p] > r) { if (ne < 4096) ext[ne++] = g.adj[p]; else c.aborted = 2; }
+      if (!c.aborted) esu_extend(&c, S, 1, ext, ne);
+    }
+#pragma omp critical
+    {
+      if (c.aborted) status = -2;
+      for (int64_t i = 0; i < n * NORB; i++) out[i] += acc[i];
+    }
+    free(acc);
+  }
+  graph_free(&g);
+  return status;
+}
+
+/* One exact row DIM(root, .) by rooted ESU (no id filter: every connected set
+ * containing root exactly once).  cap = max number of sets (0 = unlimited).
+ * Returns 0 on success, 1 if the cap was hit (row incomplete), <0 on error. */
+int oracle_orbit_row(int64_t n, int64_t m, const int32_t *edges, int64_t root,
+                     uint64_t *row, uint64_t cap) {
+  build_tables();
+  graph_t g;
+  if (root < 0 || root >= n) return -1;
+  if (graph_build(&g, n, m, edges)) return -1;
+  memset(row, 0, sizeof(uint64_t) * NORB);
+  esu_ctx c = {&g, NULL, row, 0, 0, cap, 0};
+  int S[5];
+  int ext[4096];
+  int ne = 0;
+  S[0] = (int)root;
+  for (int64_t p = g.rp[root]; p < g.rp[root + 1]; p++) {
+    if (ne >= 4096) { graph_free(&g); return -2; }
+    ext[ne++] = g.adj[p];
+  }
+  esu_extend(&c, S, 1, ext, ne);
+  graph_free(&g);
+  if (c.aborted == 2) return -2;
+  return c.aborted ? 1 : 0;
+}
+
+/* Same, for many roots (one thread per root). status[i] as oracle_orbit_row. */
+int oracle_orbit_rows(int64_t n, int64_t m, const int32_t *edges, int64_t nroots,
+                      const int64_t *roots, uint64_t *rows, int *status, uint64_t cap,
+                      int threads) {
+  build_tables();
+  graph_t g;
+  if (graph_build(&g, n, m, edges)) return -1;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < nroots; i++) {
+    int64_t root = roots[i];
+    uint64_t *row = rows + i * NORB;
+    memset(row, 0, sizeof(uint64_t) * NORB);
+    if (root < 0 || root >= n) { status[i] = -1; continue; }
+    esu_ctx c = {&g, NULL, row, 0, 0, cap, 0};
+    int S[5];
+    int ext[4096];
+    int ne = 0, bad = 0;
+    S[0] = (int)root;
+    for (int64_t p = g.rp[root]; p < g.rp[root + 1]; p++) {
+      if (ne >= 4096) { bad = 1; break; }
+      ext[ne++] = g.adj[p];
+    }
+    if (bad) { status[i] = -2; continue; }
+    esu_extend(&c, S, 1, ext, ne);
+    status[i] = c.aborted == 2 ? -2 : (c.aborted ? 1 : 0);
+  }
+  graph_free(&g);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* All-subsets brute force (pins ESU on tiny graphs): every k-subset, k=2..5, */
+/* connectivity by the mask table, credit.                                    */
+/* ------------------------------------------------------------------------- */
+int oracle_orbits_bruteforce(int64_t n, int64_t m, const int32_t *edges, uint64_t *out) {
+  build_tables();
+  graph_t g;
+  if (n > 64) return -1;
+  if (graph_build(&g, n, m, edges)) return -1;
+  memset(out, 0, sizeof(uint64_t) * (size_t)n * NORB);
+  int S[5];
+  for (int k = 2; k <= 5; k++) {
+    /* lexicographic k-subsets of 0..n-1 */
+    if (k > n) break;
+    for (int i = 0; i < k; i++) S[i] = i;
+    for (;;) {
+      int mask = subset_mask(&g, S, k);
+      signed char *row = table_row(k, mask);
+      if (row[0] >= 0)
+        for (int i = 0; i < k; i++) out[(int64_t)S[i] * NORB + row[i]] += 1u;
+      int i = k - 1;
+      while (i >= 0 && S[i] == n - k + i) i--;
+      if (i < 0) break;
+      S[i]++;
+      for (int j = i + 1; j < k; j++) S[j] = S[j - 1] + 1;
+    }
+  }
+  graph_free(&g);
+  return 0;
+}
+
+/* Non-induced brute force DM(v,theta) (Def. unlabeled-match):
+ * every k-subset U and every edge subset F of E(G[U]) that is connected and
+ * spanning on U is one distinct copy; credit its positions. Tiny graphs only. */
+int oracle_noninduced_bruteforce(int64_t n, int64_t m, const int32_t *edges, uint64_t *out) {
+  build_tables();
+  graph_t g;
+  if (n > 40) return -1;
+  if (graph_build(&g, n, m, edges)) return -1;
+  memset(out, 0, sizeof(uint64_t) * (size_t)n * NORB);
+  int S[5];
+  for (int k = 2; k <= 5; k++) {
+    if (k > n) break;
+    for (int i = 0; i < k; i++) S[i] = i;
+    for (;;) {
+      int full = subset_mask(&g, S, k);
+      /* enumerate sub-masks F of full (including full itself) */
+      for (int F = full;; F = (F - 1) & full) {
+        signed char *row = table_row(k, F);
+        if (F && row[0] >= 0)
+          for (int i = 0; i < k; i++) out[(int64_t)S[i] * NORB + row[i]] += 1u;
+        if (F == 0) break;
+      }
+      int i = k - 1;
+      while (i >= 0 && S[i] == n - k + i) i--;
+      if (i < 0) break;
+      S[i]++;
+      for (int j = i + 1; j < k; j++) S[j] = S[j - 1] + 1;
+    }
+  }
+  graph_free(&g);
+  return 0;
+}
+
+/* Simple clique / triangle totals by plain enumeration over sorted adjacency
+ * (used for whole-matrix invariants at sizes the ESU cannot reach).
+ * counts[0] = #triangles, counts[1] = #4-cliques, counts[2] = #5-cliques. */
+int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *counts, int threads) {
+  graph_t g;
+  if (graph_build(&g, n, m, edges)) return -1;
+  uint64_t t3 = 0, t4 = 0, t5 = 0;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+#pragma omp parallel for schedule(dynamic, 64) reduction(+:t3, t4, t5)
+  for (int64_t a = 0; a < n; a++) {
+    for (int64_t pb = g.rp[a]; pb < g.rp[a + 1]; pb++) {
+      int b = g.adj[pb];
+      if (b <= a) continue;
+      for (int64_t pc = pb + 1; pc < g.rp[a + 1]; pc++) {
+        int c = g.adj[pc];
+        if (!has_edge(&g, b, c)) continue;
+        t3++;
+        for (int64_t pd = pc + 1; pd < g.rp[a + 1]; pd++) {
+          int d = g.adj[pd];
+          if (!has_edge(&g, b, d) || !has_edge(&g, c, d)) continue;
+          t4++;
+          for (int64_t pe = pd + 1; pe < g.rp[a + 1]; pe++) {
+            int e = g.adj[pe];
+            if (has_edge(&g, b, e) && has_edge(&g, c, e) && has_edge(&g, d, e)) t5++;
+          }
+        }
+      }
+    }
+  }
+  counts[0] = t3; counts[1] = t4; counts[2] = t5;
+  graph_free(&g);
+  return 0;
+}
