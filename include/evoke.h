@@ -1,0 +1,119 @@
+/*
+ * evoke.h -- C ABI of the B200-native EVOKE vertex-orbit counter (arXiv 1911.10616).
+ *
+ * Operation (Sec. 1.1 "Problem Description"): for a simple
+ * undirected graph G and every vertex v and every orbit theta of the
+ * 30 connected patterns on 2..5 vertices (Fig. 2; numbering = DESIGN.md
+ * reading R1), output the number of times v occurs in a copy of theta: 73 counts per
+ * vertex.  Induced counts by default ("we ask for induced counts"); non-induced
+ * DM (Def. "unlabeled-match") on request.  The induced vector is
+ * obtained from the non-induced one per vertex by DIM = A^-1 DM (Appendix A,
+ * P:1103-1112).
+ *
+ * Method: degeneracy orientation G-> (any total order gives
+ * identical counts), directed enumerations (triangles, 4-/5-cliques by out-
+ * neighbourhood bitmaps, wedge pair tables, diamonds, the 5-cycle theorem P:866-886)
+ * feeding the equations of Lemma 4vertexorbit, Lemma 4edgeorbit
+ * and Theorem B.1, all on the GPU.
+ *
+ * Integer semantics: every count is the exact count modulo 2^64 (R20).
+ *
+ * Threading: calls are independent; one call uses one CUDA device (the current one,
+ * or opt->device) and the given stream.  No pointer is retained after return.
+ */
+#ifndef EVOKE_H_
+#define EVOKE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EVOKE_NUM_ORBITS 73
+
+enum {
+  EVOKE_OK = 0,
+  EVOKE_EINVAL = -1,    /* bad argument: n<0, m<0, n >= 2^31, null pointer with a
+                           non-zero size, vertex id outside [0,n), malformed CSR,
+                           shard_index outside [0,num_shards)                      */
+  EVOKE_ENOMEM = -2,    /* device allocation failed                                */
+  EVOKE_ECUDA = -3,     /* any other CUDA runtime error (message: evoke_last_error) */
+  EVOKE_EINTERNAL = -5, /* an internal invariant failed (e.g. graph too large:
+                           m >= 2^31 undirected edges)                             */
+};
+
+/* Optional per-call statistics (filled if opt->stats != NULL). Times in ms measured
+ * with CUDA events on the call's stream. */
+typedef struct evoke_stats {
+  int64_t n, m;                 /* vertices, undirected edges after cleaning        */
+  int64_t triangles;            /* #triangles                                        */
+  int64_t max_degree;           /* d_max                                             */
+  int64_t degeneracy;           /* max out-degree of the degeneracy orientation      */
+  int64_t wedges;               /* W(G) = sum_v C(d(v),2)                            */
+  double ms_total;              /* whole call (device work, incl. H2D/D2H copies)    */
+  double ms_pass[16];           /* per pass, see evoke_pass_name()                   */
+  int32_t num_passes;
+  int32_t kernel_launches;      /* kernels this library launched in the call         */
+} evoke_stats;
+
+typedef struct evoke_options {
+  uint32_t struct_size;   /* sizeof(evoke_options): ABI versioning; 0 = defaults   */
+  int32_t induced;        /* 1 (default): induced counts DIM; 0: non-induced DM      */
+  int32_t device_pointers;/* 1: edges / rowptr / col / out are device pointers on the
+                             call's device; 0 (default): host pointers              */
+  int32_t shard_index;    /* 0..num_shards-1                                         */
+  int32_t num_shards;     /* 1 (default): whole result.  >1: this call returns the
+                             shard's partial matrix; the element-wise sum mod 2^64 of
+                             the partials of all shards equals the full result bit
+                             for bit (multi-GPU data parallelism)         */
+  int32_t device;         /* CUDA device ordinal; -1 (default) = current device      */
+  void* stream;           /* cudaStream_t to run on; NULL = a library-owned stream   */
+  evoke_stats* stats;     /* optional output                                         */
+} evoke_options;
+
+/* Fill *opt with defaults (induced, host pointers, one shard, current device). */
+void evoke_default_options(evoke_options* opt);
+
+/*
+ * evoke_orbits_edges -- orbit counts from an edge list.
+ *   n      number of vertices; row v of the output is vertex v (ids are not compacted;
+ *          ids never mentioned get an all-zero row) (R21)
+ *   m      number of input pairs
+ *   edges  int32[2*m], pair e = (edges[2e], edges[2e+1]); any order; reverse and exact
+ *          duplicates collapse, self-loops are dropped
+ *   out    uint64[n*73], row-major: out[v*73 + j] = count of orbit j at vertex v;
+ *          caller-owned; written only on success (EVOKE_OK)
+ *   opt    NULL for defaults
+ * Host pointers are copied to the device inside the call (the copies are part of the
+ * call); with device_pointers=1 no host transfer happens.  Returns EVOKE_OK or a
+ * negative code; on error `out` is untouched and evoke_last_error() has a message.
+ */
+int evoke_orbits_edges(int64_t n, int64_t m, const int32_t* edges, uint64_t* out,
+                       const evoke_options* opt);
+
+/*
+ * evoke_orbits_csr -- same, from a CSR: rowptr int64[n+1] (non-decreasing, rowptr[0]=0),
+ * col int32[rowptr[n]].  The CSR need not be symmetric or sorted: every (v, col[k]) is an
+ * undirected edge, cleaned as above.
+ */
+int evoke_orbits_csr(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t* out,
+                     const evoke_options* opt);
+
+/* Static name of pass i of evoke_stats.ms_pass (NULL if out of range). */
+const char* evoke_pass_name(int i);
+
+/* Static text of an error code. */
+const char* evoke_strerror(int code);
+
+/* Thread-local detail of the last failure in this thread ("" if none). */
+const char* evoke_last_error(void);
+
+/* Library version string. */
+const char* evoke_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EVOKE_H_ */

@@ -1,0 +1,193 @@
+"""B200-native EVOKE: n x 73 vertex-orbit counts for all connected 2..5-vertex patterns.
+
+Thin Python binding over the C ABI in ``include/evoke.h`` (``libevoke.so`` built from
+``csrc/`` for sm_100a).  This module only marshals arguments: every step of the counted
+method runs in the CUDA kernels of the library.  There is no CPU fallback -- if the
+shared library is missing the import of a binding function raises.
+
+    evoke_orbits_edges(n, edges, ...)   -> uint64[n, 73]
+    evoke_orbits_csr(n, rowptr, col, ...) -> uint64[n, 73]
+
+Inputs may be numpy arrays (host pointers; the library copies them to the GPU inside the
+call) or CUDA torch tensors (device pointers; no host transfer).  ``num_shards`` /
+``shard_index`` select a data-parallel shard: the element-wise sum (mod 2^64) of the
+partial matrices of all shards equals the full result (see ``parallel.py``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+NUM_ORBITS = 73
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libevoke.so")
+
+EVOKE_OK, EVOKE_EINVAL, EVOKE_ENOMEM, EVOKE_ECUDA, EVOKE_EINTERNAL = 0, -1, -2, -3, -5
+
+
+class EvokeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"evoke error {code}: {msg}")
+        self.code = code
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("triangles", ctypes.c_int64),
+                ("max_degree", ctypes.c_int64), ("degeneracy", ctypes.c_int64), ("wedges", ctypes.c_int64),
+                ("ms_total", ctypes.c_double), ("ms_pass", ctypes.c_double * 16),
+                ("num_passes", ctypes.c_int32), ("kernel_launches", ctypes.c_int32)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("induced", ctypes.c_int32),
+                ("device_pointers", ctypes.c_int32), ("shard_index", ctypes.c_int32),
+                ("num_shards", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("stats", ctypes.POINTER(_Stats))]
+
+
+_lock = threading.Lock()
+_lib = None
+
+EXPORTED_SYMBOLS = ("evoke_default_options", "evoke_orbits_edges", "evoke_orbits_csr", "evoke_pass_name",
+                    "evoke_strerror", "evoke_last_error", "evoke_version")
+
+
+def lib():
+    """Load libevoke.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; "
+                                  f"g.build()'` (nvcc, sm_100a)")
+            L = ctypes.CDLL(LIB_PATH)
+            L.evoke_default_options.argtypes = [ctypes.POINTER(_Options)]
+            L.evoke_orbits_edges.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.POINTER(_Options)]
+            L.evoke_orbits_edges.restype = ctypes.c_int
+            L.evoke_orbits_csr.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.POINTER(_Options)]
+            L.evoke_orbits_csr.restype = ctypes.c_int
+            for f in ("evoke_pass_name",):
+                getattr(L, f).argtypes = [ctypes.c_int]
+                getattr(L, f).restype = ctypes.c_char_p
+            L.evoke_strerror.argtypes = [ctypes.c_int]
+            L.evoke_strerror.restype = ctypes.c_char_p
+            L.evoke_last_error.restype = ctypes.c_char_p
+            L.evoke_version.restype = ctypes.c_char_p
+            _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().evoke_version().decode()
+
+
+def pass_names() -> list[str]:
+    L = lib()
+    out = []
+    i = 0
+    while True:
+        s = L.evoke_pass_name(i)
+        if s is None:
+            break
+        out.append(s.decode())
+        i += 1
+    return out
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _make_options(induced, device_pointers, shard_index, num_shards, device, stream, stats):
+    o = _Options()
+    lib().evoke_default_options(ctypes.byref(o))
+    o.induced = 1 if induced else 0
+    o.device_pointers = 1 if device_pointers else 0
+    o.shard_index = shard_index
+    o.num_shards = num_shards
+    o.device = -1 if device is None else int(device)
+    o.stream = stream
+    o.stats = ctypes.pointer(stats) if stats is not None else None
+    return o
+
+
+def _stats_dict(s: _Stats) -> dict:
+    names = pass_names()
+    return {"n": s.n, "m": s.m, "triangles": s.triangles, "max_degree": s.max_degree,
+            "degeneracy": s.degeneracy, "wedges": s.wedges, "ms_total": s.ms_total,
+            "ms_pass": {names[i]: s.ms_pass[i] for i in range(min(s.num_passes, len(names)))},
+            "kernel_launches": s.kernel_launches}
+
+
+def _check(rc: int):
+    if rc != EVOKE_OK:
+        L = lib()
+        raise EvokeError(rc, f"{L.evoke_strerror(rc).decode()}: {L.evoke_last_error().decode()}")
+
+
+def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_index: int = 0,
+                       num_shards: int = 1, stream=None, return_stats: bool = False):
+    """Orbit counts uint64[n, 73] of the simple graph given by undirected pairs ``edges``.
+
+    ``edges``: int32 [m, 2] numpy array (host) or CUDA torch tensor (device).  Duplicates,
+    reverse duplicates and self-loops are removed by the library.
+    ``out``: optional preallocated numpy uint64 [n, 73] (host input) or torch int64/uint64
+    CUDA tensor [n, 73] (device input)."""
+    st = _Stats() if return_stats else None
+    if _is_torch(edges):
+        import torch
+        assert edges.is_cuda and edges.dtype == torch.int32, "device edges must be CUDA int32"
+        e = edges.contiguous()
+        m = e.numel() // 2
+        if out is None:
+            out = torch.empty((n, NUM_ORBITS), dtype=torch.int64, device=e.device)
+        assert out.is_cuda and out.is_contiguous() and out.numel() == n * NUM_ORBITS
+        if stream is None:
+            stream = torch.cuda.current_stream(e.device).cuda_stream
+        o = _make_options(induced, True, shard_index, num_shards, e.device.index, stream, st)
+        rc = lib().evoke_orbits_edges(n, m, e.data_ptr(), out.data_ptr(), ctypes.byref(o))
+    else:
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+        m = e.shape[0]
+        if out is None:
+            out = np.zeros((n, NUM_ORBITS), dtype=np.uint64)
+        assert out.dtype == np.uint64 and out.flags.c_contiguous and out.size == n * NUM_ORBITS
+        o = _make_options(induced, False, shard_index, num_shards, None, stream, st)
+        rc = lib().evoke_orbits_edges(n, m, e.ctypes.data if m else None, out.ctypes.data, ctypes.byref(o))
+    _check(rc)
+    if return_stats:
+        return out, _stats_dict(st)
+    return out
+
+
+def evoke_orbits_csr(n: int, rowptr, col, out=None, induced: bool = True, shard_index: int = 0,
+                     num_shards: int = 1, stream=None, return_stats: bool = False):
+    """Orbit counts from a CSR (rowptr int64[n+1], col int32[rowptr[n]]); same cleaning."""
+    st = _Stats() if return_stats else None
+    if _is_torch(rowptr):
+        import torch
+        rp = rowptr.contiguous()
+        cl = col.contiguous()
+        if out is None:
+            out = torch.empty((n, NUM_ORBITS), dtype=torch.int64, device=rp.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(rp.device).cuda_stream
+        o = _make_options(induced, True, shard_index, num_shards, rp.device.index, stream, st)
+        rc = lib().evoke_orbits_csr(n, rp.data_ptr(), cl.data_ptr(), out.data_ptr(), ctypes.byref(o))
+    else:
+        rp = np.ascontiguousarray(np.asarray(rowptr, dtype=np.int64))
+        cl = np.ascontiguousarray(np.asarray(col, dtype=np.int32))
+        if out is None:
+            out = np.zeros((n, NUM_ORBITS), dtype=np.uint64)
+        o = _make_options(induced, False, shard_index, num_shards, None, stream, st)
+        rc = lib().evoke_orbits_csr(n, rp.ctypes.data, cl.ctypes.data if cl.size else None, out.ctypes.data,
+                                    ctypes.byref(o))
+    _check(rc)
+    if return_stats:
+        return out, _stats_dict(st)
+    return out

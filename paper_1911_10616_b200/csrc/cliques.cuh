@@ -1,0 +1,181 @@
+// cliques.cuh -- steps a5 and a9 of SURVEY 8(a).
+//
+// One CTA per vertex u.  L = N+(u) (k = d+(u) <= degeneracy vertices, sorted), the
+// local graph G[L] is held as a symmetric k x k bitmap S in shared memory, built from
+// the oriented triangle lists of the edges (u, L_i) (a triangle (u, L_i, L_j) is local
+// edge (i, j)).  Every clique is counted once, from its lowest vertex u:
+//   4-cliques {u,i,j,l}   = triangles of G[L]      -> K4(v), K4(e)=E11, K4(t)
+//   5-cliques {u,i,j,l,p} = 4-cliques of G[L]      -> K5(v) = DM72
+// Per local vertex i the counts are popcounts of ANDed rows, so no per-clique atomics
+// are needed for vertex and (u, L_i) edge credits.  K4(t) of a triangle t=(a<b<c) is
+// (apexes above a, counted in a's frame) + (apexes below a: +1 from each lower u).
+//
+// MODE 1 (after K4(t) and E1 are final) credits theta66 (reading R12) and
+// theta70 per 4-clique without enumerating cliques one by one for u's own
+// theta66 credit.
+#pragma once
+#include "common.cuh"
+
+template <typename F>
+__device__ __forceinline__ void for_each_bit(u32 x, int base, F f) {
+  while (x) {
+    int b = __ffs(x) - 1;
+    x &= x - 1;
+    f(base + b);
+  }
+}
+
+// rank of local j among the set bits of row R (restricted to bits > i): number of set
+// bits of (R & GT(i)) strictly below j
+__device__ __forceinline__ int row_rank(const u32* __restrict__ R, int W, int i, int j) {
+  int r = 0;
+  const int jw = j >> 5;
+  for (int w = (i >> 5); w <= jw && w < W; w++) r += __popc(R[w] & gt_mask(i, w) & lt_mask(j, w));
+  return r;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_cliques(
+    DGraph g, const int32_t* __restrict__ ulist, int nu, int smem_words, u32* __restrict__ gscratch,
+    int64_t gscratch_words, int do_k4, int shard_index, int num_shards,
+    const u32* __restrict__ Te, u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
+    u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70) {
+  extern __shared__ u32 sh_bits[];
+  __shared__ u64 red[1][2];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  if (threadIdx.x == 0) { red[0][0] = 0; red[0][1] = 0; }
+  __syncthreads();
+  for (int idx = blockIdx.x; idx < nu; idx += gridDim.x) {
+    const int32_t u = ulist[idx];
+    const bool in_shard = (idx % num_shards) == shard_index;
+    const bool do_k5 = (MODE == 0) && in_shard;
+    if (MODE == 0 && !do_k4 && !do_k5) continue;
+    if (MODE == 1 && !in_shard) continue;
+    const int64_t ou = g.orow[u];
+    const int k = (int)(g.orow[u + 1] - ou);
+    const int W = (k + 31) >> 5;
+    u32* S = ((int64_t)k * W <= smem_words) ? sh_bits : (gscratch + (int64_t)blockIdx.x * gscratch_words);
+    for (int64_t t = threadIdx.x; t < (int64_t)k * W; t += blockDim.x) S[t] = 0u;
+    __syncthreads();
+    const int64_t q0 = g.toff[ou], q1 = g.toff[ou + k];
+    for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+      const int i = (int)(g.tab[q] - ou), j = (int)(g.tac[q] - ou);
+      atomicOr(&S[(int64_t)i * W + (j >> 5)], 1u << (j & 31));
+      atomicOr(&S[(int64_t)j * W + (i >> 5)], 1u << (i & 31));
+    }
+    __syncthreads();
+    u64 acc_u0 = 0, acc_u1 = 0;  // u's own credits (MODE 0: 3*#K4 and 4*#K5; MODE 1: th66, th70)
+    for (int i = wib; i < k; i += nwb) {
+      const u32* Si = S + (int64_t)i * W;
+      const int32_t Li = g.ocol[ou + i];
+      u64 a0 = 0, a1 = 0, a2 = 0;  // per-i accumulators
+      const int64_t qi0 = g.toff[ou + i];
+      for (int j = lane; j < k; j += 32) {
+        if (!((Si[j >> 5] >> (j & 31)) & 1u)) continue;
+        const u32* Sj = S + (int64_t)j * W;
+        if (MODE == 0) {
+          for (int w = (j >> 5); w < W; w++) {
+            const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+            if (do_k4) a0 += __popc(x);
+            if (do_k5)
+              for_each_bit(x, w << 5, [&](int l) {
+                const u32* Sl = S + (int64_t)l * W;
+                u64 c = 0;
+                for (int w2 = (l >> 5); w2 < W; w2++) c += __popc(Si[w2] & Sj[w2] & Sl[w2] & gt_mask(l, w2));
+                a1 += c;
+              });
+          }
+          if (do_k4 && j > i) {
+            u32 c = 0;
+            for (int w = 0; w < W; w++) c += __popc(Si[w] & Sj[w]);
+            const int64_t qij = qi0 + row_rank(Si, W, i, j);
+            const int32_t eij = g.tbc[qij];
+            if (c) {
+              atomicAdd(&K4e[eij], (u64)c);
+              atomicAdd(&K4t[qij], c);
+            }
+            // local triangles (i<j<l): triangle (L_i, L_j, L_l) gets apex u below it
+            int64_t lo = g.toff[eij];
+            const int64_t hi = g.toff[eij + 1];
+            for (int w = (j >> 5); w < W; w++) {
+              const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+              for_each_bit(x, w << 5, [&](int l) {
+                const int32_t Ll = g.ocol[ou + l];
+                const int64_t pos = lower_bound_dev<int32_t>(g.tc, lo, hi, Ll);
+                atomicAdd(&K4t[pos], 1u);
+                lo = pos + 1;
+              });
+            }
+          }
+        } else {
+          // theta66 / theta70 credits to L_i over the local edges (j,l) inside S_i
+          const u64 te_uj = Te[ou + j];
+          const int64_t qj0 = g.toff[ou + j];
+          for (int w = (j >> 5); w < W; w++) {
+            const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+            for_each_bit(x, w << 5, [&](int l) {
+              const int64_t qjl = qj0 + row_rank(Sj, W, j, l);
+              a0 += te_uj + (u64)Te[ou + l] + (u64)Te[g.tbc[qjl]];
+              a1 += (u64)K4t[qjl] - 1ull;
+            });
+          }
+          if (j > i) {
+            u32 c = 0;
+            for (int w = 0; w < W; w++) c += __popc(Si[w] & Sj[w]);
+            const int64_t qij = qi0 + row_rank(Si, W, i, j);
+            const int32_t eij = g.tbc[qij];
+            acc_u0 += (u64)Te[eij] * (u64)c;
+            int64_t lo = g.toff[eij];
+            const int64_t hi = g.toff[eij + 1];
+            for (int w = (j >> 5); w < W; w++) {
+              const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+              for_each_bit(x, w << 5, [&](int l) {
+                const int32_t Ll = g.ocol[ou + l];
+                const int64_t pos = lower_bound_dev<int32_t>(g.tc, lo, hi, Ll);
+                acc_u1 += (u64)K4t[pos] - 1ull;
+                lo = pos + 1;
+              });
+            }
+          }
+        }
+      }
+      a0 = warp_sum(a0);
+      a1 = warp_sum(a1);
+      (void)a2;
+      if (lane == 0) {
+        if (MODE == 0) {
+          if (do_k4 && a0) {
+            atomicAdd(&K4v[Li], a0);
+            atomicAdd(&K4e[ou + i], a0);
+          }
+          if (do_k5 && a1) atomicAdd(&K5v[Li], a1);
+          acc_u0 += a0;
+          acc_u1 += a1;
+        } else {
+          if (a0) atomicAdd(&R66[Li], a0);
+          if (a1) atomicAdd(&R70[Li], a1);
+        }
+      }
+    }
+    // block reduction of u's credits
+    acc_u0 = warp_sum(acc_u0);
+    acc_u1 = warp_sum(acc_u1);
+    if (lane == 0) {
+      atomicAdd(&red[0][0], acc_u0);
+      atomicAdd(&red[0][1], acc_u1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const u64 s0 = red[0][0], s1 = red[0][1];
+      if (MODE == 0) {
+        if (do_k4 && s0) atomicAdd(&K4v[u], s0 / 3);  // each local triangle counted at its 3 vertices
+        if (do_k5 && s1) atomicAdd(&K5v[u], s1 / 4);  // each local 4-clique counted at its 4 vertices
+      } else {
+        if (s0) atomicAdd(&R66[u], s0);
+        if (s1) atomicAdd(&R70[u], s1);
+      }
+      red[0][0] = 0; red[0][1] = 0;
+    }
+    __syncthreads();
+  }
+}

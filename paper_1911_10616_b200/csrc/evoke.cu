@@ -1,0 +1,764 @@
+// evoke.cu -- host orchestration and the C ABI (include/evoke.h) of the B200-native
+// EVOKE vertex-orbit counter.  One translation unit: the kernels live in the .cuh
+// files included below; this file sequences them on one stream (SURVEY 8(a) rows
+// a1..a12).
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/evoke.h"
+#include "common.cuh"
+#include "graph_build.cuh"
+#include "triangles.cuh"
+#include "cliques.cuh"
+#include "pairs.cuh"
+#include "hublocal.cuh"
+#include "cycles5.cuh"
+#include "gather.cuh"
+#include "transform.cuh"
+
+#define EVOKE_VERSION "0.1.0-sm100a"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+struct EvokeError {
+  int code;
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      throw EvokeError{_e == cudaErrorMemoryAllocation ? EVOKE_ENOMEM : EVOKE_ECUDA};   \
+    }                                                                                   \
+  } while (0)
+
+static const char* kPassNames[] = {
+    "h2d",        "canonicalise", "kcore_order", "csr_build",  "triangles",  "tri_lists",
+    "cliques_k4k5", "nbr_gather1", "pair_pass",  "hub_local",  "cycles5",    "cliques_66_70",
+    "nbr_gather2", "tri_gather",  "combine",    "d2h"};
+enum { P_H2D = 0, P_CANON, P_KCORE, P_CSR, P_TRI, P_TRILIST, P_CLIQ, P_NBR1, P_PAIR, P_HUB, P_C5,
+       P_CLIQ2, P_NBR2, P_TRIG, P_COMB, P_D2H, P_COUNT };
+
+// Device allocations of one call; everything is freed (stream-ordered) at the end.
+struct Arena {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Arena(cudaStream_t s) : st(s) {}
+  template <typename T>
+  T* alloc(size_t count, bool zero = false) {
+    void* p = nullptr;
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) {
+      set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+      throw EvokeError{EVOKE_ENOMEM};
+    }
+    ptrs.push_back(p);
+    if (zero) CK(cudaMemsetAsync(p, 0, bytes, st));
+    return (T*)p;
+  }
+  void release(void* p) {
+    for (auto& q : ptrs)
+      if (q == p) { cudaFreeAsync(q, st); q = nullptr; }
+  }
+  ~Arena() {
+    for (void* p : ptrs)
+      if (p) cudaFreeAsync(p, st);
+  }
+};
+
+struct Ctx {
+  cudaStream_t st;
+  int dev, num_sms;
+  int launches = 0;
+  cudaEvent_t ev[P_COUNT + 1];
+  bool timing;
+  void mark(int pass) {
+    if (timing) CK(cudaEventRecord(ev[pass], st));
+  }
+};
+
+inline int grid_for(int64_t work, int block, int num_sms) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = (int64_t)num_sms * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+template <typename T>
+T d2h_scalar(const T* dptr, cudaStream_t st) {
+  T v;
+  CK(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return v;
+}
+
+// ---- CUB wrappers (stream-ordered temp storage)
+void sort_keys_u64(Arena& A, Ctx& C, const u64* in, u64* out, int64_t N, int end_bit) {
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, in, out, (int64_t)N, 0, end_bit, C.st));
+  void* t = A.alloc<char>(tb);
+  CK(cub::DeviceRadixSort::SortKeys(t, tb, in, out, (int64_t)N, 0, end_bit, C.st));
+  A.release(t);
+  C.launches += 4;
+}
+
+template <typename Tin, typename Tout>
+void inclusive_sum(Arena& A, Ctx& C, const Tin* in, Tout* out, int64_t N) {
+  size_t tb = 0;
+  CK(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, N, C.st));
+  void* t = A.alloc<char>(tb);
+  CK(cub::DeviceScan::InclusiveSum(t, tb, in, out, N, C.st));
+  A.release(t);
+  C.launches += 2;
+}
+
+int bits_for(int64_t x) {
+  int b = 1;
+  while ((1ll << b) <= x) b++;
+  return b;
+}
+
+__global__ void k_u32_to_i64(const u32* __restrict__ a, int64_t n, int64_t* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+__global__ void k_i32_to_i64(const int32_t* __restrict__ a, int64_t n, int64_t* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+__global__ void k_max_i32(const int32_t* __restrict__ a, int64_t n, int* out) {
+  int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, a[i]);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(FULL_MASK, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+__global__ void k_max_diff_i64(const int64_t* __restrict__ a, int64_t n, int* out) {
+  int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (int)(a[i + 1] - a[i]));
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(FULL_MASK, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+// wedge total W(G) = sum C(d,2)
+__global__ void k_wedges(const int64_t* __restrict__ rp, int32_t n, u64* out) {
+  u64 s = 0;
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    s += binom2((u64)(rp[v + 1] - rp[v]));
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+// work-sorted vertex lists: key = work estimate, descending; shard by position
+__global__ void k_work_pair(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int32_t n,
+                            u64* __restrict__ keys, int32_t* __restrict__ vals) {
+  // pair pass cost ~ sum_{v in N(u)} d(v)  (approximated by d(u) * d_max-capped mean)
+  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    u64 w = 0;
+    const int64_t a = rp[u], b = rp[u + 1];
+    const int64_t lim = min(b, a + 64);
+    for (int64_t s = a; s < lim; s++) w += (u64)(rp[ci[s] + 1] - rp[ci[s]]);
+    if (b > lim) w = w * (u64)(b - a) / 64ull;
+    keys[u] = ~w;  // ascending sort of ~w = descending w
+    vals[u] = u;
+  }
+}
+
+__global__ void k_shard_list(const int32_t* __restrict__ sorted, int32_t n, int si, int ns,
+                             int32_t* __restrict__ out) {
+  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+    if (p % ns == si) out[p / ns] = sorted[p];
+}
+
+// clique bins by k = d+(u): bin 0: 3..32, 1: 33..128, 2: 129..512, 3: 513..1024, 4: >1024
+__global__ void k_clique_bins(const int64_t* __restrict__ orow, int32_t n, int32_t* __restrict__ lists,
+                              int* __restrict__ counts) {
+  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    const int64_t k = orow[u + 1] - orow[u];
+    if (k < 3) continue;
+    const int b = k <= 32 ? 0 : k <= 128 ? 1 : k <= 512 ? 2 : k <= 1024 ? 3 : 4;
+    lists[(int64_t)b * n + atomicAdd(&counts[b], 1)] = u;
+  }
+}
+
+struct Input {
+  int kind;  // 0 edges, 1 csr
+  int64_t n, m;
+  const int32_t* edges;
+  const int64_t* rowptr;
+  const int32_t* col;
+};
+
+void run(const Input& in, uint64_t* out, const evoke_options& o) {
+  int dev = o.device;
+  if (dev < 0) CK(cudaGetDevice(&dev));
+  CK(cudaSetDevice(dev));
+  Ctx C;
+  C.dev = dev;
+  CK(cudaDeviceGetAttribute(&C.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t own = nullptr;
+  if (o.stream) C.st = (cudaStream_t)o.stream;
+  else { CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking)); C.st = own; }
+  C.timing = true;
+  for (int i = 0; i <= P_COUNT; i++) CK(cudaEventCreate(&C.ev[i]));
+  struct Cleanup {
+    Ctx& C; cudaStream_t own;
+    ~Cleanup() {
+      for (int i = 0; i <= P_COUNT; i++) cudaEventDestroy(C.ev[i]);
+      if (own) { cudaStreamSynchronize(own); cudaStreamDestroy(own); }
+    }
+  } cleanup{C, own};
+
+  const auto& TF = evoke_host::transform();
+  {
+    int rp[74];
+    uint8_t col[AINV_MAX_NNZ];
+    long long val[AINV_MAX_NNZ];
+    if ((int)TF.col.size() > AINV_MAX_NNZ) { set_error("A^-1 too dense"); throw EvokeError{EVOKE_EINTERNAL}; }
+    for (int i = 0; i < 74; i++) rp[i] = TF.rp[i];
+    for (size_t i = 0; i < TF.col.size(); i++) { col[i] = (uint8_t)TF.col[i]; val[i] = TF.val[i]; }
+    CK(cudaMemcpyToSymbolAsync(c_ainv_rp, rp, sizeof(rp), 0, cudaMemcpyHostToDevice, C.st));
+    CK(cudaMemcpyToSymbolAsync(c_ainv_col, col, TF.col.size(), 0, cudaMemcpyHostToDevice, C.st));
+    CK(cudaMemcpyToSymbolAsync(c_ainv_val, val, TF.col.size() * sizeof(long long), 0,
+                               cudaMemcpyHostToDevice, C.st));
+  }
+
+  Arena A(C.st);
+  const int32_t n = (int32_t)in.n;
+  const int B = 256;
+  const int SM = C.num_sms;
+  C.mark(0);
+  // ------------------------------------------------------------------ a1: input
+  int* d_bad = A.alloc<int>(1, true);
+  int64_t mraw = 0;
+  u64* keys = nullptr;
+  if (in.kind == 0) {
+    mraw = in.m;
+    const int32_t* d_edges = in.edges;
+    if (!o.device_pointers && mraw > 0) {
+      int32_t* t = A.alloc<int32_t>(2 * mraw);
+      CK(cudaMemcpyAsync(t, in.edges, sizeof(int32_t) * 2 * mraw, cudaMemcpyHostToDevice, C.st));
+      d_edges = t;
+    }
+    C.mark(P_CANON);
+    keys = A.alloc<u64>(mraw + 1);
+    if (mraw > 0) {
+      k_make_keys<<<grid_for(mraw, B, SM), B, 0, C.st>>>(d_edges, mraw, n, keys, d_bad);
+      C.launches++;
+    }
+  } else {
+    const int64_t* d_rp = in.rowptr;
+    const int32_t* d_col = in.col;
+    if (!o.device_pointers) {
+      mraw = in.rowptr[n];
+      int64_t* t1 = A.alloc<int64_t>(n + 1);
+      CK(cudaMemcpyAsync(t1, in.rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, C.st));
+      int32_t* t2 = A.alloc<int32_t>(mraw + 1);
+      if (mraw) CK(cudaMemcpyAsync(t2, in.col, sizeof(int32_t) * mraw, cudaMemcpyHostToDevice, C.st));
+      d_rp = t1; d_col = t2;
+    } else {
+      mraw = d2h_scalar<int64_t>(in.rowptr + n, C.st);
+    }
+    C.mark(P_CANON);
+    k_check_rowptr<<<grid_for(n, B, SM), B, 0, C.st>>>(d_rp, n, d_bad);
+    if (d2h_scalar<int>(d_bad, C.st)) { set_error("malformed CSR rowptr"); throw EvokeError{EVOKE_EINVAL}; }
+    keys = A.alloc<u64>(mraw + 1);
+    if (mraw > 0) k_make_keys_csr<<<grid_for(n, B, SM), B, 0, C.st>>>(d_rp, d_col, n, keys, d_bad);
+    C.launches += 2;
+  }
+  if (d2h_scalar<int>(d_bad, C.st)) { set_error("vertex id outside [0, n)"); throw EvokeError{EVOKE_EINVAL}; }
+  int64_t m = 0;
+  u64* ukeys = A.alloc<u64>(mraw + 1);
+  if (mraw > 0) {
+    u64* sk = A.alloc<u64>(mraw);
+    sort_keys_u64(A, C, keys, sk, mraw, 64);
+    int64_t* d_nsel = A.alloc<int64_t>(1);
+    size_t tb = 0;
+    CK(cub::DeviceSelect::Unique(nullptr, tb, sk, ukeys, d_nsel, mraw, C.st));
+    void* t = A.alloc<char>(tb);
+    CK(cub::DeviceSelect::Unique(t, tb, sk, ukeys, d_nsel, mraw, C.st));
+    C.launches += 2;
+    int64_t nsel = d2h_scalar<int64_t>(d_nsel, C.st);
+    // drop the self-loop sentinel (sorted last)
+    u64 last = 0;
+    if (nsel > 0) last = d2h_scalar<u64>(ukeys + nsel - 1, C.st);
+    m = (nsel > 0 && last == ~0ull) ? nsel - 1 : nsel;
+    A.release(sk); A.release(t); A.release(keys);
+  }
+  if (m >= (1ll << 31) - 1) { set_error("graph too large: m = %lld", (long long)m); throw EvokeError{EVOKE_EINTERNAL}; }
+  const int64_t m2 = 2 * m;
+
+  // ------------------------------------------------------------------ a2: k-core order
+  C.mark(P_KCORE);
+  int32_t* deg0 = A.alloc<int32_t>(n, true);
+  int64_t* rp0 = A.alloc<int64_t>(n + 1);
+  int32_t* adj0 = A.alloc<int32_t>(m2 + 1);
+  int32_t* perm = A.alloc<int32_t>(n);
+  int32_t* inv = A.alloc<int32_t>(n);
+  int peel_rounds = 0, degeneracy_level = 0;
+  if (n > 0) {
+    if (m > 0) { k_degrees<<<grid_for(m, B, SM), B, 0, C.st>>>(ukeys, m, deg0); C.launches++; }
+    int64_t* deg64 = A.alloc<int64_t>(n);
+    k_i32_to_i64<<<grid_for(n, B, SM), B, 0, C.st>>>(deg0, n, deg64);
+    k_set_i64<<<1, 1, 0, C.st>>>(rp0, 0);
+    inclusive_sum(A, C, deg64, rp0 + 1, n);
+    C.launches += 2;
+    int64_t* cursor = A.alloc<int64_t>(n);
+    CK(cudaMemcpyAsync(cursor, rp0, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, C.st));
+    if (m > 0) { k_fill_adj0<<<grid_for(m, B, SM), B, 0, C.st>>>(ukeys, m, cursor, adj0); C.launches++; }
+    int32_t* rnd = A.alloc<int32_t>(n);
+    int32_t* l0 = A.alloc<int32_t>(n);
+    int32_t* l1 = A.alloc<int32_t>(n);
+    PeelCtl* ctl = A.alloc<PeelCtl>(1, true);
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel, 512, 0));
+    int pgrid = std::max(1, std::min(bps, 2)) * SM;
+    void* args[] = {(void*)&n, (void*)&rp0, (void*)&adj0, (void*)&deg0, (void*)&rnd, (void*)&l0,
+                    (void*)&l1, (void*)&ctl};
+    CK(cudaLaunchCooperativeKernel((void*)k_peel, pgrid, 512, args, 0, C.st));
+    C.launches++;
+    PeelCtl hc = d2h_scalar<PeelCtl>(ctl, C.st);
+    peel_rounds = hc.rounds;
+    degeneracy_level = hc.level;
+    u64* okeys = A.alloc<u64>(n);
+    u64* osorted = A.alloc<u64>(n);
+    k_order_keys<<<grid_for(n, B, SM), B, 0, C.st>>>(rnd, n, okeys);
+    C.launches++;
+    sort_keys_u64(A, C, okeys, osorted, n, 32 + bits_for(std::max(peel_rounds, 1)));
+    k_perm<<<grid_for(n, B, SM), B, 0, C.st>>>(osorted, n, perm, inv);
+    C.launches++;
+    A.release(okeys); A.release(osorted); A.release(rnd); A.release(l0); A.release(l1);
+    A.release(cursor); A.release(deg64);
+  }
+  A.release(adj0); A.release(rp0); A.release(deg0);
+  (void)degeneracy_level;
+
+  // ------------------------------------------------------------------ a3: CSR + edges
+  C.mark(P_CSR);
+  int64_t* rp = A.alloc<int64_t>(n + 1);
+  int32_t* ci = A.alloc<int32_t>(m2 + 1);
+  int32_t* dmv = A.alloc<int32_t>(n + 1);
+  int64_t* orow = A.alloc<int64_t>(n + 1);
+  int32_t* eid = A.alloc<int32_t>(m2 + 1);
+  int32_t* ocol = A.alloc<int32_t>(m + 1);
+  int32_t* esrc = A.alloc<int32_t>(m + 1);
+  int32_t* edst = A.alloc<int32_t>(m + 1);
+  int64_t* eslot_hi = A.alloc<int64_t>(m + 1);
+  int max_deg = 0, max_out = 0;
+  if (n > 0) {
+    int32_t* degc = A.alloc<int32_t>(n, true);
+    int64_t* tmp64 = A.alloc<int64_t>(n);
+    u64* dk = A.alloc<u64>(m2 + 1);
+    u64* dks = A.alloc<u64>(m2 + 1);
+    if (m > 0) {
+      k_relabel_keys<<<grid_for(m, B, SM), B, 0, C.st>>>(ukeys, m, inv, dk);
+      C.launches++;
+      sort_keys_u64(A, C, dk, dks, m2, 32 + bits_for(n));
+      k_split_keys<<<grid_for(m2, B, SM), B, 0, C.st>>>(dks, m2, ci, degc);
+      C.launches++;
+    }
+    k_i32_to_i64<<<grid_for(n, B, SM), B, 0, C.st>>>(degc, n, tmp64);
+    k_set_i64<<<1, 1, 0, C.st>>>(rp, 0);
+    inclusive_sum(A, C, tmp64, rp + 1, n);
+    k_split_counts<<<grid_for(n, B, SM), B, 0, C.st>>>(n, rp, ci, dmv, tmp64);
+    k_set_i64<<<1, 1, 0, C.st>>>(orow, 0);
+    inclusive_sum(A, C, tmp64, orow + 1, n);
+    C.launches += 4;
+    if (m > 0) {
+      k_edge_arrays<<<grid_for(m2, B, SM), B, 0, C.st>>>(dks, m2, rp, ci, dmv, orow, eid, ocol, esrc, edst,
+                                                         eslot_hi);
+      C.launches++;
+    }
+    int* d_mx = A.alloc<int>(2, true);
+    k_max_diff_i64<<<grid_for(n, B, SM), B, 0, C.st>>>(rp, n, d_mx);
+    k_max_diff_i64<<<grid_for(n, B, SM), B, 0, C.st>>>(orow, n, d_mx + 1);
+    C.launches += 2;
+    int hm[2];
+    CK(cudaMemcpyAsync(hm, d_mx, sizeof(hm), cudaMemcpyDeviceToHost, C.st));
+    CK(cudaStreamSynchronize(C.st));
+    max_deg = hm[0]; max_out = hm[1];
+    A.release(dk); A.release(dks); A.release(degc); A.release(tmp64);
+  }
+  A.release(ukeys);
+
+  DGraph g;
+  std::memset(&g, 0, sizeof(g));
+  g.n = n; g.m = m; g.max_deg = std::max(max_deg, 1); g.max_out = max_out;
+  g.rp = rp; g.ci = ci; g.dm = dmv; g.eid = eid; g.orow = orow; g.ocol = ocol; g.esrc = esrc;
+  g.edst = edst; g.eslot_hi = eslot_hi;
+
+  // per-vertex fields and per-edge arrays
+  u64* F = A.alloc<u64>((size_t)F_COUNT * std::max(n, 1), true);
+  u32* Te = A.alloc<u32>(m + 1, true);
+  u32* Tlow = A.alloc<u32>(m + 1, true);
+  u32* Tmid = A.alloc<u32>(m + 1, true);
+  u32* Thigh = A.alloc<u32>(m + 1, true);
+  u64* E7 = A.alloc<u64>(m + 1, true);
+  u64* E9f = A.alloc<u64>(m + 1, true);
+  u64* E9b = A.alloc<u64>(m + 1, true);
+  u64* K4e = A.alloc<u64>(m + 1, true);
+  u64* C4e = A.alloc<u64>(m + 1, true);
+  auto Fp = [&](int f) { return F + (size_t)f * (size_t)n; };
+
+  // ------------------------------------------------------------------ a4: triangles
+  C.mark(P_TRI);
+  int64_t* toff = A.alloc<int64_t>(m + 1);
+  int64_t ntri = 0;
+  const int tri_smem_per_warp = std::min(std::max(max_out, 1), 2048);
+  const int tri_block = 256;
+  const size_t tri_smem = (size_t)(tri_block / 32) * tri_smem_per_warp * sizeof(int32_t);
+  if (tri_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_triangles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem));
+  if (tri_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_triangles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem));
+  const int tri_grid = grid_for((int64_t)n * 32, tri_block, SM);
+  int32_t *tc = nullptr, *tab = nullptr, *tac = nullptr, *tbc = nullptr;
+  if (m > 0) {
+    k_triangles<0><<<tri_grid, tri_block, tri_smem, C.st>>>(g, tri_smem_per_warp, Thigh, Tmid, Tlow, Te,
+                                                           Fp(F_T), E7, nullptr, nullptr, nullptr, nullptr);
+    int64_t* th64 = A.alloc<int64_t>(m);
+    k_u32_to_i64<<<grid_for(m, B, SM), B, 0, C.st>>>(Thigh, m, th64);
+    k_set_i64<<<1, 1, 0, C.st>>>(toff, 0);
+    inclusive_sum(A, C, th64, toff + 1, m);
+    C.launches += 3;
+    A.release(th64);
+    ntri = d2h_scalar<int64_t>(toff + m, C.st);
+    tc = A.alloc<int32_t>(ntri + 1);
+    tab = A.alloc<int32_t>(ntri + 1);
+    tac = A.alloc<int32_t>(ntri + 1);
+    tbc = A.alloc<int32_t>(ntri + 1);
+    g.toff = toff; g.ntri = ntri; g.tc = tc; g.tab = tab; g.tac = tac; g.tbc = tbc;
+    k_triangles<1><<<tri_grid, tri_block, tri_smem, C.st>>>(g, tri_smem_per_warp, Thigh, Tmid, Tlow, Te,
+                                                           Fp(F_T), E7, tc, tab, tac, tbc);
+    C.launches++;
+  } else {
+    CK(cudaMemsetAsync(toff, 0, sizeof(int64_t) * (m + 1), C.st));
+    g.toff = toff;
+  }
+
+  // ------------------------------------------------------------------ a6: tri lists, E9, DM12
+  C.mark(P_TRILIST);
+  int64_t* foff = A.alloc<int64_t>(m + 1);
+  int32_t *fx = nullptr, *fe1 = nullptr, *fe2 = nullptr;
+  u32* K4t = A.alloc<u32>(ntri + 1, true);
+  if (ntri > 0) {
+    int64_t* te64 = A.alloc<int64_t>(m);
+    k_u32_to_i64<<<grid_for(m, B, SM), B, 0, C.st>>>(Te, m, te64);
+    k_set_i64<<<1, 1, 0, C.st>>>(foff, 0);
+    inclusive_sum(A, C, te64, foff + 1, m);
+    A.release(te64);
+    int64_t* fcur = A.alloc<int64_t>(m + 1);
+    CK(cudaMemcpyAsync(fcur, foff, sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, C.st));
+    fx = A.alloc<int32_t>(3 * ntri);
+    fe1 = A.alloc<int32_t>(3 * ntri);
+    fe2 = A.alloc<int32_t>(3 * ntri);
+    g.foff = foff; g.fx = fx; g.fe1 = fe1; g.fe2 = fe2;
+    k_tri_sweep1<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, Te, E9f, E9b, Fp(F_DM12), fcur, fx, fe1, fe2);
+    C.launches += 3;
+    A.release(fcur);
+  } else {
+    CK(cudaMemsetAsync(foff, 0, sizeof(int64_t) * (m + 1), C.st));
+    g.foff = foff;
+  }
+
+  const int si = o.shard_index, ns = o.num_shards;
+  // ------------------------------------------------------------------ a5/a9: cliques
+  C.mark(P_CLIQ);
+  int32_t* cbins = A.alloc<int32_t>((size_t)5 * std::max(n, 1));
+  int* ccounts = A.alloc<int>(5, true);
+  int hcounts[5] = {0, 0, 0, 0, 0};
+  const int bin_k[5] = {32, 128, 512, 1024, 0};
+  u32* cscratch = nullptr;
+  int64_t cscratch_words = 0;
+  int cscratch_grid = 0;
+  if (n > 0) {
+    k_clique_bins<<<grid_for(n, B, SM), B, 0, C.st>>>(orow, n, cbins, ccounts);
+    C.launches++;
+    CK(cudaMemcpyAsync(hcounts, ccounts, sizeof(hcounts), cudaMemcpyDeviceToHost, C.st));
+    CK(cudaStreamSynchronize(C.st));
+    if (hcounts[4] > 0) {
+      const int64_t kk = max_out, W = (kk + 31) / 32;
+      cscratch_words = kk * W;
+      cscratch_grid = std::min(hcounts[4], 2 * SM);
+      cscratch = A.alloc<u32>((size_t)cscratch_words * cscratch_grid);
+    }
+  }
+  auto launch_cliques = [&](int mode) {
+    for (int b = 0; b < 5; b++) {
+      if (hcounts[b] == 0) continue;
+      const int kmax = b < 4 ? bin_k[b] : 0;
+      const int W = (kmax + 31) / 32;
+      const int words = kmax * W;
+      const size_t smem = (size_t)words * sizeof(u32);
+      const int block = b == 0 ? 64 : (b == 1 ? 128 : 256);
+      int grid = b < 4 ? std::min(hcounts[b], SM * 16) : cscratch_grid;
+      if (mode == 0) {
+        if (smem > 48 * 1024)
+          CK(cudaFuncSetAttribute(k_cliques<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_cliques<0><<<grid, block, smem, C.st>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
+                                                 cscratch_words, 1, si, ns, Te, K4t, Fp(F_K4), K4e, Fp(F_K5),
+                                                 nullptr, nullptr);
+      } else {
+        if (smem > 48 * 1024)
+          CK(cudaFuncSetAttribute(k_cliques<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_cliques<1><<<grid, block, smem, C.st>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
+                                                 cscratch_words, 0, si, ns, Te, K4t, nullptr, nullptr, nullptr,
+                                                 Fp(F_R66), Fp(F_R70));
+      }
+      C.launches++;
+    }
+  };
+  if (ntri > 0) launch_cliques(0);
+
+  EdgeVals ev{Te, E9f, E9b, K4e, C4e, E7, K4t};
+  // ------------------------------------------------------------------ nbr gather 1
+  C.mark(P_NBR1);
+  const int warp_grid = grid_for((int64_t)n * 32, B, SM);
+  if (n > 0) { k_nbr1<<<warp_grid, B, 0, C.st>>>(g, ev, F); C.launches++; }
+
+  // ------------------------------------------------------------------ a7: pair pass
+  C.mark(P_PAIR);
+  int32_t* vsorted = A.alloc<int32_t>(std::max(n, 1));
+  int32_t* shard_list = A.alloc<int32_t>(std::max(n, 1));
+  int nshard = 0;
+  if (n > 0) {
+    u64* wk = A.alloc<u64>(n);
+    u64* wk2 = A.alloc<u64>(n);
+    int32_t* vv = A.alloc<int32_t>(n);
+    k_work_pair<<<grid_for(n, B, SM), B, 0, C.st>>>(rp, ci, n, wk, vv);
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, wk, wk2, vv, vsorted, (int64_t)n, 0, 64, C.st));
+    void* t = A.alloc<char>(tb);
+    CK(cub::DeviceRadixSort::SortPairs(t, tb, wk, wk2, vv, vsorted, (int64_t)n, 0, 64, C.st));
+    k_shard_list<<<grid_for(n, B, SM), B, 0, C.st>>>(vsorted, n, si, ns, shard_list);
+    C.launches += 6;
+    nshard = (n - si + ns - 1) / ns;
+    if (nshard < 0) nshard = 0;
+    A.release(t); A.release(wk); A.release(wk2); A.release(vv);
+  }
+  if (n > 0 && m > 0 && nshard > 0) {
+    // per-CTA dense tables: W u32, D u32, TT u64, F u8, list i32  (21 bytes / vertex)
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    const size_t per = (size_t)n * 21;
+    int pg = std::min<int64_t>(2 * SM, std::max<int64_t>(1, (int64_t)(freeb / 3) / (int64_t)per));
+    pg = std::min(pg, nshard);
+    u32* Wt = A.alloc<u32>((size_t)pg * n, true);
+    u32* Dt = A.alloc<u32>((size_t)pg * n, true);
+    u64* TTt = A.alloc<u64>((size_t)pg * n, true);
+    uint8_t* Ft = A.alloc<uint8_t>((size_t)pg * n, true);
+    int32_t* Lt = A.alloc<int32_t>((size_t)pg * n);
+    int* counter = A.alloc<int>(1, true);
+    PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e};
+    k_pairs<<<pg, 512, 0, C.st>>>(g, Te, shard_list, nshard, counter, Wt, Dt, TTt, Ft, Lt, po);
+    C.launches++;
+    A.release(Wt); A.release(Dt); A.release(TTt); A.release(Ft); A.release(Lt);
+  }
+
+  // ------------------------------------------------------------------ a8: hub-local
+  C.mark(P_HUB);
+  if (ntri > 0) {
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    const size_t per_warp = (size_t)g.max_deg * 12;
+    int64_t warps = std::min<int64_t>((int64_t)SM * 32, std::max<int64_t>(8, (int64_t)(freeb / 4) / (int64_t)per_warp));
+    int hb = 256;
+    int hg = (int)std::max<int64_t>(1, warps / 8);
+    u64* tabs = A.alloc<u64>((size_t)hg * 8 * g.max_deg, true);
+    int32_t* lists = A.alloc<int32_t>((size_t)hg * 8 * g.max_deg);
+    int* counter = A.alloc<int>(1, true);
+    k_hublocal<<<hg, hb, 0, C.st>>>(g, Te, counter, 64, si, ns, tabs, lists, Fp(F_R68), Fp(F_R69));
+    C.launches++;
+    A.release(tabs); A.release(lists);
+  }
+
+  // ------------------------------------------------------------------ a10: 5-cycles
+  C.mark(P_C5);
+  if (n > 0 && m > 0 && nshard > 0) {
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    const size_t per = (size_t)n * 61;
+    int cg5 = std::min<int64_t>(2 * SM, std::max<int64_t>(1, (int64_t)(freeb / 3) / (int64_t)per));
+    cg5 = std::min(cg5, nshard);
+    C5Tables tb;
+    tb.Wn = A.alloc<u32>((size_t)cg5 * n, true);
+    tb.Q = A.alloc<u32>((size_t)cg5 * n, true);
+    tb.P = A.alloc<u64>((size_t)cg5 * n, true);
+    tb.A = A.alloc<u64>((size_t)cg5 * n, true);
+    tb.QT = A.alloc<u64>((size_t)cg5 * n, true);
+    tb.QM = A.alloc<u64>((size_t)cg5 * n, true);
+    tb.S = A.alloc<u64>((size_t)cg5 * n, true);
+    tb.flag = A.alloc<u32>((size_t)cg5 * n, true);
+    tb.Li = A.alloc<int32_t>((size_t)cg5 * n);
+    tb.Lj = A.alloc<int32_t>((size_t)cg5 * n);
+    int* counter = A.alloc<int>(1, true);
+    k_cycles5<<<cg5, 512, 0, C.st>>>(g, Tlow, Tmid, Thigh, shard_list, nshard, counter, tb, Fp(F_C5));
+    C.launches++;
+    A.release(tb.Wn); A.release(tb.Q); A.release(tb.P); A.release(tb.A); A.release(tb.QT);
+    A.release(tb.QM); A.release(tb.S); A.release(tb.flag); A.release(tb.Li); A.release(tb.Lj);
+  }
+
+  // ------------------------------------------------------------------ theta66 / theta70
+  C.mark(P_CLIQ2);
+  if (ntri > 0) launch_cliques(1);
+
+  // ------------------------------------------------------------------ nbr gathers 2,3
+  C.mark(P_NBR2);
+  if (n > 0) {
+    k_nbr2<<<warp_grid, B, 0, C.st>>>(g, ev, F);
+    k_nbr3<<<warp_grid, B, 0, C.st>>>(g, F);
+    C.launches += 2;
+  }
+  // ------------------------------------------------------------------ triangle gather
+  C.mark(P_TRIG);
+  if (ntri > 0) { k_trigather<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, ev, F); C.launches++; }
+
+  // ------------------------------------------------------------------ a12: combine
+  C.mark(P_COMB);
+  u64* dout = nullptr;
+  if (n > 0) {
+    dout = o.device_pointers ? (u64*)out : A.alloc<u64>((size_t)n * 73);
+    k_combine<<<grid_for(n, 128, SM), 128, 0, C.st>>>(g, F, perm, o.induced, si == 0 ? 1 : 0, dout);
+    C.launches++;
+  }
+  C.mark(P_D2H);
+  if (n > 0 && !o.device_pointers)
+    CK(cudaMemcpyAsync(out, dout, sizeof(u64) * (size_t)n * 73, cudaMemcpyDeviceToHost, C.st));
+  C.mark(P_COUNT);
+  CK(cudaStreamSynchronize(C.st));
+  CK(cudaGetLastError());
+
+  if (o.stats) {
+    evoke_stats* s = o.stats;
+    std::memset(s, 0, sizeof(*s));
+    s->n = n; s->m = m; s->triangles = ntri; s->max_degree = max_deg; s->degeneracy = max_out;
+    u64* dw = A.alloc<u64>(1, true);
+    if (n > 0) k_wedges<<<grid_for(n, B, SM), B, 0, C.st>>>(rp, n, dw);
+    s->wedges = (int64_t)d2h_scalar<u64>(dw, C.st);
+    s->num_passes = P_COUNT;
+    for (int i = 0; i < P_COUNT; i++) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, C.ev[i], C.ev[i + 1]));
+      s->ms_pass[i] = ms;
+    }
+    float tot = 0;
+    CK(cudaEventElapsedTime(&tot, C.ev[0], C.ev[P_COUNT]));
+    s->ms_total = tot;
+    s->kernel_launches = C.launches;
+  }
+}
+
+int guarded(const Input& in, uint64_t* out, const evoke_options* opt) {
+  g_last_error.clear();
+  evoke_options o;
+  evoke_default_options(&o);
+  if (opt) {
+    if (opt->struct_size != 0 && opt->struct_size < sizeof(evoke_options)) {
+      std::memcpy(&o, opt, opt->struct_size);
+    } else {
+      o = *opt;
+    }
+  }
+  if (o.num_shards < 1 || o.shard_index < 0 || o.shard_index >= o.num_shards) {
+    set_error("bad shard %d of %d", o.shard_index, o.num_shards);
+    return EVOKE_EINVAL;
+  }
+  if (in.n < 0 || in.n >= (1ll << 31) - 1) { set_error("bad n = %lld", (long long)in.n); return EVOKE_EINVAL; }
+  if (in.kind == 0) {
+    if (in.m < 0) { set_error("bad m"); return EVOKE_EINVAL; }
+    if (in.m > 0 && !in.edges) { set_error("edges is NULL"); return EVOKE_EINVAL; }
+  } else {
+    if (!in.rowptr) { set_error("rowptr is NULL"); return EVOKE_EINVAL; }
+    if (!o.device_pointers) {
+      if (in.rowptr[0] != 0) { set_error("rowptr[0] != 0"); return EVOKE_EINVAL; }
+      for (int64_t v = 0; v < in.n; v++)
+        if (in.rowptr[v + 1] < in.rowptr[v]) { set_error("rowptr not monotone at %lld", (long long)v); return EVOKE_EINVAL; }
+      if (in.rowptr[in.n] > 0 && !in.col) { set_error("col is NULL"); return EVOKE_EINVAL; }
+    }
+  }
+  if (in.n > 0 && !out) { set_error("out is NULL"); return EVOKE_EINVAL; }
+  if (in.n == 0) {
+    if (o.stats) { std::memset(o.stats, 0, sizeof(*o.stats)); o.stats->num_passes = P_COUNT; }
+    return EVOKE_OK;
+  }
+  try {
+    run(in, out, o);
+  } catch (const EvokeError& e) {
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error("%s", e.what());
+    return EVOKE_EINTERNAL;
+  }
+  return EVOKE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void evoke_default_options(evoke_options* opt) {
+  if (!opt) return;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->struct_size = sizeof(evoke_options);
+  opt->induced = 1;
+  opt->device_pointers = 0;
+  opt->shard_index = 0;
+  opt->num_shards = 1;
+  opt->device = -1;
+  opt->stream = nullptr;
+  opt->stats = nullptr;
+}
+
+int evoke_orbits_edges(int64_t n, int64_t m, const int32_t* edges, uint64_t* out, const evoke_options* opt) {
+  Input in{0, n, m, edges, nullptr, nullptr};
+  return guarded(in, out, opt);
+}
+
+int evoke_orbits_csr(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t* out,
+                     const evoke_options* opt) {
+  Input in{1, n, 0, nullptr, rowptr, col};
+  return guarded(in, out, opt);
+}
+
+const char* evoke_pass_name(int i) {
+  if (i < 0 || i >= (int)(sizeof(kPassNames) / sizeof(kPassNames[0]))) return nullptr;
+  return kPassNames[i];
+}
+
+const char* evoke_strerror(int code) {
+  switch (code) {
+    case EVOKE_OK: return "ok";
+    case EVOKE_EINVAL: return "invalid argument";
+    case EVOKE_ENOMEM: return "out of device memory";
+    case EVOKE_ECUDA: return "CUDA error";
+    case EVOKE_EINTERNAL: return "internal error";
+    default: return "unknown error";
+  }
+}
+
+const char* evoke_last_error(void) { return g_last_error.c_str(); }
+
+const char* evoke_version(void) { return EVOKE_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,266 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Bar: bit-exact equality of the uint64 n x 73 matrix (integer work).
+Sizes span many tiles / CTAs and ragged tails; the full BASELINE configs are covered by
+sampled rows (rooted oracle) + whole-matrix invariants, the tiled graph and the closed
+forms give full-matrix parity at millions of edges and at wrap-around (>= 2^64) counts.
+"""
+from math import comb
+
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+M64 = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1911_10616_b200 as p
+    p.lib()
+    return p
+
+
+def _rand(rng, nmin, nmax, pmin, pmax, seed):
+    n = int(rng.integers(nmin, nmax + 1))
+    p = float(rng.uniform(pmin, pmax))
+    return graphgen.erdos_renyi(n, p, seed)
+
+
+def _assert_equal(got, exp, what=""):
+    got = np.asarray(got)
+    if got.dtype != np.uint64:
+        got = got.view(np.uint64)
+    bad = np.argwhere(got != exp)
+    assert bad.size == 0, f"{what}: {len(bad)} mismatches, first (vertex, orbit) {bad[:8].tolist()}"
+
+
+# ----------------------------------------------------------------- small graphs ---
+def test_small_random_graphs_induced(pkg):
+    rng = np.random.default_rng(11)
+    for t in range(240):
+        g = _rand(rng, 1, 13, 0.05, 0.95, 5000 + t)
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name)
+
+
+def test_small_random_graphs_noninduced(pkg):
+    rng = np.random.default_rng(12)
+    for t in range(80):
+        g = _rand(rng, 2, 9, 0.2, 0.95, 7000 + t)
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges, induced=False),
+                      oracle.noninduced_bruteforce(g.n, g.edges), g.name)
+
+
+def test_sparse_medium_graphs(pkg):
+    """ragged sizes spanning several CTAs/warps (n up to 3000, sparse)"""
+    rng = np.random.default_rng(13)
+    for t in range(6):
+        n = int(rng.integers(200, 3000))
+        g = graphgen.erdos_renyi(n, 6.0 / n, 9000 + t)
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name)
+
+
+def test_dense_medium_graphs(pkg):
+    """dense graphs: large out-degree bins of the clique kernel, many 5-cliques"""
+    for n, p, s in [(40, 0.5, 1), (60, 0.35, 2), (34, 0.9, 3)]:
+        g = graphgen.erdos_renyi(n, p, s)
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name)
+
+
+def test_config1_full_matrix(pkg):
+    g = graphgen.config(1)
+    _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), "config 1")
+
+
+# --------------------------------------------------------------- degenerate cases ---
+def test_degenerate_inputs(pkg):
+    assert pkg.evoke_orbits_edges(0, np.zeros((0, 2), np.int32)).shape == (0, 73)
+    out = pkg.evoke_orbits_edges(7, np.zeros((0, 2), np.int32))
+    assert (out == 0).all()
+    out = pkg.evoke_orbits_edges(5, np.array([[1, 1], [3, 3]], np.int32))  # only self-loops
+    assert (out == 0).all()
+    out = pkg.evoke_orbits_edges(6, np.array([[4, 2]], np.int32))          # one edge, isolated ids
+    exp = np.zeros((6, 73), np.uint64)
+    exp[4, 0] = exp[2, 0] = 1
+    _assert_equal(out, exp, "single edge")
+    for g in [graphgen.complete(2), graphgen.complete(3), graphgen.complete(5), graphgen.complete(6),
+              graphgen.path(5), graphgen.cycle(5), graphgen.star(4), graphgen.petersen()]:
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name)
+
+
+def test_input_cleaning(pkg):
+    g = graphgen.erdos_renyi(300, 0.03, 21)
+    noisy = graphgen.add_noise(g, 5, frac=0.5)
+    _assert_equal(pkg.evoke_orbits_edges(noisy.n, noisy.edges), oracle.orbits(g.n, g.edges), "noisy")
+
+
+def test_invalid_vertex_id(pkg):
+    with pytest.raises(pkg.EvokeError) as ei:
+        pkg.evoke_orbits_edges(3, np.array([[0, 1], [1, 3]], np.int32))
+    assert ei.value.code == pkg.EVOKE_EINVAL
+
+
+# ---------------------------------------------------------------- API variants ---
+def test_csr_and_device_pointer_paths(pkg):
+    import torch
+    g = graphgen.erdos_renyi(500, 0.02, 31)
+    ref = oracle.orbits(g.n, g.edges)
+    # CSR (directed, unsorted rows) on the host
+    e = g.edges.astype(np.int64)
+    order = np.argsort(e[:, 0], kind="stable")
+    rowptr = np.zeros(g.n + 1, np.int64)
+    np.add.at(rowptr, e[:, 0] + 1, 1)
+    rowptr = np.cumsum(rowptr)
+    col = e[order, 1].astype(np.int32)
+    _assert_equal(pkg.evoke_orbits_csr(g.n, rowptr, col), ref, "csr host")
+    dev = torch.device("cuda:0")
+    out = pkg.evoke_orbits_edges(g.n, torch.from_numpy(g.edges).to(dev))
+    torch.cuda.synchronize()
+    _assert_equal(out.cpu().numpy(), ref, "edges device")
+    out = pkg.evoke_orbits_csr(g.n, torch.from_numpy(rowptr).to(dev), torch.from_numpy(col).to(dev))
+    torch.cuda.synchronize()
+    _assert_equal(out.cpu().numpy(), ref, "csr device")
+
+
+def test_sharded_partials_sum_to_full(pkg):
+    """multi-GPU decomposition on one device: partials of every shard sum (mod 2^64) to
+    the full matrix bit for bit"""
+    for g in [graphgen.erdos_renyi(200, 0.08, 41), graphgen.config(2)]:
+        full = pkg.evoke_orbits_edges(g.n, g.edges)
+        for ns in (2, 3):
+            acc = np.zeros_like(full)
+            for si in range(ns):
+                acc += pkg.evoke_orbits_edges(g.n, g.edges, shard_index=si, num_shards=ns)
+            _assert_equal(acc, full, f"{g.name} shards={ns}")
+
+
+def test_deterministic(pkg):
+    g = graphgen.config(2)
+    a = pkg.evoke_orbits_edges(g.n, g.edges)
+    b = pkg.evoke_orbits_edges(g.n, g.edges)
+    _assert_equal(a, b, "repeat")
+
+
+# ---------------------------------------------------------- closed forms at scale ---
+def _row(**kw):
+    r = np.zeros(73, dtype=object)
+    for k, v in kw.items():
+        r[int(k[1:])] = v % (1 << 64)
+    return r
+
+
+def _rows_equal(got_row, exp_row):
+    return [int(x) for x in got_row] == [int(x) for x in exp_row]
+
+
+def test_closed_form_star_wraps_modulo_2_64(pkg):
+    """K_{1,s} with s >= 145,057: C(s,4) >= 2^64, the hub row must be exact mod 2^64 (R20)"""
+    s = 145_100
+    assert comb(s, 4) >= 1 << 64
+    g = graphgen.star(s)
+    out = pkg.evoke_orbits_edges(g.n, g.edges)
+    assert _rows_equal(out[0], _row(t0=s, t2=comb(s, 2), t7=comb(s, 3), t23=comb(s, 4)))
+    leaf = _row(t0=1, t1=s - 1, t6=comb(s - 1, 2), t22=comb(s - 1, 3))
+    for v in (1, 2, s // 2, s):
+        assert _rows_equal(out[v], leaf)
+
+
+def test_closed_form_complete_and_cycle_and_bipartite(pkg):
+    n = 48
+    out = pkg.evoke_orbits_edges(n, graphgen.complete(n).edges)
+    exp = _row(t0=n - 1, t3=comb(n - 1, 2), t14=comb(n - 1, 3), t72=comb(n - 1, 4))
+    assert all(_rows_equal(out[v], exp) for v in range(n))
+    n = 100_003
+    out = pkg.evoke_orbits_edges(n, graphgen.cycle(n).edges)
+    exp = _row(t0=2, t1=2, t2=1, t4=2, t5=2, t15=2, t16=2, t17=1)
+    assert (out == np.array([int(x) for x in exp], dtype=np.uint64)).all()
+    a, b = 9, 700
+    out = pkg.evoke_orbits_edges(a + b, graphgen.complete_bipartite(a, b).edges)
+
+    def side(a, b):
+        return _row(t0=b, t1=(a - 1) * b, t2=comb(b, 2), t6=b * comb(a - 1, 2), t7=comb(b, 3),
+                    t8=(a - 1) * comb(b, 2), t22=b * comb(a - 1, 3), t23=comb(b, 4),
+                    t49=comb(a - 1, 2) * comb(b, 2), t50=(a - 1) * comb(b, 3))
+    assert all(_rows_equal(out[v], side(a, b)) for v in range(a))
+    assert all(_rows_equal(out[v], side(b, a)) for v in range(a, a + b))
+
+
+# ------------------------------------------------------ full-matrix parity at scale ---
+def test_tiled_graph_full_matrix(pkg):
+    """~1.2M-edge disjoint union of seeded G(40, 0.15) tiles: the oracle solves only the
+    64 distinct tiles; the CUDA result must equal the tiled oracle matrix everywhere"""
+    tiles = [graphgen.erdos_renyi(40, 0.15, 77 * 1000 + i) for i in range(64)]
+    refs = [oracle.orbits(t.n, t.edges) for t in tiles]
+    rng = np.random.default_rng(77)
+    pick = rng.integers(0, 64, size=10_000)
+    g, offs = graphgen.disjoint_union([tiles[i] for i in pick], "tiled")
+    exp = np.concatenate([refs[i] for i in pick], axis=0)
+    assert g.edges.shape[0] > 1_000_000
+    _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), exp, "tiled")
+
+
+# ----------------------------------------------- BASELINE configs: rows + invariants ---
+def _invariants(g, out, check_cliques=True):
+    e = np.unique(np.sort(g.edges.astype(np.int64), axis=1), axis=0)
+    e = e[e[:, 0] != e[:, 1]]
+    deg = np.bincount(e.ravel(), minlength=g.n).astype(np.uint64)
+    assert (out[:, 0] == deg).all(), "orbit 0 = degree"
+    cat = oracle.catalog()
+    colsum = [int(x) for x in out.sum(axis=0, dtype=np.uint64)]  # mod 2^64
+    for P in cat:
+        orbs = sorted(set(P["orb"]))
+        sz = {o: P["orb"].count(o) for o in orbs}
+        for a in orbs:
+            for b in orbs:
+                assert (sz[b] * colsum[a] - sz[a] * colsum[b]) % (1 << 64) == 0, (a, b)
+    if check_cliques:
+        t3, t4, t5 = oracle.clique_totals(g.n, g.edges, threads=0)
+        assert colsum[3] == (3 * t3) % (1 << 64)
+        assert colsum[14] == (4 * t4) % (1 << 64)
+        assert colsum[72] == (5 * t5) % (1 << 64)
+
+
+def _sampled_rows(g, out, k, seed, cap):
+    rng = np.random.default_rng(seed)
+    roots = rng.choice(g.n, size=min(k, g.n), replace=False)
+    rows, st = oracle.orbit_rows(g.n, g.edges, roots, cap=cap)
+    done = 0
+    for r, row, s in zip(roots, rows, st):
+        if s == 0:
+            assert (out[r] == row).all(), f"row {r}"
+            done += 1
+    return done
+
+
+def test_config2_bench_size_rows_and_invariants(pkg):
+    g = graphgen.config(2)
+    out = pkg.evoke_orbits_edges(g.n, g.edges)
+    _invariants(g, out)
+    done = _sampled_rows(g, out, 400, 2, cap=3_000_000)
+    assert done >= 20, done
+
+
+def test_config2_low_degree_core_full_matrix(pkg):
+    """the config-2 subgraph induced by its vertices of degree <= 12: same generator and
+    degree tail cut, small enough for the full ESU oracle at n = 1e5"""
+    g = graphgen.config(2)
+    e = np.unique(np.sort(g.edges.astype(np.int64), axis=1), axis=0)
+    e = e[e[:, 0] != e[:, 1]]
+    deg = np.bincount(e.ravel(), minlength=g.n)
+    keep = deg <= 12
+    e = e[keep[e[:, 0]] & keep[e[:, 1]]].astype(np.int32)
+    _assert_equal(pkg.evoke_orbits_edges(g.n, e), oracle.orbits(g.n, e), "config2 core")
+
+
+def test_config3_rows_and_invariants(pkg):
+    g = graphgen.config(3)
+    out = pkg.evoke_orbits_edges(g.n, g.edges)
+    _invariants(g, out, check_cliques=False)
+    _sampled_rows(g, out, 64, 3, cap=2_000_000)
