@@ -312,6 +312,8 @@ static void credit(const graph_t *g, const int *S, int k, uint64_t *out) {
 /* ------------------------------------------------------------------------- */
 typedef struct {
   const graph_t *g;
+  int32_t *buf[6];     /* extension set of each depth, capacity cap_ext */
+  int64_t cap_ext;
   uint64_t *out;       /* n*73 accumulator, or NULL (rooted mode)  */
   uint64_t *row;       /* rooted mode: 73 accumulator for S[0]     */
   int root_filter;     /* 1: only extend with ids > root            */
@@ -329,7 +331,7 @@ static int adjacent_to_set(const graph_t *g, const int *S, int k, int x) {
   return 0;
 }
 
-static void esu_extend(esu_ctx *c, int *S, int k, int *ext, int next) {
+static void esu_extend(esu_ctx *c, int *S, int k, int32_t *ext, int64_t next) {
   if (c->aborted) return;
   if (k >= 2) {
     if (c->out) credit(c->g, S, k, c->out);
@@ -345,25 +347,38 @@ static void esu_extend(esu_ctx *c, int *S, int k, int *ext, int next) {
   int root = S[0];
   /* Wernicke's ESU: pick w from the extension set; the new extension set is
    * the rest of the old one plus the exclusive neighbours of w. */
+  int32_t *ext2 = c->buf[k];
   while (next > 0) {
     int w = ext[--next];
-    int ext2[4096];
-    int n2 = 0;
-    for (int i = 0; i < next; i++) ext2[n2++] = ext[i];
+    int64_t n2 = 0;
+    for (int64_t i = 0; i < next; i++) ext2[n2++] = ext[i];
     S[k] = w;
     for (int64_t p = g->rp[w]; p < g->rp[w + 1]; p++) {
       int u = g->adj[p];
       if (c->root_filter && u <= root) continue;
       if (in_set(S, k + 1, u)) continue;
       if (adjacent_to_set(g, S, k, u)) continue;  /* u in N(S) => not exclusive */
-      if (in_set(ext2, n2, u)) continue;
-      if (n2 >= 4096) { c->aborted = 2; return; }
+      if (n2 >= c->cap_ext) { c->aborted = 2; return; }
       ext2[n2++] = u;
     }
     esu_extend(c, S, k + 1, ext2, n2);
     if (c->aborted) return;
   }
 }
+
+/* per-depth extension buffers: an extension set holds at most the exclusive
+ * neighbourhoods of the (<= 4) vertices added so far */
+static int ctx_alloc(esu_ctx *c, const graph_t *g) {
+  int64_t dmax = 0;
+  for (int64_t v = 0; v < g->n; v++) if (g->rp[v + 1] - g->rp[v] > dmax) dmax = g->rp[v + 1] - g->rp[v];
+  c->cap_ext = 5 * dmax + 16;
+  for (int i = 0; i < 6; i++) {
+    c->buf[i] = (int32_t *)malloc(sizeof(int32_t) * (size_t)c->cap_ext);
+    if (!c->buf[i]) return -1;
+  }
+  return 0;
+}
+static void ctx_free(esu_ctx *c) { for (int i = 0; i < 6; i++) free(c->buf[i]); }
 
 /* Induced orbit counts of all vertices by ESU over all roots.
  * Returns 0, -1 (bad input), -2 (extension set overflow). */
@@ -381,22 +396,26 @@ int oracle_orbits_esu(int64_t n, int64_t m, const int32_t *edges, uint64_t *out,
 #pragma omp parallel
   {
     uint64_t *acc = (uint64_t *)calloc((size_t)n * NORB, sizeof(uint64_t));
-    esu_ctx c = {&g, acc, NULL, 1, 0, 0, 0};
+    esu_ctx c;
+    memset(&c, 0, sizeof(c));
+    c.g = &g; c.out = acc; c.root_filter = 1;
+    if (ctx_alloc(&c, &g)) c.aborted = 3;
 #pragma omp for schedule(dynamic, 1)
     for (int64_t r = 0; r < n; r++) {
+      if (c.aborted) continue;
       int S[5];
-      int ext[4096];
-      int ne = 0;
+      int64_t ne = 0;
       S[0] = (int)r;
       for (int64_t p = g.rp[r]; p < g.rp[r + 1]; p++)
-        if (g.adj[p] > r) { if (ne < 4096) ext[ne++] = g.adj[p]; else c.aborted = 2; }
-      if (!c.aborted) esu_extend(&c, S, 1, ext, ne);
+        if (g.adj[p] > r) c.buf[5][ne++] = g.adj[p];
+      esu_extend(&c, S, 1, c.buf[5], ne);
     }
 #pragma omp critical
     {
       if (c.aborted) status = -2;
       for (int64_t i = 0; i < n * NORB; i++) out[i] += acc[i];
     }
+    ctx_free(&c);
     free(acc);
   }
   graph_free(&g);
@@ -413,16 +432,16 @@ int oracle_orbit_row(int64_t n, int64_t m, const int32_t *edges, int64_t root,
   if (root < 0 || root >= n) return -1;
   if (graph_build(&g, n, m, edges)) return -1;
   memset(row, 0, sizeof(uint64_t) * NORB);
-  esu_ctx c = {&g, NULL, row, 0, 0, cap, 0};
+  esu_ctx c;
+  memset(&c, 0, sizeof(c));
+  c.g = &g; c.row = row; c.cap = cap;
+  if (ctx_alloc(&c, &g)) { graph_free(&g); return -2; }
   int S[5];
-  int ext[4096];
-  int ne = 0;
+  int64_t ne = 0;
   S[0] = (int)root;
-  for (int64_t p = g.rp[root]; p < g.rp[root + 1]; p++) {
-    if (ne >= 4096) { graph_free(&g); return -2; }
-    ext[ne++] = g.adj[p];
-  }
-  esu_extend(&c, S, 1, ext, ne);
+  for (int64_t p = g.rp[root]; p < g.rp[root + 1]; p++) c.buf[5][ne++] = g.adj[p];
+  esu_extend(&c, S, 1, c.buf[5], ne);
+  ctx_free(&c);
   graph_free(&g);
   if (c.aborted == 2) return -2;
   return c.aborted ? 1 : 0;
@@ -440,24 +459,26 @@ int oracle_orbit_rows(int64_t n, int64_t m, const int32_t *edges, int64_t nroots
 #else
   (void)threads;
 #endif
-#pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t i = 0; i < nroots; i++) {
-    int64_t root = roots[i];
-    uint64_t *row = rows + i * NORB;
-    memset(row, 0, sizeof(uint64_t) * NORB);
-    if (root < 0 || root >= n) { status[i] = -1; continue; }
-    esu_ctx c = {&g, NULL, row, 0, 0, cap, 0};
-    int S[5];
-    int ext[4096];
-    int ne = 0, bad = 0;
-    S[0] = (int)root;
-    for (int64_t p = g.rp[root]; p < g.rp[root + 1]; p++) {
-      if (ne >= 4096) { bad = 1; break; }
-      ext[ne++] = g.adj[p];
+#pragma omp parallel
+  {
+    esu_ctx c;
+    memset(&c, 0, sizeof(c));
+    int bad_alloc = ctx_alloc(&c, &g);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t i = 0; i < nroots; i++) {
+      int64_t root = roots[i];
+      uint64_t *row = rows + i * NORB;
+      memset(row, 0, sizeof(uint64_t) * NORB);
+      if (root < 0 || root >= n || bad_alloc) { status[i] = -1; continue; }
+      c.row = row; c.cap = cap; c.work = 0; c.aborted = 0; c.g = &g;
+      int S[5];
+      int64_t ne = 0;
+      S[0] = (int)root;
+      for (int64_t p = g.rp[root]; p < g.rp[root + 1]; p++) c.buf[5][ne++] = g.adj[p];
+      esu_extend(&c, S, 1, c.buf[5], ne);
+      status[i] = c.aborted == 2 ? -2 : (c.aborted ? 1 : 0);
     }
-    if (bad) { status[i] = -2; continue; }
-    esu_extend(&c, S, 1, ext, ne);
-    status[i] = c.aborted == 2 ? -2 : (c.aborted ? 1 : 0);
+    ctx_free(&c);
   }
   graph_free(&g);
   return 0;

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) k_cliques(
   __syncthreads();
   for (int idx = blockIdx.x; idx < nu; idx += gridDim.x) {
     const int32_t u = ulist[idx];
-    const bool in_shard = (idx % num_shards) == shard_index;
+    const bool in_shard = (u % num_shards) == shard_index;  // deterministic across calls
     const bool do_k5 = (MODE == 0) && in_shard;
     if (MODE == 0 && !do_k4 && !do_k5) continue;
     if (MODE == 1 && !in_shard) continue;

@@ -581,14 +581,16 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   if (ntri > 0) {
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
-    const size_t per_warp = (size_t)g.max_deg * 12;
-    int64_t warps = std::min<int64_t>((int64_t)SM * 32, std::max<int64_t>(8, (int64_t)(freeb / 4) / (int64_t)per_warp));
+    const size_t per_warp = (size_t)g.max_deg * 8;
+    int64_t warps = std::min<int64_t>((int64_t)SM * 24, std::max<int64_t>(8, (int64_t)(freeb / 4) / (int64_t)per_warp));
     int hb = 256;
     int hg = (int)std::max<int64_t>(1, warps / 8);
-    u64* tabs = A.alloc<u64>((size_t)hg * 8 * g.max_deg, true);
+    u32* tabs = A.alloc<u32>((size_t)hg * 8 * g.max_deg, true);
     int32_t* lists = A.alloc<int32_t>((size_t)hg * 8 * g.max_deg);
     int* counter = A.alloc<int>(1, true);
-    k_hublocal<<<hg, hb, 0, C.st>>>(g, Te, counter, 64, si, ns, tabs, lists, Fp(F_R68), Fp(F_R69));
+    const size_t hsm = (size_t)8 * HUB_SH_CAP * sizeof(u32);
+    CK(cudaFuncSetAttribute(k_hublocal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    k_hublocal<<<hg, hb, hsm, C.st>>>(g, Te, counter, 16, si, ns, tabs, lists, Fp(F_R68), Fp(F_R69));
     C.launches++;
     A.release(tabs); A.release(lists);
   }
