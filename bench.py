@@ -87,7 +87,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_sample(cfg_graph, target_deg=8):
+def cpu_sample(cfg_graph, target_deg=30):
     """Bounded sample of the workload for the CPU oracle: the subgraph of the config graph
     induced by its vertices of degree <= target_deg (same generator, tail cut)."""
     e = np.unique(np.sort(cfg_graph.edges.astype(np.int64), axis=1), axis=0)
@@ -98,7 +98,7 @@ def cpu_sample(cfg_graph, target_deg=8):
     return sub, f"config subgraph induced by vertices of degree <= {target_deg}: {sub.shape[0]} edges"
 
 
-def run_cpu_oracle(cfg_graph, steps=1, target_deg=8):
+def run_cpu_oracle(cfg_graph, steps=1, target_deg=30):
     import oracle
     threads = os.cpu_count() or 1
     sub, desc = cpu_sample(cfg_graph, target_deg)
@@ -139,7 +139,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-deg", type=int, default=8)
+    ap.add_argument("--cpu-deg", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -179,7 +179,7 @@ def main():
         step()
     torch.cuda.synchronize()
     # ---- device-resident timed steps (CUDA events on the launching stream)
-    times, pass_ms, launches = [], {}, 0
+    times, pass_ms, launches, lib_launches = [], {}, 0, 0
     st_last = None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -194,6 +194,7 @@ def main():
             barrier()
             times.append(e0.elapsed_time(e1))
             launches += st["kernel_launches"]
+            lib_launches += st["library_launches"]
             for k, v in st["ms_pass"].items():
                 pass_ms[k] = pass_ms.get(k, 0.0) + v / args.steps
             st_last = st
@@ -231,7 +232,10 @@ def main():
 
     # ---- roofline of the dominant pass (algorithmic bytes / its CUDA-event duration)
     peak, peak_src = load_peaks()
-    roof = roofline(g, st_last, pass_ms, peak, peak_src)
+    _, wm = pkg.evoke_orbits_edges(g.n, edges_dev, out=out_dev, shard_index=rank, num_shards=world,
+                                   stream=stream.cuda_stream, workmodel=True)
+    torch.cuda.synchronize()
+    roof = roofline(wm, pass_ms, peak, peak_src)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
@@ -244,6 +248,7 @@ def main():
                 "e2e": {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(g.edges.nbytes),
                         "d2h_bytes_per_step": int(g.n * 73 * 8)},
                 "gpu_launches": launches,
+                "library_launches": lib_launches,
                 "clocks": clk.summary(),
                 "roofline": roof,
                 "pass_ms": {k: round(v, 4) for k, v in pass_ms.items()}}
@@ -254,22 +259,23 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def roofline(g, st, pass_ms, peak_gbs, peak_src):
-    """Dominant pass and its achieved algorithmic GB/s."""
-    from paper_1911_10616_b200.workmodel import algorithmic_bytes
-    ab = algorithmic_bytes(g)
+def roofline(wm, pass_ms, peak_gbs, peak_src):
+    """Dominant pass and its achieved algorithmic GB/s: the
+    library's work model (units x bytes/unit, one untimed call) over the pass's mean
+    CUDA-event duration inside the timed steps."""
     compute_passes = {k: v for k, v in pass_ms.items() if k not in ("h2d", "d2h")}
     top = max(compute_passes, key=compute_passes.get)
     t = compute_passes[top] / 1e3
-    bytes_ = ab.get(top)
-    if bytes_ is None or t <= 0:
-        return {"bound": "hbm", "kernel": top, "achieved": None, "peak": peak_gbs, "unit": "GB/s",
-                "frac": None, "traffic": None, "peak_source": peak_src}
-    achieved = bytes_ / t / 1e9
-    return {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-            "frac": achieved / peak_gbs, "traffic": None, "algorithmic_bytes": bytes_,
+    bytes_ = wm["alg_bytes"].get(top, 0.0)
+    base = {"bound": "hbm", "kernel": top, "peak": peak_gbs, "unit": "GB/s", "traffic": None,
             "ms": compute_passes[top], "peak_source": peak_src,
-            "share_of_step": compute_passes[top] / sum(compute_passes.values())}
+            "share_of_step": compute_passes[top] / sum(compute_passes.values()), "units": wm["units"]}
+    if not bytes_ or t <= 0:
+        base.update({"achieved": None, "frac": None})
+        return base
+    achieved = bytes_ / t / 1e9
+    base.update({"achieved": achieved, "frac": achieved / peak_gbs, "algorithmic_bytes": bytes_})
+    return base
 
 
 if __name__ == "__main__":

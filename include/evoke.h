@@ -54,8 +54,17 @@ typedef struct evoke_stats {
   double ms_total;              /* whole call (device work, incl. H2D/D2H copies)    */
   double ms_pass[16];           /* per pass, see evoke_pass_name()                   */
   int32_t num_passes;
-  int32_t kernel_launches;      /* kernels this library launched in the call         */
+  int32_t kernel_launches;      /* kernels of this library launched in the call      */
+  int32_t library_launches;     /* CUB sort/scan/select launches in the call         */
+  int32_t reserved0;
+  /* work model (only with EVOKE_FLAG_WORKMODEL): algorithmic bytes per pass, i.e. units
+   * the pass must visit x bytes each visit must touch; 0 = not modelled */
+  double alg_bytes[16];
+  int64_t units[8];             /* sum d^2, sum T(e)^2, hub visits, c5 wedge visits,
+                                   c5 out-out visits, triangle-pass stream, -, -      */
 } evoke_stats;
+
+#define EVOKE_FLAG_WORKMODEL 1  /* fill evoke_stats.alg_bytes / units (extra kernels)  */
 
 typedef struct evoke_options {
   uint32_t struct_size;   /* sizeof(evoke_options): ABI versioning; 0 = defaults   */
@@ -68,6 +77,7 @@ typedef struct evoke_options {
                              the partials of all shards equals the full result bit
                              for bit (multi-GPU data parallelism)         */
   int32_t device;         /* CUDA device ordinal; -1 (default) = current device      */
+  int32_t flags;          /* EVOKE_FLAG_* bits; 0 default                            */
   void* stream;           /* cudaStream_t to run on; NULL = a library-owned stream   */
   evoke_stats* stats;     /* optional output                                         */
 } evoke_options;

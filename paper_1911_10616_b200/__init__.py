@@ -38,14 +38,18 @@ class _Stats(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("triangles", ctypes.c_int64),
                 ("max_degree", ctypes.c_int64), ("degeneracy", ctypes.c_int64), ("wedges", ctypes.c_int64),
                 ("ms_total", ctypes.c_double), ("ms_pass", ctypes.c_double * 16),
-                ("num_passes", ctypes.c_int32), ("kernel_launches", ctypes.c_int32)]
+                ("num_passes", ctypes.c_int32), ("kernel_launches", ctypes.c_int32),
+                ("library_launches", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("alg_bytes", ctypes.c_double * 16), ("units", ctypes.c_int64 * 8)]
 
 
 class _Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("induced", ctypes.c_int32),
                 ("device_pointers", ctypes.c_int32), ("shard_index", ctypes.c_int32),
-                ("num_shards", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("num_shards", ctypes.c_int32), ("device", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("stats", ctypes.POINTER(_Stats))]
+
+FLAG_WORKMODEL = 1
 
 
 _lock = threading.Lock()
@@ -103,9 +107,10 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def _make_options(induced, device_pointers, shard_index, num_shards, device, stream, stats):
+def _make_options(induced, device_pointers, shard_index, num_shards, device, stream, stats, flags=0):
     o = _Options()
     lib().evoke_default_options(ctypes.byref(o))
+    o.flags = flags
     o.induced = 1 if induced else 0
     o.device_pointers = 1 if device_pointers else 0
     o.shard_index = shard_index
@@ -121,7 +126,10 @@ def _stats_dict(s: _Stats) -> dict:
     return {"n": s.n, "m": s.m, "triangles": s.triangles, "max_degree": s.max_degree,
             "degeneracy": s.degeneracy, "wedges": s.wedges, "ms_total": s.ms_total,
             "ms_pass": {names[i]: s.ms_pass[i] for i in range(min(s.num_passes, len(names)))},
-            "kernel_launches": s.kernel_launches}
+            "alg_bytes": {names[i]: s.alg_bytes[i] for i in range(min(s.num_passes, len(names)))},
+            "units": {k: s.units[i] for i, k in enumerate(("sum_d2", "sum_te2", "hub", "c5_wedge", "c5_q",
+                                                           "tri_stream"))},
+            "kernel_launches": s.kernel_launches, "library_launches": s.library_launches}
 
 
 def _check(rc: int):
@@ -131,14 +139,15 @@ def _check(rc: int):
 
 
 def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_index: int = 0,
-                       num_shards: int = 1, stream=None, return_stats: bool = False):
+                       num_shards: int = 1, stream=None, return_stats: bool = False, workmodel: bool = False):
     """Orbit counts uint64[n, 73] of the simple graph given by undirected pairs ``edges``.
 
     ``edges``: int32 [m, 2] numpy array (host) or CUDA torch tensor (device).  Duplicates,
     reverse duplicates and self-loops are removed by the library.
     ``out``: optional preallocated numpy uint64 [n, 73] (host input) or torch int64/uint64
     CUDA tensor [n, 73] (device input)."""
-    st = _Stats() if return_stats else None
+    st = _Stats() if (return_stats or workmodel) else None
+    fl = FLAG_WORKMODEL if workmodel else 0
     if _is_torch(edges):
         import torch
         assert edges.is_cuda and edges.dtype == torch.int32, "device edges must be CUDA int32"
@@ -149,7 +158,7 @@ def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_inde
         assert out.is_cuda and out.is_contiguous() and out.numel() == n * NUM_ORBITS
         if stream is None:
             stream = torch.cuda.current_stream(e.device).cuda_stream
-        o = _make_options(induced, True, shard_index, num_shards, e.device.index, stream, st)
+        o = _make_options(induced, True, shard_index, num_shards, e.device.index, stream, st, fl)
         rc = lib().evoke_orbits_edges(n, m, e.data_ptr(), out.data_ptr(), ctypes.byref(o))
     else:
         e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
@@ -157,18 +166,19 @@ def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_inde
         if out is None:
             out = np.zeros((n, NUM_ORBITS), dtype=np.uint64)
         assert out.dtype == np.uint64 and out.flags.c_contiguous and out.size == n * NUM_ORBITS
-        o = _make_options(induced, False, shard_index, num_shards, None, stream, st)
+        o = _make_options(induced, False, shard_index, num_shards, None, stream, st, fl)
         rc = lib().evoke_orbits_edges(n, m, e.ctypes.data if m else None, out.ctypes.data, ctypes.byref(o))
     _check(rc)
-    if return_stats:
+    if return_stats or workmodel:
         return out, _stats_dict(st)
     return out
 
 
 def evoke_orbits_csr(n: int, rowptr, col, out=None, induced: bool = True, shard_index: int = 0,
-                     num_shards: int = 1, stream=None, return_stats: bool = False):
+                     num_shards: int = 1, stream=None, return_stats: bool = False, workmodel: bool = False):
     """Orbit counts from a CSR (rowptr int64[n+1], col int32[rowptr[n]]); same cleaning."""
-    st = _Stats() if return_stats else None
+    st = _Stats() if (return_stats or workmodel) else None
+    fl = FLAG_WORKMODEL if workmodel else 0
     if _is_torch(rowptr):
         import torch
         rp = rowptr.contiguous()
@@ -177,17 +187,17 @@ def evoke_orbits_csr(n: int, rowptr, col, out=None, induced: bool = True, shard_
             out = torch.empty((n, NUM_ORBITS), dtype=torch.int64, device=rp.device)
         if stream is None:
             stream = torch.cuda.current_stream(rp.device).cuda_stream
-        o = _make_options(induced, True, shard_index, num_shards, rp.device.index, stream, st)
+        o = _make_options(induced, True, shard_index, num_shards, rp.device.index, stream, st, fl)
         rc = lib().evoke_orbits_csr(n, rp.data_ptr(), cl.data_ptr(), out.data_ptr(), ctypes.byref(o))
     else:
         rp = np.ascontiguousarray(np.asarray(rowptr, dtype=np.int64))
         cl = np.ascontiguousarray(np.asarray(col, dtype=np.int32))
         if out is None:
             out = np.zeros((n, NUM_ORBITS), dtype=np.uint64)
-        o = _make_options(induced, False, shard_index, num_shards, None, stream, st)
+        o = _make_options(induced, False, shard_index, num_shards, None, stream, st, fl)
         rc = lib().evoke_orbits_csr(n, rp.ctypes.data, cl.ctypes.data if cl.size else None, out.ctypes.data,
                                     ctypes.byref(o))
     _check(rc)
-    if return_stats:
+    if return_stats or workmodel:
         return out, _stats_dict(st)
     return out

@@ -21,6 +21,7 @@
 #include "cycles5.cuh"
 #include "gather.cuh"
 #include "transform.cuh"
+#include "workmodel.cuh"
 
 #define EVOKE_VERSION "0.1.0-sm100a"
 
@@ -89,6 +90,7 @@ struct Ctx {
   cudaStream_t st;
   int dev, num_sms;
   int launches = 0;
+  int lib_launches = 0;
   cudaEvent_t ev[P_COUNT + 1];
   bool timing;
   void mark(int pass) {
@@ -119,7 +121,7 @@ void sort_keys_u64(Arena& A, Ctx& C, const u64* in, u64* out, int64_t N, int end
   void* t = A.alloc<char>(tb);
   CK(cub::DeviceRadixSort::SortKeys(t, tb, in, out, (int64_t)N, 0, end_bit, C.st));
   A.release(t);
-  C.launches += 4;
+  C.lib_launches += 4;
 }
 
 template <typename Tin, typename Tout>
@@ -129,7 +131,7 @@ void inclusive_sum(Arena& A, Ctx& C, const Tin* in, Tout* out, int64_t N) {
   void* t = A.alloc<char>(tb);
   CK(cub::DeviceScan::InclusiveSum(t, tb, in, out, N, C.st));
   A.release(t);
-  C.launches += 2;
+  C.lib_launches += 2;
 }
 
 int bits_for(int64_t x) {
@@ -558,22 +560,21 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     A.release(t); A.release(wk); A.release(wk2); A.release(vv);
   }
   if (n > 0 && m > 0 && nshard > 0) {
-    // per-CTA dense tables: W u32, D u32, TT u64, F u8, list i32  (21 bytes / vertex)
+    // per-CTA dense tables: W u32, D u32, F u8, list i32  (13 bytes / vertex)
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
-    const size_t per = (size_t)n * 21;
+    const size_t per = (size_t)n * 13;
     int pg = std::min<int64_t>(2 * SM, std::max<int64_t>(1, (int64_t)(freeb / 3) / (int64_t)per));
     pg = std::min(pg, nshard);
     u32* Wt = A.alloc<u32>((size_t)pg * n, true);
     u32* Dt = A.alloc<u32>((size_t)pg * n, true);
-    u64* TTt = A.alloc<u64>((size_t)pg * n, true);
     uint8_t* Ft = A.alloc<uint8_t>((size_t)pg * n, true);
     int32_t* Lt = A.alloc<int32_t>((size_t)pg * n);
     int* counter = A.alloc<int>(1, true);
     PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e};
-    k_pairs<<<pg, 512, 0, C.st>>>(g, Te, shard_list, nshard, counter, Wt, Dt, TTt, Ft, Lt, po);
+    k_pairs<<<pg, 512, 0, C.st>>>(g, Te, shard_list, nshard, counter, Wt, Dt, Ft, Lt, po);
     C.launches++;
-    A.release(Wt); A.release(Dt); A.release(TTt); A.release(Ft); A.release(Lt);
+    A.release(Wt); A.release(Dt); A.release(Ft); A.release(Lt);
   }
 
   // ------------------------------------------------------------------ a8: hub-local
@@ -655,9 +656,6 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     evoke_stats* s = o.stats;
     std::memset(s, 0, sizeof(*s));
     s->n = n; s->m = m; s->triangles = ntri; s->max_degree = max_deg; s->degeneracy = max_out;
-    u64* dw = A.alloc<u64>(1, true);
-    if (n > 0) k_wedges<<<grid_for(n, B, SM), B, 0, C.st>>>(rp, n, dw);
-    s->wedges = (int64_t)d2h_scalar<u64>(dw, C.st);
     s->num_passes = P_COUNT;
     for (int i = 0; i < P_COUNT; i++) {
       float ms = 0;
@@ -668,6 +666,25 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaEventElapsedTime(&tot, C.ev[0], C.ev[P_COUNT]));
     s->ms_total = tot;
     s->kernel_launches = C.launches;
+    s->library_launches = C.lib_launches;
+    u64* dw = A.alloc<u64>(1, true);
+    if (n > 0) k_wedges<<<grid_for(n, B, SM), B, 0, C.st>>>(rp, n, dw);
+    s->wedges = (int64_t)d2h_scalar<u64>(dw, C.st);
+    if ((o.flags & EVOKE_FLAG_WORKMODEL) && n > 0) {
+      WorkUnits* du = A.alloc<WorkUnits>(1, true);
+      k_units_vertex<<<grid_for(n, B, SM), B, 0, C.st>>>(g, du);
+      if (m > 0) k_units_edge<<<grid_for(m, B, SM), B, 0, C.st>>>(g, Te, du);
+      if (ntri > 0) k_units_hub<<<grid_for(m2, B, SM), B, 0, C.st>>>(g, Te, du);
+      WorkUnits hu = d2h_scalar<WorkUnits>(du, C.st);
+      s->units[0] = (int64_t)hu.sum_d2; s->units[1] = (int64_t)hu.sum_te2; s->units[2] = (int64_t)hu.hub;
+      s->units[3] = (int64_t)hu.c5_wedge; s->units[4] = (int64_t)hu.c5_q; s->units[5] = (int64_t)hu.tri_stream;
+      // bytes per unit: DESIGN.md section 8(d)
+      s->alg_bytes[P_TRI] = 8.0 * (double)hu.tri_stream + 16.0 * (double)ntri;
+      s->alg_bytes[P_PAIR] = 32.0 * (double)hu.sum_d2 + 28.0 * (double)hu.sum_te2;
+      s->alg_bytes[P_HUB] = 28.0 * (double)hu.hub;
+      s->alg_bytes[P_C5] = 40.0 * (double)hu.c5_wedge + 84.0 * (double)hu.c5_q;
+      s->alg_bytes[P_TRIG] = 16.0 * (double)ntri + 3.0 * 14.0 * 16.0 * (double)ntri;
+    }
   }
 }
 
@@ -730,6 +747,7 @@ void evoke_default_options(evoke_options* opt) {
   opt->device = -1;
   opt->stream = nullptr;
   opt->stats = nullptr;
+  opt->flags = 0;
 }
 
 int evoke_orbits_edges(int64_t n, int64_t m, const int32_t* edges, uint64_t* out, const evoke_options* opt) {

@@ -3,8 +3,9 @@
 // One CTA per source u holds, for every x at distance <= 2, the pair quantities of
 // Theorem B.1 (readings R11, R14):
 //   W(u,x)  = |N(u) & N(x)|                       (2-hop expansion, phase A)
-//   TTs(u,x)= sum_{v in N(u)&N(x)} T(v,x)          (phase A; TT = TTs - W*[u~x], R14)
 //   D(u,x)  = #edges inside N(u) & N(x)            (diamond expansion, phase B)
+// TT(u,x) = sum_{v in N(u)&N(x)} T(v,x) - W[u~x] (R14) enters theta51 only through
+// sum_x TT(u,x)(W-1), which is summed per wedge in phase D once W is final (no table).
 // and emits:  C4(u)=DM8, theta36, theta50, theta51, theta63 for u (phase C);
 //   E5 = C4(u,v) = sum_{x in N(v)\u} (W(u,x)-1) per edge, and the centre credits
 //   theta49(v) += C(W(u,x)-1,2), theta62(v) += D(u,x) for x>u in N(v) (phase D);
@@ -27,9 +28,8 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 __global__ void __launch_bounds__(512) k_pairs(DGraph g, const u32* __restrict__ Te,
                                                const int32_t* __restrict__ srcs, int nsrc,
                                                int* __restrict__ counter, u32* __restrict__ Wt,
-                                               u32* __restrict__ Dt, u64* __restrict__ TTt,
-                                               uint8_t* __restrict__ Ft, int32_t* __restrict__ Lt,
-                                               PairOut o) {
+                                               u32* __restrict__ Dt, uint8_t* __restrict__ Ft,
+                                               int32_t* __restrict__ Lt, PairOut o) {
   __shared__ int s_idx;
   __shared__ int s_ntouch;
   __shared__ u64 s_red[5];
@@ -37,7 +37,6 @@ __global__ void __launch_bounds__(512) k_pairs(DGraph g, const u32* __restrict__
   const size_t off = (size_t)blockIdx.x * (size_t)g.n;
   u32* W = Wt + off;
   u32* D = Dt + off;
-  u64* TT = TTt + off;
   uint8_t* F = Ft + off;
   int32_t* L = Lt + off;
   if (threadIdx.x == 0) { s_ntouch = 0; for (int t = 0; t < 5; t++) s_red[t] = 0; }
@@ -57,7 +56,6 @@ __global__ void __launch_bounds__(512) k_pairs(DGraph g, const u32* __restrict__
         if (x == u) continue;
         const u32 old = atomicAdd(&W[x], 1u);
         if (old == 0) L[atomicAdd(&s_ntouch, 1)] = x;
-        atomicAdd(&TT[x], (u64)Te[g.eid[t]]);
       }
     }
     // ---- phase B: diamonds with u and x off the chord (v,w), v<w
@@ -87,7 +85,7 @@ __global__ void __launch_bounds__(512) k_pairs(DGraph g, const u32* __restrict__
         a8 += c2;
         a36 += c2 * (u64)(int64_t)(dg_deg(g, x) - 2);
         a50 += binom3(w);
-        a51 += (TT[x] - w * (u64)F[x]) * (w - 1);
+        a51 -= (u64)F[x] * w * (w - 1);
         a63 += (u64)D[x] * (w - 2);
       }
       a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a51 = warp_sum(a51); a63 = warp_sum(a63);
@@ -101,19 +99,21 @@ __global__ void __launch_bounds__(512) k_pairs(DGraph g, const u32* __restrict__
       const int32_t v = g.ci[s];
       const int32_t euv = g.eid[s];
       const int64_t rev = (u < v) ? slot_of_lo_in_hi(g, euv) : slot_of_hi_in_lo(g, euv);
-      u64 s5 = 0, s49 = 0, s62 = 0;
+      u64 s5 = 0, s49 = 0, s62 = 0, s51 = 0;
       for (int64_t t = g.rp[v] + lane; t < g.rp[v + 1]; t += 32) {
         if (t == rev) continue;
         const int32_t x = g.ci[t];
         const u64 w = W[x];
         s5 += w - 1;
+        s51 += (u64)Te[g.eid[t]] * (w - 1);
         if (t > rev) {
           s49 += binom2(w - 1);
           s62 += D[x];
         }
       }
-      s5 = warp_sum(s5); s49 = warp_sum(s49); s62 = warp_sum(s62);
+      s5 = warp_sum(s5); s49 = warp_sum(s49); s62 = warp_sum(s62); s51 = warp_sum(s51);
       if (lane == 0) {
+        if (s51) atomicAdd(&s_red[3], s51);
         if (u < v) o.C4e[euv] = s5;
         if (s49) atomicAdd(&o.R49[v], s49);
         if (s62) atomicAdd(&o.R62[v], s62);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(512) k_pairs(DGraph g, const u32* __restrict__
     // ---- reset
     for (int t = threadIdx.x; t < ntouch; t += blockDim.x) {
       const int32_t x = L[t];
-      W[x] = 0; D[x] = 0; TT[x] = 0;
+      W[x] = 0; D[x] = 0;
     }
     for (int64_t s = r0 + threadIdx.x; s < r1; s += blockDim.x) F[g.ci[s]] = 0;
     __syncthreads();
