@@ -79,8 +79,9 @@ def orbits(n: int, edges, threads: int = 0) -> np.ndarray:
 def orbit_rows(n: int, edges, roots, cap: int = 0, threads: int = 0):
     """Exact rows DIM(r, .) for the given roots by rooted ESU.
 
-    Returns (rows uint64[len(roots), 73], status int[len(roots)]); status 0 = exact,
-    1 = work cap hit (row incomplete, must not be compared), <0 = error."""
+    ``cap`` bounds the work per root (connected sets visited + extension-set elements
+    built).  Returns (rows uint64[len(roots), 73], status int[len(roots)]); status 0 =
+    exact, 1 = work cap hit (row incomplete, must not be compared), <0 = error."""
     lib = _load()
     e = _edges(edges)
     r = np.ascontiguousarray(np.asarray(roots, dtype=np.int64))

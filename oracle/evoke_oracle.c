@@ -361,6 +361,10 @@ static void esu_extend(esu_ctx *c, int *S, int k, int32_t *ext, int64_t next) {
       if (n2 >= c->cap_ext) { c->aborted = 2; return; }
       ext2[n2++] = u;
     }
+    if (!c->out) {  /* rooted mode: the cap bounds work (sets + extension elements) */
+      c->work += (uint64_t)n2;
+      if (c->cap && c->work >= c->cap) { c->aborted = 1; return; }
+    }
     esu_extend(c, S, k + 1, ext2, n2);
     if (c->aborted) return;
   }

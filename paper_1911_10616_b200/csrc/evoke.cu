@@ -559,22 +559,52 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (nshard < 0) nshard = 0;
     A.release(t); A.release(wk); A.release(wk2); A.release(vv);
   }
-  if (n > 0 && m > 0 && nshard > 0) {
-    // per-CTA dense tables: W u32, D u32, F u8, list i32  (13 bytes / vertex)
-    size_t freeb = 0, totalb = 0;
-    CK(cudaMemGetInfo(&freeb, &totalb));
-    const size_t per = (size_t)n * 13;
-    int pg = std::min<int64_t>(2 * SM, std::max<int64_t>(1, (int64_t)(freeb / 3) / (int64_t)per));
-    pg = std::min(pg, nshard);
-    u32* Wt = A.alloc<u32>((size_t)pg * n, true);
-    u32* Dt = A.alloc<u32>((size_t)pg * n, true);
-    uint8_t* Ft = A.alloc<uint8_t>((size_t)pg * n, true);
-    int32_t* Lt = A.alloc<int32_t>((size_t)pg * n);
-    int* counter = A.alloc<int>(1, true);
+  if (n > 0 && m > 0) {
+    // source lists by 2-hop estimate (descending), sharded by position
+    u64* pk = A.alloc<u64>(n);
+    u64* pk2 = A.alloc<u64>(n);
+    int32_t* pv = A.alloc<int32_t>(n);
+    int32_t* pv2 = A.alloc<int32_t>(n);
+    int32_t* plist = A.alloc<int32_t>(n);
+    u32* pest = A.alloc<u32>(n);
+    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, pk, pv);
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
+    void* t = A.alloc<char>(tb);
+    CK(cub::DeviceRadixSort::SortPairs(t, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
+    k_pair_lists<<<grid_for(n, B, SM), B, 0, C.st>>>(pk2, pv2, n, si, ns, plist, pest);
+    C.launches += 2;
+    C.lib_launches += 4;
+    const int np = (n - si + ns - 1) / ns;
+    std::vector<u32> hest(np > 0 ? np : 1);
+    if (np > 0) CK(cudaMemcpyAsync(hest.data(), pest, sizeof(u32) * np, cudaMemcpyDeviceToHost, C.st));
+    CK(cudaStreamSynchronize(C.st));
+    int nbig = 0;
+    while (nbig < np && hest[nbig] > PAIR_HASH_CAP / 2) nbig++;
     PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e};
-    k_pairs<<<pg, 512, 0, C.st>>>(g, Te, shard_list, nshard, counter, Wt, Dt, Ft, Lt, po);
-    C.launches++;
-    A.release(Wt); A.release(Dt); A.release(Ft); A.release(Lt);
+    if (nbig > 0) {
+      // dense packed tables: keep them L2-resident (~64 MB) but use >= 1 CTA per SM
+      const int64_t l2_ctas = std::max<int64_t>(1, (64ll << 20) / ((int64_t)n * 8));
+      int pg = (int)std::min<int64_t>(std::max<int64_t>(l2_ctas, SM), 2 * SM);
+      pg = std::min(pg, nbig);
+      size_t freeb = 0, totalb = 0;
+      CK(cudaMemGetInfo(&freeb, &totalb));
+      pg = (int)std::max<int64_t>(1, std::min<int64_t>(pg, (int64_t)(freeb / 3) / ((int64_t)n * 12)));
+      u64* tabs = A.alloc<u64>((size_t)pg * n, true);
+      int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
+      int* counter = A.alloc<int>(1, true);
+      k_pairs_global<<<pg, PAIR_THREADS, 0, C.st>>>(g, Te, plist, nbig, counter, tabs, lists, po);
+      C.launches++;
+      A.release(tabs); A.release(lists);
+    }
+    if (np - nbig > 0) {
+      const size_t psm = (size_t)3 * PAIR_HASH_CAP * sizeof(int32_t);
+      CK(cudaFuncSetAttribute(k_pairs_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+      int* counter = A.alloc<int>(1, true);
+      k_pairs_shared<<<SM, PAIR_THREADS, psm, C.st>>>(g, Te, plist + nbig, pest + nbig, np - nbig, counter, po);
+      C.launches++;
+    }
+    A.release(pk); A.release(pk2); A.release(pv); A.release(pv2); A.release(t);
   }
 
   // ------------------------------------------------------------------ a8: hub-local
