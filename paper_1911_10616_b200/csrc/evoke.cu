@@ -308,7 +308,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     m = (nsel > 0 && last == ~0ull) ? nsel - 1 : nsel;
     A.release(sk); A.release(t); A.release(keys);
   }
-  if (m >= (1ll << 31) - 1) { set_error("graph too large: m = %lld", (long long)m); throw EvokeError{EVOKE_EINTERNAL}; }
+  if (m >= (1ll << 30)) { set_error("graph too large: m = %lld (limit 2^30: slot ids are int32)", (long long)m); throw EvokeError{EVOKE_EINVAL}; }
   const int64_t m2 = 2 * m;
 
   // ------------------------------------------------------------------ a2: k-core order
@@ -610,20 +610,43 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // ------------------------------------------------------------------ a8: hub-local
   C.mark(P_HUB);
   if (ntri > 0) {
-    size_t freeb = 0, totalb = 0;
-    CK(cudaMemGetInfo(&freeb, &totalb));
-    const size_t per_warp = (size_t)g.max_deg * 8;
-    int64_t warps = std::min<int64_t>((int64_t)SM * 24, std::max<int64_t>(8, (int64_t)(freeb / 4) / (int64_t)per_warp));
-    int hb = 256;
-    int hg = (int)std::max<int64_t>(1, warps / 8);
-    u32* tabs = A.alloc<u32>((size_t)hg * 8 * g.max_deg, true);
-    int32_t* lists = A.alloc<int32_t>((size_t)hg * 8 * g.max_deg);
-    int* counter = A.alloc<int>(1, true);
-    const size_t hsm = (size_t)8 * HUB_SH_CAP * sizeof(u32);
-    CK(cudaFuncSetAttribute(k_hublocal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-    k_hublocal<<<hg, hb, hsm, C.st>>>(g, Te, counter, 16, si, ns, tabs, lists, Fp(F_R68), Fp(F_R69));
+    const int64_t m2s = 2 * m;
+    int32_t* light = A.alloc<int32_t>(m2s);
+    int32_t* heavy = A.alloc<int32_t>(m2s);
+    u32* hest = A.alloc<u32>(m2s);
+    int* hcnt = A.alloc<int>(4, true);
+    k_hub_items<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, si, ns, light, hcnt, heavy, hest, hcnt + 1);
     C.launches++;
-    A.release(tabs); A.release(lists);
+    int hc[2];
+    CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));
+    CK(cudaStreamSynchronize(C.st));
+    const int n_light = hc[0], n_heavy = hc[1];
+    int32_t* heavy_sorted = heavy;
+    if (n_heavy > 1) {
+      int32_t* hs = A.alloc<int32_t>(n_heavy);
+      u32* hk = A.alloc<u32>(n_heavy);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, hest, hk, heavy, hs, n_heavy, 0, 32, C.st));
+      void* t = A.alloc<char>(tb);
+      CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, hest, hk, heavy, hs, n_heavy, 0, 32, C.st));
+      C.lib_launches += 4;
+      heavy_sorted = hs;
+    }
+    if (n_light + n_heavy > 0) {
+      int hb_per_sm = 0;
+      CK(cudaFuncSetAttribute(k_hub_process, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_SMEM));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hb_per_sm, k_hub_process, HUB_BT, HUB_SMEM));
+      const int hg = std::max(1, hb_per_sm) * SM;
+      u32* gt = nullptr;
+      int32_t* gl = nullptr;
+      if (g.max_deg > HUB_SH_DENSE && n_heavy > 0) {
+        gt = A.alloc<u32>((size_t)hg * g.max_deg, true);
+        gl = A.alloc<int32_t>((size_t)hg * g.max_deg);
+      }
+      k_hub_process<<<hg, HUB_BT, HUB_SMEM, C.st>>>(g, Te, heavy_sorted, n_heavy, light, n_light, hcnt + 2, gt, gl,
+                                                      Fp(F_R68), Fp(F_R69));
+      C.launches++;
+    }
   }
 
   // ------------------------------------------------------------------ a10: 5-cycles

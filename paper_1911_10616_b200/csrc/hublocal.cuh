@@ -5,116 +5,321 @@
 //              = sum over hubs v in N(a) of the number of 4-cycles of G[N(v)] through a
 //   theta69(v) = 1/2 sum_{a,x in N(v)} C(|N(v)&N(a)&N(x)|, 2) = #4-cycles of G[N(v)]
 //
-// Work item = ordered pair (v, a), a in N(v) with T(v,a) >= 2: a is the TOP (highest
-// rank) vertex of the 4-cycles a-b-x-b' of G[N(v)] found from this item: a warp
-// enumerates b in N(v)&N(a) with b < a and x in N(v)&N(b) with x < a and counts
-// c(x) = #such b in a table indexed by x's position inside N(v) (shared memory when
-// d(v) is small, a warp-private global region otherwise).  Each 4-cycle of G[N(v)] is
-// found exactly once (from its top vertex, opposite x); its four corners are credited:
+// Work item = slot (v, a), a in N(v) with T(v,a) >= 2: a is the TOP (highest rank)
+// vertex of the 4-cycles a-b-x-b' of G[N(v)] found from this item: the item enumerates
+// b in N(v)&N(a) with b < a and x in N(v)&N(b) with x < a and counts c(x) = #such b.
+// Each 4-cycle of G[N(v)] is found exactly once (from its top vertex, opposite x); its
+// four corners are credited:
 //   a, x    : C(c(x), 2) each           (theta68)
 //   b (mid) : c(x) - 1 for every x      (theta68)
 //   v       : C(c(x), 2)                (theta69)  -- no division modulo 2^64 needed.
 // Restricting to cycles whose top is a (Chiba-Nishizeki) is what bounds the work.
+//
+// Scheduling (B200): k_hub_items measures every item's inner work
+//   est(v,a) = sum_{b in tri(v,a), b<a} T(v,b)
+// (warp-flattened over the triangle lists) and splits the items into a heavy list
+// (est > HUB_WARP_MAX, sorted by est, descending) and a light list.  k_hub_process is
+// persistent: its CTAs first take heavy items one CTA per item (block-flattened (b, x)
+// loop, c(x) in a dense shared table indexed by x's position in N(v), or a per-CTA
+// global one for hubs beyond the shared capacity), then every warp takes light items
+// (warp-flattened loop, c(x) in a per-warp shared hash keyed by x).  Work per lane is
+// balanced no matter how heavy-tailed T(e) is.
 #pragma once
 #include "common.cuh"
+#include "sched.cuh"
 
-#define HUB_SH_CAP 2048  // u32 table entries per warp in shared memory
+#define HUB_BT 256                                   // threads per CTA (8 warps)
+#define HUB_WARP_CAP 1024                            // per-warp hash capacity (light items)
+#define HUB_WARP_MAX (HUB_WARP_CAP / 2)              // light item: est <= this
+#define HUB_SMEM (HUB_BT / 32 * HUB_WARP_CAP * 12)   // 96 KB dynamic shared memory
+#define HUB_SH_DENSE (HUB_SMEM / 8)                  // heavy item: shared table if d(v) <= this
 
-__global__ void __launch_bounds__(256) k_hublocal(DGraph g, const u32* __restrict__ Te,
-                                                  int* __restrict__ counter, int chunk,
-                                                  int shard_index, int num_shards,
-                                                  u32* __restrict__ gtabs, int32_t* __restrict__ glists,
-                                                  u64* __restrict__ R68, u64* __restrict__ R69) {
-  extern __shared__ u32 sh_tab[];  // 8 warps * HUB_SH_CAP (dynamic, 64 KB)
-  __shared__ int s_cnt[8];
-  __shared__ int64_t s_base[8];
+// position of x inside N(v) given the edge id e(v,x)
+__device__ __forceinline__ int64_t pos_in_list(const DGraph& g, int32_t v, int32_t x, int32_t evx) {
+  return (v < x) ? ((int64_t)g.dm[v] + (evx - g.orow[v])) : (g.eslot_hi[evx] - g.rp[v]);
+}
+
+// ---- item measurement and binning ---------------------------------------------------
+__global__ void __launch_bounds__(256) k_hub_items(DGraph g, const u32* __restrict__ Te, int shard_index,
+                                                   int num_shards, int32_t* __restrict__ light, int* n_light,
+                                                   int32_t* __restrict__ heavy, u32* __restrict__ heavy_est,
+                                                   int* n_heavy) {
+  __shared__ u64 acc[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  u32* stab = sh_tab + wib * HUB_SH_CAP;
-  u32* gtab = gtabs + gw * (int64_t)g.max_deg;
-  int32_t* L = glists + gw * (int64_t)g.max_deg;
-  for (int t = lane; t < HUB_SH_CAP; t += 32) stab[t] = 0u;
-  const int64_t nslots = 2 * g.m;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t m2 = 2 * g.m;
+  acc[wib][lane] = 0;
+  __syncwarp();
+  for (int64_t base = gw * 32; base < m2; base += nw * 32) {
+    const int64_t s = base + lane;
+    int32_t a = 0, v = 0, eva = 0;
+    int len = 0;
+    int64_t fo = 0;
+    bool v_lo = false;
+    if (s < m2) {
+      eva = g.eid[s];
+      a = g.ci[s];
+      const int32_t lo = g.esrc[eva];
+      v = lo + g.edst[eva] - a;
+      v_lo = lo == v;
+      const u32 t = Te[eva];
+      if (t >= 2 && v % num_shards == shard_index) {
+        len = (int)t;
+        fo = g.foff[eva];
+      }
+    }
+    warp_flat(len, [&](int j, int k, bool valid) {
+      const int32_t aj = __shfl_sync(FULL_MASK, a, j);
+      const int64_t foj = __shfl_sync(FULL_MASK, fo, j);
+      const bool vloj = __shfl_sync(FULL_MASK, v_lo, j);
+      if (!valid) return;
+      const int64_t r = foj + k;
+      if (g.fx[r] < aj) {
+        const int32_t evb = vloj ? g.fe1[r] : g.fe2[r];
+        atomicAdd(&acc[wib][j], (u64)Te[evb]);
+      }
+    });
+    __syncwarp();
+    const u64 est = acc[wib][lane];
+    acc[wib][lane] = 0;
+    __syncwarp();
+    const bool is_light = est > 0 && est <= HUB_WARP_MAX;
+    const bool is_heavy = est > HUB_WARP_MAX;
+    warp_append(is_light, (int32_t)s, light, n_light);
+    const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
+    if (bal) {
+      int hb = 0;
+      const int leader = __ffs(bal) - 1;
+      if (lane == leader) hb = atomicAdd(n_heavy, __popc(bal));
+      hb = __shfl_sync(FULL_MASK, hb, leader);
+      if (is_heavy) {
+        const int q = hb + __popc(bal & ((1u << lane) - 1u));
+        heavy[q] = (int32_t)s;
+        heavy_est[q] = (u32)min(est, (u64)0xffffffffu);
+      }
+    }
+  }
+}
+
+// ---- heavy item: one CTA --------------------------------------------------------------
+struct HubCtaShared {
+  int64_t pre[HUB_BT + 1];
+  int64_t fb[HUB_BT];
+  int32_t b[HUB_BT];
+  int32_t evb[HUB_BT];
+  u64 acc[HUB_BT];
+  int cnt;
+  u64 r69;
+};
+
+__device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_t s, u32* shm, HubCtaShared& S,
+                             u32* __restrict__ gtab, int32_t* __restrict__ glist, u64* __restrict__ R68,
+                             u64* __restrict__ R69) {
+  const int32_t eva = g.eid[s];
+  const int32_t a = g.ci[s];
+  const int32_t lo_ = g.esrc[eva];
+  const int32_t v = lo_ + g.edst[eva] - a;
+  const bool v_lo = lo_ == v;
+  const int64_t rpv = g.rp[v];
+  const int32_t dv = (int32_t)(g.rp[v + 1] - rpv);
+  const bool dense_sh = dv <= HUB_SH_DENSE;
+  u32* tab = dense_sh ? shm : gtab;
+  int32_t* list = dense_sh ? (int32_t*)(shm + HUB_SH_DENSE) : glist;
+  const int64_t fa = g.foff[eva];
+  const int64_t na = g.foff[eva + 1] - fa;
+  if (threadIdx.x == 0) { S.cnt = 0; S.r69 = 0; }
+  S.acc[threadIdx.x] = 0;
+  __syncthreads();
+  auto load = [&](int64_t i) -> int64_t {
+    const int64_t r = fa + i;
+    const int32_t b = g.fx[r];
+    S.b[threadIdx.x] = b;
+    if (b >= a) return 0;
+    const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
+    const int64_t fb = g.foff[evb];
+    S.fb[threadIdx.x] = fb;
+    S.evb[threadIdx.x] = evb;
+    return g.foff[evb + 1] - fb;
+  };
+  // pass 1: c(x) for x < a over b < a
+  block_flat<HUB_BT>(na, S.pre, load,
+      [&](int li, int64_t k) {
+        const int64_t r2 = S.fb[li] + k;
+        const int32_t x = g.fx[r2];
+        if (x >= a) return;
+        const int32_t evb = S.evb[li];
+        const int32_t evx = (g.esrc[evb] == v) ? g.fe1[r2] : g.fe2[r2];
+        const int64_t p = pos_in_list(g, v, x, evx);
+        if (atomicAdd(&tab[p], 1u) == 0u) list[atomicAdd(&S.cnt, 1)] = (int32_t)p;
+      },
+      [&](int64_t, int) {});
+  // pass 2: middles b get sum_x (c(x) - 1)
+  block_flat<HUB_BT>(na, S.pre, load,
+      [&](int li, int64_t k) {
+        const int64_t r2 = S.fb[li] + k;
+        const int32_t x = g.fx[r2];
+        if (x >= a) return;
+        const int32_t evb = S.evb[li];
+        const int32_t evx = (g.esrc[evb] == v) ? g.fe1[r2] : g.fe2[r2];
+        const int64_t p = pos_in_list(g, v, x, evx);
+        atomicAdd(&S.acc[li], (u64)tab[p] - 1ull);
+      },
+      [&](int64_t, int cn) {
+        if ((int)threadIdx.x < cn) {
+          const u64 x = S.acc[threadIdx.x];
+          if (x) atomicAdd(&R68[S.b[threadIdx.x]], x);
+          S.acc[threadIdx.x] = 0;
+        }
+      });
+  // pass 3: corners a, x and the hub v
+  const int cnt = S.cnt;
+  u64 r69 = 0;
+  for (int t = threadIdx.x; t < cnt; t += HUB_BT) {
+    const int32_t p = list[t];
+    const u64 c2 = binom2(tab[p]);
+    tab[p] = 0u;
+    if (c2) {
+      r69 += c2;
+      atomicAdd(&R68[g.ci[rpv + p]], c2);
+    }
+  }
+  r69 = warp_sum(r69);
+  if ((threadIdx.x & 31) == 0 && r69) atomicAdd(&S.r69, r69);
+  __syncthreads();
+  if (threadIdx.x == 0 && S.r69) {
+    atomicAdd(&R69[v], S.r69);
+    atomicAdd(&R68[a], S.r69);
+  }
+  __syncthreads();
+}
+
+// ---- light item: one warp, per-warp shared hash keyed by x ----------------------------
+__device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32_t s, ShCount& H, int32_t* L,
+                              int* cnt, u64* acc, u64* __restrict__ R68, u64* __restrict__ R69) {
+  const int lane = threadIdx.x & 31;
+  const int32_t eva = g.eid[s];
+  const int32_t a = g.ci[s];
+  const int32_t lo_ = g.esrc[eva];
+  const int32_t v = lo_ + g.edst[eva] - a;
+  const bool v_lo = lo_ == v;
+  const int64_t fa = g.foff[eva];
+  const int na = (int)(g.foff[eva + 1] - fa);
+  for (int o0 = 0; o0 < na; o0 += 32) {
+    const int i = o0 + lane;
+    int len = 0;
+    int64_t fb = 0;
+    int32_t b = 0;
+    if (i < na) {
+      const int64_t r = fa + i;
+      b = g.fx[r];
+      if (b < a) {
+        const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
+        fb = g.foff[evb];
+        len = (int)(g.foff[evb + 1] - fb);
+      }
+    }
+    warp_flat(len, [&](int j, int k, bool valid) {
+      const int64_t fbj = __shfl_sync(FULL_MASK, fb, j);
+      if (!valid) return;
+      const int32_t x = g.fx[fbj + k];
+      if (x >= a) return;
+      const u32 h = H.insert(x);
+      if (atomicAdd(&H.val[h], 1u) == 0u) L[atomicAdd(cnt, 1)] = (int32_t)h;
+    });
+  }
+  __syncwarp();
+  for (int o0 = 0; o0 < na; o0 += 32) {
+    const int i = o0 + lane;
+    int len = 0;
+    int64_t fb = 0;
+    int32_t b = 0;
+    if (i < na) {
+      const int64_t r = fa + i;
+      b = g.fx[r];
+      if (b < a) {
+        const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
+        fb = g.foff[evb];
+        len = (int)(g.foff[evb + 1] - fb);
+      }
+    }
+    warp_flat(len, [&](int j, int k, bool valid) {
+      const int64_t fbj = __shfl_sync(FULL_MASK, fb, j);
+      if (!valid) return;
+      const int32_t x = g.fx[fbj + k];
+      if (x >= a) return;
+      atomicAdd(&acc[j], (u64)H.val[H.find(x)] - 1ull);
+    });
+    __syncwarp();
+    const u64 sb = acc[lane];
+    acc[lane] = 0;
+    if (sb) atomicAdd(&R68[b], sb);
+    __syncwarp();
+  }
+  const int c = *cnt;
+  u64 r69 = 0;
+  for (int t = lane; t < c; t += 32) {
+    const int32_t h = L[t];
+    const u64 c2 = binom2(H.val[h]);
+    if (c2) {
+      r69 += c2;
+      atomicAdd(&R68[H.keys[h]], c2);
+    }
+    H.keys[h] = SH_EMPTY;
+    H.val[h] = 0u;
+  }
+  r69 = warp_sum(r69);
+  if (lane == 0) {
+    if (r69) {
+      atomicAdd(&R69[v], r69);
+      atomicAdd(&R68[a], r69);
+    }
+    *cnt = 0;
+  }
+  __syncwarp();
+}
+
+// ---- persistent processing kernel -------------------------------------------------------
+__global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __restrict__ Te,
+                                                        const int32_t* __restrict__ heavy, int n_heavy,
+                                                        const int32_t* __restrict__ light, int n_light,
+                                                        int* __restrict__ counters, u32* __restrict__ gtabs,
+                                                        int32_t* __restrict__ glists, u64* __restrict__ R68,
+                                                        u64* __restrict__ R69) {
+  extern __shared__ u32 hub_sh[];
+  __shared__ HubCtaShared S;
+  __shared__ int s_idx;
+  __shared__ int s_cnt[HUB_BT / 32];
+  __shared__ u64 s_acc[HUB_BT / 32][32];
+  u32* gtab = gtabs ? gtabs + (size_t)blockIdx.x * g.max_deg : nullptr;
+  int32_t* glist = glists ? glists + (size_t)blockIdx.x * g.max_deg : nullptr;
+  for (int i = threadIdx.x; i < HUB_SH_DENSE; i += HUB_BT) hub_sh[i] = 0u;  // reset by pass 3 after use
+  for (;;) {
+    if (threadIdx.x == 0) s_idx = atomicAdd(&counters[0], 1);
+    __syncthreads();
+    const int idx = s_idx;
+    __syncthreads();
+    if (idx >= n_heavy) break;
+    hub_item_cta(g, Te, heavy[idx], hub_sh, S, gtab, glist, R68, R69);
+  }
+  // light items: the dynamic shared memory becomes one hash (keys, counts, list) per warp
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  ShCount H;
+  H.keys = (int32_t*)hub_sh + wib * (3 * HUB_WARP_CAP);
+  H.val = (u32*)(H.keys + HUB_WARP_CAP);
+  H.mask = HUB_WARP_CAP - 1;
+  int32_t* L = H.keys + 2 * HUB_WARP_CAP;
+  for (int t = lane; t < HUB_WARP_CAP; t += 32) { H.keys[t] = SH_EMPTY; H.val[t] = 0u; }
+  s_acc[wib][lane] = 0;
   if (lane == 0) s_cnt[wib] = 0;
   __syncwarp();
   for (;;) {
-    if (lane == 0) s_base[wib] = (int64_t)atomicAdd(counter, 1) * chunk;
-    __syncwarp();
-    const int64_t base = s_base[wib];
-    if (base >= nslots) break;
-    const int64_t end = min(base + (int64_t)chunk, nslots);
-    int64_t lo = 0, hi = g.n;  // v with rp[v] <= base < rp[v+1]
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (g.rp[mid] <= base) lo = mid; else hi = mid;
-    }
-    int32_t v = (int32_t)lo;
-    for (int64_t s = base; s < end; s++) {
-      while (g.rp[v + 1] <= s) v++;
-      if ((v % num_shards) != shard_index) continue;
-      const int32_t eva = g.eid[s];
-      if (Te[eva] < 2) continue;
-      const int32_t a = g.ci[s];
-      const bool v_lo = g.esrc[eva] == v;
-      const int64_t rpv = g.rp[v];
-      const int32_t dv = (int32_t)(g.rp[v + 1] - rpv);
-      u32* tab = (dv <= HUB_SH_CAP) ? stab : gtab;
-      // pass 1: c(x) for x < a over b < a
-      for (int64_t r = g.foff[eva]; r < g.foff[eva + 1]; r++) {
-        const int32_t b = g.fx[r];
-        if (b >= a) continue;
-        const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
-        const bool v_lo_b = g.esrc[evb] == v;
-        for (int64_t r2 = g.foff[evb] + lane; r2 < g.foff[evb + 1]; r2 += 32) {
-          const int32_t x = g.fx[r2];
-          if (x >= a) continue;
-          const int32_t evx = v_lo_b ? g.fe1[r2] : g.fe2[r2];
-          const int64_t p = (v < x) ? ((int64_t)g.dm[v] + (evx - g.orow[v])) : (g.eslot_hi[evx] - rpv);
-          const u32 old = atomicAdd(&tab[p], 1u);
-          if (old == 0) L[atomicAdd(&s_cnt[wib], 1)] = (int32_t)p;
-        }
-      }
-      __syncwarp();
-      const int cnt = s_cnt[wib];
-      if (cnt == 0) continue;
-      // pass 2: middles b get sum_x (c(x) - 1)
-      for (int64_t r = g.foff[eva]; r < g.foff[eva + 1]; r++) {
-        const int32_t b = g.fx[r];
-        if (b >= a) continue;
-        const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
-        const bool v_lo_b = g.esrc[evb] == v;
-        u64 sb = 0;
-        for (int64_t r2 = g.foff[evb] + lane; r2 < g.foff[evb + 1]; r2 += 32) {
-          const int32_t x = g.fx[r2];
-          if (x >= a) continue;
-          const int32_t evx = v_lo_b ? g.fe1[r2] : g.fe2[r2];
-          const int64_t p = (v < x) ? ((int64_t)g.dm[v] + (evx - g.orow[v])) : (g.eslot_hi[evx] - rpv);
-          sb += (u64)tab[p] - 1ull;
-        }
-        sb = warp_sum(sb);
-        if (lane == 0 && sb) atomicAdd(&R68[b], sb);
-      }
-      __syncwarp();
-      // pass 3: corners a, x and the hub v
-      u64 r69 = 0;
-      for (int t = lane; t < cnt; t += 32) {
-        const int32_t p = L[t];
-        const u64 c2 = binom2(tab[p]);
-        tab[p] = 0u;
-        if (c2) {
-          r69 += c2;
-          atomicAdd(&R68[g.ci[rpv + p]], c2);
-        }
-      }
-      r69 = warp_sum(r69);
-      if (lane == 0) {
-        if (r69) {
-          atomicAdd(&R69[v], r69);
-          atomicAdd(&R68[a], r69);
-        }
-        s_cnt[wib] = 0;
-      }
-      __syncwarp();
-    }
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(&counters[1], 4);
+    idx = __shfl_sync(FULL_MASK, idx, 0);
+    if (idx >= n_light) break;
+    const int end = min(idx + 4, n_light);
+    for (int q = idx; q < end; q++)
+      hub_item_warp(g, Te, light[q], H, L, &s_cnt[wib], s_acc[wib], R68, R69);
   }
 }

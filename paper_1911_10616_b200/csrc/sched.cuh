@@ -1,0 +1,132 @@
+// sched.cuh -- load-balancing building blocks shared by the enumeration passes.
+//
+// The passes are nested loops "for every outer item i, for every k < len(i)" whose inner
+// lengths are heavy-tailed (adjacency and triangle lists of hubs).  These helpers flatten
+// such a loop over the 32 lanes of a warp (warp_flat) or the threads of a CTA
+// (block_flat), so every lane gets one (i, k) pair per step no matter how the lengths
+// are distributed, and give small per-warp / per-CTA open-addressing tables in shared
+// memory for the pair-keyed counts (W, D, c(x), ...) the passes join on.
+#pragma once
+#include <cub/block/block_scan.cuh>
+#include "common.cuh"
+
+// ---------------------------------------------------------------------------------
+// warp_flat: the warp visits every (j, k) where j is a lane owning an outer item with
+// len_j = the lane's `len` argument and k < len_j.  All lanes call body(j, k, valid) in
+// lock-step (warp-uniform control flow), so the body may shuffle the owner's registers
+// (__shfl_sync(FULL_MASK, reg, j)) before testing `valid`.
+// ---------------------------------------------------------------------------------
+template <typename Body>
+__device__ __forceinline__ void warp_flat(int len, Body body) {
+  const int lane = threadIdx.x & 31;
+  int incl = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int total = __shfl_sync(FULL_MASK, incl, 31);
+  for (int t0 = 0; t0 < total; t0 += 32) {
+    const int t = t0 + lane;
+    // owner = number of lanes whose inclusive prefix is <= t (binary lifting)
+    int j = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const int c = __shfl_sync(FULL_MASK, incl, j + s - 1);
+      if (c <= t) j += s;
+    }
+    const int start = __shfl_sync(FULL_MASK, incl - len, j);
+    body(j, t - start, t < total);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// block_flat: the CTA visits every (i, k), i in [0, n_outer), k in [0, len(i)), in chunks
+// of BT outer items (one per thread).  pre[] is shared scratch of BT+1 int64 entries.
+//   load(i) -> len(i) (thread threadIdx.x loads outer item c0 + threadIdx.x and may stash
+//   payload in shared arrays indexed by threadIdx.x);  body(li, k) with li = i - c0;
+//   after(c0, cn) runs (all threads) after each chunk, between two barriers.
+// ---------------------------------------------------------------------------------
+template <int BT, typename Load, typename Body, typename After>
+__device__ __forceinline__ void block_flat(int64_t n_outer, int64_t* pre, Load load, Body body, After after) {
+  typedef cub::BlockScan<int64_t, BT> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  for (int64_t c0 = 0; c0 < n_outer; c0 += BT) {
+    const int cn = (int)min((int64_t)BT, n_outer - c0);
+    int64_t a = 0;
+    if ((int)threadIdx.x < cn) a = load(c0 + threadIdx.x);
+    int64_t ex, tot;
+    Scan(scan_tmp).ExclusiveSum(a, ex, tot);
+    pre[threadIdx.x] = ex;
+    if (threadIdx.x == 0) pre[BT] = tot;
+    __syncthreads();
+    const int64_t total = pre[BT];
+    for (int64_t t = threadIdx.x; t < total; t += BT) {
+      int lo = 0, hi = cn;  // largest lo with pre[lo] <= t
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] <= t) lo = mid; else hi = mid;
+      }
+      body(lo, t - pre[lo]);
+    }
+    __syncthreads();
+    after(c0, cn);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Open-addressing counter table in shared memory (keys int32, -1 = empty; one u32 count).
+// Linear probing; capacity is a power of two >= 2 x the number of distinct keys.
+// ---------------------------------------------------------------------------------
+#define SH_EMPTY (-1)
+struct ShCount {
+  int32_t* keys;
+  u32* val;
+  u32 mask;
+  __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) >> 7 & mask; }
+  __device__ __forceinline__ u32 insert(int32_t x) {
+    u32 h = h0(x);
+    for (;;) {
+      const int32_t k = keys[h];
+      if (k == x) return h;
+      if (k == SH_EMPTY) {
+        const int32_t old = atomicCAS(&keys[h], SH_EMPTY, x);
+        if (old == SH_EMPTY || old == x) return h;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+  __device__ __forceinline__ u32 find(int32_t x) const {
+    u32 h = h0(x);
+    while (keys[h] != x) h = (h + 1) & mask;
+    return h;
+  }
+  __device__ __forceinline__ u32 find_or_miss(int32_t x) const {  // mask+1 if absent
+    u32 h = h0(x);
+    for (;;) {
+      const int32_t k = keys[h];
+      if (k == x) return h;
+      if (k == SH_EMPTY) return mask + 1;
+      h = (h + 1) & mask;
+    }
+  }
+};
+
+__device__ __forceinline__ u32 pow2_at_least(u32 x, u32 lo) {
+  u32 c = lo;
+  while (c < x) c <<= 1;
+  return c;
+}
+
+// warp-aggregated append to a global list (one atomic per warp per call)
+__device__ __forceinline__ void warp_append(bool pred, int32_t val, int32_t* list, int* counter) {
+  const u32 bal = __ballot_sync(FULL_MASK, pred);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  const int leader = __ffs(bal) - 1;
+  if (lane == leader) base = atomicAdd(counter, __popc(bal));
+  base = __shfl_sync(FULL_MASK, base, leader);
+  if (pred) list[base + __popc(bal & ((1u << lane) - 1u))] = val;
+}
