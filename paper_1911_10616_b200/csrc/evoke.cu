@@ -76,6 +76,19 @@ struct Arena {
     if (zero) CK(cudaMemsetAsync(p, 0, bytes, st));
     return (T*)p;
   }
+  template <typename T>
+  T* alloc_on(cudaStream_t s, size_t count, bool zero = false) {
+    void* p = nullptr;
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+      set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+      throw EvokeError{EVOKE_ENOMEM};
+    }
+    ptrs.push_back(p);
+    if (zero) CK(cudaMemsetAsync(p, 0, bytes, s));
+    return (T*)p;
+  }
   void release(void* p) {
     for (auto& q : ptrs)
       if (q == p) { cudaFreeAsync(q, st); q = nullptr; }
@@ -92,7 +105,13 @@ struct Ctx {
   int launches = 0;
   int lib_launches = 0;
   cudaEvent_t ev[P_COUNT + 1];
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side_st = nullptr;
   bool timing;
+  cudaStream_t side() {
+    if (!side_st) CK(cudaStreamCreateWithFlags(&side_st, cudaStreamNonBlocking));
+    return side_st;
+  }
   void mark(int pass) {
     if (timing) CK(cudaEventRecord(ev[pass], st));
   }
@@ -219,15 +238,32 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   Ctx C;
   C.dev = dev;
   CK(cudaDeviceGetAttribute(&C.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  {
+    // keep freed scratch in the device's stream-ordered pool between calls (the default
+    // release threshold of 0 would unmap and remap gigabytes of tables on every call)
+    static bool pool_set[256] = {false};
+    if (dev < 256 && !pool_set[dev]) {
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t thr = ~0ull;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      pool_set[dev] = true;
+    }
+  }
   cudaStream_t own = nullptr;
   if (o.stream) C.st = (cudaStream_t)o.stream;
   else { CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking)); C.st = own; }
   C.timing = true;
   for (int i = 0; i <= P_COUNT; i++) CK(cudaEventCreate(&C.ev[i]));
+  CK(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
   struct Cleanup {
     Ctx& C; cudaStream_t own;
     ~Cleanup() {
       for (int i = 0; i <= P_COUNT; i++) cudaEventDestroy(C.ev[i]);
+      cudaEventDestroy(C.ev_fork);
+      cudaEventDestroy(C.ev_join);
+      if (C.side_st) { cudaStreamSynchronize(C.side_st); cudaStreamDestroy(C.side_st); }
       if (own) { cudaStreamSynchronize(own); cudaStreamDestroy(own); }
     }
   } cleanup{C, own};
@@ -560,50 +596,71 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     A.release(t); A.release(wk); A.release(wk2); A.release(vv);
   }
   if (n > 0 && m > 0) {
-    // source lists by 2-hop estimate (descending), sharded by position
+    // source lists by 2-hop estimate (descending), sharded by position, split in tiers
     u64* pk = A.alloc<u64>(n);
     u64* pk2 = A.alloc<u64>(n);
     int32_t* pv = A.alloc<int32_t>(n);
     int32_t* pv2 = A.alloc<int32_t>(n);
-    int32_t* plist = A.alloc<int32_t>(n);
     u32* pest = A.alloc<u32>(n);
+    int32_t* plists = A.alloc<int32_t>((size_t)PT_COUNT * n);
+    int* tiers = A.alloc<int>(8, true);
     k_pair_est<<<warp_grid, B, 0, C.st>>>(g, pk, pv);
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
     void* t = A.alloc<char>(tb);
     CK(cub::DeviceRadixSort::SortPairs(t, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
-    k_pair_lists<<<grid_for(n, B, SM), B, 0, C.st>>>(pk2, pv2, n, si, ns, plist, pest);
+    k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, Fp(F_T), pest, plists, tiers);
     C.launches += 2;
     C.lib_launches += 4;
-    const int np = (n - si + ns - 1) / ns;
-    std::vector<u32> hest(np > 0 ? np : 1);
-    if (np > 0) CK(cudaMemcpyAsync(hest.data(), pest, sizeof(u32) * np, cudaMemcpyDeviceToHost, C.st));
+    int ht[PT_COUNT];
+    CK(cudaMemcpyAsync(ht, tiers, sizeof(ht), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
-    int nbig = 0;
-    while (nbig < np && hest[nbig] > PAIR_HASH_CAP / 2) nbig++;
+    auto plist = [&](int tier) { return plists + (size_t)tier * n; };
     PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e};
-    if (nbig > 0) {
-      // dense packed tables: keep them L2-resident (~64 MB) but use >= 1 CTA per SM
-      const int64_t l2_ctas = std::max<int64_t>(1, (64ll << 20) / ((int64_t)n * 8));
-      int pg = (int)std::min<int64_t>(std::max<int64_t>(l2_ctas, SM), 2 * SM);
-      pg = std::min(pg, nbig);
-      size_t freeb = 0, totalb = 0;
-      CK(cudaMemGetInfo(&freeb, &totalb));
-      pg = (int)std::max<int64_t>(1, std::min<int64_t>(pg, (int64_t)(freeb / 3) / ((int64_t)n * 12)));
-      u64* tabs = A.alloc<u64>((size_t)pg * n, true);
+    cudaStream_t side = nullptr;
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
+    auto heavy_grid = [&](int nsrc, size_t word, int cap) {
+      const int64_t l2_ctas = std::max<int64_t>(1, (96ll << 20) / ((int64_t)n * (int64_t)word));
+      int64_t pg = std::min<int64_t>(std::max<int64_t>(l2_ctas, SM / 2), cap);
+      pg = std::min<int64_t>(pg, nsrc);
+      pg = std::max<int64_t>(1, std::min<int64_t>(pg, (int64_t)(freeb / 4) / ((int64_t)n * (int64_t)(word + 4))));
+      return (int)pg;
+    };
+    if (ht[PT_G64] > 0) {
+      // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables, on a
+      // side stream concurrent with the other tiers
+      side = C.side();
+      CK(cudaEventRecord(C.ev_fork, C.st));
+      CK(cudaStreamWaitEvent(side, C.ev_fork, 0));
+      const int pg = heavy_grid(ht[PT_G64], 8, SM / 2);
+      u64* tabs = A.alloc_on<u64>(side, (size_t)pg * n, true);
+      int32_t* lists = A.alloc_on<int32_t>(side, (size_t)pg * n);
+      int* counter = A.alloc_on<int>(side, 1, true);
+      k_pairs_heavy<u64><<<pg, PAIR_HBT, 0, side>>>(g, Te, plist(PT_G64), ht[PT_G64], counter, tabs, lists, po);
+      C.launches++;
+      CK(cudaEventRecord(C.ev_join, side));
+    }
+    if (ht[PT_G32] > 0) {
+      const int pg = heavy_grid(ht[PT_G32], 4, 2 * SM);
+      u32* tabs = A.alloc<u32>((size_t)pg * n, true);
       int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
       int* counter = A.alloc<int>(1, true);
-      k_pairs_global<<<pg, PAIR_THREADS, 0, C.st>>>(g, Te, plist, nbig, counter, tabs, lists, po);
-      C.launches++;
-      A.release(tabs); A.release(lists);
-    }
-    if (np - nbig > 0) {
-      const size_t psm = (size_t)3 * PAIR_HASH_CAP * sizeof(int32_t);
-      CK(cudaFuncSetAttribute(k_pairs_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-      int* counter = A.alloc<int>(1, true);
-      k_pairs_shared<<<SM, PAIR_THREADS, psm, C.st>>>(g, Te, plist + nbig, pest + nbig, np - nbig, counter, po);
+      k_pairs_heavy<u32><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(PT_G32), ht[PT_G32], counter, tabs, lists, po);
       C.launches++;
     }
+    if (ht[PT_MID] + ht[PT_LIGHT] > 0) {
+      CK(cudaFuncSetAttribute(k_pairs_main, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM));
+      int bps = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_pairs_main, PAIR_BT, PAIR_SMEM));
+      int* counters = A.alloc<int>(2, true);
+      k_pairs_main<<<std::max(bps, 1) * SM, PAIR_BT, PAIR_SMEM, C.st>>>(g, Te, plist(PT_MID), ht[PT_MID],
+                                                                       plist(PT_LIGHT), ht[PT_LIGHT], pest,
+                                                                       counters, po);
+      C.launches++;
+    }
+    if (side) CK(cudaStreamWaitEvent(C.st, C.ev_join, 0));
     A.release(pk); A.release(pk2); A.release(pv); A.release(pv2); A.release(t);
   }
 

@@ -69,17 +69,25 @@ __global__ void __launch_bounds__(256) k_hub_items(DGraph g, const u32* __restri
         fo = g.foff[eva];
       }
     }
+    int cur = -1;
+    u64 cacc = 0;
     warp_flat(len, [&](int j, int k, bool valid) {
       const int32_t aj = __shfl_sync(FULL_MASK, a, j);
       const int64_t foj = __shfl_sync(FULL_MASK, fo, j);
       const bool vloj = __shfl_sync(FULL_MASK, v_lo, j);
       if (!valid) return;
+      if (j != cur) {
+        if (cur >= 0 && cacc) atomicAdd(&acc[wib][cur], cacc);
+        cur = j;
+        cacc = 0;
+      }
       const int64_t r = foj + k;
       if (g.fx[r] < aj) {
         const int32_t evb = vloj ? g.fe1[r] : g.fe2[r];
-        atomicAdd(&acc[wib][j], (u64)Te[evb]);
+        cacc += (u64)Te[evb];
       }
     });
+    if (cur >= 0 && cacc) atomicAdd(&acc[wib][cur], cacc);
     __syncwarp();
     const u64 est = acc[wib][lane];
     acc[wib][lane] = 0;
@@ -154,16 +162,23 @@ __device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_
         if (atomicAdd(&tab[p], 1u) == 0u) list[atomicAdd(&S.cnt, 1)] = (int32_t)p;
       },
       [&](int64_t, int) {});
-  // pass 2: middles b get sum_x (c(x) - 1)
+  // pass 2: middles b get sum_x (c(x) - 1) (register sums while a thread stays on one b)
+  int cur = -1;
+  u64 cacc = 0;
+  auto flush = [&]() {
+    if (cur >= 0 && cacc) atomicAdd(&S.acc[cur], cacc);
+    cacc = 0;
+  };
   block_flat<HUB_BT>(na, S.pre, load,
       [&](int li, int64_t k) {
+        if (li != cur) { flush(); cur = li; }
         const int64_t r2 = S.fb[li] + k;
         const int32_t x = g.fx[r2];
         if (x >= a) return;
         const int32_t evb = S.evb[li];
         const int32_t evx = (g.esrc[evb] == v) ? g.fe1[r2] : g.fe2[r2];
         const int64_t p = pos_in_list(g, v, x, evx);
-        atomicAdd(&S.acc[li], (u64)tab[p] - 1ull);
+        cacc += (u64)tab[p] - 1ull;
       },
       [&](int64_t, int cn) {
         if ((int)threadIdx.x < cn) {
@@ -171,7 +186,8 @@ __device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_
           if (x) atomicAdd(&R68[S.b[threadIdx.x]], x);
           S.acc[threadIdx.x] = 0;
         }
-      });
+      },
+      flush);
   // pass 3: corners a, x and the hub v
   const int cnt = S.cnt;
   u64 r69 = 0;
@@ -243,13 +259,21 @@ __device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32
         len = (int)(g.foff[evb + 1] - fb);
       }
     }
+    int cur = -1;
+    u64 cacc = 0;
     warp_flat(len, [&](int j, int k, bool valid) {
       const int64_t fbj = __shfl_sync(FULL_MASK, fb, j);
       if (!valid) return;
+      if (j != cur) {
+        if (cur >= 0 && cacc) atomicAdd(&acc[cur], cacc);
+        cur = j;
+        cacc = 0;
+      }
       const int32_t x = g.fx[fbj + k];
       if (x >= a) return;
-      atomicAdd(&acc[j], (u64)H.val[H.find(x)] - 1ull);
+      cacc += (u64)H.val[H.find(x)] - 1ull;
     });
+    if (cur >= 0 && cacc) atomicAdd(&acc[cur], cacc);
     __syncwarp();
     const u64 sb = acc[lane];
     acc[lane] = 0;

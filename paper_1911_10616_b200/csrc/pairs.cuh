@@ -1,25 +1,37 @@
 // pairs.cuh -- step a7 of SURVEY 8(a): the pair (wedge) pass.
 //
-// One CTA per source u holds, for every x at distance <= 2, the pair quantities of
-// Theorem B.1 (readings R11, R14):
-//   W(u,x)  = |N(u) & N(x)|                       (2-hop expansion, phase A)
-//   D(u,x)  = #edges inside N(u) & N(x)            (diamond expansion, phase B)
+// For every source u the pass holds, for every x at distance <= 2, the pair quantities
+// of Theorem B.1 (readings R11, R14):
+//   W(u,x)  = |N(u) & N(x)|                       (2-hop expansion)
+//   D(u,x)  = #edges inside N(u) & N(x)            (diamond expansion)
 // TT(u,x) = sum_{v in N(u)&N(x)} T(v,x) - W[u~x] (R14) enters theta51 only through
-// sum_x TT(u,x)(W-1), which is summed per wedge in phase D once W is final (no table).
-// Emits:  C4(u)=DM8, theta36, theta50, theta51, theta63 for u (phase C);
+// sum_x TT(u,x)(W-1), which is summed per wedge once W is final (no table).
+// Emits:  C4(u)=DM8, theta36, theta50, theta51, theta63 for u;
 //   E5 = C4(u,v) = sum_{x in N(v)\u} (W(u,x)-1) per edge, and the centre credits
-//   theta49(v) += C(W(u,x)-1,2), theta62(v) += D(u,x) for x>u in N(v) (phase D);
-//   theta64(v) += sum over diamonds (u; v,w; x), x>u, of W(u,x)-2 (phase E):
+//   theta49(v) += C(W(u,x)-1,2), theta62(v) += D(u,x) for x>u in N(v);
+//   theta64(v) += sum over diamonds (u; v,w; x), x>u, of W(u,x)-2:
 //   DM64(v) = sum_{pairs {a,x} in N(v)} |N(v)&N(a)&N(x)| (W(a,x)-2) seen from the pair.
 //
-// Tables: sources whose 2-hop estimate fits use an open-addressing hash in shared memory
-// (on-chip, no DRAM traffic); the others a dense packed u64 (W | D<<32) table per CTA in
-// global memory, with the CTA count chosen so the tables stay L2-resident.  All wedge and
-// diamond visits are flattened over the CTA by a block prefix sum + binary search
-// (load-balanced, coalesced along each adjacency list).
+// Two passes per source over the same items (the neighbours v of u; item v has d(v)
+// wedge elements u-v-x and T(u,v) chord elements (u; v, w)): pass 1 builds the table
+// (W from wedges, D from the diamonds behind chords w > v), pass 2 reads it (per-pair
+// terms over the table entries, per-wedge and per-diamond sums over the items).
+//
+// Scheduling (B200): sources are sorted by their 2-hop estimate est(u) = sum_{v in N(u)}
+// d(v) - d(u) (>= the number of distinct x) and split in tiers:
+//   light (est <= PAIR_WARP_MAX): one WARP per source, per-warp packed shared hash;
+//   mid   (est <= PAIR_MID_MAX) : one CTA per source, packed shared hash;
+//   heavy                       : one CTA per source, dense per-CTA table in global
+//                                 memory (u32 W|D<<16, or u64 W|D<<32 for sources past the
+//                                 16-bit bounds), CTA count sized so the tables stay in L2.
+// Inside a CTA, short items are flattened over the 32 lanes of a warp (warp_flat) and
+// long items (hub neighbours) are cut into fixed chunks that whole warps take from a
+// shared queue, so lanes stay busy however heavy-tailed the degrees are, every element
+// is found without a search, and reads stay coalesced along each adjacency list.
 #pragma once
 #include <cub/block/block_scan.cuh>
 #include "common.cuh"
+#include "sched.cuh"
 
 struct PairOut {
   u64 *R8, *R36, *R50, *R51, *R63, *R49, *R62, *R64, *C4e;
@@ -31,18 +43,26 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
   return g.rp[a] + g.dm[a] + (e - g.orow[a]);
 }
 
-#define PAIR_THREADS 512
-#define PAIR_CHUNK 1024          // neighbours of u per prefix-sum chunk
-#define PAIR_HASH_CAP 16384      // shared hash entries (keys + W + D = 192 KB)
+#define PAIR_BT 256              // mid-tier CTA (and light-tier warps) kernel
+#define PAIR_MID_CAP 8192        // mid tier: packed shared hash entries (key + W|D<<16)
+#define PAIR_SMEM (PAIR_MID_CAP * 8)     // dynamic shared memory of the mid / light kernel
+#define PAIR_MID_MAX 6144        // mid tier: est <= this (load <= 0.75)
+#define PAIR_WARP_CAP 1024       // light tier: per-warp packed hash entries (8 warps x 8 KB)
+#define PAIR_WARP_MAX 512        // light tier: est <= this
+#define PAIR_HBT 512             // heavy tier CTA
+#define PAIR_LONG 128            // item part longer than this: chunked, shared queue
+#define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
+#define PAIR_LCAP 512            // long-part queue capacity per source pass
+#define PAIR_DIAM_INLINE 32      // diamond list longer than this: queued (CTA engine)
 #define EMPTY_KEY (-1)
 
-// ---- table abstractions ---------------------------------------------------------
-struct SharedHashTable {
+// Packed variant (one u32 per key: W | D << 16).  Valid for sources with d(u) < 2^16
+// (W(u,x) <= d(u)) and T(u) < 2^16 (D(u,x) counts edges inside N(u)&N(x), at most T(u)).
+struct SharedPackedHash {
   int32_t* keys;
-  u32* w;
-  u32* d;
+  u32* val;
   u32 mask;
-  __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) & mask; }
+  __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) >> 7 & mask; }
   __device__ __forceinline__ u32 insert(int32_t x) {
     u32 h = h0(x);
     for (;;) {
@@ -60,190 +80,48 @@ struct SharedHashTable {
     while (keys[h] != x) h = (h + 1) & mask;
     return h;
   }
-  __device__ __forceinline__ void add_w(int32_t x) { atomicAdd(&w[insert(x)], 1u); }
-  __device__ __forceinline__ void add_d(int32_t x) { atomicAdd(&d[find(x)], 1u); }
+  __device__ __forceinline__ void add_w(int32_t x) { atomicAdd(&val[insert(x)], 1u); }
+  // insert, not find: pass 1 visits wedges and diamonds concurrently
+  __device__ __forceinline__ void add_d(int32_t x) { atomicAdd(&val[insert(x)], 1u << 16); }
   __device__ __forceinline__ void get(int32_t x, u64& wv, u64& dv) const {
-    const u32 h = find(x);
-    wv = w[h];
-    dv = d[h];
+    const u32 v = val[find(x)];
+    wv = v & 0xffffu;
+    dv = v >> 16;
   }
-  __device__ __forceinline__ u64 get_w(int32_t x) const { return w[find(x)]; }
-  // W(u,x) or 0 when x is not at distance 2 (not in the table)
+  __device__ __forceinline__ u64 get_w(int32_t x) const { return val[find(x)] & 0xffffu; }
   __device__ __forceinline__ u64 get_w_or0(int32_t x) const {
     u32 h = h0(x);
     for (;;) {
       const int32_t k = keys[h];
-      if (k == x) return w[h];
+      if (k == x) return val[h] & 0xffffu;
       if (k == EMPTY_KEY) return 0;
       h = (h + 1) & mask;
     }
   }
 };
 
-struct GlobalDenseTable {
-  u64* t;        // [n] W | D << 32
-  int32_t* L;    // touched list
-  int* ntouch;   // shared counter
-  __device__ __forceinline__ void add_w(int32_t x) {
-    const u64 old = atomicAdd(&t[x], 1ull);
-    if ((old & 0xffffffffull) == 0) L[atomicAdd(ntouch, 1)] = x;
+// Dense per-CTA table in global memory indexed by x; W in the low half of the word,
+// D in the high half; touched list for the entry sweep and the reset.
+template <typename Word>
+struct GlobalDense {
+  Word* t;
+  int32_t* L;
+  int* ntouch;  // shared counter
+  static constexpr int SH = (int)sizeof(Word) * 4;
+  static constexpr Word LOW = (Word)(((u64)1 << SH) - 1);
+  __device__ __forceinline__ void touch(Word old, int32_t x) {
+    if (old == 0) L[atomicAdd(ntouch, 1)] = x;
   }
-  __device__ __forceinline__ void add_d(int32_t x) { atomicAdd(&t[x], 1ull << 32); }
+  __device__ __forceinline__ void add_w(int32_t x) { touch(atomicAdd(&t[x], (Word)1), x); }
+  __device__ __forceinline__ void add_d(int32_t x) { touch(atomicAdd(&t[x], (Word)((Word)1 << SH)), x); }
   __device__ __forceinline__ void get(int32_t x, u64& wv, u64& dv) const {
-    const u64 v = t[x];
-    wv = v & 0xffffffffull;
-    dv = v >> 32;
+    const Word v = t[x];
+    wv = (u64)(v & LOW);
+    dv = (u64)(v >> SH);
   }
-  __device__ __forceinline__ u64 get_w(int32_t x) const { return t[x] & 0xffffffffull; }
-  __device__ __forceinline__ u64 get_w_or0(int32_t x) const { return t[x] & 0xffffffffull; }
+  __device__ __forceinline__ u64 get_w(int32_t x) const { return (u64)(t[x] & LOW); }
+  __device__ __forceinline__ u64 get_w_or0(int32_t x) const { return (u64)(t[x] & LOW); }
 };
-
-// ---- flattened iteration over the slots of N(v), v in N(u) -------------------------
-// f(v, s_uv, t) for every slot t of N(v), v = ci[s_uv], s_uv in [r0, r1).
-template <typename F>
-__device__ __forceinline__ void flat_wedges(const DGraph& g, int64_t r0, int64_t r1, int64_t* pre, F f) {
-  typedef cub::BlockScan<int64_t, PAIR_THREADS> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  for (int64_t c0 = r0; c0 < r1; c0 += PAIR_CHUNK) {
-    const int cn = (int)min((int64_t)PAIR_CHUNK, r1 - c0);
-    // each thread owns two entries of the chunk (PAIR_CHUNK = 2 * PAIR_THREADS)
-    int64_t a0 = 0, a1 = 0;
-    const int i0 = 2 * threadIdx.x, i1 = i0 + 1;
-    if (i0 < cn) { const int32_t v = g.ci[c0 + i0]; a0 = g.rp[v + 1] - g.rp[v]; }
-    if (i1 < cn) { const int32_t v = g.ci[c0 + i1]; a1 = g.rp[v + 1] - g.rp[v]; }
-    int64_t ex, tot;
-    Scan(scan_tmp).ExclusiveSum(a0 + a1, ex, tot);
-    pre[i0] = ex;
-    pre[i1] = ex + a0;
-    if (threadIdx.x == 0) pre[PAIR_CHUNK] = tot;
-    __syncthreads();
-    const int64_t total = pre[PAIR_CHUNK];
-    for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
-      // largest k with pre[k] <= t
-      int lo = 0, hi = cn;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (pre[mid] <= t) lo = mid; else hi = mid;
-      }
-      const int64_t s_uv = c0 + lo;
-      const int32_t v = g.ci[s_uv];
-      f(v, s_uv, g.rp[v] + (t - pre[lo]));
-    }
-    __syncthreads();
-  }
-}
-
-// f(v, s_uv, r) for every full-list entry r of edge (u, v), v = ci[s_uv]
-template <typename F>
-__device__ __forceinline__ void flat_tri(const DGraph& g, const u32* __restrict__ Te, int64_t r0, int64_t r1,
-                                         int64_t* pre, F f) {
-  typedef cub::BlockScan<int64_t, PAIR_THREADS> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp2;
-  for (int64_t c0 = r0; c0 < r1; c0 += PAIR_CHUNK) {
-    const int cn = (int)min((int64_t)PAIR_CHUNK, r1 - c0);
-    int64_t a0 = 0, a1 = 0;
-    const int i0 = 2 * threadIdx.x, i1 = i0 + 1;
-    if (i0 < cn) a0 = Te[g.eid[c0 + i0]];
-    if (i1 < cn) a1 = Te[g.eid[c0 + i1]];
-    int64_t ex, tot;
-    Scan(scan_tmp2).ExclusiveSum(a0 + a1, ex, tot);
-    pre[i0] = ex;
-    pre[i1] = ex + a0;
-    if (threadIdx.x == 0) pre[PAIR_CHUNK] = tot;
-    __syncthreads();
-    const int64_t total = pre[PAIR_CHUNK];
-    for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
-      int lo = 0, hi = cn;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (pre[mid] <= t) lo = mid; else hi = mid;
-      }
-      const int64_t s_uv = c0 + lo;
-      const int32_t euv = g.eid[s_uv];
-      f(g.ci[s_uv], s_uv, g.foff[euv] + (t - pre[lo]));
-    }
-    __syncthreads();
-  }
-}
-
-// One source u, table type T.  All threads of the CTA call this together.
-template <typename T>
-__device__ void pair_source(const DGraph& g, const u32* __restrict__ Te, int32_t u, T& tab, int64_t* pre,
-                            u64* red, const PairOut& o) {
-  const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
-  // ---- phase A: W(u,x) over all wedges u - v - x
-  flat_wedges(g, r0, r1, pre, [&](int32_t v, int64_t s_uv, int64_t t) {
-    const int32_t x = g.ci[t];
-    if (x != u) tab.add_w(x);
-  });
-  // ---- phase B: D(u,x) over diamonds (u; v<w; x), chord (v,w) inside N(u)
-  flat_tri(g, Te, r0, r1, pre, [&](int32_t v, int64_t s_uv, int64_t r) {
-    const int32_t w = g.fx[r];
-    if (w <= v) return;
-    const int32_t euv = g.eid[s_uv];
-    const int32_t evw = (g.esrc[euv] == v) ? g.fe1[r] : g.fe2[r];
-    for (int64_t r2 = g.foff[evw]; r2 < g.foff[evw + 1]; r2++) {
-      const int32_t x = g.fx[r2];
-      if (x != u) tab.add_d(x);
-    }
-  });
-  // ---- phase D (+ theta51 correction over N(u)): per wedge sums
-  // E5(u,v), theta49(v), theta62(v) are per-v sums: accumulate in registers while the
-  // flattened loop stays inside one v, flush with atomics when v changes.
-  u64 s51 = 0;
-  {
-    int32_t cur_v = -1;
-    int64_t cur_s = -1;
-    u64 s5 = 0, s49 = 0, s62 = 0;
-    auto flush = [&]() {
-      if (cur_v < 0) return;
-      const int32_t e = g.eid[cur_s];
-      if (u < cur_v && s5) atomicAdd(&o.C4e[e], s5);
-      if (s49) atomicAdd(&o.R49[cur_v], s49);
-      if (s62) atomicAdd(&o.R62[cur_v], s62);
-      s5 = s49 = s62 = 0;
-    };
-    flat_wedges(g, r0, r1, pre, [&](int32_t v, int64_t s_uv, int64_t t) {
-      if (v != cur_v) { flush(); cur_v = v; cur_s = s_uv; }
-      const int32_t x = g.ci[t];
-      if (x == u) return;
-      u64 w, d;
-      tab.get(x, w, d);
-      s5 += w - 1;
-      s51 += (u64)Te[g.eid[t]] * (w - 1);
-      if (x > u) {
-        s49 += binom2(w - 1);
-        s62 += d;
-      }
-    });
-    flush();
-  }
-  for (int64_t s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
-    const u64 w = tab.get_w_or0(g.ci[s]);
-    s51 -= w * (w - 1);
-  }
-  // ---- phase E: theta64(v) += W(u,x)-2 over diamonds (u; v, w; x), x > u
-  {
-    int32_t cur_v = -1;
-    u64 acc = 0;
-    flat_tri(g, Te, r0, r1, pre, [&](int32_t v, int64_t s_uv, int64_t r) {
-      if (v != cur_v) {
-        if (cur_v >= 0 && acc) atomicAdd(&o.R64[cur_v], acc);
-        cur_v = v;
-        acc = 0;
-      }
-      const int32_t euv = g.eid[s_uv];
-      const int32_t evw = (g.esrc[euv] == v) ? g.fe1[r] : g.fe2[r];
-      for (int64_t r2 = g.foff[evw]; r2 < g.foff[evw + 1]; r2++) {
-        const int32_t x = g.fx[r2];
-        if (x > u) acc += tab.get_w(x) - 2ull;
-      }
-    });
-    if (cur_v >= 0 && acc) atomicAdd(&o.R64[cur_v], acc);
-  }
-  s51 = warp_sum(s51);
-  if ((threadIdx.x & 31) == 0 && s51) atomicAdd(&red[3], s51);
-}
 
 // phase C contributions of one (x, W, D) pair
 __device__ __forceinline__ void pair_c_terms(const DGraph& g, int32_t x, u64 w, u64 d, u64& a8, u64& a36,
@@ -255,65 +133,447 @@ __device__ __forceinline__ void pair_c_terms(const DGraph& g, int32_t x, u64 w, 
   a63 += d * (w - 2);
 }
 
-__device__ __forceinline__ void pair_flush_u(int32_t u, u64 a8, u64 a36, u64 a50, u64 a63, u64* red,
-                                             const PairOut& o) {
-  a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63);
+// ---- per-element work (shared by the warp and CTA engines) --------------------------
+// Item v of source u.  Wedge element k: x = N(v)[k].  Chord element k: the k-th entry of
+// the full triangle list of e(u,v), i.e. w with (u, v, w) a triangle.
+struct PairItem {
+  int32_t v;
+  int32_t e;        // e(u, v)
+  int64_t rb;       // rp[v]
+  int64_t fo;       // foff[e]
+  int32_t dv;       // d(v)
+  int32_t tv;       // T(u, v)
+  bool vlo;         // v is the lower endpoint of e
+};
+
+__device__ __forceinline__ PairItem pair_item(const DGraph& g, int64_t s_uv) {
+  PairItem it;
+  it.v = g.ci[s_uv];
+  it.e = g.eid[s_uv];
+  it.rb = g.rp[it.v];
+  it.dv = (int32_t)(g.rp[it.v + 1] - it.rb);
+  it.fo = g.foff[it.e];
+  it.tv = (int32_t)(g.foff[it.e + 1] - it.fo);
+  it.vlo = g.esrc[it.e] == it.v;
+  return it;
+}
+
+// pass-2 per-item accumulators (flushed to global counters)
+struct PairAcc {
+  u64 c5, c49, c62, c64;
+  __device__ __forceinline__ void zero() { c5 = c49 = c62 = c64 = 0; }
+  __device__ __forceinline__ void flush(int32_t u, int32_t v, int32_t e, const PairOut& o) {
+    if (u < v && c5) atomicAdd(&o.C4e[e], c5);
+    if (c49) atomicAdd(&o.R49[v], c49);
+    if (c62) atomicAdd(&o.R62[v], c62);
+    if (c64) atomicAdd(&o.R64[v], c64);
+    zero();
+  }
+};
+
+template <typename Tab>
+__device__ __forceinline__ void pass1_wedge(const DGraph& g, int32_t u, int64_t rb, int k, Tab& tab) {
+  const int32_t x = g.ci[rb + k];
+  if (x != u) tab.add_w(x);
+}
+template <typename Tab>
+__device__ __forceinline__ void pass2_wedge(const DGraph& g, const u32* __restrict__ Te, int32_t u, int64_t rb,
+                                            int k, const Tab& tab, PairAcc& A, u64& s51) {
+  const int64_t t = rb + k;
+  const int32_t x = g.ci[t];
+  if (x == u) return;
+  u64 w, d;
+  tab.get(x, w, d);
+  A.c5 += w - 1;
+  s51 += (u64)Te[g.eid[t]] * (w - 1);
+  if (x > u) {
+    A.c49 += binom2(w - 1);
+    A.c62 += d;
+  }
+}
+
+// Chord element k of item v: w = k-th third vertex of e(u,v); the diamonds behind it are
+// the entries x of tri(v, w).  A long diamond list may be handed to enq(r, v, vlo) (the
+// CTA engine queues it for chunked processing); otherwise it is walked here.
+struct NoEnq {
+  __device__ __forceinline__ bool operator()(int64_t, int32_t, bool) const { return false; }
+};
+template <int PASS, typename Tab>
+__device__ __forceinline__ void diamond_elem(const DGraph& g, int32_t u, int64_t r2, Tab& tab, PairAcc& A) {
+  const int32_t x = g.fx[r2];
+  if (PASS == 1) {
+    if (x != u) tab.add_d(x);
+  } else {
+    if (x > u) A.c64 += tab.get_w(x) - 2ull;
+  }
+}
+template <int PASS, typename Tab, typename Enq>
+__device__ __forceinline__ void chord_elem(const DGraph& g, int32_t u, int32_t v, int64_t fo, bool vlo, int k,
+                                           Tab& tab, PairAcc& A, Enq& enq) {
+  const int64_t r = fo + k;
+  if (PASS == 1 && g.fx[r] <= v) return;  // D(u,x): each chord (v<w) once
+  const int32_t evw = vlo ? g.fe1[r] : g.fe2[r];
+  const int64_t f0 = g.foff[evw], f1 = g.foff[evw + 1];
+  if (f1 - f0 > PAIR_DIAM_INLINE && enq(r, v, vlo)) return;
+  for (int64_t r2 = f0; r2 < f1; r2++) diamond_elem<PASS>(g, u, r2, tab, A);
+}
+
+// ---- warp engine: the warp runs one pass over items s_uv in [r0, r1) --------------------
+// Every part (wedges, chords) of 32 items at a time is flattened over the lanes.
+template <int PASS, typename Tab>
+__device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int64_t r0,
+                                          int64_t r1, Tab& tab, u64& s51, const PairOut& o) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t o0 = r0; o0 < r1; o0 += 32) {
+    PairItem it;
+    const bool have = o0 + lane < r1;
+    if (have) it = pair_item(g, o0 + lane);
+    else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
+    PairAcc A;
+    A.zero();
+    int cur = -1;
+    int32_t cv = 0, ce = 0;
+    auto flush = [&]() {
+      if (PASS == 2 && cur >= 0) A.flush(u, cv, ce, o);
+    };
+    // wedges
+    warp_flat(it.dv, [&](int j, int k, bool valid) {
+      const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
+      if (PASS == 2) {
+        const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
+        const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
+        if (!valid) return;
+        if (j != cur) { flush(); cur = j; cv = vj; ce = ej; }
+        pass2_wedge(g, Te, u, rbj, k, tab, A, s51);
+      } else {
+        if (!valid) return;
+        pass1_wedge(g, u, rbj, k, tab);
+      }
+    });
+    flush();
+    cur = -1;
+    // chords
+    warp_flat(it.tv, [&](int j, int k, bool valid) {
+      const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
+      const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
+      const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
+      const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
+      if (!valid) return;
+      if (PASS == 2 && j != cur) { flush(); cur = j; cv = vj; ce = ej; }
+      NoEnq ne;
+      chord_elem<PASS>(g, u, vj, foj, vloj, k, tab, A, ne);
+    });
+    flush();
+  }
+}
+
+// ---- CTA engine ------------------------------------------------------------------------
+// Sweep: warps take 32 items at a time from a shared counter and flatten their short parts
+// over the lanes.  Long parts -- a wedge or chord part longer than PAIR_LONG, or the
+// diamond list behind one chord longer than PAIR_DIAM_INLINE -- go to a shared queue;
+// rounds then cut the queued parts into PAIR_CHUNK-element chunks that whole warps take
+// from a second counter (chord chunks may queue diamond lists for the next round).
+// Every element is visited exactly once; no per-element search.
+enum { PK_WEDGE = 0, PK_CHORD = 1, PK_DIAM = 2 };
+struct EngShared {
+  int next;
+  int qn;
+  int next_chunk;
+  int nchunks;
+  int64_t qslot[PAIR_LCAP];   // item slot s_uv (wedge / chord parts) or entry r (diamond)
+  int32_t qv[PAIR_LCAP];      // v (diamond parts)
+  int8_t qkind[PAIR_LCAP];
+  int8_t qvlo[PAIR_LCAP];
+  int32_t lc0[PAIR_LCAP + 1];
+};
+
+struct CtaEnq {
+  EngShared* E;
+  __device__ __forceinline__ bool operator()(int64_t r, int32_t v, bool vlo) const {
+    const int q = atomicAdd(&E->qn, 1);
+    if (q >= PAIR_LCAP) return false;
+    E->qslot[q] = r; E->qv[q] = v; E->qkind[q] = PK_DIAM; E->qvlo[q] = vlo;
+    return true;
+  }
+};
+
+__device__ __forceinline__ int part_len(const DGraph& g, const EngShared& E, int q) {
+  const int kind = E.qkind[q];
+  if (kind == PK_DIAM) {
+    const int64_t r = E.qslot[q];
+    const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
+    return (int)(g.foff[evw + 1] - g.foff[evw]);
+  }
+  const PairItem it = pair_item(g, E.qslot[q]);
+  return kind == PK_WEDGE ? it.dv : it.tv;
+}
+
+template <int PASS, typename Tab>
+__device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int64_t r0, int64_t r1, Tab& tab,
+                         EngShared& E, u64& s51, const PairOut& o) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) { E.next = 0; E.qn = 0; }
+  __syncthreads();
+  CtaEnq enq{&E};
+  const int64_t nitems = r1 - r0;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&E.next, 32);
+    base = __shfl_sync(FULL_MASK, base, 0);
+    if (base >= nitems) break;
+    PairItem it;
+    const bool have = base + lane < nitems;
+    if (have) it = pair_item(g, r0 + base + lane);
+    else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
+    // defer long parts to the queue (if it has room)
+    if (it.dv > PAIR_LONG) {
+      const int q = atomicAdd(&E.qn, 1);
+      if (q < PAIR_LCAP) { E.qslot[q] = r0 + base + lane; E.qkind[q] = PK_WEDGE; it.dv = 0; }
+    }
+    if (it.tv > PAIR_LONG) {
+      const int q = atomicAdd(&E.qn, 1);
+      if (q < PAIR_LCAP) { E.qslot[q] = r0 + base + lane; E.qkind[q] = PK_CHORD; it.tv = 0; }
+    }
+    PairAcc A;
+    A.zero();
+    int cur = -1;
+    int32_t cv = 0, ce = 0;
+    auto flush = [&]() {
+      if (PASS == 2 && cur >= 0) A.flush(u, cv, ce, o);
+    };
+    warp_flat(it.dv, [&](int j, int k, bool valid) {
+      const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
+      if (PASS == 2) {
+        const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
+        const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
+        if (!valid) return;
+        if (j != cur) { flush(); cur = j; cv = vj; ce = ej; }
+        pass2_wedge(g, Te, u, rbj, k, tab, A, s51);
+      } else {
+        if (!valid) return;
+        pass1_wedge(g, u, rbj, k, tab);
+      }
+    });
+    flush();
+    cur = -1;
+    warp_flat(it.tv, [&](int j, int k, bool valid) {
+      const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
+      const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
+      const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
+      const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
+      if (!valid) return;
+      if (PASS == 2 && j != cur) { flush(); cur = j; cv = vj; ce = ej; }
+      chord_elem<PASS>(g, u, vj, foj, vloj, k, tab, A, enq);
+    });
+    flush();
+  }
+  __syncthreads();
+  // rounds over the queued parts
+  int qb = 0;
+  for (;;) {
+    const int qe = min(E.qn, PAIR_LCAP);
+    if (qb >= qe) break;  // uniform (E.qn read after a barrier)
+    if (threadIdx.x < 32) {
+      int carry = 0;
+      for (int q0 = qb; q0 < qe; q0 += 32) {
+        const int q = q0 + lane;
+        const int nc = (q < qe) ? (part_len(g, E, q) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
+        int incl = nc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(FULL_MASK, incl, d);
+          if (lane >= d) incl += y;
+        }
+        if (q < qe) E.lc0[q - qb] = carry + incl - nc;
+        carry += __shfl_sync(FULL_MASK, incl, 31);
+      }
+      if (lane == 0) { E.lc0[qe - qb] = carry; E.nchunks = carry; E.next_chunk = 0; }
+    }
+    __syncthreads();
+    const int nchunks = E.nchunks;
+    const int nq = qe - qb;
+    for (;;) {
+      int c = 0;
+      if (lane == 0) c = atomicAdd(&E.next_chunk, 1);
+      c = __shfl_sync(FULL_MASK, c, 0);
+      if (c >= nchunks) break;
+      int lo = 0, hi = nq;  // largest part with lc0 <= c
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (E.lc0[mid] <= c) lo = mid; else hi = mid;
+      }
+      const int q = qb + lo;
+      const int kind = E.qkind[q];
+      const int k0 = (c - E.lc0[lo]) * PAIR_CHUNK;
+      PairAcc A;
+      A.zero();
+      int32_t fv = 0, fe = 0;
+      if (kind == PK_DIAM) {
+        const int64_t r = E.qslot[q];
+        const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
+        const int64_t f0 = g.foff[evw];
+        const int k1 = min((int)(g.foff[evw + 1] - f0), k0 + PAIR_CHUNK);
+        for (int k = k0 + lane; k < k1; k += 32) diamond_elem<PASS>(g, u, f0 + k, tab, A);
+        fv = E.qv[q];
+        fe = -1;  // no C4e credit from diamond parts (A.c5 stays 0)
+      } else {
+        const PairItem it = pair_item(g, E.qslot[q]);
+        fv = it.v;
+        fe = it.e;
+        if (kind == PK_WEDGE) {
+          const int k1 = min(it.dv, k0 + PAIR_CHUNK);
+          for (int k = k0 + lane; k < k1; k += 32) {
+            if (PASS == 2) pass2_wedge(g, Te, u, it.rb, k, tab, A, s51);
+            else pass1_wedge(g, u, it.rb, k, tab);
+          }
+        } else {
+          const int k1 = min(it.tv, k0 + PAIR_CHUNK);
+          for (int k = k0 + lane; k < k1; k += 32) chord_elem<PASS>(g, u, it.v, it.fo, it.vlo, k, tab, A, enq);
+        }
+      }
+      if (PASS == 2) {
+        A.c5 = warp_sum(A.c5); A.c49 = warp_sum(A.c49); A.c62 = warp_sum(A.c62); A.c64 = warp_sum(A.c64);
+        if (lane == 0) A.flush(u, fv, fe, o);
+      }
+    }
+    __syncthreads();
+    qb = qe;
+  }
+}
+
+// ---- one source on a CTA (mid and heavy tiers) ------------------------------------------
+// Tab provides add_w/add_d/get/get_w/get_w_or0; for_entries(f) runs f(x, W, D) for every
+// table entry (strided over the CTA), reset() clears the table (CTA-wide).
+template <int BT, typename Tab, typename ForEntries, typename Reset>
+__device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int32_t u, Tab& tab, EngShared& E,
+                                u64* red, const PairOut& o, ForEntries for_entries, Reset reset) {
+  const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
+  u64 s51 = 0;
+  cta_pass<1>(g, Te, u, r0, r1, tab, E, s51, o);
+  cta_pass<2>(g, Te, u, r0, r1, tab, E, s51, o);
+  u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
+  for_entries([&](int32_t x, u64 w, u64 d) { pair_c_terms(g, x, w, d, a8, a36, a50, a63); });
+  for (int64_t s = r0 + threadIdx.x; s < r1; s += BT) {
+    const u64 w = tab.get_w_or0(g.ci[s]);
+    s51 -= w * (w - 1);
+  }
+  a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
   if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&red[0], a8); atomicAdd(&red[1], a36); atomicAdd(&red[2], a50); atomicAdd(&red[4], a63);
+    if (a8) atomicAdd(&red[0], a8);
+    if (a36) atomicAdd(&red[1], a36);
+    if (a50) atomicAdd(&red[2], a50);
+    if (s51) atomicAdd(&red[3], s51);
+    if (a63) atomicAdd(&red[4], a63);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     o.R8[u] += red[0]; o.R36[u] += red[1]; o.R50[u] += red[2]; o.R51[u] += red[3]; o.R63[u] += red[4];
     for (int i = 0; i < 5; i++) red[i] = 0;
   }
+  reset();
+  __syncthreads();
 }
 
-// Sources with a small 2-hop estimate: shared-memory hash, capacity per source.
-__global__ void __launch_bounds__(PAIR_THREADS, 1) k_pairs_shared(DGraph g, const u32* __restrict__ Te,
-                                                                   const int32_t* __restrict__ srcs,
-                                                                   const u32* __restrict__ est, int nsrc,
-                                                                   int* __restrict__ counter, PairOut o) {
+// ---- light tier: one warp per source --------------------------------------------------
+__device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, int32_t u, u32 cap,
+                                 SharedPackedHash& tab, const PairOut& o) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
+  tab.mask = cap - 1;
+  u64 s51 = 0;
+  warp_pass<1>(g, Te, u, r0, r1, tab, s51, o);
+  __syncwarp();
+  warp_pass<2>(g, Te, u, r0, r1, tab, s51, o);
+  u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
+  for (u32 h = lane; h < cap; h += 32) {
+    const int32_t x = tab.keys[h];
+    if (x != EMPTY_KEY) pair_c_terms(g, x, tab.val[h] & 0xffffu, tab.val[h] >> 16, a8, a36, a50, a63);
+  }
+  for (int64_t s = r0 + lane; s < r1; s += 32) {
+    const u64 w = tab.get_w_or0(g.ci[s]);
+    s51 -= w * (w - 1);
+  }
+  a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
+  if (lane == 0) {
+    if (a8) atomicAdd(&o.R8[u], a8);
+    if (a36) atomicAdd(&o.R36[u], a36);
+    if (a50) atomicAdd(&o.R50[u], a50);
+    if (s51) atomicAdd(&o.R51[u], s51);
+    if (a63) atomicAdd(&o.R63[u], a63);
+  }
+  __syncwarp();
+  for (u32 h = lane; h < cap; h += 32) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
+  __syncwarp();
+}
+
+// Mid and light tiers: persistent CTAs take mid sources (one CTA each, packed shared
+// hash) from mid[0, n_mid), then each warp takes light sources from light[0, n_light).
+__global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __restrict__ Te,
+                                                        const int32_t* __restrict__ mid, int n_mid,
+                                                        const int32_t* __restrict__ light, int n_light,
+                                                        const u32* __restrict__ est, int* __restrict__ counters,
+                                                        PairOut o) {
   extern __shared__ int32_t sh_pairs[];
-  __shared__ int64_t pre[PAIR_CHUNK + 1];
+  __shared__ EngShared E;
   __shared__ u64 red[5];
   __shared__ int s_idx;
-  SharedHashTable tab;
-  tab.keys = sh_pairs;
-  tab.w = (u32*)(sh_pairs + PAIR_HASH_CAP);
-  tab.d = tab.w + PAIR_HASH_CAP;
   if (threadIdx.x < 5) red[threadIdx.x] = 0;
-  for (;;) {
-    if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
-    __syncthreads();
-    const int idx = s_idx;
-    if (idx >= nsrc) break;
-    const int32_t u = srcs[idx];
-    u32 cap = 64;
-    while (cap < 2u * est[idx] && cap < PAIR_HASH_CAP) cap <<= 1;
-    tab.mask = cap - 1;
-    for (u32 h = threadIdx.x; h < cap; h += blockDim.x) { tab.keys[h] = EMPTY_KEY; tab.w[h] = 0; tab.d[h] = 0; }
-    __syncthreads();
-    pair_source(g, Te, u, tab, pre, red, o);
-    __syncthreads();
-    u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
-    for (u32 h = threadIdx.x; h < cap; h += blockDim.x) {
-      const int32_t x = tab.keys[h];
-      if (x != EMPTY_KEY) pair_c_terms(g, x, tab.w[h], tab.d[h], a8, a36, a50, a63);
+  {
+    SharedPackedHash tab;
+    tab.keys = sh_pairs;
+    tab.val = (u32*)(sh_pairs + PAIR_MID_CAP);
+    for (;;) {
+      if (threadIdx.x == 0) s_idx = atomicAdd(&counters[0], 1);
+      __syncthreads();
+      const int idx = s_idx;
+      __syncthreads();
+      if (idx >= n_mid) break;
+      const int32_t u = mid[idx];
+      const u32 cap = min(pow2_at_least(2u * est[u], 64u), (u32)PAIR_MID_CAP);
+      tab.mask = cap - 1;
+      for (u32 h = threadIdx.x; h < cap; h += PAIR_BT) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
+      __syncthreads();
+      pair_source_cta<PAIR_BT>(g, Te, u, tab, E, red, o,
+          [&](auto f) {
+            for (u32 h = threadIdx.x; h < cap; h += PAIR_BT) {
+              const int32_t x = tab.keys[h];
+              if (x != EMPTY_KEY) f(x, (u64)(tab.val[h] & 0xffffu), (u64)(tab.val[h] >> 16));
+            }
+          },
+          [&]() {});
     }
-    pair_flush_u(u, a8, a36, a50, a63, red, o);
-    __syncthreads();
+  }
+  // light tier: per-warp packed hash in the dynamic shared memory
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  SharedPackedHash tab;
+  tab.keys = sh_pairs + wib * (2 * PAIR_WARP_CAP);
+  tab.val = (u32*)(tab.keys + PAIR_WARP_CAP);
+  for (int h = lane; h < PAIR_WARP_CAP; h += 32) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
+  __syncwarp();
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(&counters[1], 2);
+    idx = __shfl_sync(FULL_MASK, idx, 0);
+    if (idx >= n_light) break;
+    const int end = min(idx + 2, n_light);
+    for (int q = idx; q < end; q++) {
+      const int32_t u = light[q];
+      const u32 cap = pow2_at_least(2u * est[u], 32u);
+      pair_source_warp(g, Te, u, cap, tab, o);
+    }
   }
 }
 
-// Sources with a large 2-hop set: dense packed table per CTA (L2-sized CTA count).
-__global__ void __launch_bounds__(PAIR_THREADS, 1) k_pairs_global(DGraph g, const u32* __restrict__ Te,
-                                                                   const int32_t* __restrict__ srcs, int nsrc,
-                                                                   int* __restrict__ counter, u64* __restrict__ tabs,
-                                                                   int32_t* __restrict__ lists, PairOut o) {
-  __shared__ int64_t pre[PAIR_CHUNK + 1];
+// Heavy tier: one CTA per source, dense per-CTA table (Word = u32 packed or u64).
+template <typename Word>
+__global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* __restrict__ Te,
+                                                          const int32_t* __restrict__ srcs, int nsrc,
+                                                          int* __restrict__ counter, Word* __restrict__ tabs,
+                                                          int32_t* __restrict__ lists, PairOut o) {
+  __shared__ EngShared E;
   __shared__ u64 red[5];
   __shared__ int s_idx, s_ntouch;
-  GlobalDenseTable tab;
+  GlobalDense<Word> tab;
   tab.t = tabs + (size_t)blockIdx.x * g.n;
   tab.L = lists + (size_t)blockIdx.x * g.n;
   tab.ntouch = &s_ntouch;
@@ -323,22 +583,26 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) k_pairs_global(DGraph g, cons
     if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
     __syncthreads();
     const int idx = s_idx;
+    __syncthreads();
     if (idx >= nsrc) break;
     const int32_t u = srcs[idx];
-    pair_source(g, Te, u, tab, pre, red, o);
-    __syncthreads();
-    const int nt = s_ntouch;
-    u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-      const int32_t x = tab.L[i];
-      u64 w, d;
-      tab.get(x, w, d);
-      pair_c_terms(g, x, w, d, a8, a36, a50, a63);
-    }
-    pair_flush_u(u, a8, a36, a50, a63, red, o);
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) tab.t[tab.L[i]] = 0ull;
-    if (threadIdx.x == 0) s_ntouch = 0;
-    __syncthreads();
+    pair_source_cta<PAIR_HBT>(g, Te, u, tab, E, red, o,
+        [&](auto f) {
+          const int nt = s_ntouch;
+          for (int i = threadIdx.x; i < nt; i += PAIR_HBT) {
+            const int32_t x = tab.L[i];
+            u64 w, d;
+            tab.get(x, w, d);
+            f(x, w, d);
+          }
+        },
+        [&]() {
+          __syncthreads();
+          const int nt = s_ntouch;
+          for (int i = threadIdx.x; i < nt; i += PAIR_HBT) tab.t[tab.L[i]] = (Word)0;
+          __syncthreads();
+          if (threadIdx.x == 0) s_ntouch = 0;
+        });
   }
 }
 
@@ -360,13 +624,28 @@ __global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict
   }
 }
 
-// shard filter of the sorted list + estimate per position
-__global__ void k_pair_lists(const u64* __restrict__ skeys, const int32_t* __restrict__ svals, int32_t n,
-                             int si, int ns, int32_t* __restrict__ list, u32* __restrict__ est) {
-  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    if (p % ns == si) {
+// Shard filter of the est-sorted (descending) vertex list and tier classification.
+// Lists keep the descending order approximately (warp-aggregated appends in list order).
+enum { PT_G64 = 0, PT_G32, PT_MID, PT_LIGHT, PT_COUNT };
+__global__ void k_pair_classify(DGraph g, const u64* __restrict__ skeys, const int32_t* __restrict__ svals,
+                                int si, int ns, const u64* __restrict__ Tv, u32* __restrict__ est_v,
+                                int32_t* __restrict__ lists, int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = gw * 32; base < g.n; base += nw * 32) {
+    const int64_t p = base + lane;
+    int tier = -1;
+    int32_t u = 0;
+    if (p < g.n && p % ns == si) {
+      u = svals[p];
       const u64 e = ~skeys[p];
-      list[p / ns] = svals[p];
-      est[p / ns] = (u32)min(e, (u64)0xffffffffu);
+      est_v[u] = (u32)min(e, (u64)0xffffffffu);
+      if (e > 0) {
+        const bool packed_ok = dg_deg(g, u) < 65536 && Tv[u] < 65536ull;
+        tier = !packed_ok ? PT_G64 : e <= PAIR_WARP_MAX ? PT_LIGHT : e <= PAIR_MID_MAX ? PT_MID : PT_G32;
+      }
     }
+    for (int t = 0; t < PT_COUNT; t++) warp_append(tier == t, u, lists + (size_t)t * g.n, counts + t);
+  }
 }

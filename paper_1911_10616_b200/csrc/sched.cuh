@@ -45,10 +45,15 @@ __device__ __forceinline__ void warp_flat(int len, Body body) {
 // of BT outer items (one per thread).  pre[] is shared scratch of BT+1 int64 entries.
 //   load(i) -> len(i) (thread threadIdx.x loads outer item c0 + threadIdx.x and may stash
 //   payload in shared arrays indexed by threadIdx.x);  body(li, k) with li = i - c0;
-//   after(c0, cn) runs (all threads) after each chunk, between two barriers.
+//   after(c0, cn) runs (all threads) after each chunk, between two barriers; flush() runs
+//   in every thread before the first of them (to spill per-thread register sums).
 // ---------------------------------------------------------------------------------
-template <int BT, typename Load, typename Body, typename After>
-__device__ __forceinline__ void block_flat(int64_t n_outer, int64_t* pre, Load load, Body body, After after) {
+struct NoFlush {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <int BT, typename Load, typename Body, typename After, typename Flush = NoFlush>
+__device__ __forceinline__ void block_flat(int64_t n_outer, int64_t* pre, Load load, Body body, After after,
+                                           Flush flush = Flush()) {
   typedef cub::BlockScan<int64_t, BT> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
   for (int64_t c0 = 0; c0 < n_outer; c0 += BT) {
@@ -69,6 +74,7 @@ __device__ __forceinline__ void block_flat(int64_t n_outer, int64_t* pre, Load l
       }
       body(lo, t - pre[lo]);
     }
+    flush();
     __syncthreads();
     after(c0, cn);
     __syncthreads();
