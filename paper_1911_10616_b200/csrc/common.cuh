@@ -95,6 +95,7 @@ struct DGraph {
   const int64_t* rp;    // [n+1]
   const int32_t* ci;    // [2m]
   const int32_t* dm;    // [n]  number of lower neighbours (in-degree in G->)
+  const int32_t* deg;   // [n]  d(u) (one 4-byte load instead of two rowptr loads)
   const int32_t* eid;   // [2m] edge id of each slot
   // oriented out-CSR = edge ids
   const int64_t* orow;  // [n+1]
@@ -115,9 +116,7 @@ struct DGraph {
   const int32_t* fe2;   // [3 ntri]
 };
 
-__device__ __forceinline__ int32_t dg_deg(const DGraph& g, int32_t u) {
-  return (int32_t)(g.rp[u + 1] - g.rp[u]);
-}
+__device__ __forceinline__ int32_t dg_deg(const DGraph& g, int32_t u) { return g.deg[u]; }
 __device__ __forceinline__ int32_t dg_dplus(const DGraph& g, int32_t u) {
   return (int32_t)(g.orow[u + 1] - g.orow[u]);
 }

@@ -397,6 +397,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   int64_t* rp = A.alloc<int64_t>(n + 1);
   int32_t* ci = A.alloc<int32_t>(m2 + 1);
   int32_t* dmv = A.alloc<int32_t>(n + 1);
+  int32_t* degv = A.alloc<int32_t>(n + 1);
   int64_t* orow = A.alloc<int64_t>(n + 1);
   int32_t* eid = A.alloc<int32_t>(m2 + 1);
   int32_t* ocol = A.alloc<int32_t>(m + 1);
@@ -419,7 +420,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     k_i32_to_i64<<<grid_for(n, B, SM), B, 0, C.st>>>(degc, n, tmp64);
     k_set_i64<<<1, 1, 0, C.st>>>(rp, 0);
     inclusive_sum(A, C, tmp64, rp + 1, n);
-    k_split_counts<<<grid_for(n, B, SM), B, 0, C.st>>>(n, rp, ci, dmv, tmp64);
+    k_split_counts<<<grid_for(n, B, SM), B, 0, C.st>>>(n, rp, ci, dmv, tmp64, degv);
     k_set_i64<<<1, 1, 0, C.st>>>(orow, 0);
     inclusive_sum(A, C, tmp64, orow + 1, n);
     C.launches += 4;
@@ -443,7 +444,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   DGraph g;
   std::memset(&g, 0, sizeof(g));
   g.n = n; g.m = m; g.max_deg = std::max(max_deg, 1); g.max_out = max_out;
-  g.rp = rp; g.ci = ci; g.dm = dmv; g.eid = eid; g.orow = orow; g.ocol = ocol; g.esrc = esrc;
+  g.rp = rp; g.ci = ci; g.dm = dmv; g.deg = degv; g.eid = eid; g.orow = orow; g.ocol = ocol; g.esrc = esrc;
   g.edst = edst; g.eslot_hi = eslot_hi;
 
   // per-vertex fields and per-edge arrays
@@ -622,7 +623,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaMemGetInfo(&freeb, &totalb));
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
     auto heavy_grid = [&](int nsrc, size_t word, int cap) {
-      const int64_t l2_ctas = std::max<int64_t>(1, (96ll << 20) / ((int64_t)n * (int64_t)word));
+      const int64_t l2_ctas = std::max<int64_t>(1, (56ll << 20) / ((int64_t)n * (int64_t)word));
       int64_t pg = std::min<int64_t>(std::max<int64_t>(l2_ctas, SM / 2), cap);
       pg = std::min<int64_t>(pg, nsrc);
       pg = std::max<int64_t>(1, std::min<int64_t>(pg, (int64_t)(freeb / 4) / ((int64_t)n * (int64_t)(word + 4))));
@@ -638,16 +639,21 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       u64* tabs = A.alloc_on<u64>(side, (size_t)pg * n, true);
       int32_t* lists = A.alloc_on<int32_t>(side, (size_t)pg * n);
       int* counter = A.alloc_on<int>(side, 1, true);
-      k_pairs_heavy<u64><<<pg, PAIR_HBT, 0, side>>>(g, Te, plist(PT_G64), ht[PT_G64], counter, tabs, lists, po);
+      k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, side>>>(g, Te, plist(PT_G64), ht[PT_G64], counter, tabs, lists,
+                                                           po);
       C.launches++;
       CK(cudaEventRecord(C.ev_join, side));
     }
-    if (ht[PT_G32] > 0) {
-      const int pg = heavy_grid(ht[PT_G32], 4, 2 * SM);
+    for (int tier : {PT_G32S, PT_G32}) {
+      if (ht[tier] == 0) continue;
+      const int pg = heavy_grid(ht[tier], 4, 2 * SM);
       u32* tabs = A.alloc<u32>((size_t)pg * n, true);
-      int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
+      int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * n) : nullptr;
       int* counter = A.alloc<int>(1, true);
-      k_pairs_heavy<u32><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(PT_G32), ht[PT_G32], counter, tabs, lists, po);
+      if (tier == PT_G32S)
+        k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(tier), ht[tier], counter, tabs, lists, po);
+      else
+        k_pairs_heavy<u32, false><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(tier), ht[tier], counter, tabs, lists, po);
       C.launches++;
     }
     if (ht[PT_MID] + ht[PT_LIGHT] > 0) {

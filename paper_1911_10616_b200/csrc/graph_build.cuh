@@ -166,11 +166,12 @@ __global__ void k_split_keys(const u64* __restrict__ dk, int64_t m2, int32_t* __
 
 // dm[u] = number of neighbours < u; dplus[u] = d(u) - dm[u]
 __global__ void k_split_counts(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                               int32_t* __restrict__ dm, int64_t* __restrict__ dplus) {
+                               int32_t* __restrict__ dm, int64_t* __restrict__ dplus, int32_t* __restrict__ deg) {
   for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
     int64_t lo = lower_bound_dev<int32_t>(ci, rp[u], rp[u + 1], u);
     dm[u] = (int32_t)(lo - rp[u]);
     dplus[u] = rp[u + 1] - lo;
+    deg[u] = (int32_t)(rp[u + 1] - rp[u]);
   }
 }
 

@@ -50,7 +50,7 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_WARP_CAP 1024       // light tier: per-warp packed hash entries (8 warps x 8 KB)
 #define PAIR_WARP_MAX 512        // light tier: est <= this
 #define PAIR_HBT 512             // heavy tier CTA
-#define PAIR_LONG 128            // item part longer than this: chunked, shared queue
+#define PAIR_LONG 64             // item part longer than this: chunked, shared queue
 #define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
 #define PAIR_LCAP 512            // long-part queue capacity per source pass
 #define PAIR_DIAM_INLINE 32      // diamond list longer than this: queued (CTA engine)
@@ -102,30 +102,39 @@ struct SharedPackedHash {
 
 // Dense per-CTA table in global memory indexed by x; W in the low half of the word,
 // D in the high half; touched list for the entry sweep and the reset.
-template <typename Word>
+template <typename Word, bool SCAN>
 struct GlobalDense {
+  // SCAN: the entries are found afterwards by sweeping the whole table (used when the
+  // 2-hop set is a sizeable fraction of n), so updates are fire-and-forget reductions;
+  // otherwise the first update of an entry appends x to the touched list.
+  // Reads go through L2 (__ldcg): the entries are updated by L2 atomics.
   Word* t;
   int32_t* L;
   int* ntouch;  // shared counter
   static constexpr int SH = (int)sizeof(Word) * 4;
   static constexpr Word LOW = (Word)(((u64)1 << SH) - 1);
-  __device__ __forceinline__ void touch(Word old, int32_t x) {
-    if (old == 0) L[atomicAdd(ntouch, 1)] = x;
+  __device__ __forceinline__ void upd(int32_t x, Word inc) {
+    if (SCAN) {
+      atomicAdd(&t[x], inc);
+    } else {
+      if (atomicAdd(&t[x], inc) == 0) L[atomicAdd(ntouch, 1)] = x;
+    }
   }
-  __device__ __forceinline__ void add_w(int32_t x) { touch(atomicAdd(&t[x], (Word)1), x); }
-  __device__ __forceinline__ void add_d(int32_t x) { touch(atomicAdd(&t[x], (Word)((Word)1 << SH)), x); }
+  __device__ __forceinline__ void add_w(int32_t x) { upd(x, (Word)1); }
+  __device__ __forceinline__ void add_d(int32_t x) { upd(x, (Word)((Word)1 << SH)); }
   __device__ __forceinline__ void get(int32_t x, u64& wv, u64& dv) const {
-    const Word v = t[x];
+    const Word v = __ldcg(&t[x]);
     wv = (u64)(v & LOW);
     dv = (u64)(v >> SH);
   }
-  __device__ __forceinline__ u64 get_w(int32_t x) const { return (u64)(t[x] & LOW); }
-  __device__ __forceinline__ u64 get_w_or0(int32_t x) const { return (u64)(t[x] & LOW); }
+  __device__ __forceinline__ u64 get_w(int32_t x) const { return (u64)(__ldcg(&t[x]) & LOW); }
+  __device__ __forceinline__ u64 get_w_or0(int32_t x) const { return (u64)(__ldcg(&t[x]) & LOW); }
 };
 
 // phase C contributions of one (x, W, D) pair
 __device__ __forceinline__ void pair_c_terms(const DGraph& g, int32_t x, u64 w, u64 d, u64& a8, u64& a36,
                                              u64& a50, u64& a63) {
+  if (w < 2) return;  // W = 1: every term is 0 (and D = 0)
   const u64 c2 = binom2(w);
   a8 += c2;
   a36 += c2 * (u64)(int64_t)(dg_deg(g, x) - 2);
@@ -184,6 +193,7 @@ __device__ __forceinline__ void pass2_wedge(const DGraph& g, const u32* __restri
   if (x == u) return;
   u64 w, d;
   tab.get(x, w, d);
+  if (w < 2) return;  // W(u,x) = 1 (hence D = 0) contributes nothing below
   A.c5 += w - 1;
   s51 += (u64)Te[g.eid[t]] * (w - 1);
   if (x > u) {
@@ -316,13 +326,17 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
   __syncthreads();
   CtaEnq enq{&E};
   const int64_t nitems = r1 - r0;
+  // items per warp grab: spread few items over all warps (one item per warp when the
+  // source has fewer items than warps), 32 when there are many
+  const int grab = (int)min((int64_t)32, max((int64_t)1, (nitems + (int64_t)(blockDim.x >> 5) - 1) /
+                                                          (int64_t)(blockDim.x >> 5)));
   for (;;) {
     int base = 0;
-    if (lane == 0) base = atomicAdd(&E.next, 32);
+    if (lane == 0) base = atomicAdd(&E.next, grab);
     base = __shfl_sync(FULL_MASK, base, 0);
     if (base >= nitems) break;
     PairItem it;
-    const bool have = base + lane < nitems;
+    const bool have = lane < grab && base + lane < nitems;
     if (have) it = pair_item(g, r0 + base + lane);
     else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
     // defer long parts to the queue (if it has room)
@@ -421,10 +435,43 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
         fv = it.v;
         fe = it.e;
         if (kind == PK_WEDGE) {
+          // PAIR_CHUNK / 32 elements per lane, all loads issued before the table updates
+          constexpr int U = PAIR_CHUNK / 32;
           const int k1 = min(it.dv, k0 + PAIR_CHUNK);
-          for (int k = k0 + lane; k < k1; k += 32) {
-            if (PASS == 2) pass2_wedge(g, Te, u, it.rb, k, tab, A, s51);
-            else pass1_wedge(g, u, it.rb, k, tab);
+          int32_t xs[U];
+#pragma unroll
+          for (int i = 0; i < U; i++) {
+            const int k = k0 + lane + 32 * i;
+            xs[i] = k < k1 ? g.ci[it.rb + k] : u;
+          }
+          if (PASS == 1) {
+#pragma unroll
+            for (int i = 0; i < U; i++)
+              if (xs[i] != u) tab.add_w(xs[i]);
+          } else {
+            u32 te[U];
+            u64 wv[U], dv[U];
+#pragma unroll
+            for (int i = 0; i < U; i++) {
+              wv[i] = 0; dv[i] = 0;
+              if (xs[i] != u) tab.get(xs[i], wv[i], dv[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < U; i++) {
+              const int k = k0 + lane + 32 * i;
+              te[i] = wv[i] >= 2 ? Te[g.eid[it.rb + k]] : 0u;  // W = 1 pairs contribute nothing
+            }
+#pragma unroll
+            for (int i = 0; i < U; i++) {
+              if (wv[i] < 2) continue;
+              const u64 w = wv[i];
+              A.c5 += w - 1;
+              s51 += (u64)te[i] * (w - 1);
+              if (xs[i] > u) {
+                A.c49 += binom2(w - 1);
+                A.c62 += dv[i];
+              }
+            }
           }
         } else {
           const int k1 = min(it.tv, k0 + PAIR_CHUNK);
@@ -451,12 +498,13 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   u64 s51 = 0;
   cta_pass<1>(g, Te, u, r0, r1, tab, E, s51, o);
   cta_pass<2>(g, Te, u, r0, r1, tab, E, s51, o);
-  u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
-  for_entries([&](int32_t x, u64 w, u64 d) { pair_c_terms(g, x, w, d, a8, a36, a50, a63); });
   for (int64_t s = r0 + threadIdx.x; s < r1; s += BT) {
     const u64 w = tab.get_w_or0(g.ci[s]);
     s51 -= w * (w - 1);
   }
+  __syncthreads();  // for_entries may clear the table
+  u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
+  for_entries([&](int32_t x, u64 w, u64 d) { pair_c_terms(g, x, w, d, a8, a36, a50, a63); });
   a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
   if ((threadIdx.x & 31) == 0) {
     if (a8) atomicAdd(&red[0], a8);
@@ -564,8 +612,9 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
   }
 }
 
-// Heavy tier: one CTA per source, dense per-CTA table (Word = u32 packed or u64).
-template <typename Word>
+// Heavy tier: one CTA per source, dense per-CTA table (Word = u32 packed or u64).  With
+// SCAN the table is swept once at the end (terms of every non-zero entry, then cleared).
+template <typename Word, bool SCAN>
 __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* __restrict__ Te,
                                                           const int32_t* __restrict__ srcs, int nsrc,
                                                           int* __restrict__ counter, Word* __restrict__ tabs,
@@ -573,9 +622,9 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
   __shared__ EngShared E;
   __shared__ u64 red[5];
   __shared__ int s_idx, s_ntouch;
-  GlobalDense<Word> tab;
+  GlobalDense<Word, SCAN> tab;
   tab.t = tabs + (size_t)blockIdx.x * g.n;
-  tab.L = lists + (size_t)blockIdx.x * g.n;
+  tab.L = SCAN ? nullptr : lists + (size_t)blockIdx.x * g.n;
   tab.ntouch = &s_ntouch;
   if (threadIdx.x < 5) red[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_ntouch = 0;
@@ -588,20 +637,38 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
     const int32_t u = srcs[idx];
     pair_source_cta<PAIR_HBT>(g, Te, u, tab, E, red, o,
         [&](auto f) {
-          const int nt = s_ntouch;
-          for (int i = threadIdx.x; i < nt; i += PAIR_HBT) {
-            const int32_t x = tab.L[i];
-            u64 w, d;
-            tab.get(x, w, d);
-            f(x, w, d);
+          if (SCAN) {
+            // one coalesced sweep: terms of every entry, then clear it
+            for (int32_t x0 = threadIdx.x * 4; x0 < g.n; x0 += PAIR_HBT * 4) {
+              Word v[4];
+#pragma unroll
+              for (int i = 0; i < 4; i++) v[i] = (x0 + i < g.n) ? __ldcg(&tab.t[x0 + i]) : (Word)0;
+#pragma unroll
+              for (int i = 0; i < 4; i++)
+                if (v[i]) {
+                  const u64 w = (u64)(v[i] & GlobalDense<Word, SCAN>::LOW);
+                  if (w >= 2) f(x0 + i, w, (u64)(v[i] >> GlobalDense<Word, SCAN>::SH));
+                  tab.t[x0 + i] = (Word)0;
+                }
+            }
+          } else {
+            const int nt = s_ntouch;
+            for (int i = threadIdx.x; i < nt; i += PAIR_HBT) {
+              const int32_t x = tab.L[i];
+              u64 w, d;
+              tab.get(x, w, d);
+              f(x, w, d);
+            }
           }
         },
         [&]() {
-          __syncthreads();
-          const int nt = s_ntouch;
-          for (int i = threadIdx.x; i < nt; i += PAIR_HBT) tab.t[tab.L[i]] = (Word)0;
-          __syncthreads();
-          if (threadIdx.x == 0) s_ntouch = 0;
+          if (!SCAN) {
+            __syncthreads();
+            const int nt = s_ntouch;
+            for (int i = threadIdx.x; i < nt; i += PAIR_HBT) tab.t[tab.L[i]] = (Word)0;
+            __syncthreads();
+            if (threadIdx.x == 0) s_ntouch = 0;
+          }
         });
   }
 }
@@ -626,7 +693,7 @@ __global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict
 
 // Shard filter of the est-sorted (descending) vertex list and tier classification.
 // Lists keep the descending order approximately (warp-aggregated appends in list order).
-enum { PT_G64 = 0, PT_G32, PT_MID, PT_LIGHT, PT_COUNT };
+enum { PT_G64 = 0, PT_G32, PT_G32S, PT_MID, PT_LIGHT, PT_COUNT };
 __global__ void k_pair_classify(DGraph g, const u64* __restrict__ skeys, const int32_t* __restrict__ svals,
                                 int si, int ns, const u64* __restrict__ Tv, u32* __restrict__ est_v,
                                 int32_t* __restrict__ lists, int* __restrict__ counts) {
@@ -643,7 +710,11 @@ __global__ void k_pair_classify(DGraph g, const u64* __restrict__ skeys, const i
       est_v[u] = (u32)min(e, (u64)0xffffffffu);
       if (e > 0) {
         const bool packed_ok = dg_deg(g, u) < 65536 && Tv[u] < 65536ull;
-        tier = !packed_ok ? PT_G64 : e <= PAIR_WARP_MAX ? PT_LIGHT : e <= PAIR_MID_MAX ? PT_MID : PT_G32;
+        tier = !packed_ok ? PT_G64
+             : e <= PAIR_WARP_MAX ? PT_LIGHT
+             : e <= PAIR_MID_MAX ? PT_MID
+             : e * 16 >= (u64)g.n ? PT_G32S  // 2-hop set a sizeable part of n: sweep the table
+             : PT_G32;
       }
     }
     for (int t = 0; t < PT_COUNT; t++) warp_append(tier == t, u, lists + (size_t)t * g.n, counts + t);
