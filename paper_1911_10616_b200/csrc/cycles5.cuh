@@ -8,8 +8,8 @@
 // w=j (j~l); pass 2 credits w with P(i,l), the number of such paths from
 // i to l, minus the tailed triangles where the path runs through w.
 //
-// B200 formulation: one CTA per endpoint l.  Instead of enumerating the DP(G->) paths
-// one by one, the CTA builds dense tables keyed by vertex:
+// B200 formulation: one work unit per endpoint l.  Instead of enumerating the DP(G->)
+// paths one by one, the unit builds records keyed by vertex:
 //   Wn[i]  = #non-in-in wedges (i, w, l)
 //   Q[j]   = |N-(j) & N-(l)|   (out-out wedges k: j <- k -> l),  QT[j], QM[j] = the
 //            same sum weighted by T_high(k,j), T_mid(k,j) (typed triangle counts)
@@ -23,158 +23,362 @@
 //   w : sum over non-in-in wedges (i,w,l) of P[i] - [w<i] T_low(w,l)
 //                                   - [w<l, w<i] (T_mid(w,i) - [l<i, l~i])
 // Each (path, wedge) pair with distinct vertices is one 5-cycle; the tests check the
-// identity against brute force (tests/test_gpu_parity.py) and the prototype derivation
-// is written out in DESIGN.md.
+// identity against brute force (tests/test_gpu_parity.py).
+//
+// Scheduling (B200): k_c5_items measures every endpoint's work W(l) (steps 1/6, 2/4 and
+// an upper bound of step 3) and splits the endpoints into light ones (one WARP each,
+// records in a per-warp open-addressing region) and heavy ones (one CTA each, sorted by
+// W descending, records dense by vertex id).  Records are 64-byte AoS (one or two
+// sectors per touched vertex).  All list walks go through the load-balanced engines
+// of sched.cuh (warp_lists / cta_lists).
 #pragma once
 #include "common.cuh"
+#include "sched.cuh"
 
-struct C5Tables {
-  u32* Wn; u32* Q; u64* P; u64* A; u64* QT; u64* QM; u64* S; u32* flag; int32_t* Li; int32_t* Lj;
+struct __align__(16) C5Rec {
+  int32_t key;   // hash regions: x + 1 (0 = empty); unused in dense tables
+  u32 flag;      // C5_* bits
+  u32 Wn;
+  u32 Q;
+  u64 P, A, QT, QM, S;
+  u64 pad;
+};
+#define C5_ADJ 1u      // vertex is a neighbour of l
+#define C5_I 2u        // i-key (steps 1, 3)
+#define C5_J 4u        // j-key (step 2)
+#define C5_PRESENT 8u  // record in use (touched list)
+
+#define C5_BT 256
+#define C5_WARP_MAX 1024          // light endpoint: W(l) + d(l) <= this
+#define C5_WARP_CAP 2048          // records per warp region (load <= 0.5)
+
+// dense records indexed by vertex id; touched list holds vertex ids
+struct C5Dense {
+  C5Rec* R;
+  int32_t* L;
+  int* nL;
+  __device__ __forceinline__ C5Rec* mark(int32_t x, u32 bits, u32& old) {
+    C5Rec* r = &R[x];
+    old = atomicOr(&r->flag, bits | C5_PRESENT);
+    append_active(!(old & C5_PRESENT), x, L, nL);
+    return r;
+  }
+  __device__ __forceinline__ C5Rec* peek(int32_t x) const { return &R[x]; }
+  __device__ __forceinline__ C5Rec* touched(int t, int32_t& x) const {
+    x = L[t];
+    return &R[x];
+  }
 };
 
-__device__ __forceinline__ void c5_mark(u32* flag, int32_t* list, int* cnt, int32_t x, u32 bit) {
-  const u32 old = atomicOr(&flag[x], bit);
-  if (!(old & bit)) list[atomicAdd(cnt, 1)] = x;
-}
+// open-addressing records (key = x + 1); touched list holds slots
+struct C5Hash {
+  C5Rec* R;
+  u32 mask;
+  int32_t* L;
+  int* nL;
+  __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) >> 7 & mask; }
+  __device__ __forceinline__ C5Rec* mark(int32_t x, u32 bits, u32& old) {
+    u32 h = h0(x);
+    for (;;) {
+      const int32_t k = R[h].key;
+      if (k == x + 1) break;
+      if (k == 0) {
+        const int32_t o = atomicCAS(&R[h].key, 0, x + 1);
+        if (o == 0 || o == x + 1) break;
+      }
+      h = (h + 1) & mask;
+    }
+    C5Rec* r = &R[h];
+    old = atomicOr(&r->flag, bits | C5_PRESENT);
+    append_active(!(old & C5_PRESENT), (int32_t)h, L, nL);
+    return r;
+  }
+  __device__ __forceinline__ C5Rec* peek(int32_t x) const {
+    u32 h = h0(x);
+    for (;;) {
+      const int32_t k = R[h].key;
+      if (k == x + 1) return &R[h];
+      if (k == 0) return nullptr;
+      h = (h + 1) & mask;
+    }
+  }
+  __device__ __forceinline__ C5Rec* touched(int t, int32_t& x) const {
+    C5Rec* r = &R[L[t]];
+    x = r->key - 1;
+    return r;
+  }
+};
 
-__global__ void __launch_bounds__(512) k_cycles5(DGraph g, const u32* __restrict__ Tlow,
-                                                 const u32* __restrict__ Tmid,
-                                                 const u32* __restrict__ Thigh,
-                                                 const int32_t* __restrict__ ls, int nl,
-                                                 int* __restrict__ counter, C5Tables tb,
-                                                 u64* __restrict__ C5) {
-  __shared__ int s_idx, s_ni, s_nj;
-  __shared__ u64 s_tot;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-  const size_t off = (size_t)blockIdx.x * (size_t)g.n;
-  u32* Wn = tb.Wn + off; u32* Q = tb.Q + off; u64* P = tb.P + off; u64* A = tb.A + off;
-  u64* QT = tb.QT + off; u64* QM = tb.QM + off; u64* S = tb.S + off; u32* flag = tb.flag + off;
-  int32_t* Li = tb.Li + off; int32_t* Lj = tb.Lj + off;
-  if (threadIdx.x == 0) { s_ni = 0; s_nj = 0; s_tot = 0; }
-  for (;;) {
-    if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
-    __syncthreads();
-    const int idx = s_idx;
-    if (idx >= nl) break;
-    const int32_t l = ls[idx];
-    const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rmid = r0 + g.dm[l];
-    for (int64_t s = r0 + threadIdx.x; s < r1; s += blockDim.x) flag[g.ci[s]] = 1u;
-    __syncthreads();
-    // step 1: non-in-in wedges (i, w, l)
-    for (int64_t s = r0 + wib; s < r1; s += nwb) {
-      const int32_t w = g.ci[s];
-      const int64_t t0 = (w < l) ? g.rp[w] : g.rp[w] + g.dm[w];
-      for (int64_t t = t0 + lane; t < g.rp[w + 1]; t += 32) {
-        const int32_t i = g.ci[t];
-        if (i == l) continue;
-        atomicAdd(&Wn[i], 1u);
-        c5_mark(flag, Li, &s_ni, i, 2u);
-      }
-    }
-    // step 2: out-out wedges j <- k -> l, k in N-(l)
-    for (int64_t s = r0 + wib; s < rmid; s += nwb) {
-      const int32_t k = g.ci[s];
-      const int64_t ok = g.orow[k];
-      const int32_t dk = (int32_t)(g.orow[k + 1] - ok);
-      for (int t = lane; t < dk; t += 32) {
-        const int32_t j = g.ocol[ok + t];
-        if (j == l) continue;
-        atomicAdd(&Q[j], 1u);
-        atomicAdd(&QT[j], (u64)Thigh[ok + t]);
-        atomicAdd(&QM[j], (u64)Tmid[ok + t]);
-        c5_mark(flag, Lj, &s_nj, j, 4u);
-      }
-    }
-    __syncthreads();
-    // step 3: paths through j: P, A, S and the j credits
-    const int nj = s_nj;
-    for (int t = wib; t < nj; t += nwb) {
-      const int32_t j = Lj[t];
-      const u64 q = Q[j];
-      const bool adjj = flag[j] & 1u;
-      const u64 lj = (l > j && adjj) ? 1ull : 0ull;
-      const int64_t oj = g.orow[j];
-      const int32_t dj = (int32_t)(g.orow[j + 1] - oj);
-      u64 s = 0;
-      for (int c = lane; c < dj; c += 32) {
-        const int32_t i = g.ocol[oj + c];
-        if (i == l) continue;
-        s += Wn[i];
-        atomicAdd(&P[i], q);
-        if (adjj) atomicAdd(&A[i], q);
-        c5_mark(flag, Li, &s_ni, i, 2u);
-      }
-      s = warp_sum(s);
-      if (lane == 0) {
-        S[j] = s;
-        const u64 cj = q * s - q * (adjj ? 1ull : 0ull) * ((u64)dj - lj) - (QT[j] - q * lj);
-        if (cj) atomicAdd(&C5[j], cj);
-      }
-    }
-    __syncthreads();
-    // step 4: k credits
-    for (int64_t s = r0 + wib; s < rmid; s += nwb) {
-      const int32_t k = g.ci[s];
-      const int64_t ok = g.orow[k];
-      const int32_t dk = (int32_t)(g.orow[k + 1] - ok);
-      u64 ck = 0;
-      for (int t = lane; t < dk; t += 32) {
-        const int32_t j = g.ocol[ok + t];
-        if (j == l) continue;
-        const bool adjj = flag[j] & 1u;
+// Engine adaptors: warp (light endpoints) and CTA (heavy endpoints)
+struct WarpEng {
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  __device__ __forceinline__ int tid() const { return threadIdx.x & 31; }
+  __device__ __forceinline__ int nthr() const { return 32; }
+  template <typename I, typename E, typename F>
+  __device__ __forceinline__ void lists(int n, I info, E elem, F flush) const { warp_lists(n, info, elem, flush); }
+};
+struct CtaEng {
+  ListEng* E;
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ int nthr() const { return blockDim.x; }
+  template <typename I, typename E2, typename F>
+  __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const { cta_lists(n, *E, info, elem, flush); }
+};
+
+__device__ __forceinline__ bool c5_adj(const C5Rec* r) { return r && (r->flag & C5_ADJ); }
+
+// One endpoint l.  J: list of j-keys (counter *nJ); tot: per-engine shared u64 (zeroed).
+template <typename Eng, typename Loc>
+__device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const u32* __restrict__ Tmid,
+                            const u32* __restrict__ Thigh, int32_t l, const Eng& eng, Loc& loc, int32_t* J,
+                            int* nJ, u64* tot, u64* __restrict__ C5) {
+  const int64_t r0 = g.rp[l];
+  const int dl = g.deg[l];
+  const int dml = g.dm[l];
+  // ---- step 0: neighbours of l
+  for (int t = eng.tid(); t < dl; t += eng.nthr()) {
+    u32 old;
+    loc.mark(g.ci[r0 + t], C5_ADJ, old);
+  }
+  // wedge lists of steps 1/6: w = N(l)[t], i in N(w) (w < l) or N+(w) (w > l)
+  auto winfo = [&](int t, int64_t& base, int& len) {
+    const int32_t w = g.ci[r0 + t];
+    base = (w < l) ? g.rp[w] : g.rp[w] + g.dm[w];
+    len = (int)(g.rp[w + 1] - base);
+  };
+  // out-out lists of steps 2/4: k = N-(l)[t], j in N+(k) (edge ids orow[k] + .)
+  auto kinfo = [&](int t, int64_t& base, int& len) {
+    const int32_t k = g.ci[r0 + t];
+    base = g.orow[k];
+    len = (int)(g.orow[k + 1] - base);
+  };
+  // ---- step 1: Wn over non-in-in wedges (i, w, l)
+  eng.lists(dl, winfo,
+      [&](int, int64_t base, int k) -> u64 {
+        const int32_t i = g.ci[base + k];
+        if (i == l) return 0;
+        u32 old;
+        C5Rec* r = loc.mark(i, C5_I, old);
+        atomicAdd(&r->Wn, 1u);
+        return 0;
+      },
+      [&](int, u64) {});
+  // ---- step 2: Q, QT, QM over out-out wedges j <- k -> l
+  eng.lists(dml, kinfo,
+      [&](int, int64_t base, int k) -> u64 {
+        const int64_t e = base + k;
+        const int32_t j = g.ocol[e];
+        if (j == l) return 0;
+        u32 old;
+        C5Rec* r = loc.mark(j, C5_J, old);
+        append_active(!(old & C5_J), j, J, nJ);
+        atomicAdd(&r->Q, 1u);
+        atomicAdd(&r->QT, (u64)Thigh[e]);
+        atomicAdd(&r->QM, (u64)Tmid[e]);
+        return 0;
+      },
+      [&](int, u64) {});
+  eng.sync();
+  // ---- step 3: paths through j: P, A (to i), S and the j credits
+  const int nj = *nJ;
+  eng.lists(nj,
+      [&](int t, int64_t& base, int& len) {
+        const int32_t j = J[t];
+        base = g.orow[j];
+        len = (int)(g.orow[j + 1] - base);
+      },
+      [&](int t, int64_t base, int k) -> u64 {
+        const int32_t i = g.ocol[base + k];
+        if (i == l) return 0;
+        const C5Rec* rj = loc.peek(J[t]);
+        const u64 q = rj->Q;
+        const bool adjj = rj->flag & C5_ADJ;
+        u32 old;
+        C5Rec* ri = loc.mark(i, C5_I, old);
+        atomicAdd(&ri->P, q);
+        if (adjj) atomicAdd(&ri->A, q);
+        return (u64)ri->Wn;  // Wn is final after step 1
+      },
+      [&](int t, u64 s) {
+        C5Rec* rj = loc.peek(J[t]);
+        atomicAdd(&rj->S, s);
+        atomicAdd(&C5[J[t]], (u64)rj->Q * s);  // the j credit is linear in S
+      });
+  // constant part of the j credits
+  for (int t = eng.tid(); t < nj; t += eng.nthr()) {
+    const int32_t j = J[t];
+    const C5Rec* rj = loc.peek(j);
+    const u64 q = rj->Q;
+    const bool adjj = rj->flag & C5_ADJ;
+    const u64 lj = (l > j && adjj) ? 1ull : 0ull;
+    const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
+    const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rj->QT - q * lj);
+    if (c) atomicAdd(&C5[j], (u64)0 - c);
+  }
+  eng.sync();
+  // ---- step 4: k credits
+  eng.lists(dml, kinfo,
+      [&](int, int64_t base, int k) -> u64 {
+        const int64_t e = base + k;
+        const int32_t j = g.ocol[e];
+        if (j == l) return 0;
+        const C5Rec* rj = loc.peek(j);
+        const bool adjj = rj->flag & C5_ADJ;
         const u64 lj = (l > j && adjj) ? 1ull : 0ull;
         const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-        ck += S[j] - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[ok + t] - lj);
-      }
-      ck = warp_sum(ck);
-      if (lane == 0 && ck) atomicAdd(&C5[k], ck);
+        return rj->S - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[e] - lj);
+      },
+      [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
+  // ---- step 5: i credits (and their sum for l)
+  {
+    const int nt = *loc.nL;
+    u64 acc = 0;
+    for (int t = eng.tid(); t < nt; t += eng.nthr()) {
+      int32_t x;
+      const C5Rec* r = loc.touched(t, x);
+      if (!(r->flag & C5_I)) continue;
+      const bool adji = r->flag & C5_ADJ;
+      const u64 bi = r->QM - (u64)r->Q * ((x > l && adji) ? 1ull : 0ull);
+      const u64 ci = r->P * (u64)r->Wn - r->A - bi;
+      if (ci) atomicAdd(&C5[x], ci);
+      acc += ci;
     }
-    // step 5: i credits (and their sum for l)
-    const int ni = s_ni;
-    {
-      u64 tot = 0;
-      for (int t = threadIdx.x; t < ni; t += blockDim.x) {
-        const int32_t i = Li[t];
-        const bool adji = flag[i] & 1u;
-        const u64 bi = QM[i] - (u64)Q[i] * ((i > l && adji) ? 1ull : 0ull);
-        const u64 ci = P[i] * (u64)Wn[i] - A[i] - bi;
-        if (ci) atomicAdd(&C5[i], ci);
-        tot += ci;
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(tot, acc);
+  }
+  // ---- step 6: wedge centres w
+  eng.lists(dl, winfo,
+      [&](int t, int64_t base, int k) -> u64 {
+        const int64_t s = base + k;
+        const int32_t i = g.ci[s];
+        if (i == l) return 0;
+        const int32_t w = g.ci[r0 + t];
+        const C5Rec* ri = loc.peek(i);
+        u64 corr = (w < i) ? (u64)Tlow[g.eid[r0 + t]] : 0ull;
+        if (w < l && w < i) corr += (u64)Tmid[g.eid[s]] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
+        return ri->P - corr;
+      },
+      [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
+  eng.sync();
+}
+
+// reset every touched record (and the counters) of one endpoint
+template <typename Eng, typename Loc>
+__device__ __forceinline__ void c5_reset(const Eng& eng, Loc& loc) {
+  const int nt = *loc.nL;
+  for (int t = eng.tid(); t < nt; t += eng.nthr()) {
+    int32_t x;
+    C5Rec* r = loc.touched(t, x);
+    uint4* q = reinterpret_cast<uint4*>(r);
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    q[0] = z; q[1] = z; q[2] = z; q[3] = z;
+  }
+}
+
+// ---- per-endpoint work, binning -----------------------------------------------------------
+// W(l) = sum_{w in N(l)} |Nsel(w)| + sum_{k in N-(l)} (d+(k) + sum_{j in N+(k)} d+(j)) + d(l)
+// bounds the records an endpoint touches.  Light: W <= C5_WARP_MAX (the count stops
+// there); heavy otherwise, with sort key d(l)^2 + W (hubs first).
+__global__ void k_c5_items(DGraph g, int shard_index, int num_shards, int32_t* __restrict__ light, int* n_light,
+                           int32_t* __restrict__ heavy, u64* __restrict__ heavy_w, int* n_heavy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = gw * 32; base < g.n; base += nw * 32) {
+    const int32_t l = (int32_t)min(base + lane, (int64_t)g.n - 1);
+    const bool mine = base + lane < g.n && (l % num_shards) == shard_index && g.deg[l] > 0;
+    u64 w = 0;
+    if (mine) {
+      const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
+      w = (u64)g.deg[l];
+      for (int64_t s = r0; s < r1 && w <= C5_WARP_MAX; s++) {
+        const int32_t x = g.ci[s];
+        w += (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
+        if (s < rm) {
+          const int64_t ok = g.orow[x], ok1 = g.orow[x + 1];
+          w += (u64)(ok1 - ok);
+          for (int64_t e = ok; e < ok1 && w <= C5_WARP_MAX; e++) {
+            const int32_t j = g.ocol[e];
+            w += (u64)(g.orow[j + 1] - g.orow[j]);
+          }
+        }
       }
-      tot = warp_sum(tot);
-      if (lane == 0 && tot) atomicAdd(&s_tot, tot);
     }
-    // step 6: wedge centres w
-    for (int64_t s = r0 + wib; s < r1; s += nwb) {
-      const int32_t w = g.ci[s];
-      const u64 tlow = Tlow[g.eid[s]];
-      const int64_t t0 = (w < l) ? g.rp[w] : g.rp[w] + g.dm[w];
-      u64 acc = 0;
-      for (int64_t t = t0 + lane; t < g.rp[w + 1]; t += 32) {
-        const int32_t i = g.ci[t];
-        if (i == l) continue;
-        u64 corr = (w < i) ? tlow : 0ull;
-        if (w < l && w < i) corr += (u64)Tmid[g.eid[t]] - ((l < i && (flag[i] & 1u)) ? 1ull : 0ull);
-        acc += P[i] - corr;
+    const bool is_light = mine && w <= C5_WARP_MAX;
+    const bool is_heavy = mine && w > C5_WARP_MAX;
+    warp_append(is_light, l, light, n_light);
+    const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
+    if (bal) {
+      int hb = 0;
+      const int leader = __ffs(bal) - 1;
+      if (lane == leader) hb = atomicAdd(n_heavy, __popc(bal));
+      hb = __shfl_sync(FULL_MASK, hb, leader);
+      if (is_heavy) {
+        const int q = hb + __popc(bal & ((1u << lane) - 1u));
+        heavy[q] = l;
+        heavy_w[q] = (u64)g.deg[l] * (u64)g.deg[l] + w;
       }
-      acc = warp_sum(acc);
-      if (lane == 0 && acc) atomicAdd(&C5[w], acc);
     }
+  }
+}
+
+// Heavy endpoints: one CTA each, dense records per CTA (persistent, W-sorted list).
+__global__ void __launch_bounds__(C5_BT) k_c5_heavy(DGraph g, const u32* __restrict__ Tlow,
+                                                    const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
+                                                    const int32_t* __restrict__ heavy, int n_heavy,
+                                                    int* __restrict__ counter, C5Rec* __restrict__ dense,
+                                                    int32_t* __restrict__ dlists, u64* __restrict__ C5) {
+  __shared__ ListEng E;
+  __shared__ int s_idx, s_nL, s_nJ;
+  __shared__ u64 s_tot;
+  CtaEng eng{&E};
+  C5Dense loc;
+  loc.R = dense + (size_t)blockIdx.x * g.n;
+  loc.L = dlists + (size_t)blockIdx.x * 2 * g.n;
+  loc.nL = &s_nL;
+  int32_t* J = loc.L + g.n;
+  for (;;) {
+    if (threadIdx.x == 0) { s_idx = atomicAdd(counter, 1); s_nL = 0; s_nJ = 0; s_tot = 0; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (s_tot) atomicAdd(&C5[l], s_tot);
-      s_tot = 0; s_ni = 0; s_nj = 0;
-    }
-    // reset
-    for (int t = threadIdx.x; t < ni; t += blockDim.x) {
-      const int32_t i = Li[t];
-      Wn[i] = 0; P[i] = 0; A[i] = 0; flag[i] = 0;
-    }
-    for (int t = threadIdx.x; t < nj; t += blockDim.x) {
-      const int32_t j = Lj[t];
-      Q[j] = 0; QT[j] = 0; QM[j] = 0; S[j] = 0; flag[j] = 0;
-    }
-    for (int64_t s = r0 + threadIdx.x; s < r1; s += blockDim.x) flag[g.ci[s]] = 0;
+    const int idx = s_idx;
+    if (idx >= n_heavy) break;
+    const int32_t l = heavy[idx];
+    c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &s_nJ, &s_tot, C5);
+    if (threadIdx.x == 0 && s_tot) atomicAdd(&C5[l], s_tot);
+    c5_reset(eng, loc);
     __syncthreads();
+  }
+}
+
+// Light endpoints: one warp each, records in a per-warp open-addressing region.
+__global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restrict__ Tlow,
+                                                    const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
+                                                    const int32_t* __restrict__ light, int n_light,
+                                                    int* __restrict__ counter, C5Rec* __restrict__ wregions,
+                                                    int32_t* __restrict__ wlists, u64* __restrict__ C5) {
+  __shared__ int w_nL[C5_BT / 32], w_nJ[C5_BT / 32];
+  __shared__ u64 w_tot[C5_BT / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t gw = (size_t)blockIdx.x * (C5_BT / 32) + wib;
+  WarpEng eng;
+  C5Hash loc;
+  loc.R = wregions + gw * C5_WARP_CAP;
+  loc.L = wlists + gw * 2 * C5_WARP_CAP;
+  loc.nL = &w_nL[wib];
+  loc.mask = C5_WARP_CAP - 1;
+  int32_t* J = loc.L + C5_WARP_CAP;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1);
+    idx = __shfl_sync(FULL_MASK, idx, 0);
+    if (idx >= n_light) break;
+    const int32_t l = light[idx];
+    if (lane == 0) { w_nL[wib] = 0; w_nJ[wib] = 0; w_tot[wib] = 0; }
+    __syncwarp();
+    c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &w_nJ[wib], &w_tot[wib], C5);
+    if (lane == 0 && w_tot[wib]) atomicAdd(&C5[l], w_tot[wib]);
+    c5_reset(eng, loc);
+    __syncwarp();
   }
 }

@@ -191,27 +191,6 @@ __global__ void k_wedges(const int64_t* __restrict__ rp, int32_t n, u64* out) {
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
-// work-sorted vertex lists: key = work estimate, descending; shard by position
-__global__ void k_work_pair(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int32_t n,
-                            u64* __restrict__ keys, int32_t* __restrict__ vals) {
-  // pair pass cost ~ sum_{v in N(u)} d(v)  (approximated by d(u) * d_max-capped mean)
-  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    u64 w = 0;
-    const int64_t a = rp[u], b = rp[u + 1];
-    const int64_t lim = min(b, a + 64);
-    for (int64_t s = a; s < lim; s++) w += (u64)(rp[ci[s] + 1] - rp[ci[s]]);
-    if (b > lim) w = w * (u64)(b - a) / 64ull;
-    keys[u] = ~w;  // ascending sort of ~w = descending w
-    vals[u] = u;
-  }
-}
-
-__global__ void k_shard_list(const int32_t* __restrict__ sorted, int32_t n, int si, int ns,
-                             int32_t* __restrict__ out) {
-  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    if (p % ns == si) out[p / ns] = sorted[p];
-}
-
 // clique bins by k = d+(u): bin 0: 3..32, 1: 33..128, 2: 129..512, 3: 513..1024, 4: >1024
 __global__ void k_clique_bins(const int64_t* __restrict__ orow, int32_t n, int32_t* __restrict__ lists,
                               int* __restrict__ counts) {
@@ -369,12 +348,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* l0 = A.alloc<int32_t>(n);
     int32_t* l1 = A.alloc<int32_t>(n);
     PeelCtl* ctl = A.alloc<PeelCtl>(1, true);
+    int32_t* al0 = A.alloc<int32_t>(std::min<int64_t>(n, PEEL_SWITCH) + 1);
+    int32_t* al1 = A.alloc<int32_t>(std::min<int64_t>(n, PEEL_SWITCH) + 1);
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel, 512, 0));
-    int pgrid = std::max(1, std::min(bps, 2)) * SM;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel, PEEL_BT, 0));
+    // small graphs: the whole peel on one CTA (block barriers); large: grid-wide first
+    const int pgrid = n <= PEEL_SWITCH ? 1 : std::max(1, std::min(bps, 1)) * SM;
     void* args[] = {(void*)&n, (void*)&rp0, (void*)&adj0, (void*)&deg0, (void*)&rnd, (void*)&l0,
-                    (void*)&l1, (void*)&ctl};
-    CK(cudaLaunchCooperativeKernel((void*)k_peel, pgrid, 512, args, 0, C.st));
+                    (void*)&l1, (void*)&al0, (void*)&al1, (void*)&ctl};
+    CK(cudaLaunchCooperativeKernel((void*)k_peel, pgrid, PEEL_BT, args, 0, C.st));
     C.launches++;
     PeelCtl hc = d2h_scalar<PeelCtl>(ctl, C.st);
     peel_rounds = hc.rounds;
@@ -386,7 +368,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     sort_keys_u64(A, C, okeys, osorted, n, 32 + bits_for(std::max(peel_rounds, 1)));
     k_perm<<<grid_for(n, B, SM), B, 0, C.st>>>(osorted, n, perm, inv);
     C.launches++;
-    A.release(okeys); A.release(osorted); A.release(rnd); A.release(l0); A.release(l1);
+    A.release(okeys); A.release(osorted); A.release(rnd); A.release(l0); A.release(l1); A.release(al0); A.release(al1);
     A.release(cursor); A.release(deg64);
   }
   A.release(adj0); A.release(rp0); A.release(deg0);
@@ -578,24 +560,6 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
 
   // ------------------------------------------------------------------ a7: pair pass
   C.mark(P_PAIR);
-  int32_t* vsorted = A.alloc<int32_t>(std::max(n, 1));
-  int32_t* shard_list = A.alloc<int32_t>(std::max(n, 1));
-  int nshard = 0;
-  if (n > 0) {
-    u64* wk = A.alloc<u64>(n);
-    u64* wk2 = A.alloc<u64>(n);
-    int32_t* vv = A.alloc<int32_t>(n);
-    k_work_pair<<<grid_for(n, B, SM), B, 0, C.st>>>(rp, ci, n, wk, vv);
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, wk, wk2, vv, vsorted, (int64_t)n, 0, 64, C.st));
-    void* t = A.alloc<char>(tb);
-    CK(cub::DeviceRadixSort::SortPairs(t, tb, wk, wk2, vv, vsorted, (int64_t)n, 0, 64, C.st));
-    k_shard_list<<<grid_for(n, B, SM), B, 0, C.st>>>(vsorted, n, si, ns, shard_list);
-    C.launches += 6;
-    nshard = (n - si + ns - 1) / ns;
-    if (nshard < 0) nshard = 0;
-    A.release(t); A.release(wk); A.release(wk2); A.release(vv);
-  }
   if (n > 0 && m > 0) {
     // source lists by 2-hop estimate (descending), sharded by position, split in tiers
     u64* pk = A.alloc<u64>(n);
@@ -636,19 +600,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       CK(cudaEventRecord(C.ev_fork, C.st));
       CK(cudaStreamWaitEvent(side, C.ev_fork, 0));
       const int pg = heavy_grid(ht[PT_G64], 8, SM / 2);
-      u64* tabs = A.alloc_on<u64>(side, (size_t)pg * n, true);
-      int32_t* lists = A.alloc_on<int32_t>(side, (size_t)pg * n);
+      u64* tabs = A.alloc_on<u64>(side, (size_t)pg * (size_t)((n + 1) / 2 * 2), true);
+      int32_t* lists = A.alloc_on<int32_t>(side, (size_t)pg * 2 * n);
       int* counter = A.alloc_on<int>(side, 1, true);
-      k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, side>>>(g, Te, plist(PT_G64), ht[PT_G64], counter, tabs, lists,
-                                                           po);
+      k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, side>>>(g, Te, plist(PT_G64), ht[PT_G64], counter, tabs, lists, po);
       C.launches++;
       CK(cudaEventRecord(C.ev_join, side));
     }
     for (int tier : {PT_G32S, PT_G32}) {
       if (ht[tier] == 0) continue;
-      const int pg = heavy_grid(ht[tier], 4, 2 * SM);
-      u32* tabs = A.alloc<u32>((size_t)pg * n, true);
-      int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * n) : nullptr;
+      const int pg = heavy_grid(ht[tier], 4, SM);
+      u32* tabs = A.alloc<u32>((size_t)pg * (size_t)((n + 3) / 4 * 4), true);
+      int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * 2 * n) : nullptr;
       int* counter = A.alloc<int>(1, true);
       if (tier == PT_G32S)
         k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(tier), ht[tier], counter, tabs, lists, po);
@@ -714,28 +677,54 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
 
   // ------------------------------------------------------------------ a10: 5-cycles
   C.mark(P_C5);
-  if (n > 0 && m > 0 && nshard > 0) {
-    size_t freeb = 0, totalb = 0;
-    CK(cudaMemGetInfo(&freeb, &totalb));
-    const size_t per = (size_t)n * 61;
-    int cg5 = std::min<int64_t>(2 * SM, std::max<int64_t>(1, (int64_t)(freeb / 3) / (int64_t)per));
-    cg5 = std::min(cg5, nshard);
-    C5Tables tb;
-    tb.Wn = A.alloc<u32>((size_t)cg5 * n, true);
-    tb.Q = A.alloc<u32>((size_t)cg5 * n, true);
-    tb.P = A.alloc<u64>((size_t)cg5 * n, true);
-    tb.A = A.alloc<u64>((size_t)cg5 * n, true);
-    tb.QT = A.alloc<u64>((size_t)cg5 * n, true);
-    tb.QM = A.alloc<u64>((size_t)cg5 * n, true);
-    tb.S = A.alloc<u64>((size_t)cg5 * n, true);
-    tb.flag = A.alloc<u32>((size_t)cg5 * n, true);
-    tb.Li = A.alloc<int32_t>((size_t)cg5 * n);
-    tb.Lj = A.alloc<int32_t>((size_t)cg5 * n);
-    int* counter = A.alloc<int>(1, true);
-    k_cycles5<<<cg5, 512, 0, C.st>>>(g, Tlow, Tmid, Thigh, shard_list, nshard, counter, tb, Fp(F_C5));
+  if (n > 0 && m > 0) {
+    int32_t* c5l = A.alloc<int32_t>(n);
+    int32_t* c5h = A.alloc<int32_t>(n);
+    u64* c5w = A.alloc<u64>(n);
+    int* c5c = A.alloc<int>(4, true);
+    k_c5_items<<<warp_grid, B, 0, C.st>>>(g, si, ns, c5l, c5c, c5h, c5w, c5c + 1);
     C.launches++;
-    A.release(tb.Wn); A.release(tb.Q); A.release(tb.P); A.release(tb.A); A.release(tb.QT);
-    A.release(tb.QM); A.release(tb.S); A.release(tb.flag); A.release(tb.Li); A.release(tb.Lj);
+    int hc5[2];
+    CK(cudaMemcpyAsync(hc5, c5c, sizeof(hc5), cudaMemcpyDeviceToHost, C.st));
+    CK(cudaStreamSynchronize(C.st));
+    const int n5l = hc5[0], n5h = hc5[1];
+    cudaStream_t side5 = nullptr;
+    if (n5h > 0) {
+      int32_t* hs = c5h;
+      if (n5h > 1) {
+        hs = A.alloc<int32_t>(n5h);
+        u64* hk = A.alloc<u64>(n5h);
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c5w, hk, c5h, hs, n5h, 0, 64, C.st));
+        void* t = A.alloc<char>(tb);
+        CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, c5w, hk, c5h, hs, n5h, 0, 64, C.st));
+        C.lib_launches += 4;
+      }
+      // heavy endpoints on a side stream, concurrent with the light ones
+      side5 = C.side();
+      CK(cudaEventRecord(C.ev_fork, C.st));
+      CK(cudaStreamWaitEvent(side5, C.ev_fork, 0));
+      size_t freeb = 0, totalb = 0;
+      CK(cudaMemGetInfo(&freeb, &totalb));
+      const int64_t per = (int64_t)n * (int64_t)(sizeof(C5Rec) + 8);
+      int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, n5h), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
+      C5Rec* dense = A.alloc_on<C5Rec>(side5, (size_t)hg * n, true);
+      int32_t* dl = A.alloc_on<int32_t>(side5, (size_t)hg * 2 * n);
+      k_c5_heavy<<<hg, C5_BT, 0, side5>>>(g, Tlow, Tmid, Thigh, hs, n5h, c5c + 2, dense, dl, Fp(F_C5));
+      C.launches++;
+      CK(cudaEventRecord(C.ev_join, side5));
+    }
+    if (n5l > 0) {
+      int bps = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_light, C5_BT, 0));
+      const int lg = std::max(1, std::min(bps, 4)) * SM;
+      const size_t nw = (size_t)lg * (C5_BT / 32);
+      C5Rec* reg = A.alloc<C5Rec>(nw * C5_WARP_CAP, true);
+      int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
+      k_c5_light<<<lg, C5_BT, 0, C.st>>>(g, Tlow, Tmid, Thigh, c5l, n5l, c5c + 3, reg, wl, Fp(F_C5));
+      C.launches++;
+    }
+    if (side5) CK(cudaStreamWaitEvent(C.st, C.ev_join, 0));
   }
 
   // ------------------------------------------------------------------ theta66 / theta70

@@ -75,11 +75,25 @@ struct PeelCtl {
   int minv;
   int level;
   int rounds;
+  int nalive;
 };
 
-__global__ void k_peel(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ adj,
-                       int32_t* __restrict__ deg, int32_t* __restrict__ rnd,
-                       int32_t* __restrict__ list0, int32_t* __restrict__ list1, PeelCtl* ctl) {
+#define PEEL_BT 1024           // threads per CTA
+#define PEEL_SWITCH 8192       // alive vertices at or below which one CTA finishes the peel
+
+// Rounds of the peel are identical in both phases: the frontier L[p] (alive vertices of
+// current degree <= k) gets rnd = round, their alive neighbours lose one degree each, and
+// a neighbour whose degree drops to exactly k joins the next frontier.  When a frontier is
+// empty the level rises to the minimum alive degree.  Phase 1 runs the rounds over the
+// whole grid (grid.sync between steps) while many vertices are alive; once at most
+// PEEL_SWITCH remain, they are compacted into a list and block 0 finishes alone with
+// block barriers (each late round touches few vertices, so a grid-wide barrier per round
+// would dominate).
+__global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __restrict__ rp,
+                                                  const int32_t* __restrict__ adj, int32_t* __restrict__ deg,
+                                                  int32_t* __restrict__ rnd, int32_t* __restrict__ list0,
+                                                  int32_t* __restrict__ list1, int32_t* __restrict__ alive0,
+                                                  int32_t* __restrict__ alive1, PeelCtl* ctl) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -87,12 +101,12 @@ __global__ void k_peel(int32_t n, const int64_t* __restrict__ rp, const int32_t*
   int32_t* lists[2] = {list0, list1};
   int k = 0, round = 0, p = 0, removed = 0;
   for (int32_t v = tid; v < n; v += nthreads) rnd[v] = -1;
-  if (tid == 0) { ctl->cnt[0] = 0; ctl->cnt[1] = 0; ctl->minv = 0x7fffffff; }
+  if (tid == 0) { ctl->cnt[0] = 0; ctl->cnt[1] = 0; ctl->minv = 0x7fffffff; ctl->nalive = 0; }
   grid.sync();
-  while (removed < n) {
+  // ---- phase 1: grid-wide rounds
+  while (n - removed > PEEL_SWITCH) {
     int cur = *(volatile int*)&ctl->cnt[p];
     if (cur == 0) {
-      // level up: minimum alive degree
       for (int32_t v = tid; v < n; v += nthreads)
         if (rnd[v] < 0) atomicMin(&ctl->minv, deg[v]);
       grid.sync();
@@ -123,7 +137,67 @@ __global__ void k_peel(int32_t n, const int64_t* __restrict__ rp, const int32_t*
     grid.sync();
     p ^= 1;
   }
-  if (tid == 0) { ctl->level = k; ctl->rounds = round; }
+  if (removed >= n) {
+    if (tid == 0) { ctl->level = k; ctl->rounds = round; }
+    return;
+  }
+  // compact the alive vertices (the pending frontier L[p] stays as it is)
+  for (int32_t v = tid; v < n; v += nthreads)
+    if (rnd[v] < 0) alive0[atomicAdd(&ctl->nalive, 1)] = v;
+  grid.sync();
+  if (blockIdx.x != 0) return;
+  // ---- phase 2: one CTA
+  __shared__ int s_cnt[2], s_minv, s_na;
+  int32_t* al[2] = {alive0, alive1};
+  int ap = 0;
+  int nalive = *(volatile int*)&ctl->nalive;
+  if (threadIdx.x == 0) { s_cnt[p] = *(volatile int*)&ctl->cnt[p]; s_cnt[p ^ 1] = 0; s_minv = 0x7fffffff; s_na = 0; }
+  __syncthreads();
+  const int bw = threadIdx.x >> 5, nbw = PEEL_BT / 32;
+  while (removed < n) {
+    int cur = s_cnt[p];
+    if (cur == 0) {
+      // level up: minimum alive degree, compacting the alive list on the way
+      for (int i = threadIdx.x; i < nalive; i += PEEL_BT) {
+        const int32_t v = al[ap][i];
+        if (rnd[v] < 0) {
+          atomicMin(&s_minv, deg[v]);
+          al[ap ^ 1][atomicAdd(&s_na, 1)] = v;
+        }
+      }
+      __syncthreads();
+      ap ^= 1;
+      nalive = s_na;
+      if (s_minv > k) k = s_minv;
+      for (int i = threadIdx.x; i < nalive; i += PEEL_BT) {
+        const int32_t v = al[ap][i];
+        if (deg[v] <= k) lists[p][atomicAdd(&s_cnt[p], 1)] = v;
+      }
+      __syncthreads();
+      cur = s_cnt[p];
+      __syncthreads();
+      if (threadIdx.x == 0) { s_minv = 0x7fffffff; s_na = 0; }
+    }
+    int32_t* L = lists[p];
+    for (int i = threadIdx.x; i < cur; i += PEEL_BT) rnd[L[i]] = round;
+    if (threadIdx.x == 0) s_cnt[p ^ 1] = 0;
+    __syncthreads();
+    for (int i = bw; i < cur; i += nbw) {
+      const int32_t v = L[i];
+      for (int64_t s = rp[v] + lane; s < rp[v + 1]; s += 32) {
+        const int32_t w = adj[s];
+        if (rnd[w] < 0) {
+          const int old = atomicSub(&deg[w], 1);
+          if (old == k + 1) lists[p ^ 1][atomicAdd(&s_cnt[p ^ 1], 1)] = w;
+        }
+      }
+    }
+    removed += cur;
+    round++;
+    __syncthreads();
+    p ^= 1;
+  }
+  if (threadIdx.x == 0) { ctl->level = k; ctl->rounds = round; }
 }
 
 // order keys: (round << 32) | id

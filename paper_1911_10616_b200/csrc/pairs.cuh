@@ -49,7 +49,8 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_MID_MAX 6144        // mid tier: est <= this (load <= 0.75)
 #define PAIR_WARP_CAP 1024       // light tier: per-warp packed hash entries (8 warps x 8 KB)
 #define PAIR_WARP_MAX 512        // light tier: est <= this
-#define PAIR_HBT 512             // heavy tier CTA
+#define PAIR_HBT 1024            // heavy tier CTA
+#define PAIR_SCAN_U 4            // 16-byte loads in flight per thread in the table sweep
 #define PAIR_LONG 64             // item part longer than this: chunked, shared queue
 #define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
 #define PAIR_LCAP 512            // long-part queue capacity per source pass
@@ -59,6 +60,8 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 // Packed variant (one u32 per key: W | D << 16).  Valid for sources with d(u) < 2^16
 // (W(u,x) <= d(u)) and T(u) < 2^16 (D(u,x) counts edges inside N(u)&N(x), at most T(u)).
 struct SharedPackedHash {
+  static constexpr bool kDense = false;
+  typedef u32 WordT;
   int32_t* keys;
   u32* val;
   u32 mask;
@@ -105,23 +108,37 @@ struct SharedPackedHash {
 template <typename Word, bool SCAN>
 struct GlobalDense {
   // SCAN: the entries are found afterwards by sweeping the whole table (used when the
-  // 2-hop set is a sizeable fraction of n), so updates are fire-and-forget reductions;
-  // otherwise the first update of an entry appends x to the touched list.
+  // 2-hop set is a sizeable fraction of n), so updates are fire-and-forget reductions.
+  // Otherwise the first update of an entry appends x to the touched list L (for the
+  // reset) and the update that makes W(u,x) = 2 appends x to L2, the pairs with W >= 2 --
+  // the only ones with a non-zero term (W = 1 implies D = 0 and zero contributions).
   // Reads go through L2 (__ldcg): the entries are updated by L2 atomics.
+  static constexpr bool kDense = true;
+  typedef Word WordT;
   Word* t;
   int32_t* L;
-  int* ntouch;  // shared counter
+  int32_t* L2;
+  int* ntouch;  // shared counters
+  int* n2;
   static constexpr int SH = (int)sizeof(Word) * 4;
   static constexpr Word LOW = (Word)(((u64)1 << SH) - 1);
-  __device__ __forceinline__ void upd(int32_t x, Word inc) {
+  __device__ __forceinline__ Word raw_add(int32_t x, Word inc) {
     if (SCAN) {
       atomicAdd(&t[x], inc);
-    } else {
-      if (atomicAdd(&t[x], inc) == 0) L[atomicAdd(ntouch, 1)] = x;
+      return (Word)0;
     }
+    return atomicAdd(&t[x], inc);
   }
-  __device__ __forceinline__ void add_w(int32_t x) { upd(x, (Word)1); }
-  __device__ __forceinline__ void add_d(int32_t x) { upd(x, (Word)((Word)1 << SH)); }
+  __device__ __forceinline__ void after_w(int32_t x, Word old) {
+    if (SCAN) return;
+    append_active(old == 0, x, L, ntouch);
+    append_active((old & LOW) == 1, x, L2, n2);
+  }
+  __device__ __forceinline__ void add_w(int32_t x) { after_w(x, raw_add(x, (Word)1)); }
+  __device__ __forceinline__ void add_d(int32_t x) {
+    const Word old = raw_add(x, (Word)((Word)1 << SH));
+    if (!SCAN) append_active(old == 0, x, L, ntouch);
+  }
   __device__ __forceinline__ void get(int32_t x, u64& wv, u64& dv) const {
     const Word v = __ldcg(&t[x]);
     wv = (u64)(v & LOW);
@@ -445,9 +462,18 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
             xs[i] = k < k1 ? g.ci[it.rb + k] : u;
           }
           if (PASS == 1) {
+            if constexpr (Tab::kDense) {
+              typename Tab::WordT olds[U];
 #pragma unroll
-            for (int i = 0; i < U; i++)
-              if (xs[i] != u) tab.add_w(xs[i]);
+              for (int i = 0; i < U; i++) olds[i] = xs[i] != u ? tab.raw_add(xs[i], 1) : 1;
+#pragma unroll
+              for (int i = 0; i < U; i++)
+                if (xs[i] != u) tab.after_w(xs[i], olds[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < U; i++)
+                if (xs[i] != u) tab.add_w(xs[i]);
+            }
           } else {
             u32 te[U];
             u64 wv[U], dv[U];
@@ -612,22 +638,26 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
   }
 }
 
-// Heavy tier: one CTA per source, dense per-CTA table (Word = u32 packed or u64).  With
-// SCAN the table is swept once at the end (terms of every non-zero entry, then cleared).
+// Heavy tier: one CTA per source, dense per-CTA table (Word = u32 packed or u64).  SCAN:
+// the table is swept once at the end (terms of every W >= 2 entry; every entry cleared).
 template <typename Word, bool SCAN>
 __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* __restrict__ Te,
                                                           const int32_t* __restrict__ srcs, int nsrc,
                                                           int* __restrict__ counter, Word* __restrict__ tabs,
                                                           int32_t* __restrict__ lists, PairOut o) {
+  typedef GlobalDense<Word, SCAN> Tab;
   __shared__ EngShared E;
   __shared__ u64 red[5];
-  __shared__ int s_idx, s_ntouch;
-  GlobalDense<Word, SCAN> tab;
-  tab.t = tabs + (size_t)blockIdx.x * g.n;
-  tab.L = SCAN ? nullptr : lists + (size_t)blockIdx.x * g.n;
+  __shared__ int s_idx, s_ntouch, s_n2;
+  Tab tab;
+  constexpr int PERV = 16 / (int)sizeof(Word);
+  tab.t = tabs + (size_t)blockIdx.x * (size_t)((g.n + PERV - 1) / PERV * PERV);  // 16-byte aligned rows
+  tab.L = SCAN ? nullptr : lists + (size_t)blockIdx.x * 2 * g.n;
+  tab.L2 = SCAN ? nullptr : tab.L + g.n;
   tab.ntouch = &s_ntouch;
+  tab.n2 = &s_n2;
   if (threadIdx.x < 5) red[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_ntouch = 0;
+  if (threadIdx.x == 0) { s_ntouch = 0; s_n2 = 0; }
   for (;;) {
     if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
     __syncthreads();
@@ -638,23 +668,35 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
     pair_source_cta<PAIR_HBT>(g, Te, u, tab, E, red, o,
         [&](auto f) {
           if (SCAN) {
-            // one coalesced sweep: terms of every entry, then clear it
-            for (int32_t x0 = threadIdx.x * 4; x0 < g.n; x0 += PAIR_HBT * 4) {
-              Word v[4];
+            // 16-byte loads, PAIR_SCAN_U of them in flight per thread (the sweep is
+            // latency-bound otherwise); the table rows are padded to a multiple of 16 B
+            constexpr int PER = 16 / (int)sizeof(Word);
+            const int32_t nvec = (g.n + PER - 1) / PER;
+            uint4* tv = reinterpret_cast<uint4*>(tab.t);
+            for (int32_t v0 = threadIdx.x; v0 < nvec; v0 += PAIR_HBT * PAIR_SCAN_U) {
+              uint4 q[PAIR_SCAN_U];
 #pragma unroll
-              for (int i = 0; i < 4; i++) v[i] = (x0 + i < g.n) ? __ldcg(&tab.t[x0 + i]) : (Word)0;
+              for (int i = 0; i < PAIR_SCAN_U; i++) {
+                const int32_t vi = v0 + i * PAIR_HBT;
+                q[i] = vi < nvec ? __ldcg(&tv[vi]) : make_uint4(0, 0, 0, 0);
+              }
 #pragma unroll
-              for (int i = 0; i < 4; i++)
-                if (v[i]) {
-                  const u64 w = (u64)(v[i] & GlobalDense<Word, SCAN>::LOW);
-                  if (w >= 2) f(x0 + i, w, (u64)(v[i] >> GlobalDense<Word, SCAN>::SH));
-                  tab.t[x0 + i] = (Word)0;
+              for (int i = 0; i < PAIR_SCAN_U; i++) {
+                if ((q[i].x | q[i].y | q[i].z | q[i].w) == 0) continue;
+                const int32_t vi = v0 + i * PAIR_HBT;
+                const Word* e = reinterpret_cast<const Word*>(&q[i]);
+#pragma unroll
+                for (int c = 0; c < PER; c++) {
+                  const u64 w = (u64)(e[c] & Tab::LOW);
+                  if (w >= 2) f(vi * PER + c, w, (u64)(e[c] >> Tab::SH));
                 }
+                tv[vi] = make_uint4(0, 0, 0, 0);
+              }
             }
           } else {
-            const int nt = s_ntouch;
-            for (int i = threadIdx.x; i < nt; i += PAIR_HBT) {
-              const int32_t x = tab.L[i];
+            const int n2 = s_n2;
+            for (int i = threadIdx.x; i < n2; i += PAIR_HBT) {
+              const int32_t x = tab.L2[i];
               u64 w, d;
               tab.get(x, w, d);
               f(x, w, d);
@@ -665,9 +707,10 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
           if (!SCAN) {
             __syncthreads();
             const int nt = s_ntouch;
+#pragma unroll 4
             for (int i = threadIdx.x; i < nt; i += PAIR_HBT) tab.t[tab.L[i]] = (Word)0;
             __syncthreads();
-            if (threadIdx.x == 0) s_ntouch = 0;
+            if (threadIdx.x == 0) { s_ntouch = 0; s_n2 = 0; }
           }
         });
   }

@@ -125,6 +125,19 @@ __device__ __forceinline__ u32 pow2_at_least(u32 x, u32 lo) {
   return c;
 }
 
+// Append x to list (counter in shared memory) with one atomic per group of active lanes.
+__device__ __forceinline__ void append_active(bool pred, int32_t x, int32_t* list, int* counter) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, pred);
+  if (!pred) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(m, base, leader);
+  list[base + __popc(m & ((1u << lane) - 1u))] = x;
+}
+
 // warp-aggregated append to a global list (one atomic per warp per call)
 __device__ __forceinline__ void warp_append(bool pred, int32_t val, int32_t* list, int* counter) {
   const u32 bal = __ballot_sync(FULL_MASK, pred);
@@ -135,4 +148,136 @@ __device__ __forceinline__ void warp_append(bool pred, int32_t val, int32_t* lis
   if (lane == leader) base = atomicAdd(counter, __popc(bal));
   base = __shfl_sync(FULL_MASK, base, leader);
   if (pred) list[base + __popc(bal & ((1u << lane) - 1u))] = val;
+}
+
+// ---------------------------------------------------------------------------------
+// Generic list engines.  Items i in [0, n_items); item i is the list [base, base + len)
+// (info(i, base, len) fills both); elem(i, base, k) visits element k of item i and
+// returns its contribution to the item's sum; flush(i, sum) receives non-zero partial
+// sums (several per item are possible: callers accumulate with atomics).
+// ---------------------------------------------------------------------------------
+#define LE_LONG 64      // item longer than this: queued and cut in chunks (CTA engine)
+#define LE_CHUNK 256    // elements per chunk (8 per lane)
+#define LE_QCAP 512     // queue capacity (overflowing items are walked by the sweep warp)
+
+// warp engine: the warp walks all items, 32 at a time, flattened over the lanes
+template <typename Info, typename Elem, typename Flush>
+__device__ __forceinline__ void warp_lists(int n_items, Info info, Elem elem, Flush flush) {
+  const int lane = threadIdx.x & 31;
+  for (int o0 = 0; o0 < n_items; o0 += 32) {
+    const int i = o0 + lane;
+    int64_t base = 0;
+    int len = 0;
+    if (i < n_items) info(i, base, len);
+    int cur = -1;
+    u64 acc = 0;
+    warp_flat(len, [&](int j, int k, bool valid) {
+      const int64_t bj = __shfl_sync(FULL_MASK, base, j);
+      if (!valid) return;
+      if (j != cur) {
+        if (cur >= 0 && acc) flush(o0 + cur, acc);
+        cur = j;
+        acc = 0;
+      }
+      acc += elem(o0 + j, bj, k);
+    });
+    if (cur >= 0 && acc) flush(o0 + cur, acc);
+  }
+}
+
+struct ListEng {
+  int next;
+  int qn;
+  int next_chunk;
+  int nchunks;
+  int32_t qi[LE_QCAP];
+  int32_t lc0[LE_QCAP + 1];
+};
+
+// CTA engine: warps take items (a few per grab when items are few, up to 32), walk
+// short ones with warp_flat and queue long ones; queued items are then cut into
+// LE_CHUNK-element chunks taken by whole warps.  Ends with a barrier.
+template <typename Info, typename Elem, typename Flush>
+__device__ void cta_lists(int n_items, ListEng& E, Info info, Elem elem, Flush flush) {
+  const int lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) { E.next = 0; E.qn = 0; E.next_chunk = 0; }
+  __syncthreads();
+  const int grab = max(1, min(32, (n_items + nw - 1) / nw));
+  for (;;) {
+    int b = 0;
+    if (lane == 0) b = atomicAdd(&E.next, grab);
+    b = __shfl_sync(FULL_MASK, b, 0);
+    if (b >= n_items) break;
+    const int i = b + lane;
+    int64_t base = 0;
+    int len = 0;
+    if (lane < grab && i < n_items) info(i, base, len);
+    if (len > LE_LONG) {
+      const int q = atomicAdd(&E.qn, 1);
+      if (q < LE_QCAP) { E.qi[q] = i; len = 0; }
+    }
+    int cur = -1;
+    u64 acc = 0;
+    warp_flat(len, [&](int j, int k, bool valid) {
+      const int64_t bj = __shfl_sync(FULL_MASK, base, j);
+      if (!valid) return;
+      if (j != cur) {
+        if (cur >= 0 && acc) flush(b + cur, acc);
+        cur = j;
+        acc = 0;
+      }
+      acc += elem(b + j, bj, k);
+    });
+    if (cur >= 0 && acc) flush(b + cur, acc);
+  }
+  __syncthreads();
+  const int nq = min(E.qn, LE_QCAP);
+  if (nq == 0) return;  // uniform
+  if (threadIdx.x < 32) {
+    int carry = 0;
+    for (int q0 = 0; q0 < nq; q0 += 32) {
+      const int q = q0 + lane;
+      int nc = 0;
+      if (q < nq) {
+        int64_t base;
+        int len;
+        info(E.qi[q], base, len);
+        nc = (len + LE_CHUNK - 1) / LE_CHUNK;
+      }
+      int incl = nc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, incl, d);
+        if (lane >= d) incl += y;
+      }
+      if (q < nq) E.lc0[q] = carry + incl - nc;
+      carry += __shfl_sync(FULL_MASK, incl, 31);
+    }
+    if (lane == 0) { E.lc0[nq] = carry; E.nchunks = carry; }
+  }
+  __syncthreads();
+  const int nchunks = E.nchunks;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&E.next_chunk, 1);
+    c = __shfl_sync(FULL_MASK, c, 0);
+    if (c >= nchunks) break;
+    int lo = 0, hi = nq;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (E.lc0[mid] <= c) lo = mid; else hi = mid;
+    }
+    const int i = E.qi[lo];
+    int64_t base;
+    int len;
+    info(i, base, len);
+    const int k0 = (c - E.lc0[lo]) * LE_CHUNK;
+    const int k1 = min(len, k0 + LE_CHUNK);
+    u64 acc = 0;
+    for (int k = k0 + lane; k < k1; k += 32) acc += elem(i, base, k);
+    acc = warp_sum(acc);
+    if (lane == 0 && acc) flush(i, acc);
+  }
+  __syncthreads();
 }
