@@ -34,6 +34,7 @@
 #pragma once
 #include "common.cuh"
 #include "sched.cuh"
+#include <cooperative_groups.h>
 
 struct __align__(16) C5Rec {
   int32_t key;   // hash regions: x + 1 (0 = empty); unused in dense tables
@@ -51,6 +52,8 @@ struct __align__(16) C5Rec {
 #define C5_BT 256
 #define C5_WARP_MAX 1024          // light endpoint: W(l) + d(l) <= this
 #define C5_WARP_CAP 2048          // records per warp region (load <= 0.5)
+#define C5_GIANT (1ull << 40)     // endpoint work above which the whole grid takes it (off)
+#define C5_HBT 1024               // heavy-endpoint CTA
 
 // dense records indexed by vertex id; touched list holds vertex ids
 struct C5Dense {
@@ -124,6 +127,27 @@ struct CtaEng {
   __device__ __forceinline__ int nthr() const { return blockDim.x; }
   template <typename I, typename E2, typename F>
   __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const { cta_lists(n, *E, info, elem, flush); }
+};
+
+// whole-grid engine for the giant endpoints (cooperative launch): warp per item
+struct GridEng {
+  __device__ __forceinline__ void sync() const { cooperative_groups::this_grid().sync(); }
+  __device__ __forceinline__ int tid() const { return (int)(blockIdx.x * blockDim.x + threadIdx.x); }
+  __device__ __forceinline__ int nthr() const { return (int)(gridDim.x * blockDim.x); }
+  template <typename I, typename E2, typename F>
+  __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const {
+    const int lane = threadIdx.x & 31;
+    const int gw = tid() >> 5, nw = nthr() >> 5;
+    for (int t = gw; t < n; t += nw) {
+      int64_t base;
+      int len;
+      info(t, base, len);
+      u64 acc = 0;
+      for (int k = lane; k < len; k += 32) acc += elem(t, base, k);
+      acc = warp_sum(acc);
+      if (lane == 0 && acc) flush(t, acc);
+    }
+  }
 };
 
 __device__ __forceinline__ bool c5_adj(const C5Rec* r) { return r && (r->flag & C5_ADJ); }
@@ -324,7 +348,7 @@ __global__ void k_c5_items(DGraph g, int shard_index, int num_shards, int32_t* _
 }
 
 // Heavy endpoints: one CTA each, dense records per CTA (persistent, W-sorted list).
-__global__ void __launch_bounds__(C5_BT) k_c5_heavy(DGraph g, const u32* __restrict__ Tlow,
+__global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __restrict__ Tlow,
                                                     const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                     const int32_t* __restrict__ heavy, int n_heavy,
                                                     int* __restrict__ counter, C5Rec* __restrict__ dense,
@@ -380,5 +404,61 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
     if (lane == 0 && w_tot[wib]) atomicAdd(&C5[l], w_tot[wib]);
     c5_reset(eng, loc);
     __syncwarp();
+  }
+}
+
+// Giant endpoints (W(l) > C5_GIANT): one at a time over the whole grid (cooperative
+// launch; grid barriers between the steps), so a hub endpoint is not bound to one SM.
+// ctl: [0] touched count, [1] J count; tot: u64 scratch.
+__global__ void __launch_bounds__(1024) k_c5_giant(DGraph g, const u32* __restrict__ Tlow,
+                                                   const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
+                                                   const int32_t* __restrict__ giant, int n_giant,
+                                                   C5Rec* __restrict__ dense, int32_t* __restrict__ dlists,
+                                                   int* __restrict__ ctl, u64* __restrict__ tot,
+                                                   u64* __restrict__ C5) {
+  GridEng eng;
+  C5Dense loc;
+  loc.R = dense;
+  loc.L = dlists;
+  loc.nL = &ctl[0];
+  int32_t* J = dlists + g.n;
+  for (int q = 0; q < n_giant; q++) {
+    const int32_t l = giant[q];
+    c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &ctl[1], tot, C5);  // ends with a grid barrier
+    c5_reset(eng, loc);
+    if (eng.tid() == 0 && *tot) atomicAdd(&C5[l], *tot);
+    eng.sync();
+    if (eng.tid() == 0) { ctl[0] = 0; ctl[1] = 0; *tot = 0; }
+    eng.sync();
+  }
+}
+
+// exact W(l) of the heavy endpoints (one warp each) and the number above C5_GIANT
+__global__ void k_c5_heavy_w(DGraph g, const int32_t* __restrict__ heavy, int n_heavy, u64* __restrict__ wout,
+                             int* __restrict__ n_giant) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = gw; q < n_heavy; q += nw) {
+    const int32_t l = heavy[q];
+    const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
+    u64 w = 0;
+    for (int64_t s = r0 + lane; s < r1; s += 32) {
+      const int32_t x = g.ci[s];
+      w += (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
+      if (s < rm) {
+        const int64_t ok = g.orow[x], ok1 = g.orow[x + 1];
+        w += (u64)(ok1 - ok);
+        for (int64_t e = ok; e < ok1; e++) {
+          const int32_t j = g.ocol[e];
+          w += (u64)(g.orow[j + 1] - g.orow[j]);
+        }
+      }
+    }
+    w = warp_sum(w) + (u64)g.deg[l];
+    if (lane == 0) {
+      wout[q] = w;
+      if (w > C5_GIANT) atomicAdd(n_giant, 1);
+    }
   }
 }

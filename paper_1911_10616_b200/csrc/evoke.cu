@@ -681,7 +681,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* c5l = A.alloc<int32_t>(n);
     int32_t* c5h = A.alloc<int32_t>(n);
     u64* c5w = A.alloc<u64>(n);
-    int* c5c = A.alloc<int>(4, true);
+    int* c5c = A.alloc<int>(8, true);
+    u64* C5out = Fp(F_C5);
     k_c5_items<<<warp_grid, B, 0, C.st>>>(g, si, ns, c5l, c5c, c5h, c5w, c5c + 1);
     C.launches++;
     int hc5[2];
@@ -690,6 +691,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     const int n5l = hc5[0], n5h = hc5[1];
     cudaStream_t side5 = nullptr;
     if (n5h > 0) {
+      // exact work of the heavy endpoints, sorted descending; the giant prefix goes to the
+      // whole grid (cooperative), the rest one CTA each on a side stream
+      k_c5_heavy_w<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, c5c + 2);
+      C.launches++;
       int32_t* hs = c5h;
       if (n5h > 1) {
         hs = A.alloc<int32_t>(n5h);
@@ -700,19 +705,37 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, c5w, hk, c5h, hs, n5h, 0, 64, C.st));
         C.lib_launches += 4;
       }
-      // heavy endpoints on a side stream, concurrent with the light ones
-      side5 = C.side();
-      CK(cudaEventRecord(C.ev_fork, C.st));
-      CK(cudaStreamWaitEvent(side5, C.ev_fork, 0));
+      int ngiant = 0;
+      CK(cudaMemcpyAsync(&ngiant, c5c + 2, sizeof(int), cudaMemcpyDeviceToHost, C.st));
+      CK(cudaStreamSynchronize(C.st));
       size_t freeb = 0, totalb = 0;
       CK(cudaMemGetInfo(&freeb, &totalb));
-      const int64_t per = (int64_t)n * (int64_t)(sizeof(C5Rec) + 8);
-      int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, n5h), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
-      C5Rec* dense = A.alloc_on<C5Rec>(side5, (size_t)hg * n, true);
-      int32_t* dl = A.alloc_on<int32_t>(side5, (size_t)hg * 2 * n);
-      k_c5_heavy<<<hg, C5_BT, 0, side5>>>(g, Tlow, Tmid, Thigh, hs, n5h, c5c + 2, dense, dl, Fp(F_C5));
-      C.launches++;
-      CK(cudaEventRecord(C.ev_join, side5));
+      if (ngiant > 0) {
+        C5Rec* dense = A.alloc<C5Rec>((size_t)n, true);
+        int32_t* dl = A.alloc<int32_t>((size_t)2 * n);
+        int* ctl = A.alloc<int>(2, true);
+        u64* tot = A.alloc<u64>(1, true);
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_giant, 1024, 0));
+        const int gg = std::max(1, std::min(bps, 2)) * SM;
+        void* args[] = {(void*)&g, (void*)&Tlow, (void*)&Tmid, (void*)&Thigh, (void*)&hs, (void*)&ngiant,
+                        (void*)&dense, (void*)&dl, (void*)&ctl, (void*)&tot, (void*)&C5out};
+        CK(cudaLaunchCooperativeKernel((void*)k_c5_giant, gg, 1024, args, 0, C.st));
+        C.launches++;
+      }
+      const int nrest = n5h - ngiant;
+      if (nrest > 0) {
+        side5 = C.side();
+        CK(cudaEventRecord(C.ev_fork, C.st));
+        CK(cudaStreamWaitEvent(side5, C.ev_fork, 0));
+        const int64_t per = (int64_t)n * (int64_t)(sizeof(C5Rec) + 8);
+        int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
+        C5Rec* dense = A.alloc_on<C5Rec>(side5, (size_t)hg * n, true);
+        int32_t* dl = A.alloc_on<int32_t>(side5, (size_t)hg * 2 * n);
+        k_c5_heavy<<<hg, C5_HBT, 0, side5>>>(g, Tlow, Tmid, Thigh, hs + ngiant, nrest, c5c + 3, dense, dl, Fp(F_C5));
+        C.launches++;
+        CK(cudaEventRecord(C.ev_join, side5));
+      }
     }
     if (n5l > 0) {
       int bps = 0;
@@ -721,7 +744,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const size_t nw = (size_t)lg * (C5_BT / 32);
       C5Rec* reg = A.alloc<C5Rec>(nw * C5_WARP_CAP, true);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
-      k_c5_light<<<lg, C5_BT, 0, C.st>>>(g, Tlow, Tmid, Thigh, c5l, n5l, c5c + 3, reg, wl, Fp(F_C5));
+      k_c5_light<<<lg, C5_BT, 0, C.st>>>(g, Tlow, Tmid, Thigh, c5l, n5l, c5c + 4, reg, wl, Fp(F_C5));
       C.launches++;
     }
     if (side5) CK(cudaStreamWaitEvent(C.st, C.ev_join, 0));
