@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -569,7 +570,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     u32* pest = A.alloc<u32>(n);
     int32_t* plists = A.alloc<int32_t>((size_t)PT_COUNT * n);
     int* tiers = A.alloc<int>(8, true);
-    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, pk, pv);
+    int32_t* hstar = A.alloc<int32_t>(n);
+    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, pk, pv, hstar);
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
     void* t = A.alloc<char>(tb);
@@ -581,7 +583,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaMemcpyAsync(ht, tiers, sizeof(ht), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     auto plist = [&](int tier) { return plists + (size_t)tier * n; };
-    PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e};
+    if (getenv("EVOKE_DEBUG"))
+      fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d light %d\n", ht[PT_G64], ht[PT_G32],
+              ht[PT_G32S], ht[PT_MID], ht[PT_LIGHT]);
+    PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e, hstar};
     cudaStream_t side = nullptr;
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
@@ -595,14 +600,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     };
     if (ht[PT_G64] > 0) {
       // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables, on a
-      // side stream concurrent with the other tiers
+      // side stream concurrent with the other tiers (scratch allocated on the main stream
+      // before the fork, so the pool reuses it without new mappings)
+      const int pg = heavy_grid(ht[PT_G64], 8, SM / 2);
+      u64* tabs = A.alloc<u64>((size_t)pg * (size_t)((n + 1) / 2 * 2), true);
+      int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
+      int* counter = A.alloc<int>(1, true);
       side = C.side();
       CK(cudaEventRecord(C.ev_fork, C.st));
       CK(cudaStreamWaitEvent(side, C.ev_fork, 0));
-      const int pg = heavy_grid(ht[PT_G64], 8, SM / 2);
-      u64* tabs = A.alloc_on<u64>(side, (size_t)pg * (size_t)((n + 1) / 2 * 2), true);
-      int32_t* lists = A.alloc_on<int32_t>(side, (size_t)pg * 2 * n);
-      int* counter = A.alloc_on<int>(side, 1, true);
       k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, side>>>(g, Te, plist(PT_G64), ht[PT_G64], counter, tabs, lists, po);
       C.launches++;
       CK(cudaEventRecord(C.ev_join, side));
@@ -611,7 +617,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       if (ht[tier] == 0) continue;
       const int pg = heavy_grid(ht[tier], 4, SM);
       u32* tabs = A.alloc<u32>((size_t)pg * (size_t)((n + 3) / 4 * 4), true);
-      int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * 2 * n) : nullptr;
+      int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * n) : nullptr;
       int* counter = A.alloc<int>(1, true);
       if (tier == PT_G32S)
         k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(tier), ht[tier], counter, tabs, lists, po);
@@ -647,6 +653,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     const int n_light = hc[0], n_heavy = hc[1];
+    if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] hub items: light %d heavy %d\n", n_light, n_heavy);
     int32_t* heavy_sorted = heavy;
     if (n_heavy > 1) {
       int32_t* hs = A.alloc<int32_t>(n_heavy);
@@ -689,6 +696,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaMemcpyAsync(hc5, c5c, sizeof(hc5), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     const int n5l = hc5[0], n5h = hc5[1];
+    if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d heavy %d\n", n5l, n5h);
     cudaStream_t side5 = nullptr;
     if (n5h > 0) {
       // exact work of the heavy endpoints, sorted descending; the giant prefix goes to the
@@ -725,13 +733,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       }
       const int nrest = n5h - ngiant;
       if (nrest > 0) {
+        const int64_t per = (int64_t)n * (int64_t)(sizeof(C5Rec) + 8);
+        int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
+        C5Rec* dense = A.alloc<C5Rec>((size_t)hg * n, true);
+        int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
         side5 = C.side();
         CK(cudaEventRecord(C.ev_fork, C.st));
         CK(cudaStreamWaitEvent(side5, C.ev_fork, 0));
-        const int64_t per = (int64_t)n * (int64_t)(sizeof(C5Rec) + 8);
-        int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
-        C5Rec* dense = A.alloc_on<C5Rec>(side5, (size_t)hg * n, true);
-        int32_t* dl = A.alloc_on<int32_t>(side5, (size_t)hg * 2 * n);
         k_c5_heavy<<<hg, C5_HBT, 0, side5>>>(g, Tlow, Tmid, Thigh, hs + ngiant, nrest, c5c + 3, dense, dl, Fp(F_C5));
         C.launches++;
         CK(cudaEventRecord(C.ev_join, side5));

@@ -35,6 +35,7 @@
 
 struct PairOut {
   u64 *R8, *R36, *R50, *R51, *R63, *R49, *R62, *R64, *C4e;
+  const int32_t* hstar;  // per source: its heaviest neighbour h* (wedges through h* are not walked)
 };
 
 __device__ __forceinline__ int64_t slot_of_lo_in_hi(const DGraph& g, int32_t e) { return g.eslot_hi[e]; }
@@ -50,7 +51,7 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_WARP_CAP 1024       // light tier: per-warp packed hash entries (8 warps x 8 KB)
 #define PAIR_WARP_MAX 512        // light tier: est <= this
 #define PAIR_HBT 1024            // heavy tier CTA
-#define PAIR_SCAN_U 4            // 16-byte loads in flight per thread in the table sweep
+
 #define PAIR_LONG 64             // item part longer than this: chunked, shared queue
 #define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
 #define PAIR_LCAP 512            // long-part queue capacity per source pass
@@ -101,44 +102,61 @@ struct SharedPackedHash {
       h = (h + 1) & mask;
     }
   }
+  __device__ __forceinline__ u32* word_if(int32_t x) const {
+    u32 h = h0(x);
+    for (;;) {
+      const int32_t k = keys[h];
+      if (k == x) return &val[h];
+      if (k == EMPTY_KEY) return nullptr;
+      h = (h + 1) & mask;
+    }
+  }
+  __device__ __forceinline__ static u64 wfield(u32 v) { return (u64)(v & 0xffffu); }
+  __device__ __forceinline__ static u64 dfield(u32 v) { return (u64)(v >> 16); }
+  template <typename F>
+  __device__ __forceinline__ void for_each_mut(int tid, int nthr, F f) {
+    for (u32 h = tid; h <= mask; h += nthr) {
+      const int32_t x = keys[h];
+      if (x == EMPTY_KEY) continue;
+      const u32 v = val[h];
+      const u64 w = f(x, (u64)(v & 0xffffu), (u64)(v >> 16));
+      if (w != (u64)(v & 0xffffu)) val[h] = (v & 0xffff0000u) | (u32)w;
+    }
+  }
+  __device__ __forceinline__ void reset(int tid, int nthr) {
+    for (u32 h = tid; h <= mask; h += nthr) { keys[h] = EMPTY_KEY; val[h] = 0u; }
+  }
 };
 
 // Dense per-CTA table in global memory indexed by x; W in the low half of the word,
 // D in the high half; touched list for the entry sweep and the reset.
 template <typename Word, bool SCAN>
 struct GlobalDense {
-  // SCAN: the entries are found afterwards by sweeping the whole table (used when the
-  // 2-hop set is a sizeable fraction of n), so updates are fire-and-forget reductions.
-  // Otherwise the first update of an entry appends x to the touched list L (for the
-  // reset) and the update that makes W(u,x) = 2 appends x to L2, the pairs with W >= 2 --
-  // the only ones with a non-zero term (W = 1 implies D = 0 and zero contributions).
+  // SCAN (2-hop set a sizeable part of n): updates are fire-and-forget reductions and the
+  // entries are found by sweeping the whole table (16-byte loads).  Otherwise the first
+  // update of an entry appends x to the touched list L (entry sweep, reset).
   // Reads go through L2 (__ldcg): the entries are updated by L2 atomics.
   static constexpr bool kDense = true;
   typedef Word WordT;
   Word* t;
   int32_t* L;
-  int32_t* L2;
-  int* ntouch;  // shared counters
-  int* n2;
+  int* ntouch;  // shared counter
+  int32_t n;
   static constexpr int SH = (int)sizeof(Word) * 4;
   static constexpr Word LOW = (Word)(((u64)1 << SH) - 1);
+  static constexpr int PER = 16 / (int)sizeof(Word);
   __device__ __forceinline__ Word raw_add(int32_t x, Word inc) {
     if (SCAN) {
       atomicAdd(&t[x], inc);
-      return (Word)0;
+      return (Word)1;
     }
     return atomicAdd(&t[x], inc);
   }
   __device__ __forceinline__ void after_w(int32_t x, Word old) {
-    if (SCAN) return;
-    append_active(old == 0, x, L, ntouch);
-    append_active((old & LOW) == 1, x, L2, n2);
-  }
-  __device__ __forceinline__ void add_w(int32_t x) { after_w(x, raw_add(x, (Word)1)); }
-  __device__ __forceinline__ void add_d(int32_t x) {
-    const Word old = raw_add(x, (Word)((Word)1 << SH));
     if (!SCAN) append_active(old == 0, x, L, ntouch);
   }
+  __device__ __forceinline__ void add_w(int32_t x) { after_w(x, raw_add(x, (Word)1)); }
+  __device__ __forceinline__ void add_d(int32_t x) { after_w(x, raw_add(x, (Word)((Word)1 << SH))); }
   __device__ __forceinline__ void get(int32_t x, u64& wv, u64& dv) const {
     const Word v = __ldcg(&t[x]);
     wv = (u64)(v & LOW);
@@ -146,6 +164,69 @@ struct GlobalDense {
   }
   __device__ __forceinline__ u64 get_w(int32_t x) const { return (u64)(__ldcg(&t[x]) & LOW); }
   __device__ __forceinline__ u64 get_w_or0(int32_t x) const { return (u64)(__ldcg(&t[x]) & LOW); }
+  // entry word of x if x has an entry, else nullptr (single-writer update by the caller)
+  __device__ __forceinline__ Word* word_if(int32_t x) const {
+    Word* p = &t[x];
+    return __ldcg(p) != 0 ? p : nullptr;
+  }
+  __device__ __forceinline__ static u64 wfield(Word v) { return (u64)(v & LOW); }
+  __device__ __forceinline__ static u64 dfield(Word v) { return (u64)(v >> SH); }
+  // f(x, w, d) -> new w, for every entry (strided over `nthr` threads from `tid`)
+  template <typename F>
+  __device__ __forceinline__ void for_each_mut(int tid, int nthr, F f) {
+    if (SCAN) {
+      const int32_t nvec = (n + PER - 1) / PER;
+      const uint4* tv = reinterpret_cast<const uint4*>(t);
+      for (int32_t v0 = tid; v0 < nvec; v0 += nthr * 4) {
+        uint4 q[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int32_t vi = v0 + i * nthr;
+          q[i] = vi < nvec ? __ldcg(&tv[vi]) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          if ((q[i].x | q[i].y | q[i].z | q[i].w) == 0) continue;
+          const int32_t vi = v0 + i * nthr;
+          const Word* e = reinterpret_cast<const Word*>(&q[i]);
+#pragma unroll
+          for (int c = 0; c < PER; c++) {
+            if (e[c] == 0) continue;
+            const u64 w = f(vi * PER + c, (u64)(e[c] & LOW), (u64)(e[c] >> SH));
+            if (w != (u64)(e[c] & LOW)) t[vi * PER + c] = (Word)((e[c] & ~LOW) | (Word)w);
+          }
+        }
+      }
+      return;
+    }
+    const int nt = *ntouch;
+    for (int i = tid; i < nt; i += nthr) {
+      const int32_t x = L[i];
+      const Word v = __ldcg(&t[x]);
+      const u64 w = f(x, (u64)(v & LOW), (u64)(v >> SH));
+      if (w != (u64)(v & LOW)) t[x] = (Word)((v & ~LOW) | (Word)w);
+    }
+  }
+  __device__ __forceinline__ void reset(int tid, int nthr) {
+    if (SCAN) {
+      const int32_t nvec = (n + PER - 1) / PER;
+      uint4* tv = reinterpret_cast<uint4*>(t);
+      for (int32_t v0 = tid; v0 < nvec; v0 += nthr * 4) {
+        uint4 q[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int32_t vi = v0 + i * nthr;
+          q[i] = vi < nvec ? __ldcg(&tv[vi]) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if ((q[i].x | q[i].y | q[i].z | q[i].w) != 0) tv[v0 + i * nthr] = make_uint4(0, 0, 0, 0);
+      }
+      return;
+    }
+    const int nt = *ntouch;
+    for (int i = tid; i < nt; i += nthr) t[L[i]] = (Word)0;
+  }
 };
 
 // phase C contributions of one (x, W, D) pair
@@ -172,12 +253,14 @@ struct PairItem {
   bool vlo;         // v is the lower endpoint of e
 };
 
-__device__ __forceinline__ PairItem pair_item(const DGraph& g, int64_t s_uv) {
+// the wedge part of item h* is empty: W(u,x) gets the h* contribution from a membership
+// test over the table keys instead (see entry_terms)
+__device__ __forceinline__ PairItem pair_item(const DGraph& g, int64_t s_uv, int32_t hs) {
   PairItem it;
   it.v = g.ci[s_uv];
   it.e = g.eid[s_uv];
   it.rb = g.rp[it.v];
-  it.dv = (int32_t)(g.rp[it.v + 1] - it.rb);
+  it.dv = it.v == hs ? 0 : (int32_t)(g.rp[it.v + 1] - it.rb);
   it.fo = g.foff[it.e];
   it.tv = (int32_t)(g.foff[it.e + 1] - it.fo);
   it.vlo = g.esrc[it.e] == it.v;
@@ -248,13 +331,13 @@ __device__ __forceinline__ void chord_elem(const DGraph& g, int32_t u, int32_t v
 // ---- warp engine: the warp runs one pass over items s_uv in [r0, r1) --------------------
 // Every part (wedges, chords) of 32 items at a time is flattened over the lanes.
 template <int PASS, typename Tab>
-__device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int64_t r0,
-                                          int64_t r1, Tab& tab, u64& s51, const PairOut& o) {
+__device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
+                                          int64_t r0, int64_t r1, Tab& tab, u64& s51, const PairOut& o) {
   const int lane = threadIdx.x & 31;
   for (int64_t o0 = r0; o0 < r1; o0 += 32) {
     PairItem it;
     const bool have = o0 + lane < r1;
-    if (have) it = pair_item(g, o0 + lane);
+    if (have) it = pair_item(g, o0 + lane, hs);
     else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
     PairAcc A;
     A.zero();
@@ -324,20 +407,20 @@ struct CtaEnq {
   }
 };
 
-__device__ __forceinline__ int part_len(const DGraph& g, const EngShared& E, int q) {
+__device__ __forceinline__ int part_len(const DGraph& g, const EngShared& E, int q, int32_t hs) {
   const int kind = E.qkind[q];
   if (kind == PK_DIAM) {
     const int64_t r = E.qslot[q];
     const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
     return (int)(g.foff[evw + 1] - g.foff[evw]);
   }
-  const PairItem it = pair_item(g, E.qslot[q]);
+  const PairItem it = pair_item(g, E.qslot[q], hs);
   return kind == PK_WEDGE ? it.dv : it.tv;
 }
 
 template <int PASS, typename Tab>
-__device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int64_t r0, int64_t r1, Tab& tab,
-                         EngShared& E, u64& s51, const PairOut& o) {
+__device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs, int64_t r0, int64_t r1,
+                         Tab& tab, EngShared& E, u64& s51, const PairOut& o) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) { E.next = 0; E.qn = 0; }
   __syncthreads();
@@ -354,7 +437,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     if (base >= nitems) break;
     PairItem it;
     const bool have = lane < grab && base + lane < nitems;
-    if (have) it = pair_item(g, r0 + base + lane);
+    if (have) it = pair_item(g, r0 + base + lane, hs);
     else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
     // defer long parts to the queue (if it has room)
     if (it.dv > PAIR_LONG) {
@@ -408,7 +491,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       int carry = 0;
       for (int q0 = qb; q0 < qe; q0 += 32) {
         const int q = q0 + lane;
-        const int nc = (q < qe) ? (part_len(g, E, q) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
+        const int nc = (q < qe) ? (part_len(g, E, q, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
         int incl = nc;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -448,7 +531,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
         fv = E.qv[q];
         fe = -1;  // no C4e credit from diamond parts (A.c5 stays 0)
       } else {
-        const PairItem it = pair_item(g, E.qslot[q]);
+        const PairItem it = pair_item(g, E.qslot[q], hs);
         fv = it.v;
         fe = it.e;
         if (kind == PK_WEDGE) {
@@ -514,23 +597,105 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
   }
 }
 
+// ---- the h* contribution ----------------------------------------------------------------
+// After pass 1 the table holds W_R(u,x), the common neighbours other than h*.  Then
+// W(u,x) = W_R + [x in N(h*)] for every key, and keys absent from the table have W <= 1 and
+// contribute nothing, so the wedges u - h* - x are never inserted.  Two ways to add the
+// h* term, chosen per source by cost: walk N(h*) and look every x up in the table
+// (hstar_walk, cost d(h*)), or binary-search every key in the sorted N(h*) (hstar_search,
+// cost #keys * log d(h*)).  Both also emit the terms of the wedges u - h* - x with W >= 2
+// (E5 of e(u,h*), theta49/62 of h*, theta51 of u) into H / s51.
+template <typename Tab>
+__device__ __forceinline__ void hstar_walk(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
+                                           const Tab& tab, int tid, int nthr, PairAcc& H, u64& s51) {
+  const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
+  for (int64_t p = hb + tid; p < he; p += nthr) {
+    const int32_t x = g.ci[p];
+    if (x == u) continue;
+    auto* wp = tab.word_if(x);
+    if (!wp) continue;
+    const auto v = *wp + 1;  // x is visited once: plain update
+    *wp = v;
+    const u64 w = Tab::wfield(v), d = Tab::dfield(v);
+    H.c5 += w - 1;
+    s51 += (u64)Te[g.eid[p]] * (w - 1);
+    if (x > u) {
+      H.c49 += binom2(w - 1);
+      H.c62 += d;
+    }
+  }
+}
+
+template <typename Tab>
+__device__ __forceinline__ void hstar_search(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
+                                             Tab& tab, int tid, int nthr, PairAcc& H, u64& s51) {
+  const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
+  tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
+    const int64_t p = lower_bound_dev<int32_t>(g.ci, hb, he, x);
+    if (p < he && g.ci[p] == x) {
+      w += 1;
+      H.c5 += w - 1;
+      s51 += (u64)Te[g.eid[p]] * (w - 1);
+      if (x > u) {
+        H.c49 += binom2(w - 1);
+        H.c62 += d;
+      }
+    }
+    return w;
+  });
+}
+
+// per-pair terms over the final table (keys with W >= 2)
+template <typename Tab>
+__device__ __forceinline__ void entry_terms(const DGraph& g, Tab& tab, int tid, int nthr, u64& a8, u64& a36,
+                                            u64& a50, u64& a63) {
+  tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
+    pair_c_terms(g, x, w, d, a8, a36, a50, a63);
+    return w;
+  });
+}
+
+// walk N(h*) when that is cheaper than searching every key in it
+__device__ __forceinline__ bool hstar_prefer_walk(const DGraph& g, int32_t hs, u64 nkeys_bound) {
+  const u64 dh = (u64)dg_deg(g, hs);
+  return dh <= 12ull * nkeys_bound;
+}
+
+// slot of h* in N(u) -> edge id e(u, h*)
+__device__ __forceinline__ int32_t edge_of(const DGraph& g, int32_t u, int32_t v) {
+  const int64_t p = lower_bound_dev<int32_t>(g.ci, g.rp[u], g.rp[u + 1], v);
+  return g.eid[p];
+}
+
 // ---- one source on a CTA (mid and heavy tiers) ------------------------------------------
-// Tab provides add_w/add_d/get/get_w/get_w_or0; for_entries(f) runs f(x, W, D) for every
-// table entry (strided over the CTA), reset() clears the table (CTA-wide).
-template <int BT, typename Tab, typename ForEntries, typename Reset>
+template <int BT, typename Tab>
 __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int32_t u, Tab& tab, EngShared& E,
-                                u64* red, const PairOut& o, ForEntries for_entries, Reset reset) {
+                                u64* red, const PairOut& o, u32 tab_keys_bound) {
   const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
+  const int32_t hs = o.hstar[u];
   u64 s51 = 0;
-  cta_pass<1>(g, Te, u, r0, r1, tab, E, s51, o);
-  cta_pass<2>(g, Te, u, r0, r1, tab, E, s51, o);
+  cta_pass<1>(g, Te, u, hs, r0, r1, tab, E, s51, o);
+  u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
+  PairAcc H;
+  H.zero();
+  if (hs >= 0) {
+    if (Tab::kDense || hstar_prefer_walk(g, hs, (u64)(tab_keys_bound))) hstar_walk(g, Te, u, hs, tab, threadIdx.x, BT, H, s51);
+    else hstar_search(g, Te, u, hs, tab, threadIdx.x, BT, H, s51);
+  }
+  H.c5 = warp_sum(H.c5); H.c49 = warp_sum(H.c49); H.c62 = warp_sum(H.c62);
+  if ((threadIdx.x & 31) == 0) {
+    if (H.c5) atomicAdd(&red[5], H.c5);
+    if (H.c49) atomicAdd(&red[6], H.c49);
+    if (H.c62) atomicAdd(&red[7], H.c62);
+  }
+  __syncthreads();
+  entry_terms(g, tab, threadIdx.x, BT, a8, a36, a50, a63);
+  __syncthreads();  // W final
+  cta_pass<2>(g, Te, u, hs, r0, r1, tab, E, s51, o);
   for (int64_t s = r0 + threadIdx.x; s < r1; s += BT) {
     const u64 w = tab.get_w_or0(g.ci[s]);
     s51 -= w * (w - 1);
   }
-  __syncthreads();  // for_entries may clear the table
-  u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
-  for_entries([&](int32_t x, u64 w, u64 d) { pair_c_terms(g, x, w, d, a8, a36, a50, a63); });
   a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
   if ((threadIdx.x & 31) == 0) {
     if (a8) atomicAdd(&red[0], a8);
@@ -542,9 +707,13 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   __syncthreads();
   if (threadIdx.x == 0) {
     o.R8[u] += red[0]; o.R36[u] += red[1]; o.R50[u] += red[2]; o.R51[u] += red[3]; o.R63[u] += red[4];
-    for (int i = 0; i < 5; i++) red[i] = 0;
+    if (hs >= 0) {
+      H.c5 = red[5]; H.c49 = red[6]; H.c62 = red[7]; H.c64 = 0;
+      H.flush(u, hs, edge_of(g, u, hs), o);
+    }
+    for (int i = 0; i < 8; i++) red[i] = 0;
   }
-  reset();
+  tab.reset(threadIdx.x, BT);
   __syncthreads();
 }
 
@@ -553,30 +722,38 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
                                  SharedPackedHash& tab, const PairOut& o) {
   const int lane = threadIdx.x & 31;
   const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
+  const int32_t hs = o.hstar[u];
   tab.mask = cap - 1;
   u64 s51 = 0;
-  warp_pass<1>(g, Te, u, r0, r1, tab, s51, o);
+  warp_pass<1>(g, Te, u, hs, r0, r1, tab, s51, o);
   __syncwarp();
-  warp_pass<2>(g, Te, u, r0, r1, tab, s51, o);
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
-  for (u32 h = lane; h < cap; h += 32) {
-    const int32_t x = tab.keys[h];
-    if (x != EMPTY_KEY) pair_c_terms(g, x, tab.val[h] & 0xffffu, tab.val[h] >> 16, a8, a36, a50, a63);
+  PairAcc H;
+  H.zero();
+  if (hs >= 0) {
+    if (hstar_prefer_walk(g, hs, cap / 2)) hstar_walk(g, Te, u, hs, tab, lane, 32, H, s51);
+    else hstar_search(g, Te, u, hs, tab, lane, 32, H, s51);
   }
+  __syncwarp();
+  entry_terms(g, tab, lane, 32, a8, a36, a50, a63);
+  __syncwarp();
+  warp_pass<2>(g, Te, u, hs, r0, r1, tab, s51, o);
   for (int64_t s = r0 + lane; s < r1; s += 32) {
     const u64 w = tab.get_w_or0(g.ci[s]);
     s51 -= w * (w - 1);
   }
   a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
+  H.c5 = warp_sum(H.c5); H.c49 = warp_sum(H.c49); H.c62 = warp_sum(H.c62);
   if (lane == 0) {
     if (a8) atomicAdd(&o.R8[u], a8);
     if (a36) atomicAdd(&o.R36[u], a36);
     if (a50) atomicAdd(&o.R50[u], a50);
     if (s51) atomicAdd(&o.R51[u], s51);
     if (a63) atomicAdd(&o.R63[u], a63);
+    if (hs >= 0) H.flush(u, hs, edge_of(g, u, hs), o);
   }
   __syncwarp();
-  for (u32 h = lane; h < cap; h += 32) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
+  tab.reset(lane, 32);
   __syncwarp();
 }
 
@@ -589,13 +766,14 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
                                                         PairOut o) {
   extern __shared__ int32_t sh_pairs[];
   __shared__ EngShared E;
-  __shared__ u64 red[5];
+  __shared__ u64 red[8];
   __shared__ int s_idx;
-  if (threadIdx.x < 5) red[threadIdx.x] = 0;
+  if (threadIdx.x < 8) red[threadIdx.x] = 0;
   {
     SharedPackedHash tab;
     tab.keys = sh_pairs;
     tab.val = (u32*)(sh_pairs + PAIR_MID_CAP);
+    for (u32 h = threadIdx.x; h < PAIR_MID_CAP; h += PAIR_BT) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
     for (;;) {
       if (threadIdx.x == 0) s_idx = atomicAdd(&counters[0], 1);
       __syncthreads();
@@ -603,21 +781,12 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
       __syncthreads();
       if (idx >= n_mid) break;
       const int32_t u = mid[idx];
-      const u32 cap = min(pow2_at_least(2u * est[u], 64u), (u32)PAIR_MID_CAP);
-      tab.mask = cap - 1;
-      for (u32 h = threadIdx.x; h < cap; h += PAIR_BT) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
-      __syncthreads();
-      pair_source_cta<PAIR_BT>(g, Te, u, tab, E, red, o,
-          [&](auto f) {
-            for (u32 h = threadIdx.x; h < cap; h += PAIR_BT) {
-              const int32_t x = tab.keys[h];
-              if (x != EMPTY_KEY) f(x, (u64)(tab.val[h] & 0xffffu), (u64)(tab.val[h] >> 16));
-            }
-          },
-          [&]() {});
+      tab.mask = min(pow2_at_least(2u * est[u], 64u), (u32)PAIR_MID_CAP) - 1;
+      pair_source_cta<PAIR_BT>(g, Te, u, tab, E, red, o, est[u]);  // leaves the table clean
     }
   }
   // light tier: per-warp packed hash in the dynamic shared memory
+  __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   SharedPackedHash tab;
   tab.keys = sh_pairs + wib * (2 * PAIR_WARP_CAP);
@@ -638,101 +807,70 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
   }
 }
 
-// Heavy tier: one CTA per source, dense per-CTA table (Word = u32 packed or u64).  SCAN:
-// the table is swept once at the end (terms of every W >= 2 entry; every entry cleared).
+// Heavy tier: one CTA per source, dense per-CTA table in global memory (Word = u32
+// packed W|D<<16, or u64 W|D<<32 for sources past the 16-bit bounds).
 template <typename Word, bool SCAN>
 __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* __restrict__ Te,
                                                           const int32_t* __restrict__ srcs, int nsrc,
                                                           int* __restrict__ counter, Word* __restrict__ tabs,
                                                           int32_t* __restrict__ lists, PairOut o) {
-  typedef GlobalDense<Word, SCAN> Tab;
   __shared__ EngShared E;
-  __shared__ u64 red[5];
-  __shared__ int s_idx, s_ntouch, s_n2;
-  Tab tab;
-  constexpr int PERV = 16 / (int)sizeof(Word);
-  tab.t = tabs + (size_t)blockIdx.x * (size_t)((g.n + PERV - 1) / PERV * PERV);  // 16-byte aligned rows
-  tab.L = SCAN ? nullptr : lists + (size_t)blockIdx.x * 2 * g.n;
-  tab.L2 = SCAN ? nullptr : tab.L + g.n;
+  __shared__ u64 red[8];
+  __shared__ int s_idx, s_ntouch;
+  GlobalDense<Word, SCAN> tab;
+  constexpr int PER = GlobalDense<Word, SCAN>::PER;
+  const size_t stride = (size_t)((g.n + PER - 1) / PER * PER);  // 16-byte aligned rows
+  tab.t = tabs + (size_t)blockIdx.x * stride;
+  tab.L = SCAN ? nullptr : lists + (size_t)blockIdx.x * g.n;
   tab.ntouch = &s_ntouch;
-  tab.n2 = &s_n2;
-  if (threadIdx.x < 5) red[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { s_ntouch = 0; s_n2 = 0; }
+  tab.n = g.n;
+  if (threadIdx.x < 8) red[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_ntouch = 0;
   for (;;) {
     if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
     __syncthreads();
     const int idx = s_idx;
     __syncthreads();
     if (idx >= nsrc) break;
-    const int32_t u = srcs[idx];
-    pair_source_cta<PAIR_HBT>(g, Te, u, tab, E, red, o,
-        [&](auto f) {
-          if (SCAN) {
-            // 16-byte loads, PAIR_SCAN_U of them in flight per thread (the sweep is
-            // latency-bound otherwise); the table rows are padded to a multiple of 16 B
-            constexpr int PER = 16 / (int)sizeof(Word);
-            const int32_t nvec = (g.n + PER - 1) / PER;
-            uint4* tv = reinterpret_cast<uint4*>(tab.t);
-            for (int32_t v0 = threadIdx.x; v0 < nvec; v0 += PAIR_HBT * PAIR_SCAN_U) {
-              uint4 q[PAIR_SCAN_U];
-#pragma unroll
-              for (int i = 0; i < PAIR_SCAN_U; i++) {
-                const int32_t vi = v0 + i * PAIR_HBT;
-                q[i] = vi < nvec ? __ldcg(&tv[vi]) : make_uint4(0, 0, 0, 0);
-              }
-#pragma unroll
-              for (int i = 0; i < PAIR_SCAN_U; i++) {
-                if ((q[i].x | q[i].y | q[i].z | q[i].w) == 0) continue;
-                const int32_t vi = v0 + i * PAIR_HBT;
-                const Word* e = reinterpret_cast<const Word*>(&q[i]);
-#pragma unroll
-                for (int c = 0; c < PER; c++) {
-                  const u64 w = (u64)(e[c] & Tab::LOW);
-                  if (w >= 2) f(vi * PER + c, w, (u64)(e[c] >> Tab::SH));
-                }
-                tv[vi] = make_uint4(0, 0, 0, 0);
-              }
-            }
-          } else {
-            const int n2 = s_n2;
-            for (int i = threadIdx.x; i < n2; i += PAIR_HBT) {
-              const int32_t x = tab.L2[i];
-              u64 w, d;
-              tab.get(x, w, d);
-              f(x, w, d);
-            }
-          }
-        },
-        [&]() {
-          if (!SCAN) {
-            __syncthreads();
-            const int nt = s_ntouch;
-#pragma unroll 4
-            for (int i = threadIdx.x; i < nt; i += PAIR_HBT) tab.t[tab.L[i]] = (Word)0;
-            __syncthreads();
-            if (threadIdx.x == 0) { s_ntouch = 0; s_n2 = 0; }
-          }
-        });
+    pair_source_cta<PAIR_HBT>(g, Te, srcs[idx], tab, E, red, o, 0u);
+    if (threadIdx.x == 0) s_ntouch = 0;
   }
 }
 
-// 2-hop estimate: est(u) = sum_{v in N(u)} d(v) - d(u) >= #distinct x at distance <= 2
-__global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict__ vals) {
+// 2-hop estimate without the heaviest neighbour h*: est(u) = sum_{v in N(u), v != h*} d(v)
+// - d(u) + 1 = the number of wedge elements walked (>= the number of table keys).
+__global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict__ vals,
+                           int32_t* __restrict__ hstar) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t ui = gw; ui < g.n; ui += nw) {
     const int32_t u = (int32_t)ui;
     u64 s = 0;
-    for (int64_t t = g.rp[u] + lane; t < g.rp[u + 1]; t += 32) s += (u64)dg_deg(g, g.ci[t]);
+    int32_t best = -1, bestd = -1;
+    for (int64_t t = g.rp[u] + lane; t < g.rp[u + 1]; t += 32) {
+      const int32_t v = g.ci[t];
+      const int32_t dv = dg_deg(g, v);
+      s += (u64)dv;
+      if (dv > bestd) { bestd = dv; best = v; }
+    }
     s = warp_sum(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int32_t od = __shfl_xor_sync(FULL_MASK, bestd, o);
+      const int32_t ob = __shfl_xor_sync(FULL_MASK, best, o);
+      if (od > bestd || (od == bestd && ob < best)) { bestd = od; best = ob; }
+    }
     if (lane == 0) {
-      const u64 est = s - (u64)dg_deg(g, u);
+      const u64 du = (u64)dg_deg(g, u);
+      const u64 est = du > 0 ? s - (u64)bestd - du + 1 : 0;
       keys[u] = ~est;  // ascending sort = descending estimate
       vals[u] = u;
+      hstar[u] = best;
     }
   }
 }
+
 
 // Shard filter of the est-sorted (descending) vertex list and tier classification.
 // Lists keep the descending order approximately (warp-aggregated appends in list order).

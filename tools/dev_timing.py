@@ -1,0 +1,29 @@
+"""Per-pass timings of repeated calls (median of K) on one config: python tools/dev_timing.py CFG K"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import graphgen
+import paper_1911_10616_b200 as pkg
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+k = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+g = graphgen.config(cfg)
+dev = torch.device("cuda:0")
+edges = torch.from_numpy(g.edges).to(dev)
+out = torch.empty((g.n, 73), dtype=torch.int64, device=dev)
+rows = []
+for i in range(k + 2):
+    _, st = pkg.evoke_orbits_edges(g.n, edges, out=out, return_stats=True)
+    torch.cuda.synchronize()
+    if i >= 2:
+        rows.append(st["ms_pass"])
+keys = list(rows[0].keys())
+med = {kk: float(np.median([r[kk] for r in rows])) for kk in keys}
+mn = {kk: float(np.min([r[kk] for r in rows])) for kk in keys}
+print(f"config {cfg}: total median {sum(med.values()):.3f} ms")
+for kk in keys:
+    print(f"  {kk:14s} median {med[kk]:8.3f}  min {mn[kk]:8.3f}  all {[round(r[kk], 2) for r in rows]}")
