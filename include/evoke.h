@@ -61,7 +61,8 @@ typedef struct evoke_stats {
    * the pass must visit x bytes each visit must touch; 0 = not modelled */
   double alg_bytes[16];
   int64_t units[8];             /* sum d^2, sum T(e)^2, hub visits, c5 wedge visits,
-                                   c5 out-out visits, triangle-pass stream, -, -      */
+                                   c5 out-out + path visits, triangle-pass stream,
+                                   pair wedges walked (without h*), sum d(h*)         */
 } evoke_stats;
 
 #define EVOKE_FLAG_WORKMODEL 1  /* fill evoke_stats.alg_bytes / units (extra kernels)  */

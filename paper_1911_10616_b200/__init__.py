@@ -128,7 +128,7 @@ def _stats_dict(s: _Stats) -> dict:
             "ms_pass": {names[i]: s.ms_pass[i] for i in range(min(s.num_passes, len(names)))},
             "alg_bytes": {names[i]: s.alg_bytes[i] for i in range(min(s.num_passes, len(names)))},
             "units": {k: s.units[i] for i, k in enumerate(("sum_d2", "sum_te2", "hub", "c5_wedge", "c5_q",
-                                                           "tri_stream"))},
+                                                           "tri_stream", "pair_rwedge", "pair_hwalk"))},
             "kernel_launches": s.kernel_launches, "library_launches": s.library_launches}
 
 

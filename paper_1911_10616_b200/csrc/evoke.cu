@@ -808,17 +808,19 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     s->wedges = (int64_t)d2h_scalar<u64>(dw, C.st);
     if ((o.flags & EVOKE_FLAG_WORKMODEL) && n > 0) {
       WorkUnits* du = A.alloc<WorkUnits>(1, true);
-      k_units_vertex<<<grid_for(n, B, SM), B, 0, C.st>>>(g, du);
+      k_units_vertex<<<grid_for((int64_t)n * 32, B, SM), B, 0, C.st>>>(g, du);
       if (m > 0) k_units_edge<<<grid_for(m, B, SM), B, 0, C.st>>>(g, Te, du);
       if (ntri > 0) k_units_hub<<<grid_for(m2, B, SM), B, 0, C.st>>>(g, Te, du);
       WorkUnits hu = d2h_scalar<WorkUnits>(du, C.st);
       s->units[0] = (int64_t)hu.sum_d2; s->units[1] = (int64_t)hu.sum_te2; s->units[2] = (int64_t)hu.hub;
       s->units[3] = (int64_t)hu.c5_wedge; s->units[4] = (int64_t)hu.c5_q; s->units[5] = (int64_t)hu.tri_stream;
-      // bytes per unit: DESIGN.md section 8(d)
+      s->units[6] = (int64_t)hu.pair_rwedge; s->units[7] = (int64_t)hu.pair_hwalk;
+      // algorithmic bytes per pass = units x the bytes of graph data each unit must read
+      // (DESIGN.md section 5.2); per-source / per-endpoint tables are on-chip or L2 scratch
       s->alg_bytes[P_TRI] = 8.0 * (double)hu.tri_stream + 16.0 * (double)ntri;
-      s->alg_bytes[P_PAIR] = 32.0 * (double)hu.sum_d2 + 28.0 * (double)hu.sum_te2;
+      s->alg_bytes[P_PAIR] = 16.0 * (double)hu.pair_rwedge + 8.0 * (double)hu.pair_hwalk + 12.0 * (double)hu.sum_te2;
       s->alg_bytes[P_HUB] = 28.0 * (double)hu.hub;
-      s->alg_bytes[P_C5] = 40.0 * (double)hu.c5_wedge + 84.0 * (double)hu.c5_q;
+      s->alg_bytes[P_C5] = 12.0 * (double)hu.c5_wedge + 12.0 * (double)hu.c5_q;
       s->alg_bytes[P_TRIG] = 16.0 * (double)ntri + 3.0 * 14.0 * 16.0 * (double)ntri;
     }
   }

@@ -6,27 +6,60 @@
 #include "common.cuh"
 
 struct WorkUnits {
-  u64 sum_d2;        // sum_v d(v)^2           : pair phases A and D (wedge visits)
-  u64 sum_te2;       // sum_e T(e)^2           : pair phase B (x1), phase E (x2)
+  u64 sum_d2;        // sum_v d(v)^2           : all wedges (context: what a plain pair pass walks)
+  u64 sum_te2;       // sum_e T(e)^2           : pair diamonds (pass 1 x1, pass 2 x2)
   u64 hub;           // hub-local inner visits : sum over (v,a) of sum_{b<a in tri(v,a)} T(v,b)
-  u64 c5_wedge;      // cycles5 steps 1 and 6  : sum_w d(w) d+(w) + d-(w) d+(w)
-  u64 c5_q;          // cycles5 steps 2 and 4  : sum_k d+(k)^2
+  u64 c5_wedge;      // cycles5 steps 1 and 6  : w1 = sum_l sum_{w in N(l)} |Nsel(w)|
+  u64 c5_q;          // cycles5 steps 2/4 and 3: w2 + w3 (see cycles5.cuh)
   u64 tri_stream;    // triangle pass          : sum_{e=(a,b)} d+(b)
+  u64 pair_rwedge;   // pair wedges walked     : sum_u sum_{v in N(u), v != h*(u)} (d(v) - 1)
+  u64 pair_hwalk;    // h* term                : sum_u d(h*(u))
 };
 
+// warp per vertex u (as a pair source and as a 5-cycle endpoint l = u)
 __global__ void k_units_vertex(DGraph g, WorkUnits* out) {
-  u64 d2 = 0, c5w = 0, c5q = 0;
-  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
-    const u64 d = dg_deg(g, v), dp = dg_dplus(g, v), dmi = d - dp;
-    d2 += d * d;
-    c5w += d * dp + dmi * dp;
-    c5q += dp * dp;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  u64 d2 = 0, rw = 0, hw = 0, w1 = 0, w23 = 0;
+  for (int64_t ui = gw; ui < g.n; ui += nw) {
+    const int32_t u = (int32_t)ui;
+    const int64_t r0 = g.rp[u], r1 = g.rp[u + 1], rm = r0 + g.dm[u];
+    u64 s = 0, a1 = 0, a23 = 0;
+    int32_t dmax = 0;
+    for (int64_t t = r0 + lane; t < r1; t += 32) {
+      const int32_t v = g.ci[t];
+      const int32_t dv = dg_deg(g, v);
+      s += (u64)dv;
+      dmax = max(dmax, dv);
+      a1 += (u64)((v < u) ? dv : dv - g.dm[v]);
+      if (t < rm) {
+        const int64_t ok = g.orow[v], ok1 = g.orow[v + 1];
+        a23 += (u64)(ok1 - ok);
+        for (int64_t e = ok; e < ok1; e++) {
+          const int32_t j = g.ocol[e];
+          a23 += (u64)(g.orow[j + 1] - g.orow[j]);
+        }
+      }
+    }
+    s = warp_sum(s); a1 = warp_sum(a1); a23 = warp_sum(a23);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(FULL_MASK, dmax, o));
+    if (lane == 0) {
+      const u64 du = (u64)dg_deg(g, u);
+      d2 += du * du;
+      if (du > 0) rw += s - (u64)dmax - (du - 1);
+      hw += (u64)dmax;
+      w1 += a1;
+      w23 += a23;
+    }
   }
-  d2 = warp_sum(d2); c5w = warp_sum(c5w); c5q = warp_sum(c5q);
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     atomicAdd(&out->sum_d2, d2);
-    atomicAdd(&out->c5_wedge, c5w);
-    atomicAdd(&out->c5_q, c5q);
+    atomicAdd(&out->pair_rwedge, rw);
+    atomicAdd(&out->pair_hwalk, hw);
+    atomicAdd(&out->c5_wedge, w1);
+    atomicAdd(&out->c5_q, w23);
   }
 }
 
