@@ -13,7 +13,7 @@ struct WorkUnits {
   u64 c5_q;          // cycles5 steps 2/4 and 3: w2 + w3 (see cycles5.cuh)
   u64 tri_stream;    // triangle pass          : sum_{e=(a,b)} d+(b)
   u64 pair_rwedge;   // pair wedges walked     : sum_u sum_{v in N(u), v != h*(u)} (d(v) - 1)
-  u64 pair_hwalk;    // h* term                : sum_u d(h*(u))
+  u64 pair_hwalk;    // h* term                : sum_u min(d(h*(u)), pair wedges of u)
 };
 
 // warp per vertex u (as a pair source and as a 5-cycle endpoint l = u)
@@ -48,8 +48,9 @@ __global__ void k_units_vertex(DGraph g, WorkUnits* out) {
     if (lane == 0) {
       const u64 du = (u64)dg_deg(g, u);
       d2 += du * du;
-      if (du > 0) rw += s - (u64)dmax - (du - 1);
-      hw += (u64)dmax;
+      const u64 r = du > 0 ? s - (u64)dmax - (du - 1) : 0;
+      rw += r;
+      hw += min((u64)dmax, r);  // h* term: a walk of N(h*) or a search per key, counted as the smaller
       w1 += a1;
       w23 += a23;
     }
