@@ -6,6 +6,9 @@
 
 #include <chrono>
 #include <cstdlib>
+#include <algorithm>
+#include <functional>
+#include <utility>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -108,7 +111,23 @@ struct Ctx {
   cudaEvent_t ev[P_COUNT + 1];
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t side_st = nullptr;
+  static const int MAXJOBS = 16;
+  cudaStream_t jst[MAXJOBS] = {};
+  cudaEvent_t pev[MAXJOBS][2] = {};
+  int njobs = 0;
+  int job_pass[MAXJOBS] = {};
   bool timing;
+  // stream i with priority from rank (rank 0 = the device's greatest priority)
+  cudaStream_t stream(size_t i, int rank) {
+    if (i >= (size_t)MAXJOBS) { set_error("too many concurrent jobs"); throw EvokeError{EVOKE_EINTERNAL}; }
+    if (!jst[i]) {
+      int lo = 0, hi = 0;  // lo = least priority (numerically greatest), hi = greatest
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const int prio = std::min(lo, hi + rank);
+      CK(cudaStreamCreateWithPriority(&jst[i], cudaStreamNonBlocking, prio));
+    }
+    return jst[i];
+  }
   cudaStream_t side() {
     if (!side_st) CK(cudaStreamCreateWithFlags(&side_st, cudaStreamNonBlocking));
     return side_st;
@@ -237,12 +256,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   for (int i = 0; i <= P_COUNT; i++) CK(cudaEventCreate(&C.ev[i]));
   CK(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
+  for (int i = 0; i < Ctx::MAXJOBS; i++)
+    for (int j = 0; j < 2; j++) CK(cudaEventCreate(&C.pev[i][j]));
   struct Cleanup {
     Ctx& C; cudaStream_t own;
     ~Cleanup() {
       for (int i = 0; i <= P_COUNT; i++) cudaEventDestroy(C.ev[i]);
       cudaEventDestroy(C.ev_fork);
       cudaEventDestroy(C.ev_join);
+      for (int i = 0; i < Ctx::MAXJOBS; i++) {
+        for (int j = 0; j < 2; j++) cudaEventDestroy(C.pev[i][j]);
+        if (C.jst[i]) { cudaStreamSynchronize(C.jst[i]); cudaStreamDestroy(C.jst[i]); }
+      }
       if (C.side_st) { cudaStreamSynchronize(C.side_st); cudaStreamDestroy(C.side_st); }
       if (own) { cudaStreamSynchronize(own); cudaStreamDestroy(own); }
     }
@@ -526,7 +551,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       cscratch = A.alloc<u32>((size_t)cscratch_words * cscratch_grid);
     }
   }
-  auto launch_cliques = [&](int mode) {
+  auto launch_cliques = [&](int mode, cudaStream_t lst) {
     for (int b = 0; b < 5; b++) {
       if (hcounts[b] == 0) continue;
       const int kmax = b < 4 ? bin_k[b] : 0;
@@ -538,20 +563,20 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       if (mode == 0) {
         if (smem > 48 * 1024)
           CK(cudaFuncSetAttribute(k_cliques<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_cliques<0><<<grid, block, smem, C.st>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
+        k_cliques<0><<<grid, block, smem, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
                                                  cscratch_words, 1, si, ns, Te, K4t, Fp(F_K4), K4e, Fp(F_K5),
                                                  nullptr, nullptr);
       } else {
         if (smem > 48 * 1024)
           CK(cudaFuncSetAttribute(k_cliques<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_cliques<1><<<grid, block, smem, C.st>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
+        k_cliques<1><<<grid, block, smem, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
                                                  cscratch_words, 0, si, ns, Te, K4t, nullptr, nullptr, nullptr,
                                                  Fp(F_R66), Fp(F_R70));
       }
       C.launches++;
     }
   };
-  if (ntri > 0) launch_cliques(0);
+  if (ntri > 0) launch_cliques(0, C.st);
 
   EdgeVals ev{Te, E9f, E9b, K4e, C4e, E7, K4t};
   // ------------------------------------------------------------------ nbr gather 1
@@ -559,7 +584,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   const int warp_grid = grid_for((int64_t)n * 32, B, SM);
   if (n > 0) { k_nbr1<<<warp_grid, B, 0, C.st>>>(g, ev, F); C.launches++; }
 
-  // ------------------------------------------------------------------ a7: pair pass
+  // ------------------------------------------------------------------ a7, a8, a10, theta66/70
+  // The four passes are independent (disjoint outputs; inputs from a1-a6).  Their
+  // preparations (work estimates, sorts, tier counts: host syncs) run first on the main
+  // stream; then each pass's persistent kernels are launched on a stream of its own so the
+  // passes overlap (the GPU analogue of the paper's concurrent orbit groups).
+  struct Job { int pass; int rank; std::function<void(cudaStream_t)> fn; };
+  std::vector<Job> jobs;  // rank: launch order / stream priority (long single-item tails first)
   C.mark(P_PAIR);
   if (n > 0 && m > 0) {
     // source lists by 2-hop estimate (descending), sharded by position, split in tiers
@@ -586,8 +617,23 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (getenv("EVOKE_DEBUG"))
       fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d light %d\n", ht[PT_G64], ht[PT_G32],
               ht[PT_G32S], ht[PT_MID], ht[PT_LIGHT]);
-    PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e, hstar};
-    cudaStream_t side = nullptr;
+    // position maps of the hubs (h* membership in one load), within a memory budget
+    int32_t* hslot = A.alloc<int32_t>(n);
+    int* hcnt = A.alloc<int>(1, true);
+    const int max_maps = (int)std::min<int64_t>(4096, std::max<int64_t>(0, (256ll << 20) / ((int64_t)n * 4)));
+    k_hub_slots<<<grid_for(n, B, SM), B, 0, C.st>>>(g, max_maps, hslot, hcnt);
+    int nmaps = 0;
+    CK(cudaMemcpyAsync(&nmaps, hcnt, sizeof(int), cudaMemcpyDeviceToHost, C.st));
+    CK(cudaStreamSynchronize(C.st));
+    nmaps = std::min(nmaps, max_maps);
+    int32_t* hpos = A.alloc<int32_t>((size_t)std::max(nmaps, 1) * n);
+    if (nmaps > 0) {
+      CK(cudaMemsetAsync(hpos, 0xff, sizeof(int32_t) * (size_t)nmaps * n, C.st));
+      k_hub_maps<<<std::min(nmaps * 4, 4 * SM), 256, 0, C.st>>>(g, hslot, hpos);
+    }
+    C.launches += 2;
+    PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e, hstar,
+               hslot, hpos};
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
@@ -599,19 +645,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       return (int)pg;
     };
     if (ht[PT_G64] > 0) {
-      // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables, on a
-      // side stream concurrent with the other tiers (scratch allocated on the main stream
-      // before the fork, so the pool reuses it without new mappings)
+      // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables
       const int pg = heavy_grid(ht[PT_G64], 8, SM / 2);
       u64* tabs = A.alloc<u64>((size_t)pg * (size_t)((n + 1) / 2 * 2), true);
       int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
       int* counter = A.alloc<int>(1, true);
-      side = C.side();
-      CK(cudaEventRecord(C.ev_fork, C.st));
-      CK(cudaStreamWaitEvent(side, C.ev_fork, 0));
-      k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, side>>>(g, Te, plist(PT_G64), ht[PT_G64], counter, tabs, lists, po);
-      C.launches++;
-      CK(cudaEventRecord(C.ev_join, side));
+      const int32_t* pl = plist(PT_G64);
+      const int cnt = ht[PT_G64];
+      jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
+        k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po);
+        C.launches++;
+      }});
     }
     for (int tier : {PT_G32S, PT_G32}) {
       if (ht[tier] == 0) continue;
@@ -619,24 +663,30 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       u32* tabs = A.alloc<u32>((size_t)pg * (size_t)((n + 3) / 4 * 4), true);
       int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * n) : nullptr;
       int* counter = A.alloc<int>(1, true);
-      if (tier == PT_G32S)
-        k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(tier), ht[tier], counter, tabs, lists, po);
-      else
-        k_pairs_heavy<u32, false><<<pg, PAIR_HBT, 0, C.st>>>(g, Te, plist(tier), ht[tier], counter, tabs, lists, po);
-      C.launches++;
+      const int32_t* pl = plist(tier);
+      const int cnt = ht[tier];
+      jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
+        if (tier == PT_G32S)
+          k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po);
+        else
+          k_pairs_heavy<u32, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po);
+        C.launches++;
+      }});
     }
     if (ht[PT_MID] + ht[PT_LIGHT] > 0) {
       CK(cudaFuncSetAttribute(k_pairs_main, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM));
       int bps = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_pairs_main, PAIR_BT, PAIR_SMEM));
       int* counters = A.alloc<int>(2, true);
-      k_pairs_main<<<std::max(bps, 1) * SM, PAIR_BT, PAIR_SMEM, C.st>>>(g, Te, plist(PT_MID), ht[PT_MID],
-                                                                       plist(PT_LIGHT), ht[PT_LIGHT], pest,
-                                                                       counters, po);
-      C.launches++;
+      const int32_t* pm = plist(PT_MID);
+      const int32_t* pli = plist(PT_LIGHT);
+      const int nmid = ht[PT_MID], nli = ht[PT_LIGHT];
+      const int grid = std::max(bps, 1) * SM;
+      jobs.push_back({P_PAIR, 3, [=, &C](cudaStream_t st) {
+        k_pairs_main<<<grid, PAIR_BT, PAIR_SMEM, st>>>(g, Te, pm, nmid, pli, nli, pest, counters, po);
+        C.launches++;
+      }});
     }
-    if (side) CK(cudaStreamWaitEvent(C.st, C.ev_join, 0));
-    A.release(pk); A.release(pk2); A.release(pv); A.release(pv2); A.release(t);
   }
 
   // ------------------------------------------------------------------ a8: hub-local
@@ -676,9 +726,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         gt = A.alloc<u32>((size_t)hg * g.max_deg, true);
         gl = A.alloc<int32_t>((size_t)hg * g.max_deg);
       }
-      k_hub_process<<<hg, HUB_BT, HUB_SMEM, C.st>>>(g, Te, heavy_sorted, n_heavy, light, n_light, hcnt + 2, gt, gl,
-                                                      Fp(F_R68), Fp(F_R69));
-      C.launches++;
+      u64* r68 = Fp(F_R68);
+      u64* r69 = Fp(F_R69);
+      jobs.push_back({P_HUB, 2, [=, &C](cudaStream_t st) {
+        k_hub_process<<<hg, HUB_BT, HUB_SMEM, st>>>(g, Te, heavy_sorted, n_heavy, light, n_light, hcnt + 2, gt, gl,
+                                                    r68, r69);
+        C.launches++;
+      }});
     }
   }
 
@@ -697,7 +751,6 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaStreamSynchronize(C.st));
     const int n5l = hc5[0], n5h = hc5[1];
     if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d heavy %d\n", n5l, n5h);
-    cudaStream_t side5 = nullptr;
     if (n5h > 0) {
       // exact work of the heavy endpoints, sorted descending; the giant prefix goes to the
       // whole grid (cooperative), the rest one CTA each on a side stream
@@ -737,12 +790,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
         C5Rec* dense = A.alloc<C5Rec>((size_t)hg * n, true);
         int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
-        side5 = C.side();
-        CK(cudaEventRecord(C.ev_fork, C.st));
-        CK(cudaStreamWaitEvent(side5, C.ev_fork, 0));
-        k_c5_heavy<<<hg, C5_HBT, 0, side5>>>(g, Tlow, Tmid, Thigh, hs + ngiant, nrest, c5c + 3, dense, dl, Fp(F_C5));
-        C.launches++;
-        CK(cudaEventRecord(C.ev_join, side5));
+        const int32_t* hsr = hs + ngiant;
+        jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
+          k_c5_heavy<<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3, dense, dl, C5out);
+          C.launches++;
+        }});
       }
     }
     if (n5l > 0) {
@@ -752,15 +804,32 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const size_t nw = (size_t)lg * (C5_BT / 32);
       C5Rec* reg = A.alloc<C5Rec>(nw * C5_WARP_CAP, true);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
-      k_c5_light<<<lg, C5_BT, 0, C.st>>>(g, Tlow, Tmid, Thigh, c5l, n5l, c5c + 4, reg, wl, Fp(F_C5));
-      C.launches++;
+      jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
+        k_c5_light<<<lg, C5_BT, 0, st>>>(g, Tlow, Tmid, Thigh, c5l, n5l, c5c + 4, reg, wl, C5out);
+        C.launches++;
+      }});
     }
-    if (side5) CK(cudaStreamWaitEvent(C.st, C.ev_join, 0));
   }
 
   // ------------------------------------------------------------------ theta66 / theta70
+  if (ntri > 0) jobs.push_back({P_CLIQ2, 5, [&](cudaStream_t st) { launch_cliques(1, st); }});
+
+  // ------------------------------------------------------------------ concurrent launch
   C.mark(P_CLIQ2);
-  if (ntri > 0) launch_cliques(1);
+  // one stream per job (jobs of one pass stay in order on a shared stream when they must:
+  // the heavy and main pair kernels write different sources, so all jobs are independent)
+  std::stable_sort(jobs.begin(), jobs.end(), [](const Job& x, const Job& y) { return x.rank < y.rank; });
+  CK(cudaEventRecord(C.ev_fork, C.st));
+  for (size_t i = 0; i < jobs.size(); i++) {
+    cudaStream_t st = C.stream(i, jobs[i].rank);
+    CK(cudaStreamWaitEvent(st, C.ev_fork, 0));
+    CK(cudaEventRecord(C.pev[i][0], st));
+    jobs[i].fn(st);
+    CK(cudaEventRecord(C.pev[i][1], st));
+  }
+  for (size_t i = 0; i < jobs.size(); i++) CK(cudaStreamWaitEvent(C.st, C.pev[i][1], 0));
+  C.njobs = (int)jobs.size();
+  for (size_t i = 0; i < jobs.size(); i++) C.job_pass[i] = jobs[i].pass;
 
   // ------------------------------------------------------------------ nbr gathers 2,3
   C.mark(P_NBR2);
@@ -797,6 +866,22 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, C.ev[i], C.ev[i + 1]));
       s->ms_pass[i] = ms;
+    }
+    // the pair, hub-local, 5-cycle and theta66/70 kernels run concurrently: each of these
+    // passes reports its preparation (main stream) plus the span of its own kernels; the
+    // overlap makes the per-pass times add up to more than ms_total
+    s->ms_pass[P_CLIQ2] = 0;
+    for (int pass : {P_PAIR, P_HUB, P_C5, P_CLIQ2}) {
+      float lo = 1e30f, hi = -1e30f;
+      for (int j = 0; j < C.njobs; j++) {
+        if (C.job_pass[j] != pass) continue;
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, C.ev[0], C.pev[j][0]));
+        CK(cudaEventElapsedTime(&b, C.ev[0], C.pev[j][1]));
+        lo = std::min(lo, a);
+        hi = std::max(hi, b);
+      }
+      if (hi > lo) s->ms_pass[pass] += hi - lo;
     }
     float tot = 0;
     CK(cudaEventElapsedTime(&tot, C.ev[0], C.ev[P_COUNT]));

@@ -35,7 +35,9 @@
 
 struct PairOut {
   u64 *R8, *R36, *R50, *R51, *R63, *R49, *R62, *R64, *C4e;
-  const int32_t* hstar;  // per source: its heaviest neighbour h* (wedges through h* are not walked)
+  const int32_t* hstar;     // per source: its heaviest neighbour h* (wedges through h* are not walked)
+  const int32_t* hub_slot;  // per vertex: row of its position map, or -1
+  const int32_t* hub_pos;   // [slot][x]: position of x in N(hub) (offset), or -1
 };
 
 __device__ __forceinline__ int64_t slot_of_lo_in_hi(const DGraph& g, int32_t e) { return g.eslot_hi[e]; }
@@ -55,7 +57,8 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_LONG 64             // item part longer than this: chunked, shared queue
 #define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
 #define PAIR_LCAP 512            // long-part queue capacity per source pass
-#define PAIR_DIAM_INLINE 32      // diamond list longer than this: queued (CTA engine)
+#define PAIR_ILP 4               // independent wedge chains per lane in the pass-2 walk
+#define PAIR_HUBMAP_MIN 1024     // vertices of degree >= this get a position map (budgeted)
 #define EMPTY_KEY (-1)
 
 // Packed variant (one u32 per key: W | D << 16).  Valid for sources with d(u) < 2^16
@@ -302,37 +305,120 @@ __device__ __forceinline__ void pass2_wedge(const DGraph& g, const u32* __restri
   }
 }
 
-// Chord element k of item v: w = k-th third vertex of e(u,v); the diamonds behind it are
-// the entries x of tri(v, w).  A long diamond list may be handed to enq(r, v, vlo) (the
-// CTA engine queues it for chunked processing); otherwise it is walked here.
-struct NoEnq {
-  __device__ __forceinline__ bool operator()(int64_t, int32_t, bool) const { return false; }
-};
+// Chords and diamonds, flattened on two levels.  Every lane brings at most one chord
+// (v, w): the k-th third vertex of e(u,v) (PASS 1 keeps w > v only: D(u,x) counts each
+// chord once); the diamond lists tri(v,w) of the (up to 32) chords of the warp are then
+// flattened over the lanes with a second warp_flat.  PASS 2 adds W(u,x)-2 (x > u) into
+// acc[owner] (per-warp shared accumulators, one per item owner).  Warp-uniform call.
 template <int PASS, typename Tab>
-__device__ __forceinline__ void diamond_elem(const DGraph& g, int32_t u, int64_t r2, Tab& tab, PairAcc& A) {
-  const int32_t x = g.fx[r2];
-  if (PASS == 1) {
-    if (x != u) tab.add_d(x);
-  } else {
-    if (x > u) A.c64 += tab.get_w(x) - 2ull;
+__device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool valid, int32_t v, int64_t fo, bool vlo,
+                                            int k, int owner, Tab& tab, u64* acc) {
+  int64_t f0 = 0;
+  int len2 = 0;
+  if (valid) {
+    const int64_t r = fo + k;
+    if (!(PASS == 1 && g.fx[r] <= v)) {
+      const int32_t evw = vlo ? g.fe1[r] : g.fe2[r];
+      f0 = g.foff[evw];
+      len2 = (int)(g.foff[evw + 1] - f0);
+    }
   }
+  int cur = -1;
+  u64 c = 0;
+  warp_flat(len2, [&](int j2, int k2, bool v2) {
+    const int64_t f0j = __shfl_sync(FULL_MASK, f0, j2);
+    const int own = __shfl_sync(FULL_MASK, owner, j2);
+    if (!v2) return;
+    const int32_t x = g.fx[f0j + k2];
+    if (PASS == 1) {
+      if (x != u) tab.add_d(x);
+    } else {
+      if (own != cur) {
+        if (cur >= 0 && c) atomicAdd(&acc[cur], c);
+        cur = own;
+        c = 0;
+      }
+      if (x > u) c += tab.get_w(x) - 2ull;
+    }
+  });
+  if (PASS == 2 && cur >= 0 && c) atomicAdd(&acc[cur], c);
 }
-template <int PASS, typename Tab, typename Enq>
-__device__ __forceinline__ void chord_elem(const DGraph& g, int32_t u, int32_t v, int64_t fo, bool vlo, int k,
-                                           Tab& tab, PairAcc& A, Enq& enq) {
-  const int64_t r = fo + k;
-  if (PASS == 1 && g.fx[r] <= v) return;  // D(u,x): each chord (v<w) once
-  const int32_t evw = vlo ? g.fe1[r] : g.fe2[r];
-  const int64_t f0 = g.foff[evw], f1 = g.foff[evw + 1];
-  if (f1 - f0 > PAIR_DIAM_INLINE && enq(r, v, vlo)) return;
-  for (int64_t r2 = f0; r2 < f1; r2++) diamond_elem<PASS>(g, u, r2, tab, A);
+
+// Pass-2 wedge walk of up to 32 items (lane's item: list [rb, rb+len), vertex v, edge e),
+// flattened like warp_flat but PAIR_ILP steps at a time with every load of a step issued
+// before the dependent ones (list entry -> table entry -> edge id / T): a lane keeps
+// PAIR_ILP dependent chains in flight instead of one.
+template <typename Tab>
+__device__ __forceinline__ void wedges_pass2_ilp(const DGraph& g, const u32* __restrict__ Te, int32_t u, int len,
+                                                 int64_t rb, int32_t v, int32_t e, const Tab& tab, u64& s51,
+                                                 const PairOut& o) {
+  const int lane = threadIdx.x & 31;
+  int incl = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int total = __shfl_sync(FULL_MASK, incl, 31);
+  PairAcc A;
+  A.zero();
+  int cur = -1;
+  int32_t cv = 0, ce = 0;
+  for (int t0 = 0; t0 < total; t0 += 32 * PAIR_ILP) {
+    int32_t xs[PAIR_ILP], js[PAIR_ILP], vs[PAIR_ILP], es[PAIR_ILP];
+    int64_t ts[PAIR_ILP];
+#pragma unroll
+    for (int i = 0; i < PAIR_ILP; i++) {
+      const int t = t0 + 32 * i + lane;
+      int j = 0;
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) {
+        const int c = __shfl_sync(FULL_MASK, incl, j + s - 1);
+        if (c <= t) j += s;
+      }
+      const int start = __shfl_sync(FULL_MASK, incl - len, j);
+      const int64_t rbj = __shfl_sync(FULL_MASK, rb, j);
+      vs[i] = __shfl_sync(FULL_MASK, v, j);
+      es[i] = __shfl_sync(FULL_MASK, e, j);
+      const bool valid = t < total;
+      js[i] = valid ? j : -1;
+      ts[i] = rbj + (t - start);
+      xs[i] = valid ? g.ci[ts[i]] : u;
+    }
+    u64 wv[PAIR_ILP], dv[PAIR_ILP];
+#pragma unroll
+    for (int i = 0; i < PAIR_ILP; i++) {
+      wv[i] = 0; dv[i] = 0;
+      if (xs[i] != u) tab.get(xs[i], wv[i], dv[i]);
+    }
+    u32 te[PAIR_ILP];
+#pragma unroll
+    for (int i = 0; i < PAIR_ILP; i++) te[i] = wv[i] >= 2 ? Te[g.eid[ts[i]]] : 0u;
+#pragma unroll
+    for (int i = 0; i < PAIR_ILP; i++) {
+      if (js[i] < 0) continue;
+      if (js[i] != cur) {
+        if (cur >= 0) A.flush(u, cv, ce, o);
+        cur = js[i]; cv = vs[i]; ce = es[i];
+      }
+      if (wv[i] < 2) continue;  // W(u,x) = 1 (hence D = 0) contributes nothing
+      const u64 w = wv[i];
+      A.c5 += w - 1;
+      s51 += (u64)te[i] * (w - 1);
+      if (xs[i] > u) {
+        A.c49 += binom2(w - 1);
+        A.c62 += dv[i];
+      }
+    }
+  }
+  if (cur >= 0) A.flush(u, cv, ce, o);
 }
 
 // ---- warp engine: the warp runs one pass over items s_uv in [r0, r1) --------------------
 // Every part (wedges, chords) of 32 items at a time is flattened over the lanes.
 template <int PASS, typename Tab>
 __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
-                                          int64_t r0, int64_t r1, Tab& tab, u64& s51, const PairOut& o) {
+                                          int64_t r0, int64_t r1, Tab& tab, u64& s51, const PairOut& o, u64* acc) {
   const int lane = threadIdx.x & 31;
   for (int64_t o0 = r0; o0 < r1; o0 += 32) {
     PairItem it;
@@ -347,87 +433,61 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
       if (PASS == 2 && cur >= 0) A.flush(u, cv, ce, o);
     };
     // wedges
-    warp_flat(it.dv, [&](int j, int k, bool valid) {
-      const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
-      if (PASS == 2) {
-        const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-        const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
-        if (!valid) return;
-        if (j != cur) { flush(); cur = j; cv = vj; ce = ej; }
-        pass2_wedge(g, Te, u, rbj, k, tab, A, s51);
-      } else {
+    if (PASS == 2) {
+      wedges_pass2_ilp(g, Te, u, it.dv, it.rb, it.v, it.e, tab, s51, o);
+    } else {
+      warp_flat(it.dv, [&](int j, int k, bool valid) {
+        const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
         if (!valid) return;
         pass1_wedge(g, u, rbj, k, tab);
-      }
-    });
+      });
+    }
     flush();
     cur = -1;
-    // chords
+    // chords (two-level flattening); theta64 sums per item in acc[lane]
     warp_flat(it.tv, [&](int j, int k, bool valid) {
       const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
       const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
       const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-      const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
-      if (!valid) return;
-      if (PASS == 2 && j != cur) { flush(); cur = j; cv = vj; ce = ej; }
-      NoEnq ne;
-      chord_elem<PASS>(g, u, vj, foj, vloj, k, tab, A, ne);
+      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc);
     });
-    flush();
+    __syncwarp();
+    if (PASS == 2) {
+      if (have && acc[lane]) atomicAdd(&o.R64[it.v], acc[lane]);
+      acc[lane] = 0;
+      __syncwarp();
+    }
   }
 }
 
 // ---- CTA engine ------------------------------------------------------------------------
-// Sweep: warps take 32 items at a time from a shared counter and flatten their short parts
-// over the lanes.  Long parts -- a wedge or chord part longer than PAIR_LONG, or the
-// diamond list behind one chord longer than PAIR_DIAM_INLINE -- go to a shared queue;
-// rounds then cut the queued parts into PAIR_CHUNK-element chunks that whole warps take
-// from a second counter (chord chunks may queue diamond lists for the next round).
-// Every element is visited exactly once; no per-element search.
-enum { PK_WEDGE = 0, PK_CHORD = 1, PK_DIAM = 2 };
+// Sweep: warps take a few items at a time from a shared counter and flatten their short
+// parts over the lanes (chords and their diamond lists on two levels, chords_step).  Wedge
+// or chord parts longer than PAIR_LONG go to a shared queue; they are then cut into
+// PAIR_CHUNK-element chunks that whole warps take from a second counter.  Every element is
+// visited exactly once; no per-element search.
+enum { PK_WEDGE = 0, PK_CHORD = 1 };
 struct EngShared {
   int next;
   int qn;
   int next_chunk;
   int nchunks;
-  int64_t qslot[PAIR_LCAP];   // item slot s_uv (wedge / chord parts) or entry r (diamond)
-  int32_t qv[PAIR_LCAP];      // v (diamond parts)
+  int64_t qslot[PAIR_LCAP];   // item slot s_uv
   int8_t qkind[PAIR_LCAP];
-  int8_t qvlo[PAIR_LCAP];
   int32_t lc0[PAIR_LCAP + 1];
+  u64 acc[PAIR_HBT / 32][32];  // per-warp theta64 accumulators (chords_step)
 };
-
-struct CtaEnq {
-  EngShared* E;
-  __device__ __forceinline__ bool operator()(int64_t r, int32_t v, bool vlo) const {
-    const int q = atomicAdd(&E->qn, 1);
-    if (q >= PAIR_LCAP) return false;
-    E->qslot[q] = r; E->qv[q] = v; E->qkind[q] = PK_DIAM; E->qvlo[q] = vlo;
-    return true;
-  }
-};
-
-__device__ __forceinline__ int part_len(const DGraph& g, const EngShared& E, int q, int32_t hs) {
-  const int kind = E.qkind[q];
-  if (kind == PK_DIAM) {
-    const int64_t r = E.qslot[q];
-    const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
-    return (int)(g.foff[evw + 1] - g.foff[evw]);
-  }
-  const PairItem it = pair_item(g, E.qslot[q], hs);
-  return kind == PK_WEDGE ? it.dv : it.tv;
-}
 
 template <int PASS, typename Tab>
 __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs, int64_t r0, int64_t r1,
                          Tab& tab, EngShared& E, u64& s51, const PairOut& o) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  u64* acc = E.acc[wib];
   if (threadIdx.x == 0) { E.next = 0; E.qn = 0; }
+  acc[lane] = 0;
   __syncthreads();
-  CtaEnq enq{&E};
   const int64_t nitems = r1 - r0;
-  // items per warp grab: spread few items over all warps (one item per warp when the
-  // source has fewer items than warps), 32 when there are many
+  // items per warp grab: spread few items over all warps, 32 when there are many
   const int grab = (int)min((int64_t)32, max((int64_t)1, (nitems + (int64_t)(blockDim.x >> 5) - 1) /
                                                           (int64_t)(blockDim.x >> 5)));
   for (;;) {
@@ -455,146 +515,142 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     auto flush = [&]() {
       if (PASS == 2 && cur >= 0) A.flush(u, cv, ce, o);
     };
-    warp_flat(it.dv, [&](int j, int k, bool valid) {
-      const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
-      if (PASS == 2) {
-        const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-        const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
-        if (!valid) return;
-        if (j != cur) { flush(); cur = j; cv = vj; ce = ej; }
-        pass2_wedge(g, Te, u, rbj, k, tab, A, s51);
-      } else {
+    if (PASS == 2) {
+      wedges_pass2_ilp(g, Te, u, it.dv, it.rb, it.v, it.e, tab, s51, o);
+    } else {
+      warp_flat(it.dv, [&](int j, int k, bool valid) {
+        const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
         if (!valid) return;
         pass1_wedge(g, u, rbj, k, tab);
-      }
-    });
+      });
+    }
     flush();
-    cur = -1;
     warp_flat(it.tv, [&](int j, int k, bool valid) {
       const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
       const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
       const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-      const int32_t ej = __shfl_sync(FULL_MASK, it.e, j);
-      if (!valid) return;
-      if (PASS == 2 && j != cur) { flush(); cur = j; cv = vj; ce = ej; }
-      chord_elem<PASS>(g, u, vj, foj, vloj, k, tab, A, enq);
+      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc);
     });
-    flush();
+    __syncwarp();
+    if (PASS == 2) {
+      if (have && acc[lane]) atomicAdd(&o.R64[it.v], acc[lane]);
+      acc[lane] = 0;
+      __syncwarp();
+    }
   }
   __syncthreads();
-  // rounds over the queued parts
-  int qb = 0;
-  for (;;) {
-    const int qe = min(E.qn, PAIR_LCAP);
-    if (qb >= qe) break;  // uniform (E.qn read after a barrier)
-    if (threadIdx.x < 32) {
-      int carry = 0;
-      for (int q0 = qb; q0 < qe; q0 += 32) {
-        const int q = q0 + lane;
-        const int nc = (q < qe) ? (part_len(g, E, q, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
-        int incl = nc;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int y = __shfl_up_sync(FULL_MASK, incl, d);
-          if (lane >= d) incl += y;
-        }
-        if (q < qe) E.lc0[q - qb] = carry + incl - nc;
-        carry += __shfl_sync(FULL_MASK, incl, 31);
+  // queued long parts, cut in chunks
+  const int nq = min(E.qn, PAIR_LCAP);
+  if (nq == 0) return;  // uniform (E.qn read after a barrier)
+  if (threadIdx.x < 32) {
+    int carry = 0;
+    for (int q0 = 0; q0 < nq; q0 += 32) {
+      const int q = q0 + lane;
+      int nc = 0;
+      if (q < nq) {
+        const PairItem it = pair_item(g, E.qslot[q], hs);
+        nc = ((E.qkind[q] == PK_WEDGE ? it.dv : it.tv) + PAIR_CHUNK - 1) / PAIR_CHUNK;
       }
-      if (lane == 0) { E.lc0[qe - qb] = carry; E.nchunks = carry; E.next_chunk = 0; }
+      int incl = nc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, incl, d);
+        if (lane >= d) incl += y;
+      }
+      if (q < nq) E.lc0[q] = carry + incl - nc;
+      carry += __shfl_sync(FULL_MASK, incl, 31);
     }
-    __syncthreads();
-    const int nchunks = E.nchunks;
-    const int nq = qe - qb;
-    for (;;) {
-      int c = 0;
-      if (lane == 0) c = atomicAdd(&E.next_chunk, 1);
-      c = __shfl_sync(FULL_MASK, c, 0);
-      if (c >= nchunks) break;
+    if (lane == 0) { E.lc0[nq] = carry; E.nchunks = carry; E.next_chunk = 0; }
+  }
+  __syncthreads();
+  const int nchunks = E.nchunks;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&E.next_chunk, 1);
+    c = __shfl_sync(FULL_MASK, c, 0);
+    if (c >= nchunks) break;
+    int q = 0;
+    if (lane == 0) {
       int lo = 0, hi = nq;  // largest part with lc0 <= c
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (E.lc0[mid] <= c) lo = mid; else hi = mid;
       }
-      const int q = qb + lo;
-      const int kind = E.qkind[q];
-      const int k0 = (c - E.lc0[lo]) * PAIR_CHUNK;
-      PairAcc A;
-      A.zero();
-      int32_t fv = 0, fe = 0;
-      if (kind == PK_DIAM) {
-        const int64_t r = E.qslot[q];
-        const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
-        const int64_t f0 = g.foff[evw];
-        const int k1 = min((int)(g.foff[evw + 1] - f0), k0 + PAIR_CHUNK);
-        for (int k = k0 + lane; k < k1; k += 32) diamond_elem<PASS>(g, u, f0 + k, tab, A);
-        fv = E.qv[q];
-        fe = -1;  // no C4e credit from diamond parts (A.c5 stays 0)
-      } else {
-        const PairItem it = pair_item(g, E.qslot[q], hs);
-        fv = it.v;
-        fe = it.e;
-        if (kind == PK_WEDGE) {
-          // PAIR_CHUNK / 32 elements per lane, all loads issued before the table updates
-          constexpr int U = PAIR_CHUNK / 32;
-          const int k1 = min(it.dv, k0 + PAIR_CHUNK);
-          int32_t xs[U];
+      q = lo;
+    }
+    q = __shfl_sync(FULL_MASK, q, 0);
+    const int kind = E.qkind[q];
+    const int k0 = (c - E.lc0[q]) * PAIR_CHUNK;
+    const PairItem it = pair_item(g, E.qslot[q], hs);
+    PairAcc A;
+    A.zero();
+    if (kind == PK_WEDGE) {
+      // PAIR_CHUNK / 32 elements per lane, all loads issued before the table updates
+      constexpr int U = PAIR_CHUNK / 32;
+      const int k1 = min(it.dv, k0 + PAIR_CHUNK);
+      int32_t xs[U];
 #pragma unroll
-          for (int i = 0; i < U; i++) {
-            const int k = k0 + lane + 32 * i;
-            xs[i] = k < k1 ? g.ci[it.rb + k] : u;
-          }
-          if (PASS == 1) {
-            if constexpr (Tab::kDense) {
-              typename Tab::WordT olds[U];
+      for (int i = 0; i < U; i++) {
+        const int k = k0 + lane + 32 * i;
+        xs[i] = k < k1 ? g.ci[it.rb + k] : u;
+      }
+      if (PASS == 1) {
+        if constexpr (Tab::kDense) {
+          typename Tab::WordT olds[U];
 #pragma unroll
-              for (int i = 0; i < U; i++) olds[i] = xs[i] != u ? tab.raw_add(xs[i], 1) : 1;
+          for (int i = 0; i < U; i++) olds[i] = xs[i] != u ? tab.raw_add(xs[i], 1) : 1;
 #pragma unroll
-              for (int i = 0; i < U; i++)
-                if (xs[i] != u) tab.after_w(xs[i], olds[i]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < U; i++)
-                if (xs[i] != u) tab.add_w(xs[i]);
-            }
-          } else {
-            u32 te[U];
-            u64 wv[U], dv[U];
-#pragma unroll
-            for (int i = 0; i < U; i++) {
-              wv[i] = 0; dv[i] = 0;
-              if (xs[i] != u) tab.get(xs[i], wv[i], dv[i]);
-            }
-#pragma unroll
-            for (int i = 0; i < U; i++) {
-              const int k = k0 + lane + 32 * i;
-              te[i] = wv[i] >= 2 ? Te[g.eid[it.rb + k]] : 0u;  // W = 1 pairs contribute nothing
-            }
-#pragma unroll
-            for (int i = 0; i < U; i++) {
-              if (wv[i] < 2) continue;
-              const u64 w = wv[i];
-              A.c5 += w - 1;
-              s51 += (u64)te[i] * (w - 1);
-              if (xs[i] > u) {
-                A.c49 += binom2(w - 1);
-                A.c62 += dv[i];
-              }
-            }
-          }
+          for (int i = 0; i < U; i++)
+            if (xs[i] != u) tab.after_w(xs[i], olds[i]);
         } else {
-          const int k1 = min(it.tv, k0 + PAIR_CHUNK);
-          for (int k = k0 + lane; k < k1; k += 32) chord_elem<PASS>(g, u, it.v, it.fo, it.vlo, k, tab, A, enq);
+#pragma unroll
+          for (int i = 0; i < U; i++)
+            if (xs[i] != u) tab.add_w(xs[i]);
+        }
+      } else {
+        u32 te[U];
+        u64 wv[U], dv[U];
+#pragma unroll
+        for (int i = 0; i < U; i++) {
+          wv[i] = 0; dv[i] = 0;
+          if (xs[i] != u) tab.get(xs[i], wv[i], dv[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < U; i++) {
+          const int k = k0 + lane + 32 * i;
+          te[i] = wv[i] >= 2 ? Te[g.eid[it.rb + k]] : 0u;  // W = 1 pairs contribute nothing
+        }
+#pragma unroll
+        for (int i = 0; i < U; i++) {
+          if (wv[i] < 2) continue;
+          const u64 w = wv[i];
+          A.c5 += w - 1;
+          s51 += (u64)te[i] * (w - 1);
+          if (xs[i] > u) {
+            A.c49 += binom2(w - 1);
+            A.c62 += dv[i];
+          }
         }
       }
-      if (PASS == 2) {
-        A.c5 = warp_sum(A.c5); A.c49 = warp_sum(A.c49); A.c62 = warp_sum(A.c62); A.c64 = warp_sum(A.c64);
-        if (lane == 0) A.flush(u, fv, fe, o);
+    } else {
+      const int k1 = min(it.tv, k0 + PAIR_CHUNK);
+      for (int i = 0; i < PAIR_CHUNK / 32; i++) {
+        const int k = k0 + lane + 32 * i;
+        chords_step<PASS>(g, u, k < k1, it.v, it.fo, it.vlo, k, 0, tab, acc);
       }
+      __syncwarp();
+      if (PASS == 2 && lane == 0) {
+        A.c64 = acc[0];
+        acc[0] = 0;
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    qb = qe;
+    if (PASS == 2) {
+      A.c5 = warp_sum(A.c5); A.c49 = warp_sum(A.c49); A.c62 = warp_sum(A.c62);
+      if (lane == 0) A.flush(u, it.v, it.e, o);
+    }
   }
+  __syncthreads();
 }
 
 // ---- the h* contribution ----------------------------------------------------------------
@@ -645,6 +701,60 @@ __device__ __forceinline__ void hstar_search(const DGraph& g, const u32* __restr
   });
 }
 
+// membership through the hub's position map (one load per key)
+template <typename Tab>
+__device__ __forceinline__ void hstar_map(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
+                                          const int32_t* __restrict__ pmap, Tab& tab, int tid, int nthr,
+                                          PairAcc& H, u64& s51) {
+  const int64_t hb = g.rp[hs];
+  tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
+    const int32_t k = pmap[x];
+    if (k >= 0) {
+      w += 1;
+      H.c5 += w - 1;
+      s51 += (u64)Te[g.eid[hb + k]] * (w - 1);
+      if (x > u) {
+        H.c49 += binom2(w - 1);
+        H.c62 += d;
+      }
+    }
+    return w;
+  });
+}
+
+// the h* term by the cheapest available way
+template <typename Tab>
+__device__ __forceinline__ void hstar_term(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
+                                           const PairOut& o, Tab& tab, int tid, int nthr, u64 nkeys_bound,
+                                           PairAcc& H, u64& s51) {
+  const int32_t slot = o.hub_slot[hs];
+  if (slot >= 0) hstar_map(g, Te, u, hs, o.hub_pos + (size_t)slot * (size_t)g.n, tab, tid, nthr, H, s51);
+  else if (Tab::kDense || (u64)dg_deg(g, hs) <= 12ull * nkeys_bound) hstar_walk(g, Te, u, hs, tab, tid, nthr, H, s51);
+  else hstar_search(g, Te, u, hs, tab, tid, nthr, H, s51);
+}
+
+// position maps of the hubs (d >= PAIR_HUBMAP_MIN) up to max_slots rows
+__global__ void k_hub_slots(DGraph g, int max_slots, int32_t* __restrict__ slot, int* __restrict__ cnt) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
+    int32_t sl = -1;
+    if (dg_deg(g, v) >= PAIR_HUBMAP_MIN) {
+      const int q = atomicAdd(cnt, 1);
+      if (q < max_slots) sl = q;
+    }
+    slot[v] = sl;
+  }
+}
+__global__ void k_hub_maps(DGraph g, const int32_t* __restrict__ slot, int32_t* __restrict__ pos) {
+  // block per hub-candidate vertex range: grid-stride over vertices, block-stride over lists
+  for (int32_t v = blockIdx.x; v < g.n; v += gridDim.x) {
+    const int32_t sl = slot[v];
+    if (sl < 0) continue;
+    int32_t* row = pos + (size_t)sl * (size_t)g.n;
+    const int64_t b = g.rp[v], e = g.rp[v + 1];
+    for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)(k - b);
+  }
+}
+
 // per-pair terms over the final table (keys with W >= 2)
 template <typename Tab>
 __device__ __forceinline__ void entry_terms(const DGraph& g, Tab& tab, int tid, int nthr, u64& a8, u64& a36,
@@ -667,6 +777,17 @@ __device__ __forceinline__ int32_t edge_of(const DGraph& g, int32_t u, int32_t v
   return g.eid[p];
 }
 
+// developer phase timers (EVOKE_DEBUG): SM cycles per phase summed over sources, CTA tiers
+__device__ unsigned long long g_pair_phase[2][8];
+#define PAIR_PHASE(i)                                                                     \
+  do {                                                                                    \
+    if (threadIdx.x == 0) {                                                               \
+      const long long t_ = clock64();                                                     \
+      atomicAdd(&g_pair_phase[Tab::kDense ? 1 : 0][i], (unsigned long long)(t_ - t_prev)); \
+      t_prev = t_;                                                                        \
+    }                                                                                     \
+  } while (0)
+
 // ---- one source on a CTA (mid and heavy tiers) ------------------------------------------
 template <int BT, typename Tab>
 __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int32_t u, Tab& tab, EngShared& E,
@@ -674,14 +795,13 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
   const int32_t hs = o.hstar[u];
   u64 s51 = 0;
+  long long t_prev = clock64();
   cta_pass<1>(g, Te, u, hs, r0, r1, tab, E, s51, o);
+  PAIR_PHASE(0);
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
   PairAcc H;
   H.zero();
-  if (hs >= 0) {
-    if (Tab::kDense || hstar_prefer_walk(g, hs, (u64)(tab_keys_bound))) hstar_walk(g, Te, u, hs, tab, threadIdx.x, BT, H, s51);
-    else hstar_search(g, Te, u, hs, tab, threadIdx.x, BT, H, s51);
-  }
+  if (hs >= 0) hstar_term(g, Te, u, hs, o, tab, threadIdx.x, BT, (u64)tab_keys_bound, H, s51);
   H.c5 = warp_sum(H.c5); H.c49 = warp_sum(H.c49); H.c62 = warp_sum(H.c62);
   if ((threadIdx.x & 31) == 0) {
     if (H.c5) atomicAdd(&red[5], H.c5);
@@ -689,9 +809,12 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
     if (H.c62) atomicAdd(&red[7], H.c62);
   }
   __syncthreads();
+  PAIR_PHASE(1);
   entry_terms(g, tab, threadIdx.x, BT, a8, a36, a50, a63);
   __syncthreads();  // W final
+  PAIR_PHASE(2);
   cta_pass<2>(g, Te, u, hs, r0, r1, tab, E, s51, o);
+  PAIR_PHASE(3);
   for (int64_t s = r0 + threadIdx.x; s < r1; s += BT) {
     const u64 w = tab.get_w_or0(g.ci[s]);
     s51 -= w * (w - 1);
@@ -715,29 +838,27 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   }
   tab.reset(threadIdx.x, BT);
   __syncthreads();
+  PAIR_PHASE(4);
 }
 
 // ---- light tier: one warp per source --------------------------------------------------
 __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, int32_t u, u32 cap,
-                                 SharedPackedHash& tab, const PairOut& o) {
+                                 SharedPackedHash& tab, const PairOut& o, u64* acc) {
   const int lane = threadIdx.x & 31;
   const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
   const int32_t hs = o.hstar[u];
   tab.mask = cap - 1;
   u64 s51 = 0;
-  warp_pass<1>(g, Te, u, hs, r0, r1, tab, s51, o);
+  warp_pass<1>(g, Te, u, hs, r0, r1, tab, s51, o, acc);
   __syncwarp();
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
   PairAcc H;
   H.zero();
-  if (hs >= 0) {
-    if (hstar_prefer_walk(g, hs, cap / 2)) hstar_walk(g, Te, u, hs, tab, lane, 32, H, s51);
-    else hstar_search(g, Te, u, hs, tab, lane, 32, H, s51);
-  }
+  if (hs >= 0) hstar_term(g, Te, u, hs, o, tab, lane, 32, (u64)(cap / 2), H, s51);
   __syncwarp();
   entry_terms(g, tab, lane, 32, a8, a36, a50, a63);
   __syncwarp();
-  warp_pass<2>(g, Te, u, hs, r0, r1, tab, s51, o);
+  warp_pass<2>(g, Te, u, hs, r0, r1, tab, s51, o, acc);
   for (int64_t s = r0 + lane; s < r1; s += 32) {
     const u64 w = tab.get_w_or0(g.ci[s]);
     s51 -= w * (w - 1);
@@ -792,6 +913,8 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
   tab.keys = sh_pairs + wib * (2 * PAIR_WARP_CAP);
   tab.val = (u32*)(tab.keys + PAIR_WARP_CAP);
   for (int h = lane; h < PAIR_WARP_CAP; h += 32) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
+  u64* acc = E.acc[wib];
+  acc[lane] = 0;
   __syncwarp();
   for (;;) {
     int idx = 0;
@@ -802,7 +925,7 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
     for (int q = idx; q < end; q++) {
       const int32_t u = light[q];
       const u32 cap = pow2_at_least(2u * est[u], 32u);
-      pair_source_warp(g, Te, u, cap, tab, o);
+      pair_source_warp(g, Te, u, cap, tab, o, acc);
     }
   }
 }

@@ -156,7 +156,7 @@ __device__ __forceinline__ void warp_append(bool pred, int32_t val, int32_t* lis
 // returns its contribution to the item's sum; flush(i, sum) receives non-zero partial
 // sums (several per item are possible: callers accumulate with atomics).
 // ---------------------------------------------------------------------------------
-#define LE_LONG 64      // item longer than this: queued and cut in chunks (CTA engine)
+#define LE_LONG 32      // item longer than this: queued and cut in chunks (CTA engine)
 #define LE_CHUNK 256    // elements per chunk (8 per lane)
 #define LE_QCAP 512     // queue capacity (overflowing items are walked by the sweep warp)
 

@@ -34,5 +34,6 @@ for r in rows:
     a[0] += samp
     a[1] += ex
 tot = sum(v[0] for v in agg.values()) or 1
-for (f, ln), (s, e, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+by = 1 if (len(sys.argv) > 3 and sys.argv[3] == "inst") else 0
+for (f, ln), (s, e, src) in sorted(agg.items(), key=lambda kv: -kv[1][by])[:top]:
     print(f"{100 * s / tot:5.1f}%  inst {e:10.3g}  {f}:{ln}  {src}")
