@@ -235,7 +235,7 @@ def main():
     _, wm = pkg.evoke_orbits_edges(g.n, edges_dev, out=out_dev, shard_index=rank, num_shards=world,
                                    stream=stream.cuda_stream, workmodel=True)
     torch.cuda.synchronize()
-    roof = roofline(wm, pass_ms, peak, peak_src)
+    roof = roofline(wm, pass_ms, peak, peak_src, step_ms=ms)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
@@ -259,7 +259,19 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def roofline(wm, pass_ms, peak_gbs, peak_src):
+def traffic_of(pass_name):
+    """DRAM bytes per launch of the pass's kernels from the committed ncu --set full capture
+    (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get("passes", {}).get(pass_name)
+    except Exception:
+        return None
+
+
+def roofline(wm, pass_ms, peak_gbs, peak_src, step_ms=None):
     """Dominant pass and its achieved algorithmic GB/s: the
     library's work model (units x bytes/unit, one untimed call) over the pass's mean
     CUDA-event duration inside the timed steps."""
@@ -267,9 +279,11 @@ def roofline(wm, pass_ms, peak_gbs, peak_src):
     top = max(compute_passes, key=compute_passes.get)
     t = compute_passes[top] / 1e3
     bytes_ = wm["alg_bytes"].get(top, 0.0)
-    base = {"bound": "hbm", "kernel": top, "peak": peak_gbs, "unit": "GB/s", "traffic": None,
+    # the pair, hub-local, 5-cycle and theta66/70 passes run concurrently: each pass time is
+    # its own span, so the share is taken against the measured step, not the sum of passes
+    base = {"bound": "hbm", "kernel": top, "peak": peak_gbs, "unit": "GB/s", "traffic": traffic_of(top),
             "ms": compute_passes[top], "peak_source": peak_src,
-            "share_of_step": compute_passes[top] / sum(compute_passes.values()), "units": wm["units"]}
+            "share_of_step": compute_passes[top] / step_ms if step_ms else None, "units": wm["units"]}
     if not bytes_ or t <= 0:
         base.update({"achieved": None, "frac": None})
         return base
