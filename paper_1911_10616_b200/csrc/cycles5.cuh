@@ -52,7 +52,7 @@ struct __align__(16) C5Rec {
 #define C5_BT 256
 #define C5_WARP_MAX 1024          // light endpoint: W(l) + d(l) <= this
 #define C5_WARP_CAP 2048          // records per warp region (load <= 0.5)
-#define C5_GIANT (1ull << 40)     // endpoint work above which the whole grid takes it (off)
+#define C5_GIANT (1ull << 40)     // endpoint work above which a thread-block cluster takes it (off)
 #define C5_HBT 1024               // heavy-endpoint CTA
 
 // dense records indexed by vertex id; touched list holds vertex ids
@@ -129,11 +129,16 @@ struct CtaEng {
   __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const { cta_lists(n, *E, info, elem, flush); }
 };
 
-// whole-grid engine for the giant endpoints (cooperative launch): warp per item
-struct GridEng {
-  __device__ __forceinline__ void sync() const { cooperative_groups::this_grid().sync(); }
-  __device__ __forceinline__ int tid() const { return (int)(blockIdx.x * blockDim.x + threadIdx.x); }
-  __device__ __forceinline__ int nthr() const { return (int)(gridDim.x * blockDim.x); }
+// cluster engine for the giant endpoints: one thread-block cluster of C5_CLUSTER CTAs
+// takes an endpoint; warps of the whole cluster share each step (warp per item) and the
+// steps are separated by hardware cluster barriers (records and counters in global memory)
+#define C5_CLUSTER 8
+struct ClusterEng {
+  __device__ __forceinline__ void sync() const { cooperative_groups::this_cluster().sync(); }
+  __device__ __forceinline__ int tid() const {
+    return (int)(cooperative_groups::this_cluster().block_rank() * blockDim.x + threadIdx.x);
+  }
+  __device__ __forceinline__ int nthr() const { return (int)(C5_CLUSTER * blockDim.x); }
   template <typename I, typename E2, typename F>
   __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const {
     const int lane = threadIdx.x & 31;
@@ -407,29 +412,38 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
   }
 }
 
-// Giant endpoints (W(l) > C5_GIANT): one at a time over the whole grid (cooperative
-// launch; grid barriers between the steps), so a hub endpoint is not bound to one SM.
-// ctl: [0] touched count, [1] J count; tot: u64 scratch.
-__global__ void __launch_bounds__(1024) k_c5_giant(DGraph g, const u32* __restrict__ Tlow,
-                                                   const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
-                                                   const int32_t* __restrict__ giant, int n_giant,
-                                                   C5Rec* __restrict__ dense, int32_t* __restrict__ dlists,
-                                                   int* __restrict__ ctl, u64* __restrict__ tot,
-                                                   u64* __restrict__ C5) {
-  GridEng eng;
+// Giant endpoints (W(l) > C5_GIANT): one cluster each (persistent clusters, W-sorted list),
+// so a hub endpoint is spread over C5_CLUSTER SMs.  ctl per cluster: [nL, nJ, idx, -].
+__global__ void __cluster_dims__(C5_CLUSTER, 1, 1) __launch_bounds__(1024)
+    k_c5_cluster(DGraph g, const u32* __restrict__ Tlow, const u32* __restrict__ Tmid,
+                 const u32* __restrict__ Thigh, const int32_t* __restrict__ giant, int n_giant,
+                 int* __restrict__ counter, C5Rec* __restrict__ dense, int32_t* __restrict__ dlists,
+                 int* __restrict__ ctl, u64* __restrict__ tot, u64* __restrict__ C5) {
+  auto cluster = cooperative_groups::this_cluster();
+  const int cid = blockIdx.x / C5_CLUSTER;
+  const bool leader = cluster.block_rank() == 0 && threadIdx.x == 0;
+  ClusterEng eng;
   C5Dense loc;
-  loc.R = dense;
-  loc.L = dlists;
-  loc.nL = &ctl[0];
-  int32_t* J = dlists + g.n;
-  for (int q = 0; q < n_giant; q++) {
-    const int32_t l = giant[q];
-    c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &ctl[1], tot, C5);  // ends with a grid barrier
+  loc.R = dense + (size_t)cid * g.n;
+  loc.L = dlists + (size_t)cid * 2 * g.n;
+  loc.nL = &ctl[4 * cid + 0];
+  int32_t* J = loc.L + g.n;
+  for (;;) {
+    if (leader) ctl[4 * cid + 2] = atomicAdd(counter, 1);
+    cluster.sync();
+    const int idx = *(volatile int*)&ctl[4 * cid + 2];
+    if (idx >= n_giant) break;
+    const int32_t l = giant[idx];
+    c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &ctl[4 * cid + 1], &tot[cid], C5);  // ends with a barrier
     c5_reset(eng, loc);
-    if (eng.tid() == 0 && *tot) atomicAdd(&C5[l], *tot);
-    eng.sync();
-    if (eng.tid() == 0) { ctl[0] = 0; ctl[1] = 0; *tot = 0; }
-    eng.sync();
+    cluster.sync();
+    if (leader) {
+      const u64 t = *(volatile u64*)&tot[cid];
+      if (t) atomicAdd(&C5[l], t);
+      tot[cid] = 0;
+      ctl[4 * cid + 0] = 0;
+      ctl[4 * cid + 1] = 0;
+    }
   }
 }
 

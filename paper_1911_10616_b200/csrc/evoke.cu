@@ -772,17 +772,19 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       size_t freeb = 0, totalb = 0;
       CK(cudaMemGetInfo(&freeb, &totalb));
       if (ngiant > 0) {
-        C5Rec* dense = A.alloc<C5Rec>((size_t)n, true);
-        int32_t* dl = A.alloc<int32_t>((size_t)2 * n);
-        int* ctl = A.alloc<int>(2, true);
-        u64* tot = A.alloc<u64>(1, true);
-        int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_giant, 1024, 0));
-        const int gg = std::max(1, std::min(bps, 2)) * SM;
-        void* args[] = {(void*)&g, (void*)&Tlow, (void*)&Tmid, (void*)&Thigh, (void*)&hs, (void*)&ngiant,
-                        (void*)&dense, (void*)&dl, (void*)&ctl, (void*)&tot, (void*)&C5out};
-        CK(cudaLaunchCooperativeKernel((void*)k_c5_giant, gg, 1024, args, 0, C.st));
-        C.launches++;
+        const int nclus = std::min(ngiant, std::max(1, SM / C5_CLUSTER));
+        C5Rec* dense = A.alloc<C5Rec>((size_t)nclus * n, true);
+        int32_t* dl = A.alloc<int32_t>((size_t)nclus * 2 * n);
+        int* ctl = A.alloc<int>((size_t)4 * nclus + 4, true);
+        u64* tot = A.alloc<u64>(nclus, true);
+        int* gcounter = ctl + 4 * nclus;
+        const int32_t* hsg = hs;
+        const int ng = ngiant;
+        jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
+          k_c5_cluster<<<nclus * C5_CLUSTER, 1024, 0, st>>>(g, Tlow, Tmid, Thigh, hsg, ng, gcounter, dense, dl, ctl,
+                                                             tot, C5out);
+          C.launches++;
+        }});
       }
       const int nrest = n5h - ngiant;
       if (nrest > 0) {
