@@ -36,14 +36,21 @@
 #include "sched.cuh"
 #include <cooperative_groups.h>
 
-struct __align__(16) C5Rec {
+// Record of one vertex for one endpoint.  wf = Wn | flags << 28 (Wn < 2^28 because Wn(i)
+// <= d(l) and max degree < 2^28 is checked); V = u32 when the endpoint's work bound W(l) <
+// 2^32 (every field is at most W(l)), else u64.  32 or 64 bytes.
+template <typename V>
+struct __align__(16) C5RecT {
   int32_t key;   // hash regions: x + 1 (0 = empty); unused in dense tables
-  u32 flag;      // C5_* bits
-  u32 Wn;
-  u32 Q;
-  u64 P, A, QT, QM, S;
-  u64 pad;
+  u32 wf;        // Wn (low 28 bits) | C5_* flags (high 4 bits)
+  V Q, P, A, QT, QM, S;
 };
+typedef C5RecT<u64> C5Rec;
+#define C5_WN_MASK 0x0fffffffu
+template <typename R>
+__device__ __forceinline__ u32 c5_flags(const R* r) { return r->wf >> 28; }
+template <typename R>
+__device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MASK); }
 #define C5_ADJ 1u      // vertex is a neighbour of l
 #define C5_I 2u        // i-key (steps 1, 3)
 #define C5_J 4u        // j-key (step 2)
@@ -56,31 +63,35 @@ struct __align__(16) C5Rec {
 #define C5_HBT 1024               // heavy-endpoint CTA
 
 // dense records indexed by vertex id; touched list holds vertex ids
+template <typename Rec>
 struct C5Dense {
-  C5Rec* R;
+  typedef Rec RecT;
+  Rec* R;
   int32_t* L;
   int* nL;
-  __device__ __forceinline__ C5Rec* mark(int32_t x, u32 bits, u32& old) {
-    C5Rec* r = &R[x];
-    old = atomicOr(&r->flag, bits | C5_PRESENT);
+  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
+    Rec* r = &R[x];
+    old = atomicOr(&r->wf, (bits | C5_PRESENT) << 28) >> 28;
     append_active(!(old & C5_PRESENT), x, L, nL);
     return r;
   }
-  __device__ __forceinline__ C5Rec* peek(int32_t x) const { return &R[x]; }
-  __device__ __forceinline__ C5Rec* touched(int t, int32_t& x) const {
+  __device__ __forceinline__ Rec* peek(int32_t x) const { return &R[x]; }
+  __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
     x = L[t];
     return &R[x];
   }
 };
 
 // open-addressing records (key = x + 1); touched list holds slots
+template <typename Rec>
 struct C5Hash {
-  C5Rec* R;
+  typedef Rec RecT;
+  Rec* R;
   u32 mask;
   int32_t* L;
   int* nL;
   __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) >> 7 & mask; }
-  __device__ __forceinline__ C5Rec* mark(int32_t x, u32 bits, u32& old) {
+  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
     u32 h = h0(x);
     for (;;) {
       const int32_t k = R[h].key;
@@ -91,12 +102,12 @@ struct C5Hash {
       }
       h = (h + 1) & mask;
     }
-    C5Rec* r = &R[h];
-    old = atomicOr(&r->flag, bits | C5_PRESENT);
+    Rec* r = &R[h];
+    old = atomicOr(&r->wf, (bits | C5_PRESENT) << 28) >> 28;
     append_active(!(old & C5_PRESENT), (int32_t)h, L, nL);
     return r;
   }
-  __device__ __forceinline__ C5Rec* peek(int32_t x) const {
+  __device__ __forceinline__ Rec* peek(int32_t x) const {
     u32 h = h0(x);
     for (;;) {
       const int32_t k = R[h].key;
@@ -105,8 +116,8 @@ struct C5Hash {
       h = (h + 1) & mask;
     }
   }
-  __device__ __forceinline__ C5Rec* touched(int t, int32_t& x) const {
-    C5Rec* r = &R[L[t]];
+  __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
+    Rec* r = &R[L[t]];
     x = r->key - 1;
     return r;
   }
@@ -155,7 +166,8 @@ struct ClusterEng {
   }
 };
 
-__device__ __forceinline__ bool c5_adj(const C5Rec* r) { return r && (r->flag & C5_ADJ); }
+template <typename R>
+__device__ __forceinline__ bool c5_adj(const R* r) { return r && (c5_flags(r) & C5_ADJ); }
 
 // One endpoint l.  J: list of j-keys (counter *nJ); tot: per-engine shared u64 (zeroed).
 template <typename Eng, typename Loc>
@@ -188,8 +200,8 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int32_t i = g.ci[base + k];
         if (i == l) return 0;
         u32 old;
-        C5Rec* r = loc.mark(i, C5_I, old);
-        atomicAdd(&r->Wn, 1u);
+        auto* r = loc.mark(i, C5_I, old);
+        atomicAdd(&r->wf, 1u);  // Wn
         return 0;
       },
       [&](int, u64) {});
@@ -200,11 +212,12 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int32_t j = g.ocol[e];
         if (j == l) return 0;
         u32 old;
-        C5Rec* r = loc.mark(j, C5_J, old);
+        auto* r = loc.mark(j, C5_J, old);
         append_active(!(old & C5_J), j, J, nJ);
-        atomicAdd(&r->Q, 1u);
-        atomicAdd(&r->QT, (u64)Thigh[e]);
-        atomicAdd(&r->QM, (u64)Tmid[e]);
+        typedef decltype(r->Q) V;
+        atomicAdd(&r->Q, (V)1);
+        atomicAdd(&r->QT, (V)Thigh[e]);
+        atomicAdd(&r->QM, (V)Tmid[e]);
         return 0;
       },
       [&](int, u64) {});
@@ -220,26 +233,28 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       [&](int t, int64_t base, int k) -> u64 {
         const int32_t i = g.ocol[base + k];
         if (i == l) return 0;
-        const C5Rec* rj = loc.peek(J[t]);
-        const u64 q = rj->Q;
-        const bool adjj = rj->flag & C5_ADJ;
+        const auto* rj = loc.peek(J[t]);
+        typedef decltype(rj->Q) V;
+        const V q = rj->Q;
+        const bool adjj = c5_flags(rj) & C5_ADJ;
         u32 old;
-        C5Rec* ri = loc.mark(i, C5_I, old);
+        auto* ri = loc.mark(i, C5_I, old);
         atomicAdd(&ri->P, q);
         if (adjj) atomicAdd(&ri->A, q);
-        return (u64)ri->Wn;  // Wn is final after step 1
+        return c5_wn(ri);  // Wn is final after step 1
       },
       [&](int t, u64 s) {
-        C5Rec* rj = loc.peek(J[t]);
-        atomicAdd(&rj->S, s);
+        auto* rj = loc.peek(J[t]);
+        typedef decltype(rj->S) V;
+        atomicAdd(&rj->S, (V)s);
         atomicAdd(&C5[J[t]], (u64)rj->Q * s);  // the j credit is linear in S
       });
   // constant part of the j credits
   for (int t = eng.tid(); t < nj; t += eng.nthr()) {
     const int32_t j = J[t];
-    const C5Rec* rj = loc.peek(j);
+    const auto* rj = loc.peek(j);
     const u64 q = rj->Q;
-    const bool adjj = rj->flag & C5_ADJ;
+    const bool adjj = c5_flags(rj) & C5_ADJ;
     const u64 lj = (l > j && adjj) ? 1ull : 0ull;
     const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
     const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rj->QT - q * lj);
@@ -252,11 +267,11 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int64_t e = base + k;
         const int32_t j = g.ocol[e];
         if (j == l) return 0;
-        const C5Rec* rj = loc.peek(j);
-        const bool adjj = rj->flag & C5_ADJ;
+        const auto* rj = loc.peek(j);
+        const bool adjj = c5_flags(rj) & C5_ADJ;
         const u64 lj = (l > j && adjj) ? 1ull : 0ull;
         const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-        return rj->S - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[e] - lj);
+        return (u64)rj->S - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[e] - lj);
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
   // ---- step 5: i credits (and their sum for l)
@@ -265,11 +280,12 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
     u64 acc = 0;
     for (int t = eng.tid(); t < nt; t += eng.nthr()) {
       int32_t x;
-      const C5Rec* r = loc.touched(t, x);
-      if (!(r->flag & C5_I)) continue;
-      const bool adji = r->flag & C5_ADJ;
-      const u64 bi = r->QM - (u64)r->Q * ((x > l && adji) ? 1ull : 0ull);
-      const u64 ci = r->P * (u64)r->Wn - r->A - bi;
+      const auto* r = loc.touched(t, x);
+      const u32 fl = c5_flags(r);
+      if (!(fl & C5_I)) continue;
+      const bool adji = fl & C5_ADJ;
+      const u64 bi = (u64)r->QM - (u64)r->Q * ((x > l && adji) ? 1ull : 0ull);
+      const u64 ci = (u64)r->P * c5_wn(r) - (u64)r->A - bi;
       if (ci) atomicAdd(&C5[x], ci);
       acc += ci;
     }
@@ -283,10 +299,10 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int32_t i = g.ci[s];
         if (i == l) return 0;
         const int32_t w = g.ci[r0 + t];
-        const C5Rec* ri = loc.peek(i);
+        const auto* ri = loc.peek(i);
         u64 corr = (w < i) ? (u64)Tlow[g.eid[r0 + t]] : 0ull;
         if (w < l && w < i) corr += (u64)Tmid[g.eid[s]] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
-        return ri->P - corr;
+        return (u64)ri->P - corr;
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
   eng.sync();
@@ -298,10 +314,11 @@ __device__ __forceinline__ void c5_reset(const Eng& eng, Loc& loc) {
   const int nt = *loc.nL;
   for (int t = eng.tid(); t < nt; t += eng.nthr()) {
     int32_t x;
-    C5Rec* r = loc.touched(t, x);
+    auto* r = loc.touched(t, x);
     uint4* q = reinterpret_cast<uint4*>(r);
     const uint4 z = make_uint4(0, 0, 0, 0);
-    q[0] = z; q[1] = z; q[2] = z; q[3] = z;
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(*r) / 16); i++) q[i] = z;
   }
 }
 
@@ -309,8 +326,9 @@ __device__ __forceinline__ void c5_reset(const Eng& eng, Loc& loc) {
 // W(l) = sum_{w in N(l)} |Nsel(w)| + sum_{k in N-(l)} (d+(k) + sum_{j in N+(k)} d+(j)) + d(l)
 // bounds the records an endpoint touches.  Light: W <= C5_WARP_MAX (the count stops
 // there); heavy otherwise, with sort key d(l)^2 + W (hubs first).
-__global__ void k_c5_items(DGraph g, int shard_index, int num_shards, int32_t* __restrict__ light, int* n_light,
-                           int32_t* __restrict__ heavy, u64* __restrict__ heavy_w, int* n_heavy) {
+__global__ void k_c5_items(DGraph g, int shard_index, int num_shards, int32_t* __restrict__ light,
+                           u32* __restrict__ light_w, int* n_light, int32_t* __restrict__ heavy,
+                           u64* __restrict__ heavy_w, int* n_heavy) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -336,7 +354,20 @@ __global__ void k_c5_items(DGraph g, int shard_index, int num_shards, int32_t* _
     }
     const bool is_light = mine && w <= C5_WARP_MAX;
     const bool is_heavy = mine && w > C5_WARP_MAX;
-    warp_append(is_light, l, light, n_light);
+    {
+      const u32 bl = __ballot_sync(FULL_MASK, is_light);
+      if (bl) {
+        int lb = 0;
+        const int leader = __ffs(bl) - 1;
+        if (lane == leader) lb = atomicAdd(n_light, __popc(bl));
+        lb = __shfl_sync(FULL_MASK, lb, leader);
+        if (is_light) {
+          const int q = lb + __popc(bl & ((1u << lane) - 1u));
+          light[q] = l;
+          light_w[q] = (u32)w;
+        }
+      }
+    }
     const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
     if (bal) {
       int hb = 0;
@@ -353,16 +384,17 @@ __global__ void k_c5_items(DGraph g, int shard_index, int num_shards, int32_t* _
 }
 
 // Heavy endpoints: one CTA each, dense records per CTA (persistent, W-sorted list).
+template <typename V>
 __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __restrict__ Tlow,
                                                     const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                     const int32_t* __restrict__ heavy, int n_heavy,
-                                                    int* __restrict__ counter, C5Rec* __restrict__ dense,
+                                                    int* __restrict__ counter, C5RecT<V>* __restrict__ dense,
                                                     int32_t* __restrict__ dlists, u64* __restrict__ C5) {
   __shared__ ListEng E;
   __shared__ int s_idx, s_nL, s_nJ;
   __shared__ u64 s_tot;
   CtaEng eng{&E};
-  C5Dense loc;
+  C5Dense<C5RecT<V>> loc;
   loc.R = dense + (size_t)blockIdx.x * g.n;
   loc.L = dlists + (size_t)blockIdx.x * 2 * g.n;
   loc.nL = &s_nL;
@@ -380,22 +412,23 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
   }
 }
 
-// Light endpoints: one warp each, records in a per-warp open-addressing region.
+// Light endpoints: one warp each, 32-byte records in a per-warp open-addressing region whose
+// used part is sized per endpoint (2 x its record bound, so the records stay L2-resident).
 __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restrict__ Tlow,
                                                     const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
-                                                    const int32_t* __restrict__ light, int n_light,
-                                                    int* __restrict__ counter, C5Rec* __restrict__ wregions,
-                                                    int32_t* __restrict__ wlists, u64* __restrict__ C5) {
+                                                    const int32_t* __restrict__ light, const u32* __restrict__ lw,
+                                                    int n_light, int* __restrict__ counter,
+                                                    C5RecT<u32>* __restrict__ wregions, int32_t* __restrict__ wlists,
+                                                    u64* __restrict__ C5) {
   __shared__ int w_nL[C5_BT / 32], w_nJ[C5_BT / 32];
   __shared__ u64 w_tot[C5_BT / 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t gw = (size_t)blockIdx.x * (C5_BT / 32) + wib;
   WarpEng eng;
-  C5Hash loc;
+  C5Hash<C5RecT<u32>> loc;
   loc.R = wregions + gw * C5_WARP_CAP;
   loc.L = wlists + gw * 2 * C5_WARP_CAP;
   loc.nL = &w_nL[wib];
-  loc.mask = C5_WARP_CAP - 1;
   int32_t* J = loc.L + C5_WARP_CAP;
   for (;;) {
     int idx = 0;
@@ -403,6 +436,7 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
     idx = __shfl_sync(FULL_MASK, idx, 0);
     if (idx >= n_light) break;
     const int32_t l = light[idx];
+    loc.mask = pow2_at_least(2u * lw[idx], 64u) - 1;  // <= C5_WARP_CAP - 1
     if (lane == 0) { w_nL[wib] = 0; w_nJ[wib] = 0; w_tot[wib] = 0; }
     __syncwarp();
     c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &w_nJ[wib], &w_tot[wib], C5);
@@ -423,7 +457,7 @@ __global__ void __cluster_dims__(C5_CLUSTER, 1, 1) __launch_bounds__(1024)
   const int cid = blockIdx.x / C5_CLUSTER;
   const bool leader = cluster.block_rank() == 0 && threadIdx.x == 0;
   ClusterEng eng;
-  C5Dense loc;
+  C5Dense<C5Rec> loc;
   loc.R = dense + (size_t)cid * g.n;
   loc.L = dlists + (size_t)cid * 2 * g.n;
   loc.nL = &ctl[4 * cid + 0];

@@ -445,6 +445,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaMemcpyAsync(hm, d_mx, sizeof(hm), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     max_deg = hm[0]; max_out = hm[1];
+    if (max_deg >= (1 << 28)) {  // 5-cycle records pack Wn (<= d(l)) in 28 bits
+      set_error("maximum degree %d >= 2^28 is not supported", max_deg);
+      throw EvokeError{EVOKE_EINVAL};
+    }
     A.release(dk); A.release(dks); A.release(degc); A.release(tmp64);
   }
   A.release(ukeys);
@@ -621,7 +625,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* hslot = A.alloc<int32_t>(n);
     int* hcnt = A.alloc<int>(1, true);
     const int max_maps = (int)std::min<int64_t>(4096, std::max<int64_t>(0, (256ll << 20) / ((int64_t)n * 4)));
-    k_hub_slots<<<grid_for(n, B, SM), B, 0, C.st>>>(g, max_maps, hslot, hcnt);
+    int32_t* hubs = A.alloc<int32_t>(std::max(max_maps, 1));
+    k_hub_slots<<<grid_for(n, B, SM), B, 0, C.st>>>(g, max_maps, hslot, hubs, hcnt);
     int nmaps = 0;
     CK(cudaMemcpyAsync(&nmaps, hcnt, sizeof(int), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
@@ -629,7 +634,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* hpos = A.alloc<int32_t>((size_t)std::max(nmaps, 1) * n);
     if (nmaps > 0) {
       CK(cudaMemsetAsync(hpos, 0xff, sizeof(int32_t) * (size_t)nmaps * n, C.st));
-      k_hub_maps<<<std::min(nmaps * 4, 4 * SM), 256, 0, C.st>>>(g, hslot, hpos);
+      k_hub_maps<<<std::min(nmaps, 4 * SM), 256, 0, C.st>>>(g, hubs, nmaps, hpos);
     }
     C.launches += 2;
     PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e, hstar,
@@ -744,7 +749,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     u64* c5w = A.alloc<u64>(n);
     int* c5c = A.alloc<int>(8, true);
     u64* C5out = Fp(F_C5);
-    k_c5_items<<<warp_grid, B, 0, C.st>>>(g, si, ns, c5l, c5c, c5h, c5w, c5c + 1);
+    u32* c5lw = A.alloc<u32>(n);
+    k_c5_items<<<warp_grid, B, 0, C.st>>>(g, si, ns, c5l, c5lw, c5c, c5h, c5w, c5c + 1);
     C.launches++;
     int hc5[2];
     CK(cudaMemcpyAsync(hc5, c5c, sizeof(hc5), cudaMemcpyDeviceToHost, C.st));
@@ -757,9 +763,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       k_c5_heavy_w<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, c5c + 2);
       C.launches++;
       int32_t* hs = c5h;
+      u64* hkeys = nullptr;
       if (n5h > 1) {
         hs = A.alloc<int32_t>(n5h);
         u64* hk = A.alloc<u64>(n5h);
+        hkeys = hk;
         size_t tb = 0;
         CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c5w, hk, c5h, hs, n5h, 0, 64, C.st));
         void* t = A.alloc<char>(tb);
@@ -788,13 +796,24 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       }
       const int nrest = n5h - ngiant;
       if (nrest > 0) {
-        const int64_t per = (int64_t)n * (int64_t)(sizeof(C5Rec) + 8);
+        // u32 records when every remaining endpoint's work bound is < 2^32 (the list is sorted)
+        u64 wmax = 0;
+        CK(cudaMemcpyAsync(&wmax, (n5h > 1 ? hkeys : c5w) + ngiant, sizeof(u64), cudaMemcpyDeviceToHost, C.st));
+        CK(cudaStreamSynchronize(C.st));
+        const bool narrow = wmax < (1ull << 32);
+        const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
+        const int64_t per = (int64_t)n * (int64_t)(rec + 8);
         int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
-        C5Rec* dense = A.alloc<C5Rec>((size_t)hg * n, true);
+        char* dense = A.alloc<char>((size_t)hg * n * rec, true);
         int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
         const int32_t* hsr = hs + ngiant;
         jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
-          k_c5_heavy<<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3, dense, dl, C5out);
+          if (narrow)
+            k_c5_heavy<u32><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
+                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out);
+          else
+            k_c5_heavy<u64><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
+                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out);
           C.launches++;
         }});
       }
@@ -804,10 +823,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_light, C5_BT, 0));
       const int lg = std::max(1, std::min(bps, 4)) * SM;
       const size_t nw = (size_t)lg * (C5_BT / 32);
-      C5Rec* reg = A.alloc<C5Rec>(nw * C5_WARP_CAP, true);
+      C5RecT<u32>* reg = A.alloc<C5RecT<u32>>(nw * C5_WARP_CAP, true);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
-        k_c5_light<<<lg, C5_BT, 0, st>>>(g, Tlow, Tmid, Thigh, c5l, n5l, c5c + 4, reg, wl, C5out);
+        k_c5_light<<<lg, C5_BT, 0, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out);
         C.launches++;
       }});
     }

@@ -58,6 +58,7 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
 #define PAIR_LCAP 512            // long-part queue capacity per source pass
 #define PAIR_ILP 4               // independent wedge chains per lane in the pass-2 walk
+#define PAIR_DIAM_DEFER 256      // diamond list longer than this: queued by the CTA engine
 #define PAIR_HUBMAP_MIN 1024     // vertices of degree >= this get a position map (budgeted)
 #define EMPTY_KEY (-1)
 
@@ -310,9 +311,12 @@ __device__ __forceinline__ void pass2_wedge(const DGraph& g, const u32* __restri
 // chord once); the diamond lists tri(v,w) of the (up to 32) chords of the warp are then
 // flattened over the lanes with a second warp_flat.  PASS 2 adds W(u,x)-2 (x > u) into
 // acc[owner] (per-warp shared accumulators, one per item owner).  Warp-uniform call.
-template <int PASS, typename Tab>
+struct NoDefer {
+  __device__ __forceinline__ bool operator()(int64_t, int32_t, bool) const { return false; }
+};
+template <int PASS, typename Tab, typename Defer = NoDefer>
 __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool valid, int32_t v, int64_t fo, bool vlo,
-                                            int k, int owner, Tab& tab, u64* acc) {
+                                            int k, int owner, Tab& tab, u64* acc, Defer defer = Defer()) {
   int64_t f0 = 0;
   int len2 = 0;
   if (valid) {
@@ -321,6 +325,8 @@ __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool val
       const int32_t evw = vlo ? g.fe1[r] : g.fe2[r];
       f0 = g.foff[evw];
       len2 = (int)(g.foff[evw + 1] - f0);
+      // a long diamond list goes to the CTA's queue (chunked over whole warps) instead
+      if (len2 > PAIR_DIAM_DEFER && defer(r, v, vlo)) len2 = 0;
     }
   }
   int cur = -1;
@@ -466,17 +472,38 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
 // or chord parts longer than PAIR_LONG go to a shared queue; they are then cut into
 // PAIR_CHUNK-element chunks that whole warps take from a second counter.  Every element is
 // visited exactly once; no per-element search.
-enum { PK_WEDGE = 0, PK_CHORD = 1 };
+enum { PK_WEDGE = 0, PK_CHORD = 1, PK_DIAM = 2 };
 struct EngShared {
   int next;
   int qn;
   int next_chunk;
   int nchunks;
-  int64_t qslot[PAIR_LCAP];   // item slot s_uv
+  int64_t qslot[PAIR_LCAP];   // item slot s_uv (wedge / chord parts) or chord entry r (diamond)
+  int32_t qv[PAIR_LCAP];      // v (diamond parts)
   int8_t qkind[PAIR_LCAP];
+  int8_t qvlo[PAIR_LCAP];
   int32_t lc0[PAIR_LCAP + 1];
   u64 acc[PAIR_HBT / 32][32];  // per-warp theta64 accumulators (chords_step)
 };
+struct CtaDefer {
+  EngShared* E;
+  __device__ __forceinline__ bool operator()(int64_t r, int32_t v, bool vlo) const {
+    const int q = atomicAdd(&E->qn, 1);
+    if (q >= PAIR_LCAP) return false;
+    E->qslot[q] = r; E->qv[q] = v; E->qkind[q] = PK_DIAM; E->qvlo[q] = vlo;
+    return true;
+  }
+};
+__device__ __forceinline__ int part_len(const DGraph& g, const EngShared& E, int q, int32_t hs) {
+  const int kind = E.qkind[q];
+  if (kind == PK_DIAM) {
+    const int64_t r = E.qslot[q];
+    const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
+    return (int)(g.foff[evw + 1] - g.foff[evw]);
+  }
+  const PairItem it = pair_item(g, E.qslot[q], hs);
+  return kind == PK_WEDGE ? it.dv : it.tv;
+}
 
 template <int PASS, typename Tab>
 __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs, int64_t r0, int64_t r1,
@@ -487,9 +514,8 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
   acc[lane] = 0;
   __syncthreads();
   const int64_t nitems = r1 - r0;
-  // items per warp grab: spread few items over all warps, 32 when there are many
-  const int grab = (int)min((int64_t)32, max((int64_t)1, (nitems + (int64_t)(blockDim.x >> 5) - 1) /
-                                                          (int64_t)(blockDim.x >> 5)));
+  // items per warp grab: about four grabs per warp (dynamic balance), at most 32
+  const int grab = (int)min((int64_t)32, max((int64_t)1, nitems / (4 * (int64_t)(blockDim.x >> 5))));
   for (;;) {
     int base = 0;
     if (lane == 0) base = atomicAdd(&E.next, grab);
@@ -529,7 +555,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
       const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
       const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc);
+      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc, CtaDefer{&E});
     });
     __syncwarp();
     if (PASS == 2) {
@@ -539,18 +565,17 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     }
   }
   __syncthreads();
-  // queued long parts, cut in chunks
-  const int nq = min(E.qn, PAIR_LCAP);
-  if (nq == 0) return;  // uniform (E.qn read after a barrier)
+  // rounds over the queued parts, cut in chunks (chord chunks may queue diamond lists)
+  int qb = 0;
+  for (;;) {
+  const int qe = min(E.qn, PAIR_LCAP);
+  if (qb >= qe) break;  // uniform (E.qn read after a barrier)
+  const int nq = qe - qb;
   if (threadIdx.x < 32) {
     int carry = 0;
     for (int q0 = 0; q0 < nq; q0 += 32) {
       const int q = q0 + lane;
-      int nc = 0;
-      if (q < nq) {
-        const PairItem it = pair_item(g, E.qslot[q], hs);
-        nc = ((E.qkind[q] == PK_WEDGE ? it.dv : it.tv) + PAIR_CHUNK - 1) / PAIR_CHUNK;
-      }
+      const int nc = (q < nq) ? (part_len(g, E, qb + q, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
       int incl = nc;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -569,21 +594,41 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     if (lane == 0) c = atomicAdd(&E.next_chunk, 1);
     c = __shfl_sync(FULL_MASK, c, 0);
     if (c >= nchunks) break;
-    int q = 0;
+    int ql = 0;
     if (lane == 0) {
       int lo = 0, hi = nq;  // largest part with lc0 <= c
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (E.lc0[mid] <= c) lo = mid; else hi = mid;
       }
-      q = lo;
+      ql = lo;
     }
-    q = __shfl_sync(FULL_MASK, q, 0);
+    ql = __shfl_sync(FULL_MASK, ql, 0);
+    const int q = qb + ql;
     const int kind = E.qkind[q];
-    const int k0 = (c - E.lc0[q]) * PAIR_CHUNK;
-    const PairItem it = pair_item(g, E.qslot[q], hs);
+    const int k0 = (c - E.lc0[ql]) * PAIR_CHUNK;
     PairAcc A;
     A.zero();
+    if (kind == PK_DIAM) {
+      const int64_t r = E.qslot[q];
+      const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
+      const int64_t f0 = g.foff[evw];
+      const int k1 = min((int)(g.foff[evw + 1] - f0), k0 + PAIR_CHUNK);
+      for (int k = k0 + lane; k < k1; k += 32) {
+        const int32_t x = g.fx[f0 + k];
+        if (PASS == 1) {
+          if (x != u) tab.add_d(x);
+        } else {
+          if (x > u) A.c64 += tab.get_w(x) - 2ull;
+        }
+      }
+      if (PASS == 2) {
+        A.c64 = warp_sum(A.c64);
+        if (lane == 0 && A.c64) atomicAdd(&o.R64[E.qv[q]], A.c64);
+      }
+      continue;
+    }
+    const PairItem it = pair_item(g, E.qslot[q], hs);
     if (kind == PK_WEDGE) {
       // PAIR_CHUNK / 32 elements per lane, all loads issued before the table updates
       constexpr int U = PAIR_CHUNK / 32;
@@ -636,7 +681,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       const int k1 = min(it.tv, k0 + PAIR_CHUNK);
       for (int i = 0; i < PAIR_CHUNK / 32; i++) {
         const int k = k0 + lane + 32 * i;
-        chords_step<PASS>(g, u, k < k1, it.v, it.fo, it.vlo, k, 0, tab, acc);
+        chords_step<PASS>(g, u, k < k1, it.v, it.fo, it.vlo, k, 0, tab, acc, CtaDefer{&E});
       }
       __syncwarp();
       if (PASS == 2 && lane == 0) {
@@ -651,6 +696,8 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     }
   }
   __syncthreads();
+  qb = qe;
+  }
 }
 
 // ---- the h* contribution ----------------------------------------------------------------
@@ -734,22 +781,25 @@ __device__ __forceinline__ void hstar_term(const DGraph& g, const u32* __restric
 }
 
 // position maps of the hubs (d >= PAIR_HUBMAP_MIN) up to max_slots rows
-__global__ void k_hub_slots(DGraph g, int max_slots, int32_t* __restrict__ slot, int* __restrict__ cnt) {
+__global__ void k_hub_slots(DGraph g, int max_slots, int32_t* __restrict__ slot, int32_t* __restrict__ hubs,
+                            int* __restrict__ cnt) {
   for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
     int32_t sl = -1;
     if (dg_deg(g, v) >= PAIR_HUBMAP_MIN) {
       const int q = atomicAdd(cnt, 1);
-      if (q < max_slots) sl = q;
+      if (q < max_slots) {
+        sl = q;
+        hubs[q] = v;
+      }
     }
     slot[v] = sl;
   }
 }
-__global__ void k_hub_maps(DGraph g, const int32_t* __restrict__ slot, int32_t* __restrict__ pos) {
-  // block per hub-candidate vertex range: grid-stride over vertices, block-stride over lists
-  for (int32_t v = blockIdx.x; v < g.n; v += gridDim.x) {
-    const int32_t sl = slot[v];
-    if (sl < 0) continue;
-    int32_t* row = pos + (size_t)sl * (size_t)g.n;
+// block per hub: row[x] = position of x in N(hub)
+__global__ void k_hub_maps(DGraph g, const int32_t* __restrict__ hubs, int nhubs, int32_t* __restrict__ pos) {
+  for (int q = blockIdx.x; q < nhubs; q += gridDim.x) {
+    const int32_t v = hubs[q];
+    int32_t* row = pos + (size_t)q * (size_t)g.n;
     const int64_t b = g.rp[v], e = g.rp[v + 1];
     for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)(k - b);
   }

@@ -203,7 +203,7 @@ __device__ void cta_lists(int n_items, ListEng& E, Info info, Elem elem, Flush f
   const int nw = blockDim.x >> 5;
   if (threadIdx.x == 0) { E.next = 0; E.qn = 0; E.next_chunk = 0; }
   __syncthreads();
-  const int grab = max(1, min(32, (n_items + nw - 1) / nw));
+  const int grab = max(1, min(32, n_items / (4 * nw)));  // ~4 grabs per warp: dynamic balance
   for (;;) {
     int b = 0;
     if (lane == 0) b = atomicAdd(&E.next, grab);
