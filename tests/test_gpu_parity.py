@@ -282,3 +282,23 @@ def test_config3_rows_and_invariants(pkg):
     _invariants(g, out, check_cliques=False)
     done = _sampled_rows(g, out, 100, 3, cap=20_000_000)
     assert done >= 3, done
+
+
+def test_config4_invariants_and_low_degree_core(pkg):
+    """Holme-Kim n = 2e6, ~16M edges (BASELINE configs[3]): whole-matrix invariants (orbit 0
+    = degree, per-pattern consistency mod 2^64, clique totals from the independent CPU
+    counter) on the full graph, and the full matrix bit-exact against the ESU oracle on the
+    subgraph induced by the vertices of degree <= 11 (same generator, ~1.1M edges, n = 2e6).
+    Rooted rows are not sampled here: every vertex of this graph (degree >= 8 by
+    construction) reaches a hub within two steps, so no rooted enumeration fits a cap."""
+    g = graphgen.config(4)
+    out = pkg.evoke_orbits_edges(g.n, g.edges)
+    _invariants(g, out)
+    del out
+    e = np.unique(np.sort(g.edges.astype(np.int64), axis=1), axis=0)
+    e = e[e[:, 0] != e[:, 1]]
+    deg = np.bincount(e.ravel(), minlength=g.n)
+    keep = deg <= 11
+    e = e[keep[e[:, 0]] & keep[e[:, 1]]].astype(np.int32)
+    assert e.shape[0] > 1_000_000
+    _assert_equal(pkg.evoke_orbits_edges(g.n, e), oracle.orbits(g.n, e), "config4 core")
