@@ -389,8 +389,14 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
                                                     const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                     const int32_t* __restrict__ heavy, int n_heavy,
                                                     int* __restrict__ counter, C5RecT<V>* __restrict__ dense,
-                                                    int32_t* __restrict__ dlists, u64* __restrict__ C5) {
+                                                    int32_t* __restrict__ dlists, u64* __restrict__ C5,
+                                                    int32_t* __restrict__ qmem) {
   __shared__ ListEng E;
+  if (threadIdx.x == 0) {
+    E.qcap = g.max_deg;
+    E.qi = qmem + (size_t)blockIdx.x * (2 * (size_t)g.max_deg + 1);
+    E.lc0 = E.qi + g.max_deg;
+  }
   __shared__ int s_idx, s_nL, s_nJ;
   __shared__ u64 s_tot;
   CtaEng eng{&E};

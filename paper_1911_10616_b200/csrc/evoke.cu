@@ -657,8 +657,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(PT_G64);
       const int cnt = ht[PT_G64];
+      const int qcap = 2 * g.max_deg + 65536;
+      char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
       jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
-        k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po);
+        k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap);
         C.launches++;
       }});
     }
@@ -670,11 +672,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(tier);
       const int cnt = ht[tier];
+      const int qcap = 2 * g.max_deg + 65536;
+      char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
       jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
         if (tier == PT_G32S)
-          k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po);
+          k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap);
         else
-          k_pairs_heavy<u32, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po);
+          k_pairs_heavy<u32, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap);
         C.launches++;
       }});
     }
@@ -687,8 +691,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const int32_t* pli = plist(PT_LIGHT);
       const int nmid = ht[PT_MID], nli = ht[PT_LIGHT];
       const int grid = std::max(bps, 1) * SM;
+      const int qcap = 2 * PAIR_MID_MAX + 16384;
+      char* qmem = A.alloc<char>((size_t)grid * eng_queue_bytes(qcap));
       jobs.push_back({P_PAIR, 3, [=, &C](cudaStream_t st) {
-        k_pairs_main<<<grid, PAIR_BT, PAIR_SMEM, st>>>(g, Te, pm, nmid, pli, nli, pest, counters, po);
+        k_pairs_main<<<grid, PAIR_BT, PAIR_SMEM, st>>>(g, Te, pm, nmid, pli, nli, pest, counters, po, qmem, qcap);
         C.launches++;
       }});
     }
@@ -806,14 +812,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
         char* dense = A.alloc<char>((size_t)hg * n * rec, true);
         int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
+        int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
         const int32_t* hsr = hs + ngiant;
         jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
           if (narrow)
             k_c5_heavy<u32><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out);
+                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq);
           else
             k_c5_heavy<u64><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out);
+                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out, lq);
           C.launches++;
         }});
       }

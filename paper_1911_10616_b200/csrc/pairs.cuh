@@ -56,7 +56,6 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 
 #define PAIR_LONG 64             // item part longer than this: chunked, shared queue
 #define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
-#define PAIR_LCAP 512            // long-part queue capacity per source pass
 #define PAIR_ILP 4               // independent wedge chains per lane in the pass-2 walk
 #define PAIR_DIAM_DEFER 256      // diamond list longer than this: queued by the CTA engine
 #define PAIR_HUBMAP_MIN 1024     // vertices of degree >= this get a position map (budgeted)
@@ -466,6 +465,17 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
   }
 }
 
+// developer phase timers (EVOKE_DEBUG): SM cycles per phase summed over sources, CTA tiers
+__device__ unsigned long long g_pair_phase[2][8];
+#define PAIR_PHASE(i)                                                                     \
+  do {                                                                                    \
+    if (threadIdx.x == 0) {                                                               \
+      const long long t_ = clock64();                                                     \
+      atomicAdd(&g_pair_phase[Tab::kDense ? 1 : 0][i], (unsigned long long)(t_ - t_prev)); \
+      t_prev = t_;                                                                        \
+    }                                                                                     \
+  } while (0)
+
 // ---- CTA engine ------------------------------------------------------------------------
 // Sweep: warps take a few items at a time from a shared counter and flatten their short
 // parts over the lanes (chords and their diamond lists on two levels, chords_step).  Wedge
@@ -473,35 +483,57 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
 // PAIR_CHUNK-element chunks that whole warps take from a second counter.  Every element is
 // visited exactly once; no per-element search.
 enum { PK_WEDGE = 0, PK_CHORD = 1, PK_DIAM = 2 };
+// The queue of long parts lives in global memory (one region per CTA, capacity qcap): a hub
+// source can have thousands of long parts, and an overflowing queue would push them back
+// onto single warps.
+struct EngQueue {
+  int64_t* qslot;   // item slot s_uv (wedge / chord parts) or chord entry r (diamond)
+  int32_t* qv;      // v (diamond parts)
+  int8_t* qkind;
+  int8_t* qvlo;
+  int32_t* lc0;     // first chunk of each part of the current round (+1 entry)
+  int qcap;
+};
 struct EngShared {
   int next;
   int qn;
   int next_chunk;
   int nchunks;
-  int64_t qslot[PAIR_LCAP];   // item slot s_uv (wedge / chord parts) or chord entry r (diamond)
-  int32_t qv[PAIR_LCAP];      // v (diamond parts)
-  int8_t qkind[PAIR_LCAP];
-  int8_t qvlo[PAIR_LCAP];
-  int32_t lc0[PAIR_LCAP + 1];
+  EngQueue Q;
   u64 acc[PAIR_HBT / 32][32];  // per-warp theta64 accumulators (chords_step)
 };
+// bytes of one queue region of capacity qcap
+__host__ __device__ __forceinline__ size_t eng_queue_bytes(int qcap) {
+  const size_t b = (size_t)qcap * (8 + 4 + 1 + 1) + (size_t)(qcap + 1) * 4 + 64;
+  return (b + 255) & ~(size_t)255;  // every region starts 256-byte aligned (int64 slots first)
+}
+__device__ __forceinline__ EngQueue eng_queue_at(char* base, int qcap) {
+  EngQueue q;
+  q.qslot = reinterpret_cast<int64_t*>(base);
+  q.qv = reinterpret_cast<int32_t*>(base + (size_t)qcap * 8);
+  q.lc0 = q.qv + qcap;
+  q.qkind = reinterpret_cast<int8_t*>(q.lc0 + qcap + 1);
+  q.qvlo = q.qkind + qcap;
+  q.qcap = qcap;
+  return q;
+}
 struct CtaDefer {
   EngShared* E;
   __device__ __forceinline__ bool operator()(int64_t r, int32_t v, bool vlo) const {
     const int q = atomicAdd(&E->qn, 1);
-    if (q >= PAIR_LCAP) return false;
-    E->qslot[q] = r; E->qv[q] = v; E->qkind[q] = PK_DIAM; E->qvlo[q] = vlo;
+    if (q >= E->Q.qcap) return false;
+    E->Q.qslot[q] = r; E->Q.qv[q] = v; E->Q.qkind[q] = PK_DIAM; E->Q.qvlo[q] = vlo;
     return true;
   }
 };
-__device__ __forceinline__ int part_len(const DGraph& g, const EngShared& E, int q, int32_t hs) {
-  const int kind = E.qkind[q];
+__device__ __forceinline__ int part_len(const DGraph& g, const EngQueue& Q, int q, int32_t hs) {
+  const int kind = Q.qkind[q];
   if (kind == PK_DIAM) {
-    const int64_t r = E.qslot[q];
-    const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
+    const int64_t r = Q.qslot[q];
+    const int32_t evw = Q.qvlo[q] ? g.fe1[r] : g.fe2[r];
     return (int)(g.foff[evw + 1] - g.foff[evw]);
   }
-  const PairItem it = pair_item(g, E.qslot[q], hs);
+  const PairItem it = pair_item(g, Q.qslot[q], hs);
   return kind == PK_WEDGE ? it.dv : it.tv;
 }
 
@@ -510,6 +542,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
                          Tab& tab, EngShared& E, u64& s51, const PairOut& o) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   u64* acc = E.acc[wib];
+  long long t_prev = clock64();
   if (threadIdx.x == 0) { E.next = 0; E.qn = 0; }
   acc[lane] = 0;
   __syncthreads();
@@ -528,11 +561,11 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     // defer long parts to the queue (if it has room)
     if (it.dv > PAIR_LONG) {
       const int q = atomicAdd(&E.qn, 1);
-      if (q < PAIR_LCAP) { E.qslot[q] = r0 + base + lane; E.qkind[q] = PK_WEDGE; it.dv = 0; }
+      if (q < E.Q.qcap) { E.Q.qslot[q] = r0 + base + lane; E.Q.qkind[q] = PK_WEDGE; it.dv = 0; }
     }
     if (it.tv > PAIR_LONG) {
       const int q = atomicAdd(&E.qn, 1);
-      if (q < PAIR_LCAP) { E.qslot[q] = r0 + base + lane; E.qkind[q] = PK_CHORD; it.tv = 0; }
+      if (q < E.Q.qcap) { E.Q.qslot[q] = r0 + base + lane; E.Q.qkind[q] = PK_CHORD; it.tv = 0; }
     }
     PairAcc A;
     A.zero();
@@ -565,27 +598,52 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     }
   }
   __syncthreads();
+  PAIR_PHASE(5);
   // rounds over the queued parts, cut in chunks (chord chunks may queue diamond lists)
   int qb = 0;
   for (;;) {
-  const int qe = min(E.qn, PAIR_LCAP);
+  const int qe = min(E.qn, E.Q.qcap);
   if (qb >= qe) break;  // uniform (E.qn read after a barrier)
   const int nq = qe - qb;
-  if (threadIdx.x < 32) {
-    int carry = 0;
-    for (int q0 = 0; q0 < nq; q0 += 32) {
-      const int q = q0 + lane;
-      const int nc = (q < nq) ? (part_len(g, E, qb + q, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
-      int incl = nc;
+  {
+    // chunk table of the round: CTA-wide exclusive scan of the parts' chunk counts
+    typedef cub::BlockScan<int, PAIR_HBT> CScan;
+    __shared__ typename CScan::TempStorage cscan;
+    __shared__ int s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int q0 = 0; q0 < nq; q0 += blockDim.x) {
+      const int q = q0 + threadIdx.x;
+      const int nc = (q < nq) ? (part_len(g, E.Q, qb + q, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
+      int ex = 0, tot = 0;
+      if (blockDim.x == PAIR_HBT) {
+        CScan(cscan).ExclusiveSum(nc, ex, tot);
+      } else {
+        // smaller CTA: warp scans chained through shared memory
+        __shared__ int wsum[PAIR_HBT / 32];
+        int incl = nc;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(FULL_MASK, incl, d);
-        if (lane >= d) incl += y;
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(FULL_MASK, incl, d);
+          if (lane >= d) incl += y;
+        }
+        if (lane == 31) wsum[wib] = incl;
+        __syncthreads();
+        int before = 0;
+        tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+          if (w < wib) before += wsum[w];
+          tot += wsum[w];
+        }
+        ex = before + incl - nc;
+        __syncthreads();
       }
-      if (q < nq) E.lc0[q] = carry + incl - nc;
-      carry += __shfl_sync(FULL_MASK, incl, 31);
+      if (q < nq) E.Q.lc0[q] = s_carry + ex;
+      __syncthreads();
+      if (threadIdx.x == 0) s_carry += tot;
+      __syncthreads();
     }
-    if (lane == 0) { E.lc0[nq] = carry; E.nchunks = carry; E.next_chunk = 0; }
+    if (threadIdx.x == 0) { E.Q.lc0[nq] = s_carry; E.nchunks = s_carry; E.next_chunk = 0; }
   }
   __syncthreads();
   const int nchunks = E.nchunks;
@@ -599,19 +657,19 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       int lo = 0, hi = nq;  // largest part with lc0 <= c
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (E.lc0[mid] <= c) lo = mid; else hi = mid;
+        if (E.Q.lc0[mid] <= c) lo = mid; else hi = mid;
       }
       ql = lo;
     }
     ql = __shfl_sync(FULL_MASK, ql, 0);
     const int q = qb + ql;
-    const int kind = E.qkind[q];
-    const int k0 = (c - E.lc0[ql]) * PAIR_CHUNK;
+    const int kind = E.Q.qkind[q];
+    const int k0 = (c - E.Q.lc0[ql]) * PAIR_CHUNK;
     PairAcc A;
     A.zero();
     if (kind == PK_DIAM) {
-      const int64_t r = E.qslot[q];
-      const int32_t evw = E.qvlo[q] ? g.fe1[r] : g.fe2[r];
+      const int64_t r = E.Q.qslot[q];
+      const int32_t evw = E.Q.qvlo[q] ? g.fe1[r] : g.fe2[r];
       const int64_t f0 = g.foff[evw];
       const int k1 = min((int)(g.foff[evw + 1] - f0), k0 + PAIR_CHUNK);
       for (int k = k0 + lane; k < k1; k += 32) {
@@ -624,11 +682,11 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       }
       if (PASS == 2) {
         A.c64 = warp_sum(A.c64);
-        if (lane == 0 && A.c64) atomicAdd(&o.R64[E.qv[q]], A.c64);
+        if (lane == 0 && A.c64) atomicAdd(&o.R64[E.Q.qv[q]], A.c64);
       }
       continue;
     }
-    const PairItem it = pair_item(g, E.qslot[q], hs);
+    const PairItem it = pair_item(g, E.Q.qslot[q], hs);
     if (kind == PK_WEDGE) {
       // PAIR_CHUNK / 32 elements per lane, all loads issued before the table updates
       constexpr int U = PAIR_CHUNK / 32;
@@ -698,6 +756,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
   __syncthreads();
   qb = qe;
   }
+  PAIR_PHASE(6);
 }
 
 // ---- the h* contribution ----------------------------------------------------------------
@@ -827,17 +886,6 @@ __device__ __forceinline__ int32_t edge_of(const DGraph& g, int32_t u, int32_t v
   return g.eid[p];
 }
 
-// developer phase timers (EVOKE_DEBUG): SM cycles per phase summed over sources, CTA tiers
-__device__ unsigned long long g_pair_phase[2][8];
-#define PAIR_PHASE(i)                                                                     \
-  do {                                                                                    \
-    if (threadIdx.x == 0) {                                                               \
-      const long long t_ = clock64();                                                     \
-      atomicAdd(&g_pair_phase[Tab::kDense ? 1 : 0][i], (unsigned long long)(t_ - t_prev)); \
-      t_prev = t_;                                                                        \
-    }                                                                                     \
-  } while (0)
-
 // ---- one source on a CTA (mid and heavy tiers) ------------------------------------------
 template <int BT, typename Tab>
 __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int32_t u, Tab& tab, EngShared& E,
@@ -934,12 +982,13 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
                                                         const int32_t* __restrict__ mid, int n_mid,
                                                         const int32_t* __restrict__ light, int n_light,
                                                         const u32* __restrict__ est, int* __restrict__ counters,
-                                                        PairOut o) {
+                                                        PairOut o, char* __restrict__ qmem, int qcap) {
   extern __shared__ int32_t sh_pairs[];
   __shared__ EngShared E;
   __shared__ u64 red[8];
   __shared__ int s_idx;
   if (threadIdx.x < 8) red[threadIdx.x] = 0;
+  if (threadIdx.x == 0) E.Q = eng_queue_at(qmem + (size_t)blockIdx.x * eng_queue_bytes(qcap), qcap);
   {
     SharedPackedHash tab;
     tab.keys = sh_pairs;
@@ -986,10 +1035,12 @@ template <typename Word, bool SCAN>
 __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* __restrict__ Te,
                                                           const int32_t* __restrict__ srcs, int nsrc,
                                                           int* __restrict__ counter, Word* __restrict__ tabs,
-                                                          int32_t* __restrict__ lists, PairOut o) {
+                                                          int32_t* __restrict__ lists, PairOut o,
+                                                          char* __restrict__ qmem, int qcap) {
   __shared__ EngShared E;
   __shared__ u64 red[8];
   __shared__ int s_idx, s_ntouch;
+  if (threadIdx.x == 0) E.Q = eng_queue_at(qmem + (size_t)blockIdx.x * eng_queue_bytes(qcap), qcap);
   GlobalDense<Word, SCAN> tab;
   constexpr int PER = GlobalDense<Word, SCAN>::PER;
   const size_t stride = (size_t)((g.n + PER - 1) / PER * PER);  // 16-byte aligned rows

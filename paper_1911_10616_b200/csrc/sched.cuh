@@ -158,7 +158,6 @@ __device__ __forceinline__ void warp_append(bool pred, int32_t val, int32_t* lis
 // ---------------------------------------------------------------------------------
 #define LE_LONG 32      // item longer than this: queued and cut in chunks (CTA engine)
 #define LE_CHUNK 256    // elements per chunk (8 per lane)
-#define LE_QCAP 512     // queue capacity (overflowing items are walked by the sweep warp)
 
 // warp engine: the warp walks all items, 32 at a time, flattened over the lanes
 template <typename Info, typename Elem, typename Flush>
@@ -190,9 +189,42 @@ struct ListEng {
   int qn;
   int next_chunk;
   int nchunks;
-  int32_t qi[LE_QCAP];
-  int32_t lc0[LE_QCAP + 1];
+  int32_t* qi;   // queued items (global memory, one region per CTA)
+  int32_t* lc0;  // first chunk of each queued item (+1 entry)
+  int qcap;
 };
+
+// CTA-wide exclusive scan of one int per thread (any blockDim that is a multiple of 32,
+// <= 1024); returns the exclusive prefix, *total gets the sum.  Contains barriers.
+__device__ __forceinline__ int block_exclusive_scan(int x, int* total) {
+  __shared__ int ws[32];
+  __shared__ int wtot;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) ws[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < nw ? ws[lane] : 0;
+    int iv = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(FULL_MASK, iv, d);
+      if (lane >= d) iv += y;
+    }
+    if (lane < nw) ws[lane] = iv - v;  // exclusive prefix of warp sums
+    if (lane == 31) wtot = iv;         // total (lane 31 holds the full sum)
+  }
+  __syncthreads();
+  const int ex = ws[w] + incl - x;
+  *total = wtot;
+  __syncthreads();
+  return ex;
+}
 
 // CTA engine: warps take items (a few per grab when items are few, up to 32), walk
 // short ones with warp_flat and queue long ones; queued items are then cut into
@@ -215,7 +247,7 @@ __device__ void cta_lists(int n_items, ListEng& E, Info info, Elem elem, Flush f
     if (lane < grab && i < n_items) info(i, base, len);
     if (len > LE_LONG) {
       const int q = atomicAdd(&E.qn, 1);
-      if (q < LE_QCAP) { E.qi[q] = i; len = 0; }
+      if (q < E.qcap) { E.qi[q] = i; len = 0; }
     }
     int cur = -1;
     u64 acc = 0;
@@ -232,12 +264,14 @@ __device__ void cta_lists(int n_items, ListEng& E, Info info, Elem elem, Flush f
     if (cur >= 0 && acc) flush(b + cur, acc);
   }
   __syncthreads();
-  const int nq = min(E.qn, LE_QCAP);
+  const int nq = min(E.qn, E.qcap);
   if (nq == 0) return;  // uniform
-  if (threadIdx.x < 32) {
-    int carry = 0;
-    for (int q0 = 0; q0 < nq; q0 += 32) {
-      const int q = q0 + lane;
+  {
+    __shared__ int s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int q0 = 0; q0 < nq; q0 += blockDim.x) {
+      const int q = q0 + threadIdx.x;
       int nc = 0;
       if (q < nq) {
         int64_t base;
@@ -245,16 +279,14 @@ __device__ void cta_lists(int n_items, ListEng& E, Info info, Elem elem, Flush f
         info(E.qi[q], base, len);
         nc = (len + LE_CHUNK - 1) / LE_CHUNK;
       }
-      int incl = nc;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(FULL_MASK, incl, d);
-        if (lane >= d) incl += y;
-      }
-      if (q < nq) E.lc0[q] = carry + incl - nc;
-      carry += __shfl_sync(FULL_MASK, incl, 31);
+      int tot = 0;
+      const int ex = block_exclusive_scan(nc, &tot);
+      if (q < nq) E.lc0[q] = s_carry + ex;
+      __syncthreads();
+      if (threadIdx.x == 0) s_carry += tot;
+      __syncthreads();
     }
-    if (lane == 0) { E.lc0[nq] = carry; E.nchunks = carry; }
+    if (threadIdx.x == 0) { E.lc0[nq] = s_carry; E.nchunks = s_carry; }
   }
   __syncthreads();
   const int nchunks = E.nchunks;
