@@ -856,6 +856,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaEventRecord(C.pev[i][1], st));
   }
   for (size_t i = 0; i < jobs.size(); i++) CK(cudaStreamWaitEvent(C.st, C.pev[i][1], 0));
+  if (getenv("EVOKE_DEBUG")) {
+    unsigned long long ph[2][8];
+    CK(cudaStreamSynchronize(C.st));
+    CK(cudaMemcpyFromSymbol(ph, g_pair_phase, sizeof(ph)));
+    for (int t = 0; t < 2; t++)
+      fprintf(stderr, "[evoke] pair %s phases (Mcycles): pass1 %.1f hstar %.1f terms %.1f pass2 %.1f tail %.1f"
+              " | sweeps %.1f queue-rounds %.1f\n",
+              t ? "dense" : "mid", ph[t][0] / 1e6, ph[t][1] / 1e6, ph[t][2] / 1e6, ph[t][3] / 1e6, ph[t][4] / 1e6,
+              ph[t][5] / 1e6, ph[t][6] / 1e6);
+    unsigned long long z[2][8] = {};
+    CK(cudaMemcpyToSymbol(g_pair_phase, z, sizeof(z)));
+  }
   C.njobs = (int)jobs.size();
   for (size_t i = 0; i < jobs.size(); i++) C.job_pass[i] = jobs[i].pass;
 

@@ -559,11 +559,12 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     if (have) it = pair_item(g, r0 + base + lane, hs);
     else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
     // defer long parts to the queue (if it has room)
-    if (it.dv > PAIR_LONG) {
+    const int long_min = PAIR_LONG;
+    if (it.dv > long_min) {
       const int q = atomicAdd(&E.qn, 1);
       if (q < E.Q.qcap) { E.Q.qslot[q] = r0 + base + lane; E.Q.qkind[q] = PK_WEDGE; it.dv = 0; }
     }
-    if (it.tv > PAIR_LONG) {
+    if (it.tv > long_min) {
       const int q = atomicAdd(&E.qn, 1);
       if (q < E.Q.qcap) { E.Q.qslot[q] = r0 + base + lane; E.Q.qkind[q] = PK_CHORD; it.tv = 0; }
     }
@@ -828,15 +829,43 @@ __device__ __forceinline__ void hstar_map(const DGraph& g, const u32* __restrict
   });
 }
 
-// the h* term by the cheapest available way
+// The h* term by the cheapest available way, fused with the per-pair terms when the table
+// is swept anyway (map / key search): returns true when a8..a63 were already added.
 template <typename Tab>
-__device__ __forceinline__ void hstar_term(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
-                                           const PairOut& o, Tab& tab, int tid, int nthr, u64 nkeys_bound,
-                                           PairAcc& H, u64& s51) {
+__device__ __forceinline__ bool hstar_and_terms(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
+                                                const PairOut& o, Tab& tab, int tid, int nthr, u64 nkeys_bound,
+                                                PairAcc& H, u64& s51, u64& a8, u64& a36, u64& a50, u64& a63) {
+  if (hs < 0) return false;
   const int32_t slot = o.hub_slot[hs];
-  if (slot >= 0) hstar_map(g, Te, u, hs, o.hub_pos + (size_t)slot * (size_t)g.n, tab, tid, nthr, H, s51);
-  else if (Tab::kDense || (u64)dg_deg(g, hs) <= 12ull * nkeys_bound) hstar_walk(g, Te, u, hs, tab, tid, nthr, H, s51);
-  else hstar_search(g, Te, u, hs, tab, tid, nthr, H, s51);
+  const bool walk = Tab::kDense || (slot < 0 && (u64)dg_deg(g, hs) <= 12ull * nkeys_bound);
+  if (walk) {
+    hstar_walk(g, Te, u, hs, tab, tid, nthr, H, s51);
+    return false;
+  }
+  const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
+  const int32_t* pmap = slot >= 0 ? o.hub_pos + (size_t)slot * (size_t)g.n : nullptr;
+  tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
+    int64_t p = -1;
+    if (pmap) {
+      const int32_t k = pmap[x];
+      if (k >= 0) p = hb + k;
+    } else {
+      const int64_t q = lower_bound_dev<int32_t>(g.ci, hb, he, x);
+      if (q < he && g.ci[q] == x) p = q;
+    }
+    if (p >= 0) {
+      w += 1;
+      H.c5 += w - 1;
+      s51 += (u64)Te[g.eid[p]] * (w - 1);
+      if (x > u) {
+        H.c49 += binom2(w - 1);
+        H.c62 += d;
+      }
+    }
+    pair_c_terms(g, x, w, d, a8, a36, a50, a63);
+    return w;
+  });
+  return true;
 }
 
 // position maps of the hubs (d >= PAIR_HUBMAP_MIN) up to max_slots rows
@@ -899,7 +928,8 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
   PairAcc H;
   H.zero();
-  if (hs >= 0) hstar_term(g, Te, u, hs, o, tab, threadIdx.x, BT, (u64)tab_keys_bound, H, s51);
+  const bool fused = hstar_and_terms(g, Te, u, hs, o, tab, threadIdx.x, BT, (u64)tab_keys_bound, H, s51, a8, a36,
+                                     a50, a63);
   H.c5 = warp_sum(H.c5); H.c49 = warp_sum(H.c49); H.c62 = warp_sum(H.c62);
   if ((threadIdx.x & 31) == 0) {
     if (H.c5) atomicAdd(&red[5], H.c5);
@@ -908,8 +938,10 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   }
   __syncthreads();
   PAIR_PHASE(1);
-  entry_terms(g, tab, threadIdx.x, BT, a8, a36, a50, a63);
-  __syncthreads();  // W final
+  if (!fused) {
+    entry_terms(g, tab, threadIdx.x, BT, a8, a36, a50, a63);
+    __syncthreads();  // W final
+  }
   PAIR_PHASE(2);
   cta_pass<2>(g, Te, u, hs, r0, r1, tab, E, s51, o);
   PAIR_PHASE(3);
@@ -952,10 +984,12 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
   PairAcc H;
   H.zero();
-  if (hs >= 0) hstar_term(g, Te, u, hs, o, tab, lane, 32, (u64)(cap / 2), H, s51);
+  const bool fused = hstar_and_terms(g, Te, u, hs, o, tab, lane, 32, (u64)(cap / 2), H, s51, a8, a36, a50, a63);
   __syncwarp();
-  entry_terms(g, tab, lane, 32, a8, a36, a50, a63);
-  __syncwarp();
+  if (!fused) {
+    entry_terms(g, tab, lane, 32, a8, a36, a50, a63);
+    __syncwarp();
+  }
   warp_pass<2>(g, Te, u, hs, r0, r1, tab, s51, o, acc);
   for (int64_t s = r0 + lane; s < r1; s += 32) {
     const u64 w = tab.get_w_or0(g.ci[s]);
