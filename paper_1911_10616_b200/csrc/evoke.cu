@@ -374,14 +374,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* l0 = A.alloc<int32_t>(n);
     int32_t* l1 = A.alloc<int32_t>(n);
     PeelCtl* ctl = A.alloc<PeelCtl>(1, true);
-    int32_t* al0 = A.alloc<int32_t>(std::min<int64_t>(n, PEEL_SWITCH) + 1);
-    int32_t* al1 = A.alloc<int32_t>(std::min<int64_t>(n, PEEL_SWITCH) + 1);
+    int peel_switch = PEEL_SWITCH;
+    int32_t* al0 = A.alloc<int32_t>(std::min<int64_t>(n, peel_switch) + 1);
+    int32_t* al1 = A.alloc<int32_t>(std::min<int64_t>(n, peel_switch) + 1);
     int bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel, PEEL_BT, 0));
     // small graphs: the whole peel on one CTA (block barriers); large: grid-wide first
-    const int pgrid = n <= PEEL_SWITCH ? 1 : std::max(1, std::min(bps, 1)) * SM;
+    const int pgrid = n <= peel_switch ? 1 : std::max(1, std::min(std::min(bps, 1) * SM, PEEL_GRID));
     void* args[] = {(void*)&n, (void*)&rp0, (void*)&adj0, (void*)&deg0, (void*)&rnd, (void*)&l0,
-                    (void*)&l1, (void*)&al0, (void*)&al1, (void*)&ctl};
+                    (void*)&l1, (void*)&al0, (void*)&al1, (void*)&ctl, (void*)&peel_switch};
     CK(cudaLaunchCooperativeKernel((void*)k_peel, pgrid, PEEL_BT, args, 0, C.st));
     C.launches++;
     PeelCtl hc = d2h_scalar<PeelCtl>(ctl, C.st);

@@ -79,7 +79,8 @@ struct PeelCtl {
 };
 
 #define PEEL_BT 1024           // threads per CTA
-#define PEEL_SWITCH 8192       // alive vertices at or below which one CTA finishes the peel
+#define PEEL_SWITCH 2048       // alive vertices at or below which one CTA finishes the peel
+#define PEEL_GRID 64           // CTAs of the grid-wide phase (cheaper grid barriers; rounds are small)
 
 // Rounds of the peel are identical in both phases: the frontier L[p] (alive vertices of
 // current degree <= k) gets rnd = round, their alive neighbours lose one degree each, and
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
                                                   const int32_t* __restrict__ adj, int32_t* __restrict__ deg,
                                                   int32_t* __restrict__ rnd, int32_t* __restrict__ list0,
                                                   int32_t* __restrict__ list1, int32_t* __restrict__ alive0,
-                                                  int32_t* __restrict__ alive1, PeelCtl* ctl) {
+                                                  int32_t* __restrict__ alive1, PeelCtl* ctl, int peel_switch) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
   if (tid == 0) { ctl->cnt[0] = 0; ctl->cnt[1] = 0; ctl->minv = 0x7fffffff; ctl->nalive = 0; }
   grid.sync();
   // ---- phase 1: grid-wide rounds
-  while (n - removed > PEEL_SWITCH) {
+  while (n - removed > peel_switch) {
     int cur = *(volatile int*)&ctl->cnt[p];
     if (cur == 0) {
       for (int32_t v = tid; v < n; v += nthreads)
