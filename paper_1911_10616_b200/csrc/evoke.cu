@@ -828,13 +828,14 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     }
     if (n5l > 0) {
       int bps = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_light, C5_BT, 0));
+      CK(cudaFuncSetAttribute(k_c5_light, cudaFuncAttributeMaxDynamicSharedMemorySize, C5_SH_BYTES));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_light, C5_BT, C5_SH_BYTES));
       const int lg = std::max(1, std::min(bps, 4)) * SM;
       const size_t nw = (size_t)lg * (C5_BT / 32);
       C5RecT<u32>* reg = A.alloc<C5RecT<u32>>(nw * C5_WARP_CAP, true);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
-        k_c5_light<<<lg, C5_BT, 0, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out);
+        k_c5_light<<<lg, C5_BT, C5_SH_BYTES, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out);
         C.launches++;
       }});
     }
