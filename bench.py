@@ -236,6 +236,16 @@ def main():
                                    stream=stream.cuda_stream, workmodel=True)
     torch.cuda.synchronize()
     roof = roofline(wm, pass_ms, peak, peak_src, step_ms=ms)
+    # the same pass isolated: one untimed call with the concurrent passes run one after the
+    # other (EVOKE_FLAG_SERIAL), so its duration is not stretched by sharing the GPU
+    _, st_ser = pkg.evoke_orbits_edges(g.n, edges_dev, out=out_dev, shard_index=rank, num_shards=world,
+                                       stream=stream.cuda_stream, return_stats=True, serial=True)
+    torch.cuda.synchronize()
+    iso_ms = st_ser["ms_pass"].get(roof["kernel"])
+    if iso_ms and roof.get("algorithmic_bytes"):
+        roof["isolated"] = {"ms": iso_ms, "achieved": roof["algorithmic_bytes"] / (iso_ms / 1e3) / 1e9,
+                            "frac": roof["algorithmic_bytes"] / (iso_ms / 1e3) / 1e9 / peak,
+                            "step_ms_serial": st_ser["ms_total"]}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,

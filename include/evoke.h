@@ -66,6 +66,9 @@ typedef struct evoke_stats {
 } evoke_stats;
 
 #define EVOKE_FLAG_WORKMODEL 1  /* fill evoke_stats.alg_bytes / units (extra kernels)  */
+#define EVOKE_FLAG_SERIAL 2     /* run the pair, hub-local, 5-cycle and theta66/70 passes one
+                                   after the other on the caller's stream (isolated per-pass
+                                   timings) instead of concurrently on internal streams     */
 
 typedef struct evoke_options {
   uint32_t struct_size;   /* sizeof(evoke_options): ABI versioning; 0 = defaults   */

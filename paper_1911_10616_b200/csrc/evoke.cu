@@ -849,9 +849,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // one stream per job (jobs of one pass stay in order on a shared stream when they must:
   // the heavy and main pair kernels write different sources, so all jobs are independent)
   std::stable_sort(jobs.begin(), jobs.end(), [](const Job& x, const Job& y) { return x.rank < y.rank; });
+  const bool serial = (o.flags & EVOKE_FLAG_SERIAL) != 0;
   CK(cudaEventRecord(C.ev_fork, C.st));
   for (size_t i = 0; i < jobs.size(); i++) {
-    cudaStream_t st = C.stream(i, jobs[i].rank);
+    cudaStream_t st = serial ? C.st : C.stream(i, jobs[i].rank);
     CK(cudaStreamWaitEvent(st, C.ev_fork, 0));
     CK(cudaEventRecord(C.pev[i][0], st));
     jobs[i].fn(st);
