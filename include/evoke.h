@@ -69,6 +69,10 @@ typedef struct evoke_stats {
 #define EVOKE_FLAG_SERIAL 2     /* run the pair, hub-local, 5-cycle and theta66/70 passes one
                                    after the other on the caller's stream (isolated per-pass
                                    timings) instead of concurrently on internal streams     */
+#define EVOKE_FLAG_FOUR 4       /* 4-vertex orbits only (columns 0..14; 15..72 written as 0):
+                                   the paper's EVOKE-4 (Table 1): the 5-vertex
+                                   passes (hub-local, 5-cycles, theta66/70, 5-vertex
+                                   gathers) are skipped                                     */
 
 typedef struct evoke_options {
   uint32_t struct_size;   /* sizeof(evoke_options): ABI versioning; 0 = defaults   */

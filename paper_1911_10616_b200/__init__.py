@@ -51,6 +51,7 @@ class _Options(ctypes.Structure):
 
 FLAG_WORKMODEL = 1
 FLAG_SERIAL = 2
+FLAG_FOUR = 4
 
 
 _lock = threading.Lock()
@@ -141,7 +142,7 @@ def _check(rc: int):
 
 def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_index: int = 0,
                        num_shards: int = 1, stream=None, return_stats: bool = False, workmodel: bool = False,
-                       serial: bool = False):
+                       serial: bool = False, four_only: bool = False):
     """Orbit counts uint64[n, 73] of the simple graph given by undirected pairs ``edges``.
 
     ``edges``: int32 [m, 2] numpy array (host) or CUDA torch tensor (device).  Duplicates,
@@ -149,7 +150,7 @@ def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_inde
     ``out``: optional preallocated numpy uint64 [n, 73] (host input) or torch int64/uint64
     CUDA tensor [n, 73] (device input)."""
     st = _Stats() if (return_stats or workmodel) else None
-    fl = (FLAG_WORKMODEL if workmodel else 0) | (FLAG_SERIAL if serial else 0)
+    fl = (FLAG_WORKMODEL if workmodel else 0) | (FLAG_SERIAL if serial else 0) | (FLAG_FOUR if four_only else 0)
     if _is_torch(edges):
         import torch
         assert edges.is_cuda and edges.dtype == torch.int32, "device edges must be CUDA int32"
@@ -178,10 +179,10 @@ def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_inde
 
 def evoke_orbits_csr(n: int, rowptr, col, out=None, induced: bool = True, shard_index: int = 0,
                      num_shards: int = 1, stream=None, return_stats: bool = False, workmodel: bool = False,
-                     serial: bool = False):
+                     serial: bool = False, four_only: bool = False):
     """Orbit counts from a CSR (rowptr int64[n+1], col int32[rowptr[n]]); same cleaning."""
     st = _Stats() if (return_stats or workmodel) else None
-    fl = (FLAG_WORKMODEL if workmodel else 0) | (FLAG_SERIAL if serial else 0)
+    fl = (FLAG_WORKMODEL if workmodel else 0) | (FLAG_SERIAL if serial else 0) | (FLAG_FOUR if four_only else 0)
     if _is_torch(rowptr):
         import torch
         rp = rowptr.contiguous()

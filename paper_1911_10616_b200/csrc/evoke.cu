@@ -702,8 +702,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   }
 
   // ------------------------------------------------------------------ a8: hub-local
+  // (EVOKE_FLAG_FOUR: 4-vertex orbits only -- the 5-vertex passes a8, a10, theta66/70 and
+  // the 5-vertex gathers are skipped, as in the paper's EVOKE-4, Table 1)
+  const bool four = (o.flags & EVOKE_FLAG_FOUR) != 0;
   C.mark(P_HUB);
-  if (ntri > 0) {
+  if (ntri > 0 && !four) {
     const int64_t m2s = 2 * m;
     int32_t* light = A.alloc<int32_t>(m2s);
     int32_t* heavy = A.alloc<int32_t>(m2s);
@@ -750,7 +753,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
 
   // ------------------------------------------------------------------ a10: 5-cycles
   C.mark(P_C5);
-  if (n > 0 && m > 0) {
+  if (n > 0 && m > 0 && !four) {
     int32_t* c5l = A.alloc<int32_t>(n);
     int32_t* c5h = A.alloc<int32_t>(n);
     u64* c5w = A.alloc<u64>(n);
@@ -842,7 +845,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   }
 
   // ------------------------------------------------------------------ theta66 / theta70
-  if (ntri > 0) jobs.push_back({P_CLIQ2, 5, [&](cudaStream_t st) { launch_cliques(1, st); }});
+  if (ntri > 0 && !four) jobs.push_back({P_CLIQ2, 5, [&](cudaStream_t st) { launch_cliques(1, st); }});
 
   // ------------------------------------------------------------------ concurrent launch
   C.mark(P_CLIQ2);
@@ -878,19 +881,20 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   C.mark(P_NBR2);
   if (n > 0) {
     k_nbr2<<<warp_grid, B, 0, C.st>>>(g, ev, F);
-    k_nbr3<<<warp_grid, B, 0, C.st>>>(g, F);
+    if (!four) k_nbr3<<<warp_grid, B, 0, C.st>>>(g, F);
     C.launches += 2;
   }
   // ------------------------------------------------------------------ triangle gather
   C.mark(P_TRIG);
-  if (ntri > 0) { k_trigather<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, ev, F); C.launches++; }
+  if (ntri > 0 && !four) { k_trigather<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, ev, F); C.launches++; }
 
   // ------------------------------------------------------------------ a12: combine
   C.mark(P_COMB);
   u64* dout = nullptr;
   if (n > 0) {
     dout = o.device_pointers ? (u64*)out : A.alloc<u64>((size_t)n * 73);
-    k_combine<<<grid_for(n, 128, SM), 128, 0, C.st>>>(g, F, perm, o.induced, si == 0 ? 1 : 0, dout);
+    k_combine<<<grid_for(n, 128, SM), 128, 0, C.st>>>(g, F, perm, o.induced, si == 0 ? 1 : 0, four ? 15 : 73,
+                                                       dout);
     C.launches++;
   }
   C.mark(P_D2H);

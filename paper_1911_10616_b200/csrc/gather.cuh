@@ -259,8 +259,10 @@ __device__ void compute_dm(const DGraph& g, const u64* __restrict__ F, int32_t n
   DM[72] = f(F_K5);
 }
 
+// ncols = 73, or 15 for the 4-vertex orbits only (the 5-vertex columns are written as 0;
+// A is block diagonal by pattern size, so DIM 0..14 needs DM 0..14 only)
 __global__ void k_combine(DGraph g, const u64* __restrict__ F, const int32_t* __restrict__ perm,
-                          int induced, int primary, u64* __restrict__ out) {
+                          int induced, int primary, int ncols, u64* __restrict__ out) {
   const int32_t n = g.n;
   for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
     u64 DM[EVOKE_NUM_ORBITS_DEV];
@@ -272,12 +274,13 @@ __global__ void k_combine(DGraph g, const u64* __restrict__ F, const int32_t* __
     }
     u64* row = out + (size_t)perm[u] * EVOKE_NUM_ORBITS_DEV;
     if (!induced) {
-      for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) row[i] = DM[i];
+      for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) row[i] = i < ncols ? DM[i] : 0ull;
     } else {
       for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) {
         u64 acc = 0;
-        for (int p = c_ainv_rp[i]; p < c_ainv_rp[i + 1]; p++)
-          acc += (u64)c_ainv_val[p] * DM[c_ainv_col[p]];
+        if (i < ncols)
+          for (int p = c_ainv_rp[i]; p < c_ainv_rp[i + 1]; p++)
+            acc += (u64)c_ainv_val[p] * DM[c_ainv_col[p]];
         row[i] = acc;
       }
     }

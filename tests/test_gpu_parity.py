@@ -302,3 +302,22 @@ def test_config4_invariants_and_low_degree_core(pkg):
     e = e[keep[e[:, 0]] & keep[e[:, 1]]].astype(np.int32)
     assert e.shape[0] > 1_000_000
     _assert_equal(pkg.evoke_orbits_edges(g.n, e), oracle.orbits(g.n, e), "config4 core")
+
+
+def test_four_vertex_mode_and_serial_mode(pkg):
+    """EVOKE_FLAG_FOUR (the paper's EVOKE-4): columns 0..14 equal the oracle's,
+    15..72 are zero; EVOKE_FLAG_SERIAL (passes one after the other) gives the same matrix
+    as the concurrent default"""
+    rng = np.random.default_rng(5)
+    graphs = [graphgen.erdos_renyi(int(rng.integers(5, 14)), float(rng.uniform(0.2, 0.8)), 3000 + t)
+              for t in range(40)] + [graphgen.config(1)]
+    for g in graphs:
+        ref = oracle.orbits(g.n, g.edges)
+        got4 = pkg.evoke_orbits_edges(g.n, g.edges, four_only=True)
+        _assert_equal(got4[:, :15], ref[:, :15], g.name + " four")
+        assert (got4[:, 15:] == 0).all()
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges, serial=True), ref, g.name + " serial")
+    g = graphgen.config(2)
+    full = pkg.evoke_orbits_edges(g.n, g.edges)
+    _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges, four_only=True)[:, :15], full[:, :15], "config2 four")
+    _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges, serial=True), full, "config2 serial")
