@@ -118,6 +118,24 @@ int evoke_orbits_edges(int64_t n, int64_t m, const int32_t* edges, uint64_t* out
 int evoke_orbits_csr(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t* out,
                      const evoke_options* opt);
 
+/*
+ * evoke_ccd -- complementary cumulative distribution of one orbit (the paper's VOC
+ * distributions: "for x, ... the fraction of vertices whose orbit count is at
+ * least x").
+ *   n       number of rows of dim
+ *   dim     uint64[n*73], an output of evoke_orbits_* (row-major)
+ *   orbit   column 0..72
+ *   values  uint64[n] output: the distinct counts of the column, ascending
+ *   counts  uint64[n] output: counts[i] = number of vertices whose count is >= values[i]
+ *           (divide by n for the fraction)
+ *   nvals   output: number of entries written to values / counts
+ * Pointers are host pointers, or device pointers with opt->device_pointers = 1 (opt may be
+ * NULL: defaults).  Scratch is allocated on the device and freed before returning.
+ * Errors: EVOKE_EINVAL for a bad orbit / null pointers; outputs untouched on error.
+ */
+int evoke_ccd(int64_t n, const uint64_t* dim, int orbit, uint64_t* values, uint64_t* counts, int64_t* nvals,
+              const evoke_options* opt);
+
 /* Static name of pass i of evoke_stats.ms_pass (NULL if out of range). */
 const char* evoke_pass_name(int i);
 

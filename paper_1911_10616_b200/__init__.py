@@ -58,7 +58,7 @@ _lock = threading.Lock()
 _lib = None
 
 EXPORTED_SYMBOLS = ("evoke_default_options", "evoke_orbits_edges", "evoke_orbits_csr", "evoke_pass_name",
-                    "evoke_strerror", "evoke_last_error", "evoke_version")
+                    "evoke_strerror", "evoke_last_error", "evoke_version", "evoke_ccd")
 
 
 def lib():
@@ -77,6 +77,9 @@ def lib():
             L.evoke_orbits_csr.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.POINTER(_Options)]
             L.evoke_orbits_csr.restype = ctypes.c_int
+            L.evoke_ccd.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_Options)]
+            L.evoke_ccd.restype = ctypes.c_int
             for f in ("evoke_pass_name",):
                 getattr(L, f).argtypes = [ctypes.c_int]
                 getattr(L, f).restype = ctypes.c_char_p
@@ -205,3 +208,19 @@ def evoke_orbits_csr(n: int, rowptr, col, out=None, induced: bool = True, shard_
     if return_stats or workmodel:
         return out, _stats_dict(st)
     return out
+
+
+def evoke_ccd(dim, orbit: int):
+    """Complementary cumulative distribution of orbit column ``orbit`` of an orbit matrix
+    ``dim`` (numpy uint64 [n, 73]): returns (values, counts), values ascending distinct
+    counts, counts[i] = number of vertices whose count is >= values[i]."""
+    d = np.ascontiguousarray(dim).view(np.uint64)
+    n = d.shape[0]
+    values = np.zeros(max(n, 1), dtype=np.uint64)
+    counts = np.zeros(max(n, 1), dtype=np.uint64)
+    k = ctypes.c_int64(0)
+    o = _make_options(True, False, 0, 1, None, None, None, 0)
+    rc = lib().evoke_ccd(n, d.ctypes.data if n else None, int(orbit), values.ctypes.data, counts.ctypes.data,
+                         ctypes.byref(k), ctypes.byref(o))
+    _check(rc)
+    return values[:k.value], counts[:k.value]

@@ -26,6 +26,7 @@
 #include "gather.cuh"
 #include "transform.cuh"
 #include "workmodel.cuh"
+#include "ccd.cuh"
 
 #define EVOKE_VERSION "0.1.0-sm100a"
 
@@ -1029,6 +1030,70 @@ int evoke_orbits_csr(int64_t n, const int64_t* rowptr, const int32_t* col, uint6
                      const evoke_options* opt) {
   Input in{1, n, 0, nullptr, rowptr, col};
   return guarded(in, out, opt);
+}
+
+int evoke_ccd(int64_t n, const uint64_t* dim, int orbit, uint64_t* values, uint64_t* counts, int64_t* nvals,
+              const evoke_options* opt) {
+  g_last_error.clear();
+  evoke_options o;
+  evoke_default_options(&o);
+  if (opt) {
+    if (opt->struct_size != 0 && opt->struct_size < sizeof(evoke_options)) std::memcpy(&o, opt, opt->struct_size);
+    else o = *opt;
+  }
+  if (n < 0 || orbit < 0 || orbit >= EVOKE_NUM_ORBITS || !nvals || (n > 0 && (!dim || !values || !counts))) {
+    set_error("evoke_ccd: bad arguments");
+    return EVOKE_EINVAL;
+  }
+  *nvals = 0;
+  if (n == 0) return EVOKE_OK;
+  try {
+    int dev = o.device;
+    if (dev < 0) CK(cudaGetDevice(&dev));
+    CK(cudaSetDevice(dev));
+    int SM = 0;
+    CK(cudaDeviceGetAttribute(&SM, cudaDevAttrMultiProcessorCount, dev));
+    cudaStream_t st = (cudaStream_t)o.stream;
+    cudaStream_t own = nullptr;
+    if (!st) { CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking)); st = own; }
+    struct Own { cudaStream_t s; ~Own() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } } own_guard{own};
+    Arena A(st);
+    Ctx C;
+    C.st = st;
+    const u64* ddim = reinterpret_cast<const u64*>(dim);
+    if (!o.device_pointers) {
+      u64* t = A.alloc<u64>((size_t)n * EVOKE_NUM_ORBITS);
+      CK(cudaMemcpyAsync(t, dim, sizeof(u64) * (size_t)n * EVOKE_NUM_ORBITS, cudaMemcpyHostToDevice, st));
+      ddim = t;
+    }
+    u64* col = A.alloc<u64>(n);
+    u64* sorted = A.alloc<u64>(n);
+    k_ccd_gather<<<grid_for(n, 256, SM), 256, 0, st>>>(ddim, n, orbit, col);
+    sort_keys_u64(A, C, col, sorted, n, 64);
+    u64* uniq = A.alloc<u64>(n);
+    u64* run = A.alloc<u64>(n);
+    int64_t* nr = A.alloc<int64_t>(1);
+    size_t tb = 0;
+    CK(cub::DeviceRunLengthEncode::Encode(nullptr, tb, sorted, uniq, run, nr, n, st));
+    void* t = A.alloc<char>(tb);
+    CK(cub::DeviceRunLengthEncode::Encode(t, tb, sorted, uniq, run, nr, n, st));
+    const int64_t k = d2h_scalar<int64_t>(nr, st);
+    // suffix sums of the run lengths: reverse, inclusive scan, reverse
+    u64* rev = A.alloc<u64>(k);
+    u64* cum = A.alloc<u64>(k);
+    u64* ccd = A.alloc<u64>(k);
+    k_ccd_reverse<<<grid_for(k, 256, SM), 256, 0, st>>>(run, k, rev);
+    inclusive_sum(A, C, rev, cum, k);
+    k_ccd_reverse<<<grid_for(k, 256, SM), 256, 0, st>>>(cum, k, ccd);
+    const cudaMemcpyKind kind = o.device_pointers ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(cudaMemcpyAsync(values, uniq, sizeof(u64) * k, kind, st));
+    CK(cudaMemcpyAsync(counts, ccd, sizeof(u64) * k, kind, st));
+    CK(cudaStreamSynchronize(st));
+    *nvals = k;
+  } catch (const EvokeError& e) {
+    return e.code;
+  }
+  return EVOKE_OK;
 }
 
 const char* evoke_pass_name(int i) {

@@ -321,3 +321,18 @@ def test_four_vertex_mode_and_serial_mode(pkg):
     full = pkg.evoke_orbits_edges(g.n, g.edges)
     _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges, four_only=True)[:, :15], full[:, :15], "config2 four")
     _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges, serial=True), full, "config2 serial")
+
+
+def test_ccd_matches_definition(pkg):
+    """evoke_ccd: for each distinct count x of an orbit column, the number of
+    vertices whose count is >= x -- checked against the definition written with numpy"""
+    g = graphgen.config(2)
+    out = pkg.evoke_orbits_edges(g.n, g.edges)
+    for orbit in (0, 15, 17, 34, 70, 72):
+        col = out[:, orbit]
+        vals, cnts = pkg.evoke_ccd(out, orbit)
+        uv = np.unique(col)
+        assert np.array_equal(vals, uv), orbit
+        exp = np.array([(col >= x).sum() for x in uv[:50]], dtype=np.uint64)
+        assert np.array_equal(cnts[:50], exp), orbit
+        assert int(cnts[0]) == g.n
