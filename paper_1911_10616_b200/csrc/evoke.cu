@@ -919,8 +919,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     // passes reports its preparation (main stream) plus the span of its own kernels; the
     // overlap makes the per-pass times add up to more than ms_total
     s->ms_pass[P_CLIQ2] = 0;
+    const bool serial = (o.flags & EVOKE_FLAG_SERIAL) != 0;
     for (int pass : {P_PAIR, P_HUB, P_C5, P_CLIQ2}) {
-      float lo = 1e30f, hi = -1e30f;
+      float lo = 1e30f, hi = -1e30f, sum = 0;
       for (int j = 0; j < C.njobs; j++) {
         if (C.job_pass[j] != pass) continue;
         float a = 0, b = 0;
@@ -928,8 +929,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         CK(cudaEventElapsedTime(&b, C.ev[0], C.pev[j][1]));
         lo = std::min(lo, a);
         hi = std::max(hi, b);
+        sum += b - a;
       }
-      if (hi > lo) s->ms_pass[pass] += hi - lo;
+      // serial: the pass's own kernels (its jobs are interleaved with other passes' jobs);
+      // concurrent: the span of its kernels
+      if (hi > lo) s->ms_pass[pass] += serial ? sum : hi - lo;
     }
     float tot = 0;
     CK(cudaEventElapsedTime(&tot, C.ev[0], C.ev[P_COUNT]));

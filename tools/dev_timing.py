@@ -11,6 +11,7 @@ import paper_1911_10616_b200 as pkg
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+serial = "--serial" in sys.argv
 g = graphgen.config(cfg)
 dev = torch.device("cuda:0")
 edges = torch.from_numpy(g.edges).to(dev)
@@ -18,11 +19,13 @@ out = torch.empty((g.n, 73), dtype=torch.int64, device=dev)
 rows = []
 walls = []
 for i in range(k + 2):
-    _, st = pkg.evoke_orbits_edges(g.n, edges, out=out, return_stats=True)
+    _, st = pkg.evoke_orbits_edges(g.n, edges, out=out, return_stats=True, serial=serial)
     torch.cuda.synchronize()
     if i >= 2:
         rows.append(st["ms_pass"])
         walls.append(st["ms_total"])
+if not rows:
+    sys.exit(0)
 keys = list(rows[0].keys())
 med = {kk: float(np.median([r[kk] for r in rows])) for kk in keys}
 mn = {kk: float(np.min([r[kk] for r in rows])) for kk in keys}
