@@ -114,6 +114,7 @@ struct DGraph {
   const int32_t* fx;    // [3 ntri]
   const int32_t* fe1;   // [3 ntri]
   const int32_t* fe2;   // [3 ntri]
+  int32_t full_sorted;  // 1: every full list is sorted by x (prefix / suffix bounds by search)
 };
 
 __device__ __forceinline__ int32_t dg_deg(const DGraph& g, int32_t u) { return g.deg[u]; }

@@ -29,6 +29,7 @@
 #include "ccd.cuh"
 
 #define EVOKE_VERSION "0.1.0-sm100a"
+#define EVOKE_SORT_FULL_MIN (3ll << 20)  // full triangle lists sorted when 3 #T >= this
 
 namespace {
 
@@ -530,6 +531,33 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     k_tri_sweep1<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, Te, E9f, E9b, Fp(F_DM12), fcur, fx, fe1, fe2);
     C.launches += 3;
     A.release(fcur);
+    // triangle-heavy graphs: sort every full list by third vertex, so the passes that need
+    // only x < a (hub-local) or x > u (pair pass 2) read a prefix / suffix instead of filtering
+    const int64_t N3 = 3 * ntri;
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    const char* sort_env = getenv("EVOKE_SORT_FULL_MIN");  // test hook: force / disable the sort
+    const int64_t sort_min = sort_env ? atoll(sort_env) : EVOKE_SORT_FULL_MIN;
+    if (N3 >= sort_min && (size_t)N3 * 40 < freeb / 2) {
+      u64* k0 = A.alloc<u64>(N3);
+      u64* k1 = A.alloc<u64>(N3);
+      int32_t* i0 = A.alloc<int32_t>(N3);
+      int32_t* i1 = A.alloc<int32_t>(N3);
+      k_full_keys<<<grid_for(m, B, SM), B, 0, C.st>>>(g, k0, i0);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, i0, i1, N3, 0, 32 + bits_for(m), C.st));
+      void* t = A.alloc<char>(tb);
+      CK(cub::DeviceRadixSort::SortPairs(t, tb, k0, k1, i0, i1, N3, 0, 32 + bits_for(m), C.st));
+      int32_t* ofe1 = A.alloc<int32_t>(N3);
+      int32_t* ofe2 = A.alloc<int32_t>(N3);
+      CK(cudaMemcpyAsync(ofe1, fe1, sizeof(int32_t) * N3, cudaMemcpyDeviceToDevice, C.st));
+      CK(cudaMemcpyAsync(ofe2, fe2, sizeof(int32_t) * N3, cudaMemcpyDeviceToDevice, C.st));
+      k_full_apply<<<grid_for(N3, B, SM), B, 0, C.st>>>(N3, k1, i1, ofe1, ofe2, fx, fe1, fe2);
+      C.launches += 2;
+      C.lib_launches += 4;
+      A.release(k0); A.release(k1); A.release(i0); A.release(i1); A.release(t); A.release(ofe1); A.release(ofe2);
+      g.full_sorted = 1;
+    }
   } else {
     CK(cudaMemsetAsync(foff, 0, sizeof(int64_t) * (m + 1), C.st));
     g.foff = foff;

@@ -34,6 +34,13 @@
 #define HUB_SMEM (HUB_BT / 32 * HUB_WARP_CAP * 12)   // 96 KB dynamic shared memory
 #define HUB_SH_DENSE (HUB_SMEM / 8)                  // heavy item: shared table if d(v) <= this
 
+// number of entries of the full list [f, f+len) with third vertex < bound: a binary search
+// when the lists are sorted (g.full_sorted), else the whole list (callers then filter)
+__device__ __forceinline__ int full_prefix(const DGraph& g, int64_t f, int len, int32_t bound) {
+  if (!g.full_sorted) return len;
+  return (int)(lower_bound_dev<int32_t>(g.fx, f, f + len, bound) - f);
+}
+
 // position of x inside N(v) given the edge id e(v,x)
 __device__ __forceinline__ int64_t pos_in_list(const DGraph& g, int32_t v, int32_t x, int32_t evx) {
   return (v < x) ? ((int64_t)g.dm[v] + (evx - g.orow[v])) : (g.eslot_hi[evx] - g.rp[v]);
@@ -65,8 +72,8 @@ __global__ void __launch_bounds__(256) k_hub_items(DGraph g, const u32* __restri
       v_lo = lo == v;
       const u32 t = Te[eva];
       if (t >= 2 && v % num_shards == shard_index) {
-        len = (int)t;
         fo = g.foff[eva];
+        len = full_prefix(g, fo, (int)t, a);  // b < a
       }
     }
     int cur = -1;
@@ -135,7 +142,7 @@ __device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_
   u32* tab = dense_sh ? shm : gtab;
   int32_t* list = dense_sh ? (int32_t*)(shm + HUB_SH_DENSE) : glist;
   const int64_t fa = g.foff[eva];
-  const int64_t na = g.foff[eva + 1] - fa;
+  const int64_t na = full_prefix(g, fa, (int)(g.foff[eva + 1] - fa), a);  // b < a (or all, filtered)
   if (threadIdx.x == 0) { S.cnt = 0; S.r69 = 0; }
   S.acc[threadIdx.x] = 0;
   __syncthreads();
@@ -148,7 +155,7 @@ __device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_
     const int64_t fb = g.foff[evb];
     S.fb[threadIdx.x] = fb;
     S.evb[threadIdx.x] = evb;
-    return g.foff[evb + 1] - fb;
+    return (int64_t)full_prefix(g, fb, (int)(g.foff[evb + 1] - fb), a);  // x < a
   };
   // pass 1: c(x) for x < a over b < a
   block_flat<HUB_BT>(na, S.pre, load,
@@ -220,7 +227,7 @@ __device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32
   const int32_t v = lo_ + g.edst[eva] - a;
   const bool v_lo = lo_ == v;
   const int64_t fa = g.foff[eva];
-  const int na = (int)(g.foff[eva + 1] - fa);
+  const int na = full_prefix(g, fa, (int)(g.foff[eva + 1] - fa), a);  // b < a (or all, filtered)
   for (int o0 = 0; o0 < na; o0 += 32) {
     const int i = o0 + lane;
     int len = 0;
@@ -232,7 +239,7 @@ __device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32
       if (b < a) {
         const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
         fb = g.foff[evb];
-        len = (int)(g.foff[evb + 1] - fb);
+        len = full_prefix(g, fb, (int)(g.foff[evb + 1] - fb), a);  // x < a
       }
     }
     warp_flat(len, [&](int j, int k, bool valid) {
@@ -256,7 +263,7 @@ __device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32
       if (b < a) {
         const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
         fb = g.foff[evb];
-        len = (int)(g.foff[evb + 1] - fb);
+        len = full_prefix(g, fb, (int)(g.foff[evb + 1] - fb), a);  // x < a
       }
     }
     int cur = -1;

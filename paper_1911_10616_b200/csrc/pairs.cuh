@@ -324,6 +324,11 @@ __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool val
       const int32_t evw = vlo ? g.fe1[r] : g.fe2[r];
       f0 = g.foff[evw];
       len2 = (int)(g.foff[evw + 1] - f0);
+      if (PASS == 2 && g.full_sorted) {  // pass 2 needs x > u only: the suffix of a sorted list
+        const int64_t s0 = lower_bound_dev<int32_t>(g.fx, f0, f0 + len2, u + 1);
+        len2 -= (int)(s0 - f0);
+        f0 = s0;
+      }
       // a long diamond list goes to the CTA's queue (chunked over whole warps) instead
       if (len2 > PAIR_DIAM_DEFER && defer(r, v, vlo)) len2 = 0;
     }

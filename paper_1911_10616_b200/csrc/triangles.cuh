@@ -122,3 +122,23 @@ __global__ void k_tri_sweep1(DGraph g, const u32* __restrict__ Te, u64* __restri
     fx[r] = a; fe1[r] = eab; fe2[r] = eac;
   }
 }
+
+// Sorting the full per-edge triangle lists by third vertex (once, for triangle-heavy graphs):
+// key = (edge id << 32) | x for every entry, then one radix sort of (key, entry) pairs.
+__global__ void k_full_keys(DGraph g, u64* __restrict__ keys, int32_t* __restrict__ idx) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.m; e += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t r = g.foff[e]; r < g.foff[e + 1]; r++) {
+      keys[r] = ((u64)e << 32) | (u32)g.fx[r];
+      idx[r] = (int32_t)r;
+    }
+}
+__global__ void k_full_apply(int64_t N, const u64* __restrict__ skeys, const int32_t* __restrict__ sidx,
+                             const int32_t* __restrict__ fe1_old, const int32_t* __restrict__ fe2_old,
+                             int32_t* __restrict__ fx, int32_t* __restrict__ fe1, int32_t* __restrict__ fe2) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t q = sidx[r];
+    fx[r] = (int32_t)(u32)(skeys[r] & 0xffffffffull);
+    fe1[r] = fe1_old[q];
+    fe2[r] = fe2_old[q];
+  }
+}

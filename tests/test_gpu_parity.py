@@ -336,3 +336,15 @@ def test_ccd_matches_definition(pkg):
         exp = np.array([(col >= x).sum() for x in uv[:50]], dtype=np.uint64)
         assert np.array_equal(cnts[:50], exp), orbit
         assert int(cnts[0]) == g.n
+
+
+def test_sorted_full_lists_path(pkg, monkeypatch):
+    """the sorted-full-list path (used on triangle-heavy graphs) forced on small graphs:
+    same matrices as the oracle"""
+    monkeypatch.setenv("EVOKE_SORT_FULL_MIN", "1")
+    rng = np.random.default_rng(9)
+    for t in range(40):
+        g = graphgen.erdos_renyi(int(rng.integers(5, 14)), float(rng.uniform(0.3, 0.9)), 4000 + t)
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name + " sorted")
+    for g in (graphgen.config(1), graphgen.complete(9)):
+        _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name + " sorted")
