@@ -379,13 +379,35 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int peel_switch = PEEL_SWITCH;
     int32_t* al0 = A.alloc<int32_t>(std::min<int64_t>(n, peel_switch) + 1);
     int32_t* al1 = A.alloc<int32_t>(std::min<int64_t>(n, peel_switch) + 1);
-    int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel, PEEL_BT, 0));
-    // small graphs: the whole peel on one CTA (block barriers); large: grid-wide first
-    const int pgrid = n <= peel_switch ? 1 : std::max(1, std::min(std::min(bps, 1) * SM, PEEL_GRID));
     void* args[] = {(void*)&n, (void*)&rp0, (void*)&adj0, (void*)&deg0, (void*)&rnd, (void*)&l0,
                     (void*)&l1, (void*)&al0, (void*)&al1, (void*)&ctl, (void*)&peel_switch};
-    CK(cudaLaunchCooperativeKernel((void*)k_peel, pgrid, PEEL_BT, args, 0, C.st));
+    // graphs up to PEEL_CLUSTER_MAXN vertices: one 16-CTA cluster with hardware cluster
+    // barriers between rounds; larger: a cooperative grid (PEEL_GRID CTAs)
+    bool launched = false;
+    if (n <= PEEL_CLUSTER_MAXN && n > peel_switch) {
+      if (cudaFuncSetAttribute(k_peel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(PEEL_CLUSTER, 1, 1);
+        cfg.blockDim = dim3(PEEL_BT, 1, 1);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = C.st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = PEEL_CLUSTER;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        launched = cudaLaunchKernelExC(&cfg, (const void*)k_peel<true>, args) == cudaSuccess;
+      }
+      if (!launched) (void)cudaGetLastError();  // fall back to the cooperative grid
+    }
+    if (!launched) {
+      int bps = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel<false>, PEEL_BT, 0));
+      const int pgrid = n <= peel_switch ? 1 : std::max(1, std::min(std::min(bps, 1) * SM, PEEL_GRID));
+      CK(cudaLaunchCooperativeKernel((void*)k_peel<false>, pgrid, PEEL_BT, args, 0, C.st));
+    }
     C.launches++;
     PeelCtl hc = d2h_scalar<PeelCtl>(ctl, C.st);
     peel_rounds = hc.rounds;

@@ -5,6 +5,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
+#include "sched.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -81,6 +82,8 @@ struct PeelCtl {
 #define PEEL_BT 1024           // threads per CTA
 #define PEEL_SWITCH 2048       // alive vertices at or below which one CTA finishes the peel
 #define PEEL_GRID 64           // CTAs of the grid-wide phase (cheaper grid barriers; rounds are small)
+#define PEEL_CLUSTER 16        // CTAs of the cluster variant (non-portable cluster size)
+#define PEEL_CLUSTER_MAXN (1 << 18)  // graphs up to this many vertices use the cluster variant
 
 // Rounds of the peel are identical in both phases: the frontier L[p] (alive vertices of
 // current degree <= k) gets rnd = round, their alive neighbours lose one degree each, and
@@ -90,12 +93,21 @@ struct PeelCtl {
 // PEEL_SWITCH remain, they are compacted into a list and block 0 finishes alone with
 // block barriers (each late round touches few vertices, so a grid-wide barrier per round
 // would dominate).
+// CLUSTER: the whole grid is one thread-block cluster and the barriers between rounds are
+// hardware cluster barriers (cheaper than a cooperative grid barrier); used when the graph is
+// small enough for one cluster.
+template <bool CLUSTER>
 __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __restrict__ rp,
                                                   const int32_t* __restrict__ adj, int32_t* __restrict__ deg,
                                                   int32_t* __restrict__ rnd, int32_t* __restrict__ list0,
                                                   int32_t* __restrict__ list1, int32_t* __restrict__ alive0,
                                                   int32_t* __restrict__ alive1, PeelCtl* ctl, int peel_switch) {
-  cg::grid_group grid = cg::this_grid();
+  struct Sync {
+    __device__ __forceinline__ void sync() const {
+      if (CLUSTER) cg::this_cluster().sync();
+      else cg::this_grid().sync();
+    }
+  } grid;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int warp = (int)(tid >> 5), nwarps = (int)(nthreads >> 5), lane = threadIdx.x & 31;
@@ -183,16 +195,25 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
     for (int i = threadIdx.x; i < cur; i += PEEL_BT) rnd[L[i]] = round;
     if (threadIdx.x == 0) s_cnt[p ^ 1] = 0;
     __syncthreads();
-    for (int i = bw; i < cur; i += nbw) {
-      const int32_t v = L[i];
-      for (int64_t s = rp[v] + lane; s < rp[v + 1]; s += 32) {
-        const int32_t w = adj[s];
-        if (rnd[w] < 0) {
-          const int old = atomicSub(&deg[w], 1);
-          if (old == k + 1) lists[p ^ 1][atomicAdd(&s_cnt[p ^ 1], 1)] = w;
-        }
-      }
-    }
+    // the adjacency lists of the frontier flattened over the whole CTA: late rounds remove
+    // a few hubs with long lists, which a warp per vertex would walk alone
+    __shared__ int64_t s_pre[PEEL_BT + 1];
+    __shared__ int64_t s_base[PEEL_BT];
+    block_flat<PEEL_BT>(cur, s_pre,
+        [&](int64_t i) -> int64_t {
+          const int32_t v = L[i];
+          s_base[threadIdx.x] = rp[v];
+          return rp[v + 1] - rp[v];
+        },
+        [&](int li, int64_t kk) {
+          const int32_t w = adj[s_base[li] + kk];
+          if (rnd[w] < 0) {
+            const int old = atomicSub(&deg[w], 1);
+            if (old == k + 1) lists[p ^ 1][atomicAdd(&s_cnt[p ^ 1], 1)] = w;
+          }
+        },
+        [&](int64_t, int) {});
+    (void)bw; (void)nbw;
     removed += cur;
     round++;
     __syncthreads();
