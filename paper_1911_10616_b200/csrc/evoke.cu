@@ -638,7 +638,14 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // ------------------------------------------------------------------ nbr gather 1
   C.mark(P_NBR1);
   const int warp_grid = grid_for((int64_t)n * 32, B, SM);
-  if (n > 0) { k_nbr1<<<warp_grid, B, 0, C.st>>>(g, ev, F); C.launches++; }
+  int32_t* nbr_heavy = A.alloc<int32_t>(std::max(n, 1));
+  int* nbr_nh = A.alloc<int>(4, true);
+  auto gather = [&](auto kw, auto kh, int slot) {
+    kw<<<warp_grid, B, 0, C.st>>>(g, ev, F, nbr_heavy + 0, nbr_nh + slot);
+    kh<<<SM, 1024, 0, C.st>>>(g, ev, F, nbr_heavy, nbr_nh + slot);
+    C.launches += 2;
+  };
+  if (n > 0) gather(k_nbr<1>, k_nbr_heavy<1>, 0);
 
   // ------------------------------------------------------------------ a7, a8, a10, theta66/70
   // The four passes are independent (disjoint outputs; inputs from a1-a6).  Their
@@ -931,9 +938,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // ------------------------------------------------------------------ nbr gathers 2,3
   C.mark(P_NBR2);
   if (n > 0) {
-    k_nbr2<<<warp_grid, B, 0, C.st>>>(g, ev, F);
-    if (!four) k_nbr3<<<warp_grid, B, 0, C.st>>>(g, F);
-    C.launches += 2;
+    gather(k_nbr<2>, k_nbr_heavy<2>, 1);
+    if (!four) gather(k_nbr<3>, k_nbr_heavy<3>, 2);
   }
   // ------------------------------------------------------------------ triangle gather
   C.mark(P_TRIG);

@@ -33,102 +33,173 @@ struct EdgeVals {
 
 #define FLD(f, u) F[(size_t)(f) * (size_t)n + (u)]
 
-// ---- nbr1: needs d, T, Te
-__global__ void k_nbr1(DGraph g, EdgeVals ev, u64* __restrict__ F) {
-  const int32_t n = g.n;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u64i = gw; u64i < n; u64i += nw) {
-    const int32_t u = (int32_t)u64i;
-    u64 dm1 = 0, dm6 = 0, dm9 = 0, dm10 = 0, dm13 = 0, s22 = 0, s28 = 0, s31 = 0, s41 = 0, s55 = 0;
-    for (int64_t s = g.rp[u] + lane; s < g.rp[u + 1]; s += 32) {
-      const int32_t v = g.ci[s];
-      const u64 dv = (u64)dg_deg(g, v);
-      const u64 tv = FLD(F_T, v);
-      const u64 te = ev.Te[g.eid[s]];
-      dm1 += dv - 1;
-      dm6 += binom2(dv - 1);
-      dm9 += tv - te;
-      dm10 += te * (dv - 2);
-      dm13 += binom2(te);
-      s22 += binom3(dv - 1);
-      s28 += tv;
-      s31 += (dv - 1) * tv;
-      s41 += binom2(te) * (dv - 3);
-      s55 += binom3(te);
-    }
-    dm1 = warp_sum(dm1); dm6 = warp_sum(dm6); dm9 = warp_sum(dm9); dm10 = warp_sum(dm10);
-    dm13 = warp_sum(dm13); s22 = warp_sum(s22); s28 = warp_sum(s28); s31 = warp_sum(s31);
-    s41 = warp_sum(s41); s55 = warp_sum(s55);
-    if (lane == 0) {
-      FLD(F_DM1, u) = dm1; FLD(F_DM6, u) = dm6; FLD(F_DM9, u) = dm9; FLD(F_DM10, u) = dm10;
-      FLD(F_DM13, u) = dm13; FLD(F_S22, u) = s22; FLD(F_S28, u) = s28; FLD(F_S31, u) = s31;
-      FLD(F_S41, u) = s41; FLD(F_S55, u) = s55;
-    }
+// Neighbour gathers.  Vertices of degree <= NBR_HEAVY: one warp each (warp reduction);
+// the others (hubs) are appended to a list by the warp kernel and summed by a second kernel
+// with one CTA per hub (block reduction), so a hub's list is not walked by a single warp.
+#define NBR_HEAVY 2048
+
+// block-wide sum of NS values (blockDim.x = 1024 or 256); result valid in thread 0
+template <int NS>
+__device__ __forceinline__ void block_sum_vals(u64 (&a)[NS], u64* sh) {
+#pragma unroll
+  for (int i = 0; i < NS; i++) a[i] = warp_sum(a[i]);
+  if (threadIdx.x < NS) sh[threadIdx.x] = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; i++)
+      if (a[i]) atomicAdd(&sh[i], a[i]);
   }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NS; i++) a[i] = sh[i];
+  __syncthreads();
+}
+
+// ---- nbr1: needs d, T, Te
+__device__ __forceinline__ void nbr1_acc(const DGraph& g, const EdgeVals& ev, const u64* __restrict__ F, int32_t n,
+                                         int32_t u, int64_t start, int stride, u64 (&a)[10]) {
+  for (int64_t s = g.rp[u] + start; s < g.rp[u + 1]; s += stride) {
+    const int32_t v = g.ci[s];
+    const u64 dv = (u64)dg_deg(g, v);
+    const u64 tv = FLD(F_T, v);
+    const u64 te = ev.Te[g.eid[s]];
+    a[0] += dv - 1;
+    a[1] += binom2(dv - 1);
+    a[2] += tv - te;
+    a[3] += te * (dv - 2);
+    a[4] += binom2(te);
+    a[5] += binom3(dv - 1);
+    a[6] += tv;
+    a[7] += (dv - 1) * tv;
+    a[8] += binom2(te) * (dv - 3);
+    a[9] += binom3(te);
+  }
+}
+__device__ __forceinline__ void nbr1_store(u64* __restrict__ F, int32_t n, int32_t u, const u64 (&a)[10]) {
+  FLD(F_DM1, u) = a[0]; FLD(F_DM6, u) = a[1]; FLD(F_DM9, u) = a[2]; FLD(F_DM10, u) = a[3];
+  FLD(F_DM13, u) = a[4]; FLD(F_S22, u) = a[5]; FLD(F_S28, u) = a[6]; FLD(F_S31, u) = a[7];
+  FLD(F_S41, u) = a[8]; FLD(F_S55, u) = a[9];
 }
 
 // ---- nbr2: needs DM1, DM6, DM9, DM10, DM12, DM13, K4, R8 of neighbours and E5/E9/E11
-__global__ void k_nbr2(DGraph g, EdgeVals ev, u64* __restrict__ F) {
-  const int32_t n = g.n;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u64i = gw; u64i < n; u64i += nw) {
-    const int32_t u = (int32_t)u64i;
-    u64 s4 = 0, s18 = 0, s19 = 0, s24 = 0, s27 = 0, s39 = 0, s40 = 0, s45 = 0, s56 = 0, s57 = 0,
-        s60 = 0, s67 = 0, s35 = 0, s37 = 0;
-    for (int64_t s = g.rp[u] + lane; s < g.rp[u + 1]; s += 32) {
-      const int32_t v = g.ci[s];
-      const int32_t e = g.eid[s];
-      const u64 dv = (u64)dg_deg(g, v);
-      const u64 dm1v = FLD(F_DM1, v);
-      const u64 te = ev.Te[e];
-      const u64 e9vu = (v < u) ? ev.E9f[e] : ev.E9b[e];  // E9<v,u>
-      const u64 k4e = ev.K4e[e];
-      s4 += dm1v;
-      s18 += FLD(F_DM6, v);
-      s19 += dm1v * (dv - 1) - 2 * FLD(F_T, v);           // DM5(v)
-      s24 += FLD(F_DM10, v);
-      s27 += FLD(F_DM9, v);
-      s39 += FLD(F_DM13, v);
-      s40 += e9vu * (dv - 3);
-      s45 += FLD(F_DM12, v);
-      s56 += FLD(F_K4, v);
-      s57 += k4e * (dv - 3);
-      s60 += e9vu * (te - 1);
-      s67 += k4e * (te - 2);
-      s35 += FLD(F_R8, v);
-      s37 += ev.C4e[e] * (dv - 2);
-    }
-    s4 = warp_sum(s4); s18 = warp_sum(s18); s19 = warp_sum(s19); s24 = warp_sum(s24);
-    s27 = warp_sum(s27); s39 = warp_sum(s39); s40 = warp_sum(s40); s45 = warp_sum(s45);
-    s56 = warp_sum(s56); s57 = warp_sum(s57); s60 = warp_sum(s60); s67 = warp_sum(s67);
-    s35 = warp_sum(s35); s37 = warp_sum(s37);
-    if (lane == 0) {
-      const u64 d = (u64)dg_deg(g, u);
-      FLD(F_DM4, u) = s4 - 2 * binom2(d) - 2 * FLD(F_T, u);
-      FLD(F_S18, u) = s18; FLD(F_S19, u) = s19; FLD(F_S24, u) = s24; FLD(F_S27, u) = s27;
-      FLD(F_S39, u) = s39; FLD(F_S40, u) = s40; FLD(F_S45, u) = s45; FLD(F_S56, u) = s56;
-      FLD(F_S57, u) = s57; FLD(F_S60, u) = s60; FLD(F_S67, u) = s67;
-      FLD(F_S35, u) = s35; FLD(F_S37, u) = s37;
-    }
+__device__ __forceinline__ void nbr2_acc(const DGraph& g, const EdgeVals& ev, const u64* __restrict__ F, int32_t n,
+                                         int32_t u, int64_t start, int stride, u64 (&a)[14]) {
+  for (int64_t s = g.rp[u] + start; s < g.rp[u + 1]; s += stride) {
+    const int32_t v = g.ci[s];
+    const int32_t e = g.eid[s];
+    const u64 dv = (u64)dg_deg(g, v);
+    const u64 dm1v = FLD(F_DM1, v);
+    const u64 te = ev.Te[e];
+    const u64 e9vu = (v < u) ? ev.E9f[e] : ev.E9b[e];  // E9<v,u>
+    const u64 k4e = ev.K4e[e];
+    a[0] += dm1v;
+    a[1] += FLD(F_DM6, v);
+    a[2] += dm1v * (dv - 1) - 2 * FLD(F_T, v);           // DM5(v)
+    a[3] += FLD(F_DM10, v);
+    a[4] += FLD(F_DM9, v);
+    a[5] += FLD(F_DM13, v);
+    a[6] += e9vu * (dv - 3);
+    a[7] += FLD(F_DM12, v);
+    a[8] += FLD(F_K4, v);
+    a[9] += k4e * (dv - 3);
+    a[10] += e9vu * (te - 1);
+    a[11] += k4e * (te - 2);
+    a[12] += FLD(F_R8, v);
+    a[13] += ev.C4e[e] * (dv - 2);
   }
+}
+__device__ __forceinline__ void nbr2_store(const DGraph& g, u64* __restrict__ F, int32_t n, int32_t u,
+                                           const u64 (&a)[14]) {
+  const u64 d = (u64)dg_deg(g, u);
+  FLD(F_DM4, u) = a[0] - 2 * binom2(d) - 2 * FLD(F_T, u);
+  FLD(F_S18, u) = a[1]; FLD(F_S19, u) = a[2]; FLD(F_S24, u) = a[3]; FLD(F_S27, u) = a[4];
+  FLD(F_S39, u) = a[5]; FLD(F_S40, u) = a[6]; FLD(F_S45, u) = a[7]; FLD(F_S56, u) = a[8];
+  FLD(F_S57, u) = a[9]; FLD(F_S60, u) = a[10]; FLD(F_S67, u) = a[11];
+  FLD(F_S35, u) = a[12]; FLD(F_S37, u) = a[13];
 }
 
 // ---- nbr3: sum of DM4 over neighbours (theta15)
-__global__ void k_nbr3(DGraph g, u64* __restrict__ F) {
+__device__ __forceinline__ void nbr3_acc(const DGraph& g, const EdgeVals&, const u64* __restrict__ F, int32_t n,
+                                         int32_t u, int64_t start, int stride, u64 (&a)[1]) {
+  for (int64_t t = g.rp[u] + start; t < g.rp[u + 1]; t += stride) a[0] += FLD(F_DM4, g.ci[t]);
+}
+__device__ __forceinline__ void nbr3_store(const DGraph&, u64* __restrict__ F, int32_t n, int32_t u,
+                                           const u64 (&a)[1]) {
+  FLD(F_S15, u) = a[0];
+}
+
+template <int K>
+struct NbrK;
+template <>
+struct NbrK<1> {
+  static constexpr int NS = 10;
+  __device__ static void acc(const DGraph& g, const EdgeVals& ev, const u64* F, int32_t n, int32_t u, int64_t st,
+                             int sd, u64 (&a)[NS]) { nbr1_acc(g, ev, F, n, u, st, sd, a); }
+  __device__ static void store(const DGraph&, u64* F, int32_t n, int32_t u, const u64 (&a)[NS]) {
+    nbr1_store(F, n, u, a);
+  }
+};
+template <>
+struct NbrK<2> {
+  static constexpr int NS = 14;
+  __device__ static void acc(const DGraph& g, const EdgeVals& ev, const u64* F, int32_t n, int32_t u, int64_t st,
+                             int sd, u64 (&a)[NS]) { nbr2_acc(g, ev, F, n, u, st, sd, a); }
+  __device__ static void store(const DGraph& g, u64* F, int32_t n, int32_t u, const u64 (&a)[NS]) {
+    nbr2_store(g, F, n, u, a);
+  }
+};
+template <>
+struct NbrK<3> {
+  static constexpr int NS = 1;
+  __device__ static void acc(const DGraph& g, const EdgeVals& ev, const u64* F, int32_t n, int32_t u, int64_t st,
+                             int sd, u64 (&a)[NS]) { nbr3_acc(g, ev, F, n, u, st, sd, a); }
+  __device__ static void store(const DGraph& g, u64* F, int32_t n, int32_t u, const u64 (&a)[NS]) {
+    nbr3_store(g, F, n, u, a);
+  }
+};
+
+// warp per vertex of degree <= NBR_HEAVY; heavier vertices go to `heavy` (count *nheavy)
+template <int K>
+__global__ void k_nbr(DGraph g, EdgeVals ev, u64* __restrict__ F, int32_t* __restrict__ heavy,
+                      int* __restrict__ nheavy) {
+  constexpr int NS = NbrK<K>::NS;
   const int32_t n = g.n;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u64i = gw; u64i < n; u64i += nw) {
     const int32_t u = (int32_t)u64i;
-    u64 s = 0;
-    for (int64_t t = g.rp[u] + lane; t < g.rp[u + 1]; t += 32) s += FLD(F_DM4, g.ci[t]);
-    s = warp_sum(s);
-    if (lane == 0) FLD(F_S15, u) = s;
+    if (dg_deg(g, u) > NBR_HEAVY) {
+      if (lane == 0) heavy[atomicAdd(nheavy, 1)] = u;
+      continue;
+    }
+    u64 a[NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) a[i] = 0;
+    NbrK<K>::acc(g, ev, F, n, u, lane, 32, a);
+#pragma unroll
+    for (int i = 0; i < NS; i++) a[i] = warp_sum(a[i]);
+    if (lane == 0) NbrK<K>::store(g, F, n, u, a);
+  }
+}
+
+// one CTA per hub of the list
+template <int K>
+__global__ void __launch_bounds__(1024) k_nbr_heavy(DGraph g, EdgeVals ev, u64* __restrict__ F,
+                                                    const int32_t* __restrict__ heavy, const int* __restrict__ nheavy) {
+  constexpr int NS = NbrK<K>::NS;
+  __shared__ u64 sh[NS];
+  const int32_t n = g.n;
+  const int nh = *nheavy;
+  for (int q = blockIdx.x; q < nh; q += gridDim.x) {
+    const int32_t u = heavy[q];
+    u64 a[NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) a[i] = 0;
+    NbrK<K>::acc(g, ev, F, n, u, threadIdx.x, blockDim.x, a);
+    block_sum_vals<NS>(a, sh);
+    if (threadIdx.x == 0) NbrK<K>::store(g, F, n, u, a);
   }
 }
 
