@@ -828,8 +828,16 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (n5h > 0) {
       // exact work of the heavy endpoints, sorted descending; the giant prefix goes to the
       // whole grid (cooperative), the rest one CTA each on a side stream
-      k_c5_heavy_w<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, c5c + 2);
-      C.launches++;
+      // A global bound on every endpoint's work, W(l) <= d(l) (d_max + k (k + 1)) with k the
+      // maximum out-degree, decides the record width without the exact per-endpoint count;
+      // the exact count (and the giant-endpoint split) is needed only beyond 2^32 / with the
+      // cluster path enabled.
+      const u64 wbound = (u64)max_deg * ((u64)max_deg + (u64)max_out * ((u64)max_out + 1));
+      const bool exact_w = wbound >= (1ull << 32) || C5_GIANT < (1ull << 40);
+      if (exact_w) {
+        k_c5_heavy_w<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, c5c + 2);
+        C.launches++;
+      }
       int32_t* hs = c5h;
       u64* hkeys = nullptr;
       if (n5h > 1) {
@@ -843,8 +851,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         C.lib_launches += 4;
       }
       int ngiant = 0;
-      CK(cudaMemcpyAsync(&ngiant, c5c + 2, sizeof(int), cudaMemcpyDeviceToHost, C.st));
-      CK(cudaStreamSynchronize(C.st));
+      if (exact_w) {
+        CK(cudaMemcpyAsync(&ngiant, c5c + 2, sizeof(int), cudaMemcpyDeviceToHost, C.st));
+        CK(cudaStreamSynchronize(C.st));
+      }
       size_t freeb = 0, totalb = 0;
       CK(cudaMemGetInfo(&freeb, &totalb));
       if (ngiant > 0) {
@@ -865,9 +875,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const int nrest = n5h - ngiant;
       if (nrest > 0) {
         // u32 records when every remaining endpoint's work bound is < 2^32 (the list is sorted)
-        u64 wmax = 0;
-        CK(cudaMemcpyAsync(&wmax, (n5h > 1 ? hkeys : c5w) + ngiant, sizeof(u64), cudaMemcpyDeviceToHost, C.st));
-        CK(cudaStreamSynchronize(C.st));
+        u64 wmax = wbound;
+        if (exact_w) {
+          CK(cudaMemcpyAsync(&wmax, (n5h > 1 ? hkeys : c5w) + ngiant, sizeof(u64), cudaMemcpyDeviceToHost, C.st));
+          CK(cudaStreamSynchronize(C.st));
+        }
         const bool narrow = wmax < (1ull << 32);
         const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
         const int64_t per = (int64_t)n * (int64_t)(rec + 8);
