@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <functional>
+#include <mutex>
 #include <utility>
 #include <cstdarg>
 #include <cstdio>
@@ -48,8 +49,24 @@ struct EvokeError {
   int code;
 };
 
+// EVOKE_HOSTPROF=1: report every CUDA API call that blocks the host for more than 2 ms
+inline bool hostprof() {
+  static const bool on = std::getenv("EVOKE_HOSTPROF") != nullptr;
+  return on;
+}
+struct HostTimer {
+  const char* what; int line; std::chrono::steady_clock::time_point t0;
+  HostTimer(const char* w, int l) : what(w), line(l) { if (hostprof()) t0 = std::chrono::steady_clock::now(); }
+  ~HostTimer() {
+    if (!hostprof()) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 2.0) fprintf(stderr, "[evoke hostprof] %.2f ms line %d: %.80s\n", ms, line, what);
+  }
+};
+
 #define CK(call)                                                                        \
   do {                                                                                  \
+    HostTimer _ht(#call, __LINE__);                                                     \
     cudaError_t _e = (call);                                                            \
     if (_e != cudaSuccess) {                                                            \
       set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
@@ -119,23 +136,46 @@ struct Ctx {
   int njobs = 0;
   int job_pass[MAXJOBS] = {};
   bool timing;
-  // stream i with priority from rank (rank 0 = the device's greatest priority)
+  // stream for job i with the priority of its rank (rank 0 = the device's greatest priority).
+  // Streams are created once per (device, rank) and kept for the process lifetime: creating
+  // and destroying them on every call costs more than the calls' shorter passes.
   cudaStream_t stream(size_t i, int rank) {
     if (i >= (size_t)MAXJOBS) { set_error("too many concurrent jobs"); throw EvokeError{EVOKE_EINTERNAL}; }
-    if (!jst[i]) {
+    static std::mutex mu;
+    static cudaStream_t pool[64][MAXJOBS] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) { set_error("device ordinal out of range"); throw EvokeError{EVOKE_EINTERNAL}; }
+    if (!pool[dev][i]) {
       int lo = 0, hi = 0;  // lo = least priority (numerically greatest), hi = greatest
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       const int prio = std::min(lo, hi + rank);
-      CK(cudaStreamCreateWithPriority(&jst[i], cudaStreamNonBlocking, prio));
+      CK(cudaStreamCreateWithPriority(&pool[dev][i], cudaStreamNonBlocking, prio));
     }
-    return jst[i];
+    return pool[dev][i];
   }
   cudaStream_t side() {
     if (!side_st) CK(cudaStreamCreateWithFlags(&side_st, cudaStreamNonBlocking));
     return side_st;
   }
+  std::chrono::steady_clock::time_point hts[P_COUNT + 1];
+  bool hset[P_COUNT + 1] = {};
   void mark(int pass) {
     if (timing) CK(cudaEventRecord(ev[pass], st));
+    if (hostprof()) { hts[pass] = std::chrono::steady_clock::now(); hset[pass] = true; }
+  }
+  void host_report() {
+    if (!hostprof() || !hset[0]) return;
+    std::string line;
+    int prev = 0;
+    for (int p = 1; p <= P_COUNT; p++) {
+      if (!hset[p]) continue;
+      const double ms = std::chrono::duration<double, std::milli>(hts[p] - hts[prev]).count();
+      char b[64];
+      snprintf(b, sizeof(b), " %s=%.1f", kPassNames[prev], ms);
+      line += b;
+      prev = p;
+    }
+    fprintf(stderr, "[evoke hostprof] host segments:%s\n", line.c_str());
   }
 };
 
@@ -145,6 +185,34 @@ inline int grid_for(int64_t work, int block, int num_sms) {
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
+}
+
+// Device memory this call may still take.  cudaMemGetInfo can block the host for tens of
+// milliseconds while stream-ordered frees are in flight, so it is read once per device;
+// afterwards the estimate is that first reading minus what the stream-ordered pool (which
+// keeps its memory between calls, see run()) currently has in use:
+// avail = free0 + reserved0 - used_now.
+size_t avail_bytes(int dev) {
+  static std::mutex mu;
+  static size_t base[256] = {};
+  static bool have[256] = {};
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 256) { set_error("device ordinal out of range"); throw EvokeError{EVOKE_EINTERNAL}; }
+    if (!have[dev]) {
+      size_t freeb = 0, totalb = 0;
+      uint64_t reserved = 0;
+      CK(cudaMemGetInfo(&freeb, &totalb));
+      CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+      base[dev] = freeb + (size_t)reserved;
+      have[dev] = true;
+    }
+  }
+  uint64_t used = 0;
+  CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  return base[dev] > used ? base[dev] - (size_t)used : 0;
 }
 
 template <typename T>
@@ -266,10 +334,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       for (int i = 0; i <= P_COUNT; i++) cudaEventDestroy(C.ev[i]);
       cudaEventDestroy(C.ev_fork);
       cudaEventDestroy(C.ev_join);
-      for (int i = 0; i < Ctx::MAXJOBS; i++) {
+      for (int i = 0; i < Ctx::MAXJOBS; i++)
         for (int j = 0; j < 2; j++) cudaEventDestroy(C.pev[i][j]);
-        if (C.jst[i]) { cudaStreamSynchronize(C.jst[i]); cudaStreamDestroy(C.jst[i]); }
-      }
       if (C.side_st) { cudaStreamSynchronize(C.side_st); cudaStreamDestroy(C.side_st); }
       if (own) { cudaStreamSynchronize(own); cudaStreamDestroy(own); }
     }
@@ -556,8 +622,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     // triangle-heavy graphs: sort every full list by third vertex, so the passes that need
     // only x < a (hub-local) or x > u (pair pass 2) read a prefix / suffix instead of filtering
     const int64_t N3 = 3 * ntri;
-    size_t freeb = 0, totalb = 0;
-    CK(cudaMemGetInfo(&freeb, &totalb));
+    const size_t freeb = avail_bytes(C.dev);
     const char* sort_env = getenv("EVOKE_SORT_FULL_MIN");  // test hook: force / disable the sort
     const int64_t sort_min = sort_env ? atoll(sort_env) : EVOKE_SORT_FULL_MIN;
     if (N3 >= sort_min && (size_t)N3 * 40 < freeb / 2) {
@@ -698,8 +763,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     C.launches += 2;
     PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e, hstar,
                hslot, hpos};
-    size_t freeb = 0, totalb = 0;
-    CK(cudaMemGetInfo(&freeb, &totalb));
+    const size_t freeb = avail_bytes(C.dev);
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
     auto heavy_grid = [&](int nsrc, size_t word, int cap) {
       const int64_t l2_ctas = std::max<int64_t>(1, (56ll << 20) / ((int64_t)n * (int64_t)word));
@@ -855,8 +919,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         CK(cudaMemcpyAsync(&ngiant, c5c + 2, sizeof(int), cudaMemcpyDeviceToHost, C.st));
         CK(cudaStreamSynchronize(C.st));
       }
-      size_t freeb = 0, totalb = 0;
-      CK(cudaMemGetInfo(&freeb, &totalb));
+      const size_t freeb = avail_bytes(C.dev);
       if (ngiant > 0) {
         const int nclus = std::min(ngiant, std::max(1, SM / C5_CLUSTER));
         C5Rec* dense = A.alloc<C5Rec>((size_t)nclus * n, true);
@@ -972,6 +1035,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   C.mark(P_COUNT);
   CK(cudaStreamSynchronize(C.st));
   CK(cudaGetLastError());
+  if (hostprof()) {
+    float gms = 0;
+    CK(cudaEventElapsedTime(&gms, C.ev[0], C.ev[P_COUNT]));
+    const double hms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - C.hts[0]).count();
+    if (hms > 25.0) {
+      fprintf(stderr, "[evoke hostprof] call host %.1f ms gpu %.1f ms\n", hms, gms);
+      C.host_report();
+    }
+  }
 
   if (o.stats) {
     evoke_stats* s = o.stats;
