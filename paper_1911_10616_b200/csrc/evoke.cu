@@ -442,11 +442,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* l0 = A.alloc<int32_t>(n);
     int32_t* l1 = A.alloc<int32_t>(n);
     PeelCtl* ctl = A.alloc<PeelCtl>(1, true);
-    int peel_switch = PEEL_SWITCH;
-    int32_t* al0 = A.alloc<int32_t>(std::min<int64_t>(n, peel_switch) + 1);
-    int32_t* al1 = A.alloc<int32_t>(std::min<int64_t>(n, peel_switch) + 1);
+    int peel_switch = (int)std::min<int64_t>(n, PEEL_SWITCH);
+    int32_t* lidmap = A.alloc<int32_t>(n);
+    int32_t* loc = A.alloc<int32_t>(peel_switch + 1);
+    int32_t* lcnt = A.alloc<int32_t>(peel_switch + 1);
+    uint16_t* ladj = A.alloc<uint16_t>(2 * m + 1);
+    const size_t peel_smem = (size_t)peel_switch * PEEL_LOCAL_BYTES;
+    CK(cudaFuncSetAttribute(k_peel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)peel_smem));
+    CK(cudaFuncSetAttribute(k_peel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)peel_smem));
     void* args[] = {(void*)&n, (void*)&rp0, (void*)&adj0, (void*)&deg0, (void*)&rnd, (void*)&l0,
-                    (void*)&l1, (void*)&al0, (void*)&al1, (void*)&ctl, (void*)&peel_switch};
+                    (void*)&l1, (void*)&lidmap, (void*)&loc, (void*)&lcnt, (void*)&ladj, (void*)&ctl,
+                    (void*)&peel_switch};
     // graphs up to PEEL_CLUSTER_MAXN vertices: one 16-CTA cluster with hardware cluster
     // barriers between rounds; larger: a cooperative grid (PEEL_GRID CTAs)
     bool launched = false;
@@ -455,7 +461,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(PEEL_CLUSTER, 1, 1);
         cfg.blockDim = dim3(PEEL_BT, 1, 1);
-        cfg.dynamicSmemBytes = 0;
+        cfg.dynamicSmemBytes = peel_smem;
         cfg.stream = C.st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -470,13 +476,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     }
     if (!launched) {
       int bps = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel<false>, PEEL_BT, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel<false>, PEEL_BT, peel_smem));
       const int pgrid = n <= peel_switch ? 1 : std::max(1, std::min(std::min(bps, 1) * SM, PEEL_GRID));
-      CK(cudaLaunchCooperativeKernel((void*)k_peel<false>, pgrid, PEEL_BT, args, 0, C.st));
+      CK(cudaLaunchCooperativeKernel((void*)k_peel<false>, pgrid, PEEL_BT, args, peel_smem, C.st));
     }
     C.launches++;
     PeelCtl hc = d2h_scalar<PeelCtl>(ctl, C.st);
     peel_rounds = hc.rounds;
+    if (getenv("EVOKE_DEBUG"))
+      fprintf(stderr, "[evoke] peel: %d rounds (%d grid-wide, %.3f ms; %d in one CTA, %.3f ms), level %d\n",
+              hc.rounds, hc.rounds1, (hc.t1 - hc.t0) * 1e-6, hc.rounds - hc.rounds1, (hc.t2 - hc.t1) * 1e-6,
+              hc.level);
     degeneracy_level = hc.level;
     u64* okeys = A.alloc<u64>(n);
     u64* osorted = A.alloc<u64>(n);
@@ -485,7 +495,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     sort_keys_u64(A, C, okeys, osorted, n, 32 + bits_for(std::max(peel_rounds, 1)));
     k_perm<<<grid_for(n, B, SM), B, 0, C.st>>>(osorted, n, perm, inv);
     C.launches++;
-    A.release(okeys); A.release(osorted); A.release(rnd); A.release(l0); A.release(l1); A.release(al0); A.release(al1);
+    A.release(okeys); A.release(osorted); A.release(rnd); A.release(l0); A.release(l1); A.release(lidmap);
+    A.release(loc); A.release(lcnt); A.release(ladj);
     A.release(cursor); A.release(deg64);
   }
   A.release(adj0); A.release(rp0); A.release(deg0);

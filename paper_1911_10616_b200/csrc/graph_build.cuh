@@ -72,27 +72,46 @@ __global__ void k_fill_adj0(const u64* __restrict__ keys, int64_t m, int64_t* __
 // degree.  The total order (rnd, id) is a degeneracy order: every vertex has at most
 // k_max = degeneracy later neighbours (reading R19).
 struct PeelCtl {
-  int cnt[2];
+  int cnt[3];
   int minv;
   int level;
   int rounds;
+  int rounds1;  // rounds of the grid-wide phase
   int nalive;
+  unsigned long long t0, t1, t2;  // %globaltimer at start, at the phase switch, at the end
 };
 
 #define PEEL_BT 1024           // threads per CTA
-#define PEEL_SWITCH 2048       // alive vertices at or below which one CTA finishes the peel
+#define PEEL_SWITCH 8192       // vertices left at or below which one CTA finishes the peel locally
 #define PEEL_GRID 64           // CTAs of the grid-wide phase (cheaper grid barriers; rounds are small)
 #define PEEL_CLUSTER 16        // CTAs of the cluster variant (non-portable cluster size)
 #define PEEL_CLUSTER_MAXN (1 << 18)  // graphs up to this many vertices use the cluster variant
+// shared bytes per local vertex of phase 2: ldeg, lrnd (int32), lbeg (u32), lcnt, two frontier
+// lists (u16)
+#define PEEL_LOCAL_BYTES 20
 
-// Rounds of the peel are identical in both phases: the frontier L[p] (alive vertices of
-// current degree <= k) gets rnd = round, their alive neighbours lose one degree each, and
-// a neighbour whose degree drops to exactly k joins the next frontier.  When a frontier is
-// empty the level rises to the minimum alive degree.  Phase 1 runs the rounds over the
-// whole grid (grid.sync between steps) while many vertices are alive; once at most
-// PEEL_SWITCH remain, they are compacted into a list and block 0 finishes alone with
-// block barriers (each late round touches few vertices, so a grid-wide barrier per round
-// would dominate).
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Round r removes the frontier L_r: alive vertices whose current degree is <= k (the current
+// core level).  A vertex is stamped rnd = r when it joins L_r, so one barrier per round
+// suffices: while L_r is walked, every neighbour w not yet stamped loses one degree, and the
+// one decrement that takes d(w) from k+1 to k stamps w with r+1 and appends it to L_{r+1}
+// (decrements of stamped vertices are skipped; their degree no longer matters).  When a
+// frontier is empty the level rises to the minimum degree of the unstamped vertices, which
+// are stamped as the next frontier if their degree is <= that level.  The three frontier
+// counters rotate (read r, append r+1, reset r+2) so no counter is reset while it is read.
+// Phase 1 runs the rounds over the whole grid while many vertices are alive.  Once at most
+// peel_switch (<= PEEL_SWITCH) vertices are left (unstamped, or stamped for the pending
+// round), the grid gives them local ids and copies the subgraph they induce into ladj
+// (local ids, at the vertices' own CSR positions); block 0 then finishes with every per-vertex
+// state in shared memory and block barriers: the late rounds touch few vertices each, so the
+// grid-wide barrier and the dependent L2 round trips of a global round would dominate.  The
+// result -- rnd, hence the order (rnd, id) -- is the same in both phases and for any grid
+// size: the set L_{r+1} is fixed by the degrees, not by the schedule.
 // CLUSTER: the whole grid is one thread-block cluster and the barriers between rounds are
 // hardware cluster barriers (cheaper than a cooperative grid barrier); used when the graph is
 // small enough for one cluster.
@@ -100,8 +119,9 @@ template <bool CLUSTER>
 __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __restrict__ rp,
                                                   const int32_t* __restrict__ adj, int32_t* __restrict__ deg,
                                                   int32_t* __restrict__ rnd, int32_t* __restrict__ list0,
-                                                  int32_t* __restrict__ list1, int32_t* __restrict__ alive0,
-                                                  int32_t* __restrict__ alive1, PeelCtl* ctl, int peel_switch) {
+                                                  int32_t* __restrict__ list1, int32_t* __restrict__ lidmap,
+                                                  int32_t* __restrict__ loc, int32_t* __restrict__ lcnt,
+                                                  uint16_t* __restrict__ ladj, PeelCtl* ctl, int peel_switch) {
   struct Sync {
     __device__ __forceinline__ void sync() const {
       if (CLUSTER) cg::this_cluster().sync();
@@ -111,37 +131,48 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int warp = (int)(tid >> 5), nwarps = (int)(nthreads >> 5), lane = threadIdx.x & 31;
-  int32_t* lists[2] = {list0, list1};
   int k = 0, round = 0, p = 0, removed = 0;
-  for (int32_t v = tid; v < n; v += nthreads) rnd[v] = -1;
-  if (tid == 0) { ctl->cnt[0] = 0; ctl->cnt[1] = 0; ctl->minv = 0x7fffffff; ctl->nalive = 0; }
+  // (selects instead of an array indexed by p: a dynamically indexed local array lives in
+  // local memory)
+  auto lists = [&](int q) { return q ? list1 : list0; };
+  for (int32_t v = tid; v < n; v += nthreads) { rnd[v] = -1; lidmap[v] = -1; }
+  if (tid == 0) {
+    ctl->cnt[0] = 0; ctl->cnt[1] = 0; ctl->cnt[2] = 0; ctl->minv = 0x7fffffff; ctl->nalive = 0;
+    ctl->t0 = globaltimer();
+  }
   grid.sync();
-  // ---- phase 1: grid-wide rounds
+  // ---- phase 1: grid-wide rounds, one barrier each
   while (n - removed > peel_switch) {
-    int cur = *(volatile int*)&ctl->cnt[p];
+    const int c = round % 3, c1 = (round + 1) % 3, c2 = (round + 2) % 3;
+    int cur = *(volatile int*)&ctl->cnt[c];
     if (cur == 0) {
       for (int32_t v = tid; v < n; v += nthreads)
         if (rnd[v] < 0) atomicMin(&ctl->minv, deg[v]);
       grid.sync();
-      int mv = *(volatile int*)&ctl->minv;
+      const int mv = *(volatile int*)&ctl->minv;
       if (mv > k) k = mv;
       for (int32_t v = tid; v < n; v += nthreads)
-        if (rnd[v] < 0 && deg[v] <= k) lists[p][atomicAdd(&ctl->cnt[p], 1)] = v;
+        if (rnd[v] < 0 && deg[v] <= k) {
+          rnd[v] = round;
+          lists(p)[atomicAdd(&ctl->cnt[c], 1)] = v;
+        }
       grid.sync();
-      cur = *(volatile int*)&ctl->cnt[p];
-      if (tid == 0) ctl->minv = 0x7fffffff;
+      cur = *(volatile int*)&ctl->cnt[c];
+      if (tid == 0) ctl->minv = 0x7fffffff;  // read again only after the next round's barrier
     }
-    int32_t* L = lists[p];
-    for (int64_t i = tid; i < cur; i += nthreads) rnd[L[i]] = round;
-    if (tid == 0) ctl->cnt[p ^ 1] = 0;
-    grid.sync();
+    if (tid == 0) ctl->cnt[c2] = 0;
+    const int32_t* L = lists(p);
+    int32_t* Ln = lists(p ^ 1);
     for (int i = warp; i < cur; i += nwarps) {
-      int32_t v = L[i];
+      const int32_t v = L[i];
       for (int64_t s = rp[v] + lane; s < rp[v + 1]; s += 32) {
-        int32_t w = adj[s];
+        const int32_t w = adj[s];
         if (rnd[w] < 0) {
-          int old = atomicSub(&deg[w], 1);
-          if (old == k + 1) lists[p ^ 1][atomicAdd(&ctl->cnt[p ^ 1], 1)] = w;
+          const int old = atomicSub(&deg[w], 1);
+          if (old == k + 1) {
+            rnd[w] = round + 1;
+            Ln[atomicAdd(&ctl->cnt[c1], 1)] = w;
+          }
         }
       }
     }
@@ -150,76 +181,125 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
     grid.sync();
     p ^= 1;
   }
+  if (tid == 0) { ctl->rounds1 = round; ctl->t1 = globaltimer(); }
   if (removed >= n) {
-    if (tid == 0) { ctl->level = k; ctl->rounds = round; }
+    if (tid == 0) { ctl->level = k; ctl->rounds = round; ctl->t2 = ctl->t1; }
     return;
   }
-  // compact the alive vertices (the pending frontier L[p] stays as it is)
-  for (int32_t v = tid; v < n; v += nthreads)
-    if (rnd[v] < 0) alive0[atomicAdd(&ctl->nalive, 1)] = v;
+  // ---- switch: local ids for the vertices left (unstamped, or stamped for the pending round)
+  for (int32_t v = tid; v < n; v += nthreads) {
+    const int r = rnd[v];
+    if (r < 0 || r == round) {
+      const int l = atomicAdd(&ctl->nalive, 1);
+      loc[l] = v;
+      lidmap[v] = l;
+    }
+  }
+  grid.sync();
+  const int S = *(volatile int*)&ctl->nalive;
+  // the induced subgraph in local ids, ladj[rp[v] + j] for j < lcnt[l] (warp per vertex,
+  // ballot compaction keeps the neighbours in CSR order)
+  for (int l = warp; l < S; l += nwarps) {
+    const int32_t v = loc[l];
+    const int64_t b = rp[v], e = rp[v + 1];
+    int cnt = 0;
+    for (int64_t s0 = b; s0 < e; s0 += 32) {
+      const int64_t s = s0 + lane;
+      const int lw = s < e ? lidmap[adj[s]] : -1;
+      const unsigned bal = __ballot_sync(FULL_MASK, lw >= 0);
+      if (lw >= 0) ladj[b + cnt + __popc(bal & ((1u << lane) - 1))] = (uint16_t)lw;
+      cnt += __popc(bal);
+    }
+    if (lane == 0) lcnt[l] = cnt;
+  }
   grid.sync();
   if (blockIdx.x != 0) return;
-  // ---- phase 2: one CTA
-  __shared__ int s_cnt[2], s_minv, s_na;
-  int32_t* al[2] = {alive0, alive1};
-  int ap = 0;
-  int nalive = *(volatile int*)&ctl->nalive;
-  if (threadIdx.x == 0) { s_cnt[p] = *(volatile int*)&ctl->cnt[p]; s_cnt[p ^ 1] = 0; s_minv = 0x7fffffff; s_na = 0; }
+  // ---- phase 2: block 0, per-vertex state in shared memory
+  extern __shared__ int32_t peel_sh[];
+  int32_t* ldeg = peel_sh;                                   // current degree
+  int32_t* lrnd = ldeg + peel_switch;                        // round, -1 = unstamped
+  u32* lbeg = (u32*)(lrnd + peel_switch);                    // CSR position (2m < 2^31)
+  uint16_t* lc = (uint16_t*)(lbeg + peel_switch);            // local degree at the switch
+  uint16_t* lq0 = lc + peel_switch;
+  uint16_t* lq1 = lq0 + peel_switch;
+  auto lq = [&](int q) { return q ? lq1 : lq0; };
+  __shared__ int s_cnt[3], s_minv;
+  __shared__ int s_pre[PEEL_BT + 1];
+  __shared__ u32 s_base[PEEL_BT];
+  typedef cub::BlockScan<int, PEEL_BT> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_minv = 0x7fffffff;
   __syncthreads();
-  const int bw = threadIdx.x >> 5, nbw = PEEL_BT / 32;
-  while (removed < n) {
-    int cur = s_cnt[p];
+  const int c0 = round % 3;
+  for (int l = threadIdx.x; l < S; l += PEEL_BT) {
+    const int32_t v = loc[l];
+    const int r = rnd[v];
+    ldeg[l] = lcnt[l];
+    lc[l] = (uint16_t)lcnt[l];
+    lbeg[l] = (u32)rp[v];
+    lrnd[l] = r;
+    if (r >= 0) lq(p)[atomicAdd(&s_cnt[c0], 1)] = (uint16_t)l;  // the pending frontier
+  }
+  __syncthreads();
+  const int removed0 = removed;
+  while (removed - removed0 < S) {
+    const int c = round % 3, c1 = (round + 1) % 3, c2 = (round + 2) % 3;
+    int cur = s_cnt[c];
     if (cur == 0) {
-      // level up: minimum alive degree, compacting the alive list on the way
-      for (int i = threadIdx.x; i < nalive; i += PEEL_BT) {
-        const int32_t v = al[ap][i];
-        if (rnd[v] < 0) {
-          atomicMin(&s_minv, deg[v]);
-          al[ap ^ 1][atomicAdd(&s_na, 1)] = v;
+      for (int l = threadIdx.x; l < S; l += PEEL_BT)
+        if (lrnd[l] < 0) atomicMin(&s_minv, ldeg[l]);
+      __syncthreads();
+      if (s_minv > k) k = s_minv;
+      for (int l = threadIdx.x; l < S; l += PEEL_BT)
+        if (lrnd[l] < 0 && ldeg[l] <= k) {
+          lrnd[l] = round;
+          lq(p)[atomicAdd(&s_cnt[c], 1)] = (uint16_t)l;
+        }
+      __syncthreads();
+      cur = s_cnt[c];
+      __syncthreads();
+      if (threadIdx.x == 0) s_minv = 0x7fffffff;
+    }
+    if (threadIdx.x == 0) s_cnt[c2] = 0;
+    const uint16_t* L = lq(p);
+    uint16_t* Ln = lq(p ^ 1);
+    // the frontier's local lists flattened over the CTA
+    for (int f0 = 0; f0 < cur; f0 += PEEL_BT) {
+      const int cn = min(PEEL_BT, cur - f0);
+      int len = 0;
+      if ((int)threadIdx.x < cn) {
+        const int l = L[f0 + threadIdx.x];
+        len = lc[l];
+        s_base[threadIdx.x] = lbeg[l];
+      }
+      int ex, tot;
+      Scan(scan_tmp).ExclusiveSum(len, ex, tot);
+      s_pre[threadIdx.x] = ex;
+      __syncthreads();
+      for (int t = threadIdx.x; t < tot; t += PEEL_BT) {
+        int lo = 0, hi = cn;  // largest lo with s_pre[lo] <= t
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_pre[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int w = ladj[s_base[lo] + (u32)(t - s_pre[lo])];
+        if (lrnd[w] < 0) {
+          const int old = atomicSub(&ldeg[w], 1);
+          if (old == k + 1) {
+            lrnd[w] = round + 1;
+            Ln[atomicAdd(&s_cnt[c1], 1)] = (uint16_t)w;
+          }
         }
       }
       __syncthreads();
-      ap ^= 1;
-      nalive = s_na;
-      if (s_minv > k) k = s_minv;
-      for (int i = threadIdx.x; i < nalive; i += PEEL_BT) {
-        const int32_t v = al[ap][i];
-        if (deg[v] <= k) lists[p][atomicAdd(&s_cnt[p], 1)] = v;
-      }
-      __syncthreads();
-      cur = s_cnt[p];
-      __syncthreads();
-      if (threadIdx.x == 0) { s_minv = 0x7fffffff; s_na = 0; }
     }
-    int32_t* L = lists[p];
-    for (int i = threadIdx.x; i < cur; i += PEEL_BT) rnd[L[i]] = round;
-    if (threadIdx.x == 0) s_cnt[p ^ 1] = 0;
-    __syncthreads();
-    // the adjacency lists of the frontier flattened over the whole CTA: late rounds remove
-    // a few hubs with long lists, which a warp per vertex would walk alone
-    __shared__ int64_t s_pre[PEEL_BT + 1];
-    __shared__ int64_t s_base[PEEL_BT];
-    block_flat<PEEL_BT>(cur, s_pre,
-        [&](int64_t i) -> int64_t {
-          const int32_t v = L[i];
-          s_base[threadIdx.x] = rp[v];
-          return rp[v + 1] - rp[v];
-        },
-        [&](int li, int64_t kk) {
-          const int32_t w = adj[s_base[li] + kk];
-          if (rnd[w] < 0) {
-            const int old = atomicSub(&deg[w], 1);
-            if (old == k + 1) lists[p ^ 1][atomicAdd(&s_cnt[p ^ 1], 1)] = w;
-          }
-        },
-        [&](int64_t, int) {});
-    (void)bw; (void)nbw;
     removed += cur;
     round++;
-    __syncthreads();
     p ^= 1;
   }
-  if (threadIdx.x == 0) { ctl->level = k; ctl->rounds = round; }
+  for (int l = threadIdx.x; l < S; l += PEEL_BT) rnd[loc[l]] = lrnd[l];
+  if (threadIdx.x == 0) { ctl->level = k; ctl->rounds = round; ctl->t2 = globaltimer(); }
 }
 
 // order keys: (round << 32) | id

@@ -11,7 +11,8 @@ out = {"how": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --se
        "passes": {}, "kernels": {}}
 for arg in sys.argv[1:]:
     pas, rep = arg.split("=", 1)
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = (open(rep).read() if rep.endswith(".csv") else
+           subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
     rows = list(csv.reader(io.StringIO(raw)))
     h, units, v = rows[0], rows[1], rows[2]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
