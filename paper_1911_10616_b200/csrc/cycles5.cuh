@@ -60,8 +60,8 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 #define C5_WARP_MAX 1024          // light endpoint: W(l) + d(l) <= this
 #define C5_WARP_CAP 2048          // records per warp region (load <= 0.5)
 #define C5_SH_CAP 256             // light endpoints with a region of <= this many slots: shared memory
-#define C5_SH_WARP_BYTES (C5_SH_CAP * 32 + 2 * C5_SH_CAP * 4)   // records + touched + J lists
-#define C5_SH_BYTES ((C5_BT / 32) * C5_SH_WARP_BYTES)
+#define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (32 + 2 * 4))   // records + touched + J lists
+#define C5_SH_BYTES(cap) ((C5_BT / 32) * C5_SH_WARP_BYTES(cap))
 #define C5_GIANT (1ull << 40)     // endpoint work above which a thread-block cluster takes it (off)
 #define C5_HBT 1024               // heavy-endpoint CTA
 
@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
                                                     const int32_t* __restrict__ light, const u32* __restrict__ lw,
                                                     int n_light, int* __restrict__ counter,
                                                     C5RecT<u32>* __restrict__ wregions, int32_t* __restrict__ wlists,
-                                                    u64* __restrict__ C5) {
-  // endpoints whose region needs at most C5_SH_CAP slots keep records and lists in shared
+                                                    u64* __restrict__ C5, int sh_cap) {
+  // endpoints whose region needs at most sh_cap (<= C5_SH_CAP) slots keep records and lists in shared
   // memory (per warp); larger ones use the warp's global region
   extern __shared__ unsigned char c5_sh[];
   __shared__ int w_nL[C5_BT / 32], w_nJ[C5_BT / 32];
@@ -437,11 +437,11 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t gw = (size_t)blockIdx.x * (C5_BT / 32) + wib;
   WarpEng eng;
-  C5RecT<u32>* shR = reinterpret_cast<C5RecT<u32>*>(c5_sh + (size_t)wib * C5_SH_WARP_BYTES);
-  int32_t* shL = reinterpret_cast<int32_t*>(shR + C5_SH_CAP);
+  C5RecT<u32>* shR = reinterpret_cast<C5RecT<u32>*>(c5_sh + (size_t)wib * C5_SH_WARP_BYTES(sh_cap));
+  int32_t* shL = reinterpret_cast<int32_t*>(shR + sh_cap);
   {
     uint4* z = reinterpret_cast<uint4*>(shR);
-    for (int i = lane; i < (int)(C5_SH_CAP * sizeof(C5RecT<u32>) / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = lane; i < (int)(sh_cap * sizeof(C5RecT<u32>) / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
   }
   __syncwarp();
   C5Hash<C5RecT<u32>> loc;
@@ -454,10 +454,10 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
     const int32_t l = light[idx];
     const u32 cap = pow2_at_least(2u * lw[idx], 64u);  // <= C5_WARP_CAP
     int32_t* J;
-    if (cap <= C5_SH_CAP) {
+    if (cap <= (u32)sh_cap) {
       loc.R = shR;
       loc.L = shL;
-      J = shL + C5_SH_CAP;
+      J = shL + sh_cap;
     } else {
       loc.R = wregions + gw * C5_WARP_CAP;
       loc.L = wlists + gw * 2 * C5_WARP_CAP;

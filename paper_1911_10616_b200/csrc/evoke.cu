@@ -135,6 +135,7 @@ struct Ctx {
   cudaEvent_t pev[MAXJOBS][2] = {};
   int njobs = 0;
   int job_pass[MAXJOBS] = {};
+  int job_rank[MAXJOBS] = {};
   bool timing;
   // stream for job i with the priority of its rank (rank 0 = the device's greatest priority).
   // Streams are created once per (device, rank) and kept for the process lifetime: creating
@@ -754,8 +755,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaStreamSynchronize(C.st));
     auto plist = [&](int tier) { return plists + (size_t)tier * n; };
     if (getenv("EVOKE_DEBUG"))
-      fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d light %d\n", ht[PT_G64], ht[PT_G32],
-              ht[PT_G32S], ht[PT_MID], ht[PT_LIGHT]);
+      fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d small-mid %d light %d\n", ht[PT_G64],
+              ht[PT_G32], ht[PT_G32S], ht[PT_MID], ht[PT_MIDS], ht[PT_LIGHT]);
     // position maps of the hubs (h* membership in one load), within a memory budget
     int32_t* hslot = A.alloc<int32_t>(n);
     int* hcnt = A.alloc<int>(1, true);
@@ -816,6 +817,25 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         C.launches++;
       }});
     }
+    // the small-mid kernel runs on the main tier's stream, ahead of it (one more concurrent
+    // grid would take SMs from the other passes' persistent kernels)
+    std::function<void(cudaStream_t)> mids_fn;
+    if (ht[PT_MIDS] > 0) {
+      const int smem = PAIR_MIDS_CAP * 8;
+      CK(cudaFuncSetAttribute(k_pairs_mids, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      int bps = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_pairs_mids, PAIR_MIDS_BT, smem));
+      int* counter = A.alloc<int>(1, true);
+      const int32_t* pms = plist(PT_MIDS);
+      const int nms = ht[PT_MIDS];
+      const int grid = std::max(bps, 1) * SM;
+      const int qcap = 2 * PAIR_MIDS_MAX + 16384;
+      char* qmem = A.alloc<char>((size_t)grid * eng_queue_bytes(qcap));
+      mids_fn = [=, &C](cudaStream_t st) {
+        k_pairs_mids<<<grid, PAIR_MIDS_BT, smem, st>>>(g, Te, pms, nms, pest, counter, po, qmem, qcap);
+        C.launches++;
+      };
+    }
     if (ht[PT_MID] + ht[PT_LIGHT] > 0) {
       CK(cudaFuncSetAttribute(k_pairs_main, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM));
       int bps = 0;
@@ -828,9 +848,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const int qcap = 2 * PAIR_MID_MAX + 16384;
       char* qmem = A.alloc<char>((size_t)grid * eng_queue_bytes(qcap));
       jobs.push_back({P_PAIR, 3, [=, &C](cudaStream_t st) {
+        if (mids_fn) mids_fn(st);
         k_pairs_main<<<grid, PAIR_BT, PAIR_SMEM, st>>>(g, Te, pm, nmid, pli, nli, pest, counters, po, qmem, qcap);
         C.launches++;
       }});
+    } else if (mids_fn) {
+      jobs.push_back({P_PAIR, 3, mids_fn});
     }
   }
 
@@ -957,7 +980,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         const bool narrow = wmax < (1ull << 32);
         const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
         const int64_t per = (int64_t)n * (int64_t)(rec + 8);
-        int hg = (int)std::min<int64_t>(std::min<int64_t>(SM, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
+        const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: heavy-endpoint CTAs
+        const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
+        int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
         char* dense = A.alloc<char>((size_t)hg * n * rec, true);
         int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
         int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
@@ -975,14 +1000,19 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     }
     if (n5l > 0) {
       int bps = 0;
-      CK(cudaFuncSetAttribute(k_c5_light, cudaFuncAttributeMaxDynamicSharedMemorySize, C5_SH_BYTES));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_light, C5_BT, C5_SH_BYTES));
-      const int lg = std::max(1, std::min(bps, 4)) * SM;
+      const char* shc_env = getenv("EVOKE_C5_SHCAP");  // developer knob: shared records per warp
+      const int sh_cap = shc_env ? std::max(64, std::min(C5_SH_CAP, atoi(shc_env))) : C5_SH_CAP;
+      const size_t sh_bytes = C5_SH_BYTES(sh_cap);
+      CK(cudaFuncSetAttribute(k_c5_light, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_bytes));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_light, C5_BT, sh_bytes));
+      const char* lb_env = getenv("EVOKE_C5_LBPS");  // developer knob: light CTAs per SM
+      const int lg = std::max(1, std::min(bps, lb_env ? atoi(lb_env) : 4)) * SM;
       const size_t nw = (size_t)lg * (C5_BT / 32);
       C5RecT<u32>* reg = A.alloc<C5RecT<u32>>(nw * C5_WARP_CAP, true);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
-        k_c5_light<<<lg, C5_BT, C5_SH_BYTES, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out);
+        k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out,
+                                                sh_cap);
         C.launches++;
       }});
     }
@@ -1019,7 +1049,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     CK(cudaMemcpyToSymbol(g_pair_phase, z, sizeof(z)));
   }
   C.njobs = (int)jobs.size();
-  for (size_t i = 0; i < jobs.size(); i++) C.job_pass[i] = jobs[i].pass;
+  for (size_t i = 0; i < jobs.size(); i++) { C.job_pass[i] = jobs[i].pass; C.job_rank[i] = jobs[i].rank; }
 
   // ------------------------------------------------------------------ nbr gathers 2,3
   C.mark(P_NBR2);
@@ -1085,6 +1115,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       // serial: the pass's own kernels (its jobs are interleaved with other passes' jobs);
       // concurrent: the span of its kernels
       if (hi > lo) s->ms_pass[pass] += serial ? sum : hi - lo;
+    }
+    if (getenv("EVOKE_JOBS")) {  // developer trace: start / end of every concurrent job
+      std::string line;
+      for (int j = 0; j < C.njobs; j++) {
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, C.ev[0], C.pev[j][0]));
+        CK(cudaEventElapsedTime(&b, C.ev[0], C.pev[j][1]));
+        char buf[96];
+        snprintf(buf, sizeof(buf), " %s/r%d %.2f-%.2f", kPassNames[C.job_pass[j]], C.job_rank[j], a, b);
+        line += buf;
+      }
+      fprintf(stderr, "[evoke jobs]%s\n", line.c_str());
     }
     float tot = 0;
     CK(cudaEventElapsedTime(&tot, C.ev[0], C.ev[P_COUNT]));

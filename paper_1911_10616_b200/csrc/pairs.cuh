@@ -50,6 +50,9 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_MID_CAP 8192        // mid tier: packed shared hash entries (key + W|D<<16)
 #define PAIR_SMEM (PAIR_MID_CAP * 8)     // dynamic shared memory of the mid / light kernel
 #define PAIR_MID_MAX 6144        // mid tier: est <= this (load <= 0.75)
+#define PAIR_MIDS_BT 128         // small-mid tier: CTA of 4 warps per source ...
+#define PAIR_MIDS_CAP 4096       // ... with a 32 KB packed shared hash: five sources share an SM
+#define PAIR_MIDS_MAX 2048       // small-mid tier: est <= this
 #define PAIR_WARP_CAP 1024       // light tier: per-warp packed hash entries (8 warps x 8 KB)
 #define PAIR_WARP_MAX 512        // light tier: est <= this
 #define PAIR_HBT 1024            // heavy tier CTA
@@ -499,13 +502,14 @@ struct EngQueue {
   int32_t* lc0;     // first chunk of each part of the current round (+1 entry)
   int qcap;
 };
-struct EngShared {
+template <int NW>
+struct EngSharedT {
   int next;
   int qn;
   int next_chunk;
   int nchunks;
   EngQueue Q;
-  u64 acc[PAIR_HBT / 32][32];  // per-warp theta64 accumulators (chords_step)
+  u64 acc[NW][32];  // per-warp theta64 accumulators (chords_step)
 };
 // bytes of one queue region of capacity qcap
 __host__ __device__ __forceinline__ size_t eng_queue_bytes(int qcap) {
@@ -522,8 +526,9 @@ __device__ __forceinline__ EngQueue eng_queue_at(char* base, int qcap) {
   q.qcap = qcap;
   return q;
 }
+template <typename ES>
 struct CtaDefer {
-  EngShared* E;
+  ES* E;
   __device__ __forceinline__ bool operator()(int64_t r, int32_t v, bool vlo) const {
     const int q = atomicAdd(&E->qn, 1);
     if (q >= E->Q.qcap) return false;
@@ -542,9 +547,9 @@ __device__ __forceinline__ int part_len(const DGraph& g, const EngQueue& Q, int 
   return kind == PK_WEDGE ? it.dv : it.tv;
 }
 
-template <int PASS, typename Tab>
+template <int PASS, int BT, typename Tab, typename ES>
 __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs, int64_t r0, int64_t r1,
-                         Tab& tab, EngShared& E, u64& s51, const PairOut& o) {
+                         Tab& tab, ES& E, u64& s51, const PairOut& o) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   u64* acc = E.acc[wib];
   long long t_prev = clock64();
@@ -594,7 +599,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
       const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
       const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc, CtaDefer{&E});
+      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc, CtaDefer<ES>{&E});
     });
     __syncwarp();
     if (PASS == 2) {
@@ -613,7 +618,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
   const int nq = qe - qb;
   {
     // chunk table of the round: CTA-wide exclusive scan of the parts' chunk counts
-    typedef cub::BlockScan<int, PAIR_HBT> CScan;
+    typedef cub::BlockScan<int, BT> CScan;
     __shared__ typename CScan::TempStorage cscan;
     __shared__ int s_carry;
     if (threadIdx.x == 0) s_carry = 0;
@@ -622,11 +627,11 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       const int q = q0 + threadIdx.x;
       const int nc = (q < nq) ? (part_len(g, E.Q, qb + q, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
       int ex = 0, tot = 0;
-      if (blockDim.x == PAIR_HBT) {
+      if (blockDim.x == BT) {
         CScan(cscan).ExclusiveSum(nc, ex, tot);
       } else {
         // smaller CTA: warp scans chained through shared memory
-        __shared__ int wsum[PAIR_HBT / 32];
+        __shared__ int wsum[BT / 32];
         int incl = nc;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -745,7 +750,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       const int k1 = min(it.tv, k0 + PAIR_CHUNK);
       for (int i = 0; i < PAIR_CHUNK / 32; i++) {
         const int k = k0 + lane + 32 * i;
-        chords_step<PASS>(g, u, k < k1, it.v, it.fo, it.vlo, k, 0, tab, acc, CtaDefer{&E});
+        chords_step<PASS>(g, u, k < k1, it.v, it.fo, it.vlo, k, 0, tab, acc, CtaDefer<ES>{&E});
       }
       __syncwarp();
       if (PASS == 2 && lane == 0) {
@@ -921,14 +926,14 @@ __device__ __forceinline__ int32_t edge_of(const DGraph& g, int32_t u, int32_t v
 }
 
 // ---- one source on a CTA (mid and heavy tiers) ------------------------------------------
-template <int BT, typename Tab>
-__device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int32_t u, Tab& tab, EngShared& E,
+template <int BT, typename Tab, typename ES>
+__device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int32_t u, Tab& tab, ES& E,
                                 u64* red, const PairOut& o, u32 tab_keys_bound) {
   const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
   const int32_t hs = o.hstar[u];
   u64 s51 = 0;
   long long t_prev = clock64();
-  cta_pass<1>(g, Te, u, hs, r0, r1, tab, E, s51, o);
+  cta_pass<1, BT>(g, Te, u, hs, r0, r1, tab, E, s51, o);
   PAIR_PHASE(0);
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
   PairAcc H;
@@ -948,7 +953,7 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
     __syncthreads();  // W final
   }
   PAIR_PHASE(2);
-  cta_pass<2>(g, Te, u, hs, r0, r1, tab, E, s51, o);
+  cta_pass<2, BT>(g, Te, u, hs, r0, r1, tab, E, s51, o);
   PAIR_PHASE(3);
   for (int64_t s = r0 + threadIdx.x; s < r1; s += BT) {
     const u64 w = tab.get_w_or0(g.ci[s]);
@@ -1017,13 +1022,13 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
 
 // Mid and light tiers: persistent CTAs take mid sources (one CTA each, packed shared
 // hash) from mid[0, n_mid), then each warp takes light sources from light[0, n_light).
-__global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __restrict__ Te,
+__global__ void __launch_bounds__(PAIR_BT, 3) k_pairs_main(DGraph g, const u32* __restrict__ Te,
                                                         const int32_t* __restrict__ mid, int n_mid,
                                                         const int32_t* __restrict__ light, int n_light,
                                                         const u32* __restrict__ est, int* __restrict__ counters,
                                                         PairOut o, char* __restrict__ qmem, int qcap) {
   extern __shared__ int32_t sh_pairs[];
-  __shared__ EngShared E;
+  __shared__ EngSharedT<PAIR_BT / 32> E;
   __shared__ u64 red[8];
   __shared__ int s_idx;
   if (threadIdx.x < 8) red[threadIdx.x] = 0;
@@ -1068,6 +1073,36 @@ __global__ void __launch_bounds__(PAIR_BT) k_pairs_main(DGraph g, const u32* __r
   }
 }
 
+// Small-mid tier: persistent CTAs of PAIR_MIDS_BT threads take one source each (packed
+// shared hash of PAIR_MIDS_CAP entries).  Smaller CTAs than the mid tier: a source's phases
+// are latency-bound and separated by CTA barriers, so more sources in flight per SM (five
+// instead of three) hide more of the latency than more threads per source would.
+__global__ void __launch_bounds__(PAIR_MIDS_BT) k_pairs_mids(DGraph g, const u32* __restrict__ Te,
+                                                             const int32_t* __restrict__ mids, int n_mids,
+                                                             const u32* __restrict__ est, int* __restrict__ counter,
+                                                             PairOut o, char* __restrict__ qmem, int qcap) {
+  extern __shared__ int32_t sh_pairs[];
+  __shared__ EngSharedT<PAIR_MIDS_BT / 32> E;
+  __shared__ u64 red[8];
+  __shared__ int s_idx;
+  if (threadIdx.x < 8) red[threadIdx.x] = 0;
+  if (threadIdx.x == 0) E.Q = eng_queue_at(qmem + (size_t)blockIdx.x * eng_queue_bytes(qcap), qcap);
+  SharedPackedHash tab;
+  tab.keys = sh_pairs;
+  tab.val = (u32*)(sh_pairs + PAIR_MIDS_CAP);
+  for (u32 h = threadIdx.x; h < PAIR_MIDS_CAP; h += PAIR_MIDS_BT) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
+  for (;;) {
+    if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
+    __syncthreads();
+    const int idx = s_idx;
+    __syncthreads();
+    if (idx >= n_mids) break;
+    const int32_t u = mids[idx];
+    tab.mask = min(pow2_at_least(2u * est[u], 64u), (u32)PAIR_MIDS_CAP) - 1;
+    pair_source_cta<PAIR_MIDS_BT>(g, Te, u, tab, E, red, o, est[u]);  // leaves the table clean
+  }
+}
+
 // Heavy tier: one CTA per source, dense per-CTA table in global memory (Word = u32
 // packed W|D<<16, or u64 W|D<<32 for sources past the 16-bit bounds).
 template <typename Word, bool SCAN>
@@ -1076,7 +1111,7 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
                                                           int* __restrict__ counter, Word* __restrict__ tabs,
                                                           int32_t* __restrict__ lists, PairOut o,
                                                           char* __restrict__ qmem, int qcap) {
-  __shared__ EngShared E;
+  __shared__ EngSharedT<PAIR_HBT / 32> E;
   __shared__ u64 red[8];
   __shared__ int s_idx, s_ntouch;
   if (threadIdx.x == 0) E.Q = eng_queue_at(qmem + (size_t)blockIdx.x * eng_queue_bytes(qcap), qcap);
@@ -1137,7 +1172,7 @@ __global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict
 
 // Shard filter of the est-sorted (descending) vertex list and tier classification.
 // Lists keep the descending order approximately (warp-aggregated appends in list order).
-enum { PT_G64 = 0, PT_G32, PT_G32S, PT_MID, PT_LIGHT, PT_COUNT };
+enum { PT_G64 = 0, PT_G32, PT_G32S, PT_MID, PT_LIGHT, PT_MIDS, PT_COUNT };
 __global__ void k_pair_classify(DGraph g, const u64* __restrict__ skeys, const int32_t* __restrict__ svals,
                                 int si, int ns, const u64* __restrict__ Tv, u32* __restrict__ est_v,
                                 int32_t* __restrict__ lists, int* __restrict__ counts) {
@@ -1156,6 +1191,7 @@ __global__ void k_pair_classify(DGraph g, const u64* __restrict__ skeys, const i
         const bool packed_ok = dg_deg(g, u) < 65536 && Tv[u] < 65536ull;
         tier = !packed_ok ? PT_G64
              : e <= PAIR_WARP_MAX ? PT_LIGHT
+             : e <= PAIR_MIDS_MAX ? PT_MIDS
              : e <= PAIR_MID_MAX ? PT_MID
              : e * 16 >= (u64)g.n ? PT_G32S  // 2-hop set a sizeable part of n: sweep the table
              : PT_G32;

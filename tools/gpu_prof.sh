@@ -4,8 +4,10 @@
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-for k in ${PROF_KERNELS:-k_pairs_main k_c5_heavy}; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s ${PROF_SKIP:-3} -c 1 \
+# entries are NAME or NAME:SKIP (launches of NAME to skip; default PROF_SKIP or 3)
+for ks in ${PROF_KERNELS:-k_pairs_main k_c5_heavy}; do
+  k=${ks%%:*}; skip=${PROF_SKIP:-3}; [ "$k" != "$ks" ] && skip=${ks#*:}
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
      -o gpurun_out/prof_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/prof_$k.log 2>&1
   echo $k=$?
   python tools/ncu_summary.py gpurun_out/prof_$k.ncu-rep > gpurun_out/prof_$k.txt 2>&1
