@@ -189,16 +189,23 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _, st = step(stats=True)
+            step()
             e1.record(stream)
             torch.cuda.synchronize()
             barrier()
             times.append(e0.elapsed_time(e1))
-            launches += st["kernel_launches"]
-            lib_launches += st["library_launches"]
+        # per-pass times and launch counts from the same call with statistics on (untimed:
+        # the statistics add a host read after the result is complete)
+        for _ in range(min(args.steps, 3)):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            _, st = step(stats=True)
+            torch.cuda.synchronize()
             for k, v in st["ms_pass"].items():
-                pass_ms[k] = pass_ms.get(k, 0.0) + v / args.steps
+                pass_ms[k] = pass_ms.get(k, 0.0) + v / min(args.steps, 3)
             st_last = st
+        launches = st_last["kernel_launches"] * args.steps
+        lib_launches = st_last["library_launches"] * args.steps
     ms = float(np.mean(times))
     if world > 1:
         t = torch.tensor([ms], device=dev)

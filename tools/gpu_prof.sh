@@ -12,6 +12,6 @@ for ks in ${PROF_KERNELS:-k_pairs_main k_c5_heavy}; do
   echo $k=$?
   python tools/ncu_summary.py gpurun_out/prof_$k.ncu-rep > gpurun_out/prof_$k.txt 2>&1
   ncu -i gpurun_out/prof_$k.ncu-rep --page raw --csv > gpurun_out/prof_${k}_raw.csv 2>/dev/null
-  ncu -i gpurun_out/prof_$k.ncu-rep --page source --csv > gpurun_out/prof_${k}_source.csv 2>/dev/null
+  python tools/ncu_lines.py gpurun_out/prof_$k.ncu-rep ${PROF_LINES:-80} > gpurun_out/prof_${k}_lines.txt 2>&1
   [ "${KEEP_REP:-0}" = 1 ] || rm -f gpurun_out/prof_$k.ncu-rep
 done
