@@ -803,7 +803,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
                hslot, hpos};
     const size_t freeb = avail_bytes(C.dev);
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
+    const char* phg_env = getenv("EVOKE_PAIR_HG");  // developer knob: heavy-source CTAs
     auto heavy_grid = [&](int nsrc, size_t word, int cap) {
+      if (phg_env) cap = std::min(cap, std::max(1, atoi(phg_env)));
       const int64_t l2_ctas = std::max<int64_t>(1, (56ll << 20) / ((int64_t)n * (int64_t)word));
       int64_t pg = std::min<int64_t>(std::max<int64_t>(l2_ctas, SM / 2), cap);
       pg = std::min<int64_t>(pg, nsrc);
