@@ -64,6 +64,10 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 #define C5_SH_BYTES(cap) ((C5_BT / 32) * C5_SH_WARP_BYTES(cap))
 #define C5_GIANT (1ull << 40)     // endpoint work above which a thread-block cluster takes it (off)
 #define C5_HBT 1024               // heavy-endpoint CTA
+#define C5_MID_MAX 4096           // mid endpoint: C5_WARP_MAX < W(l) <= this ...
+#define C5_MID_CAP (2 * C5_MID_MAX)  // ... hashed records in a per-CTA global region (load <= 0.5)
+#define C5_MBT 128                // mid-endpoint CTA (several endpoints in flight per SM)
+#define C5_BIG_KEY (1ull << 62)   // sort-key bit of the endpoints above C5_MID_MAX
 
 // dense records indexed by vertex id; touched list holds vertex ids
 template <typename Rec>
@@ -393,7 +397,11 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
                                                     const int32_t* __restrict__ heavy, int n_heavy,
                                                     int* __restrict__ counter, C5RecT<V>* __restrict__ dense,
                                                     int32_t* __restrict__ dlists, u64* __restrict__ C5,
-                                                    int32_t* __restrict__ qmem) {
+                                                    int32_t* __restrict__ qmem, const int* __restrict__ nbig,
+                                                    int ngiant) {
+  // the list is sorted: the endpoints past C5_MID_MAX come first, *nbig of them (with the
+  // giant prefix); the rest belong to k_c5_mid
+  if (nbig) n_heavy = min(n_heavy, *nbig - ngiant);
   __shared__ ListEng E;
   if (threadIdx.x == 0) {
     E.qcap = g.max_deg;
@@ -505,6 +513,90 @@ __global__ void __cluster_dims__(C5_CLUSTER, 1, 1) __launch_bounds__(1024)
       ctl[4 * cid + 0] = 0;
       ctl[4 * cid + 1] = 0;
     }
+  }
+}
+
+// Split of the heavy endpoints: W(l) counted by a warp per endpoint, stopping past
+// C5_MID_MAX (or taken from the exact count when `exact`).  Sort key: W for the mid
+// endpoints; C5_BIG_KEY | (exact W, or d(l)^2 + the partial count) for the others, so a
+// descending sort puts the big endpoints first; *nbig counts them.
+__global__ void k_c5_split(DGraph g, const int32_t* __restrict__ heavy, int n_heavy, u64* __restrict__ keys,
+                           int exact, int* __restrict__ nbig) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = gw; q < n_heavy; q += nw) {
+    const int32_t l = heavy[q];
+    u64 w;
+    if (exact) {
+      w = keys[q];
+    } else {
+      const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
+      w = (u64)g.deg[l];
+      for (int64_t s0 = r0; s0 < r1 && w <= C5_MID_MAX; s0 += 32) {
+        const int64_t s = s0 + lane;
+        u64 c = 0;
+        if (s < r1) {
+          const int32_t x = g.ci[s];
+          c = (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
+          if (s < rm) {
+            const int64_t ok = g.orow[x], ok1 = g.orow[x + 1];
+            c += (u64)(ok1 - ok);
+            for (int64_t e = ok; e < ok1; e++) {
+              const int32_t j = g.ocol[e];
+              c += (u64)(g.orow[j + 1] - g.orow[j]);
+            }
+          }
+        }
+        w += warp_sum(c);
+      }
+    }
+    const bool big = w > C5_MID_MAX;
+    if (lane == 0) {
+      const u64 d = (u64)g.deg[l];
+      keys[q] = !big ? w : C5_BIG_KEY | min(exact ? w : d * d + w, C5_BIG_KEY - 1);
+      if (big) atomicAdd(nbig, 1);
+    }
+  }
+}
+
+// Mid endpoints (C5_WARP_MAX < W(l) <= C5_MID_MAX): one C5_MBT-thread CTA each, records in
+// a per-CTA open-addressing region of 2 x W(l) slots in global memory (the region is reused
+// endpoint after endpoint, so it stays in L2).  A 1024-thread CTA per such endpoint would
+// spend its time in barriers and dependent round trips with most warps idle.
+__global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restrict__ Tlow,
+                                                   const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
+                                                   const int32_t* __restrict__ sorted, const u64* __restrict__ keys,
+                                                   const int* __restrict__ nbig, int n_total,
+                                                   int* __restrict__ counter, C5RecT<u32>* __restrict__ regions,
+                                                   int32_t* __restrict__ rlists, u64* __restrict__ C5,
+                                                   int32_t* __restrict__ qmem) {
+  __shared__ ListEng E;
+  if (threadIdx.x == 0) {
+    E.qcap = g.max_deg;
+    E.qi = qmem + (size_t)blockIdx.x * (2 * (size_t)g.max_deg + 1);
+    E.lc0 = E.qi + g.max_deg;
+  }
+  __shared__ int s_idx, s_nL, s_nJ;
+  __shared__ u64 s_tot;
+  CtaEng eng{&E};
+  C5Hash<C5RecT<u32>> loc;
+  loc.R = regions + (size_t)blockIdx.x * C5_MID_CAP;
+  loc.L = rlists + (size_t)blockIdx.x * 2 * C5_MID_CAP;
+  loc.nL = &s_nL;
+  int32_t* J = loc.L + C5_MID_CAP;
+  const int begin = *nbig;
+  for (;;) {
+    if (threadIdx.x == 0) { s_idx = begin + atomicAdd(counter, 1); s_nL = 0; s_nJ = 0; s_tot = 0; }
+    __syncthreads();
+    const int idx = s_idx;
+    if (idx >= n_total) break;
+    const int32_t l = sorted[idx];
+    loc.mask = pow2_at_least(2u * (u32)keys[idx], 64u) - 1;  // keys[idx] = W(l) <= C5_MID_MAX
+    c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &s_nJ, &s_tot, C5);
+    if (threadIdx.x == 0 && s_tot) atomicAdd(&C5[l], s_tot);
+    c5_reset(eng, loc);
+    __syncthreads();
   }
 }
 

@@ -959,11 +959,31 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       // the exact count (and the giant-endpoint split) is needed only beyond 2^32 / with the
       // cluster path enabled.
       const u64 wbound = (u64)max_deg * ((u64)max_deg + (u64)max_out * ((u64)max_out + 1));
-      const bool exact_w = wbound >= (1ull << 32) || C5_GIANT < (1ull << 40);
+      const bool c5_hist = getenv("EVOKE_C5_HIST") != nullptr;  // developer: W histogram of heavy endpoints
+      const bool exact_w = wbound >= (1ull << 32) || C5_GIANT < (1ull << 40) || c5_hist;
       if (exact_w) {
         k_c5_heavy_w<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, c5c + 2);
         C.launches++;
       }
+      if (c5_hist) {
+        std::vector<u64> hw(n5h);
+        std::vector<int32_t> hl(n5h);
+        CK(cudaMemcpyAsync(hw.data(), c5w, sizeof(u64) * n5h, cudaMemcpyDeviceToHost, C.st));
+        CK(cudaMemcpyAsync(hl.data(), c5h, sizeof(int32_t) * n5h, cudaMemcpyDeviceToHost, C.st));
+        CK(cudaStreamSynchronize(C.st));
+        const u64 edges_[] = {2048, 4096, 8192, 16384, 65536, 1ull << 20, ~0ull};
+        u64 cnt[7] = {}, sumw[7] = {};
+        for (int q = 0; q < n5h; q++)
+          for (int b = 0; b < 7; b++)
+            if (hw[q] <= edges_[b]) { cnt[b]++; sumw[b] += hw[q]; break; }
+        for (int b = 0; b < 7; b++)
+          fprintf(stderr, "[evoke] c5 heavy W <= %llu: %llu endpoints, work %llu\n", (unsigned long long)edges_[b],
+                  (unsigned long long)cnt[b], (unsigned long long)sumw[b]);
+      }
+      // mid endpoints (W <= C5_MID_MAX) to k_c5_mid, the rest (sorted first) to k_c5_heavy
+      int* nbig_dev = c5c + 5;
+      k_c5_split<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, exact_w ? 1 : 0, nbig_dev);
+      C.launches++;
       int32_t* hs = c5h;
       u64* hkeys = nullptr;
       if (n5h > 1) {
@@ -1004,6 +1024,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         if (exact_w) {
           CK(cudaMemcpyAsync(&wmax, (n5h > 1 ? hkeys : c5w) + ngiant, sizeof(u64), cudaMemcpyDeviceToHost, C.st));
           CK(cudaStreamSynchronize(C.st));
+          wmax &= ~C5_BIG_KEY;
         }
         const bool narrow = wmax < (1ull << 32);
         const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
@@ -1015,14 +1036,31 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
         int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
         const int32_t* hsr = hs + ngiant;
+        const int ngi = ngiant;
+        // mid endpoints: several 4-warp CTAs per SM, hashed records in per-CTA regions; they run
+        // after the big endpoints on the same stream (as one more concurrent grid they would take
+        // SMs from the other passes' persistent kernels)
+        int bpm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_c5_mid, C5_MBT, 0));
+        const char* mb_env = getenv("EVOKE_C5_MBPS");  // developer knob: mid CTAs per SM
+        const int gm = std::max(1, std::min(bpm, mb_env ? atoi(mb_env) : 4)) * SM;
+        C5RecT<u32>* mreg = A.alloc<C5RecT<u32>>((size_t)gm * C5_MID_CAP, true);
+        int32_t* mlists = A.alloc<int32_t>((size_t)gm * 2 * C5_MID_CAP);
+        int32_t* mq = A.alloc<int32_t>((size_t)gm * (2 * (size_t)g.max_deg + 1));
+        const u64* mkeys = n5h > 1 ? hkeys : c5w;
+        const int32_t* hsm = hs;
+        const int n5h_ = n5h;
         jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
           if (narrow)
             k_c5_heavy<u32><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq);
+                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq,
+                                                   nbig_dev, ngi);
           else
             k_c5_heavy<u64><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out, lq);
-          C.launches++;
+                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, nbig_dev, ngi);
+          k_c5_mid<<<gm, C5_MBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsm, mkeys, nbig_dev, n5h_, c5c + 6, mreg, mlists,
+                                          C5out, mq);
+          C.launches += 2;
         }});
       }
     }
