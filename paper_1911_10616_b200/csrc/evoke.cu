@@ -895,9 +895,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* light = A.alloc<int32_t>(m2s);
     int32_t* heavy = A.alloc<int32_t>(m2s);
     u32* hest = A.alloc<u32>(m2s);
-    int* hcnt = A.alloc<int>(4, true);
-    k_hub_items<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, si, ns, light, hcnt, heavy, hest, hcnt + 1);
-    C.launches++;
+    int* hcnt = A.alloc<int>(5, true);  // n_light, n_heavy, process counters [2], [3], n_long
+    int32_t* hlong = A.alloc<int32_t>(m2s);
+    k_hub_items<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, si, ns, light, hcnt, heavy, hest, hcnt + 1, hlong,
+                                                          hcnt + 4);
+    k_hub_items_long<<<4 * SM, 256, 0, C.st>>>(g, Te, si, ns, hlong, hcnt + 4, light, hcnt, heavy, hest, hcnt + 1);
+    C.launches += 2;
     int hc[2];
     CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
@@ -1143,6 +1146,14 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   C.mark(P_COUNT);
   CK(cudaStreamSynchronize(C.st));
   CK(cudaGetLastError());
+  if (getenv("EVOKE_DEBUG")) {  // main-stream preparation time of the concurrent passes
+    float a = 0, b = 0, c = 0, d = 0;
+    CK(cudaEventElapsedTime(&a, C.ev[P_PAIR], C.ev[P_HUB]));
+    CK(cudaEventElapsedTime(&b, C.ev[P_HUB], C.ev[P_C5]));
+    CK(cudaEventElapsedTime(&c, C.ev[P_C5], C.ev[P_CLIQ2]));
+    CK(cudaEventElapsedTime(&d, C.ev[0], C.ev[P_PAIR]));
+    fprintf(stderr, "[evoke] preparations: pair %.3f hub %.3f c5 %.3f ms (stages before them %.3f ms)\n", a, b, c, d);
+  }
   if (hostprof()) {
     float gms = 0;
     CK(cudaEventElapsedTime(&gms, C.ev[0], C.ev[P_COUNT]));

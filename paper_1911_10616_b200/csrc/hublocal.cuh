@@ -47,10 +47,90 @@ __device__ __forceinline__ int64_t pos_in_list(const DGraph& g, int32_t v, int32
 }
 
 // ---- item measurement and binning ---------------------------------------------------
+#define HUB_ITEM_LONG 256  // items whose triangle list is longer are measured by k_hub_items_long
+
+// item s = slot of a in N(v): a, v, the full list of edge (v,a) and the length to walk
+struct HubItem {
+  int32_t a, v;
+  int64_t fo;
+  int len;
+  bool v_lo;
+};
+__device__ __forceinline__ HubItem hub_item(const DGraph& g, const u32* __restrict__ Te, int64_t s, int shard_index,
+                                            int num_shards) {
+  HubItem it;
+  const int32_t eva = g.eid[s];
+  it.a = g.ci[s];
+  const int32_t lo = g.esrc[eva];
+  it.v = lo + g.edst[eva] - it.a;
+  it.v_lo = lo == it.v;
+  it.fo = 0;
+  it.len = 0;
+  const u32 t = Te[eva];
+  if (t >= 2 && it.v % num_shards == shard_index) {
+    it.fo = g.foff[eva];
+    it.len = full_prefix(g, it.fo, (int)t, it.a);  // b < a
+  }
+  return it;
+}
+
+__device__ __forceinline__ void hub_bin(int64_t s, u64 est, int32_t* __restrict__ light, int* n_light,
+                                        int32_t* __restrict__ heavy, u32* __restrict__ heavy_est, int* n_heavy) {
+  if (est == 0) return;
+  if (est <= HUB_WARP_MAX) {
+    light[atomicAdd(n_light, 1)] = (int32_t)s;
+  } else {
+    const int q = atomicAdd(n_heavy, 1);
+    heavy[q] = (int32_t)s;
+    heavy_est[q] = (u32)min(est, (u64)0xffffffffu);
+  }
+}
+
+// items with more than HUB_ITEM_LONG list entries: one CTA each (a warp per such item would
+// set the measuring kernel's duration alone: hub edges carry lists of thousands)
+__global__ void __launch_bounds__(256) k_hub_items_long(DGraph g, const u32* __restrict__ Te, int shard_index,
+                                                        int num_shards, const int32_t* __restrict__ longs,
+                                                        const int* __restrict__ n_long, int32_t* __restrict__ light,
+                                                        int* n_light, int32_t* __restrict__ heavy,
+                                                        u32* __restrict__ heavy_est, int* n_heavy) {
+  __shared__ u64 red[8];
+  const int nl = *n_long;
+  for (int q = blockIdx.x; q < nl; q += gridDim.x) {
+    const int64_t s = longs[q];
+    const HubItem it = hub_item(g, Te, s, shard_index, num_shards);
+    u64 acc = 0;
+    for (int k0 = threadIdx.x; k0 < it.len; k0 += 4 * 256) {
+      int32_t x[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int k = k0 + 256 * i;
+        x[i] = k < it.len ? g.fx[it.fo + k] : it.a;
+      }
+      u32 te[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int64_t r = it.fo + k0 + 256 * i;
+        te[i] = x[i] < it.a ? Te[it.v_lo ? g.fe1[r] : g.fe2[r]] : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i++) acc += te[i];
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u64 est = 0;
+      for (int w = 0; w < 8; w++) est += red[w];
+      hub_bin(s, est, light, n_light, heavy, heavy_est, n_heavy);
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) k_hub_items(DGraph g, const u32* __restrict__ Te, int shard_index,
                                                    int num_shards, int32_t* __restrict__ light, int* n_light,
                                                    int32_t* __restrict__ heavy, u32* __restrict__ heavy_est,
-                                                   int* n_heavy) {
+                                                   int* n_heavy, int32_t* __restrict__ longs, int* n_long) {
   __shared__ u64 acc[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -76,6 +156,9 @@ __global__ void __launch_bounds__(256) k_hub_items(DGraph g, const u32* __restri
         len = full_prefix(g, fo, (int)t, a);  // b < a
       }
     }
+    const bool is_long = len > HUB_ITEM_LONG;
+    warp_append(is_long, (int32_t)s, longs, n_long);
+    if (is_long) len = 0;
     int cur = -1;
     u64 cacc = 0;
     warp_flat(len, [&](int j, int k, bool valid) {

@@ -142,10 +142,13 @@ def test_sharded_partials_sum_to_full(pkg):
 
 
 def test_deterministic(pkg):
+    """Repeated calls are bit-identical (exact integer sums; any schedule).  Several repeats:
+    a work-list or counter race shows up as an occasional difference, not on every call."""
     g = graphgen.config(2)
     a = pkg.evoke_orbits_edges(g.n, g.edges)
-    b = pkg.evoke_orbits_edges(g.n, g.edges)
-    _assert_equal(a, b, "repeat")
+    for r in range(8):
+        b = pkg.evoke_orbits_edges(g.n, g.edges, serial=(r % 4 == 3))
+        _assert_equal(b, a, f"repeat {r}")
 
 
 # ---------------------------------------------------------- closed forms at scale ---
