@@ -81,6 +81,76 @@ static const char* kPassNames[] = {
 enum { P_H2D = 0, P_CANON, P_KCORE, P_CSR, P_TRI, P_TRILIST, P_CLIQ, P_NBR1, P_PAIR, P_HUB, P_C5,
        P_CLIQ2, P_NBR2, P_TRIG, P_COMB, P_D2H, P_COUNT };
 
+// ---- zero-invariant scratch, kept between calls --------------------------------------
+// The per-CTA tables of the pair, hub-local and 5-cycle passes start zeroed and every kernel
+// that uses them resets what it touched before it finishes (touched lists / sweeps), so at
+// the end of a successful call they are all zero again.  One buffer per device keeps them
+// between calls: a call leases it (exclusively; a concurrent call on the same device falls
+// back to fresh zeroed allocations), carves its tables out of it, and the next call skips
+// the memsets (≈ 0.9 GB at config 2).  A call that fails leaves the buffer marked dirty and
+// the next lease zeroes it again; a call that needed more than the buffer holds got fresh
+// allocations for the rest, and the next lease grows the buffer to that size.
+struct ZeroPool {
+  std::mutex mu;
+  char* p = nullptr;
+  size_t bytes = 0;
+  size_t target = 0;
+  bool dirty = false;
+};
+ZeroPool& zero_pool(int dev) {
+  static ZeroPool pools[64];
+  if (dev < 0 || dev >= 64) { set_error("device ordinal out of range"); throw EvokeError{EVOKE_EINTERNAL}; }
+  return pools[dev];
+}
+struct ZeroLease {
+  ZeroPool* zp = nullptr;
+  size_t used = 0, need = 0;
+  bool ok = false;  // set when the call completed (the tables are zero again)
+  void acquire(int dev, cudaStream_t st) {
+    ZeroPool& z = zero_pool(dev);
+    if (std::getenv("EVOKE_NO_ZERO_POOL") || !z.mu.try_lock()) return;
+    zp = &z;
+    if (z.target > z.bytes) {
+      if (z.p) CK(cudaFreeAsync(z.p, st));
+      z.p = nullptr;
+      z.bytes = 0;
+      void* q = nullptr;
+      if (cudaMallocAsync(&q, z.target, st) != cudaSuccess) {
+        (void)cudaGetLastError();
+        z.target = 0;
+        return;
+      }
+      z.p = (char*)q;
+      z.bytes = z.target;
+      z.dirty = true;
+    }
+    if (z.dirty && z.p) {
+      CK(cudaMemsetAsync(z.p, 0, z.bytes, st));
+      z.dirty = false;
+    }
+  }
+  // zeroed region of `bytes` from the lease, or nullptr (the caller allocates)
+  void* take(size_t bytes) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    need += bytes;
+    if (!zp || !zp->p || used + bytes > zp->bytes) return nullptr;
+    void* q = zp->p + used;
+    used += bytes;
+    return q;
+  }
+  ~ZeroLease() {
+    if (!zp) return;
+    if (!ok) {
+      // a failed call may leave kernels writing into the buffer on any of its streams
+      (void)cudaDeviceSynchronize();
+      (void)cudaGetLastError();
+      zp->dirty = true;
+    }
+    if (need > zp->target) zp->target = need;
+    zp->mu.unlock();
+  }
+};
+
 // Device allocations of one call; everything is freed (stream-ordered) at the end.
 struct Arena {
   cudaStream_t st;
@@ -111,6 +181,17 @@ struct Arena {
     ptrs.push_back(p);
     if (zero) CK(cudaMemsetAsync(p, 0, bytes, s));
     return (T*)p;
+  }
+  ZeroLease* lease = nullptr;
+  // zero-invariant table (see ZeroPool): from the lease when it has room, else a fresh
+  // zeroed allocation
+  template <typename T>
+  T* zalloc(size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (lease) {
+      if (void* q = lease->take(bytes)) return (T*)q;
+    }
+    return alloc<T>(count, true);
   }
   void release(void* p) {
     for (auto& q : ptrs)
@@ -163,6 +244,30 @@ struct Ctx {
   }
   std::chrono::steady_clock::time_point hts[P_COUNT + 1];
   bool hset[P_COUNT + 1] = {};
+  // developer timeline (EVOKE_TICKS=1): named events on the main stream, printed at the end
+  std::vector<std::pair<const char*, cudaEvent_t>> ticks;
+  void tick(const char* what) {
+    static const bool on = std::getenv("EVOKE_TICKS") != nullptr;
+    if (!on) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, st));
+    ticks.emplace_back(what, e);
+  }
+  void print_ticks() {
+    if (ticks.empty()) return;
+    std::string line;
+    for (size_t i = 1; i < ticks.size(); i++) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ticks[i - 1].second, ticks[i].second));
+      char b[96];
+      snprintf(b, sizeof(b), " %s %.3f", ticks[i].first, ms);
+      line += b;
+    }
+    for (auto& t : ticks) cudaEventDestroy(t.second);
+    ticks.clear();
+    fprintf(stderr, "[evoke ticks]%s\n", line.c_str());
+  }
   void mark(int pass) {
     if (timing) CK(cudaEventRecord(ev[pass], st));
     if (hostprof()) { hts[pass] = std::chrono::steady_clock::now(); hset[pass] = true; }
@@ -276,6 +381,13 @@ __global__ void k_max_diff_i64(const int64_t* __restrict__ a, int64_t n, int* ou
   for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(FULL_MASK, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
+// EVOKE_CHECK_ZERO: flag any nonzero 16-byte word of a zero-invariant region
+__global__ void k_check_zero(const uint4* __restrict__ p, size_t n16, int* flag) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 q = p[i];
+    if (q.x | q.y | q.z | q.w) { *flag = 1; return; }
+  }
+}
 // wedge total W(G) = sum C(d,2)
 __global__ void k_wedges(const int64_t* __restrict__ rp, int32_t n, u64* out) {
   u64 s = 0;
@@ -366,6 +478,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   }
 
   Arena A(C.st);
+  ZeroLease lease;  // destroyed before A (its buffer is not A's)
+  lease.acquire(dev, C.st);
+  A.lease = &lease;
   const int32_t n = (int32_t)in.n;
   const int B = 256;
   const int SM = C.num_sms;
@@ -758,6 +873,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   struct Job { int pass; int rank; std::function<void(cudaStream_t)> fn; };
   std::vector<Job> jobs;  // rank: launch order / stream priority (long single-item tails first)
   C.mark(P_PAIR);
+  C.tick("start");
   if (n > 0 && m > 0) {
     // source lists by 2-hop estimate (descending), sharded by position, split in tiers
     u64* pk = A.alloc<u64>(n);
@@ -769,16 +885,19 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int* tiers = A.alloc<int>(8, true);
     int32_t* hstar = A.alloc<int32_t>(n);
     k_pair_est<<<warp_grid, B, 0, C.st>>>(g, pk, pv, hstar);
+    C.tick("pair_est");
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
     void* t = A.alloc<char>(tb);
     CK(cub::DeviceRadixSort::SortPairs(t, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
+    C.tick("pair_sort");
     k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, Fp(F_T), pest, plists, tiers);
     C.launches += 2;
     C.lib_launches += 4;
     int ht[PT_COUNT];
     CK(cudaMemcpyAsync(ht, tiers, sizeof(ht), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
+    C.tick("pair_classify+sync");
     auto plist = [&](int tier) { return plists + (size_t)tier * n; };
     if (getenv("EVOKE_DEBUG"))
       fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d small-mid %d light %d\n", ht[PT_G64],
@@ -815,7 +934,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (ht[PT_G64] > 0) {
       // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables
       const int pg = heavy_grid(ht[PT_G64], 8, SM / 2);
-      u64* tabs = A.alloc<u64>((size_t)pg * (size_t)((n + 1) / 2 * 2), true);
+      u64* tabs = A.zalloc<u64>((size_t)pg * (size_t)((n + 1) / 2 * 2));
       int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(PT_G64);
@@ -830,7 +949,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     for (int tier : {PT_G32S, PT_G32}) {
       if (ht[tier] == 0) continue;
       const int pg = heavy_grid(ht[tier], 4, SM);
-      u32* tabs = A.alloc<u32>((size_t)pg * (size_t)((n + 3) / 4 * 4), true);
+      u32* tabs = A.zalloc<u32>((size_t)pg * (size_t)((n + 3) / 4 * 4));
       int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * n) : nullptr;
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(tier);
@@ -890,6 +1009,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // the 5-vertex gathers are skipped, as in the paper's EVOKE-4, Table 1)
   const bool four = (o.flags & EVOKE_FLAG_FOUR) != 0;
   C.mark(P_HUB);
+  C.tick("pair_rest");
   if (ntri > 0 && !four) {
     const int64_t m2s = 2 * m;
     int32_t* light = A.alloc<int32_t>(m2s);
@@ -904,6 +1024,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int hc[2];
     CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
+    C.tick("hub_items+sync");
     const int n_light = hc[0], n_heavy = hc[1];
     if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] hub items: light %d heavy %d\n", n_light, n_heavy);
     int32_t* heavy_sorted = heavy;
@@ -925,7 +1046,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       u32* gt = nullptr;
       int32_t* gl = nullptr;
       if (g.max_deg > HUB_SH_DENSE && n_heavy > 0) {
-        gt = A.alloc<u32>((size_t)hg * g.max_deg, true);
+        gt = A.zalloc<u32>((size_t)hg * g.max_deg);
         gl = A.alloc<int32_t>((size_t)hg * g.max_deg);
       }
       u64* r68 = Fp(F_R68);
@@ -940,6 +1061,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
 
   // ------------------------------------------------------------------ a10: 5-cycles
   C.mark(P_C5);
+  C.tick("hub_rest");
   if (n > 0 && m > 0 && !four) {
     int32_t* c5l = A.alloc<int32_t>(n);
     int32_t* c5h = A.alloc<int32_t>(n);
@@ -952,6 +1074,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int hc5[2];
     CK(cudaMemcpyAsync(hc5, c5c, sizeof(hc5), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
+    C.tick("c5_items+sync");
     const int n5l = hc5[0], n5h = hc5[1];
     if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d heavy %d\n", n5l, n5h);
     if (n5h > 0) {
@@ -1035,7 +1158,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: heavy-endpoint CTAs
         const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
         int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
-        char* dense = A.alloc<char>((size_t)hg * n * rec, true);
+        char* dense = A.zalloc<char>((size_t)hg * n * rec);
         int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
         int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
         const int32_t* hsr = hs + ngiant;
@@ -1047,7 +1170,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_c5_mid, C5_MBT, 0));
         const char* mb_env = getenv("EVOKE_C5_MBPS");  // developer knob: mid CTAs per SM
         const int gm = std::max(1, std::min(bpm, mb_env ? atoi(mb_env) : 4)) * SM;
-        C5RecT<u32>* mreg = A.alloc<C5RecT<u32>>((size_t)gm * C5_MID_CAP, true);
+        C5RecT<u32>* mreg = A.zalloc<C5RecT<u32>>((size_t)gm * C5_MID_CAP);
         int32_t* mlists = A.alloc<int32_t>((size_t)gm * 2 * C5_MID_CAP);
         int32_t* mq = A.alloc<int32_t>((size_t)gm * (2 * (size_t)g.max_deg + 1));
         const u64* mkeys = n5h > 1 ? hkeys : c5w;
@@ -1077,7 +1200,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const char* lb_env = getenv("EVOKE_C5_LBPS");  // developer knob: light CTAs per SM
       const int lg = std::max(1, std::min(bps, lb_env ? atoi(lb_env) : 4)) * SM;
       const size_t nw = (size_t)lg * (C5_BT / 32);
-      C5RecT<u32>* reg = A.alloc<C5RecT<u32>>(nw * C5_WARP_CAP, true);
+      C5RecT<u32>* reg = A.zalloc<C5RecT<u32>>(nw * C5_WARP_CAP);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
         k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out,
@@ -1092,6 +1215,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
 
   // ------------------------------------------------------------------ concurrent launch
   C.mark(P_CLIQ2);
+  C.tick("c5_rest");
   // one stream per job (jobs of one pass stay in order on a shared stream when they must:
   // the heavy and main pair kernels write different sources, so all jobs are independent)
   std::stable_sort(jobs.begin(), jobs.end(), [](const Job& x, const Job& y) { return x.rank < y.rank; });
@@ -1146,6 +1270,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   C.mark(P_COUNT);
   CK(cudaStreamSynchronize(C.st));
   CK(cudaGetLastError());
+  lease.ok = true;  // every pass has reset its tables
+  if (lease.zp && lease.used > 0 && getenv("EVOKE_CHECK_ZERO")) {
+    int* flag = A.alloc<int>(1, true);
+    k_check_zero<<<4 * SM, 256, 0, C.st>>>((const uint4*)lease.zp->p, lease.used / 16, flag);
+    if (d2h_scalar<int>(flag, C.st)) {
+      lease.ok = false;
+      set_error("a pass left its scratch table nonzero (EVOKE_CHECK_ZERO)");
+      throw EvokeError{EVOKE_EINTERNAL};
+    }
+  }
+  C.print_ticks();
   if (getenv("EVOKE_DEBUG")) {  // main-stream preparation time of the concurrent passes
     float a = 0, b = 0, c = 0, d = 0;
     CK(cudaEventElapsedTime(&a, C.ev[P_PAIR], C.ev[P_HUB]));

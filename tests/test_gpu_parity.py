@@ -351,3 +351,21 @@ def test_sorted_full_lists_path(pkg, monkeypatch):
         _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name + " sorted")
     for g in (graphgen.config(1), graphgen.complete(9)):
         _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), g.name + " sorted")
+
+
+def test_scratch_tables_left_zero(pkg, monkeypatch):
+    """The per-CTA tables kept between calls (zero-invariant scratch) are all zero again after
+    every call: EVOKE_CHECK_ZERO makes the library verify it and fail otherwise.  Runs the
+    paths that use them: heavy pair sources (dense and swept tables), hub-local heavy items,
+    5-cycle big / mid / light endpoints, on graphs with hubs."""
+    monkeypatch.setenv("EVOKE_CHECK_ZERO", "1")
+    first = None
+    for g in [graphgen.config(2), graphgen.rmat(15, 16, 0.57, 0.19, 0.19, 0.05, 9)]:
+        a = pkg.evoke_orbits_edges(g.n, g.edges)
+        b = pkg.evoke_orbits_edges(g.n, g.edges, serial=True)
+        _assert_equal(b, a, f"{g.name} after reuse")
+        first = a if first is None else first
+    monkeypatch.setenv("EVOKE_NO_ZERO_POOL", "1")
+    g = graphgen.config(2)
+    c = pkg.evoke_orbits_edges(g.n, g.edges)
+    _assert_equal(c, first, "fresh zeroed tables")
