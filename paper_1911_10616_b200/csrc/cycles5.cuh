@@ -76,11 +76,18 @@ struct C5Dense {
   Rec* R;
   int32_t* L;
   int* nL;
-  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
+  // old = the flags before; word = the whole wf word before (its Wn bits are unchanged by
+  // the Or, so callers that need Wn take it from here instead of loading it again)
+  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old, u32& word) {
     Rec* r = &R[x];
-    old = atomicOr(&r->wf, (bits | C5_PRESENT) << 28) >> 28;
+    word = atomicOr(&r->wf, (bits | C5_PRESENT) << 28);
+    old = word >> 28;
     append_active(!(old & C5_PRESENT), x, L, nL);
     return r;
+  }
+  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
+    u32 word;
+    return mark(x, bits, old, word);
   }
   __device__ __forceinline__ Rec* peek(int32_t x) const { return &R[x]; }
   __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
@@ -98,7 +105,7 @@ struct C5Hash {
   int32_t* L;
   int* nL;
   __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) >> 7 & mask; }
-  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
+  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old, u32& word) {
     u32 h = h0(x);
     for (;;) {
       const int32_t k = R[h].key;
@@ -110,9 +117,14 @@ struct C5Hash {
       h = (h + 1) & mask;
     }
     Rec* r = &R[h];
-    old = atomicOr(&r->wf, (bits | C5_PRESENT) << 28) >> 28;
+    word = atomicOr(&r->wf, (bits | C5_PRESENT) << 28);
+    old = word >> 28;
     append_active(!(old & C5_PRESENT), (int32_t)h, L, nL);
     return r;
+  }
+  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
+    u32 word;
+    return mark(x, bits, old, word);
   }
   __device__ __forceinline__ Rec* peek(int32_t x) const {
     u32 h = h0(x);
@@ -132,6 +144,7 @@ struct C5Hash {
 
 // Engine adaptors: warp (light endpoints) and CTA (heavy endpoints)
 struct WarpEng {
+  static constexpr bool kCta = false;
   __device__ __forceinline__ void sync() const { __syncwarp(); }
   __device__ __forceinline__ int tid() const { return threadIdx.x & 31; }
   __device__ __forceinline__ int nthr() const { return 32; }
@@ -139,6 +152,7 @@ struct WarpEng {
   __device__ __forceinline__ void lists(int n, I info, E elem, F flush) const { warp_lists(n, info, elem, flush); }
 };
 struct CtaEng {
+  static constexpr bool kCta = true;
   ListEng* E;
   __device__ __forceinline__ void sync() const { __syncthreads(); }
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
@@ -152,6 +166,7 @@ struct CtaEng {
 // steps are separated by hardware cluster barriers (records and counters in global memory)
 #define C5_CLUSTER 8
 struct ClusterEng {
+  static constexpr bool kCta = false;
   __device__ __forceinline__ void sync() const { cooperative_groups::this_cluster().sync(); }
   __device__ __forceinline__ int tid() const {
     return (int)(cooperative_groups::this_cluster().block_rank() * blockDim.x + threadIdx.x);
@@ -176,6 +191,18 @@ struct ClusterEng {
 template <typename R>
 __device__ __forceinline__ bool c5_adj(const R* r) { return r && (c5_flags(r) & C5_ADJ); }
 
+// developer step timers (EVOKE_DEBUG): SM cycles of thread 0 per step, summed over the
+// endpoints of the CTA engines ([0] heavy 1024-thread CTAs, [1] mid CTAs)
+__device__ unsigned long long g_c5_phase[2][8];
+#define C5_PHASE(i)                                                                              \
+  do {                                                                                           \
+    if (Eng::kCta && threadIdx.x == 0) {                                                         \
+      const long long t_ = clock64();                                                            \
+      atomicAdd(&g_c5_phase[blockDim.x == C5_HBT ? 0 : 1][i], (unsigned long long)(t_ - t_prev)); \
+      t_prev = t_;                                                                               \
+    }                                                                                            \
+  } while (0)
+
 // One endpoint l.  J: list of j-keys (counter *nJ); tot: per-engine shared u64 (zeroed).
 template <typename Eng, typename Loc>
 __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const u32* __restrict__ Tmid,
@@ -184,6 +211,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
   const int64_t r0 = g.rp[l];
   const int dl = g.deg[l];
   const int dml = g.dm[l];
+  long long t_prev = clock64();
   // ---- step 0: neighbours of l
   for (int t = eng.tid(); t < dl; t += eng.nthr()) {
     u32 old;
@@ -201,6 +229,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
     base = g.orow[k];
     len = (int)(g.orow[k + 1] - base);
   };
+  C5_PHASE(0);
   // ---- step 1: Wn over non-in-in wedges (i, w, l)
   eng.lists(dl, winfo,
       [&](int, int64_t base, int k) -> u64 {
@@ -212,6 +241,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         return 0;
       },
       [&](int, u64) {});
+  C5_PHASE(1);
   // ---- step 2: Q, QT, QM over out-out wedges j <- k -> l
   eng.lists(dml, kinfo,
       [&](int, int64_t base, int k) -> u64 {
@@ -229,6 +259,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       },
       [&](int, u64) {});
   eng.sync();
+  C5_PHASE(2);
   // ---- step 3: paths through j: P, A (to i), S and the j credits
   const int nj = *nJ;
   eng.lists(nj,
@@ -244,11 +275,11 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         typedef decltype(rj->Q) V;
         const V q = rj->Q;
         const bool adjj = c5_flags(rj) & C5_ADJ;
-        u32 old;
-        auto* ri = loc.mark(i, C5_I, old);
+        u32 old, word;
+        auto* ri = loc.mark(i, C5_I, old, word);
         atomicAdd(&ri->P, q);
         if (adjj) atomicAdd(&ri->A, q);
-        return c5_wn(ri);  // Wn is final after step 1
+        return (u64)(word & C5_WN_MASK);  // Wn is final after step 1 (and untouched by the Or)
       },
       [&](int t, u64 s) {
         auto* rj = loc.peek(J[t]);
@@ -268,6 +299,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
     if (c) atomicAdd(&C5[j], (u64)0 - c);
   }
   eng.sync();
+  C5_PHASE(3);
   // ---- step 4: k credits
   eng.lists(dml, kinfo,
       [&](int, int64_t base, int k) -> u64 {
@@ -281,6 +313,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         return (u64)rj->S - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[e] - lj);
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
+  C5_PHASE(4);
   // ---- step 5: i credits (and their sum for l)
   {
     const int nt = *loc.nL;
@@ -299,6 +332,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
     acc = warp_sum(acc);
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(tot, acc);
   }
+  C5_PHASE(5);
   // ---- step 6: wedge centres w
   eng.lists(dl, winfo,
       [&](int t, int64_t base, int k) -> u64 {
@@ -313,6 +347,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
   eng.sync();
+  C5_PHASE(6);
 }
 
 // reset every touched record (and the counters) of one endpoint

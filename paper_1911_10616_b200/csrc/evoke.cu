@@ -876,8 +876,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   C.tick("start");
   if (n > 0 && m > 0) {
     // source lists by 2-hop estimate (descending), sharded by position, split in tiers
-    u64* pk = A.alloc<u64>(n);
-    u64* pk2 = A.alloc<u64>(n);
+    u32* pk = A.alloc<u32>(n);
+    u32* pk2 = A.alloc<u32>(n);
     int32_t* pv = A.alloc<int32_t>(n);
     int32_t* pv2 = A.alloc<int32_t>(n);
     u32* pest = A.alloc<u32>(n);
@@ -887,9 +887,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     k_pair_est<<<warp_grid, B, 0, C.st>>>(g, pk, pv, hstar);
     C.tick("pair_est");
     size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 32, C.st));
     void* t = A.alloc<char>(tb);
-    CK(cub::DeviceRadixSort::SortPairs(t, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 64, C.st));
+    CK(cub::DeviceRadixSort::SortPairs(t, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 32, C.st));
     C.tick("pair_sort");
     k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, Fp(F_T), pest, plists, tiers);
     C.launches += 2;
@@ -1241,6 +1241,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
               ph[t][5] / 1e6, ph[t][6] / 1e6);
     unsigned long long z[2][8] = {};
     CK(cudaMemcpyToSymbol(g_pair_phase, z, sizeof(z)));
+    unsigned long long c5p[2][8];
+    CK(cudaMemcpyFromSymbol(c5p, g_c5_phase, sizeof(c5p)));
+    for (int t = 0; t < 2; t++)
+      fprintf(stderr, "[evoke] c5 %s steps (Mcycles): s0 %.1f s1 %.1f s2 %.1f s3 %.1f s4 %.1f s5 %.1f s6 %.1f\n",
+              t ? "mid" : "heavy", c5p[t][0] / 1e6, c5p[t][1] / 1e6, c5p[t][2] / 1e6, c5p[t][3] / 1e6,
+              c5p[t][4] / 1e6, c5p[t][5] / 1e6, c5p[t][6] / 1e6);
+    CK(cudaMemcpyToSymbol(g_c5_phase, z, sizeof(z)));
   }
   C.njobs = (int)jobs.size();
   for (size_t i = 0; i < jobs.size(); i++) { C.job_pass[i] = jobs[i].pass; C.job_rank[i] = jobs[i].rank; }

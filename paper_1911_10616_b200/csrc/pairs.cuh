@@ -1137,7 +1137,7 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
 
 // 2-hop estimate without the heaviest neighbour h*: est(u) = sum_{v in N(u), v != h*} d(v)
 // - d(u) + 1 = the number of wedge elements walked (>= the number of table keys).
-__global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict__ vals,
+__global__ void k_pair_est(DGraph g, u32* __restrict__ keys, int32_t* __restrict__ vals,
                            int32_t* __restrict__ hstar) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1162,7 +1162,7 @@ __global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict
     if (lane == 0) {
       const u64 du = (u64)dg_deg(g, u);
       const u64 est = du > 0 ? s - (u64)bestd - du + 1 : 0;
-      keys[u] = ~est;  // ascending sort = descending estimate
+      keys[u] = ~(u32)min(est, (u64)0xffffffffu);  // ascending sort = descending estimate (est <= 2m < 2^31)
       vals[u] = u;
       hstar[u] = best;
     }
@@ -1173,7 +1173,7 @@ __global__ void k_pair_est(DGraph g, u64* __restrict__ keys, int32_t* __restrict
 // Shard filter of the est-sorted (descending) vertex list and tier classification.
 // Lists keep the descending order approximately (warp-aggregated appends in list order).
 enum { PT_G64 = 0, PT_G32, PT_G32S, PT_MID, PT_LIGHT, PT_MIDS, PT_COUNT };
-__global__ void k_pair_classify(DGraph g, const u64* __restrict__ skeys, const int32_t* __restrict__ svals,
+__global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const int32_t* __restrict__ svals,
                                 int si, int ns, const u64* __restrict__ Tv, u32* __restrict__ est_v,
                                 int32_t* __restrict__ lists, int* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
@@ -1185,7 +1185,7 @@ __global__ void k_pair_classify(DGraph g, const u64* __restrict__ skeys, const i
     int32_t u = 0;
     if (p < g.n && p % ns == si) {
       u = svals[p];
-      const u64 e = ~skeys[p];
+      const u64 e = (u64)(u32)~skeys[p];
       est_v[u] = (u32)min(e, (u64)0xffffffffu);
       if (e > 0) {
         const bool packed_ok = dg_deg(g, u) < 65536 && Tv[u] < 65536ull;
