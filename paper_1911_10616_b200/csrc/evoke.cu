@@ -1015,11 +1015,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* light = A.alloc<int32_t>(m2s);
     int32_t* heavy = A.alloc<int32_t>(m2s);
     u32* hest = A.alloc<u32>(m2s);
-    int* hcnt = A.alloc<int>(5, true);  // n_light, n_heavy, process counters [2], [3], n_long
-    int32_t* hlong = A.alloc<int32_t>(m2s);
-    k_hub_items<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, si, ns, light, hcnt, heavy, hest, hcnt + 1, hlong,
-                                                          hcnt + 4);
-    k_hub_items_long<<<4 * SM, 256, 0, C.st>>>(g, Te, si, ns, hlong, hcnt + 4, light, hcnt, heavy, hest, hcnt + 1);
+    int* hcnt = A.alloc<int>(4, true);  // n_light, n_heavy, process counters [2], [3]
+    u64* hitem_est = A.alloc<u64>(m2s, true);
+    if (ntri > 0)
+      k_hub_est<<<grid_for(ntri, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est);
+    k_hub_bin<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est, si, ns, light, hcnt, heavy, hest,
+                                                        hcnt + 1);
     C.launches += 2;
     int hc[2];
     CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));

@@ -15,9 +15,9 @@
 //   v       : C(c(x), 2)                (theta69)  -- no division modulo 2^64 needed.
 // Restricting to cycles whose top is a (Chiba-Nishizeki) is what bounds the work.
 //
-// Scheduling (B200): k_hub_items measures every item's inner work
+// Scheduling (B200): k_hub_est measures every item's inner work
 //   est(v,a) = sum_{b in tri(v,a), b<a} T(v,b)
-// (warp-flattened over the triangle lists) and splits the items into a heavy list
+// (one thread per triangle) and k_hub_bin splits the items into a heavy list
 // (est > HUB_WARP_MAX, sorted by est, descending) and a light list.  k_hub_process is
 // persistent: its CTAs first take heavy items one CTA per item (block-flattened (b, x)
 // loop, c(x) in a dense shared table indexed by x's position in N(v), or a per-CTA
@@ -47,144 +47,41 @@ __device__ __forceinline__ int64_t pos_in_list(const DGraph& g, int32_t v, int32
 }
 
 // ---- item measurement and binning ---------------------------------------------------
-#define HUB_ITEM_LONG 256  // items whose triangle list is longer are measured by k_hub_items_long
-
-// item s = slot of a in N(v): a, v, the full list of edge (v,a) and the length to walk
-struct HubItem {
-  int32_t a, v;
-  int64_t fo;
-  int len;
-  bool v_lo;
-};
-__device__ __forceinline__ HubItem hub_item(const DGraph& g, const u32* __restrict__ Te, int64_t s, int shard_index,
-                                            int num_shards) {
-  HubItem it;
-  const int32_t eva = g.eid[s];
-  it.a = g.ci[s];
-  const int32_t lo = g.esrc[eva];
-  it.v = lo + g.edst[eva] - it.a;
-  it.v_lo = lo == it.v;
-  it.fo = 0;
-  it.len = 0;
-  const u32 t = Te[eva];
-  if (t >= 2 && it.v % num_shards == shard_index) {
-    it.fo = g.foff[eva];
-    it.len = full_prefix(g, it.fo, (int)t, it.a);  // b < a
-  }
-  return it;
-}
-
-__device__ __forceinline__ void hub_bin(int64_t s, u64 est, int32_t* __restrict__ light, int* n_light,
-                                        int32_t* __restrict__ heavy, u32* __restrict__ heavy_est, int* n_heavy) {
-  if (est == 0) return;
-  if (est <= HUB_WARP_MAX) {
-    light[atomicAdd(n_light, 1)] = (int32_t)s;
-  } else {
-    const int q = atomicAdd(n_heavy, 1);
-    heavy[q] = (int32_t)s;
-    heavy_est[q] = (u32)min(est, (u64)0xffffffffu);
+// est(v,a) = sum_{b in tri(v,a), b<a} T(v,b) summed per triangle instead of per item: a
+// triangle a<b<c (ranks) has a third vertex below the item's far end exactly for the items
+// (a,c) [b<c], (b,c) [a<c] and (c,b) [a<b], which receive T(a,b), T(b,a) and T(c,a).  One
+// thread per triangle, three atomics: balanced however heavy-tailed the lists are (a warp
+// per item would leave the hub edges' thousands of entries to single warps).
+__global__ void k_hub_est(DGraph g, const u32* __restrict__ Te, u64* __restrict__ est) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.ntri;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t eab = g.tab[q], eac = g.tac[q], ebc = g.tbc[q];
+    const u64 tab_ = Te[eab], tac_ = Te[eac];
+    atomicAdd((unsigned long long*)&est[slot_of_hi_in_lo(g, eac)], tab_);  // item (a, c)
+    atomicAdd((unsigned long long*)&est[slot_of_hi_in_lo(g, ebc)], tab_);  // item (b, c)
+    atomicAdd((unsigned long long*)&est[g.eslot_hi[ebc]], tac_);          // item (c, b)
   }
 }
 
-// items with more than HUB_ITEM_LONG list entries: one CTA each (a warp per such item would
-// set the measuring kernel's duration alone: hub edges carry lists of thousands)
-__global__ void __launch_bounds__(256) k_hub_items_long(DGraph g, const u32* __restrict__ Te, int shard_index,
-                                                        int num_shards, const int32_t* __restrict__ longs,
-                                                        const int* __restrict__ n_long, int32_t* __restrict__ light,
-                                                        int* n_light, int32_t* __restrict__ heavy,
-                                                        u32* __restrict__ heavy_est, int* n_heavy) {
-  __shared__ u64 red[8];
-  const int nl = *n_long;
-  for (int q = blockIdx.x; q < nl; q += gridDim.x) {
-    const int64_t s = longs[q];
-    const HubItem it = hub_item(g, Te, s, shard_index, num_shards);
-    u64 acc = 0;
-    for (int k0 = threadIdx.x; k0 < it.len; k0 += 4 * 256) {
-      int32_t x[4];
-#pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int k = k0 + 256 * i;
-        x[i] = k < it.len ? g.fx[it.fo + k] : it.a;
-      }
-      u32 te[4];
-#pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int64_t r = it.fo + k0 + 256 * i;
-        te[i] = x[i] < it.a ? Te[it.v_lo ? g.fe1[r] : g.fe2[r]] : 0u;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; i++) acc += te[i];
-    }
-    acc = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      u64 est = 0;
-      for (int w = 0; w < 8; w++) est += red[w];
-      hub_bin(s, est, light, n_light, heavy, heavy_est, n_heavy);
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(256) k_hub_items(DGraph g, const u32* __restrict__ Te, int shard_index,
-                                                   int num_shards, int32_t* __restrict__ light, int* n_light,
-                                                   int32_t* __restrict__ heavy, u32* __restrict__ heavy_est,
-                                                   int* n_heavy, int32_t* __restrict__ longs, int* n_long) {
-  __shared__ u64 acc[8][32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// items (slot s of a in N(v)) with T(v,a) >= 2 and est > 0, of this shard (v mod shards):
+// light (est <= HUB_WARP_MAX) or heavy (with est for the sort)
+__global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __restrict__ est, int shard_index,
+                          int num_shards, int32_t* __restrict__ light, int* n_light, int32_t* __restrict__ heavy,
+                          u32* __restrict__ heavy_est, int* n_heavy) {
+  const int lane = threadIdx.x & 31;
   const int64_t m2 = 2 * g.m;
-  acc[wib][lane] = 0;
-  __syncwarp();
-  for (int64_t base = gw * 32; base < m2; base += nw * 32) {
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < m2;
+       base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = base + lane;
-    int32_t a = 0, v = 0, eva = 0;
-    int len = 0;
-    int64_t fo = 0;
-    bool v_lo = false;
+    u64 e = 0;
     if (s < m2) {
-      eva = g.eid[s];
-      a = g.ci[s];
-      const int32_t lo = g.esrc[eva];
-      v = lo + g.edst[eva] - a;
-      v_lo = lo == v;
-      const u32 t = Te[eva];
-      if (t >= 2 && v % num_shards == shard_index) {
-        fo = g.foff[eva];
-        len = full_prefix(g, fo, (int)t, a);  // b < a
-      }
+      const int32_t eva = g.eid[s];
+      const int32_t a = g.ci[s];
+      const int32_t v = g.esrc[eva] + g.edst[eva] - a;
+      if (Te[eva] >= 2 && v % num_shards == shard_index) e = est[s];
     }
-    const bool is_long = len > HUB_ITEM_LONG;
-    warp_append(is_long, (int32_t)s, longs, n_long);
-    if (is_long) len = 0;
-    int cur = -1;
-    u64 cacc = 0;
-    warp_flat(len, [&](int j, int k, bool valid) {
-      const int32_t aj = __shfl_sync(FULL_MASK, a, j);
-      const int64_t foj = __shfl_sync(FULL_MASK, fo, j);
-      const bool vloj = __shfl_sync(FULL_MASK, v_lo, j);
-      if (!valid) return;
-      if (j != cur) {
-        if (cur >= 0 && cacc) atomicAdd(&acc[wib][cur], cacc);
-        cur = j;
-        cacc = 0;
-      }
-      const int64_t r = foj + k;
-      if (g.fx[r] < aj) {
-        const int32_t evb = vloj ? g.fe1[r] : g.fe2[r];
-        cacc += (u64)Te[evb];
-      }
-    });
-    if (cur >= 0 && cacc) atomicAdd(&acc[wib][cur], cacc);
-    __syncwarp();
-    const u64 est = acc[wib][lane];
-    acc[wib][lane] = 0;
-    __syncwarp();
-    const bool is_light = est > 0 && est <= HUB_WARP_MAX;
-    const bool is_heavy = est > HUB_WARP_MAX;
-    warp_append(is_light, (int32_t)s, light, n_light);
+    warp_append(e > 0 && e <= HUB_WARP_MAX, (int32_t)s, light, n_light);
+    const bool is_heavy = e > HUB_WARP_MAX;
     const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
     if (bal) {
       int hb = 0;
@@ -194,7 +91,7 @@ __global__ void __launch_bounds__(256) k_hub_items(DGraph g, const u32* __restri
       if (is_heavy) {
         const int q = hb + __popc(bal & ((1u << lane) - 1u));
         heavy[q] = (int32_t)s;
-        heavy_est[q] = (u32)min(est, (u64)0xffffffffu);
+        heavy_est[q] = (u32)min(e, (u64)0xffffffffu);
       }
     }
   }
