@@ -68,6 +68,7 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 #define C5_MID_CAP (2 * C5_MID_MAX)  // ... hashed records in a per-CTA global region (load <= 0.5)
 #define C5_MBT 128                // mid-endpoint CTA (several endpoints in flight per SM)
 #define C5_BIG_KEY (1ull << 62)   // sort-key bit of the endpoints above C5_MID_MAX
+#define C5_BITS_SMEM_MAX (160 << 10)  // heavy CTAs: shared first-touch bitmaps up to this size
 
 // dense records indexed by vertex id; touched list holds vertex ids
 template <typename Rec>
@@ -76,6 +77,12 @@ struct C5Dense {
   Rec* R;
   int32_t* L;
   int* nL;
+  // optional shared-memory bitmaps by vertex id (present, j-key): first-touch detection by a
+  // shared atomic, so the record's flag update becomes a fire-and-forget global atomic and
+  // no element waits for a global round trip to learn whether to append (nullptr: the
+  // record's own atomicOr decides, for graphs whose bitmaps do not fit)
+  u32* bP = nullptr;
+  u32* bJ = nullptr;
   // old = the flags before; word = the whole wf word before (its Wn bits are unchanged by
   // the Or, so callers that need Wn take it from here instead of loading it again)
   __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old, u32& word) {
@@ -89,10 +96,51 @@ struct C5Dense {
     u32 word;
     return mark(x, bits, old, word);
   }
+  // mark without needing the old flags
+  __device__ __forceinline__ Rec* mark_nr(int32_t x, u32 bits) {
+    if (!bP) {
+      u32 old;
+      return mark(x, bits, old);
+    }
+    Rec* r = &R[x];
+    const u32 bit = 1u << (x & 31);
+    const u32 ob = atomicOr(&bP[x >> 5], bit);
+    append_active(!(ob & bit), x, L, nL);
+    atomicOr(&r->wf, (bits | C5_PRESENT) << 28);  // result unused: a reduction
+    return r;
+  }
+  // j-key mark: newj = first C5_J mark of x
+  __device__ __forceinline__ Rec* mark_j(int32_t x, bool& newj) {
+    if (!bP) {
+      u32 old;
+      Rec* r = mark(x, C5_J, old);
+      newj = !(old & C5_J);
+      return r;
+    }
+    const u32 bit = 1u << (x & 31);
+    newj = !(atomicOr(&bJ[x >> 5], bit) & bit);
+    return mark_nr(x, C5_J);
+  }
+  // i-key mark in step 3, returning Wn (final since step 1)
+  __device__ __forceinline__ Rec* mark_wn(int32_t x, u64& wn) {
+    if (!bP) {
+      u32 old, word;
+      Rec* r = mark(x, C5_I, old, word);
+      wn = (u64)(word & C5_WN_MASK);
+      return r;
+    }
+    Rec* r = &R[x];
+    wn = (u64)(__ldcg(&r->wf) & C5_WN_MASK);
+    mark_nr(x, C5_I);
+    return r;
+  }
   __device__ __forceinline__ Rec* peek(int32_t x) const { return &R[x]; }
   __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
     x = L[t];
     return &R[x];
+  }
+  __device__ __forceinline__ void clear_bits(int32_t x) const {
+    if (bP) { bP[x >> 5] = 0u; bJ[x >> 5] = 0u; }
   }
 };
 
@@ -105,27 +153,52 @@ struct C5Hash {
   int32_t* L;
   int* nL;
   __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) >> 7 & mask; }
-  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old, u32& word) {
+  // find or claim the slot of x; the thread whose CAS claims it appends the slot to the
+  // touched list (so no mark has to wait for the flags' old value to decide that)
+  __device__ __forceinline__ Rec* probe(int32_t x) {
     u32 h = h0(x);
+    bool claimed = false;
     for (;;) {
       const int32_t k = R[h].key;
       if (k == x + 1) break;
       if (k == 0) {
         const int32_t o = atomicCAS(&R[h].key, 0, x + 1);
-        if (o == 0 || o == x + 1) break;
+        if (o == 0) { claimed = true; break; }
+        if (o == x + 1) break;
       }
       h = (h + 1) & mask;
     }
-    Rec* r = &R[h];
+    append_active(claimed, (int32_t)h, L, nL);
+    return &R[h];
+  }
+  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old, u32& word) {
+    Rec* r = probe(x);
     word = atomicOr(&r->wf, (bits | C5_PRESENT) << 28);
     old = word >> 28;
-    append_active(!(old & C5_PRESENT), (int32_t)h, L, nL);
     return r;
   }
   __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
     u32 word;
     return mark(x, bits, old, word);
   }
+  __device__ __forceinline__ Rec* mark_nr(int32_t x, u32 bits) {
+    Rec* r = probe(x);
+    atomicOr(&r->wf, (bits | C5_PRESENT) << 28);  // result unused: a reduction
+    return r;
+  }
+  __device__ __forceinline__ Rec* mark_j(int32_t x, bool& newj) {
+    u32 old;
+    Rec* r = mark(x, C5_J, old);
+    newj = !(old & C5_J);
+    return r;
+  }
+  __device__ __forceinline__ Rec* mark_wn(int32_t x, u64& wn) {
+    u32 old, word;
+    Rec* r = mark(x, C5_I, old, word);
+    wn = (u64)(word & C5_WN_MASK);
+    return r;
+  }
+  __device__ __forceinline__ void clear_bits(int32_t) const {}
   __device__ __forceinline__ Rec* peek(int32_t x) const {
     u32 h = h0(x);
     for (;;) {
@@ -213,10 +286,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
   const int dml = g.dm[l];
   long long t_prev = clock64();
   // ---- step 0: neighbours of l
-  for (int t = eng.tid(); t < dl; t += eng.nthr()) {
-    u32 old;
-    loc.mark(g.ci[r0 + t], C5_ADJ, old);
-  }
+  for (int t = eng.tid(); t < dl; t += eng.nthr()) loc.mark_nr(g.ci[r0 + t], C5_ADJ);
   // wedge lists of steps 1/6: w = N(l)[t], i in N(w) (w < l) or N+(w) (w > l)
   auto winfo = [&](int t, int64_t& base, int& len) {
     const int32_t w = g.ci[r0 + t];
@@ -235,8 +305,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       [&](int, int64_t base, int k) -> u64 {
         const int32_t i = g.ci[base + k];
         if (i == l) return 0;
-        u32 old;
-        auto* r = loc.mark(i, C5_I, old);
+        auto* r = loc.mark_nr(i, C5_I);
         atomicAdd(&r->wf, 1u);  // Wn
         return 0;
       },
@@ -248,9 +317,9 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int64_t e = base + k;
         const int32_t j = g.ocol[e];
         if (j == l) return 0;
-        u32 old;
-        auto* r = loc.mark(j, C5_J, old);
-        append_active(!(old & C5_J), j, J, nJ);
+        bool newj;
+        auto* r = loc.mark_j(j, newj);
+        append_active(newj, j, J, nJ);
         typedef decltype(r->Q) V;
         atomicAdd(&r->Q, (V)1);
         atomicAdd(&r->QT, (V)Thigh[e]);
@@ -275,11 +344,11 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         typedef decltype(rj->Q) V;
         const V q = rj->Q;
         const bool adjj = c5_flags(rj) & C5_ADJ;
-        u32 old, word;
-        auto* ri = loc.mark(i, C5_I, old, word);
+        u64 wn;
+        auto* ri = loc.mark_wn(i, wn);  // Wn is final after step 1
         atomicAdd(&ri->P, q);
         if (adjj) atomicAdd(&ri->A, q);
-        return (u64)(word & C5_WN_MASK);  // Wn is final after step 1 (and untouched by the Or)
+        return wn;
       },
       [&](int t, u64 s) {
         auto* rj = loc.peek(J[t]);
@@ -357,6 +426,7 @@ __device__ __forceinline__ void c5_reset(const Eng& eng, Loc& loc) {
   for (int t = eng.tid(); t < nt; t += eng.nthr()) {
     int32_t x;
     auto* r = loc.touched(t, x);
+    loc.clear_bits(x);
     uint4* q = reinterpret_cast<uint4*>(r);
     const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -433,7 +503,7 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
                                                     int* __restrict__ counter, C5RecT<V>* __restrict__ dense,
                                                     int32_t* __restrict__ dlists, u64* __restrict__ C5,
                                                     int32_t* __restrict__ qmem, const int* __restrict__ nbig,
-                                                    int ngiant) {
+                                                    int ngiant, int use_bits) {
   // the list is sorted: the endpoints past C5_MID_MAX come first, *nbig of them (with the
   // giant prefix); the rest belong to k_c5_mid
   if (nbig) n_heavy = min(n_heavy, *nbig - ngiant);
@@ -445,8 +515,16 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
   }
   __shared__ int s_idx, s_nL, s_nJ;
   __shared__ u64 s_tot;
+  extern __shared__ u32 c5_bits[];  // 2 x ceil(n/32) words when the launch provides them
   CtaEng eng{&E};
   C5Dense<C5RecT<V>> loc;
+  if (use_bits) {
+    const int nwd = (g.n + 31) >> 5;
+    for (int i = threadIdx.x; i < 2 * nwd; i += blockDim.x) c5_bits[i] = 0u;
+    loc.bP = c5_bits;
+    loc.bJ = c5_bits + nwd;
+    __syncthreads();
+  }
   loc.R = dense + (size_t)blockIdx.x * g.n;
   loc.L = dlists + (size_t)blockIdx.x * 2 * g.n;
   loc.nL = &s_nL;

@@ -1177,14 +1177,23 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         const u64* mkeys = n5h > 1 ? hkeys : c5w;
         const int32_t* hsm = hs;
         const int n5h_ = n5h;
+        // first-touch bitmaps (present, j-key) in shared memory when they fit
+        const size_t bits_smem = (size_t)2 * ((n + 31) / 32) * sizeof(u32);
+        const int use_bits = bits_smem <= C5_BITS_SMEM_MAX && !getenv("EVOKE_C5_NO_BITS") ? 1 : 0;
+        const size_t bsm = use_bits ? bits_smem : 0;
+        if (use_bits) {
+          CK(cudaFuncSetAttribute(k_c5_heavy<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+          CK(cudaFuncSetAttribute(k_c5_heavy<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+        }
         jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
           if (narrow)
-            k_c5_heavy<u32><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq,
-                                                   nbig_dev, ngi);
+            k_c5_heavy<u32><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
+                                                     reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq,
+                                                     nbig_dev, ngi, use_bits);
           else
-            k_c5_heavy<u64><<<hg, C5_HBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, nbig_dev, ngi);
+            k_c5_heavy<u64><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
+                                                     reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, nbig_dev,
+                                                     ngi, use_bits);
           k_c5_mid<<<gm, C5_MBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsm, mkeys, nbig_dev, n5h_, c5c + 6, mreg, mlists,
                                           C5out, mq);
           C.launches += 2;
