@@ -213,6 +213,8 @@ struct Ctx {
   cudaEvent_t ev_pre = nullptr, ev_side = nullptr;  // side stream of a5/a9 + gather 1
   cudaEvent_t sev[3] = {};                          // side timing: start, after cliques, end
   bool side_used = false;
+  cudaEvent_t gev[3] = {};  // early tail gathers: start, after gathers 2/3, after the triangle gather
+  bool gathers_early = false;
   cudaStream_t side_st = nullptr;
   static const int MAXJOBS = 16;
   cudaStream_t jst[MAXJOBS] = {};
@@ -444,6 +446,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   CK(cudaEventCreateWithFlags(&C.ev_pre, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&C.ev_side, cudaEventDisableTiming));
   for (int i = 0; i < 3; i++) CK(cudaEventCreate(&C.sev[i]));
+  for (int i = 0; i < 3; i++) CK(cudaEventCreate(&C.gev[i]));
   CK(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
   for (int i = 0; i < Ctx::MAXJOBS; i++)
     for (int j = 0; j < 2; j++) CK(cudaEventCreate(&C.pev[i][j]));
@@ -455,6 +458,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       cudaEventDestroy(C.ev_pre);
       cudaEventDestroy(C.ev_side);
       for (int i = 0; i < 3; i++) cudaEventDestroy(C.sev[i]);
+      for (int i = 0; i < 3; i++) cudaEventDestroy(C.gev[i]);
       cudaEventDestroy(C.ev_join);
       for (int i = 0; i < Ctx::MAXJOBS; i++)
         for (int j = 0; j < 2; j++) cudaEventDestroy(C.pev[i][j]);
@@ -1241,6 +1245,31 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     jobs[i].fn(st);
     CK(cudaEventRecord(C.pev[i][1], st));
   }
+  // gathers 2/3 and the triangle gather read, of the concurrent passes' outputs, only the
+  // pair pass's (R8, C4e): they start on a stream of their own when the pair jobs end and run
+  // beside the 5-cycle / hub-local / theta66-70 tails
+  auto gathers23 = [&](cudaStream_t gs) {
+    if (n > 0) {
+      gather_on(gs, k_nbr<2>, k_nbr_heavy<2>, 1);
+      if (!four) gather_on(gs, k_nbr<3>, k_nbr_heavy<3>, 2);
+    }
+  };
+  auto trigather = [&](cudaStream_t gs) {
+    if (ntri > 0 && !four) { k_trigather<<<grid_for(ntri, B, SM), B, 0, gs>>>(g, ev, F); C.launches++; }
+  };
+  if (!serial && n > 0) {
+    C.gathers_early = true;
+    cudaStream_t gs = C.stream(Ctx::MAXJOBS - 2, 0);
+    CK(cudaStreamWaitEvent(gs, C.ev_fork, 0));
+    for (size_t i = 0; i < jobs.size(); i++)
+      if (jobs[i].pass == P_PAIR) CK(cudaStreamWaitEvent(gs, C.pev[i][1], 0));
+    CK(cudaEventRecord(C.gev[0], gs));
+    gathers23(gs);
+    CK(cudaEventRecord(C.gev[1], gs));
+    trigather(gs);
+    CK(cudaEventRecord(C.gev[2], gs));
+    CK(cudaStreamWaitEvent(C.st, C.gev[2], 0));
+  }
   for (size_t i = 0; i < jobs.size(); i++) CK(cudaStreamWaitEvent(C.st, C.pev[i][1], 0));
   if (getenv("EVOKE_DEBUG")) {
     unsigned long long ph[2][8];
@@ -1266,13 +1295,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
 
   // ------------------------------------------------------------------ nbr gathers 2,3
   C.mark(P_NBR2);
-  if (n > 0) {
-    gather(k_nbr<2>, k_nbr_heavy<2>, 1);
-    if (!four) gather(k_nbr<3>, k_nbr_heavy<3>, 2);
-  }
+  if (!C.gathers_early) gathers23(C.st);  // (serial mode: here, in order)
   // ------------------------------------------------------------------ triangle gather
   C.mark(P_TRIG);
-  if (ntri > 0 && !four) { k_trigather<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, ev, F); C.launches++; }
+  if (!C.gathers_early) trigather(C.st);
 
   // ------------------------------------------------------------------ a12: combine
   C.mark(P_COMB);
@@ -1327,6 +1353,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, C.ev[i], C.ev[i + 1]));
       s->ms_pass[i] = ms;
+    }
+    if (C.gathers_early) {  // gathers 2/3 and the triangle gather ran beside the 5-cycle tail
+      float a = 0, b = 0;
+      CK(cudaEventElapsedTime(&a, C.gev[0], C.gev[1]));
+      CK(cudaEventElapsedTime(&b, C.gev[1], C.gev[2]));
+      s->ms_pass[P_NBR2] = a;
+      s->ms_pass[P_TRIG] = b;
     }
     if (C.side_used) {  // a5/a9 and gather 1 ran on the side stream, beside the preparations
       float a = 0, b = 0;
