@@ -265,7 +265,8 @@ def main():
                            "wedges": st_last["wedges"], "parallelism": f"dp{world} (work-unit shards + NCCL reduce)",
                            "l2": "flushed between timed steps (256 MiB write)"},
                 "e2e": {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(g.edges.nbytes),
-                        "d2h_bytes_per_step": int(g.n * 73 * 8)},
+                        "d2h_bytes_per_step": int(g.n * 73 * 8),
+                        "step_ms": [round(1e3 * t, 3) for t in e2e_times]},
                 "gpu_launches": launches,
                 "library_launches": lib_launches,
                 "clocks": clk.summary(),
