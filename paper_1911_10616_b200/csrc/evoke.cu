@@ -906,7 +906,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (getenv("EVOKE_DEBUG"))
       fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d small-mid %d light %d\n", ht[PT_G64],
               ht[PT_G32], ht[PT_G32S], ht[PT_MID], ht[PT_MIDS], ht[PT_LIGHT]);
-    // position maps of the hubs (h* membership in one load), within a memory budget
+    // adjacency maps of the hubs (h* membership and T(h*, x) in one load), within a memory budget
     int32_t* hslot = A.alloc<int32_t>(n);
     int* hcnt = A.alloc<int>(1, true);
     const int max_maps = (int)std::min<int64_t>(4096, std::max<int64_t>(0, (256ll << 20) / ((int64_t)n * 4)));
@@ -919,7 +919,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* hpos = A.alloc<int32_t>((size_t)std::max(nmaps, 1) * n);
     if (nmaps > 0) {
       CK(cudaMemsetAsync(hpos, 0xff, sizeof(int32_t) * (size_t)nmaps * n, C.st));
-      k_hub_maps<<<std::min(nmaps, 4 * SM), 256, 0, C.st>>>(g, hubs, nmaps, hpos);
+      k_hub_maps<<<std::min(nmaps, 4 * SM), 256, 0, C.st>>>(g, Te, hubs, nmaps, hpos);
     }
     C.launches += 2;
     PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e, hstar,

@@ -37,7 +37,7 @@ struct PairOut {
   u64 *R8, *R36, *R50, *R51, *R63, *R49, *R62, *R64, *C4e;
   const int32_t* hstar;     // per source: its heaviest neighbour h* (wedges through h* are not walked)
   const int32_t* hub_slot;  // per vertex: row of its position map, or -1
-  const int32_t* hub_pos;   // [slot][x]: position of x in N(hub) (offset), or -1
+  const int32_t* hub_pos;   // [slot][x]: T(hub, x) if x ~ hub, else -1
 };
 
 __device__ __forceinline__ int64_t slot_of_lo_in_hi(const DGraph& g, int32_t e) { return g.eslot_hi[e]; }
@@ -818,27 +818,6 @@ __device__ __forceinline__ void hstar_search(const DGraph& g, const u32* __restr
   });
 }
 
-// membership through the hub's position map (one load per key)
-template <typename Tab>
-__device__ __forceinline__ void hstar_map(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
-                                          const int32_t* __restrict__ pmap, Tab& tab, int tid, int nthr,
-                                          PairAcc& H, u64& s51) {
-  const int64_t hb = g.rp[hs];
-  tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
-    const int32_t k = pmap[x];
-    if (k >= 0) {
-      w += 1;
-      H.c5 += w - 1;
-      s51 += (u64)Te[g.eid[hb + k]] * (w - 1);
-      if (x > u) {
-        H.c49 += binom2(w - 1);
-        H.c62 += d;
-      }
-    }
-    return w;
-  });
-}
-
 // The h* term by the cheapest available way, fused with the per-pair terms when the table
 // is swept anyway (map / key search): returns true when a8..a63 were already added.
 template <typename Tab>
@@ -855,18 +834,17 @@ __device__ __forceinline__ bool hstar_and_terms(const DGraph& g, const u32* __re
   const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
   const int32_t* pmap = slot >= 0 ? o.hub_pos + (size_t)slot * (size_t)g.n : nullptr;
   tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
-    int64_t p = -1;
+    int64_t te = -1;  // T(h*, x) when x ~ h*
     if (pmap) {
-      const int32_t k = pmap[x];
-      if (k >= 0) p = hb + k;
+      te = pmap[x];  // the map holds T(h*, x) directly (one load instead of three)
     } else {
       const int64_t q = lower_bound_dev<int32_t>(g.ci, hb, he, x);
-      if (q < he && g.ci[q] == x) p = q;
+      if (q < he && g.ci[q] == x) te = (int64_t)Te[g.eid[q]];
     }
-    if (p >= 0) {
+    if (te >= 0) {
       w += 1;
       H.c5 += w - 1;
-      s51 += (u64)Te[g.eid[p]] * (w - 1);
+      s51 += (u64)te * (w - 1);
       if (x > u) {
         H.c49 += binom2(w - 1);
         H.c62 += d;
@@ -878,7 +856,7 @@ __device__ __forceinline__ bool hstar_and_terms(const DGraph& g, const u32* __re
   return true;
 }
 
-// position maps of the hubs (d >= PAIR_HUBMAP_MIN) up to max_slots rows
+// adjacency maps of the hubs (d >= PAIR_HUBMAP_MIN) up to max_slots rows
 __global__ void k_hub_slots(DGraph g, int max_slots, int32_t* __restrict__ slot, int32_t* __restrict__ hubs,
                             int* __restrict__ cnt) {
   for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
@@ -893,13 +871,14 @@ __global__ void k_hub_slots(DGraph g, int max_slots, int32_t* __restrict__ slot,
     slot[v] = sl;
   }
 }
-// block per hub: row[x] = position of x in N(hub)
-__global__ void k_hub_maps(DGraph g, const int32_t* __restrict__ hubs, int nhubs, int32_t* __restrict__ pos) {
+// block per hub: row[x] = T(hub, x) for x in N(hub) (the rows start at -1)
+__global__ void k_hub_maps(DGraph g, const u32* __restrict__ Te, const int32_t* __restrict__ hubs, int nhubs,
+                           int32_t* __restrict__ pos) {
   for (int q = blockIdx.x; q < nhubs; q += gridDim.x) {
     const int32_t v = hubs[q];
     int32_t* row = pos + (size_t)q * (size_t)g.n;
     const int64_t b = g.rp[v], e = g.rp[v + 1];
-    for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)(k - b);
+    for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)Te[g.eid[k]];
   }
 }
 
