@@ -115,6 +115,11 @@ struct DGraph {
   const int32_t* fe1;   // [3 ntri]
   const int32_t* fe2;   // [3 ntri]
   int32_t full_sorted;  // 1: every full list is sorted by x (prefix / suffix bounds by search)
+  // per-slot copies of per-edge triangle counts, aligned with ci (streamed with the list
+  // instead of a dependent load through eid): T(e), T_low(e), T_mid(e) of e = eid[s]
+  const u32* tes;       // [2m]
+  const u32* tlows;     // [2m]
+  const u32* tmids;     // [2m]
 };
 
 __device__ __forceinline__ int32_t dg_deg(const DGraph& g, int32_t u) { return g.deg[u]; }

@@ -410,8 +410,8 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         if (i == l) return 0;
         const int32_t w = g.ci[r0 + t];
         const auto* ri = loc.peek(i);
-        u64 corr = (w < i) ? (u64)Tlow[g.eid[r0 + t]] : 0ull;
-        if (w < l && w < i) corr += (u64)Tmid[g.eid[s]] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
+        u64 corr = (w < i) ? (u64)g.tlows[r0 + t] : 0ull;
+        if (w < l && w < i) corr += (u64)g.tmids[s] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
         return (u64)ri->P - corr;
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });

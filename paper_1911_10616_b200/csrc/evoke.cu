@@ -390,6 +390,17 @@ __global__ void k_check_zero(const uint4* __restrict__ p, size_t n16, int* flag)
     if (q.x | q.y | q.z | q.w) { *flag = 1; return; }
   }
 }
+// per-slot copies of the per-edge triangle counts (DGraph::tes, tlows, tmids)
+__global__ void k_slot_counts(const int32_t* __restrict__ eid, int64_t m2, const u32* __restrict__ Te,
+                              const u32* __restrict__ Tlow, const u32* __restrict__ Tmid, u32* __restrict__ tes,
+                              u32* __restrict__ tlows, u32* __restrict__ tmids) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2; s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e = eid[s];
+    tes[s] = Te[e];
+    tlows[s] = Tlow[e];
+    tmids[s] = Tmid[e];
+  }
+}
 // wedge total W(G) = sum C(d,2)
 __global__ void k_wedges(const int64_t* __restrict__ rp, int32_t n, u64* out) {
   u64 s = 0;
@@ -790,6 +801,16 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     g.foff = foff;
   }
 
+  {
+    u32* tes = A.alloc<u32>(m2 + 1);
+    u32* tlows = A.alloc<u32>(m2 + 1);
+    u32* tmids = A.alloc<u32>(m2 + 1);
+    if (m2 > 0) {
+      k_slot_counts<<<grid_for(m2, B, SM), B, 0, C.st>>>(g.eid, m2, Te, Tlow, Tmid, tes, tlows, tmids);
+      C.launches++;
+    }
+    g.tes = tes; g.tlows = tlows; g.tmids = tmids;
+  }
   const int si = o.shard_index, ns = o.num_shards;
   // ------------------------------------------------------------------ a5/a9: cliques
   C.mark(P_CLIQ);

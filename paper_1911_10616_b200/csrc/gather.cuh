@@ -63,7 +63,7 @@ __device__ __forceinline__ void nbr1_acc(const DGraph& g, const EdgeVals& ev, co
     const int32_t v = g.ci[s];
     const u64 dv = (u64)dg_deg(g, v);
     const u64 tv = FLD(F_T, v);
-    const u64 te = ev.Te[g.eid[s]];
+    const u64 te = g.tes[s];
     a[0] += dv - 1;
     a[1] += binom2(dv - 1);
     a[2] += tv - te;

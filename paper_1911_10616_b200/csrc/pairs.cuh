@@ -301,7 +301,7 @@ __device__ __forceinline__ void pass2_wedge(const DGraph& g, const u32* __restri
   tab.get(x, w, d);
   if (w < 2) return;  // W(u,x) = 1 (hence D = 0) contributes nothing below
   A.c5 += w - 1;
-  s51 += (u64)Te[g.eid[t]] * (w - 1);
+  s51 += (u64)g.tes[t] * (w - 1);
   if (x > u) {
     A.c49 += binom2(w - 1);
     A.c62 += d;
@@ -406,7 +406,7 @@ __device__ __forceinline__ void wedges_pass2_ilp(const DGraph& g, const u32* __r
     }
     u32 te[PAIR_ILP];
 #pragma unroll
-    for (int i = 0; i < PAIR_ILP; i++) te[i] = wv[i] >= 2 ? Te[g.eid[ts[i]]] : 0u;
+    for (int i = 0; i < PAIR_ILP; i++) te[i] = wv[i] >= 2 ? g.tes[ts[i]] : 0u;
 #pragma unroll
     for (int i = 0; i < PAIR_ILP; i++) {
       if (js[i] < 0) continue;
@@ -732,7 +732,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
 #pragma unroll
         for (int i = 0; i < U; i++) {
           const int k = k0 + lane + 32 * i;
-          te[i] = wv[i] >= 2 ? Te[g.eid[it.rb + k]] : 0u;  // W = 1 pairs contribute nothing
+          te[i] = wv[i] >= 2 ? g.tes[it.rb + k] : 0u;  // W = 1 pairs contribute nothing
         }
 #pragma unroll
         for (int i = 0; i < U; i++) {
@@ -791,7 +791,7 @@ __device__ __forceinline__ void hstar_walk(const DGraph& g, const u32* __restric
     *wp = v;
     const u64 w = Tab::wfield(v), d = Tab::dfield(v);
     H.c5 += w - 1;
-    s51 += (u64)Te[g.eid[p]] * (w - 1);
+    s51 += (u64)g.tes[p] * (w - 1);
     if (x > u) {
       H.c49 += binom2(w - 1);
       H.c62 += d;
@@ -808,7 +808,7 @@ __device__ __forceinline__ void hstar_search(const DGraph& g, const u32* __restr
     if (p < he && g.ci[p] == x) {
       w += 1;
       H.c5 += w - 1;
-      s51 += (u64)Te[g.eid[p]] * (w - 1);
+      s51 += (u64)g.tes[p] * (w - 1);
       if (x > u) {
         H.c49 += binom2(w - 1);
         H.c62 += d;
@@ -839,7 +839,7 @@ __device__ __forceinline__ bool hstar_and_terms(const DGraph& g, const u32* __re
       te = pmap[x];  // the map holds T(h*, x) directly (one load instead of three)
     } else {
       const int64_t q = lower_bound_dev<int32_t>(g.ci, hb, he, x);
-      if (q < he && g.ci[q] == x) te = (int64_t)Te[g.eid[q]];
+      if (q < he && g.ci[q] == x) te = (int64_t)g.tes[q];
     }
     if (te >= 0) {
       w += 1;
@@ -878,7 +878,7 @@ __global__ void k_hub_maps(DGraph g, const u32* __restrict__ Te, const int32_t* 
     const int32_t v = hubs[q];
     int32_t* row = pos + (size_t)q * (size_t)g.n;
     const int64_t b = g.rp[v], e = g.rp[v + 1];
-    for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)Te[g.eid[k]];
+    for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)g.tes[k];
   }
 }
 
