@@ -46,6 +46,61 @@ struct __align__(16) C5RecT {
   V Q, P, A, QT, QM, S;
 };
 typedef C5RecT<u64> C5Rec;
+// Packed record of the light and mid endpoints (W(l) <= C5_MID_MAX < 2^16, so every field
+// fits 16 bits and two share a word: the additions of one never carry into the other).
+// 20 bytes instead of 32, and step 2 needs two atomics instead of three.
+struct __align__(4) C5RecP {
+  int32_t key;
+  u32 wf;
+  u32 qp;   // Q | P << 16
+  u32 as;   // A | S << 16
+  u32 qtm;  // QT | QM << 16
+};
+// field access for both layouts
+template <typename V>
+__device__ __forceinline__ void rec_add_q(C5RecT<V>* r, u32 th, u32 tm) {
+  atomicAdd(&r->Q, (V)1);
+  atomicAdd(&r->QT, (V)th);
+  atomicAdd(&r->QM, (V)tm);
+}
+__device__ __forceinline__ void rec_add_q(C5RecP* r, u32 th, u32 tm) {
+  atomicAdd(&r->qp, 1u);
+  atomicAdd(&r->qtm, th | (tm << 16));
+}
+template <typename V> __device__ __forceinline__ u64 rec_q(const C5RecT<V>* r) { return (u64)r->Q; }
+template <typename V> __device__ __forceinline__ u64 rec_p(const C5RecT<V>* r) { return (u64)r->P; }
+template <typename V> __device__ __forceinline__ u64 rec_a(const C5RecT<V>* r) { return (u64)r->A; }
+template <typename V> __device__ __forceinline__ u64 rec_s(const C5RecT<V>* r) { return (u64)r->S; }
+template <typename V> __device__ __forceinline__ u64 rec_qt(const C5RecT<V>* r) { return (u64)r->QT; }
+template <typename V> __device__ __forceinline__ u64 rec_qm(const C5RecT<V>* r) { return (u64)r->QM; }
+__device__ __forceinline__ u64 rec_q(const C5RecP* r) { return (u64)(r->qp & 0xffffu); }
+__device__ __forceinline__ u64 rec_p(const C5RecP* r) { return (u64)(r->qp >> 16); }
+__device__ __forceinline__ u64 rec_a(const C5RecP* r) { return (u64)(r->as & 0xffffu); }
+__device__ __forceinline__ u64 rec_s(const C5RecP* r) { return (u64)(r->as >> 16); }
+__device__ __forceinline__ u64 rec_qt(const C5RecP* r) { return (u64)(r->qtm & 0xffffu); }
+__device__ __forceinline__ u64 rec_qm(const C5RecP* r) { return (u64)(r->qtm >> 16); }
+template <typename V>
+__device__ __forceinline__ void rec_add_pa(C5RecT<V>* r, u64 q, bool adj) {
+  atomicAdd(&r->P, (V)q);
+  if (adj) atomicAdd(&r->A, (V)q);
+}
+__device__ __forceinline__ void rec_add_pa(C5RecP* r, u64 q, bool adj) {
+  atomicAdd(&r->qp, (u32)q << 16);
+  if (adj) atomicAdd(&r->as, (u32)q);
+}
+template <typename V>
+__device__ __forceinline__ void rec_add_s(C5RecT<V>* r, u64 s) { atomicAdd(&r->S, (V)s); }
+__device__ __forceinline__ void rec_add_s(C5RecP* r, u64 s) { atomicAdd(&r->as, (u32)s << 16); }
+template <typename V>
+__device__ __forceinline__ void rec_zero(C5RecT<V>* r) {
+  uint4* q = reinterpret_cast<uint4*>(r);
+  const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(*r) / 16); i++) q[i] = z;
+}
+__device__ __forceinline__ void rec_zero(C5RecP* r) {
+  r->key = 0; r->wf = 0u; r->qp = 0u; r->as = 0u; r->qtm = 0u;
+}
 #define C5_WN_MASK 0x0fffffffu
 template <typename R>
 __device__ __forceinline__ u32 c5_flags(const R* r) { return r->wf >> 28; }
@@ -60,7 +115,7 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 #define C5_WARP_MAX 1024          // light endpoint: W(l) + d(l) <= this
 #define C5_WARP_CAP 2048          // records per warp region (load <= 0.5)
 #define C5_SH_CAP 256             // light endpoints with a region of <= this many slots: shared memory
-#define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (32 + 2 * 4))   // records + touched + J lists
+#define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (sizeof(C5RecP) + 2 * 4))   // records + touched + J lists
 #define C5_SH_BYTES(cap) ((C5_BT / 32) * C5_SH_WARP_BYTES(cap))
 #define C5_GIANT (1ull << 40)     // endpoint work above which a thread-block cluster takes it (off)
 #define C5_HBT 1024               // heavy-endpoint CTA
@@ -320,10 +375,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         bool newj;
         auto* r = loc.mark_j(j, newj);
         append_active(newj, j, J, nJ);
-        typedef decltype(r->Q) V;
-        atomicAdd(&r->Q, (V)1);
-        atomicAdd(&r->QT, (V)Thigh[e]);
-        atomicAdd(&r->QM, (V)Tmid[e]);
+        rec_add_q(r, Thigh[e], Tmid[e]);
         return 0;
       },
       [&](int, u64) {});
@@ -341,30 +393,27 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int32_t i = g.ocol[base + k];
         if (i == l) return 0;
         const auto* rj = loc.peek(J[t]);
-        typedef decltype(rj->Q) V;
-        const V q = rj->Q;
+        const u64 q = rec_q(rj);
         const bool adjj = c5_flags(rj) & C5_ADJ;
         u64 wn;
         auto* ri = loc.mark_wn(i, wn);  // Wn is final after step 1
-        atomicAdd(&ri->P, q);
-        if (adjj) atomicAdd(&ri->A, q);
+        rec_add_pa(ri, q, adjj);
         return wn;
       },
       [&](int t, u64 s) {
         auto* rj = loc.peek(J[t]);
-        typedef decltype(rj->S) V;
-        atomicAdd(&rj->S, (V)s);
-        atomicAdd(&C5[J[t]], (u64)rj->Q * s);  // the j credit is linear in S
+        rec_add_s(rj, s);
+        atomicAdd(&C5[J[t]], rec_q(rj) * s);  // the j credit is linear in S
       });
   // constant part of the j credits
   for (int t = eng.tid(); t < nj; t += eng.nthr()) {
     const int32_t j = J[t];
     const auto* rj = loc.peek(j);
-    const u64 q = rj->Q;
+    const u64 q = rec_q(rj);
     const bool adjj = c5_flags(rj) & C5_ADJ;
     const u64 lj = (l > j && adjj) ? 1ull : 0ull;
     const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-    const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rj->QT - q * lj);
+    const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rec_qt(rj) - q * lj);
     if (c) atomicAdd(&C5[j], (u64)0 - c);
   }
   eng.sync();
@@ -379,7 +428,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const bool adjj = c5_flags(rj) & C5_ADJ;
         const u64 lj = (l > j && adjj) ? 1ull : 0ull;
         const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-        return (u64)rj->S - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[e] - lj);
+        return rec_s(rj) - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[e] - lj);
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
   C5_PHASE(4);
@@ -393,8 +442,8 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       const u32 fl = c5_flags(r);
       if (!(fl & C5_I)) continue;
       const bool adji = fl & C5_ADJ;
-      const u64 bi = (u64)r->QM - (u64)r->Q * ((x > l && adji) ? 1ull : 0ull);
-      const u64 ci = (u64)r->P * c5_wn(r) - (u64)r->A - bi;
+      const u64 bi = rec_qm(r) - rec_q(r) * ((x > l && adji) ? 1ull : 0ull);
+      const u64 ci = rec_p(r) * c5_wn(r) - rec_a(r) - bi;
       if (ci) atomicAdd(&C5[x], ci);
       acc += ci;
     }
@@ -412,7 +461,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const auto* ri = loc.peek(i);
         u64 corr = (w < i) ? (u64)g.tlows[r0 + t] : 0ull;
         if (w < l && w < i) corr += (u64)g.tmids[s] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
-        return (u64)ri->P - corr;
+        return rec_p(ri) - corr;
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
   eng.sync();
@@ -427,10 +476,7 @@ __device__ __forceinline__ void c5_reset(const Eng& eng, Loc& loc) {
     int32_t x;
     auto* r = loc.touched(t, x);
     loc.clear_bits(x);
-    uint4* q = reinterpret_cast<uint4*>(r);
-    const uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < (int)(sizeof(*r) / 16); i++) q[i] = z;
+    rec_zero(r);
   }
 }
 
@@ -548,7 +594,7 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
                                                     const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                     const int32_t* __restrict__ light, const u32* __restrict__ lw,
                                                     int n_light, int* __restrict__ counter,
-                                                    C5RecT<u32>* __restrict__ wregions, int32_t* __restrict__ wlists,
+                                                    C5RecP* __restrict__ wregions, int32_t* __restrict__ wlists,
                                                     u64* __restrict__ C5, int sh_cap) {
   // endpoints whose region needs at most sh_cap (<= C5_SH_CAP) slots keep records and lists in shared
   // memory (per warp); larger ones use the warp's global region
@@ -558,14 +604,14 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t gw = (size_t)blockIdx.x * (C5_BT / 32) + wib;
   WarpEng eng;
-  C5RecT<u32>* shR = reinterpret_cast<C5RecT<u32>*>(c5_sh + (size_t)wib * C5_SH_WARP_BYTES(sh_cap));
+  C5RecP* shR = reinterpret_cast<C5RecP*>(c5_sh + (size_t)wib * C5_SH_WARP_BYTES(sh_cap));
   int32_t* shL = reinterpret_cast<int32_t*>(shR + sh_cap);
   {
     uint4* z = reinterpret_cast<uint4*>(shR);
-    for (int i = lane; i < (int)(sh_cap * sizeof(C5RecT<u32>) / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = lane; i < (int)(sh_cap * sizeof(C5RecP) / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
   }
   __syncwarp();
-  C5Hash<C5RecT<u32>> loc;
+  C5Hash<C5RecP> loc;
   loc.nL = &w_nL[wib];
   for (;;) {
     int idx = 0;
@@ -681,7 +727,7 @@ __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restri
                                                    const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                    const int32_t* __restrict__ sorted, const u64* __restrict__ keys,
                                                    const int* __restrict__ nbig, int n_total,
-                                                   int* __restrict__ counter, C5RecT<u32>* __restrict__ regions,
+                                                   int* __restrict__ counter, C5RecP* __restrict__ regions,
                                                    int32_t* __restrict__ rlists, u64* __restrict__ C5,
                                                    int32_t* __restrict__ qmem) {
   __shared__ ListEng E;
@@ -693,7 +739,7 @@ __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restri
   __shared__ int s_idx, s_nL, s_nJ;
   __shared__ u64 s_tot;
   CtaEng eng{&E};
-  C5Hash<C5RecT<u32>> loc;
+  C5Hash<C5RecP> loc;
   loc.R = regions + (size_t)blockIdx.x * C5_MID_CAP;
   loc.L = rlists + (size_t)blockIdx.x * 2 * C5_MID_CAP;
   loc.nL = &s_nL;

@@ -1198,7 +1198,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_c5_mid, C5_MBT, 0));
         const char* mb_env = getenv("EVOKE_C5_MBPS");  // developer knob: mid CTAs per SM
         const int gm = std::max(1, std::min(bpm, mb_env ? atoi(mb_env) : 4)) * SM;
-        C5RecT<u32>* mreg = A.zalloc<C5RecT<u32>>((size_t)gm * C5_MID_CAP);
+        C5RecP* mreg = A.zalloc<C5RecP>((size_t)gm * C5_MID_CAP);
         int32_t* mlists = A.alloc<int32_t>((size_t)gm * 2 * C5_MID_CAP);
         int32_t* mq = A.alloc<int32_t>((size_t)gm * (2 * (size_t)g.max_deg + 1));
         const u64* mkeys = n5h > 1 ? hkeys : c5w;
@@ -1237,7 +1237,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const char* lb_env = getenv("EVOKE_C5_LBPS");  // developer knob: light CTAs per SM
       const int lg = std::max(1, std::min(bps, lb_env ? atoi(lb_env) : 4)) * SM;
       const size_t nw = (size_t)lg * (C5_BT / 32);
-      C5RecT<u32>* reg = A.zalloc<C5RecT<u32>>(nw * C5_WARP_CAP);
+      C5RecP* reg = A.zalloc<C5RecP>(nw * C5_WARP_CAP);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
         k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out,
