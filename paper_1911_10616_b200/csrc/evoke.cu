@@ -582,7 +582,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* l0 = A.alloc<int32_t>(n);
     int32_t* l1 = A.alloc<int32_t>(n);
     PeelCtl* ctl = A.alloc<PeelCtl>(1, true);
-    int peel_switch = (int)std::min<int64_t>(n, PEEL_SWITCH);
+    const char* psw_env = getenv("EVOKE_PEEL_SWITCH");  // developer knob (<= PEEL_SWITCH)
+    int peel_switch = (int)std::min<int64_t>(n, psw_env ? std::max(64, std::min(PEEL_SWITCH, atoi(psw_env))) : PEEL_SWITCH);
     int32_t* lidmap = A.alloc<int32_t>(n);
     int32_t* loc = A.alloc<int32_t>(peel_switch + 1);
     int32_t* lcnt = A.alloc<int32_t>(peel_switch + 1);
