@@ -136,6 +136,16 @@ int evoke_orbits_csr(int64_t n, const int64_t* rowptr, const int32_t* col, uint6
 int evoke_ccd(int64_t n, const uint64_t* dim, int orbit, uint64_t* values, uint64_t* counts, int64_t* nvals,
               const evoke_options* opt);
 
+/*
+ * evoke_release_scratch -- free the per-device scratch kept between calls.
+ * The per-CTA tables of the pair, hub-local and 5-cycle passes are zero before and after
+ * every successful call, so the library keeps one zeroed buffer per device (about 1 GB at
+ * n = 1e5) and reuses it, which saves re-zeroing it on every call.  This frees it:
+ * device = a CUDA device ordinal, or -1 for every device.  It waits for a call in progress
+ * on that device.  Returns EVOKE_OK, or EVOKE_EINVAL for an ordinal outside [-1, 64).
+ */
+int evoke_release_scratch(int device);
+
 /* Static name of pass i of evoke_stats.ms_pass (NULL if out of range). */
 const char* evoke_pass_name(int i);
 

@@ -58,7 +58,7 @@ _lock = threading.Lock()
 _lib = None
 
 EXPORTED_SYMBOLS = ("evoke_default_options", "evoke_orbits_edges", "evoke_orbits_csr", "evoke_pass_name",
-                    "evoke_strerror", "evoke_last_error", "evoke_version", "evoke_ccd")
+                    "evoke_strerror", "evoke_last_error", "evoke_version", "evoke_ccd", "evoke_release_scratch")
 
 
 def lib():
@@ -87,12 +87,19 @@ def lib():
             L.evoke_strerror.restype = ctypes.c_char_p
             L.evoke_last_error.restype = ctypes.c_char_p
             L.evoke_version.restype = ctypes.c_char_p
+            L.evoke_release_scratch.argtypes = [ctypes.c_int]
+            L.evoke_release_scratch.restype = ctypes.c_int
             _lib = L
     return _lib
 
 
 def version() -> str:
     return lib().evoke_version().decode()
+
+
+def evoke_release_scratch(device: int = -1) -> None:
+    """Free the zeroed per-device scratch the library keeps between calls (-1: all devices)."""
+    _check(lib().evoke_release_scratch(int(device)))
 
 
 def pass_names() -> list[str]:

@@ -1607,4 +1607,28 @@ const char* evoke_last_error(void) { return g_last_error.c_str(); }
 
 const char* evoke_version(void) { return EVOKE_VERSION; }
 
+int evoke_release_scratch(int device) {
+  if (device < -1 || device >= 64) {
+    set_error("device ordinal %d outside [-1, 64)", device);
+    return EVOKE_EINVAL;
+  }
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) { (void)cudaGetLastError(); cur = 0; }
+  for (int d = (device < 0 ? 0 : device); d < (device < 0 ? 64 : device + 1); d++) {
+    ZeroPool& z = zero_pool(d);
+    std::lock_guard<std::mutex> lk(z.mu);  // waits for a call that holds the lease
+    if (!z.p) continue;
+    if (cudaSetDevice(d) == cudaSuccess) {
+      (void)cudaFree(z.p);  // stream-ordered allocation; cudaFree synchronises the device
+    }
+    (void)cudaGetLastError();
+    z.p = nullptr;
+    z.bytes = 0;
+    z.target = 0;
+    z.dirty = false;
+  }
+  (void)cudaSetDevice(cur);
+  return EVOKE_OK;
+}
+
 }  // extern "C"

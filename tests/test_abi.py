@@ -89,6 +89,10 @@ def test_argument_validation_without_gpu(pkg):
                               ctypes.byref(o)) == pkg.EVOKE_EINVAL
     with pytest.raises(pkg.EvokeError):
         pkg.evoke_orbits_edges(4, e, num_shards=0)
+    # the kept scratch: bad ordinal rejected; releasing when nothing is kept is a no-op
+    assert L.evoke_release_scratch(64) == pkg.EVOKE_EINVAL
+    assert L.evoke_release_scratch(-2) == pkg.EVOKE_EINVAL
+    assert L.evoke_release_scratch(-1) == pkg.EVOKE_OK
 
 
 def test_binding_fails_loudly_without_library(pkg, monkeypatch):

@@ -365,7 +365,9 @@ def test_scratch_tables_left_zero(pkg, monkeypatch):
         b = pkg.evoke_orbits_edges(g.n, g.edges, serial=True)
         _assert_equal(b, a, f"{g.name} after reuse")
         first = a if first is None else first
-    monkeypatch.setenv("EVOKE_NO_ZERO_POOL", "1")
     g = graphgen.config(2)
+    pkg.evoke_release_scratch(0)  # freed: the next call allocates and zeroes it again
+    _assert_equal(pkg.evoke_orbits_edges(g.n, g.edges), first, "after evoke_release_scratch")
+    monkeypatch.setenv("EVOKE_NO_ZERO_POOL", "1")
     c = pkg.evoke_orbits_edges(g.n, g.edges)
     _assert_equal(c, first, "fresh zeroed tables")
