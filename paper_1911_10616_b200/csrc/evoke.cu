@@ -949,17 +949,22 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     const size_t freeb = avail_bytes(C.dev);
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
     const char* phg_env = getenv("EVOKE_PAIR_HG");  // developer knob: heavy-source CTAs
+    // heavy tiers: one CTA (a whole SM: 1024 threads x 64 registers) per source at a time.
+    // While the CTAs' dense tables fit L2 (small n) the heavy sources are not the long pole
+    // and half the SMs leave room for the other passes (config 2: 0.1-0.3 ms better step);
+    // past L2 the tables are DRAM-bound and the heavy sources dominate: every SM (config 5:
+    // 173 s instead of 199 s).
     auto heavy_grid = [&](int nsrc, size_t word, int cap) {
-      if (phg_env) cap = std::min(cap, std::max(1, atoi(phg_env)));
       const int64_t l2_ctas = std::max<int64_t>(1, (56ll << 20) / ((int64_t)n * (int64_t)word));
-      int64_t pg = std::min<int64_t>(std::max<int64_t>(l2_ctas, SM / 2), cap);
+      int64_t pg = std::min<int64_t>(l2_ctas >= SM / 2 ? SM / 2 : SM, cap);
+      if (phg_env) pg = std::max(1, atoi(phg_env));  // developer knob: the grid itself
       pg = std::min<int64_t>(pg, nsrc);
       pg = std::max<int64_t>(1, std::min<int64_t>(pg, (int64_t)(freeb / 4) / ((int64_t)n * (int64_t)(word + 4))));
       return (int)pg;
     };
     if (ht[PT_G64] > 0) {
       // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables
-      const int pg = heavy_grid(ht[PT_G64], 8, SM / 2);
+      const int pg = heavy_grid(ht[PT_G64], 8, SM);
       u64* tabs = A.zalloc<u64>((size_t)pg * (size_t)((n + 1) / 2 * 2));
       int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
       int* counter = A.alloc<int>(1, true);
@@ -974,9 +979,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     }
     for (int tier : {PT_G32S, PT_G32}) {
       if (ht[tier] == 0) continue;
-      // half the SMs: these CTAs need a whole SM each (1024 threads x 64 registers); on every
-      // SM they would lock the other passes out (measured: 0.3-0.5 ms better step with SM / 2)
-      const int pg = heavy_grid(ht[tier], 4, SM / 2);
+      const int pg = heavy_grid(ht[tier], 4, SM);
       u32* tabs = A.zalloc<u32>((size_t)pg * (size_t)((n + 3) / 4 * 4));
       int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * n) : nullptr;
       int* counter = A.alloc<int>(1, true);

@@ -21,6 +21,7 @@ torch.cuda.synchronize()
 t1 = time.perf_counter()
 print(f"config 5: n {g.n} m {st['m']} wall {t1 - t0:.1f} s, lib {st['ms_total'] / 1e3:.1f} s")
 print({k: round(v / 1e3, 2) for k, v in st["ms_pass"].items() if v > 100})
-x = out.cpu().numpy().view("uint64")
-_invariants(g, x, check_cliques=False)
-print("invariants ok")
+if "--no-check" not in sys.argv:
+    x = out.cpu().numpy().view("uint64")
+    _invariants(g, x, check_cliques=False)
+    print("invariants ok")
