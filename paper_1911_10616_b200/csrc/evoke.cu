@@ -1363,7 +1363,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     float gms = 0;
     CK(cudaEventElapsedTime(&gms, C.ev[0], C.ev[P_COUNT]));
     const double hms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - C.hts[0]).count();
-    if (hms > 25.0) {
+    if (hms > std::max(0.0, atof(getenv("EVOKE_HOSTPROF")))) {  // EVOKE_HOSTPROF=<ms>: report calls slower than this
       fprintf(stderr, "[evoke hostprof] call host %.1f ms gpu %.1f ms\n", hms, gms);
       C.host_report();
     }
