@@ -19,7 +19,10 @@
  * Integer semantics: every count is the exact count modulo 2^64 (R20).
  *
  * Threading: calls are independent; one call uses one CUDA device (the current one,
- * or opt->device) and the given stream.  No pointer is retained after return.
+ * or opt->device) and the given stream.  No caller pointer is retained after return.
+ * The library keeps, per device, a few CUDA streams and a zeroed scratch buffer for its
+ * per-CTA tables between calls (a call running concurrently with another on the same
+ * device allocates its own); evoke_release_scratch frees the buffer.
  */
 #ifndef EVOKE_H_
 #define EVOKE_H_
