@@ -1074,7 +1074,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       int hb_per_sm = 0;
       CK(cudaFuncSetAttribute(k_hub_process, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_SMEM));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hb_per_sm, k_hub_process, HUB_BT, HUB_SMEM));
-      const int hg = std::max(1, hb_per_sm) * SM;
+      const char* hhg_env = getenv("EVOKE_HUB_HG");  // developer knob: hub-local CTAs
+      // a short hub-local pass (few items) gets one CTA per SM, not as many as fit: its CTAs
+      // placed ahead of the heavy pair sources' whole-SM CTAs delay those (config 2: 0.1 ms
+      // better); a long one (diamond-heavy graphs) keeps full occupancy (config 3: 4.6 s, not 6.7)
+      const int hub_ctas_per_sm = (int64_t)n_light + n_heavy <= HUB_FEW_ITEMS ? 1 : std::max(1, hb_per_sm);
+      const int hg = hhg_env ? std::max(1, atoi(hhg_env)) : std::min(std::max(1, hb_per_sm), hub_ctas_per_sm) * SM;
       u32* gt = nullptr;
       int32_t* gl = nullptr;
       if (g.max_deg > HUB_SH_DENSE && n_heavy > 0) {

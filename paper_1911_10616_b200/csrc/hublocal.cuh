@@ -33,6 +33,7 @@
 #define HUB_WARP_MAX (HUB_WARP_CAP / 2)              // light item: est <= this
 #define HUB_SMEM (HUB_BT / 32 * HUB_WARP_CAP * 12)   // 96 KB dynamic shared memory
 #define HUB_SH_DENSE (HUB_SMEM / 8)                  // heavy item: shared table if d(v) <= this
+#define HUB_FEW_ITEMS 262144                         // at most this many items: one CTA per SM
 
 // number of entries of the full list [f, f+len) with third vertex < bound: a binary search
 // when the lists are sorted (g.full_sorted), else the whole list (callers then filter)
