@@ -450,7 +450,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   }
   cudaStream_t own = nullptr;
   if (o.stream) C.st = (cudaStream_t)o.stream;
-  else { CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking)); C.st = own; }
+  else C.st = C.stream(Ctx::MAXJOBS - 3, 0);  // the device's kept non-blocking stream (the call ends with a sync)
   C.timing = true;
   for (int i = 0; i <= P_COUNT; i++) CK(cudaEventCreate(&C.ev[i]));
   CK(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
@@ -1265,6 +1265,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // one stream per job (jobs of one pass stay in order on a shared stream when they must:
   // the heavy and main pair kernels write different sources, so all jobs are independent)
   std::stable_sort(jobs.begin(), jobs.end(), [](const Job& x, const Job& y) { return x.rank < y.rank; });
+  // kept streams 0..MAXJOBS-4 are the jobs'; the last three: main (no caller stream), tail
+  // gathers, side
+  if (jobs.size() > (size_t)Ctx::MAXJOBS - 3) { set_error("too many concurrent jobs"); throw EvokeError{EVOKE_EINTERNAL}; }
   const bool serial = (o.flags & EVOKE_FLAG_SERIAL) != 0;
   if (C.side_used) CK(cudaStreamWaitEvent(C.st, C.ev_side, 0));
   CK(cudaEventRecord(C.ev_fork, C.st));
