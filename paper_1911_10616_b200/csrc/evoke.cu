@@ -874,7 +874,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   auto gather = [&](auto kw, auto kh, int slot) { gather_on(C.st, kw, kh, slot); };
   const bool serial_flag = (o.flags & EVOKE_FLAG_SERIAL) != 0;
   cudaStream_t pre = C.st;
-  if (!serial_flag && n > 0) {
+  if (!serial_flag && n > 0 && !getenv("EVOKE_NO_SIDE")) {  // (EVOKE_NO_SIDE: developer A/B)
     pre = C.stream(Ctx::MAXJOBS - 1, 0);
     C.side_used = true;
     CK(cudaEventRecord(C.ev_pre, C.st));
@@ -1290,7 +1290,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   auto trigather = [&](cudaStream_t gs) {
     if (ntri > 0 && !four) { k_trigather<<<grid_for(ntri, B, SM), B, 0, gs>>>(g, ev, F); C.launches++; }
   };
-  if (!serial && n > 0) {
+  if (!serial && n > 0 && !getenv("EVOKE_NO_EARLY_GATHERS")) {
     C.gathers_early = true;
     cudaStream_t gs = C.stream(Ctx::MAXJOBS - 2, 0);
     CK(cudaStreamWaitEvent(gs, C.ev_fork, 0));
