@@ -552,12 +552,32 @@ int oracle_noninduced_bruteforce(int64_t n, int64_t m, const int32_t *edges, uin
   return 0;
 }
 
-/* Simple clique / triangle totals by plain enumeration over sorted adjacency
- * (used for whole-matrix invariants at sizes the ESU cannot reach).
+/* Simple clique / triangle totals by plain enumeration (used for whole-matrix
+ * invariants at sizes the ESU cannot reach: Sigma_v DIM3 = 3 #K3, Sigma_v DIM14 =
+ * 4 #K4, Sigma_v DIM72 = 5 #K5; cliques = P:702 / P:861-864).
+ * Each clique is counted once, at its first vertex in the paper's degree order
+ * (vertices ordered by degree, ties by id): for every vertex a, the
+ * pairwise-adjacent 2-, 3- and 4-subsets of its later neighbours N>(a), taken
+ * in increasing list position.  The order only bounds |N>(a)|; any total order
+ * counts every clique exactly once.
  * counts[0] = #triangles, counts[1] = #4-cliques, counts[2] = #5-cliques. */
+static int later(const graph_t *g, int a, int b) {  /* b after a in degree order */
+  int64_t da = g->rp[a + 1] - g->rp[a], db = g->rp[b + 1] - g->rp[b];
+  return db > da || (db == da && b > a);
+}
+
 int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *counts, int threads) {
   graph_t g;
   if (graph_build(&g, n, m, edges)) return -1;
+  /* N>(a) for every a, in increasing id order (a filtered copy of the sorted list) */
+  int64_t *orp = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  int32_t *oadj = (int32_t *)malloc(sizeof(int32_t) * (size_t)(g.rp[n] / 2 + 1));
+  if (!orp || !oadj) { free(orp); free(oadj); graph_free(&g); return -1; }
+  for (int64_t a = 0; a < n; a++) {
+    orp[a + 1] = orp[a];
+    for (int64_t p = g.rp[a]; p < g.rp[a + 1]; p++)
+      if (later(&g, (int)a, g.adj[p])) oadj[orp[a + 1]++] = g.adj[p];
+  }
   uint64_t t3 = 0, t4 = 0, t5 = 0;
 #ifdef _OPENMP
   if (threads > 0) omp_set_num_threads(threads);
@@ -566,19 +586,18 @@ int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *c
 #endif
 #pragma omp parallel for schedule(dynamic, 64) reduction(+:t3, t4, t5)
   for (int64_t a = 0; a < n; a++) {
-    for (int64_t pb = g.rp[a]; pb < g.rp[a + 1]; pb++) {
-      int b = g.adj[pb];
-      if (b <= a) continue;
-      for (int64_t pc = pb + 1; pc < g.rp[a + 1]; pc++) {
-        int c = g.adj[pc];
+    for (int64_t pb = orp[a]; pb < orp[a + 1]; pb++) {
+      int b = oadj[pb];
+      for (int64_t pc = pb + 1; pc < orp[a + 1]; pc++) {
+        int c = oadj[pc];
         if (!has_edge(&g, b, c)) continue;
         t3++;
-        for (int64_t pd = pc + 1; pd < g.rp[a + 1]; pd++) {
-          int d = g.adj[pd];
+        for (int64_t pd = pc + 1; pd < orp[a + 1]; pd++) {
+          int d = oadj[pd];
           if (!has_edge(&g, b, d) || !has_edge(&g, c, d)) continue;
           t4++;
-          for (int64_t pe = pd + 1; pe < g.rp[a + 1]; pe++) {
-            int e = g.adj[pe];
+          for (int64_t pe = pd + 1; pe < orp[a + 1]; pe++) {
+            int e = oadj[pe];
             if (has_edge(&g, b, e) && has_edge(&g, c, e) && has_edge(&g, d, e)) t5++;
           }
         }
@@ -586,6 +605,7 @@ int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *c
     }
   }
   counts[0] = t3; counts[1] = t4; counts[2] = t5;
+  free(orp); free(oadj);
   graph_free(&g);
   return 0;
 }

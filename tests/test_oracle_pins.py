@@ -339,3 +339,54 @@ def test_whole_matrix_invariants():
         sz = {o: P["orb"].count(o) for o in orbs}
         for a_, b_ in itertools.combinations(orbs, 2):
             assert sz[b_] * out[:, a_].sum() == sz[a_] * out[:, b_].sum()
+
+
+# ------------------------------------------------------------ clique totals ---
+# oracle.clique_totals feeds the whole-matrix invariants Sigma DIM3 = 3 #K3, Sigma DIM14 =
+# 4 #K4, Sigma DIM72 = 5 #K5 (cliques: P:702) on configs the ESU cannot reach.
+def _cliques_by_subsets(n, edges):
+    adj = [set() for _ in range(n)]
+    for a, b in edges:
+        if a != b:
+            adj[a].add(b)
+            adj[b].add(a)
+    out = []
+    for k in (3, 4, 5):
+        out.append(sum(1 for S in itertools.combinations(range(n), k)
+                       if all(y in adj[x] for x, y in itertools.combinations(S, 2))))
+    return tuple(out)
+
+
+def test_clique_totals_vs_all_subsets():
+    rng = random.Random(71)
+    for _ in range(60):
+        n, e = rand_graph(rng, 3, 14, 0.2, 0.95)
+        assert oracle.clique_totals(n, e) == _cliques_by_subsets(n, e), (n, e)
+
+
+def test_clique_totals_vs_esu_on_dense_graphs():
+    """the ESU's column sums (pinned to all-subsets brute force above) divided by the orbit
+    multiplicity: Sigma DIM3 / 3, Sigma DIM14 / 4, Sigma DIM72 / 5"""
+    rng = random.Random(72)
+    for t in range(24):
+        n, e = rand_graph(rng, 15, 32, 0.45, 0.92)
+        dim = oracle.orbits(n, e).astype(object)
+        s3, s14, s72 = dim[:, 3].sum(), dim[:, 14].sum(), dim[:, 72].sum()
+        assert s3 % 3 == 0 and s14 % 4 == 0 and s72 % 5 == 0
+        assert oracle.clique_totals(n, e) == (s3 // 3, s14 // 4, s72 // 5), (t, n, len(e))
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 9, 17, 40])
+def test_clique_totals_complete_graph(n):
+    assert oracle.clique_totals(n, graphgen.complete(n).edges) == (C(n, 3), C(n, 4), C(n, 5))
+
+
+def test_clique_totals_complete_multipartite():
+    """K_{p1,...,pr}: #K_k = e_k(p1..pr) (elementary symmetric polynomial: one vertex from each of
+    k distinct parts); equal degrees inside a part exercise the order's id tie-break"""
+    for parts in [(2, 3, 4), (1, 1, 5, 2), (3, 3, 3, 3, 3), (4, 1, 2, 6, 3)]:
+        offs = np.cumsum((0,) + parts)
+        e = [(a, b) for i in range(len(parts)) for j in range(i + 1, len(parts))
+             for a in range(offs[i], offs[i + 1]) for b in range(offs[j], offs[j + 1])]
+        ek = [sum(int(np.prod(c)) for c in itertools.combinations(parts, k)) for k in (3, 4, 5)]
+        assert oracle.clique_totals(int(offs[-1]), e) == tuple(ek), parts
