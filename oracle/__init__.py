@@ -48,7 +48,7 @@ def _load():
                                               ip, ctypes.c_uint64, ctypes.c_int]
             lib.oracle_orbits_bruteforce.argtypes = [i64, i64, i32p, u64p]
             lib.oracle_noninduced_bruteforce.argtypes = [i64, i64, i32p, u64p]
-            lib.oracle_clique_totals.argtypes = [i64, i64, i32p, u64p, ctypes.c_int]
+            lib.oracle_clique_totals.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_pattern.argtypes = [ctypes.c_int, ip, ip, ip, ip]
             lib.oracle_automorphism_classes.argtypes = [ctypes.c_int, ip, ip]
             lib.oracle_classify.argtypes = [ctypes.c_int, ctypes.c_int, ip]
@@ -114,14 +114,16 @@ def noninduced_bruteforce(n: int, edges) -> np.ndarray:
     return out
 
 
-def clique_totals(n: int, edges, threads: int = 0):
-    """(#triangles, #4-cliques, #5-cliques) by plain nested enumeration."""
+def clique_totals(n: int, edges, threads: int = 0, kmax: int = 5):
+    """(#triangles, #4-cliques, #5-cliques) by plain nested enumeration; cliques larger than
+    ``kmax`` (3..5) are not counted and come back as None."""
     lib = _load()
     e = _edges(edges)
     c = np.zeros(3, dtype=np.uint64)
-    if lib.oracle_clique_totals(n, e.shape[0], _ptr(e, ctypes.c_int32), _ptr(c, ctypes.c_uint64), threads):
+    if lib.oracle_clique_totals(n, e.shape[0], _ptr(e, ctypes.c_int32), _ptr(c, ctypes.c_uint64), threads,
+                                int(kmax)):
         raise RuntimeError("oracle_clique_totals failed")
-    return int(c[0]), int(c[1]), int(c[2])
+    return int(c[0]), (int(c[1]) if kmax >= 4 else None), (int(c[2]) if kmax >= 5 else None)
 
 
 def catalog():

@@ -560,13 +560,15 @@ int oracle_noninduced_bruteforce(int64_t n, int64_t m, const int32_t *edges, uin
  * pairwise-adjacent 2-, 3- and 4-subsets of its later neighbours N>(a), taken
  * in increasing list position.  The order only bounds |N>(a)|; any total order
  * counts every clique exactly once.
- * counts[0] = #triangles, counts[1] = #4-cliques, counts[2] = #5-cliques. */
+ * counts[0] = #triangles, counts[1] = #4-cliques, counts[2] = #5-cliques; only cliques
+ * of at most kmax (3..5) vertices are counted (the others are left 0), so the invariants
+ * reach graphs whose 5-cliques number in the 10^10s. */
 static int later(const graph_t *g, int a, int b) {  /* b after a in degree order */
   int64_t da = g->rp[a + 1] - g->rp[a], db = g->rp[b + 1] - g->rp[b];
   return db > da || (db == da && b > a);
 }
 
-int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *counts, int threads) {
+int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *counts, int threads, int kmax) {
   graph_t g;
   if (graph_build(&g, n, m, edges)) return -1;
   /* N>(a) for every a, in increasing id order (a filtered copy of the sorted list) */
@@ -592,10 +594,12 @@ int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *c
         int c = oadj[pc];
         if (!has_edge(&g, b, c)) continue;
         t3++;
+        if (kmax < 4) continue;
         for (int64_t pd = pc + 1; pd < orp[a + 1]; pd++) {
           int d = oadj[pd];
           if (!has_edge(&g, b, d) || !has_edge(&g, c, d)) continue;
           t4++;
+          if (kmax < 5) continue;
           for (int64_t pe = pd + 1; pe < orp[a + 1]; pe++) {
             int e = oadj[pe];
             if (has_edge(&g, b, e) && has_edge(&g, c, e) && has_edge(&g, d, e)) t5++;

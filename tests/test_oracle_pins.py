@@ -390,3 +390,30 @@ def test_clique_totals_complete_multipartite():
              for a in range(offs[i], offs[i + 1]) for b in range(offs[j], offs[j + 1])]
         ek = [sum(int(np.prod(c)) for c in itertools.combinations(parts, k)) for k in (3, 4, 5)]
         assert oracle.clique_totals(int(offs[-1]), e) == tuple(ek), parts
+
+
+def test_clique_totals_kmax():
+    rng = random.Random(73)
+    for _ in range(10):
+        n, e = rand_graph(rng, 8, 14, 0.5, 0.95)
+        t3, t4, t5 = _cliques_by_subsets(n, e)
+        assert oracle.clique_totals(n, e, kmax=3) == (t3, None, None)
+        assert oracle.clique_totals(n, e, kmax=4) == (t3, t4, None)
+
+
+def test_degree_forms_vs_noninduced_bruteforce():
+    """the degree-only closed forms the GPU tests apply to every vertex of configs 2-4
+    (tests/degree_forms.py) equal the non-induced brute force on random graphs"""
+    from degree_forms import COLUMNS, degree_forms
+    rng = random.Random(74)
+    for _ in range(40):
+        n, e = rand_graph(rng, 2, 10, 0.15, 0.95)
+        dm = oracle.noninduced_bruteforce(n, e)
+        f = degree_forms(n, e)
+        for c in COLUMNS:
+            assert (dm[:, c] == f[c]).all(), (c, n, e)
+    # wrap-around: C(s, 4) >= 2^64 for the centre of K_{1,s}, s = 145,100 (R20)
+    s = 145_100
+    f = degree_forms(s + 1, graphgen.star(s).edges)
+    assert comb(s, 4) >= 1 << 64 and int(f[23][0]) == comb(s, 4) % (1 << 64)
+    assert int(f[22][1]) == comb(s - 1, 3) and int(f[6][1]) == comb(s - 1, 2) and int(f[1][1]) == s - 1
