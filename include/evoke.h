@@ -66,6 +66,11 @@ typedef struct evoke_stats {
   int64_t units[8];             /* sum d^2, sum T(e)^2, hub visits, c5 wedge visits,
                                    c5 out-out + path visits, triangle-pass stream,
                                    pair wedges walked (without h*), sum d(h*)         */
+  /* work-balanced sharding (num_shards > 1): the work estimates of the sharded passes
+   * [pair, hub-local, 5-cycle, 4/5-clique] summed over this shard's units and over all
+   * units; max over shards / (total / num_shards) is the imbalance */
+  uint64_t work_shard[4];
+  uint64_t work_total[4];
 } evoke_stats;
 
 #define EVOKE_FLAG_WORKMODEL 1  /* fill evoke_stats.alg_bytes / units (extra kernels)  */
@@ -89,7 +94,10 @@ typedef struct evoke_options {
                              for bit (multi-GPU data parallelism)         */
   int32_t device;         /* CUDA device ordinal; -1 (default) = current device      */
   int32_t flags;          /* EVOKE_FLAG_* bits; 0 default                            */
-  void* stream;           /* cudaStream_t to run on; NULL = a library-owned stream   */
+  void* stream;           /* cudaStream_t to run on; NULL = a library-owned stream,
+                             ordered after the work already queued on the legacy
+                             default stream (so device-pointer inputs produced there,
+                             e.g. by torch's default stream, are complete)            */
   evoke_stats* stats;     /* optional output                                         */
 } evoke_options;
 
@@ -108,7 +116,9 @@ void evoke_default_options(evoke_options* opt);
  *   opt    NULL for defaults
  * Host pointers are copied to the device inside the call (the copies are part of the
  * call); with device_pointers=1 no host transfer happens.  Returns EVOKE_OK or a
- * negative code; on error `out` is untouched and evoke_last_error() has a message.
+ * negative code; on error `out` is untouched and evoke_last_error() has a message (the
+ * result is staged in library scratch and copied to `out` only after the final checks,
+ * for host and device pointers alike).
  */
 int evoke_orbits_edges(int64_t n, int64_t m, const int32_t* edges, uint64_t* out,
                        const evoke_options* opt);
@@ -145,7 +155,10 @@ int evoke_ccd(int64_t n, const uint64_t* dim, int orbit, uint64_t* values, uint6
  * every successful call, so the library keeps one zeroed buffer per device (about 1 GB at
  * n = 1e5) and reuses it, which saves re-zeroing it on every call.  This frees it:
  * device = a CUDA device ordinal, or -1 for every device.  It waits for a call in progress
- * on that device.  Returns EVOKE_OK, or EVOKE_EINVAL for an ordinal outside [-1, 64).
+ * on that device, and also trims the library's private stream-ordered memory pool (the
+ * scratch of earlier calls it keeps mapped for reuse) back to zero bytes, so the memory is
+ * available to other allocators again.  Returns EVOKE_OK, or EVOKE_EINVAL for an ordinal
+ * outside [-1, 64).
  */
 int evoke_release_scratch(int device);
 

@@ -40,7 +40,8 @@ class _Stats(ctypes.Structure):
                 ("ms_total", ctypes.c_double), ("ms_pass", ctypes.c_double * 16),
                 ("num_passes", ctypes.c_int32), ("kernel_launches", ctypes.c_int32),
                 ("library_launches", ctypes.c_int32), ("reserved0", ctypes.c_int32),
-                ("alg_bytes", ctypes.c_double * 16), ("units", ctypes.c_int64 * 8)]
+                ("alg_bytes", ctypes.c_double * 16), ("units", ctypes.c_int64 * 8),
+                ("work_shard", ctypes.c_uint64 * 4), ("work_total", ctypes.c_uint64 * 4)]
 
 
 class _Options(ctypes.Structure):
@@ -49,6 +50,7 @@ class _Options(ctypes.Structure):
                 ("num_shards", ctypes.c_int32), ("device", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("stats", ctypes.POINTER(_Stats))]
 
+SHARDED_PASSES = ("pair_pass", "hub_local", "cycles5", "cliques")
 FLAG_WORKMODEL = 1
 FLAG_SERIAL = 2
 FLAG_FOUR = 4
@@ -141,7 +143,9 @@ def _stats_dict(s: _Stats) -> dict:
             "alg_bytes": {names[i]: s.alg_bytes[i] for i in range(min(s.num_passes, len(names)))},
             "units": {k: s.units[i] for i, k in enumerate(("sum_d2", "sum_te2", "hub", "c5_wedge", "c5_q",
                                                            "tri_stream", "pair_rwedge", "pair_hwalk"))},
-            "kernel_launches": s.kernel_launches, "library_launches": s.library_launches}
+            "kernel_launches": s.kernel_launches, "library_launches": s.library_launches,
+            "work_shard": {k: s.work_shard[i] for i, k in enumerate(SHARDED_PASSES)},
+            "work_total": {k: s.work_total[i] for i, k in enumerate(SHARDED_PASSES)}}
 
 
 def _check(rc: int):
@@ -168,7 +172,7 @@ def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_inde
         m = e.numel() // 2
         if out is None:
             out = torch.empty((n, NUM_ORBITS), dtype=torch.int64, device=e.device)
-        assert out.is_cuda and out.is_contiguous() and out.numel() == n * NUM_ORBITS
+        assert out.is_cuda and out.device == e.device and out.is_contiguous() and out.numel() == n * NUM_ORBITS
         if stream is None:
             stream = torch.cuda.current_stream(e.device).cuda_stream
         o = _make_options(induced, True, shard_index, num_shards, e.device.index, stream, st, fl)
@@ -195,10 +199,14 @@ def evoke_orbits_csr(n: int, rowptr, col, out=None, induced: bool = True, shard_
     fl = (FLAG_WORKMODEL if workmodel else 0) | (FLAG_SERIAL if serial else 0) | (FLAG_FOUR if four_only else 0)
     if _is_torch(rowptr):
         import torch
+        assert rowptr.is_cuda and rowptr.dtype == torch.int64, "device rowptr must be CUDA int64"
+        assert col.is_cuda and col.dtype == torch.int32, "device col must be CUDA int32"
+        assert rowptr.device == col.device and rowptr.numel() == n + 1
         rp = rowptr.contiguous()
         cl = col.contiguous()
         if out is None:
             out = torch.empty((n, NUM_ORBITS), dtype=torch.int64, device=rp.device)
+        assert out.is_cuda and out.device == rp.device and out.is_contiguous() and out.numel() == n * NUM_ORBITS
         if stream is None:
             stream = torch.cuda.current_stream(rp.device).cuda_stream
         o = _make_options(induced, True, shard_index, num_shards, rp.device.index, stream, st, fl)
@@ -206,8 +214,10 @@ def evoke_orbits_csr(n: int, rowptr, col, out=None, induced: bool = True, shard_
     else:
         rp = np.ascontiguousarray(np.asarray(rowptr, dtype=np.int64))
         cl = np.ascontiguousarray(np.asarray(col, dtype=np.int32))
+        assert rp.size == n + 1, "rowptr must have n + 1 entries"
         if out is None:
             out = np.zeros((n, NUM_ORBITS), dtype=np.uint64)
+        assert out.dtype == np.uint64 and out.flags.c_contiguous and out.size == n * NUM_ORBITS
         o = _make_options(induced, False, shard_index, num_shards, None, stream, st, fl)
         rc = lib().evoke_orbits_csr(n, rp.ctypes.data, cl.ctypes.data if cl.size else None, out.ctypes.data,
                                     ctypes.byref(o))

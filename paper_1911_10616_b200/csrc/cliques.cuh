@@ -37,7 +37,7 @@ __device__ __forceinline__ int row_rank(const u32* __restrict__ R, int W, int i,
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cliques(
     DGraph g, const int32_t* __restrict__ ulist, int nu, int smem_words, u32* __restrict__ gscratch,
-    int64_t gscratch_words, int do_k4, int shard_index, int num_shards,
+    int64_t gscratch_words, int do_k4, const uint8_t* __restrict__ mine,
     const u32* __restrict__ Te, u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
     u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70) {
   extern __shared__ u32 sh_bits[];
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) k_cliques(
   __syncthreads();
   for (int idx = blockIdx.x; idx < nu; idx += gridDim.x) {
     const int32_t u = ulist[idx];
-    const bool in_shard = (u % num_shards) == shard_index;  // deterministic across calls
+    const bool in_shard = !mine || mine[u];  // this shard's units (work-balanced, deterministic)
     const bool do_k5 = (MODE == 0) && in_shard;
     if (MODE == 0 && !do_k4 && !do_k5) continue;
     if (MODE == 1 && !in_shard) continue;

@@ -25,16 +25,15 @@
 // Each (path, wedge) pair with distinct vertices is one 5-cycle; the tests check the
 // identity against brute force (tests/test_gpu_parity.py).
 //
-// Scheduling (B200): k_c5_items measures every endpoint's work W(l) (steps 1/6, 2/4 and
-// an upper bound of step 3) and splits the endpoints into light ones (one WARP each,
-// records in a per-warp open-addressing region) and heavy ones (one CTA each, sorted by
-// W descending, records dense by vertex id).  Records are 64-byte AoS (one or two
-// sectors per touched vertex).  All list walks go through the load-balanced engines
-// of sched.cuh (warp_lists / cta_lists).
+// Scheduling (B200): k_c5_splus / k_c5_work give every endpoint its exact work W(l) and
+// record bound R(l) in O(m) total; k_c5_bin splits this shard's endpoints into light ones
+// (one WARP each, packed records in a per-warp open-addressing region, shared memory when
+// small), mid ones (one 128-thread CTA each, packed records in a per-CTA hash region) and
+// big ones (one 1024-thread CTA each, sorted by W descending, records dense by vertex id).
+// All list walks go through the load-balanced engines of sched.cuh (warp_lists / cta_lists).
 #pragma once
 #include "common.cuh"
 #include "sched.cuh"
-#include <cooperative_groups.h>
 
 // Record of one vertex for one endpoint.  wf = Wn | flags << 28 (Wn < 2^28 because Wn(i)
 // <= d(l) and max degree < 2^28 is checked); V = u32 when the endpoint's work bound W(l) <
@@ -112,17 +111,17 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 #define C5_PRESENT 8u  // record in use (touched list)
 
 #define C5_BT 256
-#define C5_WARP_MAX 1024          // light endpoint: W(l) + d(l) <= this
+#define C5_WARP_MAX 1024          // light endpoint: record bound R(l) <= this ...
+#define C5_WARP_WORK 8192         // ... and work W(l) <= this
 #define C5_WARP_CAP 2048          // records per warp region (load <= 0.5)
 #define C5_SH_CAP 256             // light endpoints with a region of <= this many slots: shared memory
 #define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (sizeof(C5RecP) + 2 * 4))   // records + touched + J lists
 #define C5_SH_BYTES(cap) ((C5_BT / 32) * C5_SH_WARP_BYTES(cap))
-#define C5_GIANT (1ull << 40)     // endpoint work above which a thread-block cluster takes it (off)
 #define C5_HBT 1024               // heavy-endpoint CTA
-#define C5_MID_MAX 4096           // mid endpoint: C5_WARP_MAX < W(l) <= this ...
-#define C5_MID_CAP (2 * C5_MID_MAX)  // ... hashed records in a per-CTA global region (load <= 0.5)
+#define C5_MID_MAX 4096           // mid endpoint: R(l) <= this ...
+#define C5_MID_WORK 65535         // ... and W(l) <= this (packed 16-bit record fields)
+#define C5_MID_CAP (2 * C5_MID_MAX)  // hashed records in a per-CTA global region (load <= 0.5)
 #define C5_MBT 128                // mid-endpoint CTA (several endpoints in flight per SM)
-#define C5_BIG_KEY (1ull << 62)   // sort-key bit of the endpoints above C5_MID_MAX
 #define C5_BITS_SMEM_MAX (160 << 10)  // heavy CTAs: shared first-touch bitmaps up to this size
 
 // dense records indexed by vertex id; touched list holds vertex ids
@@ -176,18 +175,10 @@ struct C5Dense {
     newj = !(atomicOr(&bJ[x >> 5], bit) & bit);
     return mark_nr(x, C5_J);
   }
-  // i-key mark in step 3, returning Wn (final since step 1)
-  __device__ __forceinline__ Rec* mark_wn(int32_t x, u64& wn) {
-    if (!bP) {
-      u32 old, word;
-      Rec* r = mark(x, C5_I, old, word);
-      wn = (u64)(word & C5_WN_MASK);
-      return r;
-    }
+  // record of x if Wn[x] > 0 (step 3; Wn is final since step 1), else nullptr
+  __device__ __forceinline__ Rec* peek_i(int32_t x) const {
     Rec* r = &R[x];
-    wn = (u64)(__ldcg(&r->wf) & C5_WN_MASK);
-    mark_nr(x, C5_I);
-    return r;
+    return (__ldcg(&r->wf) & C5_WN_MASK) ? r : nullptr;
   }
   __device__ __forceinline__ Rec* peek(int32_t x) const { return &R[x]; }
   __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
@@ -247,12 +238,6 @@ struct C5Hash {
     newj = !(old & C5_J);
     return r;
   }
-  __device__ __forceinline__ Rec* mark_wn(int32_t x, u64& wn) {
-    u32 old, word;
-    Rec* r = mark(x, C5_I, old, word);
-    wn = (u64)(word & C5_WN_MASK);
-    return r;
-  }
   __device__ __forceinline__ void clear_bits(int32_t) const {}
   __device__ __forceinline__ Rec* peek(int32_t x) const {
     u32 h = h0(x);
@@ -262,6 +247,10 @@ struct C5Hash {
       if (k == 0) return nullptr;
       h = (h + 1) & mask;
     }
+  }
+  __device__ __forceinline__ Rec* peek_i(int32_t x) const {
+    Rec* r = peek(x);
+    return (r && (r->wf & C5_WN_MASK)) ? r : nullptr;
   }
   __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
     Rec* r = &R[L[t]];
@@ -287,33 +276,6 @@ struct CtaEng {
   __device__ __forceinline__ int nthr() const { return blockDim.x; }
   template <typename I, typename E2, typename F>
   __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const { cta_lists(n, *E, info, elem, flush); }
-};
-
-// cluster engine for the giant endpoints: one thread-block cluster of C5_CLUSTER CTAs
-// takes an endpoint; warps of the whole cluster share each step (warp per item) and the
-// steps are separated by hardware cluster barriers (records and counters in global memory)
-#define C5_CLUSTER 8
-struct ClusterEng {
-  static constexpr bool kCta = false;
-  __device__ __forceinline__ void sync() const { cooperative_groups::this_cluster().sync(); }
-  __device__ __forceinline__ int tid() const {
-    return (int)(cooperative_groups::this_cluster().block_rank() * blockDim.x + threadIdx.x);
-  }
-  __device__ __forceinline__ int nthr() const { return (int)(C5_CLUSTER * blockDim.x); }
-  template <typename I, typename E2, typename F>
-  __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const {
-    const int lane = threadIdx.x & 31;
-    const int gw = tid() >> 5, nw = nthr() >> 5;
-    for (int t = gw; t < n; t += nw) {
-      int64_t base;
-      int len;
-      info(t, base, len);
-      u64 acc = 0;
-      for (int k = lane; k < len; k += 32) acc += elem(t, base, k);
-      acc = warp_sum(acc);
-      if (lane == 0 && acc) flush(t, acc);
-    }
-  }
 };
 
 template <typename R>
@@ -390,15 +352,17 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         len = (int)(g.orow[j + 1] - base);
       },
       [&](int t, int64_t base, int k) -> u64 {
+        // Only i with Wn[i] > 0 can close a 5-cycle: a path i <- j <- k -> l with Wn[i] = 0
+        // has j !~ l and i !~ k (both would be wedges (i, w, l)), so its every term (P Wn,
+        // A, the QM correction, its share of S[j]) is zero.  The lookup is read-only: no
+        // record is created for such i (Wn is final after step 1).
         const int32_t i = g.ocol[base + k];
         if (i == l) return 0;
+        auto* ri = loc.peek_i(i);
+        if (!ri) return 0;
         const auto* rj = loc.peek(J[t]);
-        const u64 q = rec_q(rj);
-        const bool adjj = c5_flags(rj) & C5_ADJ;
-        u64 wn;
-        auto* ri = loc.mark_wn(i, wn);  // Wn is final after step 1
-        rec_add_pa(ri, q, adjj);
-        return wn;
+        rec_add_pa(ri, rec_q(rj), c5_flags(rj) & C5_ADJ);
+        return c5_wn(ri);
       },
       [&](int t, u64 s) {
         auto* rj = loc.peek(J[t]);
@@ -481,62 +445,83 @@ __device__ __forceinline__ void c5_reset(const Eng& eng, Loc& loc) {
 }
 
 // ---- per-endpoint work, binning -----------------------------------------------------------
-// W(l) = sum_{w in N(l)} |Nsel(w)| + sum_{k in N-(l)} (d+(k) + sum_{j in N+(k)} d+(j)) + d(l)
-// bounds the records an endpoint touches.  Light: W <= C5_WARP_MAX (the count stops
-// there); heavy otherwise, with sort key d(l)^2 + W (hubs first).
-__global__ void k_c5_items(DGraph g, int shard_index, int num_shards, int32_t* __restrict__ light,
-                           u32* __restrict__ light_w, int* n_light, int32_t* __restrict__ heavy,
-                           u64* __restrict__ heavy_w, int* n_heavy) {
+// Work of endpoint l (every element its steps visit):
+//   W(l) = d(l) + sum_{w in N(l)} |Nsel(w)| + sum_{k in N-(l)} (d+(k) + s+(k)),
+//   s+(k) = sum_{j in N+(k)} d+(j)     (step-3 path elements through k),
+// and the bound on the records it creates (steps 0-2; step 3 creates none):
+//   R(l) = d(l) + sum_{w in N(l)} |Nsel(w)| + sum_{k in N-(l)} d+(k).
+// Every record field is at most W(l) (Wn <= d(l), Q <= d-(l), QT and QM <= sum d+(k),
+// P and A <= #paths, S <= #wedges), which decides the record width.
+__global__ void k_c5_splus(DGraph g, u32* __restrict__ splus) {
+  for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < g.n; k += gridDim.x * blockDim.x) {
+    u32 s = 0;  // <= kappa^2 < 2^31 (kappa <= sqrt(2m), m < 2^30)
+    for (int64_t e = g.orow[k]; e < g.orow[k + 1]; e++) {
+      const int32_t j = g.ocol[e];
+      s += (u32)(g.orow[j + 1] - g.orow[j]);
+    }
+    splus[k] = s;
+  }
+}
+
+// W(l) and R(l) of every vertex, one warp per vertex (hubs' lists split over the lanes)
+__global__ void k_c5_work(DGraph g, const u32* __restrict__ splus, u64* __restrict__ W, u64* __restrict__ R) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = gw * 32; base < g.n; base += nw * 32) {
+  for (int64_t q = gw; q < g.n; q += nw) {
+    const int32_t l = (int32_t)q;
+    const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
+    u64 w = 0, r = 0;
+    for (int64_t s = r0 + lane; s < r1; s += 32) {
+      const int32_t x = g.ci[s];
+      const u64 sel = (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
+      w += sel;
+      r += sel;
+      if (s < rm) {
+        const u64 dpx = (u64)(g.orow[x + 1] - g.orow[x]);
+        w += dpx + (u64)splus[x];
+        r += dpx;
+      }
+    }
+    w = warp_sum(w);
+    r = warp_sum(r);
+    if (lane == 0) {
+      const u64 d = (u64)(r1 - r0);
+      W[l] = d > 0 ? w + d : 0;
+      R[l] = d > 0 ? r + d : 0;
+    }
+  }
+}
+
+// Tiers of this shard's endpoints (mine == nullptr: every endpoint):
+//   light (one warp):  R <= rec_light  and W <= work_light   (packed records, per-warp hash)
+//   mid (128 threads): R <= rec_mid    and W <= work_mid     (packed records, per-CTA hash)
+//   big (1024 threads): the rest (dense records by vertex id, sorted by W descending)
+// Packed 16-bit record fields need W < 2^16 for the light and mid tiers (work_mid < 2^16).
+__global__ void k_c5_bin(DGraph g, const u64* __restrict__ W, const u64* __restrict__ R,
+                         const uint8_t* __restrict__ mine, u64 rec_light, u64 work_light, u64 rec_mid, u64 work_mid,
+                         int32_t* __restrict__ light, u32* __restrict__ light_r, int32_t* __restrict__ mid,
+                         u32* __restrict__ mid_r, int32_t* __restrict__ big, u64* __restrict__ big_w,
+                         int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < g.n;
+       base += (int64_t)gridDim.x * blockDim.x) {
     const int32_t l = (int32_t)min(base + lane, (int64_t)g.n - 1);
-    const bool mine = base + lane < g.n && (l % num_shards) == shard_index && g.deg[l] > 0;
-    u64 w = 0;
-    if (mine) {
-      const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
-      w = (u64)g.deg[l];
-      for (int64_t s = r0; s < r1 && w <= C5_WARP_MAX; s++) {
-        const int32_t x = g.ci[s];
-        w += (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
-        if (s < rm) {
-          const int64_t ok = g.orow[x], ok1 = g.orow[x + 1];
-          w += (u64)(ok1 - ok);
-          for (int64_t e = ok; e < ok1 && w <= C5_WARP_MAX; e++) {
-            const int32_t j = g.ocol[e];
-            w += (u64)(g.orow[j + 1] - g.orow[j]);
-          }
-        }
-      }
-    }
-    const bool is_light = mine && w <= C5_WARP_MAX;
-    const bool is_heavy = mine && w > C5_WARP_MAX;
-    {
-      const u32 bl = __ballot_sync(FULL_MASK, is_light);
-      if (bl) {
-        int lb = 0;
-        const int leader = __ffs(bl) - 1;
-        if (lane == leader) lb = atomicAdd(n_light, __popc(bl));
-        lb = __shfl_sync(FULL_MASK, lb, leader);
-        if (is_light) {
-          const int q = lb + __popc(bl & ((1u << lane) - 1u));
-          light[q] = l;
-          light_w[q] = (u32)w;
-        }
-      }
-    }
-    const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
-    if (bal) {
-      int hb = 0;
+    const bool ok = base + lane < g.n && W[l] > 0 && (!mine || mine[l]);
+    const u64 w = ok ? W[l] : 0, r = ok ? R[l] : 0;
+    const int tier = !ok ? -1 : (r <= rec_light && w <= work_light) ? 0 : (r <= rec_mid && w <= work_mid) ? 1 : 2;
+    for (int t = 0; t < 3; t++) {
+      const u32 bal = __ballot_sync(FULL_MASK, tier == t);
+      if (!bal) continue;
+      int b0 = 0;
       const int leader = __ffs(bal) - 1;
-      if (lane == leader) hb = atomicAdd(n_heavy, __popc(bal));
-      hb = __shfl_sync(FULL_MASK, hb, leader);
-      if (is_heavy) {
-        const int q = hb + __popc(bal & ((1u << lane) - 1u));
-        heavy[q] = l;
-        heavy_w[q] = (u64)g.deg[l] * (u64)g.deg[l] + w;
-      }
+      if (lane == leader) b0 = atomicAdd(&counts[t], __popc(bal));
+      b0 = __shfl_sync(FULL_MASK, b0, leader);
+      if (tier != t) continue;
+      const int q = b0 + __popc(bal & ((1u << lane) - 1u));
+      if (t == 0) { light[q] = l; light_r[q] = (u32)r; }
+      else if (t == 1) { mid[q] = l; mid_r[q] = (u32)r; }
+      else { big[q] = l; big_w[q] = w; }
     }
   }
 }
@@ -548,11 +533,7 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
                                                     const int32_t* __restrict__ heavy, int n_heavy,
                                                     int* __restrict__ counter, C5RecT<V>* __restrict__ dense,
                                                     int32_t* __restrict__ dlists, u64* __restrict__ C5,
-                                                    int32_t* __restrict__ qmem, const int* __restrict__ nbig,
-                                                    int ngiant, int use_bits) {
-  // the list is sorted: the endpoints past C5_MID_MAX come first, *nbig of them (with the
-  // giant prefix); the rest belong to k_c5_mid
-  if (nbig) n_heavy = min(n_heavy, *nbig - ngiant);
+                                                    int32_t* __restrict__ qmem, int use_bits) {
   __shared__ ListEng E;
   if (threadIdx.x == 0) {
     E.qcap = g.max_deg;
@@ -619,7 +600,7 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
     idx = __shfl_sync(FULL_MASK, idx, 0);
     if (idx >= n_light) break;
     const int32_t l = light[idx];
-    const u32 cap = pow2_at_least(2u * lw[idx], 64u);  // <= C5_WARP_CAP
+    const u32 cap = pow2_at_least(2u * lw[idx], 64u);  // 2 x the record bound R(l): <= C5_WARP_CAP
     int32_t* J;
     if (cap <= (u32)sh_cap) {
       loc.R = shR;
@@ -640,94 +621,14 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
   }
 }
 
-// Giant endpoints (W(l) > C5_GIANT): one cluster each (persistent clusters, W-sorted list),
-// so a hub endpoint is spread over C5_CLUSTER SMs.  ctl per cluster: [nL, nJ, idx, -].
-__global__ void __cluster_dims__(C5_CLUSTER, 1, 1) __launch_bounds__(1024)
-    k_c5_cluster(DGraph g, const u32* __restrict__ Tlow, const u32* __restrict__ Tmid,
-                 const u32* __restrict__ Thigh, const int32_t* __restrict__ giant, int n_giant,
-                 int* __restrict__ counter, C5Rec* __restrict__ dense, int32_t* __restrict__ dlists,
-                 int* __restrict__ ctl, u64* __restrict__ tot, u64* __restrict__ C5) {
-  auto cluster = cooperative_groups::this_cluster();
-  const int cid = blockIdx.x / C5_CLUSTER;
-  const bool leader = cluster.block_rank() == 0 && threadIdx.x == 0;
-  ClusterEng eng;
-  C5Dense<C5Rec> loc;
-  loc.R = dense + (size_t)cid * g.n;
-  loc.L = dlists + (size_t)cid * 2 * g.n;
-  loc.nL = &ctl[4 * cid + 0];
-  int32_t* J = loc.L + g.n;
-  for (;;) {
-    if (leader) ctl[4 * cid + 2] = atomicAdd(counter, 1);
-    cluster.sync();
-    const int idx = *(volatile int*)&ctl[4 * cid + 2];
-    if (idx >= n_giant) break;
-    const int32_t l = giant[idx];
-    c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &ctl[4 * cid + 1], &tot[cid], C5);  // ends with a barrier
-    c5_reset(eng, loc);
-    cluster.sync();
-    if (leader) {
-      const u64 t = *(volatile u64*)&tot[cid];
-      if (t) atomicAdd(&C5[l], t);
-      tot[cid] = 0;
-      ctl[4 * cid + 0] = 0;
-      ctl[4 * cid + 1] = 0;
-    }
-  }
-}
-
-// Split of the heavy endpoints: W(l) counted by a warp per endpoint, stopping past
-// C5_MID_MAX (or taken from the exact count when `exact`).  Sort key: W for the mid
-// endpoints; C5_BIG_KEY | (exact W, or d(l)^2 + the partial count) for the others, so a
-// descending sort puts the big endpoints first; *nbig counts them.
-__global__ void k_c5_split(DGraph g, const int32_t* __restrict__ heavy, int n_heavy, u64* __restrict__ keys,
-                           int exact, int* __restrict__ nbig) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t q = gw; q < n_heavy; q += nw) {
-    const int32_t l = heavy[q];
-    u64 w;
-    if (exact) {
-      w = keys[q];
-    } else {
-      const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
-      w = (u64)g.deg[l];
-      for (int64_t s0 = r0; s0 < r1 && w <= C5_MID_MAX; s0 += 32) {
-        const int64_t s = s0 + lane;
-        u64 c = 0;
-        if (s < r1) {
-          const int32_t x = g.ci[s];
-          c = (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
-          if (s < rm) {
-            const int64_t ok = g.orow[x], ok1 = g.orow[x + 1];
-            c += (u64)(ok1 - ok);
-            for (int64_t e = ok; e < ok1; e++) {
-              const int32_t j = g.ocol[e];
-              c += (u64)(g.orow[j + 1] - g.orow[j]);
-            }
-          }
-        }
-        w += warp_sum(c);
-      }
-    }
-    const bool big = w > C5_MID_MAX;
-    if (lane == 0) {
-      const u64 d = (u64)g.deg[l];
-      keys[q] = !big ? w : C5_BIG_KEY | min(exact ? w : d * d + w, C5_BIG_KEY - 1);
-      if (big) atomicAdd(nbig, 1);
-    }
-  }
-}
-
-// Mid endpoints (C5_WARP_MAX < W(l) <= C5_MID_MAX): one C5_MBT-thread CTA each, records in
-// a per-CTA open-addressing region of 2 x W(l) slots in global memory (the region is reused
-// endpoint after endpoint, so it stays in L2).  A 1024-thread CTA per such endpoint would
-// spend its time in barriers and dependent round trips with most warps idle.
+// Mid endpoints: one C5_MBT-thread CTA each, records in a per-CTA open-addressing region of
+// 2 x R(l) slots in global memory (the region is reused endpoint after endpoint, so it stays
+// in L2).  A 1024-thread CTA per such endpoint would spend its time in barriers and
+// dependent round trips with most warps idle.
 __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restrict__ Tlow,
                                                    const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
-                                                   const int32_t* __restrict__ sorted, const u64* __restrict__ keys,
-                                                   const int* __restrict__ nbig, int n_total,
-                                                   int* __restrict__ counter, C5RecP* __restrict__ regions,
+                                                   const int32_t* __restrict__ list, const u32* __restrict__ rb,
+                                                   int n_mid, int* __restrict__ counter, C5RecP* __restrict__ regions,
                                                    int32_t* __restrict__ rlists, u64* __restrict__ C5,
                                                    int32_t* __restrict__ qmem) {
   __shared__ ListEng E;
@@ -744,47 +645,16 @@ __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restri
   loc.L = rlists + (size_t)blockIdx.x * 2 * C5_MID_CAP;
   loc.nL = &s_nL;
   int32_t* J = loc.L + C5_MID_CAP;
-  const int begin = *nbig;
   for (;;) {
-    if (threadIdx.x == 0) { s_idx = begin + atomicAdd(counter, 1); s_nL = 0; s_nJ = 0; s_tot = 0; }
+    if (threadIdx.x == 0) { s_idx = atomicAdd(counter, 1); s_nL = 0; s_nJ = 0; s_tot = 0; }
     __syncthreads();
     const int idx = s_idx;
-    if (idx >= n_total) break;
-    const int32_t l = sorted[idx];
-    loc.mask = pow2_at_least(2u * (u32)keys[idx], 64u) - 1;  // keys[idx] = W(l) <= C5_MID_MAX
+    if (idx >= n_mid) break;
+    const int32_t l = list[idx];
+    loc.mask = pow2_at_least(2u * rb[idx], 64u) - 1;  // rb[idx] = R(l) <= C5_MID_MAX
     c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &s_nJ, &s_tot, C5);
     if (threadIdx.x == 0 && s_tot) atomicAdd(&C5[l], s_tot);
     c5_reset(eng, loc);
     __syncthreads();
-  }
-}
-
-// exact W(l) of the heavy endpoints (one warp each) and the number above C5_GIANT
-__global__ void k_c5_heavy_w(DGraph g, const int32_t* __restrict__ heavy, int n_heavy, u64* __restrict__ wout,
-                             int* __restrict__ n_giant) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t q = gw; q < n_heavy; q += nw) {
-    const int32_t l = heavy[q];
-    const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
-    u64 w = 0;
-    for (int64_t s = r0 + lane; s < r1; s += 32) {
-      const int32_t x = g.ci[s];
-      w += (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
-      if (s < rm) {
-        const int64_t ok = g.orow[x], ok1 = g.orow[x + 1];
-        w += (u64)(ok1 - ok);
-        for (int64_t e = ok; e < ok1; e++) {
-          const int32_t j = g.ocol[e];
-          w += (u64)(g.orow[j + 1] - g.orow[j]);
-        }
-      }
-    }
-    w = warp_sum(w) + (u64)g.deg[l];
-    if (lane == 0) {
-      wout[q] = w;
-      if (w > C5_GIANT) atomicAdd(n_giant, 1);
-    }
   }
 }

@@ -81,6 +81,35 @@ static const char* kPassNames[] = {
 enum { P_H2D = 0, P_CANON, P_KCORE, P_CSR, P_TRI, P_TRILIST, P_CLIQ, P_NBR1, P_PAIR, P_HUB, P_C5,
        P_CLIQ2, P_NBR2, P_TRIG, P_COMB, P_D2H, P_COUNT };
 
+// ---- the library's own stream-ordered memory pool (one per device) -------------------
+// Scratch comes from a private pool whose release threshold keeps freed memory mapped
+// between calls (the default threshold of 0 would unmap and remap gigabytes of tables on
+// every call).  Private, so the process-wide default pool that other libraries use keeps
+// its own settings; evoke_release_scratch trims it back to nothing.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[256] = {};
+cudaMemPool_t evoke_pool(int dev) {
+  cudaMemPool_t* pools = g_pools;
+  if (dev < 0 || dev >= 256) { set_error("device ordinal out of range"); throw EvokeError{EVOKE_EINTERNAL}; }
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props;
+    std::memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CK(cudaMemPoolCreate(&pools[dev], &props));
+    uint64_t thr = ~0ull;
+    CK(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return pools[dev];
+}
+cudaMemPool_t evoke_pool_if_any(int dev) {  // the pool if one was created (never creates)
+  if (dev < 0 || dev >= 256) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  return g_pools[dev];
+}
+
 // ---- zero-invariant scratch, kept between calls --------------------------------------
 // The per-CTA tables of the pair, hub-local and 5-cycle passes start zeroed and every kernel
 // that uses them resets what it touched before it finishes (touched lists / sweeps), so at
@@ -115,7 +144,7 @@ struct ZeroLease {
       z.p = nullptr;
       z.bytes = 0;
       void* q = nullptr;
-      if (cudaMallocAsync(&q, z.target, st) != cudaSuccess) {
+      if (cudaMallocFromPoolAsync(&q, z.target, evoke_pool(dev), st) != cudaSuccess) {
         (void)cudaGetLastError();
         z.target = 0;
         return;
@@ -154,32 +183,28 @@ struct ZeroLease {
 // Device allocations of one call; everything is freed (stream-ordered) at the end.
 struct Arena {
   cudaStream_t st;
+  cudaMemPool_t pool;
   std::vector<void*> ptrs;
-  explicit Arena(cudaStream_t s) : st(s) {}
+  Arena(cudaStream_t s, int dev) : st(s), pool(evoke_pool(dev)) {}
   template <typename T>
   T* alloc(size_t count, bool zero = false) {
+    T* p = try_alloc<T>(count, zero);
+    if (!p) throw EvokeError{EVOKE_ENOMEM};
+    return p;
+  }
+  // nullptr (and the error recorded) when the pool cannot grow by `count` elements
+  template <typename T>
+  T* try_alloc(size_t count, bool zero = false) {
     void* p = nullptr;
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, st);
     if (e != cudaSuccess) {
-      set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
-      throw EvokeError{EVOKE_ENOMEM};
+      (void)cudaGetLastError();
+      set_error("cudaMallocFromPoolAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+      return nullptr;
     }
     ptrs.push_back(p);
     if (zero) CK(cudaMemsetAsync(p, 0, bytes, st));
-    return (T*)p;
-  }
-  template <typename T>
-  T* alloc_on(cudaStream_t s, size_t count, bool zero = false) {
-    void* p = nullptr;
-    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
-    if (e != cudaSuccess) {
-      set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
-      throw EvokeError{EVOKE_ENOMEM};
-    }
-    ptrs.push_back(p);
-    if (zero) CK(cudaMemsetAsync(p, 0, bytes, s));
     return (T*)p;
   }
   ZeroLease* lease = nullptr;
@@ -307,8 +332,7 @@ size_t avail_bytes(int dev) {
   static std::mutex mu;
   static size_t base[256] = {};
   static bool have[256] = {};
-  cudaMemPool_t pool;
-  CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  cudaMemPool_t pool = evoke_pool(dev);
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev < 0 || dev >= 256) { set_error("device ordinal out of range"); throw EvokeError{EVOKE_EINTERNAL}; }
@@ -354,12 +378,89 @@ void inclusive_sum(Arena& A, Ctx& C, const Tin* in, Tout* out, int64_t N) {
   C.lib_launches += 2;
 }
 
+// Work-balanced shard membership (north star: units "partitioned by balanced work
+// estimate"; the paper's parallel orbit groups): the N items sorted by estimate,
+// descending (CUB's radix sort is stable, so ties keep index order and every rank computes
+// the same list), and position p belongs to shard p mod ns.  Returns nullptr (every item is
+// this shard's) when ns == 1; sums[0..1] (device) receive this shard's and all estimates.
+__global__ void k_iota_i32(int32_t* __restrict__ a, int64_t n);
+__global__ void k_shard_mask(const u64* __restrict__ skeys, const int32_t* __restrict__ sidx, int64_t n, int si,
+                             int ns, uint8_t* __restrict__ mine, u64* __restrict__ sums);
+uint8_t* shard_mask(Arena& A, Ctx& C, const u64* est, int64_t N, int si, int ns, u64* sums);
+
 int bits_for(int64_t x) {
   int b = 1;
   while ((1ll << b) <= x) b++;
   return b;
 }
 
+// Test / developer override of a tier limit: the compiled default, or a LOWER value from the
+// environment (a lower limit only moves work items onto a heavier tier's code path, whose
+// tables are sized for anything; a higher one could overflow a lighter tier's tables).
+u64 env_cap(const char* name, u64 dflt) {
+  const char* e = getenv(name);
+  if (!e || !*e) return dflt;
+  const long long v = atoll(e);
+  return v < 0 ? 0 : std::min<u64>((u64)v, dflt);
+}
+
+__global__ void k_iota_i32(int32_t* __restrict__ a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (int32_t)i;
+}
+// position p of the estimate-sorted (descending) item list belongs to shard p mod ns;
+// sums[0] += the estimates of this shard's items, sums[1] += all estimates
+__global__ void k_shard_mask(const u64* __restrict__ skeys, const int32_t* __restrict__ sidx, int64_t n, int si,
+                             int ns, uint8_t* __restrict__ mine, u64* __restrict__ sums) {
+  u64 own = 0, all = 0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const bool m = (p % ns) == si;
+    mine[sidx[p]] = m ? 1 : 0;
+    all += skeys[p];
+    if (m) own += skeys[p];
+  }
+  own = warp_sum(own);
+  all = warp_sum(all);
+  if ((threadIdx.x & 31) == 0) {
+    if (own) atomicAdd(&sums[0], own);
+    if (all) atomicAdd(&sums[1], all);
+  }
+}
+// the pair pass's own sorted list (keys = ~est, u32): this shard's and all estimates
+__global__ void k_shard_sum_u32(const u32* __restrict__ skeys, int64_t n, int si, int ns, u64* __restrict__ sums) {
+  u64 own = 0, all = 0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const u64 e = (u64)(u32)~skeys[p];
+    all += e;
+    if ((p % ns) == si) own += e;
+  }
+  own = warp_sum(own);
+  all = warp_sum(all);
+  if ((threadIdx.x & 31) == 0) {
+    if (own) atomicAdd(&sums[0], own);
+    if (all) atomicAdd(&sums[1], all);
+  }
+}
+// (k = d+(u))^3: the 4/5-clique unit's work estimate
+__global__ void k_clique_est(const int64_t* __restrict__ orow, int32_t n, u64* __restrict__ est) {
+  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    const u64 k = (u64)(orow[u + 1] - orow[u]);
+    est[u] = k >= 3 ? k * k * k : 0;
+  }
+}
+
+__global__ void k_gather_u64(const u64* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                             u64* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
+__global__ void k_permute_c5(const int32_t* __restrict__ perm, int64_t n, const int32_t* __restrict__ l,
+                             const u32* __restrict__ r, int32_t* __restrict__ lo, u32* __restrict__ ro) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    lo[i] = l[perm[i]];
+    ro[i] = r[perm[i]];
+  }
+}
 __global__ void k_u32_to_i64(const u32* __restrict__ a, int64_t n, int64_t* __restrict__ b) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -421,6 +522,25 @@ __global__ void k_clique_bins(const int64_t* __restrict__ orow, int32_t n, int32
   }
 }
 
+uint8_t* shard_mask(Arena& A, Ctx& C, const u64* est, int64_t N, int si, int ns, u64* sums) {
+  if (ns <= 1 || N <= 0) return nullptr;
+  const int B = 256;
+  int32_t* idx = A.alloc<int32_t>(N);
+  int32_t* sidx = A.alloc<int32_t>(N);
+  u64* skeys = A.alloc<u64>(N);
+  uint8_t* mine = A.alloc<uint8_t>(N);
+  k_iota_i32<<<grid_for(N, B, C.num_sms), B, 0, C.st>>>(idx, N);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, est, skeys, idx, sidx, N, 0, 64, C.st));
+  void* t = A.alloc<char>(tb);
+  CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, est, skeys, idx, sidx, N, 0, 64, C.st));
+  k_shard_mask<<<grid_for(N, B, C.num_sms), B, 0, C.st>>>(skeys, sidx, N, si, ns, mine, sums);
+  C.launches += 2;
+  C.lib_launches += 4;
+  A.release(idx); A.release(sidx); A.release(skeys); A.release(t);
+  return mine;
+}
+
 struct Input {
   int kind;  // 0 edges, 1 csr
   int64_t n, m;
@@ -436,21 +556,20 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   Ctx C;
   C.dev = dev;
   CK(cudaDeviceGetAttribute(&C.num_sms, cudaDevAttrMultiProcessorCount, dev));
-  {
-    // keep freed scratch in the device's stream-ordered pool between calls (the default
-    // release threshold of 0 would unmap and remap gigabytes of tables on every call)
-    static bool pool_set[256] = {false};
-    if (dev < 256 && !pool_set[dev]) {
-      cudaMemPool_t pool;
-      CK(cudaDeviceGetDefaultMemPool(&pool, dev));
-      uint64_t thr = ~0ull;
-      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-      pool_set[dev] = true;
-    }
+  if (o.stream) {
+    C.st = (cudaStream_t)o.stream;
+  } else {
+    // no caller stream (torch's default stream also arrives as NULL): the device's kept
+    // non-blocking stream, ordered after all work already queued on the legacy default
+    // stream (device-pointer inputs may still be in production there, and the caching
+    // allocator may have handed `out` over from work still queued on it)
+    C.st = C.stream(Ctx::MAXJOBS - 3, 0);
+    cudaEvent_t e0;
+    CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    CK(cudaEventRecord(e0, cudaStreamLegacy));
+    CK(cudaStreamWaitEvent(C.st, e0, 0));
+    CK(cudaEventDestroy(e0));
   }
-  cudaStream_t own = nullptr;
-  if (o.stream) C.st = (cudaStream_t)o.stream;
-  else C.st = C.stream(Ctx::MAXJOBS - 3, 0);  // the device's kept non-blocking stream (the call ends with a sync)
   C.timing = true;
   for (int i = 0; i <= P_COUNT; i++) CK(cudaEventCreate(&C.ev[i]));
   CK(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
@@ -462,7 +581,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   for (int i = 0; i < Ctx::MAXJOBS; i++)
     for (int j = 0; j < 2; j++) CK(cudaEventCreate(&C.pev[i][j]));
   struct Cleanup {
-    Ctx& C; cudaStream_t own;
+    Ctx& C;
     ~Cleanup() {
       for (int i = 0; i <= P_COUNT; i++) cudaEventDestroy(C.ev[i]);
       cudaEventDestroy(C.ev_fork);
@@ -474,9 +593,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       for (int i = 0; i < Ctx::MAXJOBS; i++)
         for (int j = 0; j < 2; j++) cudaEventDestroy(C.pev[i][j]);
       if (C.side_st) { cudaStreamSynchronize(C.side_st); cudaStreamDestroy(C.side_st); }
-      if (own) { cudaStreamSynchronize(own); cudaStreamDestroy(own); }
     }
-  } cleanup{C, own};
+  } cleanup{C};
 
   const auto& TF = evoke_host::transform();
   {
@@ -492,7 +610,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
                                cudaMemcpyHostToDevice, C.st));
   }
 
-  Arena A(C.st);
+  Arena A(C.st, dev);
   ZeroLease lease;  // destroyed before A (its buffer is not A's)
   lease.acquire(dev, C.st);
   A.lease = &lease;
@@ -813,8 +931,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     g.tes = tes; g.tlows = tlows; g.tmids = tmids;
   }
   const int si = o.shard_index, ns = o.num_shards;
+  // per sharded pass (pair, hub-local, 5-cycle, cliques): this shard's and all work estimates
+  u64* d_work = A.alloc<u64>(8, true);
   // ------------------------------------------------------------------ a5/a9: cliques
   C.mark(P_CLIQ);
+  const uint8_t* cmine = nullptr;
+  if (ns > 1 && n > 0) {
+    u64* cest = A.alloc<u64>(n);
+    k_clique_est<<<grid_for(n, B, SM), B, 0, C.st>>>(orow, n, cest);
+    C.launches++;
+    cmine = shard_mask(A, C, cest, n, si, ns, d_work + 6);
+  }
   int32_t* cbins = A.alloc<int32_t>((size_t)5 * std::max(n, 1));
   int* ccounts = A.alloc<int>(5, true);
   int hcounts[5] = {0, 0, 0, 0, 0};
@@ -847,13 +974,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         if (smem > 48 * 1024)
           CK(cudaFuncSetAttribute(k_cliques<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_cliques<0><<<grid, block, smem, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
-                                                 cscratch_words, 1, si, ns, Te, K4t, Fp(F_K4), K4e, Fp(F_K5),
+                                                 cscratch_words, 1, cmine, Te, K4t, Fp(F_K4), K4e, Fp(F_K5),
                                                  nullptr, nullptr);
       } else {
         if (smem > 48 * 1024)
           CK(cudaFuncSetAttribute(k_cliques<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_cliques<1><<<grid, block, smem, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
-                                                 cscratch_words, 0, si, ns, Te, K4t, nullptr, nullptr, nullptr,
+                                                 cscratch_words, 0, cmine, Te, K4t, nullptr, nullptr, nullptr,
                                                  Fp(F_R66), Fp(F_R70));
       }
       C.launches++;
@@ -917,8 +1044,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     void* t = A.alloc<char>(tb);
     CK(cub::DeviceRadixSort::SortPairs(t, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 32, C.st));
     C.tick("pair_sort");
-    k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, Fp(F_T), pest, plists, tiers);
-    C.launches += 2;
+    PairTiers ptiers;
+    ptiers.packed_lim = env_cap("EVOKE_PAIR_PACKED_LIM", 65536);
+    ptiers.light_max = env_cap("EVOKE_PAIR_LIGHT_MAX", PAIR_WARP_MAX);
+    ptiers.mids_max = env_cap("EVOKE_PAIR_MIDS_MAX", PAIR_MIDS_MAX);
+    ptiers.mid_max = env_cap("EVOKE_PAIR_MID_MAX", PAIR_MID_MAX);
+    ptiers.sweep = getenv("EVOKE_PAIR_SWEEP") ? atoi(getenv("EVOKE_PAIR_SWEEP")) : -1;
+    k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, ptiers, Fp(F_T), pest, plists, tiers);
+    k_shard_sum_u32<<<grid_for(n, B, SM), B, 0, C.st>>>(pk2, n, si, ns, d_work + 0);
+    C.launches += 3;
     C.lib_launches += 4;
     int ht[PT_COUNT];
     CK(cudaMemcpyAsync(ht, tiers, sizeof(ht), cudaMemcpyDeviceToHost, C.st));
@@ -954,12 +1088,19 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     // and half the SMs leave room for the other passes (config 2: 0.1-0.3 ms better step);
     // past L2 the tables are DRAM-bound and the heavy sources dominate: every SM (config 5:
     // 173 s instead of 199 s).
+    // The three heavy tiers share one memory budget (half the free estimate); each CTA
+    // needs its dense table (word bytes per vertex), its touched list (4 per vertex) and its
+    // engine queue, and each tier's share is taken off the budget before the next is sized.
+    int64_t heavy_budget = (int64_t)(freeb / 2);
+    const int heavy_qcap = 2 * g.max_deg + 65536;
     auto heavy_grid = [&](int nsrc, size_t word, int cap) {
       const int64_t l2_ctas = std::max<int64_t>(1, (56ll << 20) / ((int64_t)n * (int64_t)word));
       int64_t pg = std::min<int64_t>(l2_ctas >= SM / 2 ? SM / 2 : SM, cap);
       if (phg_env) pg = std::max(1, atoi(phg_env));  // developer knob: the grid itself
       pg = std::min<int64_t>(pg, nsrc);
-      pg = std::max<int64_t>(1, std::min<int64_t>(pg, (int64_t)(freeb / 4) / ((int64_t)n * (int64_t)(word + 4))));
+      const int64_t per_cta = (int64_t)n * (int64_t)(word + 4) + (int64_t)eng_queue_bytes(heavy_qcap);
+      pg = std::max<int64_t>(1, std::min<int64_t>(pg, heavy_budget / per_cta));
+      heavy_budget -= pg * per_cta;
       return (int)pg;
     };
     if (ht[PT_G64] > 0) {
@@ -970,7 +1111,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(PT_G64);
       const int cnt = ht[PT_G64];
-      const int qcap = 2 * g.max_deg + 65536;
+      const int qcap = heavy_qcap;
       char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
       jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
         k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap);
@@ -985,7 +1126,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(tier);
       const int cnt = ht[tier];
-      const int qcap = 2 * g.max_deg + 65536;
+      const int qcap = heavy_qcap;
       char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
       jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
         if (tier == PT_G32S)
@@ -1050,8 +1191,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     u64* hitem_est = A.alloc<u64>(m2s, true);
     if (ntri > 0)
       k_hub_est<<<grid_for(ntri, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est);
-    k_hub_bin<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est, si, ns, light, hcnt, heavy, hest,
-                                                        hcnt + 1);
+    const uint8_t* hmine = shard_mask(A, C, hitem_est, m2s, si, ns, d_work + 2);
+    k_hub_bin<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est, hmine, env_cap("EVOKE_HUB_WARP_MAX", HUB_WARP_MAX),
+                                                        light, hcnt, heavy, hest, hcnt + 1);
     C.launches += 2;
     int hc[2];
     CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));
@@ -1082,7 +1224,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const int hg = hhg_env ? std::max(1, atoi(hhg_env)) : std::min(std::max(1, hb_per_sm), hub_ctas_per_sm) * SM;
       u32* gt = nullptr;
       int32_t* gl = nullptr;
-      if (g.max_deg > HUB_SH_DENSE && n_heavy > 0) {
+      const int sh_dense_max = (int)env_cap("EVOKE_HUB_SH_DENSE", HUB_SH_DENSE);
+      if (g.max_deg > sh_dense_max && n_heavy > 0) {
         gt = A.zalloc<u32>((size_t)hg * g.max_deg);
         gl = A.alloc<int32_t>((size_t)hg * g.max_deg);
       }
@@ -1090,7 +1233,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       u64* r69 = Fp(F_R69);
       jobs.push_back({P_HUB, 2, [=, &C](cudaStream_t st) {
         k_hub_process<<<hg, HUB_BT, HUB_SMEM, st>>>(g, Te, heavy_sorted, n_heavy, light, n_light, hcnt + 2, gt, gl,
-                                                    r68, r69);
+                                                    r68, r69, sh_dense_max);
         C.launches++;
       }});
     }
@@ -1100,140 +1243,141 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   C.mark(P_C5);
   C.tick("hub_rest");
   if (n > 0 && m > 0 && !four) {
+    // exact work W(l) and record bound R(l) of every endpoint (O(m)), this shard's endpoints
+    // by position in the W-sorted list, tiers
+    u32* splus = A.alloc<u32>(n);
+    u64* c5W = A.alloc<u64>(n);
+    u64* c5R = A.alloc<u64>(n);
+    k_c5_splus<<<grid_for(n, B, SM), B, 0, C.st>>>(g, splus);
+    k_c5_work<<<warp_grid, B, 0, C.st>>>(g, splus, c5W, c5R);
+    C.launches += 2;
+    const uint8_t* c5mine = shard_mask(A, C, c5W, n, si, ns, d_work + 4);
     int32_t* c5l = A.alloc<int32_t>(n);
-    int32_t* c5h = A.alloc<int32_t>(n);
-    u64* c5w = A.alloc<u64>(n);
-    int* c5c = A.alloc<int>(8, true);
+    u32* c5lr = A.alloc<u32>(n);
+    int32_t* c5m = A.alloc<int32_t>(n);
+    u32* c5mr = A.alloc<u32>(n);
+    int32_t* c5b = A.alloc<int32_t>(n);
+    u64* c5bw = A.alloc<u64>(n);
+    int* c5c = A.alloc<int>(8, true);  // tier sizes [0..2], persistent-kernel counters [3..5]
     u64* C5out = Fp(F_C5);
-    u32* c5lw = A.alloc<u32>(n);
-    k_c5_items<<<warp_grid, B, 0, C.st>>>(g, si, ns, c5l, c5lw, c5c, c5h, c5w, c5c + 1);
+    // tier limits (lower only: env for tests); mid work < 2^16 keeps the packed records exact
+    const u64 rec_light = env_cap("EVOKE_C5_LIGHT_REC", C5_WARP_MAX), work_light = env_cap("EVOKE_C5_LIGHT_WORK", C5_WARP_WORK);
+    const u64 rec_mid = env_cap("EVOKE_C5_MID_REC", C5_MID_MAX), work_mid = env_cap("EVOKE_C5_MID_WORK", C5_MID_WORK);
+    k_c5_bin<<<grid_for(n, B, SM), B, 0, C.st>>>(g, c5W, c5R, c5mine, rec_light, work_light, rec_mid, work_mid, c5l,
+                                                 c5lr, c5m, c5mr, c5b, c5bw, c5c);
     C.launches++;
-    int hc5[2];
+    int hc5[3];
     CK(cudaMemcpyAsync(hc5, c5c, sizeof(hc5), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     C.tick("c5_items+sync");
-    const int n5l = hc5[0], n5h = hc5[1];
-    if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d heavy %d\n", n5l, n5h);
-    if (n5h > 0) {
-      // exact work of the heavy endpoints, sorted descending; the giant prefix goes to the
-      // whole grid (cooperative), the rest one CTA each on a side stream
-      // A global bound on every endpoint's work, W(l) <= d(l) (d_max + k (k + 1)) with k the
-      // maximum out-degree, decides the record width without the exact per-endpoint count;
-      // the exact count (and the giant-endpoint split) is needed only beyond 2^32 / with the
-      // cluster path enabled.
-      const u64 wbound = (u64)max_deg * ((u64)max_deg + (u64)max_out * ((u64)max_out + 1));
-      const bool c5_hist = getenv("EVOKE_C5_HIST") != nullptr;  // developer: W histogram of heavy endpoints
-      const bool exact_w = wbound >= (1ull << 32) || C5_GIANT < (1ull << 40) || c5_hist;
-      if (exact_w) {
-        k_c5_heavy_w<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, c5c + 2);
-        C.launches++;
-      }
-      if (c5_hist) {
-        std::vector<u64> hw(n5h);
-        std::vector<int32_t> hl(n5h);
-        CK(cudaMemcpyAsync(hw.data(), c5w, sizeof(u64) * n5h, cudaMemcpyDeviceToHost, C.st));
-        CK(cudaMemcpyAsync(hl.data(), c5h, sizeof(int32_t) * n5h, cudaMemcpyDeviceToHost, C.st));
-        CK(cudaStreamSynchronize(C.st));
-        const u64 edges_[] = {2048, 4096, 8192, 16384, 65536, 1ull << 20, ~0ull};
-        u64 cnt[7] = {}, sumw[7] = {};
-        for (int q = 0; q < n5h; q++)
-          for (int b = 0; b < 7; b++)
-            if (hw[q] <= edges_[b]) { cnt[b]++; sumw[b] += hw[q]; break; }
-        for (int b = 0; b < 7; b++)
-          fprintf(stderr, "[evoke] c5 heavy W <= %llu: %llu endpoints, work %llu\n", (unsigned long long)edges_[b],
-                  (unsigned long long)cnt[b], (unsigned long long)sumw[b]);
-      }
-      // mid endpoints (W <= C5_MID_MAX) to k_c5_mid, the rest (sorted first) to k_c5_heavy
-      int* nbig_dev = c5c + 5;
-      k_c5_split<<<grid_for((int64_t)n5h * 32, B, SM), B, 0, C.st>>>(g, c5h, n5h, c5w, exact_w ? 1 : 0, nbig_dev);
-      C.launches++;
-      int32_t* hs = c5h;
-      u64* hkeys = nullptr;
-      if (n5h > 1) {
-        hs = A.alloc<int32_t>(n5h);
-        u64* hk = A.alloc<u64>(n5h);
-        hkeys = hk;
+    const int n5l = hc5[0], n5m = hc5[1], n5b = hc5[2];
+    if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d mid %d big %d\n", n5l, n5m, n5b);
+    if (getenv("EVOKE_C5_HIST")) {  // developer: W / R histogram of every endpoint
+      std::vector<u64> hw(n), hr(n);
+      CK(cudaMemcpyAsync(hw.data(), c5W, sizeof(u64) * n, cudaMemcpyDeviceToHost, C.st));
+      CK(cudaMemcpyAsync(hr.data(), c5R, sizeof(u64) * n, cudaMemcpyDeviceToHost, C.st));
+      CK(cudaStreamSynchronize(C.st));
+      const u64 edges_[] = {256, 1024, 4096, 16384, 65536, 1ull << 20, ~0ull};
+      u64 cw[7] = {}, sw[7] = {}, cr[7] = {};
+      for (int32_t q = 0; q < n; q++)
+        for (int b2 = 0; b2 < 7; b2++) {
+          if (hw[q] <= edges_[b2]) { cw[b2]++; sw[b2] += hw[q]; break; }
+        }
+      for (int32_t q = 0; q < n; q++)
+        for (int b2 = 0; b2 < 7; b2++)
+          if (hr[q] <= edges_[b2]) { cr[b2]++; break; }
+      for (int b2 = 0; b2 < 7; b2++)
+        fprintf(stderr, "[evoke] c5 W <= %llu: %llu endpoints (work %llu); R <= it: %llu endpoints\n",
+                (unsigned long long)edges_[b2], (unsigned long long)cw[b2], (unsigned long long)sw[b2],
+                (unsigned long long)cr[b2]);
+    }
+    const size_t freeb = avail_bytes(C.dev);
+    if (n5b > 0) {
+      // big endpoints, W descending
+      int32_t* bs = c5b;
+      u64 wmax = 0;
+      if (n5b > 1) {
+        bs = A.alloc<int32_t>(n5b);
+        u64* bk = A.alloc<u64>(n5b);
         size_t tb = 0;
-        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c5w, hk, c5h, hs, n5h, 0, 64, C.st));
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c5bw, bk, c5b, bs, n5b, 0, 64, C.st));
         void* t = A.alloc<char>(tb);
-        CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, c5w, hk, c5h, hs, n5h, 0, 64, C.st));
+        CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, c5bw, bk, c5b, bs, n5b, 0, 64, C.st));
+        C.lib_launches += 4;
+        wmax = d2h_scalar<u64>(bk, C.st);
+      } else {
+        wmax = d2h_scalar<u64>(c5bw, C.st);
+      }
+      // u32 record fields when every big endpoint's W < 2^32 (every field is <= W(l))
+      const bool narrow = wmax < (1ull << 32) && !getenv("EVOKE_C5_WIDE");
+      const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
+      const int64_t per = (int64_t)n * (int64_t)(rec + 8);
+      const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: big-endpoint CTAs
+      const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
+      const int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, n5b), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
+      char* dense = A.zalloc<char>((size_t)hg * n * rec);
+      int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
+      int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
+      // first-touch bitmaps (present, j-key) in shared memory when they fit
+      const size_t bits_smem = (size_t)2 * ((n + 31) / 32) * sizeof(u32);
+      const int use_bits = bits_smem <= C5_BITS_SMEM_MAX && !getenv("EVOKE_C5_NO_BITS") ? 1 : 0;
+      const size_t bsm = use_bits ? bits_smem : 0;
+      if (use_bits) {
+        CK(cudaFuncSetAttribute(k_c5_heavy<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+        CK(cudaFuncSetAttribute(k_c5_heavy<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      }
+      jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
+        if (narrow)
+          k_c5_heavy<u32><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 3,
+                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq, use_bits);
+        else
+          k_c5_heavy<u64><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 3,
+                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, use_bits);
+        C.launches++;
+      }});
+    }
+    if (n5m > 0) {
+      // mid endpoints, W descending: several 4-warp CTAs per SM, hashed records in per-CTA
+      // regions; they run after the big endpoints on the same stream (as one more concurrent
+      // grid they would take SMs from the other passes' persistent kernels)
+      int32_t* ms = c5m;
+      u32* mr = c5mr;
+      if (n5m > 1) {
+        u64* mw = A.alloc<u64>(n5m);
+        k_gather_u64<<<grid_for(n5m, B, SM), B, 0, C.st>>>(c5W, c5m, n5m, mw);
+        int32_t* idx = A.alloc<int32_t>(n5m);
+        int32_t* sidx = A.alloc<int32_t>(n5m);
+        u64* sk = A.alloc<u64>(n5m);
+        k_iota_i32<<<grid_for(n5m, B, SM), B, 0, C.st>>>(idx, n5m);
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, mw, sk, idx, sidx, n5m, 0, 64, C.st));
+        void* t = A.alloc<char>(tb);
+        CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, mw, sk, idx, sidx, n5m, 0, 64, C.st));
+        ms = A.alloc<int32_t>(n5m);
+        mr = A.alloc<u32>(n5m);
+        k_permute_c5<<<grid_for(n5m, B, SM), B, 0, C.st>>>(sidx, n5m, c5m, c5mr, ms, mr);
+        C.launches += 3;
         C.lib_launches += 4;
       }
-      int ngiant = 0;
-      if (exact_w) {
-        CK(cudaMemcpyAsync(&ngiant, c5c + 2, sizeof(int), cudaMemcpyDeviceToHost, C.st));
-        CK(cudaStreamSynchronize(C.st));
-      }
-      const size_t freeb = avail_bytes(C.dev);
-      if (ngiant > 0) {
-        const int nclus = std::min(ngiant, std::max(1, SM / C5_CLUSTER));
-        C5Rec* dense = A.alloc<C5Rec>((size_t)nclus * n, true);
-        int32_t* dl = A.alloc<int32_t>((size_t)nclus * 2 * n);
-        int* ctl = A.alloc<int>((size_t)4 * nclus + 4, true);
-        u64* tot = A.alloc<u64>(nclus, true);
-        int* gcounter = ctl + 4 * nclus;
-        const int32_t* hsg = hs;
-        const int ng = ngiant;
-        jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
-          k_c5_cluster<<<nclus * C5_CLUSTER, 1024, 0, st>>>(g, Tlow, Tmid, Thigh, hsg, ng, gcounter, dense, dl, ctl,
-                                                             tot, C5out);
-          C.launches++;
-        }});
-      }
-      const int nrest = n5h - ngiant;
-      if (nrest > 0) {
-        // u32 records when every remaining endpoint's work bound is < 2^32 (the list is sorted)
-        u64 wmax = wbound;
-        if (exact_w) {
-          CK(cudaMemcpyAsync(&wmax, (n5h > 1 ? hkeys : c5w) + ngiant, sizeof(u64), cudaMemcpyDeviceToHost, C.st));
-          CK(cudaStreamSynchronize(C.st));
-          wmax &= ~C5_BIG_KEY;
-        }
-        const bool narrow = wmax < (1ull << 32);
-        const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
-        const int64_t per = (int64_t)n * (int64_t)(rec + 8);
-        const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: heavy-endpoint CTAs
-        const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
-        int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, nrest), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
-        char* dense = A.zalloc<char>((size_t)hg * n * rec);
-        int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
-        int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
-        const int32_t* hsr = hs + ngiant;
-        const int ngi = ngiant;
-        // mid endpoints: several 4-warp CTAs per SM, hashed records in per-CTA regions; they run
-        // after the big endpoints on the same stream (as one more concurrent grid they would take
-        // SMs from the other passes' persistent kernels)
-        int bpm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_c5_mid, C5_MBT, 0));
-        const char* mb_env = getenv("EVOKE_C5_MBPS");  // developer knob: mid CTAs per SM
-        const int gm = std::max(1, std::min(bpm, mb_env ? atoi(mb_env) : 4)) * SM;
-        C5RecP* mreg = A.zalloc<C5RecP>((size_t)gm * C5_MID_CAP);
-        int32_t* mlists = A.alloc<int32_t>((size_t)gm * 2 * C5_MID_CAP);
-        int32_t* mq = A.alloc<int32_t>((size_t)gm * (2 * (size_t)g.max_deg + 1));
-        const u64* mkeys = n5h > 1 ? hkeys : c5w;
-        const int32_t* hsm = hs;
-        const int n5h_ = n5h;
-        // first-touch bitmaps (present, j-key) in shared memory when they fit
-        const size_t bits_smem = (size_t)2 * ((n + 31) / 32) * sizeof(u32);
-        const int use_bits = bits_smem <= C5_BITS_SMEM_MAX && !getenv("EVOKE_C5_NO_BITS") ? 1 : 0;
-        const size_t bsm = use_bits ? bits_smem : 0;
-        if (use_bits) {
-          CK(cudaFuncSetAttribute(k_c5_heavy<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-          CK(cudaFuncSetAttribute(k_c5_heavy<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-        }
-        jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
-          if (narrow)
-            k_c5_heavy<u32><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                     reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq,
-                                                     nbig_dev, ngi, use_bits);
-          else
-            k_c5_heavy<u64><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, hsr, nrest, c5c + 3,
-                                                     reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, nbig_dev,
-                                                     ngi, use_bits);
-          k_c5_mid<<<gm, C5_MBT, 0, st>>>(g, Tlow, Tmid, Thigh, hsm, mkeys, nbig_dev, n5h_, c5c + 6, mreg, mlists,
-                                          C5out, mq);
-          C.launches += 2;
-        }});
+      int bpm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_c5_mid, C5_MBT, 0));
+      const char* mb_env = getenv("EVOKE_C5_MBPS");  // developer knob: mid CTAs per SM
+      const int gm = (int)std::min<int64_t>(std::max(1, std::min(bpm, mb_env ? atoi(mb_env) : 4)) * SM, n5m);
+      C5RecP* mreg = A.zalloc<C5RecP>((size_t)gm * C5_MID_CAP);
+      int32_t* mlists = A.alloc<int32_t>((size_t)gm * 2 * C5_MID_CAP);
+      int32_t* mq = A.alloc<int32_t>((size_t)gm * (2 * (size_t)g.max_deg + 1));
+      const int32_t* ms_ = ms;
+      const u32* mr_ = mr;
+      const int job = n5b > 0 ? (int)jobs.size() - 1 : -1;
+      auto mid_fn = [=, &C](cudaStream_t st) {
+        k_c5_mid<<<gm, C5_MBT, 0, st>>>(g, Tlow, Tmid, Thigh, ms_, mr_, n5m, c5c + 4, mreg, mlists, C5out, mq);
+        C.launches++;
+      };
+      if (job >= 0) {
+        auto big_fn = jobs[job].fn;
+        jobs[job].fn = [=](cudaStream_t st) { big_fn(st); mid_fn(st); };
+      } else {
+        jobs.push_back({P_C5, 0, mid_fn});
       }
     }
     if (n5l > 0) {
@@ -1249,7 +1393,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       C5RecP* reg = A.zalloc<C5RecP>(nw * C5_WARP_CAP);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
-        k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lw, n5l, c5c + 4, reg, wl, C5out,
+        k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lr, n5l, c5c + 5, reg, wl, C5out,
                                                 sh_cap);
         C.launches++;
       }});
@@ -1337,15 +1481,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   C.mark(P_COMB);
   u64* dout = nullptr;
   if (n > 0) {
-    dout = o.device_pointers ? (u64*)out : A.alloc<u64>((size_t)n * 73);
+    dout = A.alloc<u64>((size_t)n * 73);  // staged: `out` is written only after every check passed
     k_combine<<<grid_for(n, 128, SM), 128, 0, C.st>>>(g, F, perm, o.induced, si == 0 ? 1 : 0, four ? 15 : 73,
                                                        dout);
     C.launches++;
   }
-  C.mark(P_D2H);
-  if (n > 0 && !o.device_pointers)
-    CK(cudaMemcpyAsync(out, dout, sizeof(u64) * (size_t)n * 73, cudaMemcpyDeviceToHost, C.st));
-  C.mark(P_COUNT);
+  // every check before `out` is touched: kernel faults (sync), and in the developer mode
+  // the zero invariant of the kept scratch
   CK(cudaStreamSynchronize(C.st));
   CK(cudaGetLastError());
   lease.ok = true;  // every pass has reset its tables
@@ -1358,6 +1500,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       throw EvokeError{EVOKE_EINTERNAL};
     }
   }
+  C.mark(P_D2H);
+  if (n > 0)
+    CK(cudaMemcpyAsync(out, dout, sizeof(u64) * (size_t)n * 73,
+                       o.device_pointers ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, C.st));
+  C.mark(P_COUNT);
+  CK(cudaStreamSynchronize(C.st));
   C.print_ticks();
   if (getenv("EVOKE_DEBUG")) {  // main-stream preparation time of the concurrent passes
     float a = 0, b = 0, c = 0, d = 0;
@@ -1436,6 +1584,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     float tot = 0;
     CK(cudaEventElapsedTime(&tot, C.ev[0], C.ev[P_COUNT]));
     s->ms_total = tot;
+    {
+      u64 hw[8];
+      CK(cudaMemcpyAsync(hw, d_work, sizeof(hw), cudaMemcpyDeviceToHost, C.st));
+      CK(cudaStreamSynchronize(C.st));
+      for (int q = 0; q < 4; q++) { s->work_shard[q] = hw[2 * q]; s->work_total[q] = hw[2 * q + 1]; }
+    }
     s->kernel_launches = C.launches;
     s->library_launches = C.lib_launches;
     u64* dw = A.alloc<u64>(1, true);
@@ -1559,7 +1713,7 @@ int evoke_ccd(int64_t n, const uint64_t* dim, int orbit, uint64_t* values, uint6
     cudaStream_t own = nullptr;
     if (!st) { CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking)); st = own; }
     struct Own { cudaStream_t s; ~Own() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } } own_guard{own};
-    Arena A(st);
+    Arena A(st, dev);
     Ctx C;
     C.st = st;
     const u64* ddim = reinterpret_cast<const u64*>(dim);
@@ -1637,6 +1791,14 @@ int evoke_release_scratch(int device) {
     z.bytes = 0;
     z.target = 0;
     z.dirty = false;
+  }
+  // hand the pools' cached memory back to the device (other allocators, NCCL)
+  for (int d = (device < 0 ? 0 : device); d < (device < 0 ? 64 : device + 1); d++) {
+    cudaMemPool_t pool = evoke_pool_if_any(d);
+    if (!pool || cudaSetDevice(d) != cudaSuccess) continue;
+    (void)cudaDeviceSynchronize();
+    (void)cudaMemPoolTrimTo(pool, 0);
+    (void)cudaGetLastError();
   }
   (void)cudaSetDevice(cur);
   return EVOKE_OK;

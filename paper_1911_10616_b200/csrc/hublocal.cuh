@@ -64,11 +64,11 @@ __global__ void k_hub_est(DGraph g, const u32* __restrict__ Te, u64* __restrict_
   }
 }
 
-// items (slot s of a in N(v)) with T(v,a) >= 2 and est > 0, of this shard (v mod shards):
-// light (est <= HUB_WARP_MAX) or heavy (with est for the sort)
-__global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __restrict__ est, int shard_index,
-                          int num_shards, int32_t* __restrict__ light, int* n_light, int32_t* __restrict__ heavy,
-                          u32* __restrict__ heavy_est, int* n_heavy) {
+// items (slot s of a in N(v)) with T(v,a) >= 2 and est > 0, of this shard (mine[s], nullptr:
+// every item): light (est <= warp_max <= HUB_WARP_MAX) or heavy (with est for the sort)
+__global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __restrict__ est,
+                          const uint8_t* __restrict__ mine, u64 warp_max, int32_t* __restrict__ light, int* n_light,
+                          int32_t* __restrict__ heavy, u32* __restrict__ heavy_est, int* n_heavy) {
   const int lane = threadIdx.x & 31;
   const int64_t m2 = 2 * g.m;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < m2;
@@ -77,12 +77,10 @@ __global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __res
     u64 e = 0;
     if (s < m2) {
       const int32_t eva = g.eid[s];
-      const int32_t a = g.ci[s];
-      const int32_t v = g.esrc[eva] + g.edst[eva] - a;
-      if (Te[eva] >= 2 && v % num_shards == shard_index) e = est[s];
+      if (Te[eva] >= 2 && (!mine || mine[s])) e = est[s];
     }
-    warp_append(e > 0 && e <= HUB_WARP_MAX, (int32_t)s, light, n_light);
-    const bool is_heavy = e > HUB_WARP_MAX;
+    warp_append(e > 0 && e <= warp_max, (int32_t)s, light, n_light);
+    const bool is_heavy = e > warp_max;
     const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
     if (bal) {
       int hb = 0;
@@ -111,7 +109,7 @@ struct HubCtaShared {
 
 __device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_t s, u32* shm, HubCtaShared& S,
                              u32* __restrict__ gtab, int32_t* __restrict__ glist, u64* __restrict__ R68,
-                             u64* __restrict__ R69) {
+                             u64* __restrict__ R69, int sh_dense_max) {
   const int32_t eva = g.eid[s];
   const int32_t a = g.ci[s];
   const int32_t lo_ = g.esrc[eva];
@@ -119,7 +117,7 @@ __device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_
   const bool v_lo = lo_ == v;
   const int64_t rpv = g.rp[v];
   const int32_t dv = (int32_t)(g.rp[v + 1] - rpv);
-  const bool dense_sh = dv <= HUB_SH_DENSE;
+  const bool dense_sh = dv <= sh_dense_max;  // (<= HUB_SH_DENSE; lower only in tests)
   u32* tab = dense_sh ? shm : gtab;
   int32_t* list = dense_sh ? (int32_t*)(shm + HUB_SH_DENSE) : glist;
   const int64_t fa = g.foff[eva];
@@ -297,7 +295,7 @@ __global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __r
                                                         const int32_t* __restrict__ light, int n_light,
                                                         int* __restrict__ counters, u32* __restrict__ gtabs,
                                                         int32_t* __restrict__ glists, u64* __restrict__ R68,
-                                                        u64* __restrict__ R69) {
+                                                        u64* __restrict__ R69, int sh_dense_max) {
   extern __shared__ u32 hub_sh[];
   __shared__ HubCtaShared S;
   __shared__ int s_idx;
@@ -312,7 +310,7 @@ __global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __r
     const int idx = s_idx;
     __syncthreads();
     if (idx >= n_heavy) break;
-    hub_item_cta(g, Te, heavy[idx], hub_sh, S, gtab, glist, R68, R69);
+    hub_item_cta(g, Te, heavy[idx], hub_sh, S, gtab, glist, R68, R69, sh_dense_max);
   }
   // light items: the dynamic shared memory becomes one hash (keys, counts, list) per warp
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

@@ -1152,8 +1152,15 @@ __global__ void k_pair_est(DGraph g, u32* __restrict__ keys, int32_t* __restrict
 // Shard filter of the est-sorted (descending) vertex list and tier classification.
 // Lists keep the descending order approximately (warp-aggregated appends in list order).
 enum { PT_G64 = 0, PT_G32, PT_G32S, PT_MID, PT_LIGHT, PT_MIDS, PT_COUNT };
+// tier limits: the defaults are the capacities of each tier's tables; tests lower them (env
+// EVOKE_PAIR_*) to force sources onto the heavier tiers' code paths on small graphs
+struct PairTiers {
+  u64 packed_lim;  // d(u) and T(u) below this: packed 16-bit W | D (<= 65536)
+  u64 light_max, mids_max, mid_max;  // <= PAIR_WARP_MAX, PAIR_MIDS_MAX, PAIR_MID_MAX
+  int sweep;       // -1: by size (2-hop set >= n/16), 0: never, 1: always sweep the table
+};
 __global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const int32_t* __restrict__ svals,
-                                int si, int ns, const u64* __restrict__ Tv, u32* __restrict__ est_v,
+                                int si, int ns, PairTiers pt, const u64* __restrict__ Tv, u32* __restrict__ est_v,
                                 int32_t* __restrict__ lists, int* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1167,12 +1174,13 @@ __global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const i
       const u64 e = (u64)(u32)~skeys[p];
       est_v[u] = (u32)min(e, (u64)0xffffffffu);
       if (e > 0) {
-        const bool packed_ok = dg_deg(g, u) < 65536 && Tv[u] < 65536ull;
+        const bool packed_ok = (u64)dg_deg(g, u) < pt.packed_lim && Tv[u] < pt.packed_lim;
+        const bool sweep = pt.sweep < 0 ? e * 16 >= (u64)g.n : pt.sweep > 0;
         tier = !packed_ok ? PT_G64
-             : e <= PAIR_WARP_MAX ? PT_LIGHT
-             : e <= PAIR_MIDS_MAX ? PT_MIDS
-             : e <= PAIR_MID_MAX ? PT_MID
-             : e * 16 >= (u64)g.n ? PT_G32S  // 2-hop set a sizeable part of n: sweep the table
+             : e <= pt.light_max ? PT_LIGHT
+             : e <= pt.mids_max ? PT_MIDS
+             : e <= pt.mid_max ? PT_MID
+             : sweep ? PT_G32S  // 2-hop set a sizeable part of n: sweep the table
              : PT_G32;
       }
     }
