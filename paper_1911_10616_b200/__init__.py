@@ -23,7 +23,8 @@ import numpy as np
 
 NUM_ORBITS = 73
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libevoke.so")
+# (EVOKE_LIB_PATH: developer A/B of two builds of the library; default the in-tree build)
+LIB_PATH = os.environ.get("EVOKE_LIB_PATH") or os.path.join(_HERE, "libevoke.so")
 
 EVOKE_OK, EVOKE_EINVAL, EVOKE_ENOMEM, EVOKE_ECUDA, EVOKE_EINTERNAL = 0, -1, -2, -3, -5
 

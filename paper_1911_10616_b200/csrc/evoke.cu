@@ -1065,7 +1065,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     // adjacency maps of the hubs (h* membership and T(h*, x) in one load), within a memory budget
     int32_t* hslot = A.alloc<int32_t>(n);
     int* hcnt = A.alloc<int>(1, true);
-    const int max_maps = (int)std::min<int64_t>(4096, std::max<int64_t>(0, (256ll << 20) / ((int64_t)n * 4)));
+    const int max_maps = getenv("EVOKE_PAIR_NO_MAPS") ? 0  // (developer A/B: key search instead)
+                         : (int)std::min<int64_t>(4096, std::max<int64_t>(0, (256ll << 20) / ((int64_t)n * 4)));
     int32_t* hubs = A.alloc<int32_t>(std::max(max_maps, 1));
     k_hub_slots<<<grid_for(n, B, SM), B, 0, C.st>>>(g, max_maps, hslot, hubs, hcnt);
     int nmaps = 0;

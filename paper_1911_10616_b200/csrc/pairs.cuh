@@ -12,10 +12,16 @@
 //   theta64(v) += sum over diamonds (u; v,w; x), x>u, of W(u,x)-2:
 //   DM64(v) = sum_{pairs {a,x} in N(v)} |N(v)&N(a)&N(x)| (W(a,x)-2) seen from the pair.
 //
-// Two passes per source over the same items (the neighbours v of u; item v has d(v)
-// wedge elements u-v-x and T(u,v) chord elements (u; v, w)): pass 1 builds the table
+// Two passes per source over the same items (the neighbours v of u; item v has the wedge
+// elements u-v-x with x > u and T(u,v) chord elements (u; v, w)): pass 1 builds the table
 // (W from wedges, D from the diamonds behind chords w > v), pass 2 reads it (per-pair
 // terms over the table entries, per-wedge and per-diamond sums over the items).
+//
+// Each unordered pair {u, x} is formed once, from its lower end u (rank order; N(v) is
+// sorted, so the x > u part of N(v) is the suffix after u's own slot, found in O(1) from the
+// edge's slot map): the wedge walks are half of sum_v d(v)(d(v)-1).  A pair's terms are
+// credited to both ends (the x side with atomics, only for pairs with W >= 2), and so are
+// the per-wedge terms of both wedge edges (E5 of e(x,v), theta51 of x).
 //
 // Scheduling (B200): sources are sorted by their 2-hop estimate est(u) = sum_{v in N(u)}
 // d(v) - d(u) (>= the number of distinct x) and split in tiers:
@@ -37,7 +43,7 @@ struct PairOut {
   u64 *R8, *R36, *R50, *R51, *R63, *R49, *R62, *R64, *C4e;
   const int32_t* hstar;     // per source: its heaviest neighbour h* (wedges through h* are not walked)
   const int32_t* hub_slot;  // per vertex: row of its position map, or -1
-  const int32_t* hub_pos;   // [slot][x]: T(hub, x) if x ~ hub, else -1
+  const int32_t* hub_pos;   // [slot][x]: position of x in N(hub) if x ~ hub, else -1
 };
 
 __device__ __forceinline__ int64_t slot_of_lo_in_hi(const DGraph& g, int32_t e) { return g.eslot_hi[e]; }
@@ -235,15 +241,20 @@ struct GlobalDense {
   }
 };
 
-// phase C contributions of one (x, W, D) pair
-__device__ __forceinline__ void pair_c_terms(const DGraph& g, int32_t x, u64 w, u64 d, u64& a8, u64& a36,
-                                             u64& a50, u64& a63) {
+// phase C contributions of one (x, W, D) pair {u, x}, x > u: to u (summed by the caller)
+// and to x (atomics; du = d(u))
+__device__ __forceinline__ void pair_c_terms(const DGraph& g, const PairOut& o, u64 du, int32_t x, u64 w, u64 d,
+                                             u64& a8, u64& a36, u64& a50, u64& a63) {
   if (w < 2) return;  // W = 1: every term is 0 (and D = 0)
-  const u64 c2 = binom2(w);
+  const u64 c2 = binom2(w), c3 = binom3(w), t63 = d * (w - 2);
   a8 += c2;
   a36 += c2 * (u64)(int64_t)(dg_deg(g, x) - 2);
-  a50 += binom3(w);
-  a63 += d * (w - 2);
+  a50 += c3;
+  a63 += t63;
+  atomicAdd(&o.R8[x], c2);
+  atomicAdd(&o.R36[x], c2 * (du - 2));  // du >= w >= 2
+  if (c3) atomicAdd(&o.R50[x], c3);
+  if (t63) atomicAdd(&o.R63[x], t63);
 }
 
 // ---- per-element work (shared by the warp and CTA engines) --------------------------
@@ -259,17 +270,22 @@ struct PairItem {
   bool vlo;         // v is the lower endpoint of e
 };
 
-// the wedge part of item h* is empty: W(u,x) gets the h* contribution from a membership
-// test over the table keys instead (see entry_terms)
+// slot of u in N(v) for the edge e = e(u, v) (vlo: v is its lower endpoint)
+__device__ __forceinline__ int64_t slot_in_other(const DGraph& g, int32_t v, int32_t e, bool vlo) {
+  return vlo ? g.rp[v] + g.dm[v] + (e - g.orow[v]) : g.eslot_hi[e];
+}
+// Item v of source u: its wedge part is the suffix of N(v) after u (x > u); the wedge part of
+// item h* is empty: W(u,x) gets the h* contribution from a membership test over the table
+// keys instead (see hstar_and_terms)
 __device__ __forceinline__ PairItem pair_item(const DGraph& g, int64_t s_uv, int32_t hs) {
   PairItem it;
   it.v = g.ci[s_uv];
   it.e = g.eid[s_uv];
-  it.rb = g.rp[it.v];
+  it.vlo = g.esrc[it.e] == it.v;
+  it.rb = slot_in_other(g, it.v, it.e, it.vlo) + 1;
   it.dv = it.v == hs ? 0 : (int32_t)(g.rp[it.v + 1] - it.rb);
   it.fo = g.foff[it.e];
   it.tv = (int32_t)(g.foff[it.e + 1] - it.fo);
-  it.vlo = g.esrc[it.e] == it.v;
   return it;
 }
 
@@ -287,25 +303,16 @@ struct PairAcc {
 };
 
 template <typename Tab>
-__device__ __forceinline__ void pass1_wedge(const DGraph& g, int32_t u, int64_t rb, int k, Tab& tab) {
-  const int32_t x = g.ci[rb + k];
-  if (x != u) tab.add_w(x);
+__device__ __forceinline__ void pass1_wedge(const DGraph& g, int64_t rb, int k, Tab& tab) {
+  tab.add_w(g.ci[rb + k]);  // x > u: the item's list is the suffix after u
 }
-template <typename Tab>
-__device__ __forceinline__ void pass2_wedge(const DGraph& g, const u32* __restrict__ Te, int32_t u, int64_t rb,
-                                            int k, const Tab& tab, PairAcc& A, u64& s51) {
-  const int64_t t = rb + k;
-  const int32_t x = g.ci[t];
-  if (x == u) return;
-  u64 w, d;
-  tab.get(x, w, d);
-  if (w < 2) return;  // W(u,x) = 1 (hence D = 0) contributes nothing below
-  A.c5 += w - 1;
-  s51 += (u64)g.tes[t] * (w - 1);
-  if (x > u) {
-    A.c49 += binom2(w - 1);
-    A.c62 += d;
-  }
+// The x-side terms of a wedge u - v - x (x > u, W = W(u,x) >= 2, t = the slot of x in N(v),
+// tuv = T(u,v)): E5 of e(x,v) (counted from its lower end, as PairAcc::flush does for e(u,v))
+// and theta51 of x.
+__device__ __forceinline__ void wedge_x_side(const DGraph& g, const PairOut& o, int32_t x, int32_t v, int64_t t,
+                                             int tuv, u64 w) {
+  if (x < v) atomicAdd(&o.C4e[g.eid[t]], w - 1);
+  if (tuv) atomicAdd(&o.R51[x], (u64)tuv * (w - 1));
 }
 
 // Chords and diamonds, flattened on two levels.  Every lane brings at most one chord
@@ -327,7 +334,7 @@ __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool val
       const int32_t evw = vlo ? g.fe1[r] : g.fe2[r];
       f0 = g.foff[evw];
       len2 = (int)(g.foff[evw + 1] - f0);
-      if (PASS == 2 && g.full_sorted) {  // pass 2 needs x > u only: the suffix of a sorted list
+      if (g.full_sorted) {  // both passes need x > u only: the suffix of a sorted list
         const int64_t s0 = lower_bound_dev<int32_t>(g.fx, f0, f0 + len2, u + 1);
         len2 -= (int)(s0 - f0);
         f0 = s0;
@@ -344,7 +351,7 @@ __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool val
     if (!v2) return;
     const int32_t x = g.fx[f0j + k2];
     if (PASS == 1) {
-      if (x != u) tab.add_d(x);
+      if (x > u) tab.add_d(x);
     } else {
       if (own != cur) {
         if (cur >= 0 && c) atomicAdd(&acc[cur], c);
@@ -363,7 +370,7 @@ __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool val
 // PAIR_ILP dependent chains in flight instead of one.
 template <typename Tab>
 __device__ __forceinline__ void wedges_pass2_ilp(const DGraph& g, const u32* __restrict__ Te, int32_t u, int len,
-                                                 int64_t rb, int32_t v, int32_t e, const Tab& tab, u64& s51,
+                                                 int64_t rb, int32_t v, int32_t e, int tv, const Tab& tab, u64& s51,
                                                  const PairOut& o) {
   const int lane = threadIdx.x & 31;
   int incl = len;
@@ -378,7 +385,7 @@ __device__ __forceinline__ void wedges_pass2_ilp(const DGraph& g, const u32* __r
   int cur = -1;
   int32_t cv = 0, ce = 0;
   for (int t0 = 0; t0 < total; t0 += 32 * PAIR_ILP) {
-    int32_t xs[PAIR_ILP], js[PAIR_ILP], vs[PAIR_ILP], es[PAIR_ILP];
+    int32_t xs[PAIR_ILP], js[PAIR_ILP], vs[PAIR_ILP], es[PAIR_ILP], tvs[PAIR_ILP];
     int64_t ts[PAIR_ILP];
 #pragma unroll
     for (int i = 0; i < PAIR_ILP; i++) {
@@ -393,6 +400,7 @@ __device__ __forceinline__ void wedges_pass2_ilp(const DGraph& g, const u32* __r
       const int64_t rbj = __shfl_sync(FULL_MASK, rb, j);
       vs[i] = __shfl_sync(FULL_MASK, v, j);
       es[i] = __shfl_sync(FULL_MASK, e, j);
+      tvs[i] = __shfl_sync(FULL_MASK, tv, j);
       const bool valid = t < total;
       js[i] = valid ? j : -1;
       ts[i] = rbj + (t - start);
@@ -418,10 +426,9 @@ __device__ __forceinline__ void wedges_pass2_ilp(const DGraph& g, const u32* __r
       const u64 w = wv[i];
       A.c5 += w - 1;
       s51 += (u64)te[i] * (w - 1);
-      if (xs[i] > u) {
-        A.c49 += binom2(w - 1);
-        A.c62 += dv[i];
-      }
+      A.c49 += binom2(w - 1);
+      A.c62 += dv[i];
+      wedge_x_side(g, o, xs[i], vs[i], ts[i], tvs[i], w);
     }
   }
   if (cur >= 0) A.flush(u, cv, ce, o);
@@ -447,12 +454,12 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
     };
     // wedges
     if (PASS == 2) {
-      wedges_pass2_ilp(g, Te, u, it.dv, it.rb, it.v, it.e, tab, s51, o);
+      wedges_pass2_ilp(g, Te, u, it.dv, it.rb, it.v, it.e, it.tv, tab, s51, o);
     } else {
       warp_flat(it.dv, [&](int j, int k, bool valid) {
         const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
         if (!valid) return;
-        pass1_wedge(g, u, rbj, k, tab);
+        pass1_wedge(g, rbj, k, tab);
       });
     }
     flush();
@@ -568,6 +575,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     const bool have = lane < grab && base + lane < nitems;
     if (have) it = pair_item(g, r0 + base + lane, hs);
     else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
+    const int tuv = it.tv;  // T(u,v) for the wedges' x-side terms (it.tv is zeroed if the chords are queued)
     // defer long parts to the queue (if it has room)
     const int long_min = PAIR_LONG;
     if (it.dv > long_min) {
@@ -586,12 +594,12 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       if (PASS == 2 && cur >= 0) A.flush(u, cv, ce, o);
     };
     if (PASS == 2) {
-      wedges_pass2_ilp(g, Te, u, it.dv, it.rb, it.v, it.e, tab, s51, o);
+      wedges_pass2_ilp(g, Te, u, it.dv, it.rb, it.v, it.e, tuv, tab, s51, o);
     } else {
       warp_flat(it.dv, [&](int j, int k, bool valid) {
         const int64_t rbj = __shfl_sync(FULL_MASK, it.rb, j);
         if (!valid) return;
-        pass1_wedge(g, u, rbj, k, tab);
+        pass1_wedge(g, rbj, k, tab);
       });
     }
     flush();
@@ -686,7 +694,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       for (int k = k0 + lane; k < k1; k += 32) {
         const int32_t x = g.fx[f0 + k];
         if (PASS == 1) {
-          if (x != u) tab.add_d(x);
+          if (x > u) tab.add_d(x);
         } else {
           if (x > u) A.c64 += tab.get_w(x) - 2ull;
         }
@@ -727,7 +735,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
 #pragma unroll
         for (int i = 0; i < U; i++) {
           wv[i] = 0; dv[i] = 0;
-          if (xs[i] != u) tab.get(xs[i], wv[i], dv[i]);
+          if (xs[i] > u) tab.get(xs[i], wv[i], dv[i]);
         }
 #pragma unroll
         for (int i = 0; i < U; i++) {
@@ -740,10 +748,9 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
           const u64 w = wv[i];
           A.c5 += w - 1;
           s51 += (u64)te[i] * (w - 1);
-          if (xs[i] > u) {
-            A.c49 += binom2(w - 1);
-            A.c62 += dv[i];
-          }
+          A.c49 += binom2(w - 1);
+          A.c62 += dv[i];
+          wedge_x_side(g, o, xs[i], it.v, it.rb + k0 + lane + 32 * i, it.tv, w);
         }
       }
     } else {
@@ -779,78 +786,62 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
 // cost #keys * log d(h*)).  Both also emit the terms of the wedges u - h* - x with W >= 2
 // (E5 of e(u,h*), theta49/62 of h*, theta51 of u) into H / s51.
 template <typename Tab>
-__device__ __forceinline__ void hstar_walk(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
-                                           const Tab& tab, int tid, int nthr, PairAcc& H, u64& s51) {
-  const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
-  for (int64_t p = hb + tid; p < he; p += nthr) {
+__device__ __forceinline__ void hstar_walk(const DGraph& g, const PairOut& o, int32_t u, int32_t hs, int64_t hfrom,
+                                           int tuh, const Tab& tab, int tid, int nthr, PairAcc& H, u64& s51) {
+  const int64_t he = g.rp[hs + 1];
+  for (int64_t p = hfrom + tid; p < he; p += nthr) {  // x > u: the suffix of N(h*) after u
     const int32_t x = g.ci[p];
-    if (x == u) continue;
     auto* wp = tab.word_if(x);
     if (!wp) continue;
     const auto v = *wp + 1;  // x is visited once: plain update
     *wp = v;
     const u64 w = Tab::wfield(v), d = Tab::dfield(v);
+    if (w < 2) continue;
     H.c5 += w - 1;
     s51 += (u64)g.tes[p] * (w - 1);
-    if (x > u) {
-      H.c49 += binom2(w - 1);
-      H.c62 += d;
-    }
+    H.c49 += binom2(w - 1);
+    H.c62 += d;
+    wedge_x_side(g, o, x, hs, p, tuh, w);
   }
-}
-
-template <typename Tab>
-__device__ __forceinline__ void hstar_search(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
-                                             Tab& tab, int tid, int nthr, PairAcc& H, u64& s51) {
-  const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
-  tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
-    const int64_t p = lower_bound_dev<int32_t>(g.ci, hb, he, x);
-    if (p < he && g.ci[p] == x) {
-      w += 1;
-      H.c5 += w - 1;
-      s51 += (u64)g.tes[p] * (w - 1);
-      if (x > u) {
-        H.c49 += binom2(w - 1);
-        H.c62 += d;
-      }
-    }
-    return w;
-  });
 }
 
 // The h* term by the cheapest available way, fused with the per-pair terms when the table
 // is swept anyway (map / key search): returns true when a8..a63 were already added.
+// hfrom = the first slot of N(h*) above u; tuh = T(u, h*)
 template <typename Tab>
-__device__ __forceinline__ bool hstar_and_terms(const DGraph& g, const u32* __restrict__ Te, int32_t u, int32_t hs,
+__device__ __forceinline__ bool hstar_and_terms(const DGraph& g, int32_t u, int32_t hs, int64_t hfrom, int tuh,
                                                 const PairOut& o, Tab& tab, int tid, int nthr, u64 nkeys_bound,
                                                 PairAcc& H, u64& s51, u64& a8, u64& a36, u64& a50, u64& a63) {
   if (hs < 0) return false;
   const int32_t slot = o.hub_slot[hs];
-  const bool walk = Tab::kDense || (slot < 0 && (u64)dg_deg(g, hs) <= 12ull * nkeys_bound);
+  const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
+  const bool walk = Tab::kDense || (slot < 0 && (u64)(he - hfrom) <= 12ull * nkeys_bound);
   if (walk) {
-    hstar_walk(g, Te, u, hs, tab, tid, nthr, H, s51);
+    hstar_walk(g, o, u, hs, hfrom, tuh, tab, tid, nthr, H, s51);
     return false;
   }
-  const int64_t hb = g.rp[hs], he = g.rp[hs + 1];
   const int32_t* pmap = slot >= 0 ? o.hub_pos + (size_t)slot * (size_t)g.n : nullptr;
+  const u64 du = (u64)dg_deg(g, u);
   tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
-    int64_t te = -1;  // T(h*, x) when x ~ h*
+    int64_t p = -1;  // slot of x in N(h*) when x ~ h*
     if (pmap) {
-      te = pmap[x];  // the map holds T(h*, x) directly (one load instead of three)
+      const int32_t q = pmap[x];  // position of x in N(h*), or -1
+      if (q >= 0) p = hb + q;
     } else {
-      const int64_t q = lower_bound_dev<int32_t>(g.ci, hb, he, x);
-      if (q < he && g.ci[q] == x) te = (int64_t)g.tes[q];
+      const int64_t q = lower_bound_dev<int32_t>(g.ci, hfrom, he, x);
+      if (q < he && g.ci[q] == x) p = q;
     }
-    if (te >= 0) {
+    if (p >= 0) {
       w += 1;
-      H.c5 += w - 1;
-      s51 += (u64)te * (w - 1);
-      if (x > u) {
+      if (w >= 2) {
+        H.c5 += w - 1;
+        s51 += (u64)g.tes[p] * (w - 1);
         H.c49 += binom2(w - 1);
         H.c62 += d;
+        wedge_x_side(g, o, x, hs, p, tuh, w);
       }
     }
-    pair_c_terms(g, x, w, d, a8, a36, a50, a63);
+    pair_c_terms(g, o, du, x, w, d, a8, a36, a50, a63);
     return w;
   });
   return true;
@@ -871,31 +862,51 @@ __global__ void k_hub_slots(DGraph g, int max_slots, int32_t* __restrict__ slot,
     slot[v] = sl;
   }
 }
-// block per hub: row[x] = T(hub, x) for x in N(hub) (the rows start at -1)
+// block per hub: row[x] = position of x in N(hub) for x in N(hub) (the rows start at -1)
 __global__ void k_hub_maps(DGraph g, const u32* __restrict__ Te, const int32_t* __restrict__ hubs, int nhubs,
                            int32_t* __restrict__ pos) {
   for (int q = blockIdx.x; q < nhubs; q += gridDim.x) {
     const int32_t v = hubs[q];
     int32_t* row = pos + (size_t)q * (size_t)g.n;
     const int64_t b = g.rp[v], e = g.rp[v + 1];
-    for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)g.tes[k];
+    for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) row[g.ci[k]] = (int32_t)(k - b);
   }
 }
 
 // per-pair terms over the final table (keys with W >= 2)
 template <typename Tab>
-__device__ __forceinline__ void entry_terms(const DGraph& g, Tab& tab, int tid, int nthr, u64& a8, u64& a36,
-                                            u64& a50, u64& a63) {
+__device__ __forceinline__ void entry_terms(const DGraph& g, const PairOut& o, int32_t u, Tab& tab, int tid,
+                                            int nthr, u64& a8, u64& a36, u64& a50, u64& a63) {
+  const u64 du = (u64)dg_deg(g, u);
   tab.for_each_mut(tid, nthr, [&](int32_t x, u64 w, u64 d) -> u64 {
-    pair_c_terms(g, x, w, d, a8, a36, a50, a63);
+    pair_c_terms(g, o, du, x, w, d, a8, a36, a50, a63);
     return w;
   });
 }
 
-// walk N(h*) when that is cheaper than searching every key in it
-__device__ __forceinline__ bool hstar_prefer_walk(const DGraph& g, int32_t hs, u64 nkeys_bound) {
-  const u64 dh = (u64)dg_deg(g, hs);
-  return dh <= 12ull * nkeys_bound;
+// theta51 correction sum_{x in N(u)} W(u,x)(W(u,x)-1), from the pairs' lower ends: the
+// neighbours x > u of u (the suffix of N(u) after its dm(u) lower neighbours)
+template <typename Tab>
+__device__ __forceinline__ void s51_adjacent(const DGraph& g, const PairOut& o, int32_t u, const Tab& tab, int tid,
+                                             int nthr, u64& s51) {
+  for (int64_t s = g.rp[u] + g.dm[u] + tid; s < g.rp[u + 1]; s += nthr) {
+    const int32_t x = g.ci[s];
+    const u64 w = tab.get_w_or0(x);
+    if (w < 2) continue;
+    s51 -= w * (w - 1);
+    atomicAdd(&o.R51[x], (u64)0 - w * (w - 1));
+  }
+}
+
+// h* of u: the first slot of N(h*) above u, and T(u, h*)
+__device__ __forceinline__ void hstar_info(const DGraph& g, int32_t u, int32_t hs, int64_t& hfrom, int& tuh,
+                                           int32_t& euh) {
+  hfrom = 0; tuh = 0; euh = -1;
+  if (hs < 0) return;
+  const int64_t p = lower_bound_dev<int32_t>(g.ci, g.rp[u], g.rp[u + 1], hs);
+  euh = g.eid[p];
+  tuh = (int)g.tes[p];
+  hfrom = slot_in_other(g, hs, euh, g.esrc[euh] == hs) + 1;
 }
 
 // slot of h* in N(u) -> edge id e(u, h*)
@@ -910,6 +921,10 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
                                 u64* red, const PairOut& o, u32 tab_keys_bound) {
   const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
   const int32_t hs = o.hstar[u];
+  int64_t hfrom;
+  int tuh;
+  int32_t euh;
+  hstar_info(g, u, hs, hfrom, tuh, euh);
   u64 s51 = 0;
   long long t_prev = clock64();
   cta_pass<1, BT>(g, Te, u, hs, r0, r1, tab, E, s51, o);
@@ -917,8 +932,8 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
   PairAcc H;
   H.zero();
-  const bool fused = hstar_and_terms(g, Te, u, hs, o, tab, threadIdx.x, BT, (u64)tab_keys_bound, H, s51, a8, a36,
-                                     a50, a63);
+  const bool fused = hstar_and_terms(g, u, hs, hfrom, tuh, o, tab, threadIdx.x, BT, (u64)tab_keys_bound, H, s51, a8,
+                                     a36, a50, a63);
   H.c5 = warp_sum(H.c5); H.c49 = warp_sum(H.c49); H.c62 = warp_sum(H.c62);
   if ((threadIdx.x & 31) == 0) {
     if (H.c5) atomicAdd(&red[5], H.c5);
@@ -928,16 +943,13 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   __syncthreads();
   PAIR_PHASE(1);
   if (!fused) {
-    entry_terms(g, tab, threadIdx.x, BT, a8, a36, a50, a63);
+    entry_terms(g, o, u, tab, threadIdx.x, BT, a8, a36, a50, a63);
     __syncthreads();  // W final
   }
   PAIR_PHASE(2);
   cta_pass<2, BT>(g, Te, u, hs, r0, r1, tab, E, s51, o);
   PAIR_PHASE(3);
-  for (int64_t s = r0 + threadIdx.x; s < r1; s += BT) {
-    const u64 w = tab.get_w_or0(g.ci[s]);
-    s51 -= w * (w - 1);
-  }
+  s51_adjacent(g, o, u, tab, threadIdx.x, BT, s51);
   a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
   if ((threadIdx.x & 31) == 0) {
     if (a8) atomicAdd(&red[0], a8);
@@ -948,10 +960,15 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    o.R8[u] += red[0]; o.R36[u] += red[1]; o.R50[u] += red[2]; o.R51[u] += red[3]; o.R63[u] += red[4];
+    // atomics: the pairs' lower ends credit their upper ends concurrently
+    if (red[0]) atomicAdd(&o.R8[u], red[0]);
+    if (red[1]) atomicAdd(&o.R36[u], red[1]);
+    if (red[2]) atomicAdd(&o.R50[u], red[2]);
+    if (red[3]) atomicAdd(&o.R51[u], red[3]);
+    if (red[4]) atomicAdd(&o.R63[u], red[4]);
     if (hs >= 0) {
       H.c5 = red[5]; H.c49 = red[6]; H.c62 = red[7]; H.c64 = 0;
-      H.flush(u, hs, edge_of(g, u, hs), o);
+      H.flush(u, hs, euh, o);
     }
     for (int i = 0; i < 8; i++) red[i] = 0;
   }
@@ -966,6 +983,10 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
   const int lane = threadIdx.x & 31;
   const int64_t r0 = g.rp[u], r1 = g.rp[u + 1];
   const int32_t hs = o.hstar[u];
+  int64_t hfrom;
+  int tuh;
+  int32_t euh;
+  hstar_info(g, u, hs, hfrom, tuh, euh);
   tab.mask = cap - 1;
   u64 s51 = 0;
   warp_pass<1>(g, Te, u, hs, r0, r1, tab, s51, o, acc);
@@ -973,17 +994,15 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
   u64 a8 = 0, a36 = 0, a50 = 0, a63 = 0;
   PairAcc H;
   H.zero();
-  const bool fused = hstar_and_terms(g, Te, u, hs, o, tab, lane, 32, (u64)(cap / 2), H, s51, a8, a36, a50, a63);
+  const bool fused = hstar_and_terms(g, u, hs, hfrom, tuh, o, tab, lane, 32, (u64)(cap / 2), H, s51, a8, a36, a50,
+                                     a63);
   __syncwarp();
   if (!fused) {
-    entry_terms(g, tab, lane, 32, a8, a36, a50, a63);
+    entry_terms(g, o, u, tab, lane, 32, a8, a36, a50, a63);
     __syncwarp();
   }
   warp_pass<2>(g, Te, u, hs, r0, r1, tab, s51, o, acc);
-  for (int64_t s = r0 + lane; s < r1; s += 32) {
-    const u64 w = tab.get_w_or0(g.ci[s]);
-    s51 -= w * (w - 1);
-  }
+  s51_adjacent(g, o, u, tab, lane, 32, s51);
   a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
   H.c5 = warp_sum(H.c5); H.c49 = warp_sum(H.c49); H.c62 = warp_sum(H.c62);
   if (lane == 0) {
@@ -992,7 +1011,7 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
     if (a50) atomicAdd(&o.R50[u], a50);
     if (s51) atomicAdd(&o.R51[u], s51);
     if (a63) atomicAdd(&o.R63[u], a63);
-    if (hs >= 0) H.flush(u, hs, edge_of(g, u, hs), o);
+    if (hs >= 0) H.flush(u, hs, euh, o);
   }
   __syncwarp();
   tab.reset(lane, 32);
@@ -1114,8 +1133,9 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
   }
 }
 
-// 2-hop estimate without the heaviest neighbour h*: est(u) = sum_{v in N(u), v != h*} d(v)
-// - d(u) + 1 = the number of wedge elements walked (>= the number of table keys).
+// Work estimate of source u: est(u) = sum_{v in N(u), v != h*} |{x in N(v) : x > u}|, the
+// wedge elements walked (>= the number of table keys: every diamond end is also the end of a
+// walked wedge).  h*(u) = the neighbour with the longest such suffix (ties: lower id).
 __global__ void k_pair_est(DGraph g, u32* __restrict__ keys, int32_t* __restrict__ vals,
                            int32_t* __restrict__ hstar) {
   const int lane = threadIdx.x & 31;
@@ -1124,24 +1144,24 @@ __global__ void k_pair_est(DGraph g, u32* __restrict__ keys, int32_t* __restrict
   for (int64_t ui = gw; ui < g.n; ui += nw) {
     const int32_t u = (int32_t)ui;
     u64 s = 0;
-    int32_t best = -1, bestd = -1;
+    int32_t best = -1, bestl = -1;
     for (int64_t t = g.rp[u] + lane; t < g.rp[u + 1]; t += 32) {
       const int32_t v = g.ci[t];
-      const int32_t dv = dg_deg(g, v);
-      s += (u64)dv;
-      if (dv > bestd) { bestd = dv; best = v; }
+      const int32_t e = g.eid[t];
+      const int32_t len = (int32_t)(g.rp[v + 1] - slot_in_other(g, v, e, g.esrc[e] == v) - 1);
+      s += (u64)len;
+      if (len > bestl || (len == bestl && v < best)) { bestl = len; best = v; }
     }
     s = warp_sum(s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const int32_t od = __shfl_xor_sync(FULL_MASK, bestd, o);
+      const int32_t ol = __shfl_xor_sync(FULL_MASK, bestl, o);
       const int32_t ob = __shfl_xor_sync(FULL_MASK, best, o);
-      if (od > bestd || (od == bestd && ob < best)) { bestd = od; best = ob; }
+      if (ol > bestl || (ol == bestl && ob < best)) { bestl = ol; best = ob; }
     }
     if (lane == 0) {
-      const u64 du = (u64)dg_deg(g, u);
-      const u64 est = du > 0 ? s - (u64)bestd - du + 1 : 0;
-      keys[u] = ~(u32)min(est, (u64)0xffffffffu);  // ascending sort = descending estimate (est <= 2m < 2^31)
+      const u64 est = best >= 0 ? s - (u64)bestl : 0;
+      keys[u] = ~(u32)min(est, (u64)0xffffffffu);  // ascending sort = descending estimate
       vals[u] = u;
       hstar[u] = best;
     }

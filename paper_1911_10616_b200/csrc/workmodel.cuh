@@ -12,8 +12,8 @@ struct WorkUnits {
   u64 c5_wedge;      // cycles5 steps 1 and 6  : w1 = sum_l sum_{w in N(l)} |Nsel(w)|
   u64 c5_q;          // cycles5 steps 2/4 and 3: w2 + w3 (see cycles5.cuh)
   u64 tri_stream;    // triangle pass          : sum_{e=(a,b)} d+(b)
-  u64 pair_rwedge;   // pair wedges walked     : sum_u sum_{v in N(u), v != h*(u)} (d(v) - 1)
-  u64 pair_hwalk;    // h* term                : sum_u min(d(h*(u)), pair wedges of u)
+  u64 pair_rwedge;   // pair wedges walked     : sum_u sum_{v in N(u), v != h*(u)} |N(v) & (u, n)|
+  u64 pair_hwalk;    // h* term                : sum_u min(|N(h*) & (u, n)|, pair wedges of u)
 };
 
 // warp per vertex u (as a pair source and as a 5-cycle endpoint l = u)
@@ -26,31 +26,35 @@ __global__ void k_units_vertex(DGraph g, WorkUnits* out) {
     const int32_t u = (int32_t)ui;
     const int64_t r0 = g.rp[u], r1 = g.rp[u + 1], rm = r0 + g.dm[u];
     u64 s = 0, a1 = 0, a23 = 0;
-    int32_t dmax = 0;
+    int32_t lmax = 0;
     for (int64_t t = r0 + lane; t < r1; t += 32) {
       const int32_t v = g.ci[t];
       const int32_t dv = dg_deg(g, v);
-      s += (u64)dv;
-      dmax = max(dmax, dv);
+      // the part of N(v) above u (the pair pass forms each pair from its lower end)
+      const int32_t e = g.eid[t];
+      const int64_t pos = (g.esrc[e] == v) ? g.rp[v] + g.dm[v] + (e - g.orow[v]) : g.eslot_hi[e];
+      const int32_t len = (int32_t)(g.rp[v + 1] - pos - 1);
+      s += (u64)len;
+      lmax = max(lmax, len);
       a1 += (u64)((v < u) ? dv : dv - g.dm[v]);
       if (t < rm) {
         const int64_t ok = g.orow[v], ok1 = g.orow[v + 1];
         a23 += (u64)(ok1 - ok);
-        for (int64_t e = ok; e < ok1; e++) {
-          const int32_t j = g.ocol[e];
+        for (int64_t e2 = ok; e2 < ok1; e2++) {
+          const int32_t j = g.ocol[e2];
           a23 += (u64)(g.orow[j + 1] - g.orow[j]);
         }
       }
     }
     s = warp_sum(s); a1 = warp_sum(a1); a23 = warp_sum(a23);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(FULL_MASK, dmax, o));
+    for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(FULL_MASK, lmax, o));
     if (lane == 0) {
       const u64 du = (u64)dg_deg(g, u);
       d2 += du * du;
-      const u64 r = du > 0 ? s - (u64)dmax - (du - 1) : 0;
+      const u64 r = du > 0 ? s - (u64)lmax : 0;
       rw += r;
-      hw += min((u64)dmax, r);  // h* term: a walk of N(h*) or a search per key, counted as the smaller
+      hw += min((u64)lmax, r);  // h* term: a walk of N(h*) or a search per key, counted as the smaller
       w1 += a1;
       w23 += a23;
     }

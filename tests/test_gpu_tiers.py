@@ -46,6 +46,15 @@ def pkg():
     return p
 
 
+def _book(pages, p, seed):
+    """book graph: the spine edge (0, 1) and `pages` vertices adjacent to both ends (T(0,1) =
+    pages), plus seeded random page-page edges"""
+    rng = np.random.default_rng(seed)
+    e = [(0, 1)] + [(0, 2 + i) for i in range(pages)] + [(1, 2 + i) for i in range(pages)]
+    e += [(2 + i, 2 + j) for i in range(pages) for j in range(i + 1, pages) if rng.random() < p]
+    return graphgen.Graph(f"book{pages}_p{p}", pages + 2, np.array(e, dtype=np.int32))
+
+
 @pytest.fixture(scope="module")
 def corpus():
     rng = np.random.default_rng(21)
@@ -53,6 +62,7 @@ def corpus():
     for t in range(30):
         n = int(rng.integers(4, 14))
         gs.append(graphgen.erdos_renyi(n, float(rng.uniform(0.15, 0.95)), 12000 + t))
+    gs += [_book(70, 0.0, 1), _book(80, 0.04, 2)]  # T(a,b) > 64: long chord parts (the CTA queue)
     gs += [graphgen.config(1), graphgen.erdos_renyi(40, 0.5, 1), graphgen.erdos_renyi(34, 0.9, 3),
            graphgen.erdos_renyi(500, 0.02, 31), graphgen.erdos_renyi(2500, 0.004, 32), graphgen.petersen(),
            graphgen.complete(9), graphgen.complete_bipartite(4, 9)]
