@@ -113,8 +113,9 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 #define C5_BT 256
 #define C5_WARP_MAX 1024          // light endpoint: record bound R(l) <= this ...
 #define C5_WARP_WORK 8192         // ... and work W(l) <= this
-#define C5_WARP_CAP 2048          // records per warp region (load <= 0.5)
-#define C5_SH_CAP 256             // light endpoints with a region of <= this many slots: shared memory
+#define C5_WARP_CAP (2 * C5_WARP_MAX)  // records per warp region (load <= 0.5; global only when EVOKE_C5_SHCAP < it)
+#define C5_SH_CAP 512             // light endpoints with a region of <= sh_cap (<= this) slots: shared memory
+#define C5_SH_CAP_DEFAULT 256
 #define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (sizeof(C5RecP) + 2 * 4))   // records + touched + J lists
 #define C5_SH_BYTES(cap) ((C5_BT / 32) * C5_SH_WARP_BYTES(cap))
 #define C5_HBT 1024               // heavy-endpoint CTA
@@ -494,14 +495,18 @@ __global__ void k_c5_work(DGraph g, const u32* __restrict__ splus, u64* __restri
 }
 
 // Tiers of this shard's endpoints (mine == nullptr: every endpoint):
-//   light (one warp):  R <= rec_light  and W <= work_light   (packed records, per-warp hash)
-//   mid (128 threads): R <= rec_mid    and W <= work_mid     (packed records, per-CTA hash)
-//   big (1024 threads): the rest (dense records by vertex id, sorted by W descending)
-// Packed 16-bit record fields need W < 2^16 for the light and mid tiers (work_mid < 2^16).
+//   light (one warp):    R <= rec_light and W <= work_light (packed records, per-warp hash;
+//                        shared memory when 2R fits the warp's shared region, else global)
+//   mid (128 threads):   R <= rec_mid   and W <= work_mid   (packed records, per-CTA hash in global memory)
+//   big (1024 threads):  the rest (dense records by vertex id, sorted by W descending)
+// Packed 16-bit record fields need W < 2^16 for the hashed tiers (work_mid < 2^16).  Measured
+// on config 4: a warp per endpoint with its records in an L2 region beats a CTA per endpoint
+// with the records in shared memory (78 vs 124 ms): the CTA engine's barriers and idle warps
+// cost more than the region's L2 round trips, which many resident warps hide.
+// Lists: tier t in lists[t * n ...], with R (t < 2) or W (big) beside it.
 __global__ void k_c5_bin(DGraph g, const u64* __restrict__ W, const u64* __restrict__ R,
-                         const uint8_t* __restrict__ mine, u64 rec_light, u64 work_light, u64 rec_mid, u64 work_mid,
-                         int32_t* __restrict__ light, u32* __restrict__ light_r, int32_t* __restrict__ mid,
-                         u32* __restrict__ mid_r, int32_t* __restrict__ big, u64* __restrict__ big_w,
+                         const uint8_t* __restrict__ mine, u64 rec_light, u64 work_light, u64 rec_mid,
+                         u64 work_mid, int32_t* __restrict__ lists, u32* __restrict__ rbs, u64* __restrict__ big_w,
                          int* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < g.n;
@@ -509,7 +514,9 @@ __global__ void k_c5_bin(DGraph g, const u64* __restrict__ W, const u64* __restr
     const int32_t l = (int32_t)min(base + lane, (int64_t)g.n - 1);
     const bool ok = base + lane < g.n && W[l] > 0 && (!mine || mine[l]);
     const u64 w = ok ? W[l] : 0, r = ok ? R[l] : 0;
-    const int tier = !ok ? -1 : (r <= rec_light && w <= work_light) ? 0 : (r <= rec_mid && w <= work_mid) ? 1 : 2;
+    const int tier = !ok ? -1
+                   : (r <= rec_light && w <= work_light) ? 0
+                   : (r <= rec_mid && w <= work_mid) ? 1 : 2;
     for (int t = 0; t < 3; t++) {
       const u32 bal = __ballot_sync(FULL_MASK, tier == t);
       if (!bal) continue;
@@ -519,9 +526,9 @@ __global__ void k_c5_bin(DGraph g, const u64* __restrict__ W, const u64* __restr
       b0 = __shfl_sync(FULL_MASK, b0, leader);
       if (tier != t) continue;
       const int q = b0 + __popc(bal & ((1u << lane) - 1u));
-      if (t == 0) { light[q] = l; light_r[q] = (u32)r; }
-      else if (t == 1) { mid[q] = l; mid_r[q] = (u32)r; }
-      else { big[q] = l; big_w[q] = w; }
+      lists[(size_t)t * g.n + q] = l;
+      if (t < 2) rbs[(size_t)t * g.n + q] = (u32)r;
+      else big_w[q] = w;
     }
   }
 }
@@ -623,8 +630,8 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
 
 // Mid endpoints: one C5_MBT-thread CTA each, records in a per-CTA open-addressing region of
 // 2 x R(l) slots in global memory (the region is reused endpoint after endpoint, so it stays
-// in L2).  A 1024-thread CTA per such endpoint would spend its time in barriers and
-// dependent round trips with most warps idle.
+// in L2).  A 1024-thread CTA per such endpoint would spend its time in barriers and dependent
+// round trips with most warps idle.
 __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restrict__ Tlow,
                                                    const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                    const int32_t* __restrict__ list, const u32* __restrict__ rb,
@@ -643,8 +650,8 @@ __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restri
   C5Hash<C5RecP> loc;
   loc.R = regions + (size_t)blockIdx.x * C5_MID_CAP;
   loc.L = rlists + (size_t)blockIdx.x * 2 * C5_MID_CAP;
-  loc.nL = &s_nL;
   int32_t* J = loc.L + C5_MID_CAP;
+  loc.nL = &s_nL;
   for (;;) {
     if (threadIdx.x == 0) { s_idx = atomicAdd(counter, 1); s_nL = 0; s_nJ = 0; s_tot = 0; }
     __syncthreads();

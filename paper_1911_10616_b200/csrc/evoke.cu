@@ -240,6 +240,7 @@ struct Ctx {
   bool side_used = false;
   cudaEvent_t gev[3] = {};  // early tail gathers: start, after gathers 2/3, after the triangle gather
   bool gathers_early = false;
+  bool serial_run = false;  // the concurrent passes ran one after the other on the main stream
   cudaStream_t side_st = nullptr;
   static const int MAXJOBS = 16;
   cudaStream_t jst[MAXJOBS] = {};
@@ -931,6 +932,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     g.tes = tes; g.tlows = tlows; g.tmids = tmids;
   }
   const int si = o.shard_index, ns = o.num_shards;
+  // Concurrent passes pay off while the passes are short (their tails and the host-visible
+  // preparations overlap); on large graphs every pass fills the GPU by itself and running
+  // them side by side only splits L2 between their tables (config 4: 190 ms serial, 209 ms
+  // concurrent), so from EVOKE_CONCURRENT_MAX_M edges on they run one after the other, and
+  // each takes every SM at the occupancy that hides most latency (config 4, 5-cycles: 78 ms
+  // at the concurrent-mode grids, 63 ms at full occupancy).
+  const char* cmax_env = getenv("EVOKE_CONCURRENT_MAX_M");
+  const int64_t concurrent_max_m = cmax_env ? atoll(cmax_env) : (4ll << 20);
+  const bool whole_gpu_passes = m > concurrent_max_m;
   // per sharded pass (pair, hub-local, 5-cycle, cliques): this shard's and all work estimates
   u64* d_work = A.alloc<u64>(8, true);
   // ------------------------------------------------------------------ a5/a9: cliques
@@ -1069,10 +1079,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
                          : (int)std::min<int64_t>(4096, std::max<int64_t>(0, (256ll << 20) / ((int64_t)n * 4)));
     int32_t* hubs = A.alloc<int32_t>(std::max(max_maps, 1));
     k_hub_slots<<<grid_for(n, B, SM), B, 0, C.st>>>(g, max_maps, hslot, hubs, hcnt);
-    int nmaps = 0;
-    CK(cudaMemcpyAsync(&nmaps, hcnt, sizeof(int), cudaMemcpyDeviceToHost, C.st));
+    int hcs[1] = {0};
+    CK(cudaMemcpyAsync(&hcs[0], hcnt, sizeof(int), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
-    nmaps = std::min(nmaps, max_maps);
+    const int nmaps = std::min(hcs[0], max_maps);
     int32_t* hpos = A.alloc<int32_t>((size_t)std::max(nmaps, 1) * n);
     if (nmaps > 0) {
       CK(cudaMemsetAsync(hpos, 0xff, sizeof(int32_t) * (size_t)nmaps * n, C.st));
@@ -1096,7 +1106,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     const int heavy_qcap = 2 * g.max_deg + 65536;
     auto heavy_grid = [&](int nsrc, size_t word, int cap) {
       const int64_t l2_ctas = std::max<int64_t>(1, (56ll << 20) / ((int64_t)n * (int64_t)word));
-      int64_t pg = std::min<int64_t>(l2_ctas >= SM / 2 ? SM / 2 : SM, cap);
+      int64_t pg = std::min<int64_t>((l2_ctas >= SM / 2 && !whole_gpu_passes) ? SM / 2 : SM, cap);
       if (phg_env) pg = std::max(1, atoi(phg_env));  // developer knob: the grid itself
       pg = std::min<int64_t>(pg, nsrc);
       const int64_t per_cta = (int64_t)n * (int64_t)(word + 4) + (int64_t)eng_queue_bytes(heavy_qcap);
@@ -1221,7 +1231,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       // a short hub-local pass (few items) gets one CTA per SM, not as many as fit: its CTAs
       // placed ahead of the heavy pair sources' whole-SM CTAs delay those (config 2: 0.1 ms
       // better); a long one (diamond-heavy graphs) keeps full occupancy (config 3: 4.6 s, not 6.7)
-      const int hub_ctas_per_sm = (int64_t)n_light + n_heavy <= HUB_FEW_ITEMS ? 1 : std::max(1, hb_per_sm);
+      const int hub_ctas_per_sm =
+          ((int64_t)n_light + n_heavy <= HUB_FEW_ITEMS && !whole_gpu_passes) ? 1 : std::max(1, hb_per_sm);
       const int hg = hhg_env ? std::max(1, atoi(hhg_env)) : std::min(std::max(1, hb_per_sm), hub_ctas_per_sm) * SM;
       u32* gt = nullptr;
       int32_t* gl = nullptr;
@@ -1253,25 +1264,25 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     k_c5_work<<<warp_grid, B, 0, C.st>>>(g, splus, c5W, c5R);
     C.launches += 2;
     const uint8_t* c5mine = shard_mask(A, C, c5W, n, si, ns, d_work + 4);
-    int32_t* c5l = A.alloc<int32_t>(n);
-    u32* c5lr = A.alloc<u32>(n);
-    int32_t* c5m = A.alloc<int32_t>(n);
-    u32* c5mr = A.alloc<u32>(n);
-    int32_t* c5b = A.alloc<int32_t>(n);
-    u64* c5bw = A.alloc<u64>(n);
-    int* c5c = A.alloc<int>(8, true);  // tier sizes [0..2], persistent-kernel counters [3..5]
+    int32_t* c5lists = A.alloc<int32_t>((size_t)3 * n);  // light, mid, big
+    u32* c5rb = A.alloc<u32>((size_t)2 * n);              // R(l) of the hashed tiers
+    u64* c5bw = A.alloc<u64>(n);                          // W(l) of the big tier
+    int* c5c = A.alloc<int>(8, true);  // tier sizes [0..2], persistent-kernel counters [4..6]
     u64* C5out = Fp(F_C5);
     // tier limits (lower only: env for tests); mid work < 2^16 keeps the packed records exact
     const u64 rec_light = env_cap("EVOKE_C5_LIGHT_REC", C5_WARP_MAX), work_light = env_cap("EVOKE_C5_LIGHT_WORK", C5_WARP_WORK);
     const u64 rec_mid = env_cap("EVOKE_C5_MID_REC", C5_MID_MAX), work_mid = env_cap("EVOKE_C5_MID_WORK", C5_MID_WORK);
-    k_c5_bin<<<grid_for(n, B, SM), B, 0, C.st>>>(g, c5W, c5R, c5mine, rec_light, work_light, rec_mid, work_mid, c5l,
-                                                 c5lr, c5m, c5mr, c5b, c5bw, c5c);
+    k_c5_bin<<<grid_for(n, B, SM), B, 0, C.st>>>(g, c5W, c5R, c5mine, rec_light, work_light, rec_mid, work_mid,
+                                                 c5lists, c5rb, c5bw, c5c);
     C.launches++;
     int hc5[3];
     CK(cudaMemcpyAsync(hc5, c5c, sizeof(hc5), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     C.tick("c5_items+sync");
     const int n5l = hc5[0], n5m = hc5[1], n5b = hc5[2];
+    int32_t* c5l = c5lists;
+    u32* c5lr = c5rb;
+    int32_t* c5b = c5lists + (size_t)2 * n;
     if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d mid %d big %d\n", n5l, n5m, n5b);
     if (getenv("EVOKE_C5_HIST")) {  // developer: W / R histogram of every endpoint
       std::vector<u64> hw(n), hr(n);
@@ -1293,6 +1304,30 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
                 (unsigned long long)cr[b2]);
     }
     const size_t freeb = avail_bytes(C.dev);
+    // W-descending order of a hashed tier's list (heaviest endpoints first)
+    auto sort_tier = [&](int t, int cnt, int32_t*& ls, u32*& rs) {
+      ls = c5lists + (size_t)t * n;
+      rs = c5rb + (size_t)t * n;
+      if (cnt <= 1) return;
+      u64* mw = A.alloc<u64>(cnt);
+      k_gather_u64<<<grid_for(cnt, B, SM), B, 0, C.st>>>(c5W, ls, cnt, mw);
+      int32_t* idx = A.alloc<int32_t>(cnt);
+      int32_t* sidx = A.alloc<int32_t>(cnt);
+      u64* sk = A.alloc<u64>(cnt);
+      k_iota_i32<<<grid_for(cnt, B, SM), B, 0, C.st>>>(idx, cnt);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, mw, sk, idx, sidx, cnt, 0, 64, C.st));
+      void* t2 = A.alloc<char>(tb);
+      CK(cub::DeviceRadixSort::SortPairsDescending(t2, tb, mw, sk, idx, sidx, cnt, 0, 64, C.st));
+      int32_t* lo = A.alloc<int32_t>(cnt);
+      u32* ro = A.alloc<u32>(cnt);
+      k_permute_c5<<<grid_for(cnt, B, SM), B, 0, C.st>>>(sidx, cnt, ls, rs, lo, ro);
+      C.launches += 3;
+      C.lib_launches += 4;
+      ls = lo;
+      rs = ro;
+    };
+    std::vector<std::function<void(cudaStream_t)>> c5chain;  // big, then mid: one stream
     if (n5b > 0) {
       // big endpoints, W descending
       int32_t* bs = c5b;
@@ -1327,74 +1362,52 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         CK(cudaFuncSetAttribute(k_c5_heavy<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
         CK(cudaFuncSetAttribute(k_c5_heavy<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
       }
-      jobs.push_back({P_C5, 0, [=, &C](cudaStream_t st) {
+      c5chain.push_back([=, &C](cudaStream_t st) {
         if (narrow)
-          k_c5_heavy<u32><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 3,
+          k_c5_heavy<u32><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 6,
                                                    reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq, use_bits);
         else
-          k_c5_heavy<u64><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 3,
+          k_c5_heavy<u64><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 6,
                                                    reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, use_bits);
         C.launches++;
-      }});
+      });
     }
     if (n5m > 0) {
       // mid endpoints, W descending: several 4-warp CTAs per SM, hashed records in per-CTA
-      // regions; they run after the big endpoints on the same stream (as one more concurrent
-      // grid they would take SMs from the other passes' persistent kernels)
-      int32_t* ms = c5m;
-      u32* mr = c5mr;
-      if (n5m > 1) {
-        u64* mw = A.alloc<u64>(n5m);
-        k_gather_u64<<<grid_for(n5m, B, SM), B, 0, C.st>>>(c5W, c5m, n5m, mw);
-        int32_t* idx = A.alloc<int32_t>(n5m);
-        int32_t* sidx = A.alloc<int32_t>(n5m);
-        u64* sk = A.alloc<u64>(n5m);
-        k_iota_i32<<<grid_for(n5m, B, SM), B, 0, C.st>>>(idx, n5m);
-        size_t tb = 0;
-        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, mw, sk, idx, sidx, n5m, 0, 64, C.st));
-        void* t = A.alloc<char>(tb);
-        CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, mw, sk, idx, sidx, n5m, 0, 64, C.st));
-        ms = A.alloc<int32_t>(n5m);
-        mr = A.alloc<u32>(n5m);
-        k_permute_c5<<<grid_for(n5m, B, SM), B, 0, C.st>>>(sidx, n5m, c5m, c5mr, ms, mr);
-        C.launches += 3;
-        C.lib_launches += 4;
-      }
+      // global regions
+      int32_t* ms;
+      u32* mr;
+      sort_tier(1, n5m, ms, mr);
       int bpm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_c5_mid, C5_MBT, 0));
       const char* mb_env = getenv("EVOKE_C5_MBPS");  // developer knob: mid CTAs per SM
-      const int gm = (int)std::min<int64_t>(std::max(1, std::min(bpm, mb_env ? atoi(mb_env) : 4)) * SM, n5m);
+      const int mbps = mb_env ? atoi(mb_env) : (whole_gpu_passes ? 16 : 4);
+      const int gm = (int)std::min<int64_t>(std::max(1, std::min(bpm, mbps)) * SM, n5m);
       C5RecP* mreg = A.zalloc<C5RecP>((size_t)gm * C5_MID_CAP);
       int32_t* mlists = A.alloc<int32_t>((size_t)gm * 2 * C5_MID_CAP);
       int32_t* mq = A.alloc<int32_t>((size_t)gm * (2 * (size_t)g.max_deg + 1));
-      const int32_t* ms_ = ms;
-      const u32* mr_ = mr;
-      const int job = n5b > 0 ? (int)jobs.size() - 1 : -1;
-      auto mid_fn = [=, &C](cudaStream_t st) {
-        k_c5_mid<<<gm, C5_MBT, 0, st>>>(g, Tlow, Tmid, Thigh, ms_, mr_, n5m, c5c + 4, mreg, mlists, C5out, mq);
+      c5chain.push_back([=, &C](cudaStream_t st) {
+        k_c5_mid<<<gm, C5_MBT, 0, st>>>(g, Tlow, Tmid, Thigh, ms, mr, n5m, c5c + 5, mreg, mlists, C5out, mq);
         C.launches++;
-      };
-      if (job >= 0) {
-        auto big_fn = jobs[job].fn;
-        jobs[job].fn = [=](cudaStream_t st) { big_fn(st); mid_fn(st); };
-      } else {
-        jobs.push_back({P_C5, 0, mid_fn});
-      }
+      });
     }
+    if (!c5chain.empty())
+      jobs.push_back({P_C5, 0, [c5chain](cudaStream_t st) { for (auto& f : c5chain) f(st); }});
     if (n5l > 0) {
       int bps = 0;
       const char* shc_env = getenv("EVOKE_C5_SHCAP");  // developer knob: shared records per warp
-      const int sh_cap = shc_env ? std::max(64, std::min(C5_SH_CAP, atoi(shc_env))) : C5_SH_CAP;
+      // (whole-GPU passes: smaller shared regions, more warps resident)
+      const int sh_cap = shc_env ? std::max(64, std::min(C5_SH_CAP, atoi(shc_env))) : (whole_gpu_passes ? 64 : C5_SH_CAP_DEFAULT);
       const size_t sh_bytes = C5_SH_BYTES(sh_cap);
       CK(cudaFuncSetAttribute(k_c5_light, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_bytes));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_c5_light, C5_BT, sh_bytes));
       const char* lb_env = getenv("EVOKE_C5_LBPS");  // developer knob: light CTAs per SM
-      const int lg = std::max(1, std::min(bps, lb_env ? atoi(lb_env) : 4)) * SM;
+      const int lg = std::max(1, std::min(bps, lb_env ? atoi(lb_env) : (whole_gpu_passes ? 8 : 4))) * SM;
       const size_t nw = (size_t)lg * (C5_BT / 32);
       C5RecP* reg = A.zalloc<C5RecP>(nw * C5_WARP_CAP);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
-        k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lr, n5l, c5c + 5, reg, wl, C5out,
+        k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lr, n5l, c5c + 4, reg, wl, C5out,
                                                 sh_cap);
         C.launches++;
       }});
@@ -1413,7 +1426,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // kept streams 0..MAXJOBS-4 are the jobs'; the last three: main (no caller stream), tail
   // gathers, side
   if (jobs.size() > (size_t)Ctx::MAXJOBS - 3) { set_error("too many concurrent jobs"); throw EvokeError{EVOKE_EINTERNAL}; }
-  const bool serial = (o.flags & EVOKE_FLAG_SERIAL) != 0;
+  const bool serial = (o.flags & EVOKE_FLAG_SERIAL) != 0 || whole_gpu_passes;
+  C.serial_run = serial;
   if (C.side_used) CK(cudaStreamWaitEvent(C.st, C.ev_side, 0));
   CK(cudaEventRecord(C.ev_fork, C.st));
   for (size_t i = 0; i < jobs.size(); i++) {
@@ -1554,7 +1568,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     // passes reports its preparation (main stream) plus the span of its own kernels; the
     // overlap makes the per-pass times add up to more than ms_total
     s->ms_pass[P_CLIQ2] = 0;
-    const bool serial = (o.flags & EVOKE_FLAG_SERIAL) != 0;
+    const bool serial = C.serial_run;
     for (int pass : {P_PAIR, P_HUB, P_C5, P_CLIQ2}) {
       float lo = 1e30f, hi = -1e30f, sum = 0;
       for (int j = 0; j < C.njobs; j++) {

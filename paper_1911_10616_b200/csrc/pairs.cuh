@@ -45,7 +45,7 @@ struct PairOut {
   const int32_t* hub_slot;  // per vertex: row of its position map, or -1
   const int32_t* hub_pos;   // [slot][x]: position of x in N(hub) if x ~ hub, else -1
 };
-
+__device__ __forceinline__ void xadd(u64* field, int32_t x, u64 v) { atomicAdd(&field[x], v); }
 __device__ __forceinline__ int64_t slot_of_lo_in_hi(const DGraph& g, int32_t e) { return g.eslot_hi[e]; }
 __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) {
   const int32_t a = g.esrc[e];
@@ -251,10 +251,10 @@ __device__ __forceinline__ void pair_c_terms(const DGraph& g, const PairOut& o, 
   a36 += c2 * (u64)(int64_t)(dg_deg(g, x) - 2);
   a50 += c3;
   a63 += t63;
-  atomicAdd(&o.R8[x], c2);
-  atomicAdd(&o.R36[x], c2 * (du - 2));  // du >= w >= 2
-  if (c3) atomicAdd(&o.R50[x], c3);
-  if (t63) atomicAdd(&o.R63[x], t63);
+  xadd(o.R8, x, c2);
+  xadd(o.R36, x, c2 * (du - 2));  // du >= w >= 2
+  if (c3) xadd(o.R50, x, c3);
+  if (t63) xadd(o.R63, x, t63);
 }
 
 // ---- per-element work (shared by the warp and CTA engines) --------------------------
@@ -312,7 +312,7 @@ __device__ __forceinline__ void pass1_wedge(const DGraph& g, int64_t rb, int k, 
 __device__ __forceinline__ void wedge_x_side(const DGraph& g, const PairOut& o, int32_t x, int32_t v, int64_t t,
                                              int tuv, u64 w) {
   if (x < v) atomicAdd(&o.C4e[g.eid[t]], w - 1);
-  if (tuv) atomicAdd(&o.R51[x], (u64)tuv * (w - 1));
+  if (tuv) xadd(o.R51, x, (u64)tuv * (w - 1));
 }
 
 // Chords and diamonds, flattened on two levels.  Every lane brings at most one chord
@@ -894,7 +894,7 @@ __device__ __forceinline__ void s51_adjacent(const DGraph& g, const PairOut& o, 
     const u64 w = tab.get_w_or0(x);
     if (w < 2) continue;
     s51 -= w * (w - 1);
-    atomicAdd(&o.R51[x], (u64)0 - w * (w - 1));
+    xadd(o.R51, x, (u64)0 - w * (w - 1));
   }
 }
 
@@ -1024,11 +1024,12 @@ __global__ void __launch_bounds__(PAIR_BT, 3) k_pairs_main(DGraph g, const u32* 
                                                         const int32_t* __restrict__ mid, int n_mid,
                                                         const int32_t* __restrict__ light, int n_light,
                                                         const u32* __restrict__ est, int* __restrict__ counters,
-                                                        PairOut o, char* __restrict__ qmem, int qcap) {
+                                                        PairOut o_, char* __restrict__ qmem, int qcap) {
   extern __shared__ int32_t sh_pairs[];
   __shared__ EngSharedT<PAIR_BT / 32> E;
   __shared__ u64 red[8];
   __shared__ int s_idx;
+  const PairOut& o = o_;
   if (threadIdx.x < 8) red[threadIdx.x] = 0;
   if (threadIdx.x == 0) E.Q = eng_queue_at(qmem + (size_t)blockIdx.x * eng_queue_bytes(qcap), qcap);
   {
@@ -1078,11 +1079,12 @@ __global__ void __launch_bounds__(PAIR_BT, 3) k_pairs_main(DGraph g, const u32* 
 __global__ void __launch_bounds__(PAIR_MIDS_BT) k_pairs_mids(DGraph g, const u32* __restrict__ Te,
                                                              const int32_t* __restrict__ mids, int n_mids,
                                                              const u32* __restrict__ est, int* __restrict__ counter,
-                                                             PairOut o, char* __restrict__ qmem, int qcap) {
+                                                             PairOut o_, char* __restrict__ qmem, int qcap) {
   extern __shared__ int32_t sh_pairs[];
   __shared__ EngSharedT<PAIR_MIDS_BT / 32> E;
   __shared__ u64 red[8];
   __shared__ int s_idx;
+  const PairOut& o = o_;
   if (threadIdx.x < 8) red[threadIdx.x] = 0;
   if (threadIdx.x == 0) E.Q = eng_queue_at(qmem + (size_t)blockIdx.x * eng_queue_bytes(qcap), qcap);
   SharedPackedHash tab;
@@ -1107,11 +1109,12 @@ template <typename Word, bool SCAN>
 __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* __restrict__ Te,
                                                           const int32_t* __restrict__ srcs, int nsrc,
                                                           int* __restrict__ counter, Word* __restrict__ tabs,
-                                                          int32_t* __restrict__ lists, PairOut o,
+                                                          int32_t* __restrict__ lists, PairOut o_,
                                                           char* __restrict__ qmem, int qcap) {
   __shared__ EngSharedT<PAIR_HBT / 32> E;
   __shared__ u64 red[8];
   __shared__ int s_idx, s_ntouch;
+  const PairOut& o = o_;
   if (threadIdx.x == 0) E.Q = eng_queue_at(qmem + (size_t)blockIdx.x * eng_queue_bytes(qcap), qcap);
   GlobalDense<Word, SCAN> tab;
   constexpr int PER = GlobalDense<Word, SCAN>::PER;

@@ -17,6 +17,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 HEAVY_PAIR = {"EVOKE_PAIR_LIGHT_MAX": "0", "EVOKE_PAIR_MIDS_MAX": "0", "EVOKE_PAIR_MID_MAX": "0"}
+C5_BIG = {"EVOKE_C5_LIGHT_REC": "0", "EVOKE_C5_MID_REC": "0"}
 COMBOS = {
     "pair_u64_tables": {"EVOKE_PAIR_PACKED_LIM": "0"},                 # k_pairs_heavy<u64>
     "pair_dense_touched": dict(HEAVY_PAIR, EVOKE_PAIR_SWEEP="0"),      # k_pairs_heavy<u32, false>
@@ -25,14 +26,14 @@ COMBOS = {
     "pair_small_mid": {"EVOKE_PAIR_LIGHT_MAX": "0"},                  # k_pairs_mids
     "hub_heavy_shared": {"EVOKE_HUB_WARP_MAX": "0"},                  # hub_item_cta, shared table
     "hub_heavy_global": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_SH_DENSE": "0"},  # global tables
+    "c5_light_global": {"EVOKE_C5_SHCAP": "64"},                       # k_c5_light, global regions
     "c5_mid": {"EVOKE_C5_LIGHT_REC": "0"},                             # k_c5_mid
-    "c5_big_u32": {"EVOKE_C5_LIGHT_REC": "0", "EVOKE_C5_MID_REC": "0"},  # k_c5_heavy<u32> + bitmaps
-    "c5_big_u64": {"EVOKE_C5_LIGHT_REC": "0", "EVOKE_C5_MID_REC": "0", "EVOKE_C5_WIDE": "1"},
-    "c5_big_nobits": {"EVOKE_C5_LIGHT_REC": "0", "EVOKE_C5_MID_REC": "0", "EVOKE_C5_NO_BITS": "1"},
+    "c5_big_u32": dict(C5_BIG),                                        # k_c5_heavy<u32> + bitmaps
+    "c5_big_u64": dict(C5_BIG, EVOKE_C5_WIDE="1"),
+    "c5_big_nobits": dict(C5_BIG, EVOKE_C5_NO_BITS="1"),
     "c5_light_by_work": {"EVOKE_C5_LIGHT_WORK": "40", "EVOKE_C5_MID_WORK": "200"},
-    "all_heavy_sorted": dict(HEAVY_PAIR, EVOKE_PAIR_PACKED_LIM="0", EVOKE_HUB_WARP_MAX="0", EVOKE_HUB_SH_DENSE="0",
-                             EVOKE_C5_LIGHT_REC="0", EVOKE_C5_MID_REC="0", EVOKE_C5_WIDE="1",
-                             EVOKE_SORT_FULL_MIN="1"),
+    "all_heavy_sorted": dict(HEAVY_PAIR, **C5_BIG, EVOKE_PAIR_PACKED_LIM="0", EVOKE_HUB_WARP_MAX="0",
+                             EVOKE_HUB_SH_DENSE="0", EVOKE_C5_WIDE="1", EVOKE_SORT_FULL_MIN="1"),
 }
 
 
