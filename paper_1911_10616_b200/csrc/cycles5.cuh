@@ -117,13 +117,15 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 #define C5_SH_CAP 512             // light endpoints with a region of <= sh_cap (<= this) slots: shared memory
 #define C5_SH_CAP_DEFAULT 256
 #define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (sizeof(C5RecP) + 2 * 4))   // records + touched + J lists
-#define C5_SH_BYTES(cap) ((C5_BT / 32) * C5_SH_WARP_BYTES(cap))
+#define C5_SH_BYTES(cap) ((C5_BT / 32) * (C5_SH_WARP_BYTES(cap) + C5_FB_WARP * 4))
 #define C5_HBT 1024               // heavy-endpoint CTA
 #define C5_MID_MAX 4096           // mid endpoint: R(l) <= this ...
 #define C5_MID_WORK 65535         // ... and W(l) <= this (packed 16-bit record fields)
 #define C5_MID_CAP (2 * C5_MID_MAX)  // hashed records in a per-CTA global region (load <= 0.5)
 #define C5_MBT 128                // mid-endpoint CTA (several endpoints in flight per SM)
 #define C5_BITS_SMEM_MAX (160 << 10)  // heavy CTAs: shared first-touch bitmaps up to this size
+#define C5_FB_WARP 128            // i-key filter words per light warp (4096 bits)
+#define C5_FB_CTA 256             // i-key filter words per mid CTA (8192 bits)
 
 // dense records indexed by vertex id; touched list holds vertex ids
 template <typename Rec>
@@ -176,6 +178,7 @@ struct C5Dense {
     newj = !(atomicOr(&bJ[x >> 5], bit) & bit);
     return mark_nr(x, C5_J);
   }
+  __device__ __forceinline__ void note_i(int32_t) const {}
   // record of x if Wn[x] > 0 (step 3; Wn is final since step 1), else nullptr
   __device__ __forceinline__ Rec* peek_i(int32_t x) const {
     Rec* r = &R[x];
@@ -199,6 +202,18 @@ struct C5Hash {
   u32 mask;
   int32_t* L;
   int* nL;
+  // Bit filter of the i-keys (vertices with Wn > 0), in shared memory: step 3 looks up every
+  // path end i, most of which have no record (or Wn = 0), and a clear bit answers those
+  // without a probe of the (L2-resident) region.  fb == nullptr: no filter.
+  u32* fb = nullptr;
+  int fshift = 0;  // 32 - log2(filter bits)
+  __device__ __forceinline__ u32 hf(int32_t x) const { return ((u32)x * 0x85EBCA6Bu) >> fshift; }
+  __device__ __forceinline__ void note_i(int32_t x) {
+    if (fb) {
+      const u32 b = hf(x);
+      atomicOr(&fb[b >> 5], 1u << (b & 31));
+    }
+  }
   __device__ __forceinline__ u32 h0(int32_t x) const { return ((u32)x * 0x9E3779B1u) >> 7 & mask; }
   // find or claim the slot of x; the thread whose CAS claims it appends the slot to the
   // touched list (so no mark has to wait for the flags' old value to decide that)
@@ -250,6 +265,10 @@ struct C5Hash {
     }
   }
   __device__ __forceinline__ Rec* peek_i(int32_t x) const {
+    if (fb) {
+      const u32 b = hf(x);
+      if (!(fb[b >> 5] & (1u << (b & 31)))) return nullptr;
+    }
     Rec* r = peek(x);
     return (r && (r->wf & C5_WN_MASK)) ? r : nullptr;
   }
@@ -325,6 +344,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         if (i == l) return 0;
         auto* r = loc.mark_nr(i, C5_I);
         atomicAdd(&r->wf, 1u);  // Wn
+        loc.note_i(i);
         return 0;
       },
       [&](int, u64) {});
@@ -594,13 +614,17 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
   WarpEng eng;
   C5RecP* shR = reinterpret_cast<C5RecP*>(c5_sh + (size_t)wib * C5_SH_WARP_BYTES(sh_cap));
   int32_t* shL = reinterpret_cast<int32_t*>(shR + sh_cap);
+  u32* fb = reinterpret_cast<u32*>(c5_sh + (size_t)(C5_BT / 32) * C5_SH_WARP_BYTES(sh_cap)) + wib * C5_FB_WARP;
   {
     uint4* z = reinterpret_cast<uint4*>(shR);
     for (int i = lane; i < (int)(sh_cap * sizeof(C5RecP) / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = lane; i < C5_FB_WARP; i += 32) fb[i] = 0u;
   }
   __syncwarp();
   C5Hash<C5RecP> loc;
   loc.nL = &w_nL[wib];
+  loc.fb = fb;
+  loc.fshift = 32 - 12;  // 4096 bits
   for (;;) {
     int idx = 0;
     if (lane == 0) idx = atomicAdd(counter, 1);
@@ -624,6 +648,7 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
     c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &w_nJ[wib], &w_tot[wib], C5);
     if (lane == 0 && w_tot[wib]) atomicAdd(&C5[l], w_tot[wib]);
     c5_reset(eng, loc);
+    for (int i = lane; i < C5_FB_WARP; i += 32) fb[i] = 0u;
     __syncwarp();
   }
 }
@@ -652,6 +677,10 @@ __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restri
   loc.L = rlists + (size_t)blockIdx.x * 2 * C5_MID_CAP;
   int32_t* J = loc.L + C5_MID_CAP;
   loc.nL = &s_nL;
+  __shared__ u32 s_fb[C5_FB_CTA];
+  for (int i = threadIdx.x; i < C5_FB_CTA; i += blockDim.x) s_fb[i] = 0u;
+  loc.fb = s_fb;
+  loc.fshift = 32 - 13;  // 8192 bits
   for (;;) {
     if (threadIdx.x == 0) { s_idx = atomicAdd(counter, 1); s_nL = 0; s_nJ = 0; s_tot = 0; }
     __syncthreads();
@@ -662,6 +691,7 @@ __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restri
     c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &s_nJ, &s_tot, C5);
     if (threadIdx.x == 0 && s_tot) atomicAdd(&C5[l], s_tot);
     c5_reset(eng, loc);
+    for (int i = threadIdx.x; i < C5_FB_CTA; i += blockDim.x) s_fb[i] = 0u;
     __syncthreads();
   }
 }
