@@ -100,11 +100,38 @@ __device__ __forceinline__ void rec_zero(C5RecT<V>* r) {
 __device__ __forceinline__ void rec_zero(C5RecP* r) {
   r->key = 0; r->wf = 0u; r->qp = 0u; r->as = 0u; r->qtm = 0u;
 }
+// Record of the light endpoints (W(l) < 2^12, so every field fits 12 bits): 16 bytes, one
+// aligned half-sector, instead of 20 (which straddles sectors).  wf = Wn | Q << 12 | flags << 28;
+// rest = P | A << 12 | S << 24 | QT << 36 | QM << 48; step 3's P and A in one 64-bit atomic.
+struct __align__(16) C5RecL {
+  int32_t key;
+  u32 wf;
+  unsigned long long rest;
+};
+#define C5L_BITS 12
+#define C5L_MASK 0xfffull
+__device__ __forceinline__ void rec_add_q(C5RecL* r, u32 th, u32 tm) {
+  atomicAdd(&r->wf, 1u << C5L_BITS);
+  atomicAdd(&r->rest, ((u64)th << 36) | ((u64)tm << 48));
+}
+__device__ __forceinline__ u64 rec_q(const C5RecL* r) { return (u64)(r->wf >> C5L_BITS) & C5L_MASK; }
+__device__ __forceinline__ u64 rec_p(const C5RecL* r) { return r->rest & C5L_MASK; }
+__device__ __forceinline__ u64 rec_a(const C5RecL* r) { return (r->rest >> 12) & C5L_MASK; }
+__device__ __forceinline__ u64 rec_s(const C5RecL* r) { return (r->rest >> 24) & C5L_MASK; }
+__device__ __forceinline__ u64 rec_qt(const C5RecL* r) { return (r->rest >> 36) & C5L_MASK; }
+__device__ __forceinline__ u64 rec_qm(const C5RecL* r) { return (r->rest >> 48) & C5L_MASK; }
+__device__ __forceinline__ void rec_add_pa(C5RecL* r, u64 q, bool adj) {
+  atomicAdd(&r->rest, adj ? (q | (q << 12)) : q);
+}
+__device__ __forceinline__ void rec_add_s(C5RecL* r, u64 s) { atomicAdd(&r->rest, s << 24); }
+__device__ __forceinline__ void rec_zero(C5RecL* r) { *reinterpret_cast<uint4*>(r) = make_uint4(0, 0, 0, 0); }
+
 #define C5_WN_MASK 0x0fffffffu
 template <typename R>
 __device__ __forceinline__ u32 c5_flags(const R* r) { return r->wf >> 28; }
 template <typename R>
 __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MASK); }
+__device__ __forceinline__ u64 c5_wn(const C5RecL* r) { return (u64)(r->wf & (u32)C5L_MASK); }
 #define C5_ADJ 1u      // vertex is a neighbour of l
 #define C5_I 2u        // i-key (steps 1, 3)
 #define C5_J 4u        // j-key (step 2)
@@ -112,11 +139,11 @@ __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MA
 
 #define C5_BT 256
 #define C5_WARP_MAX 1024          // light endpoint: record bound R(l) <= this ...
-#define C5_WARP_WORK 8192         // ... and work W(l) <= this
+#define C5_WARP_WORK 4095         // ... and work W(l) <= this (12-bit record fields)
 #define C5_WARP_CAP (2 * C5_WARP_MAX)  // records per warp region (load <= 0.5; global only when EVOKE_C5_SHCAP < it)
 #define C5_SH_CAP 512             // light endpoints with a region of <= sh_cap (<= this) slots: shared memory
 #define C5_SH_CAP_DEFAULT 256
-#define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (sizeof(C5RecP) + 2 * 4))   // records + touched + J lists
+#define C5_SH_WARP_BYTES(cap) ((size_t)(cap) * (sizeof(C5RecL) + 2 * 4))   // records + touched + J lists
 #define C5_SH_BYTES(cap) ((C5_BT / 32) * (C5_SH_WARP_BYTES(cap) + C5_FB_WARP * 4))
 #define C5_HBT 1024               // heavy-endpoint CTA
 #define C5_MID_MAX 4096           // mid endpoint: R(l) <= this ...
@@ -270,7 +297,7 @@ struct C5Hash {
       if (!(fb[b >> 5] & (1u << (b & 31)))) return nullptr;
     }
     Rec* r = peek(x);
-    return (r && (r->wf & C5_WN_MASK)) ? r : nullptr;
+    return (r && c5_wn(r)) ? r : nullptr;
   }
   __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
     Rec* r = &R[L[t]];
@@ -596,13 +623,13 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
   }
 }
 
-// Light endpoints: one warp each, 32-byte records in a per-warp open-addressing region whose
+// Light endpoints: one warp each, 16-byte records in a per-warp open-addressing region whose
 // used part is sized per endpoint (2 x its record bound, so the records stay L2-resident).
 __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restrict__ Tlow,
                                                     const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                     const int32_t* __restrict__ light, const u32* __restrict__ lw,
                                                     int n_light, int* __restrict__ counter,
-                                                    C5RecP* __restrict__ wregions, int32_t* __restrict__ wlists,
+                                                    C5RecL* __restrict__ wregions, int32_t* __restrict__ wlists,
                                                     u64* __restrict__ C5, int sh_cap) {
   // endpoints whose region needs at most sh_cap (<= C5_SH_CAP) slots keep records and lists in shared
   // memory (per warp); larger ones use the warp's global region
@@ -612,16 +639,16 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t gw = (size_t)blockIdx.x * (C5_BT / 32) + wib;
   WarpEng eng;
-  C5RecP* shR = reinterpret_cast<C5RecP*>(c5_sh + (size_t)wib * C5_SH_WARP_BYTES(sh_cap));
+  C5RecL* shR = reinterpret_cast<C5RecL*>(c5_sh + (size_t)wib * C5_SH_WARP_BYTES(sh_cap));
   int32_t* shL = reinterpret_cast<int32_t*>(shR + sh_cap);
   u32* fb = reinterpret_cast<u32*>(c5_sh + (size_t)(C5_BT / 32) * C5_SH_WARP_BYTES(sh_cap)) + wib * C5_FB_WARP;
   {
     uint4* z = reinterpret_cast<uint4*>(shR);
-    for (int i = lane; i < (int)(sh_cap * sizeof(C5RecP) / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = lane; i < (int)(sh_cap * sizeof(C5RecL) / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
     for (int i = lane; i < C5_FB_WARP; i += 32) fb[i] = 0u;
   }
   __syncwarp();
-  C5Hash<C5RecP> loc;
+  C5Hash<C5RecL> loc;
   loc.nL = &w_nL[wib];
   loc.fb = fb;
   loc.fshift = 32 - 12;  // 4096 bits

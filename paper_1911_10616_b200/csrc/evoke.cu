@@ -1404,7 +1404,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const char* lb_env = getenv("EVOKE_C5_LBPS");  // developer knob: light CTAs per SM
       const int lg = std::max(1, std::min(bps, lb_env ? atoi(lb_env) : (whole_gpu_passes ? 8 : 4))) * SM;
       const size_t nw = (size_t)lg * (C5_BT / 32);
-      C5RecP* reg = A.zalloc<C5RecP>(nw * C5_WARP_CAP);
+      C5RecL* reg = A.zalloc<C5RecL>(nw * C5_WARP_CAP);
       int32_t* wl = A.alloc<int32_t>(nw * 2 * C5_WARP_CAP);
       jobs.push_back({P_C5, 4, [=, &C](cudaStream_t st) {
         k_c5_light<<<lg, C5_BT, sh_bytes, st>>>(g, Tlow, Tmid, Thigh, c5l, c5lr, n5l, c5c + 4, reg, wl, C5out,
