@@ -515,11 +515,17 @@ __global__ void k_wedges(const int64_t* __restrict__ rp, int32_t n, u64* out) {
 // clique bins by k = d+(u): bin 0: 3..32, 1: 33..128, 2: 129..512, 3: 513..1024, 4: >1024
 __global__ void k_clique_bins(const int64_t* __restrict__ orow, int32_t n, int32_t* __restrict__ lists,
                               int* __restrict__ counts) {
-  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    const int64_t k = orow[u + 1] - orow[u];
-    if (k < 3) continue;
-    const int b = k <= 32 ? 0 : k <= 128 ? 1 : k <= 512 ? 2 : k <= 1024 ? 3 : 4;
-    lists[(int64_t)b * n + atomicAdd(&counts[b], 1)] = u;
+  // warp-aggregated appends (one atomic per warp and bin, not per vertex: 2M vertices
+  // appending to one counter serialise on it)
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = (int32_t)(base + (threadIdx.x & 31));
+    int b = -1;
+    if (u < n) {
+      const int64_t k = orow[u + 1] - orow[u];
+      if (k >= 3) b = k <= 32 ? 0 : k <= 128 ? 1 : k <= 512 ? 2 : k <= 1024 ? 3 : 4;
+    }
+    for (int t = 0; t < 5; t++) warp_append(b == t, u, lists + (int64_t)t * n, counts + t);
   }
 }
 
@@ -1198,20 +1204,24 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* light = A.alloc<int32_t>(m2s);
     int32_t* heavy = A.alloc<int32_t>(m2s);
     u32* hest = A.alloc<u32>(m2s);
-    int* hcnt = A.alloc<int>(4, true);  // n_light, n_heavy, process counters [2], [3]
+    int* hcnt = A.alloc<int>(5, true);  // n_light, n_heavy, process counters [2], [3], n_micro [4]
+    int32_t* micro = A.alloc<int32_t>(m2s);
     u64* hitem_est = A.alloc<u64>(m2s, true);
     if (ntri > 0)
       k_hub_est<<<grid_for(ntri, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est);
     const uint8_t* hmine = shard_mask(A, C, hitem_est, m2s, si, ns, d_work + 2);
-    k_hub_bin<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est, hmine, env_cap("EVOKE_HUB_WARP_MAX", HUB_WARP_MAX),
-                                                        light, hcnt, heavy, hest, hcnt + 1);
+    const u64 hub_warp_max = env_cap("EVOKE_HUB_WARP_MAX", HUB_WARP_MAX);
+    const u64 hub_micro_max = std::min(hub_warp_max, env_cap("EVOKE_HUB_MICRO_MAX", HUB_MICRO_MAX));
+    k_hub_bin<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est, hmine, hub_micro_max, hub_warp_max, micro,
+                                                        hcnt + 4, light, hcnt, heavy, hest, hcnt + 1);
     C.launches += 2;
-    int hc[2];
+    int hc[5];
     CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     C.tick("hub_items+sync");
-    const int n_light = hc[0], n_heavy = hc[1];
-    if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] hub items: light %d heavy %d\n", n_light, n_heavy);
+    const int n_light = hc[0], n_heavy = hc[1], n_micro = hc[4];
+    if (getenv("EVOKE_DEBUG"))
+      fprintf(stderr, "[evoke] hub items: micro %d light %d heavy %d\n", n_micro, n_light, n_heavy);
     int32_t* heavy_sorted = heavy;
     if (n_heavy > 1) {
       int32_t* hs = A.alloc<int32_t>(n_heavy);
@@ -1246,6 +1256,14 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       jobs.push_back({P_HUB, 2, [=, &C](cudaStream_t st) {
         k_hub_process<<<hg, HUB_BT, HUB_SMEM, st>>>(g, Te, heavy_sorted, n_heavy, light, n_light, hcnt + 2, gt, gl,
                                                     r68, r69, sh_dense_max);
+        if (n_micro > 0) k_hub_micro<<<grid_for(n_micro, 128, SM), 128, 0, st>>>(g, micro, n_micro, r68, r69);
+        C.launches += 1 + (n_micro > 0);
+      }});
+    } else if (n_micro > 0) {
+      u64* r68 = Fp(F_R68);
+      u64* r69 = Fp(F_R69);
+      jobs.push_back({P_HUB, 2, [=, &C](cudaStream_t st) {
+        k_hub_micro<<<grid_for(n_micro, 128, SM), 128, 0, st>>>(g, micro, n_micro, r68, r69);
         C.launches++;
       }});
     }
@@ -1282,7 +1300,6 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     const int n5l = hc5[0], n5m = hc5[1], n5b = hc5[2];
     int32_t* c5l = c5lists;
     u32* c5lr = c5rb;
-    int32_t* c5b = c5lists + (size_t)2 * n;
     if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d mid %d big %d\n", n5l, n5m, n5b);
     if (getenv("EVOKE_C5_HIST")) {  // developer: W / R histogram of every endpoint
       std::vector<u64> hw(n), hr(n);
@@ -1328,28 +1345,29 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       rs = ro;
     };
     std::vector<std::function<void(cudaStream_t)>> c5chain;  // big, then mid: one stream
+    // big endpoints, W descending; returns W max
+    auto sort_big = [&](int cnt, int32_t*& bs) -> u64 {
+      int32_t* src = c5lists + (size_t)2 * n;
+      bs = src;
+      if (cnt <= 1) return d2h_scalar<u64>(c5bw, C.st);
+      bs = A.alloc<int32_t>(cnt);
+      u64* bk = A.alloc<u64>(cnt);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c5bw, bk, src, bs, cnt, 0, 64, C.st));
+      void* t2 = A.alloc<char>(tb);
+      CK(cub::DeviceRadixSort::SortPairsDescending(t2, tb, c5bw, bk, src, bs, cnt, 0, 64, C.st));
+      C.lib_launches += 4;
+      return d2h_scalar<u64>(bk, C.st);
+    };
+    const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: big-endpoint CTAs
+    const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
     if (n5b > 0) {
-      // big endpoints, W descending
-      int32_t* bs = c5b;
-      u64 wmax = 0;
-      if (n5b > 1) {
-        bs = A.alloc<int32_t>(n5b);
-        u64* bk = A.alloc<u64>(n5b);
-        size_t tb = 0;
-        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c5bw, bk, c5b, bs, n5b, 0, 64, C.st));
-        void* t = A.alloc<char>(tb);
-        CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, c5bw, bk, c5b, bs, n5b, 0, 64, C.st));
-        C.lib_launches += 4;
-        wmax = d2h_scalar<u64>(bk, C.st);
-      } else {
-        wmax = d2h_scalar<u64>(c5bw, C.st);
-      }
+      int32_t* bs = nullptr;
+      const u64 wmax = sort_big(n5b, bs);
       // u32 record fields when every big endpoint's W < 2^32 (every field is <= W(l))
       const bool narrow = wmax < (1ull << 32) && !getenv("EVOKE_C5_WIDE");
       const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
       const int64_t per = (int64_t)n * (int64_t)(rec + 8);
-      const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: big-endpoint CTAs
-      const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
       const int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, n5b), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
       char* dense = A.zalloc<char>((size_t)hg * n * rec);
       int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);

@@ -34,6 +34,7 @@
 #define HUB_SMEM (HUB_BT / 32 * HUB_WARP_CAP * 12)   // 96 KB dynamic shared memory
 #define HUB_SH_DENSE (HUB_SMEM / 8)                  // heavy item: shared table if d(v) <= this
 #define HUB_FEW_ITEMS 262144                         // at most this many items: one CTA per SM
+#define HUB_MICRO_MAX 16                             // micro item: est <= this, one THREAD per item
 
 // number of entries of the full list [f, f+len) with third vertex < bound: a binary search
 // when the lists are sorted (g.full_sorted), else the whole list (callers then filter)
@@ -65,10 +66,12 @@ __global__ void k_hub_est(DGraph g, const u32* __restrict__ Te, u64* __restrict_
 }
 
 // items (slot s of a in N(v)) with T(v,a) >= 2 and est > 0, of this shard (mine[s], nullptr:
-// every item): light (est <= warp_max <= HUB_WARP_MAX) or heavy (with est for the sort)
+// every item): micro (est <= micro_max <= HUB_MICRO_MAX), light (est <= warp_max <=
+// HUB_WARP_MAX) or heavy (with est for the sort)
 __global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __restrict__ est,
-                          const uint8_t* __restrict__ mine, u64 warp_max, int32_t* __restrict__ light, int* n_light,
-                          int32_t* __restrict__ heavy, u32* __restrict__ heavy_est, int* n_heavy) {
+                          const uint8_t* __restrict__ mine, u64 micro_max, u64 warp_max, int32_t* __restrict__ micro,
+                          int* n_micro, int32_t* __restrict__ light, int* n_light, int32_t* __restrict__ heavy,
+                          u32* __restrict__ heavy_est, int* n_heavy) {
   const int lane = threadIdx.x & 31;
   const int64_t m2 = 2 * g.m;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < m2;
@@ -79,7 +82,8 @@ __global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __res
       const int32_t eva = g.eid[s];
       if (Te[eva] >= 2 && (!mine || mine[s])) e = est[s];
     }
-    warp_append(e > 0 && e <= warp_max, (int32_t)s, light, n_light);
+    warp_append(e > 0 && e <= micro_max, (int32_t)s, micro, n_micro);
+    warp_append(e > micro_max && e <= warp_max, (int32_t)s, light, n_light);
     const bool is_heavy = e > warp_max;
     const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
     if (bal) {
@@ -92,6 +96,69 @@ __global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __res
         heavy[q] = (int32_t)s;
         heavy_est[q] = (u32)min(e, (u64)0xffffffffu);
       }
+    }
+  }
+}
+
+// ---- micro item: one thread ------------------------------------------------------------
+// Items with est <= HUB_MICRO_MAX (most items of a sparse graph: config 4 averages 4.5 inner
+// visits per item) are too small for a warp: one lane per item keeps its (b, x) pairs in a
+// local array and counts c(x) by comparison, so a warp works on 32 items at once.
+__global__ void k_hub_micro(DGraph g, const int32_t* __restrict__ items, int n_items, u64* __restrict__ R68,
+                            u64* __restrict__ R69) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_items; q += gridDim.x * blockDim.x) {
+    const int32_t s = items[q];
+    const int32_t eva = g.eid[s];
+    const int32_t a = g.ci[s];
+    const int32_t lo_ = g.esrc[eva];
+    const int32_t v = lo_ + g.edst[eva] - a;
+    const bool v_lo = lo_ == v;
+    const int64_t fa = g.foff[eva];
+    const int na = full_prefix(g, fa, (int)(g.foff[eva + 1] - fa), a);  // b < a (or all, filtered)
+    int32_t xs[HUB_MICRO_MAX];
+    int8_t xb[HUB_MICRO_MAX];
+    int32_t bs[HUB_MICRO_MAX];
+    int cnt = 0, nb = 0;
+    for (int i = 0; i < na; i++) {
+      const int64_t r = fa + i;
+      const int32_t b = g.fx[r];
+      if (b >= a) continue;
+      const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
+      const int64_t fb = g.foff[evb];
+      const int len = full_prefix(g, fb, (int)(g.foff[evb + 1] - fb), a);  // x < a
+      for (int k = 0; k < len; k++) {
+        const int32_t x = g.fx[fb + k];
+        if (x >= a) continue;
+        xs[cnt] = x;  // cnt <= est(v,a) <= HUB_MICRO_MAX
+        xb[cnt] = (int8_t)nb;
+        cnt++;
+      }
+      bs[nb++] = b;  // T(v,b) >= 1 (a is a common neighbour), so nb <= est
+    }
+    u64 sb[HUB_MICRO_MAX];
+    for (int t = 0; t < nb; t++) sb[t] = 0;
+    u64 r69 = 0;
+    for (int p = 0; p < cnt; p++) {
+      int c = 0;
+      bool first = true;
+      for (int t = 0; t < cnt; t++) {
+        if (xs[t] == xs[p]) {
+          c++;
+          if (t < p) first = false;
+        }
+      }
+      sb[xb[p]] += (u64)(c - 1);  // R68[b] += c(x) - 1 for every x of b
+      if (first && c >= 2) {
+        const u64 c2 = binom2((u64)c);
+        r69 += c2;
+        atomicAdd(&R68[xs[p]], c2);
+      }
+    }
+    for (int t = 0; t < nb; t++)
+      if (sb[t]) atomicAdd(&R68[bs[t]], sb[t]);
+    if (r69) {
+      atomicAdd(&R69[v], r69);
+      atomicAdd(&R68[a], r69);
     }
   }
 }

@@ -24,6 +24,7 @@ COMBOS = {
     "pair_dense_swept": dict(HEAVY_PAIR, EVOKE_PAIR_SWEEP="1"),        # k_pairs_heavy<u32, true>
     "pair_mid": {"EVOKE_PAIR_LIGHT_MAX": "0", "EVOKE_PAIR_MIDS_MAX": "0"},  # k_pairs_main CTA tier
     "pair_small_mid": {"EVOKE_PAIR_LIGHT_MAX": "0"},                  # k_pairs_mids
+    "hub_warp": {"EVOKE_HUB_MICRO_MAX": "0"},                         # hub_item_warp (no micro items)
     "hub_heavy_shared": {"EVOKE_HUB_WARP_MAX": "0"},                  # hub_item_cta, shared table
     "hub_heavy_global": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_SH_DENSE": "0"},  # global tables
     "c5_light_global": {"EVOKE_C5_SHCAP": "64"},                       # k_c5_light, global regions
