@@ -34,6 +34,107 @@ __device__ __forceinline__ int row_rank(const u32* __restrict__ R, int W, int i,
   return r;
 }
 
+// One row i of the bitmap S of G[N+(u)] (k local vertices, W words per row): lanes take the
+// columns j; the credits of L_i, of the local edges and triangles through i, and u's own
+// sums (acc_u0, acc_u1; per lane, the caller reduces them).
+template <int MODE>
+__device__ __forceinline__ void clique_row(const DGraph& g, const u32* S, int W, int k, int64_t ou, int i,
+                                           int lane, bool do_k4, bool do_k5, const u32* __restrict__ Te,
+                                           u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
+                                           u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70,
+                                           u64& acc_u0, u64& acc_u1) {
+  const u32* Si = S + (int64_t)i * W;
+  const int32_t Li = g.ocol[ou + i];
+  u64 a0 = 0, a1 = 0, a2 = 0;  // per-i accumulators
+  const int64_t qi0 = g.toff[ou + i];
+  for (int j = lane; j < k; j += 32) {
+    if (!((Si[j >> 5] >> (j & 31)) & 1u)) continue;
+    const u32* Sj = S + (int64_t)j * W;
+    if (MODE == 0) {
+      for (int w = (j >> 5); w < W; w++) {
+        const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+        if (do_k4) a0 += __popc(x);
+        if (do_k5)
+          for_each_bit(x, w << 5, [&](int l) {
+            const u32* Sl = S + (int64_t)l * W;
+            u64 c = 0;
+            for (int w2 = (l >> 5); w2 < W; w2++) c += __popc(Si[w2] & Sj[w2] & Sl[w2] & gt_mask(l, w2));
+            a1 += c;
+          });
+      }
+      if (do_k4 && j > i) {
+        u32 c = 0;
+        for (int w = 0; w < W; w++) c += __popc(Si[w] & Sj[w]);
+        const int64_t qij = qi0 + row_rank(Si, W, i, j);
+        const int32_t eij = g.tbc[qij];
+        if (c) {
+          atomicAdd(&K4e[eij], (u64)c);
+          atomicAdd(&K4t[qij], c);
+        }
+        // local triangles (i<j<l): triangle (L_i, L_j, L_l) gets apex u below it
+        int64_t lo = g.toff[eij];
+        const int64_t hi = g.toff[eij + 1];
+        for (int w = (j >> 5); w < W; w++) {
+          const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+          for_each_bit(x, w << 5, [&](int l) {
+            const int32_t Ll = g.ocol[ou + l];
+            const int64_t pos = lower_bound_dev<int32_t>(g.tc, lo, hi, Ll);
+            atomicAdd(&K4t[pos], 1u);
+            lo = pos + 1;
+          });
+        }
+      }
+    } else {
+      // theta66 / theta70 credits to L_i over the local edges (j,l) inside S_i
+      const u64 te_uj = Te[ou + j];
+      const int64_t qj0 = g.toff[ou + j];
+      for (int w = (j >> 5); w < W; w++) {
+        const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+        for_each_bit(x, w << 5, [&](int l) {
+          const int64_t qjl = qj0 + row_rank(Sj, W, j, l);
+          a0 += te_uj + (u64)Te[ou + l] + (u64)Te[g.tbc[qjl]];
+          a1 += (u64)K4t[qjl] - 1ull;
+        });
+      }
+      if (j > i) {
+        u32 c = 0;
+        for (int w = 0; w < W; w++) c += __popc(Si[w] & Sj[w]);
+        const int64_t qij = qi0 + row_rank(Si, W, i, j);
+        const int32_t eij = g.tbc[qij];
+        acc_u0 += (u64)Te[eij] * (u64)c;
+        int64_t lo = g.toff[eij];
+        const int64_t hi = g.toff[eij + 1];
+        for (int w = (j >> 5); w < W; w++) {
+          const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
+          for_each_bit(x, w << 5, [&](int l) {
+            const int32_t Ll = g.ocol[ou + l];
+            const int64_t pos = lower_bound_dev<int32_t>(g.tc, lo, hi, Ll);
+            acc_u1 += (u64)K4t[pos] - 1ull;
+            lo = pos + 1;
+          });
+        }
+      }
+    }
+  }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  (void)a2;
+  if (lane == 0) {
+    if (MODE == 0) {
+      if (do_k4 && a0) {
+        atomicAdd(&K4v[Li], a0);
+        atomicAdd(&K4e[ou + i], a0);
+      }
+      if (do_k5 && a1) atomicAdd(&K5v[Li], a1);
+      acc_u0 += a0;
+      acc_u1 += a1;
+    } else {
+      if (a0) atomicAdd(&R66[Li], a0);
+      if (a1) atomicAdd(&R70[Li], a1);
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cliques(
     DGraph g, const int32_t* __restrict__ ulist, int nu, int smem_words, u32* __restrict__ gscratch,
@@ -65,98 +166,8 @@ __global__ void __launch_bounds__(256) k_cliques(
     }
     __syncthreads();
     u64 acc_u0 = 0, acc_u1 = 0;  // u's own credits (MODE 0: 3*#K4 and 4*#K5; MODE 1: th66, th70)
-    for (int i = wib; i < k; i += nwb) {
-      const u32* Si = S + (int64_t)i * W;
-      const int32_t Li = g.ocol[ou + i];
-      u64 a0 = 0, a1 = 0, a2 = 0;  // per-i accumulators
-      const int64_t qi0 = g.toff[ou + i];
-      for (int j = lane; j < k; j += 32) {
-        if (!((Si[j >> 5] >> (j & 31)) & 1u)) continue;
-        const u32* Sj = S + (int64_t)j * W;
-        if (MODE == 0) {
-          for (int w = (j >> 5); w < W; w++) {
-            const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
-            if (do_k4) a0 += __popc(x);
-            if (do_k5)
-              for_each_bit(x, w << 5, [&](int l) {
-                const u32* Sl = S + (int64_t)l * W;
-                u64 c = 0;
-                for (int w2 = (l >> 5); w2 < W; w2++) c += __popc(Si[w2] & Sj[w2] & Sl[w2] & gt_mask(l, w2));
-                a1 += c;
-              });
-          }
-          if (do_k4 && j > i) {
-            u32 c = 0;
-            for (int w = 0; w < W; w++) c += __popc(Si[w] & Sj[w]);
-            const int64_t qij = qi0 + row_rank(Si, W, i, j);
-            const int32_t eij = g.tbc[qij];
-            if (c) {
-              atomicAdd(&K4e[eij], (u64)c);
-              atomicAdd(&K4t[qij], c);
-            }
-            // local triangles (i<j<l): triangle (L_i, L_j, L_l) gets apex u below it
-            int64_t lo = g.toff[eij];
-            const int64_t hi = g.toff[eij + 1];
-            for (int w = (j >> 5); w < W; w++) {
-              const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
-              for_each_bit(x, w << 5, [&](int l) {
-                const int32_t Ll = g.ocol[ou + l];
-                const int64_t pos = lower_bound_dev<int32_t>(g.tc, lo, hi, Ll);
-                atomicAdd(&K4t[pos], 1u);
-                lo = pos + 1;
-              });
-            }
-          }
-        } else {
-          // theta66 / theta70 credits to L_i over the local edges (j,l) inside S_i
-          const u64 te_uj = Te[ou + j];
-          const int64_t qj0 = g.toff[ou + j];
-          for (int w = (j >> 5); w < W; w++) {
-            const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
-            for_each_bit(x, w << 5, [&](int l) {
-              const int64_t qjl = qj0 + row_rank(Sj, W, j, l);
-              a0 += te_uj + (u64)Te[ou + l] + (u64)Te[g.tbc[qjl]];
-              a1 += (u64)K4t[qjl] - 1ull;
-            });
-          }
-          if (j > i) {
-            u32 c = 0;
-            for (int w = 0; w < W; w++) c += __popc(Si[w] & Sj[w]);
-            const int64_t qij = qi0 + row_rank(Si, W, i, j);
-            const int32_t eij = g.tbc[qij];
-            acc_u0 += (u64)Te[eij] * (u64)c;
-            int64_t lo = g.toff[eij];
-            const int64_t hi = g.toff[eij + 1];
-            for (int w = (j >> 5); w < W; w++) {
-              const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
-              for_each_bit(x, w << 5, [&](int l) {
-                const int32_t Ll = g.ocol[ou + l];
-                const int64_t pos = lower_bound_dev<int32_t>(g.tc, lo, hi, Ll);
-                acc_u1 += (u64)K4t[pos] - 1ull;
-                lo = pos + 1;
-              });
-            }
-          }
-        }
-      }
-      a0 = warp_sum(a0);
-      a1 = warp_sum(a1);
-      (void)a2;
-      if (lane == 0) {
-        if (MODE == 0) {
-          if (do_k4 && a0) {
-            atomicAdd(&K4v[Li], a0);
-            atomicAdd(&K4e[ou + i], a0);
-          }
-          if (do_k5 && a1) atomicAdd(&K5v[Li], a1);
-          acc_u0 += a0;
-          acc_u1 += a1;
-        } else {
-          if (a0) atomicAdd(&R66[Li], a0);
-          if (a1) atomicAdd(&R70[Li], a1);
-        }
-      }
-    }
+    for (int i = wib; i < k; i += nwb)
+      clique_row<MODE>(g, S, W, k, ou, i, lane, do_k4, do_k5, Te, K4t, K4v, K4e, K5v, R66, R70, acc_u0, acc_u1);
     // block reduction of u's credits
     acc_u0 = warp_sum(acc_u0);
     acc_u1 = warp_sum(acc_u1);
@@ -177,5 +188,54 @@ __global__ void __launch_bounds__(256) k_cliques(
       red[0][0] = 0; red[0][1] = 0;
     }
     __syncthreads();
+  }
+}
+
+// Units with k = d+(u) <= 32 (one bitmap word per row): one WARP per unit instead of a CTA,
+// the rows in a per-warp 32-word slice of shared memory (most units of a sparse graph:
+// config 4 has degeneracy 8, so every unit is this small and a CTA per unit spent its time
+// in barriers).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_cliques_warp(
+    DGraph g, const int32_t* __restrict__ ulist, int nu, int do_k4, const uint8_t* __restrict__ mine,
+    const u32* __restrict__ Te, u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
+    u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70) {
+  __shared__ u32 sh_rows[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  u32* S = sh_rows[wib & 7];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t idx = gw; idx < nu; idx += nw) {
+    const int32_t u = ulist[idx];
+    const bool in_shard = !mine || mine[u];
+    const bool do_k5 = (MODE == 0) && in_shard;
+    if (MODE == 0 && !do_k4 && !do_k5) continue;
+    if (MODE == 1 && !in_shard) continue;
+    const int64_t ou = g.orow[u];
+    const int k = (int)(g.orow[u + 1] - ou);  // <= 32
+    S[lane] = 0u;
+    __syncwarp();
+    const int64_t q0 = g.toff[ou], q1 = g.toff[ou + k];
+    for (int64_t q = q0 + lane; q < q1; q += 32) {
+      const int i = (int)(g.tab[q] - ou), j = (int)(g.tac[q] - ou);
+      atomicOr(&S[i], 1u << j);
+      atomicOr(&S[j], 1u << i);
+    }
+    __syncwarp();
+    u64 acc_u0 = 0, acc_u1 = 0;
+    for (int i = 0; i < k; i++)
+      clique_row<MODE>(g, S, 1, k, ou, i, lane, do_k4, do_k5, Te, K4t, K4v, K4e, K5v, R66, R70, acc_u0, acc_u1);
+    acc_u0 = warp_sum(acc_u0);
+    acc_u1 = warp_sum(acc_u1);
+    if (lane == 0) {
+      if (MODE == 0) {
+        if (do_k4 && acc_u0) atomicAdd(&K4v[u], acc_u0 / 3);  // each local triangle counted at its 3 vertices
+        if (do_k5 && acc_u1) atomicAdd(&K5v[u], acc_u1 / 4);  // each local 4-clique counted at its 4 vertices
+      } else {
+        if (acc_u0) atomicAdd(&R66[u], acc_u0);
+        if (acc_u1) atomicAdd(&R70[u], acc_u1);
+      }
+    }
+    __syncwarp();
   }
 }

@@ -986,6 +986,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const size_t smem = (size_t)words * sizeof(u32);
       const int block = b == 0 ? 64 : (b == 1 ? 128 : 256);
       int grid = b < 4 ? std::min(hcounts[b], SM * 16) : cscratch_grid;
+      if (b == 0) {  // k <= 32: a warp per unit
+        const int wg = std::max(1, std::min((hcounts[0] + 7) / 8, SM * 8));
+        if (mode == 0)
+          k_cliques_warp<0><<<wg, 256, 0, lst>>>(g, cbins, hcounts[0], 1, cmine, Te, K4t, Fp(F_K4), K4e, Fp(F_K5),
+                                                 nullptr, nullptr);
+        else
+          k_cliques_warp<1><<<wg, 256, 0, lst>>>(g, cbins, hcounts[0], 0, cmine, Te, K4t, nullptr, nullptr, nullptr,
+                                                 Fp(F_R66), Fp(F_R70));
+        C.launches++;
+        continue;
+      }
       if (mode == 0) {
         if (smem > 48 * 1024)
           CK(cudaFuncSetAttribute(k_cliques<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
