@@ -1064,7 +1064,14 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* plists = A.alloc<int32_t>((size_t)PT_COUNT * n);
     int* tiers = A.alloc<int>(8, true);
     int32_t* hstar = A.alloc<int32_t>(n);
-    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, pk, pv, hstar);
+    u32* pwest = A.alloc<u32>(n);
+    u64* dwork = nullptr;
+    if (ntri > 0 && !getenv("EVOKE_PAIR_NO_DWORK")) {  // (env: developer A/B)
+      dwork = A.alloc<u64>(n, true);
+      k_pair_dwork<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, Te, dwork);
+      C.launches++;
+    }
+    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, dwork, pk, pv, pwest, hstar);
     C.tick("pair_est");
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 32, C.st));
@@ -1077,7 +1084,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     ptiers.mids_max = env_cap("EVOKE_PAIR_MIDS_MAX", PAIR_MIDS_MAX);
     ptiers.mid_max = env_cap("EVOKE_PAIR_MID_MAX", PAIR_MID_MAX);
     ptiers.sweep = getenv("EVOKE_PAIR_SWEEP") ? atoi(getenv("EVOKE_PAIR_SWEEP")) : -1;
-    k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, ptiers, Fp(F_T), pest, plists, tiers);
+    k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, ptiers, Fp(F_T), pwest, pest, plists, tiers);
     k_shard_sum_u32<<<grid_for(n, B, SM), B, 0, C.st>>>(pk2, n, si, ns, d_work + 0);
     C.launches += 3;
     C.lib_launches += 4;

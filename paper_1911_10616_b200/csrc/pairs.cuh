@@ -1136,11 +1136,26 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
   }
 }
 
-// Work estimate of source u: est(u) = sum_{v in N(u), v != h*} |{x in N(v) : x > u}|, the
+// Diamond work of every source u: D(u) = sum over the triangles (u, v, w) of T(v, w), the
+// diamond elements its chords lead to.  One thread per triangle, three atomics (a triangle
+// a, b, c gives T(b,c) to a, T(a,c) to b and T(a,b) to c).
+__global__ void k_pair_dwork(DGraph g, const u32* __restrict__ Te, u64* __restrict__ dwork) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.ntri; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t eab = g.tab[q], eac = g.tac[q], ebc = g.tbc[q];
+    atomicAdd((unsigned long long*)&dwork[g.esrc[eab]], (u64)Te[ebc]);
+    atomicAdd((unsigned long long*)&dwork[g.edst[eab]], (u64)Te[eac]);
+    atomicAdd((unsigned long long*)&dwork[g.tc[q]], (u64)Te[eab]);
+  }
+}
+
+// Work estimate of source u: west(u) = sum_{v in N(u), v != h*} |{x in N(v) : x > u}|, the
 // wedge elements walked (>= the number of table keys: every diamond end is also the end of a
-// walked wedge).  h*(u) = the neighbour with the longest such suffix (ties: lower id).
-__global__ void k_pair_est(DGraph g, u32* __restrict__ keys, int32_t* __restrict__ vals,
-                           int32_t* __restrict__ hstar) {
+// walked wedge), and the sort key ~(west + D(u)) (D: the diamond work, nullptr: none), so
+// the tiers and the heaviest-first order see the chords' diamond lists too (a source with
+// few wedges can own long diamond lists).  h*(u) = the neighbour with the longest such suffix
+// (ties: lower id).
+__global__ void k_pair_est(DGraph g, const u64* __restrict__ dwork, u32* __restrict__ keys,
+                           int32_t* __restrict__ vals, u32* __restrict__ west, int32_t* __restrict__ hstar) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1164,8 +1179,10 @@ __global__ void k_pair_est(DGraph g, u32* __restrict__ keys, int32_t* __restrict
     }
     if (lane == 0) {
       const u64 est = best >= 0 ? s - (u64)bestl : 0;
-      keys[u] = ~(u32)min(est, (u64)0xffffffffu);  // ascending sort = descending estimate
+      const u64 tot = est > 0 ? est + (dwork ? dwork[u] : 0) : 0;
+      keys[u] = ~(u32)min(tot, (u64)0xffffffffu);  // ascending sort = descending estimate
       vals[u] = u;
+      west[u] = (u32)min(est, (u64)0xffffffffu);
       hstar[u] = best;
     }
   }
@@ -1183,8 +1200,8 @@ struct PairTiers {
   int sweep;       // -1: by size (2-hop set >= n/16), 0: never, 1: always sweep the table
 };
 __global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const int32_t* __restrict__ svals,
-                                int si, int ns, PairTiers pt, const u64* __restrict__ Tv, u32* __restrict__ est_v,
-                                int32_t* __restrict__ lists, int* __restrict__ counts) {
+                                int si, int ns, PairTiers pt, const u64* __restrict__ Tv, const u32* __restrict__ west,
+                                u32* __restrict__ est_v, int32_t* __restrict__ lists, int* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1194,11 +1211,12 @@ __global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const i
     int32_t u = 0;
     if (p < g.n && p % ns == si) {
       u = svals[p];
-      const u64 e = (u64)(u32)~skeys[p];
-      est_v[u] = (u32)min(e, (u64)0xffffffffu);
-      if (e > 0) {
+      const u64 e = (u64)(u32)~skeys[p];  // wedges + diamonds: the tier
+      const u64 ew = west[u];             // wedges: bounds the table keys
+      est_v[u] = (u32)ew;
+      if (ew > 0) {
         const bool packed_ok = (u64)dg_deg(g, u) < pt.packed_lim && Tv[u] < pt.packed_lim;
-        const bool sweep = pt.sweep < 0 ? e * 16 >= (u64)g.n : pt.sweep > 0;
+        const bool sweep = pt.sweep < 0 ? ew * 16 >= (u64)g.n : pt.sweep > 0;
         tier = !packed_ok ? PT_G64
              : e <= pt.light_max ? PT_LIGHT
              : e <= pt.mids_max ? PT_MIDS
