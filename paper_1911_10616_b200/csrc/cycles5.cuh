@@ -56,6 +56,19 @@ struct __align__(4) C5RecP {
   u32 qtm;  // QT | QM << 16
 };
 // field access for both layouts
+// Q += 1, QT += th, QM += tm, returning whether this was the record's first j-mark (Q was 0)
+template <typename V>
+__device__ __forceinline__ bool rec_add_q_first(C5RecT<V>* r, u32 th, u32 tm) {
+  const V old = atomicAdd(&r->Q, (V)1);
+  atomicAdd(&r->QT, (V)th);
+  atomicAdd(&r->QM, (V)tm);
+  return old == 0;
+}
+__device__ __forceinline__ bool rec_add_q_first(C5RecP* r, u32 th, u32 tm) {
+  const u32 old = atomicAdd(&r->qp, 1u);
+  atomicAdd(&r->qtm, th | (tm << 16));
+  return (old & 0xffffu) == 0;
+}
 template <typename V>
 __device__ __forceinline__ void rec_add_q(C5RecT<V>* r, u32 th, u32 tm) {
   atomicAdd(&r->Q, (V)1);
@@ -114,6 +127,11 @@ __device__ __forceinline__ void rec_add_q(C5RecL* r, u32 th, u32 tm) {
   atomicAdd(&r->wf, 1u << C5L_BITS);
   atomicAdd(&r->rest, ((u64)th << 36) | ((u64)tm << 48));
 }
+__device__ __forceinline__ bool rec_add_q_first(C5RecL* r, u32 th, u32 tm) {
+  const u32 old = atomicAdd(&r->wf, 1u << C5L_BITS);
+  atomicAdd(&r->rest, ((u64)th << 36) | ((u64)tm << 48));
+  return ((old >> C5L_BITS) & (u32)C5L_MASK) == 0;
+}
 __device__ __forceinline__ u64 rec_q(const C5RecL* r) { return (u64)(r->wf >> C5L_BITS) & C5L_MASK; }
 __device__ __forceinline__ u64 rec_p(const C5RecL* r) { return r->rest & C5L_MASK; }
 __device__ __forceinline__ u64 rec_a(const C5RecL* r) { return (r->rest >> 12) & C5L_MASK; }
@@ -133,7 +151,7 @@ template <typename R>
 __device__ __forceinline__ u64 c5_wn(const R* r) { return (u64)(r->wf & C5_WN_MASK); }
 __device__ __forceinline__ u64 c5_wn(const C5RecL* r) { return (u64)(r->wf & (u32)C5L_MASK); }
 #define C5_ADJ 1u      // vertex is a neighbour of l
-#define C5_I 2u        // i-key (steps 1, 3)
+#define C5_I 2u        // i-key: Wn > 0 (dense records; hashed records test Wn itself)
 #define C5_J 4u        // j-key (step 2)
 #define C5_PRESENT 8u  // record in use (touched list)
 
@@ -191,6 +209,18 @@ struct C5Dense {
     const u32 ob = atomicOr(&bP[x >> 5], bit);
     append_active(!(ob & bit), x, L, nL);
     atomicOr(&r->wf, (bits | C5_PRESENT) << 28);  // result unused: a reduction
+    return r;
+  }
+  // step-1 mark of a wedge end: Wn += 1 (its first mark makes it an i-key: Wn > 0)
+  __device__ __forceinline__ Rec* mark_wedge(int32_t x) {
+    Rec* r = mark_nr(x, C5_I);
+    atomicAdd(&r->wf, 1u);
+    return r;
+  }
+  // step-2 mark of a j-key with its Q, QT, QM updates
+  __device__ __forceinline__ Rec* mark_j_q(int32_t x, u32 th, u32 tm, bool& newj) {
+    Rec* r = mark_j(x, newj);
+    rec_add_q(r, th, tm);
     return r;
   }
   // j-key mark: newj = first C5_J mark of x
@@ -260,25 +290,23 @@ struct C5Hash {
     append_active(claimed, (int32_t)h, L, nL);
     return &R[h];
   }
-  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old, u32& word) {
-    Rec* r = probe(x);
-    word = atomicOr(&r->wf, (bits | C5_PRESENT) << 28);
-    old = word >> 28;
-    return r;
-  }
-  __device__ __forceinline__ Rec* mark(int32_t x, u32 bits, u32& old) {
-    u32 word;
-    return mark(x, bits, old, word);
-  }
   __device__ __forceinline__ Rec* mark_nr(int32_t x, u32 bits) {
     Rec* r = probe(x);
     atomicOr(&r->wf, (bits | C5_PRESENT) << 28);  // result unused: a reduction
     return r;
   }
-  __device__ __forceinline__ Rec* mark_j(int32_t x, bool& newj) {
-    u32 old;
-    Rec* r = mark(x, C5_J, old);
-    newj = !(old & C5_J);
+  // step-1 mark of a wedge end: Wn += 1, one atomic (a claimed key is present, and Wn > 0 is
+  // what makes it an i-key, so no flag update is needed)
+  __device__ __forceinline__ Rec* mark_wedge(int32_t x) {
+    Rec* r = probe(x);
+    atomicAdd(&r->wf, 1u);
+    return r;
+  }
+  // step-2 mark of a j-key: the Q increment's old value tells a new j-key (Q was 0), so no
+  // flag update is needed either
+  __device__ __forceinline__ Rec* mark_j_q(int32_t x, u32 th, u32 tm, bool& newj) {
+    Rec* r = probe(x);
+    newj = rec_add_q_first(r, th, tm);
     return r;
   }
   __device__ __forceinline__ void clear_bits(int32_t) const {}
@@ -369,8 +397,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       [&](int, int64_t base, int k) -> u64 {
         const int32_t i = g.ci[base + k];
         if (i == l) return 0;
-        auto* r = loc.mark_nr(i, C5_I);
-        atomicAdd(&r->wf, 1u);  // Wn
+        loc.mark_wedge(i);  // Wn += 1
         loc.note_i(i);
         return 0;
       },
@@ -383,9 +410,8 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int32_t j = g.ocol[e];
         if (j == l) return 0;
         bool newj;
-        auto* r = loc.mark_j(j, newj);
+        loc.mark_j_q(j, Thigh[e], Tmid[e], newj);
         append_active(newj, j, J, nJ);
-        rec_add_q(r, Thigh[e], Tmid[e]);
         return 0;
       },
       [&](int, u64) {});
@@ -452,7 +478,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       int32_t x;
       const auto* r = loc.touched(t, x);
       const u32 fl = c5_flags(r);
-      if (!(fl & C5_I)) continue;
+      if (!c5_wn(r)) continue;  // not an i-key
       const bool adji = fl & C5_ADJ;
       const u64 bi = rec_qm(r) - rec_q(r) * ((x > l && adji) ? 1ull : 0ull);
       const u64 ci = rec_p(r) * c5_wn(r) - rec_a(r) - bi;
