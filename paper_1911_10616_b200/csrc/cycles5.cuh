@@ -242,6 +242,7 @@ struct C5Dense {
     return (__ldcg(&r->wf) & C5_WN_MASK) ? r : nullptr;
   }
   __device__ __forceinline__ Rec* peek(int32_t x) const { return &R[x]; }
+  __device__ __forceinline__ int32_t id_of(int32_t idx) const { return idx; }  // record index -> vertex
   __device__ __forceinline__ Rec* touched(int t, int32_t& x) const {
     x = L[t];
     return &R[x];
@@ -332,6 +333,7 @@ struct C5Hash {
     x = r->key - 1;
     return r;
   }
+  __device__ __forceinline__ int32_t id_of(int32_t idx) const { return R[idx].key - 1; }  // slot -> vertex
 };
 
 // Engine adaptors: warp (light endpoints) and CTA (heavy endpoints)
@@ -358,12 +360,16 @@ __device__ __forceinline__ bool c5_adj(const R* r) { return r && (c5_flags(r) & 
 
 // developer step timers (EVOKE_DEBUG): SM cycles of thread 0 per step, summed over the
 // endpoints of the CTA engines ([0] heavy 1024-thread CTAs, [1] mid CTAs)
-__device__ unsigned long long g_c5_phase[2][8];
+// developer step timers (EVOKE_DEBUG sets g_c5_prof): SM cycles per step summed over the
+// endpoints, [0] heavy 1024-thread CTAs, [1] mid CTAs (thread 0), [2] light warps (lane 0)
+__device__ unsigned long long g_c5_phase[3][8];
+__device__ int g_c5_prof;
 #define C5_PHASE(i)                                                                              \
   do {                                                                                           \
-    if (Eng::kCta && threadIdx.x == 0) {                                                         \
+    if (g_c5_prof && (Eng::kCta ? threadIdx.x == 0 : (threadIdx.x & 31) == 0)) {                 \
       const long long t_ = clock64();                                                            \
-      atomicAdd(&g_c5_phase[blockDim.x == C5_HBT ? 0 : 1][i], (unsigned long long)(t_ - t_prev)); \
+      atomicAdd(&g_c5_phase[!Eng::kCta ? 2 : blockDim.x == C5_HBT ? 0 : 1][i],                   \
+                (unsigned long long)(t_ - t_prev));                                              \
       t_prev = t_;                                                                               \
     }                                                                                            \
   } while (0)
@@ -410,8 +416,8 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const int32_t j = g.ocol[e];
         if (j == l) return 0;
         bool newj;
-        loc.mark_j_q(j, Thigh[e], Tmid[e], newj);
-        append_active(newj, j, J, nJ);
+        auto* r = loc.mark_j_q(j, Thigh[e], Tmid[e], newj);
+        append_active(newj, (int32_t)(r - loc.R), J, nJ);  // J holds record indices (no lookups later)
         return 0;
       },
       [&](int, u64) {});
@@ -421,7 +427,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
   const int nj = *nJ;
   eng.lists(nj,
       [&](int t, int64_t& base, int& len) {
-        const int32_t j = J[t];
+        const int32_t j = loc.id_of(J[t]);
         base = g.orow[j];
         len = (int)(g.orow[j + 1] - base);
       },
@@ -434,19 +440,19 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         if (i == l) return 0;
         auto* ri = loc.peek_i(i);
         if (!ri) return 0;
-        const auto* rj = loc.peek(J[t]);
+        const auto* rj = &loc.R[J[t]];
         rec_add_pa(ri, rec_q(rj), c5_flags(rj) & C5_ADJ);
         return c5_wn(ri);
       },
       [&](int t, u64 s) {
-        auto* rj = loc.peek(J[t]);
+        auto* rj = &loc.R[J[t]];
         rec_add_s(rj, s);
-        atomicAdd(&C5[J[t]], rec_q(rj) * s);  // the j credit is linear in S
+        atomicAdd(&C5[loc.id_of(J[t])], rec_q(rj) * s);  // the j credit is linear in S
       });
   // constant part of the j credits
   for (int t = eng.tid(); t < nj; t += eng.nthr()) {
-    const int32_t j = J[t];
-    const auto* rj = loc.peek(j);
+    const int32_t j = loc.id_of(J[t]);
+    const auto* rj = &loc.R[J[t]];
     const u64 q = rec_q(rj);
     const bool adjj = c5_flags(rj) & C5_ADJ;
     const u64 lj = (l > j && adjj) ? 1ull : 0ull;

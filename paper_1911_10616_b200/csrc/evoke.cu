@@ -617,6 +617,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
                                cudaMemcpyHostToDevice, C.st));
   }
 
+  {
+    const int prof = getenv("EVOKE_DEBUG") ? 1 : 0;  // developer step / phase timers
+    CK(cudaMemcpyToSymbolAsync(g_c5_prof, &prof, sizeof(int), 0, cudaMemcpyHostToDevice, C.st));
+    CK(cudaMemcpyToSymbolAsync(g_pair_prof, &prof, sizeof(int), 0, cudaMemcpyHostToDevice, C.st));
+  }
   Arena A(C.st, dev);
   ZeroLease lease;  // destroyed before A (its buffer is not A's)
   lease.acquire(dev, C.st);
@@ -1510,13 +1515,14 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
               ph[t][5] / 1e6, ph[t][6] / 1e6);
     unsigned long long z[2][8] = {};
     CK(cudaMemcpyToSymbol(g_pair_phase, z, sizeof(z)));
-    unsigned long long c5p[2][8];
+    unsigned long long c5p[3][8];
     CK(cudaMemcpyFromSymbol(c5p, g_c5_phase, sizeof(c5p)));
-    for (int t = 0; t < 2; t++)
+    for (int t = 0; t < 3; t++)
       fprintf(stderr, "[evoke] c5 %s steps (Mcycles): s0 %.1f s1 %.1f s2 %.1f s3 %.1f s4 %.1f s5 %.1f s6 %.1f\n",
-              t ? "mid" : "heavy", c5p[t][0] / 1e6, c5p[t][1] / 1e6, c5p[t][2] / 1e6, c5p[t][3] / 1e6,
-              c5p[t][4] / 1e6, c5p[t][5] / 1e6, c5p[t][6] / 1e6);
-    CK(cudaMemcpyToSymbol(g_c5_phase, z, sizeof(z)));
+              t == 2 ? "light" : t ? "mid" : "heavy", c5p[t][0] / 1e6, c5p[t][1] / 1e6, c5p[t][2] / 1e6,
+              c5p[t][3] / 1e6, c5p[t][4] / 1e6, c5p[t][5] / 1e6, c5p[t][6] / 1e6);
+    unsigned long long z3[3][8] = {};
+    CK(cudaMemcpyToSymbol(g_c5_phase, z3, sizeof(z3)));
   }
   C.njobs = (int)jobs.size();
   for (size_t i = 0; i < jobs.size(); i++) { C.job_pass[i] = jobs[i].pass; C.job_rank[i] = jobs[i].rank; }

@@ -480,11 +480,13 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
   }
 }
 
-// developer phase timers (EVOKE_DEBUG): SM cycles per phase summed over sources, CTA tiers
+// developer phase timers (EVOKE_DEBUG sets g_pair_prof): SM cycles per phase summed over
+// sources, CTA tiers
 __device__ unsigned long long g_pair_phase[2][8];
+__device__ int g_pair_prof;
 #define PAIR_PHASE(i)                                                                     \
   do {                                                                                    \
-    if (threadIdx.x == 0) {                                                               \
+    if (g_pair_prof && threadIdx.x == 0) {                                                \
       const long long t_ = clock64();                                                     \
       atomicAdd(&g_pair_phase[Tab::kDense ? 1 : 0][i], (unsigned long long)(t_ - t_prev)); \
       t_prev = t_;                                                                        \
