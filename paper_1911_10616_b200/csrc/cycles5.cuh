@@ -690,7 +690,10 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
     idx = __shfl_sync(FULL_MASK, idx, 0);
     if (idx >= n_light) break;
     const int32_t l = light[idx];
-    const u32 cap = pow2_at_least(2u * lw[idx], 64u);  // 2 x the record bound R(l): <= C5_WARP_CAP
+    // region of at least 1.25 R(l) + 1 slots: R(l) bounds the records (typically a quarter of
+    // it are distinct), so the load stays <= 0.8 and the probes terminate; a smaller region
+    // keeps more of the warps' records in L2 (config 4: 23 % of 2R slots were used)
+    const u32 cap = pow2_at_least(lw[idx] + lw[idx] / 4 + 1, 64u);  // <= C5_WARP_CAP
     int32_t* J;
     if (cap <= (u32)sh_cap) {
       loc.R = shR;
@@ -706,6 +709,10 @@ __global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restr
     __syncwarp();
     c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &w_nJ[wib], &w_tot[wib], C5);
     if (lane == 0 && w_tot[wib]) atomicAdd(&C5[l], w_tot[wib]);
+    if (g_c5_prof && lane == 0) {  // developer: records used vs region slots
+      atomicAdd(&g_c5_phase[2][7], (unsigned long long)w_nL[wib]);
+      atomicAdd(&g_c5_phase[1][7], (unsigned long long)cap);
+    }
     c5_reset(eng, loc);
     for (int i = lane; i < C5_FB_WARP; i += 32) fb[i] = 0u;
     __syncwarp();
@@ -746,7 +753,7 @@ __global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restri
     const int idx = s_idx;
     if (idx >= n_mid) break;
     const int32_t l = list[idx];
-    loc.mask = pow2_at_least(2u * rb[idx], 64u) - 1;  // rb[idx] = R(l) <= C5_MID_MAX
+    loc.mask = pow2_at_least(rb[idx] + rb[idx] / 4 + 1, 64u) - 1;  // rb[idx] = R(l) <= C5_MID_MAX (load <= 0.8)
     c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &s_nJ, &s_tot, C5);
     if (threadIdx.x == 0 && s_tot) atomicAdd(&C5[l], s_tot);
     c5_reset(eng, loc);

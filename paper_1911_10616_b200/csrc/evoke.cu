@@ -1521,6 +1521,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       fprintf(stderr, "[evoke] c5 %s steps (Mcycles): s0 %.1f s1 %.1f s2 %.1f s3 %.1f s4 %.1f s5 %.1f s6 %.1f\n",
               t == 2 ? "light" : t ? "mid" : "heavy", c5p[t][0] / 1e6, c5p[t][1] / 1e6, c5p[t][2] / 1e6,
               c5p[t][3] / 1e6, c5p[t][4] / 1e6, c5p[t][5] / 1e6, c5p[t][6] / 1e6);
+    fprintf(stderr, "[evoke] c5 light records used %llu of %llu region slots\n", c5p[2][7], c5p[1][7]);
     unsigned long long z3[3][8] = {};
     CK(cudaMemcpyToSymbol(g_c5_phase, z3, sizeof(z3)));
   }
