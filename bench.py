@@ -400,7 +400,7 @@ def traffic_of(pass_name, config):
         return None
     try:
         d = json.load(open(p))
-        if d.get("config") not in (None, config):
+        if d.get("config") != config:  # a capture of another config (or of unknown config) says nothing here
             return None
         return d.get("passes", {}).get(pass_name)
     except Exception:

@@ -12,16 +12,17 @@ import paper_1911_10616_b200 as pkg
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 serial = "--serial" in sys.argv
+warm = int(sys.argv[sys.argv.index("--warm") + 1]) if "--warm" in sys.argv else 2
 g = graphgen.config(cfg)
 dev = torch.device("cuda:0")
 edges = torch.from_numpy(g.edges).to(dev)
 out = torch.empty((g.n, 73), dtype=torch.int64, device=dev)
 rows = []
 walls = []
-for i in range(k + 2):
+for i in range(k + warm):
     _, st = pkg.evoke_orbits_edges(g.n, edges, out=out, return_stats=True, serial=serial)
     torch.cuda.synchronize()
-    if i >= 2:
+    if i >= warm:
         rows.append(st["ms_pass"])
         walls.append(st["ms_total"])
 if not rows:

@@ -1,6 +1,8 @@
 """Write profiles/traffic.json: DRAM bytes per launch of each pass's kernels, from ncu
 --set full reports (one report per kernel, as captured by tools/gpu_prof.sh).
-    python tools/ncu_traffic.py pass=report.ncu-rep [pass=report.ncu-rep ...]"""
+    python tools/ncu_traffic.py CONFIG pass=report.ncu-rep [pass=report.ncu-rep ...]
+CONFIG = the BASELINE config index the captures were taken on (bench.py only uses the file
+for that config)."""
 import csv
 import io
 import json
@@ -8,8 +10,8 @@ import subprocess
 import sys
 
 out = {"how": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full --clock-control none",
-       "passes": {}, "kernels": {}}
-for arg in sys.argv[1:]:
+       "config": int(sys.argv[1]), "passes": {}, "kernels": {}}
+for arg in sys.argv[2:]:
     pas, rep = arg.split("=", 1)
     raw = (open(rep).read() if rep.endswith(".csv") else
            subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
