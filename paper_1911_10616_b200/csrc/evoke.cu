@@ -1246,6 +1246,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (getenv("EVOKE_DEBUG"))
       fprintf(stderr, "[evoke] hub items: micro %d light %d heavy %d\n", n_micro, n_light, n_heavy);
     int32_t* heavy_sorted = heavy;
+    u32* heavy_est_sorted = hest;
     if (n_heavy > 1) {
       int32_t* hs = A.alloc<int32_t>(n_heavy);
       u32* hk = A.alloc<u32>(n_heavy);
@@ -1255,6 +1256,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       CK(cub::DeviceRadixSort::SortPairsDescending(t, tb, hest, hk, heavy, hs, n_heavy, 0, 32, C.st));
       C.lib_launches += 4;
       heavy_sorted = hs;
+      heavy_est_sorted = hk;
     }
     if (n_light + n_heavy > 0) {
       int hb_per_sm = 0;
@@ -1270,6 +1272,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       u32* gt = nullptr;
       int32_t* gl = nullptr;
       const int sh_dense_max = (int)env_cap("EVOKE_HUB_SH_DENSE", HUB_SH_DENSE);
+      const int hash_max = (int)env_cap("EVOKE_HUB_HASH_MAX", HUB_HASH_MAX);
       if (g.max_deg > sh_dense_max && n_heavy > 0) {
         gt = A.zalloc<u32>((size_t)hg * g.max_deg);
         gl = A.alloc<int32_t>((size_t)hg * g.max_deg);
@@ -1277,8 +1280,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       u64* r68 = Fp(F_R68);
       u64* r69 = Fp(F_R69);
       jobs.push_back({P_HUB, 2, [=, &C](cudaStream_t st) {
-        k_hub_process<<<hg, HUB_BT, HUB_SMEM, st>>>(g, Te, heavy_sorted, n_heavy, light, n_light, hcnt + 2, gt, gl,
-                                                    r68, r69, sh_dense_max);
+        k_hub_process<<<hg, HUB_BT, HUB_SMEM, st>>>(g, Te, heavy_sorted, heavy_est_sorted, n_heavy, light, n_light,
+                                                    hcnt + 2, gt, gl, r68, r69, sh_dense_max, hash_max);
         if (n_micro > 0) k_hub_micro<<<grid_for(n_micro, 128, SM), 128, 0, st>>>(g, micro, n_micro, r68, r69);
         C.launches += 1 + (n_micro > 0);
       }});

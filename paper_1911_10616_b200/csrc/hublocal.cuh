@@ -32,8 +32,12 @@
 #define HUB_WARP_CAP 1024                            // per-warp hash capacity (light items)
 #define HUB_WARP_MAX (HUB_WARP_CAP / 2)              // light item: est <= this
 #define HUB_SMEM (HUB_BT / 32 * HUB_WARP_CAP * 12)   // 96 KB dynamic shared memory
-#define HUB_SH_DENSE (HUB_SMEM / 8)                  // heavy item: shared table if d(v) <= this
+#define HUB_SH_DENSE (HUB_SMEM / 4)                  // heavy item: shared counts by position if d(v) <= this
+#define HUB_HASH_SLOTS (HUB_SMEM / 8)                // heavy item: x-keyed shared hash, (x+1, count) slots ...
+#define HUB_HASH_MAX (HUB_HASH_SLOTS * 3 / 4)        // ... used when min(d(v)-1, est) <= this (load <= 0.75)
 #define HUB_FEW_ITEMS 262144                         // at most this many items: one CTA per SM
+#define HUB_LONG 32                                  // heavy item: x-lists this long are streamed by a whole warp
+#define HUB_ILP 4                                    // ... with this many loads per lane in flight
 #define HUB_MICRO_MAX 16                             // micro item: est <= this, one THREAD per item
 
 // number of entries of the full list [f, f+len) with third vertex < bound: a binary search
@@ -163,20 +167,32 @@ __global__ void k_hub_micro(DGraph g, const int32_t* __restrict__ items, int n_i
   }
 }
 
-// ---- heavy item: one CTA --------------------------------------------------------------
+// ---- heavy item: one CTA ----------------------------------------------------------------
+// The CTA's warps take the item's middles b in groups of 32 (a shared counter) and flatten
+// their x-lists over the lanes (warp_flat): no per-element search, and the pass-2 sums of a
+// middle stay in a lane's register while the lane stays on it.  c(x) lives in one of three
+// tables, chosen per item:
+//   HUB_T_HASH : shared open-addressing hash keyed by x (x+1, 0 = empty) when the number of
+//                distinct x, at most min(d(v)-1, est(v,a)), fits HUB_HASH_MAX -- no per-element
+//                position lookup (fe1/fe2 and the slot map of x in N(v) are never read);
+//   HUB_T_SHPOS: shared counts dense by x's position in N(v) (d(v) <= sh_dense_max), swept;
+//   HUB_T_GLPOS: a per-CTA global table by position with a touched list (larger hubs).
+// All three are left zeroed (shared memory is zero between items in every mode).
+enum { HUB_T_HASH = 0, HUB_T_SHPOS = 1, HUB_T_GLPOS = 2 };
 struct HubCtaShared {
-  int64_t pre[HUB_BT + 1];
-  int64_t fb[HUB_BT];
-  int32_t b[HUB_BT];
-  int32_t evb[HUB_BT];
-  u64 acc[HUB_BT];
-  int cnt;
+  int next;  // group counter of the current pass
+  int cnt;   // touched entries (global table)
   u64 r69;
+  u64 acc[HUB_BT / 32][32];  // per-warp sums of the current 32 middles (pass 2)
 };
 
-__device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_t s, u32* shm, HubCtaShared& S,
+__device__ __forceinline__ u32 hub_h0(int32_t x, u32 cap) { return __umulhi((u32)x * 0x9E3779B1u, cap); }
+
+template <int MODE>
+__device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubCtaShared& S,
                              u32* __restrict__ gtab, int32_t* __restrict__ glist, u64* __restrict__ R68,
-                             u64* __restrict__ R69, int sh_dense_max) {
+                             u64* __restrict__ R69) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int32_t eva = g.eid[s];
   const int32_t a = g.ci[s];
   const int32_t lo_ = g.esrc[eva];
@@ -184,77 +200,168 @@ __device__ void hub_item_cta(const DGraph& g, const u32* __restrict__ Te, int32_
   const bool v_lo = lo_ == v;
   const int64_t rpv = g.rp[v];
   const int32_t dv = (int32_t)(g.rp[v + 1] - rpv);
-  const bool dense_sh = dv <= sh_dense_max;  // (<= HUB_SH_DENSE; lower only in tests)
-  u32* tab = dense_sh ? shm : gtab;
-  int32_t* list = dense_sh ? (int32_t*)(shm + HUB_SH_DENSE) : glist;
   const int64_t fa = g.foff[eva];
-  const int64_t na = full_prefix(g, fa, (int)(g.foff[eva + 1] - fa), a);  // b < a (or all, filtered)
+  const int na = full_prefix(g, fa, (int)(g.foff[eva + 1] - fa), a);  // b < a (or all, filtered)
+  int32_t* hkeys = reinterpret_cast<int32_t*>(shm);                 // HUB_T_HASH: x + 1
+  u32* hval = shm + cap;
+  u32* tab = MODE == HUB_T_GLPOS ? gtab : shm;                       // by position
+  u64* acc = S.acc[wib];
   if (threadIdx.x == 0) { S.cnt = 0; S.r69 = 0; }
-  S.acc[threadIdx.x] = 0;
-  __syncthreads();
-  auto load = [&](int64_t i) -> int64_t {
-    const int64_t r = fa + i;
-    const int32_t b = g.fx[r];
-    S.b[threadIdx.x] = b;
-    if (b >= a) return 0;
-    const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
-    const int64_t fb = g.foff[evb];
-    S.fb[threadIdx.x] = fb;
-    S.evb[threadIdx.x] = evb;
-    return (int64_t)full_prefix(g, fb, (int)(g.foff[evb + 1] - fb), a);  // x < a
-  };
-  // pass 1: c(x) for x < a over b < a
-  block_flat<HUB_BT>(na, S.pre, load,
-      [&](int li, int64_t k) {
-        const int64_t r2 = S.fb[li] + k;
-        const int32_t x = g.fx[r2];
-        if (x >= a) return;
-        const int32_t evb = S.evb[li];
-        const int32_t evx = (g.esrc[evb] == v) ? g.fe1[r2] : g.fe2[r2];
-        const int64_t p = pos_in_list(g, v, x, evx);
-        if (atomicAdd(&tab[p], 1u) == 0u) list[atomicAdd(&S.cnt, 1)] = (int32_t)p;
-      },
-      [&](int64_t, int) {});
-  // pass 2: middles b get sum_x (c(x) - 1) (register sums while a thread stays on one b)
-  int cur = -1;
-  u64 cacc = 0;
-  auto flush = [&]() {
-    if (cur >= 0 && cacc) atomicAdd(&S.acc[cur], cacc);
-    cacc = 0;
-  };
-  block_flat<HUB_BT>(na, S.pre, load,
-      [&](int li, int64_t k) {
-        if (li != cur) { flush(); cur = li; }
-        const int64_t r2 = S.fb[li] + k;
-        const int32_t x = g.fx[r2];
-        if (x >= a) return;
-        const int32_t evb = S.evb[li];
-        const int32_t evx = (g.esrc[evb] == v) ? g.fe1[r2] : g.fe2[r2];
-        const int64_t p = pos_in_list(g, v, x, evx);
-        cacc += (u64)tab[p] - 1ull;
-      },
-      [&](int64_t, int cn) {
-        if ((int)threadIdx.x < cn) {
-          const u64 x = S.acc[threadIdx.x];
-          if (x) atomicAdd(&R68[S.b[threadIdx.x]], x);
-          S.acc[threadIdx.x] = 0;
+  acc[lane] = 0;
+#pragma unroll 1
+  for (int pass = 1; pass <= 2; pass++) {
+    if (threadIdx.x == 0) S.next = 0;
+    __syncthreads();
+    for (;;) {
+      int i0 = 0;
+      if (lane == 0) i0 = atomicAdd(&S.next, 32);
+      i0 = __shfl_sync(FULL_MASK, i0, 0);
+      if (i0 >= na) break;
+      const int i = i0 + lane;
+      int len = 0;
+      int64_t fb = 0;
+      int32_t b = 0;
+      bool vl = false;  // v is the lower end of e(v,b): fe1 holds e(v,x)
+      if (i < na) {
+        const int64_t r = fa + i;
+        b = g.fx[r];
+        if (b < a) {
+          const int32_t evb = v_lo ? g.fe1[r] : g.fe2[r];
+          fb = g.foff[evb];
+          len = full_prefix(g, fb, (int)(g.foff[evb + 1] - fb), a);  // x < a
+          if (MODE != HUB_T_HASH) vl = g.esrc[evb] == v;
         }
-      },
-      flush);
-  // pass 3: corners a, x and the hub v
-  const int cnt = S.cnt;
+      }
+      // the count cell of x (pass 1: found or claimed; pass 2: found -- every x of pass 2 was
+      // inserted by pass 1); r2 = x's entry in the full list, vlj: fe1 holds e(v,x)
+      auto cell_of = [&](int32_t x, int64_t r2, bool vlj) -> u32* {
+        if (MODE == HUB_T_HASH) {
+          u32 h = hub_h0(x, cap);
+          if (pass == 1) {
+            for (;;) {
+              const int32_t kk = hkeys[h];
+              if (kk == x + 1) break;
+              if (kk == 0) {
+                const int32_t o = atomicCAS(&hkeys[h], 0, x + 1);
+                if (o == 0 || o == x + 1) break;
+              }
+              h = (h + 1 == cap) ? 0 : h + 1;
+            }
+          } else {
+            while (hkeys[h] != x + 1) h = (h + 1 == cap) ? 0 : h + 1;
+          }
+          return &hval[h];
+        }
+        const int32_t evx = vlj ? g.fe1[r2] : g.fe2[r2];
+        return &tab[pos_in_list(g, v, x, evx)];
+      };
+      auto bump = [&](u32* cell) {
+        const u32 old = atomicAdd(cell, 1u);
+        if (MODE == HUB_T_GLPOS && old == 0u) glist[atomicAdd(&S.cnt, 1)] = (int32_t)(cell - tab);
+      };
+      // long lists: the whole warp streams one list at a time, HUB_ILP loads per lane in
+      // flight, and the middle's pass-2 sum is one warp reduction
+      unsigned lm = __ballot_sync(FULL_MASK, len >= HUB_LONG);
+      while (lm) {
+        const int j = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const int64_t fbj = __shfl_sync(FULL_MASK, fb, j);
+        const int lenj = __shfl_sync(FULL_MASK, len, j);
+        const bool vlj = MODE != HUB_T_HASH && __shfl_sync(FULL_MASK, vl, j);
+        const int32_t bj = __shfl_sync(FULL_MASK, b, j);
+        u64 sum = 0;
+        for (int k0 = 0; k0 < lenj; k0 += 32 * HUB_ILP) {
+          int32_t xs[HUB_ILP];
+#pragma unroll
+          for (int u = 0; u < HUB_ILP; u++) {
+            const int k = k0 + 32 * u + lane;
+            xs[u] = k < lenj ? g.fx[fbj + k] : a;
+          }
+#pragma unroll
+          for (int u = 0; u < HUB_ILP; u++) {
+            if (xs[u] >= a) continue;
+            u32* c = cell_of(xs[u], fbj + k0 + 32 * u + lane, vlj);
+            if (pass == 1) bump(c);
+            else sum += (u64)*c - 1ull;
+          }
+        }
+        if (pass == 2) {
+          sum = warp_sum(sum);
+          if (lane == 0 && sum) atomicAdd(&R68[bj], sum);
+        }
+        if (lane == j) len = 0;
+      }
+      int cur = -1;
+      u64 cacc = 0;
+      warp_flat(len, [&](int j, int k, bool valid) {
+        const int64_t fbj = __shfl_sync(FULL_MASK, fb, j);
+        const bool vlj = MODE != HUB_T_HASH && __shfl_sync(FULL_MASK, vl, j);
+        if (!valid) return;
+        const int64_t r2 = fbj + k;
+        const int32_t x = g.fx[r2];
+        if (x >= a) return;
+        u32* cell = cell_of(x, r2, vlj);
+        if (pass == 1) {
+          bump(cell);
+        } else {
+          if (j != cur) {
+            if (cur >= 0 && cacc) atomicAdd(&acc[cur], cacc);
+            cur = j;
+            cacc = 0;
+          }
+          cacc += (u64)*cell - 1ull;  // middles b get sum over their x of c(x) - 1
+        }
+      });
+      if (pass == 2) {
+        if (cur >= 0 && cacc) atomicAdd(&acc[cur], cacc);
+        __syncwarp();
+        const u64 sb = acc[lane];
+        acc[lane] = 0;
+        if (sb) atomicAdd(&R68[b], sb);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  // pass 3: corners a, x and the hub v; clear the table
   u64 r69 = 0;
-  for (int t = threadIdx.x; t < cnt; t += HUB_BT) {
-    const int32_t p = list[t];
-    const u64 c2 = binom2(tab[p]);
-    tab[p] = 0u;
-    if (c2) {
-      r69 += c2;
-      atomicAdd(&R68[g.ci[rpv + p]], c2);
+  if (MODE == HUB_T_HASH) {
+    for (u32 h = threadIdx.x; h < cap; h += HUB_BT) {
+      const int32_t kk = hkeys[h];
+      if (kk == 0) continue;
+      const u64 c2 = binom2(hval[h]);
+      hkeys[h] = 0;
+      hval[h] = 0u;
+      if (c2) {
+        r69 += c2;
+        atomicAdd(&R68[kk - 1], c2);
+      }
+    }
+  } else if (MODE == HUB_T_SHPOS) {
+    for (int32_t p = threadIdx.x; p < dv; p += HUB_BT) {
+      const u32 c = tab[p];
+      if (!c) continue;
+      tab[p] = 0u;
+      const u64 c2 = binom2(c);
+      if (c2) {
+        r69 += c2;
+        atomicAdd(&R68[g.ci[rpv + p]], c2);
+      }
+    }
+  } else {
+    const int cnt = S.cnt;
+    for (int t = threadIdx.x; t < cnt; t += HUB_BT) {
+      const int32_t p = glist[t];
+      const u64 c2 = binom2(tab[p]);
+      tab[p] = 0u;
+      if (c2) {
+        r69 += c2;
+        atomicAdd(&R68[g.ci[rpv + p]], c2);
+      }
     }
   }
   r69 = warp_sum(r69);
-  if ((threadIdx.x & 31) == 0 && r69) atomicAdd(&S.r69, r69);
+  if (lane == 0 && r69) atomicAdd(&S.r69, r69);
   __syncthreads();
   if (threadIdx.x == 0 && S.r69) {
     atomicAdd(&R69[v], S.r69);
@@ -358,26 +465,40 @@ __device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32
 
 // ---- persistent processing kernel -------------------------------------------------------
 __global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __restrict__ Te,
-                                                        const int32_t* __restrict__ heavy, int n_heavy,
+                                                        const int32_t* __restrict__ heavy,
+                                                        const u32* __restrict__ heavy_est, int n_heavy,
                                                         const int32_t* __restrict__ light, int n_light,
                                                         int* __restrict__ counters, u32* __restrict__ gtabs,
                                                         int32_t* __restrict__ glists, u64* __restrict__ R68,
-                                                        u64* __restrict__ R69, int sh_dense_max) {
+                                                        u64* __restrict__ R69, int sh_dense_max, int hash_max) {
   extern __shared__ u32 hub_sh[];
   __shared__ HubCtaShared S;
   __shared__ int s_idx;
   __shared__ int s_cnt[HUB_BT / 32];
-  __shared__ u64 s_acc[HUB_BT / 32][32];
   u32* gtab = gtabs ? gtabs + (size_t)blockIdx.x * g.max_deg : nullptr;
   int32_t* glist = glists ? glists + (size_t)blockIdx.x * g.max_deg : nullptr;
-  for (int i = threadIdx.x; i < HUB_SH_DENSE; i += HUB_BT) hub_sh[i] = 0u;  // reset by pass 3 after use
+  for (int i = threadIdx.x; i < HUB_SMEM / 4; i += HUB_BT) hub_sh[i] = 0u;  // cleared by pass 3 after use
+  __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) s_idx = atomicAdd(&counters[0], 1);
     __syncthreads();
     const int idx = s_idx;
     __syncthreads();
     if (idx >= n_heavy) break;
-    hub_item_cta(g, Te, heavy[idx], hub_sh, S, gtab, glist, R68, R69, sh_dense_max);
+    const int32_t s = heavy[idx];
+    const int32_t a = g.ci[s];
+    const int32_t eva = g.eid[s];
+    const int32_t v = g.esrc[eva] + g.edst[eva] - a;
+    const u64 dv = (u64)g.deg[v];
+    const u64 bound = min(dv - 1, (u64)heavy_est[idx]);  // distinct x of the item
+    if (bound <= (u64)hash_max) {
+      const u32 cap = (u32)min((u64)HUB_HASH_SLOTS, bound + bound / 3 + 64);
+      hub_item_cta<HUB_T_HASH>(g, s, cap, hub_sh, S, gtab, glist, R68, R69);
+    } else if (dv <= (u64)sh_dense_max) {
+      hub_item_cta<HUB_T_SHPOS>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
+    } else {
+      hub_item_cta<HUB_T_GLPOS>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
+    }
   }
   // light items: the dynamic shared memory becomes one hash (keys, counts, list) per warp
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -387,7 +508,7 @@ __global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __r
   H.mask = HUB_WARP_CAP - 1;
   int32_t* L = H.keys + 2 * HUB_WARP_CAP;
   for (int t = lane; t < HUB_WARP_CAP; t += 32) { H.keys[t] = SH_EMPTY; H.val[t] = 0u; }
-  s_acc[wib][lane] = 0;
+  S.acc[wib][lane] = 0;
   if (lane == 0) s_cnt[wib] = 0;
   __syncwarp();
   for (;;) {
@@ -397,6 +518,6 @@ __global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __r
     if (idx >= n_light) break;
     const int end = min(idx + 4, n_light);
     for (int q = idx; q < end; q++)
-      hub_item_warp(g, Te, light[q], H, L, &s_cnt[wib], s_acc[wib], R68, R69);
+      hub_item_warp(g, Te, light[q], H, L, &s_cnt[wib], S.acc[wib], R68, R69);
   }
 }

@@ -25,8 +25,11 @@ COMBOS = {
     "pair_mid": {"EVOKE_PAIR_LIGHT_MAX": "0", "EVOKE_PAIR_MIDS_MAX": "0"},  # k_pairs_main CTA tier
     "pair_small_mid": {"EVOKE_PAIR_LIGHT_MAX": "0"},                  # k_pairs_mids
     "hub_warp": {"EVOKE_HUB_MICRO_MAX": "0"},                         # hub_item_warp (no micro items)
-    "hub_heavy_shared": {"EVOKE_HUB_WARP_MAX": "0"},                  # hub_item_cta, shared table
-    "hub_heavy_global": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_SH_DENSE": "0"},  # global tables
+    "hub_heavy_hash": {"EVOKE_HUB_WARP_MAX": "0"},                    # hub_item_cta<HUB_T_HASH>
+    "hub_heavy_shared": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_HASH_MAX": "0"},  # <HUB_T_SHPOS>
+    "hub_heavy_global": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_HASH_MAX": "0",
+                         "EVOKE_HUB_SH_DENSE": "0"},                  # <HUB_T_GLPOS>
+    "hub_heavy_hash_tight": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_HASH_MAX": "8"},  # mixed per item
     "c5_light_global": {"EVOKE_C5_SHCAP": "64"},                       # k_c5_light, global regions
     "c5_mid": {"EVOKE_C5_LIGHT_REC": "0"},                             # k_c5_mid
     "c5_big_u32": dict(C5_BIG),                                        # k_c5_heavy<u32> + bitmaps
@@ -34,7 +37,7 @@ COMBOS = {
     "c5_big_nobits": dict(C5_BIG, EVOKE_C5_NO_BITS="1"),
     "c5_light_by_work": {"EVOKE_C5_LIGHT_WORK": "40", "EVOKE_C5_MID_WORK": "200"},
     "all_heavy_sorted": dict(HEAVY_PAIR, **C5_BIG, EVOKE_PAIR_PACKED_LIM="0", EVOKE_HUB_WARP_MAX="0",
-                             EVOKE_HUB_SH_DENSE="0", EVOKE_C5_WIDE="1", EVOKE_SORT_FULL_MIN="1"),
+                             EVOKE_HUB_HASH_MAX="0", EVOKE_HUB_SH_DENSE="0", EVOKE_C5_WIDE="1", EVOKE_SORT_FULL_MIN="1"),
 }
 
 
