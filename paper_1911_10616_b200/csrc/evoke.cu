@@ -1259,16 +1259,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       heavy_est_sorted = hk;
     }
     if (n_light + n_heavy > 0) {
-      int hb_per_sm = 0;
-      CK(cudaFuncSetAttribute(k_hub_process, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_SMEM));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hb_per_sm, k_hub_process, HUB_BT, HUB_SMEM));
+      int hb_per_sm = 0, lb_per_sm = 0;
+      CK(cudaFuncSetAttribute(k_hub_heavy<HUB_HBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_SMEM));
+      CK(cudaFuncSetAttribute(k_hub_light, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_SMEM));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hb_per_sm, k_hub_heavy<HUB_HBT>, HUB_HBT, HUB_SMEM));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lb_per_sm, k_hub_light, HUB_BT, HUB_SMEM));
       const char* hhg_env = getenv("EVOKE_HUB_HG");  // developer knob: hub-local CTAs
       // a short hub-local pass (few items) gets one CTA per SM, not as many as fit: its CTAs
       // placed ahead of the heavy pair sources' whole-SM CTAs delay those (config 2: 0.1 ms
-      // better); a long one (diamond-heavy graphs) keeps full occupancy (config 3: 4.6 s, not 6.7)
-      const int hub_ctas_per_sm =
-          ((int64_t)n_light + n_heavy <= HUB_FEW_ITEMS && !whole_gpu_passes) ? 1 : std::max(1, hb_per_sm);
-      const int hg = hhg_env ? std::max(1, atoi(hhg_env)) : std::min(std::max(1, hb_per_sm), hub_ctas_per_sm) * SM;
+      // better); a long one (diamond-heavy graphs) keeps full occupancy
+      const bool few = (int64_t)n_light + n_heavy <= HUB_FEW_ITEMS && !whole_gpu_passes;
+      const int hg = hhg_env ? std::max(1, atoi(hhg_env)) : (few ? 1 : std::max(1, hb_per_sm)) * SM;
+      const int lg = hhg_env ? std::max(1, atoi(hhg_env)) : (few ? 1 : std::max(1, lb_per_sm)) * SM;
       u32* gt = nullptr;
       int32_t* gl = nullptr;
       const int sh_dense_max = (int)env_cap("EVOKE_HUB_SH_DENSE", HUB_SH_DENSE);
@@ -1280,10 +1282,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       u64* r68 = Fp(F_R68);
       u64* r69 = Fp(F_R69);
       jobs.push_back({P_HUB, 2, [=, &C](cudaStream_t st) {
-        k_hub_process<<<hg, HUB_BT, HUB_SMEM, st>>>(g, Te, heavy_sorted, heavy_est_sorted, n_heavy, light, n_light,
-                                                    hcnt + 2, gt, gl, r68, r69, sh_dense_max, hash_max);
+        if (n_heavy > 0)
+          k_hub_heavy<HUB_HBT><<<hg, HUB_HBT, HUB_SMEM, st>>>(g, heavy_sorted, heavy_est_sorted, n_heavy, hcnt + 2, gt,
+                                                             gl, r68, r69, sh_dense_max, hash_max);
+        if (n_light > 0) k_hub_light<<<lg, HUB_BT, HUB_SMEM, st>>>(g, Te, light, n_light, hcnt + 3, r68, r69);
         if (n_micro > 0) k_hub_micro<<<grid_for(n_micro, 128, SM), 128, 0, st>>>(g, micro, n_micro, r68, r69);
-        C.launches += 1 + (n_micro > 0);
+        C.launches += (n_heavy > 0) + (n_light > 0) + (n_micro > 0);
       }});
     } else if (n_micro > 0) {
       u64* r68 = Fp(F_R68);

@@ -28,7 +28,8 @@
 #include "common.cuh"
 #include "sched.cuh"
 
-#define HUB_BT 256                                   // threads per CTA (8 warps)
+#define HUB_BT 256                                   // threads per CTA of the light-item kernel (8 warps)
+#define HUB_HBT 512                                  // threads per CTA of the heavy-item kernel
 #define HUB_WARP_CAP 1024                            // per-warp hash capacity (light items)
 #define HUB_WARP_MAX (HUB_WARP_CAP / 2)              // light item: est <= this
 #define HUB_SMEM (HUB_BT / 32 * HUB_WARP_CAP * 12)   // 96 KB dynamic shared memory
@@ -179,17 +180,18 @@ __global__ void k_hub_micro(DGraph g, const int32_t* __restrict__ items, int n_i
 //   HUB_T_GLPOS: a per-CTA global table by position with a touched list (larger hubs).
 // All three are left zeroed (shared memory is zero between items in every mode).
 enum { HUB_T_HASH = 0, HUB_T_SHPOS = 1, HUB_T_GLPOS = 2 };
-struct HubCtaShared {
+template <int BT>
+struct HubCtaSharedT {
   int next;  // group counter of the current pass
   int cnt;   // touched entries (global table)
   u64 r69;
-  u64 acc[HUB_BT / 32][32];  // per-warp sums of the current 32 middles (pass 2)
+  u64 acc[BT / 32][32];  // per-warp sums of the current 32 middles (pass 2)
 };
 
 __device__ __forceinline__ u32 hub_h0(int32_t x, u32 cap) { return __umulhi((u32)x * 0x9E3779B1u, cap); }
 
-template <int MODE>
-__device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubCtaShared& S,
+template <int MODE, int BT>
+__device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubCtaSharedT<BT>& S,
                              u32* __restrict__ gtab, int32_t* __restrict__ glist, u64* __restrict__ R68,
                              u64* __restrict__ R69) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -326,7 +328,7 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
   // pass 3: corners a, x and the hub v; clear the table
   u64 r69 = 0;
   if (MODE == HUB_T_HASH) {
-    for (u32 h = threadIdx.x; h < cap; h += HUB_BT) {
+    for (u32 h = threadIdx.x; h < cap; h += BT) {
       const int32_t kk = hkeys[h];
       if (kk == 0) continue;
       const u64 c2 = binom2(hval[h]);
@@ -338,7 +340,7 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
       }
     }
   } else if (MODE == HUB_T_SHPOS) {
-    for (int32_t p = threadIdx.x; p < dv; p += HUB_BT) {
+    for (int32_t p = threadIdx.x; p < dv; p += BT) {
       const u32 c = tab[p];
       if (!c) continue;
       tab[p] = 0u;
@@ -350,7 +352,7 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
     }
   } else {
     const int cnt = S.cnt;
-    for (int t = threadIdx.x; t < cnt; t += HUB_BT) {
+    for (int t = threadIdx.x; t < cnt; t += BT) {
       const int32_t p = glist[t];
       const u64 c2 = binom2(tab[p]);
       tab[p] = 0u;
@@ -463,24 +465,24 @@ __device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32
   __syncwarp();
 }
 
-// ---- persistent processing kernel -------------------------------------------------------
-__global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __restrict__ Te,
-                                                        const int32_t* __restrict__ heavy,
-                                                        const u32* __restrict__ heavy_est, int n_heavy,
-                                                        const int32_t* __restrict__ light, int n_light,
-                                                        int* __restrict__ counters, u32* __restrict__ gtabs,
-                                                        int32_t* __restrict__ glists, u64* __restrict__ R68,
-                                                        u64* __restrict__ R69, int sh_dense_max, int hash_max) {
+// ---- persistent kernels -------------------------------------------------------------------
+// Heavy items: one BT-thread CTA per item (persistent, est-sorted list), c(x) table chosen per
+// item (hash / shared by position / global by position).
+template <int BT>
+__global__ void __launch_bounds__(BT) k_hub_heavy(DGraph g, const int32_t* __restrict__ heavy,
+                                                  const u32* __restrict__ heavy_est, int n_heavy,
+                                                  int* __restrict__ counter, u32* __restrict__ gtabs,
+                                                  int32_t* __restrict__ glists, u64* __restrict__ R68,
+                                                  u64* __restrict__ R69, int sh_dense_max, int hash_max) {
   extern __shared__ u32 hub_sh[];
-  __shared__ HubCtaShared S;
+  __shared__ HubCtaSharedT<BT> S;
   __shared__ int s_idx;
-  __shared__ int s_cnt[HUB_BT / 32];
   u32* gtab = gtabs ? gtabs + (size_t)blockIdx.x * g.max_deg : nullptr;
   int32_t* glist = glists ? glists + (size_t)blockIdx.x * g.max_deg : nullptr;
-  for (int i = threadIdx.x; i < HUB_SMEM / 4; i += HUB_BT) hub_sh[i] = 0u;  // cleared by pass 3 after use
+  for (int i = threadIdx.x; i < HUB_SMEM / 4; i += BT) hub_sh[i] = 0u;  // cleared by pass 3 after use
   __syncthreads();
   for (;;) {
-    if (threadIdx.x == 0) s_idx = atomicAdd(&counters[0], 1);
+    if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
     __syncthreads();
     const int idx = s_idx;
     __syncthreads();
@@ -493,14 +495,24 @@ __global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __r
     const u64 bound = min(dv - 1, (u64)heavy_est[idx]);  // distinct x of the item
     if (bound <= (u64)hash_max) {
       const u32 cap = (u32)min((u64)HUB_HASH_SLOTS, bound + bound / 3 + 64);
-      hub_item_cta<HUB_T_HASH>(g, s, cap, hub_sh, S, gtab, glist, R68, R69);
+      hub_item_cta<HUB_T_HASH, BT>(g, s, cap, hub_sh, S, gtab, glist, R68, R69);
     } else if (dv <= (u64)sh_dense_max) {
-      hub_item_cta<HUB_T_SHPOS>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
+      hub_item_cta<HUB_T_SHPOS, BT>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
     } else {
-      hub_item_cta<HUB_T_GLPOS>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
+      hub_item_cta<HUB_T_GLPOS, BT>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
     }
   }
-  // light items: the dynamic shared memory becomes one hash (keys, counts, list) per warp
+}
+
+// Light items: every warp takes items from a counter (per-warp hash keyed by x in the
+// dynamic shared memory: keys, counts, touched list).
+__global__ void __launch_bounds__(HUB_BT) k_hub_light(DGraph g, const u32* __restrict__ Te,
+                                                      const int32_t* __restrict__ light, int n_light,
+                                                      int* __restrict__ counter, u64* __restrict__ R68,
+                                                      u64* __restrict__ R69) {
+  extern __shared__ u32 hub_sh[];
+  __shared__ int s_cnt[HUB_BT / 32];
+  __shared__ u64 s_acc[HUB_BT / 32][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   ShCount H;
   H.keys = (int32_t*)hub_sh + wib * (3 * HUB_WARP_CAP);
@@ -508,16 +520,16 @@ __global__ void __launch_bounds__(HUB_BT) k_hub_process(DGraph g, const u32* __r
   H.mask = HUB_WARP_CAP - 1;
   int32_t* L = H.keys + 2 * HUB_WARP_CAP;
   for (int t = lane; t < HUB_WARP_CAP; t += 32) { H.keys[t] = SH_EMPTY; H.val[t] = 0u; }
-  S.acc[wib][lane] = 0;
+  s_acc[wib][lane] = 0;
   if (lane == 0) s_cnt[wib] = 0;
   __syncwarp();
   for (;;) {
     int idx = 0;
-    if (lane == 0) idx = atomicAdd(&counters[1], 4);
+    if (lane == 0) idx = atomicAdd(counter, 4);
     idx = __shfl_sync(FULL_MASK, idx, 0);
     if (idx >= n_light) break;
     const int end = min(idx + 4, n_light);
     for (int q = idx; q < end; q++)
-      hub_item_warp(g, Te, light[q], H, L, &s_cnt[wib], S.acc[wib], R68, R69);
+      hub_item_warp(g, Te, light[q], H, L, &s_cnt[wib], s_acc[wib], R68, R69);
   }
 }
