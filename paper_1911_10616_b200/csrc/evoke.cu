@@ -1227,7 +1227,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* light = A.alloc<int32_t>(m2s);
     int32_t* heavy = A.alloc<int32_t>(m2s);
     u32* hest = A.alloc<u32>(m2s);
-    int* hcnt = A.alloc<int>(5, true);  // n_light, n_heavy, process counters [2], [3], n_micro [4]
+    int* hcnt = A.alloc<int>(8, true);  // n_light, n_heavy, counters [2], [3], [6], n_micro [4], n_giant [5]
     int32_t* micro = A.alloc<int32_t>(m2s);
     u64* hitem_est = A.alloc<u64>(m2s, true);
     if (ntri > 0)
@@ -1235,16 +1235,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     const uint8_t* hmine = shard_mask(A, C, hitem_est, m2s, si, ns, d_work + 2);
     const u64 hub_warp_max = env_cap("EVOKE_HUB_WARP_MAX", HUB_WARP_MAX);
     const u64 hub_micro_max = std::min(hub_warp_max, env_cap("EVOKE_HUB_MICRO_MAX", HUB_MICRO_MAX));
+    const u64 hub_giant = env_cap("EVOKE_HUB_GIANT", HUB_GIANT);
     k_hub_bin<<<grid_for(m2s, 256, SM), 256, 0, C.st>>>(g, Te, hitem_est, hmine, hub_micro_max, hub_warp_max, micro,
-                                                        hcnt + 4, light, hcnt, heavy, hest, hcnt + 1);
+                                                        hcnt + 4, light, hcnt, heavy, hest, hcnt + 1, hub_giant,
+                                                        hcnt + 5);
     C.launches += 2;
-    int hc[5];
+    int hc[6];
     CK(cudaMemcpyAsync(hc, hcnt, sizeof(hc), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     C.tick("hub_items+sync");
-    const int n_light = hc[0], n_heavy = hc[1], n_micro = hc[4];
+    const int n_light = hc[0], n_heavy = hc[1], n_micro = hc[4], n_giant = hc[5];
     if (getenv("EVOKE_DEBUG"))
-      fprintf(stderr, "[evoke] hub items: micro %d light %d heavy %d\n", n_micro, n_light, n_heavy);
+      fprintf(stderr, "[evoke] hub items: micro %d light %d heavy %d (giant %d)\n", n_micro, n_light, n_heavy, n_giant);
     int32_t* heavy_sorted = heavy;
     u32* heavy_est_sorted = hest;
     if (n_heavy > 1) {
@@ -1259,35 +1261,48 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       heavy_est_sorted = hk;
     }
     if (n_light + n_heavy > 0) {
+      // giant items (the est-sorted list's head): one 1024-thread CTA per SM with a large shared
+      // table; the other heavy items: 256-thread CTAs, four per SM (a CTA per item, and most
+      // items have too few middles to keep 32 warps busy)
+      auto kgiant = k_hub_heavy<1024, HUB_GSMEM>;
+      auto kheavy = k_hub_heavy<256, HUB_HSMEM>;
       int hb_per_sm = 0, lb_per_sm = 0;
-      CK(cudaFuncSetAttribute(k_hub_heavy<HUB_HBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_SMEM));
+      CK(cudaFuncSetAttribute(kgiant, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_GSMEM));
+      CK(cudaFuncSetAttribute(kheavy, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_HSMEM));
       CK(cudaFuncSetAttribute(k_hub_light, cudaFuncAttributeMaxDynamicSharedMemorySize, HUB_SMEM));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hb_per_sm, k_hub_heavy<HUB_HBT>, HUB_HBT, HUB_SMEM));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hb_per_sm, kheavy, 256, HUB_HSMEM));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lb_per_sm, k_hub_light, HUB_BT, HUB_SMEM));
       const char* hhg_env = getenv("EVOKE_HUB_HG");  // developer knob: hub-local CTAs
       // a short hub-local pass (few items) gets one CTA per SM, not as many as fit: its CTAs
       // placed ahead of the heavy pair sources' whole-SM CTAs delay those (config 2: 0.1 ms
       // better); a long one (diamond-heavy graphs) keeps full occupancy
       const bool few = (int64_t)n_light + n_heavy <= HUB_FEW_ITEMS && !whole_gpu_passes;
+      const int gg = std::max(1, std::min(n_giant, SM));
       const int hg = hhg_env ? std::max(1, atoi(hhg_env)) : (few ? 1 : std::max(1, hb_per_sm)) * SM;
       const int lg = hhg_env ? std::max(1, atoi(hhg_env)) : (few ? 1 : std::max(1, lb_per_sm)) * SM;
       u32* gt = nullptr;
       int32_t* gl = nullptr;
       const int sh_dense_max = (int)env_cap("EVOKE_HUB_SH_DENSE", HUB_SH_DENSE);
       const int hash_max = (int)env_cap("EVOKE_HUB_HASH_MAX", HUB_HASH_MAX);
-      if (g.max_deg > sh_dense_max && n_heavy > 0) {
-        gt = A.zalloc<u32>((size_t)hg * g.max_deg);
-        gl = A.alloc<int32_t>((size_t)hg * g.max_deg);
+      const int split = (int)std::max<u64>(1, env_cap("EVOKE_HUB_SPLIT", HUB_SPLIT));
+      if (n_heavy > 0 && (g.max_deg > std::min(sh_dense_max, HUB_HSMEM / 2) || g.max_deg >= 65536)) {
+        const int tg = std::max(gg, hg);
+        gt = A.zalloc<u32>((size_t)tg * g.max_deg);
+        gl = A.alloc<int32_t>((size_t)tg * g.max_deg);
       }
       u64* r68 = Fp(F_R68);
       u64* r69 = Fp(F_R69);
+      const int n_rest = n_heavy - n_giant;
       jobs.push_back({P_HUB, 2, [=, &C](cudaStream_t st) {
-        if (n_heavy > 0)
-          k_hub_heavy<HUB_HBT><<<hg, HUB_HBT, HUB_SMEM, st>>>(g, heavy_sorted, heavy_est_sorted, n_heavy, hcnt + 2, gt,
-                                                             gl, r68, r69, sh_dense_max, hash_max);
+        if (n_giant > 0)
+          kgiant<<<gg, 1024, HUB_GSMEM, st>>>(g, heavy_sorted, heavy_est_sorted, n_giant, hcnt + 2, gt, gl, r68, r69,
+                                              sh_dense_max, hash_max, split);
+        if (n_rest > 0)
+          kheavy<<<hg, 256, HUB_HSMEM, st>>>(g, heavy_sorted + n_giant, heavy_est_sorted + n_giant, n_rest, hcnt + 6,
+                                             gt, gl, r68, r69, sh_dense_max, hash_max, split);
         if (n_light > 0) k_hub_light<<<lg, HUB_BT, HUB_SMEM, st>>>(g, Te, light, n_light, hcnt + 3, r68, r69);
         if (n_micro > 0) k_hub_micro<<<grid_for(n_micro, 128, SM), 128, 0, st>>>(g, micro, n_micro, r68, r69);
-        C.launches += (n_heavy > 0) + (n_light > 0) + (n_micro > 0);
+        C.launches += (n_giant > 0) + (n_rest > 0) + (n_light > 0) + (n_micro > 0);
       }});
     } else if (n_micro > 0) {
       u64* r68 = Fp(F_R68);
@@ -1441,6 +1456,25 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     }
     if (!c5chain.empty())
       jobs.push_back({P_C5, 0, [c5chain](cudaStream_t st) { for (auto& f : c5chain) f(st); }});
+    if (n5l > 1 && !getenv("EVOKE_C5_BIN_ORDER")) {
+      // light endpoints grouped by anchor (L2 reuse of shared neighbourhoods)
+      u32* ak = A.alloc<u32>(n5l);
+      u32* ak2 = A.alloc<u32>(n5l);
+      int32_t* ai = A.alloc<int32_t>(n5l);
+      int32_t* ai2 = A.alloc<int32_t>(n5l);
+      k_c5_anchor<<<grid_for(n5l, B, SM), B, 0, C.st>>>(g, c5l, n5l, ak, ai);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ak, ak2, ai, ai2, n5l, 0, bits_for(n), C.st));
+      void* t2 = A.alloc<char>(tb);
+      CK(cub::DeviceRadixSort::SortPairs(t2, tb, ak, ak2, ai, ai2, n5l, 0, bits_for(n), C.st));
+      int32_t* lo = A.alloc<int32_t>(n5l);
+      u32* ro = A.alloc<u32>(n5l);
+      k_permute_c5<<<grid_for(n5l, B, SM), B, 0, C.st>>>(ai2, n5l, c5l, c5lr, lo, ro);
+      C.launches += 2;
+      C.lib_launches += 4;
+      c5l = lo;
+      c5lr = ro;
+    }
     if (n5l > 0) {
       int bps = 0;
       const char* shc_env = getenv("EVOKE_C5_SHCAP");  // developer knob: shared records per warp

@@ -166,13 +166,13 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
     for (int i = warp; i < cur; i += nwarps) {
       const int32_t v = L[i];
       for (int64_t s = rp[v] + lane; s < rp[v + 1]; s += 32) {
+        // no stamp test first: a stamped vertex had degree <= k when stamped and k only
+        // grows, so its decrement can never return k + 1 (one dependent load less per round)
         const int32_t w = adj[s];
-        if (rnd[w] < 0) {
-          const int old = atomicSub(&deg[w], 1);
-          if (old == k + 1) {
-            rnd[w] = round + 1;
-            Ln[atomicAdd(&ctl->cnt[c1], 1)] = w;
-          }
+        const int old = atomicSub(&deg[w], 1);
+        if (old == k + 1) {
+          rnd[w] = round + 1;
+          Ln[atomicAdd(&ctl->cnt[c1], 1)] = w;
         }
       }
     }
@@ -224,10 +224,6 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
   uint16_t* lq1 = lq0 + peel_switch;
   auto lq = [&](int q) { return q ? lq1 : lq0; };
   __shared__ int s_cnt[3], s_minv;
-  __shared__ int s_pre[PEEL_BT + 1];
-  __shared__ u32 s_base[PEEL_BT];
-  typedef cub::BlockScan<int, PEEL_BT> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
   if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_minv = 0x7fffffff;
   __syncthreads();
@@ -264,36 +260,23 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
     if (threadIdx.x == 0) s_cnt[c2] = 0;
     const uint16_t* L = lq(p);
     uint16_t* Ln = lq(p ^ 1);
-    // the frontier's local lists flattened over the CTA
-    for (int f0 = 0; f0 < cur; f0 += PEEL_BT) {
-      const int cn = min(PEEL_BT, cur - f0);
-      int len = 0;
-      if ((int)threadIdx.x < cn) {
-        const int l = L[f0 + threadIdx.x];
-        len = lc[l];
-        s_base[threadIdx.x] = lbeg[l];
-      }
-      int ex, tot;
-      Scan(scan_tmp).ExclusiveSum(len, ex, tot);
-      s_pre[threadIdx.x] = ex;
-      __syncthreads();
-      for (int t = threadIdx.x; t < tot; t += PEEL_BT) {
-        int lo = 0, hi = cn;  // largest lo with s_pre[lo] <= t
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_pre[mid] <= t) lo = mid; else hi = mid;
-        }
-        const int w = ladj[s_base[lo] + (u32)(t - s_pre[lo])];
-        if (lrnd[w] < 0) {
-          const int old = atomicSub(&ldeg[w], 1);
-          if (old == k + 1) {
-            lrnd[w] = round + 1;
-            Ln[atomicAdd(&s_cnt[c1], 1)] = (uint16_t)w;
-          }
+    // a warp per frontier vertex, its local list over the lanes (no scan or search: one
+    // barrier per round)
+    const int wl = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    for (int f = wl; f < cur; f += PEEL_BT / 32) {
+      const int l = L[f];
+      const u32 b0 = lbeg[l];
+      const int len = lc[l];
+      for (int t = ln; t < len; t += 32) {
+        const int w = ladj[b0 + (u32)t];
+        const int old = atomicSub(&ldeg[w], 1);  // stamped w: old <= k (see phase 1)
+        if (old == k + 1) {
+          lrnd[w] = round + 1;
+          Ln[atomicAdd(&s_cnt[c1], 1)] = (uint16_t)w;
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
     removed += cur;
     round++;
     p ^= 1;

@@ -29,16 +29,18 @@
 #include "sched.cuh"
 
 #define HUB_BT 256                                   // threads per CTA of the light-item kernel (8 warps)
-#define HUB_HBT 512                                  // threads per CTA of the heavy-item kernel
 #define HUB_WARP_CAP 1024                            // per-warp hash capacity (light items)
 #define HUB_WARP_MAX (HUB_WARP_CAP / 2)              // light item: est <= this
 #define HUB_SMEM (HUB_BT / 32 * HUB_WARP_CAP * 12)   // 96 KB dynamic shared memory
-#define HUB_SH_DENSE (HUB_SMEM / 4)                  // heavy item: shared counts by position if d(v) <= this
-#define HUB_HASH_SLOTS (HUB_SMEM / 8)                // heavy item: x-keyed shared hash, (x+1, count) slots ...
-#define HUB_HASH_MAX (HUB_HASH_SLOTS * 3 / 4)        // ... used when min(d(v)-1, est) <= this (load <= 0.75)
+#define HUB_GSMEM (200 << 10)                        // giant items: 1024-thread CTA (one per SM), this much shared memory
+#define HUB_HSMEM (44 << 10)                         // heavy items: 256-thread CTAs (four per SM), this much each
+#define HUB_GIANT (1u << 20)                         // item est above this: giant
+#define HUB_SH_DENSE (HUB_GSMEM / 2)                 // shared 16-bit counts by position if d(v) <= min(this, smem / 2)
+#define HUB_HASH_MAX (((HUB_GSMEM / 6) & ~1) * 3 / 4)  // x-keyed shared hash if min(d(v)-1, est) <= min(this, 3/4 slots)
 #define HUB_FEW_ITEMS 262144                         // at most this many items: one CTA per SM
 #define HUB_LONG 32                                  // heavy item: x-lists this long are streamed by a whole warp
 #define HUB_ILP 4                                    // ... with this many loads per lane in flight
+#define HUB_SPLIT 256                                // heavy item: longer x-lists are chunked over the CTA
 #define HUB_MICRO_MAX 16                             // micro item: est <= this, one THREAD per item
 
 // number of entries of the full list [f, f+len) with third vertex < bound: a binary search
@@ -76,7 +78,7 @@ __global__ void k_hub_est(DGraph g, const u32* __restrict__ Te, u64* __restrict_
 __global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __restrict__ est,
                           const uint8_t* __restrict__ mine, u64 micro_max, u64 warp_max, int32_t* __restrict__ micro,
                           int* n_micro, int32_t* __restrict__ light, int* n_light, int32_t* __restrict__ heavy,
-                          u32* __restrict__ heavy_est, int* n_heavy) {
+                          u32* __restrict__ heavy_est, int* n_heavy, u64 giant_min, int* n_giant) {
   const int lane = threadIdx.x & 31;
   const int64_t m2 = 2 * g.m;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < m2;
@@ -90,6 +92,10 @@ __global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __res
     warp_append(e > 0 && e <= micro_max, (int32_t)s, micro, n_micro);
     warp_append(e > micro_max && e <= warp_max, (int32_t)s, light, n_light);
     const bool is_heavy = e > warp_max;
+    {
+      const u32 gb = __ballot_sync(FULL_MASK, is_heavy && e > giant_min);
+      if (lane == 0 && gb) atomicAdd(n_giant, __popc(gb));
+    }
     const u32 bal = __ballot_sync(FULL_MASK, is_heavy);
     if (bal) {
       int hb = 0;
@@ -170,22 +176,35 @@ __global__ void k_hub_micro(DGraph g, const int32_t* __restrict__ items, int n_i
 
 // ---- heavy item: one CTA ----------------------------------------------------------------
 // The CTA's warps take the item's middles b in groups of 32 (a shared counter) and flatten
-// their x-lists over the lanes (warp_flat): no per-element search, and the pass-2 sums of a
-// middle stay in a lane's register while the lane stays on it.  c(x) lives in one of three
-// tables, chosen per item:
+// their short x-lists over the lanes (warp_flat): no per-element search, and the pass-2 sums
+// of a middle stay in a lane's register while the lane stays on it.  Lists of HUB_LONG or
+// more elements are streamed by a whole warp (HUB_ILP loads per lane in flight); lists longer
+// than HUB_SPLIT go to a CTA queue and are cut into HUB_SPLIT-element chunks that all warps
+// share, so one hub middle does not keep the other warps waiting at the pass barrier.
+// c(x) lives in one of three tables, chosen per item:
 //   HUB_T_HASH : shared open-addressing hash keyed by x (x+1, 0 = empty) when the number of
-//                distinct x, at most min(d(v)-1, est(v,a)), fits HUB_HASH_MAX -- no per-element
+//                distinct x, at most min(d(v)-1, est(v,a)), fits hash_max -- no per-element
 //                position lookup (fe1/fe2 and the slot map of x in N(v) are never read);
 //   HUB_T_SHPOS: shared counts dense by x's position in N(v) (d(v) <= sh_dense_max), swept;
-//   HUB_T_GLPOS: a per-CTA global table by position with a touched list (larger hubs).
-// All three are left zeroed (shared memory is zero between items in every mode).
+//   HUB_T_GLPOS: a per-CTA global u32 table by position with a touched list (larger hubs).
+// The shared tables hold 16-bit counts, two per word: c(x) <= #middles <= T(v,a) < 2^16
+// (checked per item), so an increment never carries into the neighbouring count.  All three
+// are left zeroed (shared memory is zero between items in every mode).
 enum { HUB_T_HASH = 0, HUB_T_SHPOS = 1, HUB_T_GLPOS = 2 };
+#define HUB_QCAP 256   // queued long lists per CTA and pass
 template <int BT>
 struct HubCtaSharedT {
-  int next;  // group counter of the current pass
-  int cnt;   // touched entries (global table)
+  int next;   // group counter of the current pass
+  int cnt;    // touched entries (global table)
+  int qn;     // queued long lists
+  int qnext;  // chunk counter of the queue
   u64 r69;
   u64 acc[BT / 32][32];  // per-warp sums of the current 32 middles (pass 2)
+  int64_t qfb[HUB_QCAP];
+  int qlen[HUB_QCAP];
+  int32_t qb[HUB_QCAP];
+  int qc0[HUB_QCAP + 1];  // first chunk of every queued list
+  bool qvl[HUB_QCAP];
 };
 
 __device__ __forceinline__ u32 hub_h0(int32_t x, u32 cap) { return __umulhi((u32)x * 0x9E3779B1u, cap); }
@@ -193,7 +212,7 @@ __device__ __forceinline__ u32 hub_h0(int32_t x, u32 cap) { return __umulhi((u32
 template <int MODE, int BT>
 __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubCtaSharedT<BT>& S,
                              u32* __restrict__ gtab, int32_t* __restrict__ glist, u64* __restrict__ R68,
-                             u64* __restrict__ R69) {
+                             u64* __restrict__ R69, int split) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int32_t eva = g.eid[s];
   const int32_t a = g.ci[s];
@@ -205,14 +224,68 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
   const int64_t fa = g.foff[eva];
   const int na = full_prefix(g, fa, (int)(g.foff[eva + 1] - fa), a);  // b < a (or all, filtered)
   int32_t* hkeys = reinterpret_cast<int32_t*>(shm);                 // HUB_T_HASH: x + 1
-  u32* hval = shm + cap;
-  u32* tab = MODE == HUB_T_GLPOS ? gtab : shm;                       // by position
+  u32* c16 = MODE == HUB_T_HASH ? shm + cap : shm;                   // shared 16-bit counts
+  u32* tab = gtab;                                                   // HUB_T_GLPOS
   u64* acc = S.acc[wib];
   if (threadIdx.x == 0) { S.cnt = 0; S.r69 = 0; }
   acc[lane] = 0;
+  // the count slot of x (pass 1: found or claimed; pass 2: found -- every x of pass 2 was
+  // inserted by pass 1); r2 = x's entry in the full list, vlj: fe1 holds e(v,x)
+  auto slot_of = [&](int pass, int32_t x, int64_t r2, bool vlj) -> u32 {
+    if (MODE == HUB_T_HASH) {
+      u32 h = hub_h0(x, cap);
+      if (pass == 1) {
+        for (;;) {
+          const int32_t kk = hkeys[h];
+          if (kk == x + 1) break;
+          if (kk == 0) {
+            const int32_t o = atomicCAS(&hkeys[h], 0, x + 1);
+            if (o == 0 || o == x + 1) break;
+          }
+          h = (h + 1 == cap) ? 0 : h + 1;
+        }
+      } else {
+        while (hkeys[h] != x + 1) h = (h + 1 == cap) ? 0 : h + 1;
+      }
+      return h;
+    }
+    const int32_t evx = vlj ? g.fe1[r2] : g.fe2[r2];
+    return (u32)pos_in_list(g, v, x, evx);
+  };
+  auto bump = [&](u32 h) {
+    if (MODE == HUB_T_GLPOS) {
+      if (atomicAdd(&tab[h], 1u) == 0u) glist[atomicAdd(&S.cnt, 1)] = (int32_t)h;
+    } else {
+      atomicAdd(&c16[h >> 1], 1u << ((h & 1) * 16));
+    }
+  };
+  auto count = [&](u32 h) -> u64 {
+    if (MODE == HUB_T_GLPOS) return (u64)tab[h];
+    return (u64)((c16[h >> 1] >> ((h & 1) * 16)) & 0xffffu);
+  };
+  // the whole warp streams elements [k0, k1) of one list; returns the lane's pass-2 sum
+  auto stream = [&](int pass, int64_t fbj, int k0, int k1, bool vlj) -> u64 {
+    u64 sum = 0;
+    for (int kb = k0; kb < k1; kb += 32 * HUB_ILP) {
+      int32_t xs[HUB_ILP];
+#pragma unroll
+      for (int u = 0; u < HUB_ILP; u++) {
+        const int k = kb + 32 * u + lane;
+        xs[u] = k < k1 ? g.fx[fbj + k] : a;
+      }
+#pragma unroll
+      for (int u = 0; u < HUB_ILP; u++) {
+        if (xs[u] >= a) continue;
+        const u32 h = slot_of(pass, xs[u], fbj + kb + 32 * u + lane, vlj);
+        if (pass == 1) bump(h);
+        else sum += count(h) - 1ull;
+      }
+    }
+    return sum;
+  };
 #pragma unroll 1
   for (int pass = 1; pass <= 2; pass++) {
-    if (threadIdx.x == 0) S.next = 0;
+    if (threadIdx.x == 0) { S.next = 0; S.qn = 0; S.qnext = 0; }
     __syncthreads();
     for (;;) {
       int i0 = 0;
@@ -234,35 +307,15 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
           if (MODE != HUB_T_HASH) vl = g.esrc[evb] == v;
         }
       }
-      // the count cell of x (pass 1: found or claimed; pass 2: found -- every x of pass 2 was
-      // inserted by pass 1); r2 = x's entry in the full list, vlj: fe1 holds e(v,x)
-      auto cell_of = [&](int32_t x, int64_t r2, bool vlj) -> u32* {
-        if (MODE == HUB_T_HASH) {
-          u32 h = hub_h0(x, cap);
-          if (pass == 1) {
-            for (;;) {
-              const int32_t kk = hkeys[h];
-              if (kk == x + 1) break;
-              if (kk == 0) {
-                const int32_t o = atomicCAS(&hkeys[h], 0, x + 1);
-                if (o == 0 || o == x + 1) break;
-              }
-              h = (h + 1 == cap) ? 0 : h + 1;
-            }
-          } else {
-            while (hkeys[h] != x + 1) h = (h + 1 == cap) ? 0 : h + 1;
-          }
-          return &hval[h];
+      // very long lists: to the CTA queue (chunks shared by all warps) while it has room
+      if (len > split) {
+        const int q = atomicAdd(&S.qn, 1);
+        if (q < HUB_QCAP) {
+          S.qfb[q] = fb; S.qlen[q] = len; S.qb[q] = b; S.qvl[q] = vl;
+          len = 0;
         }
-        const int32_t evx = vlj ? g.fe1[r2] : g.fe2[r2];
-        return &tab[pos_in_list(g, v, x, evx)];
-      };
-      auto bump = [&](u32* cell) {
-        const u32 old = atomicAdd(cell, 1u);
-        if (MODE == HUB_T_GLPOS && old == 0u) glist[atomicAdd(&S.cnt, 1)] = (int32_t)(cell - tab);
-      };
-      // long lists: the whole warp streams one list at a time, HUB_ILP loads per lane in
-      // flight, and the middle's pass-2 sum is one warp reduction
+      }
+      // long lists: the whole warp streams one list at a time
       unsigned lm = __ballot_sync(FULL_MASK, len >= HUB_LONG);
       while (lm) {
         const int j = __ffs(lm) - 1;
@@ -271,26 +324,8 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
         const int lenj = __shfl_sync(FULL_MASK, len, j);
         const bool vlj = MODE != HUB_T_HASH && __shfl_sync(FULL_MASK, vl, j);
         const int32_t bj = __shfl_sync(FULL_MASK, b, j);
-        u64 sum = 0;
-        for (int k0 = 0; k0 < lenj; k0 += 32 * HUB_ILP) {
-          int32_t xs[HUB_ILP];
-#pragma unroll
-          for (int u = 0; u < HUB_ILP; u++) {
-            const int k = k0 + 32 * u + lane;
-            xs[u] = k < lenj ? g.fx[fbj + k] : a;
-          }
-#pragma unroll
-          for (int u = 0; u < HUB_ILP; u++) {
-            if (xs[u] >= a) continue;
-            u32* c = cell_of(xs[u], fbj + k0 + 32 * u + lane, vlj);
-            if (pass == 1) bump(c);
-            else sum += (u64)*c - 1ull;
-          }
-        }
-        if (pass == 2) {
-          sum = warp_sum(sum);
-          if (lane == 0 && sum) atomicAdd(&R68[bj], sum);
-        }
+        const u64 sum = warp_sum(stream(pass, fbj, 0, lenj, vlj));
+        if (pass == 2 && lane == 0 && sum) atomicAdd(&R68[bj], sum);
         if (lane == j) len = 0;
       }
       int cur = -1;
@@ -302,16 +337,16 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
         const int64_t r2 = fbj + k;
         const int32_t x = g.fx[r2];
         if (x >= a) return;
-        u32* cell = cell_of(x, r2, vlj);
+        const u32 h = slot_of(pass, x, r2, vlj);
         if (pass == 1) {
-          bump(cell);
+          bump(h);
         } else {
           if (j != cur) {
             if (cur >= 0 && cacc) atomicAdd(&acc[cur], cacc);
             cur = j;
             cacc = 0;
           }
-          cacc += (u64)*cell - 1ull;  // middles b get sum over their x of c(x) - 1
+          cacc += count(h) - 1ull;  // middles b get sum over their x of c(x) - 1
         }
       });
       if (pass == 2) {
@@ -324,6 +359,33 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
       }
     }
     __syncthreads();
+    // the queued lists, in HUB_SPLIT-element chunks over all warps
+    const int nq = min(S.qn, HUB_QCAP);
+    if (nq > 0) {
+      if (threadIdx.x == 0) {
+        int c = 0;
+        for (int q = 0; q < nq; q++) { S.qc0[q] = c; c += (S.qlen[q] + split - 1) / split; }
+        S.qc0[nq] = c;
+      }
+      __syncthreads();
+      const int nchunks = S.qc0[nq];
+      for (;;) {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(&S.qnext, 1);
+        c = __shfl_sync(FULL_MASK, c, 0);
+        if (c >= nchunks) break;
+        int lo = 0, hi = nq;  // the list of chunk c: largest lo with qc0[lo] <= c
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (S.qc0[mid] <= c) lo = mid; else hi = mid;
+        }
+        const int k0 = (c - S.qc0[lo]) * split;
+        const int k1 = min(S.qlen[lo], k0 + split);
+        const u64 sum = warp_sum(stream(pass, S.qfb[lo], k0, k1, S.qvl[lo]));
+        if (pass == 2 && lane == 0 && sum) atomicAdd(&R68[S.qb[lo]], sum);
+      }
+      __syncthreads();
+    }
   }
   // pass 3: corners a, x and the hub v; clear the table
   u64 r69 = 0;
@@ -331,25 +393,25 @@ __device__ void hub_item_cta(const DGraph& g, int32_t s, u32 cap, u32* shm, HubC
     for (u32 h = threadIdx.x; h < cap; h += BT) {
       const int32_t kk = hkeys[h];
       if (kk == 0) continue;
-      const u64 c2 = binom2(hval[h]);
+      const u64 c2 = binom2(count(h));
       hkeys[h] = 0;
-      hval[h] = 0u;
       if (c2) {
         r69 += c2;
         atomicAdd(&R68[kk - 1], c2);
       }
     }
+    __syncthreads();
+    for (u32 w = threadIdx.x; w < (cap + 1) / 2; w += BT) c16[w] = 0u;
   } else if (MODE == HUB_T_SHPOS) {
     for (int32_t p = threadIdx.x; p < dv; p += BT) {
-      const u32 c = tab[p];
-      if (!c) continue;
-      tab[p] = 0u;
-      const u64 c2 = binom2(c);
+      const u64 c2 = binom2(count((u32)p));
       if (c2) {
         r69 += c2;
         atomicAdd(&R68[g.ci[rpv + p]], c2);
       }
     }
+    __syncthreads();
+    for (int32_t w = threadIdx.x; w < (dv + 1) / 2; w += BT) c16[w] = 0u;
   } else {
     const int cnt = S.cnt;
     for (int t = threadIdx.x; t < cnt; t += BT) {
@@ -468,18 +530,19 @@ __device__ void hub_item_warp(const DGraph& g, const u32* __restrict__ Te, int32
 // ---- persistent kernels -------------------------------------------------------------------
 // Heavy items: one BT-thread CTA per item (persistent, est-sorted list), c(x) table chosen per
 // item (hash / shared by position / global by position).
-template <int BT>
+template <int BT, int SMEM>
 __global__ void __launch_bounds__(BT) k_hub_heavy(DGraph g, const int32_t* __restrict__ heavy,
                                                   const u32* __restrict__ heavy_est, int n_heavy,
                                                   int* __restrict__ counter, u32* __restrict__ gtabs,
                                                   int32_t* __restrict__ glists, u64* __restrict__ R68,
-                                                  u64* __restrict__ R69, int sh_dense_max, int hash_max) {
+                                                  u64* __restrict__ R69, int sh_dense_max, int hash_max, int split) {
   extern __shared__ u32 hub_sh[];
   __shared__ HubCtaSharedT<BT> S;
   __shared__ int s_idx;
+  constexpr u32 kSlots = (SMEM / 6) & ~1u;  // (x+1, 16-bit count) hash slots
   u32* gtab = gtabs ? gtabs + (size_t)blockIdx.x * g.max_deg : nullptr;
   int32_t* glist = glists ? glists + (size_t)blockIdx.x * g.max_deg : nullptr;
-  for (int i = threadIdx.x; i < HUB_SMEM / 4; i += BT) hub_sh[i] = 0u;  // cleared by pass 3 after use
+  for (int i = threadIdx.x; i < SMEM / 4; i += BT) hub_sh[i] = 0u;  // cleared by pass 3 after use
   __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) s_idx = atomicAdd(counter, 1);
@@ -493,13 +556,14 @@ __global__ void __launch_bounds__(BT) k_hub_heavy(DGraph g, const int32_t* __res
     const int32_t v = g.esrc[eva] + g.edst[eva] - a;
     const u64 dv = (u64)g.deg[v];
     const u64 bound = min(dv - 1, (u64)heavy_est[idx]);  // distinct x of the item
-    if (bound <= (u64)hash_max) {
-      const u32 cap = (u32)min((u64)HUB_HASH_SLOTS, bound + bound / 3 + 64);
-      hub_item_cta<HUB_T_HASH, BT>(g, s, cap, hub_sh, S, gtab, glist, R68, R69);
-    } else if (dv <= (u64)sh_dense_max) {
-      hub_item_cta<HUB_T_SHPOS, BT>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
+    const bool c16 = g.foff[eva + 1] - g.foff[eva] < 65536;  // T(v,a) bounds every c(x)
+    if (c16 && bound <= (u64)min(hash_max, (int)(kSlots * 3 / 4))) {
+      const u32 cap = (u32)min((u64)kSlots, bound + bound / 3 + 64);
+      hub_item_cta<HUB_T_HASH, BT>(g, s, cap, hub_sh, S, gtab, glist, R68, R69, split);
+    } else if (c16 && dv <= (u64)min(sh_dense_max, SMEM / 2)) {
+      hub_item_cta<HUB_T_SHPOS, BT>(g, s, 0, hub_sh, S, gtab, glist, R68, R69, split);
     } else {
-      hub_item_cta<HUB_T_GLPOS, BT>(g, s, 0, hub_sh, S, gtab, glist, R68, R69);
+      hub_item_cta<HUB_T_GLPOS, BT>(g, s, 0, hub_sh, S, gtab, glist, R68, R69, split);
     }
   }
 }

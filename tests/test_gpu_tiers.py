@@ -30,6 +30,9 @@ COMBOS = {
     "hub_heavy_global": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_HASH_MAX": "0",
                          "EVOKE_HUB_SH_DENSE": "0"},                  # <HUB_T_GLPOS>
     "hub_heavy_hash_tight": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_HASH_MAX": "8"},  # mixed per item
+    "hub_giant": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_GIANT": "40"},  # k_hub_heavy<1024> + <256>
+    "hub_split_queue": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_SPLIT": "40"},  # long lists chunked over the CTA
+    "hub_giant_positions": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_GIANT": "0", "EVOKE_HUB_HASH_MAX": "0"},
     "c5_light_global": {"EVOKE_C5_SHCAP": "64"},                       # k_c5_light, global regions
     "c5_mid": {"EVOKE_C5_LIGHT_REC": "0"},                             # k_c5_mid
     "c5_big_u32": dict(C5_BIG),                                        # k_c5_heavy<u32> + bitmaps
