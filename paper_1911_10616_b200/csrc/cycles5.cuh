@@ -612,26 +612,6 @@ __global__ void k_c5_bin(DGraph g, const u64* __restrict__ W, const u64* __restr
   }
 }
 
-// Locality order of a tier's endpoints: key = the anchor of l, its neighbour w with the most
-// common neighbours T(l,w) (ties: lower w).  Endpoints that share an anchor share much of
-// their 2-hop neighbourhood (a vertex attached to a hub tends to be attached to the hub's
-// neighbours too), so processing them side by side lets their list reads hit in L2.  The
-// order changes no result (every credit is an integer atomic sum).
-__global__ void k_c5_anchor(DGraph g, const int32_t* __restrict__ list, int n_list, u32* __restrict__ key,
-                            int32_t* __restrict__ idx) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_list; q += gridDim.x * blockDim.x) {
-    const int32_t l = list[q];
-    u32 bt = 0;
-    int32_t bw = l;
-    for (int64_t s = g.rp[l]; s < g.rp[l + 1]; s++) {
-      const u32 t = g.tes[s];
-      if (t > bt) { bt = t; bw = g.ci[s]; }  // ascending list: the first maximum is the lowest w
-    }
-    key[q] = (u32)bw;
-    idx[q] = q;
-  }
-}
-
 // Heavy endpoints: one CTA each, dense records per CTA (persistent, W-sorted list).
 template <typename V>
 __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __restrict__ Tlow,

@@ -1456,25 +1456,6 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     }
     if (!c5chain.empty())
       jobs.push_back({P_C5, 0, [c5chain](cudaStream_t st) { for (auto& f : c5chain) f(st); }});
-    if (n5l > 1 && !getenv("EVOKE_C5_BIN_ORDER")) {
-      // light endpoints grouped by anchor (L2 reuse of shared neighbourhoods)
-      u32* ak = A.alloc<u32>(n5l);
-      u32* ak2 = A.alloc<u32>(n5l);
-      int32_t* ai = A.alloc<int32_t>(n5l);
-      int32_t* ai2 = A.alloc<int32_t>(n5l);
-      k_c5_anchor<<<grid_for(n5l, B, SM), B, 0, C.st>>>(g, c5l, n5l, ak, ai);
-      size_t tb = 0;
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ak, ak2, ai, ai2, n5l, 0, bits_for(n), C.st));
-      void* t2 = A.alloc<char>(tb);
-      CK(cub::DeviceRadixSort::SortPairs(t2, tb, ak, ak2, ai, ai2, n5l, 0, bits_for(n), C.st));
-      int32_t* lo = A.alloc<int32_t>(n5l);
-      u32* ro = A.alloc<u32>(n5l);
-      k_permute_c5<<<grid_for(n5l, B, SM), B, 0, C.st>>>(ai2, n5l, c5l, c5lr, lo, ro);
-      C.launches += 2;
-      C.lib_launches += 4;
-      c5l = lo;
-      c5lr = ro;
-    }
     if (n5l > 0) {
       int bps = 0;
       const char* shc_env = getenv("EVOKE_C5_SHCAP");  // developer knob: shared records per warp
