@@ -169,6 +169,9 @@ __device__ __forceinline__ u64 c5_wn(const C5RecL* r) { return (u64)(r->wf & (u3
 #define C5_MID_CAP (2 * C5_MID_MAX)  // hashed records in a per-CTA global region (load <= 0.5)
 #define C5_MBT 128                // mid-endpoint CTA (several endpoints in flight per SM)
 #define C5_BITS_SMEM_MAX (160 << 10)  // heavy CTAs: shared first-touch bitmaps up to this size
+#define C5_HOT_MAX 16384              // heavy CTAs (u32 records): hot-vertex cache of up to this many top ranks
+#define C5_SMEM_MAX (208 << 10)       // heavy CTAs: bitmaps + hot cache within this
+#define C5_HOT_MIN_W (1ull << 22)     // hot cache only when the largest big endpoint's W(l) reaches this
 #define C5_FB_WARP 128            // i-key filter words per light warp (4096 bits)
 #define C5_FB_CTA 256             // i-key filter words per mid CTA (8192 bits)
 
@@ -211,11 +214,50 @@ struct C5Dense {
     atomicOr(&r->wf, (bits | C5_PRESENT) << 28);  // result unused: a reduction
     return r;
   }
+  // Hot-vertex cache (big endpoints of large graphs, u32 records): the step-3 path ends i
+  // are out-neighbours of out-neighbours, which in the degeneracy order concentrate on the
+  // highest ranks (the dense core).  For i >= hot0, Wn[i] is mirrored in shared memory by
+  // step 1 and step 3 adds P[i] and A[i] with shared atomics, flushed into the records once
+  // per endpoint (hot_flush) -- instead of an L2 load and one or two L2 atomics per path.
+  u32* hWn = nullptr;
+  u32* hP = nullptr;
+  u32* hA = nullptr;
+  int32_t hot0 = 0x7fffffff;
+  int hotK = 0;
   // step-1 mark of a wedge end: Wn += 1 (its first mark makes it an i-key: Wn > 0)
   __device__ __forceinline__ Rec* mark_wedge(int32_t x) {
     Rec* r = mark_nr(x, C5_I);
     atomicAdd(&r->wf, 1u);
+    if (x >= hot0) atomicAdd(&hWn[x - hot0], 1u);
     return r;
+  }
+  // step 3 for a hot path end i: true if i is hot (wn = Wn[i]; P, A added when wn > 0)
+  __device__ __forceinline__ bool hot_pa(int32_t i, u64 q, bool adj, u64& wn) {
+    if (i < hot0) return false;
+    const int x = i - hot0;
+    wn = hWn[x];
+    if (wn) {
+      atomicAdd(&hP[x], (u32)q);
+      if (adj) atomicAdd(&hA[x], (u32)q);
+    }
+    return true;
+  }
+  // after step 3 (all threads, between barriers): P, A of the hot records; clear the cache
+  template <typename Eng>
+  __device__ __forceinline__ void hot_flush(const Eng& eng) {
+    if constexpr (sizeof(Rec) == sizeof(C5RecT<u32>)) {
+      for (int x = eng.tid(); x < hotK; x += eng.nthr()) {
+        const u32 p = hP[x], a = hA[x];
+        if (p | a) {
+          Rec* r = &R[hot0 + x];
+          r->P += p;  // this thread is the records' only writer now
+          r->A += a;
+          hP[x] = 0u;
+          hA[x] = 0u;
+        }
+        hWn[x] = 0u;
+      }
+    }
   }
   // step-2 mark of a j-key with its Q, QT, QM updates
   __device__ __forceinline__ Rec* mark_j_q(int32_t x, u32 th, u32 tm, bool& newj) {
@@ -333,6 +375,9 @@ struct C5Hash {
     x = r->key - 1;
     return r;
   }
+  __device__ __forceinline__ bool hot_pa(int32_t, u64, bool, u64&) const { return false; }
+  template <typename Eng>
+  __device__ __forceinline__ void hot_flush(const Eng&) const {}
   __device__ __forceinline__ int32_t id_of(int32_t idx) const { return R[idx].key - 1; }  // slot -> vertex
 };
 
@@ -438,9 +483,11 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         // record is created for such i (Wn is final after step 1).
         const int32_t i = g.ocol[base + k];
         if (i == l) return 0;
+        const auto* rj = &loc.R[J[t]];
+        u64 wn;
+        if (loc.hot_pa(i, rec_q(rj), c5_flags(rj) & C5_ADJ, wn)) return wn;
         auto* ri = loc.peek_i(i);
         if (!ri) return 0;
-        const auto* rj = &loc.R[J[t]];
         rec_add_pa(ri, rec_q(rj), c5_flags(rj) & C5_ADJ);
         return c5_wn(ri);
       },
@@ -460,6 +507,8 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
     const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rec_qt(rj) - q * lj);
     if (c) atomicAdd(&C5[j], (u64)0 - c);
   }
+  eng.sync();
+  loc.hot_flush(eng);
   eng.sync();
   C5_PHASE(3);
   // ---- step 4: k credits
@@ -619,7 +668,7 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
                                                     const int32_t* __restrict__ heavy, int n_heavy,
                                                     int* __restrict__ counter, C5RecT<V>* __restrict__ dense,
                                                     int32_t* __restrict__ dlists, u64* __restrict__ C5,
-                                                    int32_t* __restrict__ qmem, int use_bits) {
+                                                    int32_t* __restrict__ qmem, int use_bits, int hot_k) {
   __shared__ ListEng E;
   if (threadIdx.x == 0) {
     E.qcap = g.max_deg;
@@ -636,6 +685,16 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
     for (int i = threadIdx.x; i < 2 * nwd; i += blockDim.x) c5_bits[i] = 0u;
     loc.bP = c5_bits;
     loc.bJ = c5_bits + nwd;
+    __syncthreads();
+  }
+  if (hot_k > 0) {  // (u32 records only; the host passes 0 otherwise)
+    u32* hb = c5_bits + (use_bits ? 2 * ((g.n + 31) >> 5) : 0);
+    for (int i = threadIdx.x; i < 3 * hot_k; i += blockDim.x) hb[i] = 0u;
+    loc.hWn = hb;
+    loc.hP = hb + hot_k;
+    loc.hA = hb + 2 * hot_k;
+    loc.hot0 = g.n - hot_k;
+    loc.hotK = hot_k;
     __syncthreads();
   }
   loc.R = dense + (size_t)blockIdx.x * g.n;

@@ -1143,6 +1143,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       heavy_budget -= pg * per_cta;
       return (int)pg;
     };
+    // hot entries of the heavy tables: the top ranks in shared memory (EVOKE_PAIR_HOT: count cap)
+    auto pair_hot_k = [&](int word) {
+      return (int)std::min<int64_t>({(int64_t)env_cap("EVOKE_PAIR_HOT", PAIR_HOT_BYTES / word), (int64_t)n,
+                                     (int64_t)(PAIR_HOT_BYTES / word)});
+    };
     if (ht[PT_G64] > 0) {
       // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables
       const int pg = heavy_grid(ht[PT_G64], 8, SM);
@@ -1153,8 +1158,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const int cnt = ht[PT_G64];
       const int qcap = heavy_qcap;
       char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
+      const int hk = pair_hot_k(8);
+      CK(cudaFuncSetAttribute(k_pairs_heavy<u64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hk * 8));
       jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
-        k_pairs_heavy<u64, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap);
+        k_pairs_heavy<u64, false><<<pg, PAIR_HBT, hk * 8, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap,
+                                                                hk);
         C.launches++;
       }});
     }
@@ -1168,11 +1176,16 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const int cnt = ht[tier];
       const int qcap = heavy_qcap;
       char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
+      const int hk = pair_hot_k(4);
+      CK(cudaFuncSetAttribute(k_pairs_heavy<u32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hk * 4));
+      CK(cudaFuncSetAttribute(k_pairs_heavy<u32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hk * 4));
       jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
         if (tier == PT_G32S)
-          k_pairs_heavy<u32, true><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap);
+          k_pairs_heavy<u32, true><<<pg, PAIR_HBT, hk * 4, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem,
+                                                                 qcap, hk);
         else
-          k_pairs_heavy<u32, false><<<pg, PAIR_HBT, 0, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem, qcap);
+          k_pairs_heavy<u32, false><<<pg, PAIR_HBT, hk * 4, st>>>(g, Te, pl, cnt, counter, tabs, lists, po, qmem,
+                                                                  qcap, hk);
         C.launches++;
       }});
     }
@@ -1420,18 +1433,25 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       // first-touch bitmaps (present, j-key) in shared memory when they fit
       const size_t bits_smem = (size_t)2 * ((n + 31) / 32) * sizeof(u32);
       const int use_bits = bits_smem <= C5_BITS_SMEM_MAX && !getenv("EVOKE_C5_NO_BITS") ? 1 : 0;
-      const size_t bsm = use_bits ? bits_smem : 0;
-      if (use_bits) {
+      // hot-vertex cache of the top ranks (u32 records): 12 bytes per cached vertex
+      const size_t bits_b = use_bits ? bits_smem : 0;
+      // (only when the big endpoints are large enough to repay the shared memory taken from L1)
+      const int hot_k = (!narrow || wmax < env_cap("EVOKE_C5_HOT_MIN_W", C5_HOT_MIN_W)) ? 0
+                        : (int)std::min<int64_t>({(int64_t)env_cap("EVOKE_C5_HOT", C5_HOT_MAX), (int64_t)n,
+                                                  (int64_t)((C5_SMEM_MAX - bits_b) / 12)});
+      const size_t bsm = bits_b + (size_t)12 * hot_k;
+      if (bsm > 0) {
         CK(cudaFuncSetAttribute(k_c5_heavy<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
         CK(cudaFuncSetAttribute(k_c5_heavy<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
       }
       c5chain.push_back([=, &C](cudaStream_t st) {
         if (narrow)
           k_c5_heavy<u32><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 6,
-                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq, use_bits);
+                                                   reinterpret_cast<C5RecT<u32>*>(dense), dl, C5out, lq, use_bits,
+                                                   hot_k);
         else
           k_c5_heavy<u64><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 6,
-                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, use_bits);
+                                                   reinterpret_cast<C5Rec*>(dense), dl, C5out, lq, use_bits, 0);
         C.launches++;
       });
     }

@@ -62,6 +62,7 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_WARP_CAP 1024       // light tier: per-warp packed hash entries (8 warps x 8 KB)
 #define PAIR_WARP_MAX 512        // light tier: est <= this
 #define PAIR_HBT 1024            // heavy tier CTA
+#define PAIR_HOT_BYTES (192 << 10)  // heavy tier: shared table entries of the top ranks (hot x)
 
 #define PAIR_LONG 64             // item part longer than this: chunked, shared queue
 #define PAIR_CHUNK 256           // elements per long-item chunk (8 per lane)
@@ -148,16 +149,23 @@ struct GlobalDense {
   // entries are found by sweeping the whole table (16-byte loads).  Otherwise the first
   // update of an entry appends x to the touched list L (entry sweep, reset).
   // Reads go through L2 (__ldcg): the entries are updated by L2 atomics.
+  // Hot entries: x >= hot0 (the hotK highest ranks, where the 2-hop ends of a hub source
+  // concentrate in the degeneracy order) live in shared memory instead (hot[x - hot0]):
+  // shared atomics, swept by for_each_mut / reset, never on the touched list.
   static constexpr bool kDense = true;
   typedef Word WordT;
   Word* t;
   int32_t* L;
   int* ntouch;  // shared counter
   int32_t n;
+  Word* hot = nullptr;
+  int32_t hot0 = 0x7fffffff;
+  int hotK = 0;
   static constexpr int SH = (int)sizeof(Word) * 4;
   static constexpr Word LOW = (Word)(((u64)1 << SH) - 1);
   static constexpr int PER = 16 / (int)sizeof(Word);
   __device__ __forceinline__ Word raw_add(int32_t x, Word inc) {
+    if (x >= hot0) return atomicAdd(&hot[x - hot0], inc);
     if (SCAN) {
       atomicAdd(&t[x], inc);
       return (Word)1;
@@ -165,29 +173,36 @@ struct GlobalDense {
     return atomicAdd(&t[x], inc);
   }
   __device__ __forceinline__ void after_w(int32_t x, Word old) {
-    if (!SCAN) append_active(old == 0, x, L, ntouch);
+    if (!SCAN && x < hot0) append_active(old == 0, x, L, ntouch);
   }
   __device__ __forceinline__ void add_w(int32_t x) { after_w(x, raw_add(x, (Word)1)); }
   __device__ __forceinline__ void add_d(int32_t x) { after_w(x, raw_add(x, (Word)((Word)1 << SH))); }
+  __device__ __forceinline__ Word load(int32_t x) const { return x >= hot0 ? hot[x - hot0] : __ldcg(&t[x]); }
   __device__ __forceinline__ void get(int32_t x, u64& wv, u64& dv) const {
-    const Word v = __ldcg(&t[x]);
+    const Word v = load(x);
     wv = (u64)(v & LOW);
     dv = (u64)(v >> SH);
   }
-  __device__ __forceinline__ u64 get_w(int32_t x) const { return (u64)(__ldcg(&t[x]) & LOW); }
-  __device__ __forceinline__ u64 get_w_or0(int32_t x) const { return (u64)(__ldcg(&t[x]) & LOW); }
+  __device__ __forceinline__ u64 get_w(int32_t x) const { return (u64)(load(x) & LOW); }
+  __device__ __forceinline__ u64 get_w_or0(int32_t x) const { return (u64)(load(x) & LOW); }
   // entry word of x if x has an entry, else nullptr (single-writer update by the caller)
   __device__ __forceinline__ Word* word_if(int32_t x) const {
-    Word* p = &t[x];
-    return __ldcg(p) != 0 ? p : nullptr;
+    Word* p = x >= hot0 ? &hot[x - hot0] : &t[x];
+    return load(x) != 0 ? p : nullptr;
   }
   __device__ __forceinline__ static u64 wfield(Word v) { return (u64)(v & LOW); }
   __device__ __forceinline__ static u64 dfield(Word v) { return (u64)(v >> SH); }
   // f(x, w, d) -> new w, for every entry (strided over `nthr` threads from `tid`)
   template <typename F>
   __device__ __forceinline__ void for_each_mut(int tid, int nthr, F f) {
+    for (int i = tid; i < hotK; i += nthr) {
+      const Word v = hot[i];
+      if (v == 0) continue;
+      const u64 w = f(hot0 + i, (u64)(v & LOW), (u64)(v >> SH));
+      if (w != (u64)(v & LOW)) hot[i] = (Word)((v & ~LOW) | (Word)w);
+    }
     if (SCAN) {
-      const int32_t nvec = (n + PER - 1) / PER;
+      const int32_t nvec = (min(n, hot0) + PER - 1) / PER;  // (a vector across hot0 holds no hot entry)
       const uint4* tv = reinterpret_cast<const uint4*>(t);
       for (int32_t v0 = tid; v0 < nvec; v0 += nthr * 4) {
         uint4 q[4];
@@ -220,8 +235,9 @@ struct GlobalDense {
     }
   }
   __device__ __forceinline__ void reset(int tid, int nthr) {
+    for (int i = tid; i < hotK; i += nthr) hot[i] = (Word)0;
     if (SCAN) {
-      const int32_t nvec = (n + PER - 1) / PER;
+      const int32_t nvec = (min(n, hot0) + PER - 1) / PER;
       uint4* tv = reinterpret_cast<uint4*>(t);
       for (int32_t v0 = tid; v0 < nvec; v0 += nthr * 4) {
         uint4 q[4];
@@ -1112,7 +1128,8 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
                                                           const int32_t* __restrict__ srcs, int nsrc,
                                                           int* __restrict__ counter, Word* __restrict__ tabs,
                                                           int32_t* __restrict__ lists, PairOut o_,
-                                                          char* __restrict__ qmem, int qcap) {
+                                                          char* __restrict__ qmem, int qcap, int hot_k) {
+  extern __shared__ __align__(16) unsigned char pair_hot_sh[];
   __shared__ EngSharedT<PAIR_HBT / 32> E;
   __shared__ u64 red[8];
   __shared__ int s_idx, s_ntouch;
@@ -1125,6 +1142,13 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
   tab.L = SCAN ? nullptr : lists + (size_t)blockIdx.x * g.n;
   tab.ntouch = &s_ntouch;
   tab.n = g.n;
+  if (hot_k > 0) {
+    tab.hot = reinterpret_cast<Word*>(pair_hot_sh);
+    tab.hot0 = g.n - hot_k;
+    tab.hotK = hot_k;
+    for (int i = threadIdx.x; i < hot_k; i += PAIR_HBT) tab.hot[i] = (Word)0;
+    __syncthreads();
+  }
   if (threadIdx.x < 8) red[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_ntouch = 0;
   for (;;) {

@@ -24,6 +24,8 @@ COMBOS = {
     "pair_dense_swept": dict(HEAVY_PAIR, EVOKE_PAIR_SWEEP="1"),        # k_pairs_heavy<u32, true>
     "pair_mid": {"EVOKE_PAIR_LIGHT_MAX": "0", "EVOKE_PAIR_MIDS_MAX": "0"},  # k_pairs_main CTA tier
     "pair_small_mid": {"EVOKE_PAIR_LIGHT_MAX": "0"},                  # k_pairs_mids
+    "pair_dense_hot_partial": dict(HEAVY_PAIR, EVOKE_PAIR_HOT="16"),   # heavy tables, top 16 ranks shared
+    "pair_dense_nohot": dict(HEAVY_PAIR, EVOKE_PAIR_HOT="0"),
     "hub_warp": {"EVOKE_HUB_MICRO_MAX": "0"},                         # hub_item_warp (no micro items)
     "hub_heavy_hash": {"EVOKE_HUB_WARP_MAX": "0"},                    # hub_item_cta<HUB_T_HASH>
     "hub_heavy_shared": {"EVOKE_HUB_WARP_MAX": "0", "EVOKE_HUB_HASH_MAX": "0"},  # <HUB_T_SHPOS>
@@ -38,6 +40,8 @@ COMBOS = {
     "c5_big_u32": dict(C5_BIG),                                        # k_c5_heavy<u32> + bitmaps
     "c5_big_u64": dict(C5_BIG, EVOKE_C5_WIDE="1"),
     "c5_big_nobits": dict(C5_BIG, EVOKE_C5_NO_BITS="1"),
+    "c5_big_hot": dict(C5_BIG, EVOKE_C5_HOT_MIN_W="0"),              # hot-vertex cache of every rank
+    "c5_big_hot_partial": dict(C5_BIG, EVOKE_C5_HOT_MIN_W="0", EVOKE_C5_HOT="16"),  # of the top 16 ranks
     "c5_light_by_work": {"EVOKE_C5_LIGHT_WORK": "40", "EVOKE_C5_MID_WORK": "200"},
     "all_heavy_sorted": dict(HEAVY_PAIR, **C5_BIG, EVOKE_PAIR_PACKED_LIM="0", EVOKE_HUB_WARP_MAX="0",
                              EVOKE_HUB_HASH_MAX="0", EVOKE_HUB_SH_DENSE="0", EVOKE_C5_WIDE="1", EVOKE_SORT_FULL_MIN="1"),
