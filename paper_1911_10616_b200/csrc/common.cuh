@@ -131,3 +131,18 @@ __device__ __forceinline__ int32_t dg_dplus(const DGraph& g, int32_t u) {
 __device__ __forceinline__ int32_t full_other_edge(const DGraph& g, int64_t r, int32_t e, int32_t w) {
   return (g.esrc[e] == w) ? g.fe1[r] : g.fe2[r];
 }
+
+// developer unit timers (EVOKE_DEBUG): per heavy persistent kernel ([0] pair heavy, [1]
+// hub-local heavy, [2] 5-cycle big), SM cycles of the longest single unit, its list index,
+// and the cycles summed over all units (thread 0 of the CTA)
+__device__ unsigned long long g_unit_max[4], g_unit_sum[4];
+__device__ int g_unit_arg[4];
+__device__ int g_unit_prof;
+__device__ __forceinline__ long long unit_t0() { return g_unit_prof && threadIdx.x == 0 ? clock64() : 0; }
+__device__ __forceinline__ void unit_t1(int k, long long t0, int idx) {
+  if (g_unit_prof && threadIdx.x == 0) {
+    const unsigned long long d = (unsigned long long)(clock64() - t0);
+    atomicAdd(&g_unit_sum[k], d);
+    if (atomicMax(&g_unit_max[k], d) < d) g_unit_arg[k] = idx;
+  }
+}

@@ -172,6 +172,7 @@ __device__ __forceinline__ u64 c5_wn(const C5RecL* r) { return (u64)(r->wf & (u3
 #define C5_HOT_MAX 16384              // heavy CTAs (u32 records): hot-vertex cache of up to this many top ranks
 #define C5_SMEM_MAX (208 << 10)       // heavy CTAs: bitmaps + hot cache within this
 #define C5_HOT_MIN_W (1ull << 22)     // hot cache only when the largest big endpoint's W(l) reaches this
+#define C5_GIANT_W (1ull << 32)   // endpoints with W(l) >= this: whole-GPU kernels (k_c5_giant)
 #define C5_FB_WARP 128            // i-key filter words per light warp (4096 bits)
 #define C5_FB_CTA 256             // i-key filter words per mid CTA (8192 bits)
 
@@ -384,6 +385,7 @@ struct C5Hash {
 // Engine adaptors: warp (light endpoints) and CTA (heavy endpoints)
 struct WarpEng {
   static constexpr bool kCta = false;
+  static constexpr bool kGrid = false;
   __device__ __forceinline__ void sync() const { __syncwarp(); }
   __device__ __forceinline__ int tid() const { return threadIdx.x & 31; }
   __device__ __forceinline__ int nthr() const { return 32; }
@@ -392,12 +394,33 @@ struct WarpEng {
 };
 struct CtaEng {
   static constexpr bool kCta = true;
+  static constexpr bool kGrid = false;
   ListEng* E;
   __device__ __forceinline__ void sync() const { __syncthreads(); }
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
   __device__ __forceinline__ int nthr() const { return blockDim.x; }
   template <typename I, typename E2, typename F>
   __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const { cta_lists(n, *E, info, elem, flush); }
+};
+
+// Whole-grid engine (giant endpoints): list items are dealt round robin to the CTAs, each
+// walks its share with the CTA engine; flat loops run over every thread of the grid.  There
+// is no grid barrier: the step groups are separate kernels.
+struct GridEng {
+  static constexpr bool kCta = true;
+  static constexpr bool kGrid = true;
+  ListEng* E;
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ int tid() const { return blockIdx.x * blockDim.x + threadIdx.x; }
+  __device__ __forceinline__ int nthr() const { return gridDim.x * blockDim.x; }
+  template <typename I, typename E2, typename F>
+  __device__ __forceinline__ void lists(int n, I info, E2 elem, F flush) const {
+    const int G = gridDim.x, b = blockIdx.x;
+    const int cnt = n > b ? (n - b + G - 1) / G : 0;
+    cta_lists(cnt, *E, [&](int i, int64_t& base, int& len) { info(i * G + b, base, len); },
+              [&](int i, int64_t base, int k) -> u64 { return elem(i * G + b, base, k); },
+              [&](int i, u64 v) { flush(i * G + b, v); });
+  }
 };
 
 template <typename R>
@@ -411,7 +434,7 @@ __device__ unsigned long long g_c5_phase[3][8];
 __device__ int g_c5_prof;
 #define C5_PHASE(i)                                                                              \
   do {                                                                                           \
-    if (g_c5_prof && (Eng::kCta ? threadIdx.x == 0 : (threadIdx.x & 31) == 0)) {                 \
+    if (g_c5_prof && !Eng::kGrid && (Eng::kCta ? threadIdx.x == 0 : (threadIdx.x & 31) == 0)) {  \
       const long long t_ = clock64();                                                            \
       atomicAdd(&g_c5_phase[!Eng::kCta ? 2 : blockDim.x == C5_HBT ? 0 : 1][i],                   \
                 (unsigned long long)(t_ - t_prev));                                              \
@@ -419,32 +442,53 @@ __device__ int g_c5_prof;
     }                                                                                            \
   } while (0)
 
-// One endpoint l.  J: list of j-keys (counter *nJ); tot: per-engine shared u64 (zeroed).
-template <typename Eng, typename Loc>
-__device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const u32* __restrict__ Tmid,
-                            const u32* __restrict__ Thigh, int32_t l, const Eng& eng, Loc& loc, int32_t* J,
-                            int* nJ, u64* tot, u64* __restrict__ C5) {
-  const int64_t r0 = g.rp[l];
-  const int dl = g.deg[l];
-  const int dml = g.dm[l];
-  long long t_prev = clock64();
-  // ---- step 0: neighbours of l
-  for (int t = eng.tid(); t < dl; t += eng.nthr()) loc.mark_nr(g.ci[r0 + t], C5_ADJ);
-  // wedge lists of steps 1/6: w = N(l)[t], i in N(w) (w < l) or N+(w) (w > l)
-  auto winfo = [&](int t, int64_t& base, int& len) {
+// One endpoint l, in three step groups separated by barriers (the giant endpoints run each
+// group as a whole-GPU kernel, k_c5_giant_*).  J: list of j-keys (counter *nJ); tot: u64
+// accumulator of the l credit (zeroed).  Step 3 is the only step whose work is split across
+// shards for a giant endpoint: its outputs P, A, S enter every credit linearly, so shard si of
+// ns takes the j-keys with j % ns == si, and the constant terms (those not multiplied by P, A
+// or S) are added by shard 0 alone (consts).
+struct C5Split {
+  int ns = 1, si = 0;
+  __device__ __forceinline__ bool mine(int32_t j) const { return ns == 1 || j % ns == si; }
+  __device__ __forceinline__ bool consts() const { return si == 0; }
+};
+
+// wedge lists of steps 1/6: w = N(l)[t], i in N(w) (w < l) or N+(w) (w > l)
+struct C5WInfo {
+  const DGraph& g;
+  int64_t r0;
+  int32_t l;
+  __device__ __forceinline__ void operator()(int t, int64_t& base, int& len) const {
     const int32_t w = g.ci[r0 + t];
     base = (w < l) ? g.rp[w] : g.rp[w] + g.dm[w];
     len = (int)(g.rp[w + 1] - base);
-  };
-  // out-out lists of steps 2/4: k = N-(l)[t], j in N+(k) (edge ids orow[k] + .)
-  auto kinfo = [&](int t, int64_t& base, int& len) {
+  }
+};
+// out-out lists of steps 2/4: k = N-(l)[t], j in N+(k) (edge ids orow[k] + .)
+struct C5KInfo {
+  const DGraph& g;
+  int64_t r0;
+  __device__ __forceinline__ void operator()(int t, int64_t& base, int& len) const {
     const int32_t k = g.ci[r0 + t];
     base = g.orow[k];
     len = (int)(g.orow[k + 1] - base);
-  };
+  }
+};
+
+// steps 0-2: ADJ flags, Wn, Q/QT/QM and the j-key list
+template <typename Eng, typename Loc>
+__device__ __forceinline__ void c5_steps012(const DGraph& g, const u32* __restrict__ Tmid,
+                                            const u32* __restrict__ Thigh, int32_t l, const Eng& eng, Loc& loc,
+                                            int32_t* J, int* nJ, long long& t_prev) {
+  const int64_t r0 = g.rp[l];
+  const int dl = g.deg[l];
+  const int dml = g.dm[l];
+  // ---- step 0: neighbours of l
+  for (int t = eng.tid(); t < dl; t += eng.nthr()) loc.mark_nr(g.ci[r0 + t], C5_ADJ);
   C5_PHASE(0);
   // ---- step 1: Wn over non-in-in wedges (i, w, l)
-  eng.lists(dl, winfo,
+  eng.lists(dl, C5WInfo{g, r0, l},
       [&](int, int64_t base, int k) -> u64 {
         const int32_t i = g.ci[base + k];
         if (i == l) return 0;
@@ -455,7 +499,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       [&](int, u64) {});
   C5_PHASE(1);
   // ---- step 2: Q, QT, QM over out-out wedges j <- k -> l
-  eng.lists(dml, kinfo,
+  eng.lists(dml, C5KInfo{g, r0},
       [&](int, int64_t base, int k) -> u64 {
         const int64_t e = base + k;
         const int32_t j = g.ocol[e];
@@ -466,15 +510,17 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         return 0;
       },
       [&](int, u64) {});
-  eng.sync();
-  C5_PHASE(2);
-  // ---- step 3: paths through j: P, A (to i), S and the j credits
-  const int nj = *nJ;
+}
+
+// step 3: paths through j: P, A (to i), S and the j credits
+template <typename Eng, typename Loc>
+__device__ __forceinline__ void c5_step3(const DGraph& g, int32_t l, const Eng& eng, Loc& loc, const int32_t* J,
+                                         int nj, u64* __restrict__ C5, C5Split sp) {
   eng.lists(nj,
       [&](int t, int64_t& base, int& len) {
         const int32_t j = loc.id_of(J[t]);
         base = g.orow[j];
-        len = (int)(g.orow[j + 1] - base);
+        len = sp.mine(j) ? (int)(g.orow[j + 1] - base) : 0;
       },
       [&](int t, int64_t base, int k) -> u64 {
         // Only i with Wn[i] > 0 can close a 5-cycle: a path i <- j <- k -> l with Wn[i] = 0
@@ -497,22 +543,30 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         atomicAdd(&C5[loc.id_of(J[t])], rec_q(rj) * s);  // the j credit is linear in S
       });
   // constant part of the j credits
-  for (int t = eng.tid(); t < nj; t += eng.nthr()) {
-    const int32_t j = loc.id_of(J[t]);
-    const auto* rj = &loc.R[J[t]];
-    const u64 q = rec_q(rj);
-    const bool adjj = c5_flags(rj) & C5_ADJ;
-    const u64 lj = (l > j && adjj) ? 1ull : 0ull;
-    const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-    const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rec_qt(rj) - q * lj);
-    if (c) atomicAdd(&C5[j], (u64)0 - c);
-  }
-  eng.sync();
-  loc.hot_flush(eng);
-  eng.sync();
-  C5_PHASE(3);
+  if (sp.consts())
+    for (int t = eng.tid(); t < nj; t += eng.nthr()) {
+      const int32_t j = loc.id_of(J[t]);
+      const auto* rj = &loc.R[J[t]];
+      const u64 q = rec_q(rj);
+      const bool adjj = c5_flags(rj) & C5_ADJ;
+      const u64 lj = (l > j && adjj) ? 1ull : 0ull;
+      const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
+      const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rec_qt(rj) - q * lj);
+      if (c) atomicAdd(&C5[j], (u64)0 - c);
+    }
+}
+
+// steps 4-6: k, i (and l) and w credits; every record is final
+template <typename Eng, typename Loc>
+__device__ __forceinline__ void c5_steps456(const DGraph& g, const u32* __restrict__ Thigh, int32_t l,
+                                            const Eng& eng, Loc& loc, u64* tot, u64* __restrict__ C5,
+                                            C5Split sp, long long& t_prev) {
+  const int64_t r0 = g.rp[l];
+  const int dl = g.deg[l];
+  const int dml = g.dm[l];
+  const u64 cm = sp.consts() ? ~0ull : 0ull;  // constant terms: shard 0 only
   // ---- step 4: k credits
-  eng.lists(dml, kinfo,
+  eng.lists(dml, C5KInfo{g, r0},
       [&](int, int64_t base, int k) -> u64 {
         const int64_t e = base + k;
         const int32_t j = g.ocol[e];
@@ -521,7 +575,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const bool adjj = c5_flags(rj) & C5_ADJ;
         const u64 lj = (l > j && adjj) ? 1ull : 0ull;
         const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-        return rec_s(rj) - (adjj ? (dj - lj) : 0ull) - ((u64)Thigh[e] - lj);
+        return rec_s(rj) - (((adjj ? (dj - lj) : 0ull) + ((u64)Thigh[e] - lj)) & cm);
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
   C5_PHASE(4);
@@ -535,7 +589,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
       const u32 fl = c5_flags(r);
       if (!c5_wn(r)) continue;  // not an i-key
       const bool adji = fl & C5_ADJ;
-      const u64 bi = rec_qm(r) - rec_q(r) * ((x > l && adji) ? 1ull : 0ull);
+      const u64 bi = (rec_qm(r) - rec_q(r) * ((x > l && adji) ? 1ull : 0ull)) & cm;
       const u64 ci = rec_p(r) * c5_wn(r) - rec_a(r) - bi;
       if (ci) atomicAdd(&C5[x], ci);
       acc += ci;
@@ -545,7 +599,7 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
   }
   C5_PHASE(5);
   // ---- step 6: wedge centres w
-  eng.lists(dl, winfo,
+  eng.lists(dl, C5WInfo{g, r0, l},
       [&](int t, int64_t base, int k) -> u64 {
         const int64_t s = base + k;
         const int32_t i = g.ci[s];
@@ -554,9 +608,25 @@ __device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const
         const auto* ri = loc.peek(i);
         u64 corr = (w < i) ? (u64)g.tlows[r0 + t] : 0ull;
         if (w < l && w < i) corr += (u64)g.tmids[s] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
-        return rec_p(ri) - corr;
+        return rec_p(ri) - (corr & cm);
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
+}
+
+template <typename Eng, typename Loc>
+__device__ void c5_endpoint(const DGraph& g, const u32* __restrict__ Tlow, const u32* __restrict__ Tmid,
+                            const u32* __restrict__ Thigh, int32_t l, const Eng& eng, Loc& loc, int32_t* J,
+                            int* nJ, u64* tot, u64* __restrict__ C5) {
+  long long t_prev = clock64();
+  c5_steps012(g, Tmid, Thigh, l, eng, loc, J, nJ, t_prev);
+  eng.sync();
+  C5_PHASE(2);
+  c5_step3(g, l, eng, loc, J, *nJ, C5, C5Split{});
+  eng.sync();
+  loc.hot_flush(eng);
+  eng.sync();
+  C5_PHASE(3);
+  c5_steps456(g, Thigh, l, eng, loc, tot, C5, C5Split{}, t_prev);
   eng.sync();
   C5_PHASE(6);
 }
@@ -622,7 +692,8 @@ __global__ void k_c5_work(DGraph g, const u32* __restrict__ splus, u64* __restri
   }
 }
 
-// Tiers of this shard's endpoints (mine == nullptr: every endpoint):
+// Tiers of this shard's endpoints (mine == nullptr: every endpoint), and the giants (W >=
+// giant_w, tier 3, list order = vertex order, on every shard):
 //   light (one warp):    R <= rec_light and W <= work_light (packed records, per-warp hash;
 //                        shared memory when 2R fits the warp's shared region, else global)
 //   mid (128 threads):   R <= rec_mid   and W <= work_mid   (packed records, per-CTA hash in global memory)
@@ -634,18 +705,21 @@ __global__ void k_c5_work(DGraph g, const u32* __restrict__ splus, u64* __restri
 // Lists: tier t in lists[t * n ...], with R (t < 2) or W (big) beside it.
 __global__ void k_c5_bin(DGraph g, const u64* __restrict__ W, const u64* __restrict__ R,
                          const uint8_t* __restrict__ mine, u64 rec_light, u64 work_light, u64 rec_mid,
-                         u64 work_mid, int32_t* __restrict__ lists, u32* __restrict__ rbs, u64* __restrict__ big_w,
-                         int* __restrict__ counts) {
+                         u64 work_mid, u64 giant_w, int32_t* __restrict__ lists, u32* __restrict__ rbs,
+                         u64* __restrict__ big_w, int* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < g.n;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int32_t l = (int32_t)min(base + lane, (int64_t)g.n - 1);
-    const bool ok = base + lane < g.n && W[l] > 0 && (!mine || mine[l]);
-    const u64 w = ok ? W[l] : 0, r = ok ? R[l] : 0;
-    const int tier = !ok ? -1
+    const bool any = base + lane < g.n && W[l] > 0;
+    const u64 w = any ? W[l] : 0, r = any ? R[l] : 0;
+    // giants: every shard (their step 3 is split by j-key); the rest: this shard's own
+    const int tier = !any ? -1
+                   : w >= giant_w ? 3
+                   : (mine && !mine[l]) ? -1
                    : (r <= rec_light && w <= work_light) ? 0
                    : (r <= rec_mid && w <= work_mid) ? 1 : 2;
-    for (int t = 0; t < 3; t++) {
+    for (int t = 0; t < 4; t++) {
       const u32 bal = __ballot_sync(FULL_MASK, tier == t);
       if (!bal) continue;
       int b0 = 0;
@@ -656,7 +730,7 @@ __global__ void k_c5_bin(DGraph g, const u64* __restrict__ W, const u64* __restr
       const int q = b0 + __popc(bal & ((1u << lane) - 1u));
       lists[(size_t)t * g.n + q] = l;
       if (t < 2) rbs[(size_t)t * g.n + q] = (u32)r;
-      else big_w[q] = w;
+      else if (t == 2) big_w[q] = w;
     }
   }
 }
@@ -707,10 +781,54 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_heavy(DGraph g, const u32* __rest
     const int idx = s_idx;
     if (idx >= n_heavy) break;
     const int32_t l = heavy[idx];
+    const long long ut = unit_t0();
     c5_endpoint(g, Tlow, Tmid, Thigh, l, eng, loc, J, &s_nJ, &s_tot, C5);
     if (threadIdx.x == 0 && s_tot) atomicAdd(&C5[l], s_tot);
     c5_reset(eng, loc);
     __syncthreads();
+    unit_t1(2, ut, idx);
+  }
+}
+
+// Giant endpoints (W(l) past C5_GIANT_W, or any W(l) >= 2^32): one endpoint at a time on the
+// whole GPU, one kernel per step group (part 0: steps 0-2, 1: step 3, 2: steps 4-6, 3: reset
+// and the l credit), u64 records dense by vertex id.  Counters per giant: cnt[2 gi] = touched
+// records, cnt[2 gi + 1] = j-keys; tot[gi] = the l credit (all zeroed before the first part).
+// With shards, step 3's j-keys are split by j % ns (C5Split) and every shard runs the other
+// parts, so one hub's endpoint is spread over every rank.
+__global__ void __launch_bounds__(C5_HBT) k_c5_giant(int part, DGraph g, const u32* __restrict__ Tmid,
+                                                    const u32* __restrict__ Thigh, const int32_t* __restrict__ giants,
+                                                    int gi, C5Rec* __restrict__ dense, int32_t* __restrict__ dlist,
+                                                    int* __restrict__ cnt, u64* __restrict__ tot,
+                                                    u64* __restrict__ C5, int32_t* __restrict__ qmem, int ns, int si) {
+  __shared__ ListEng E;
+  if (threadIdx.x == 0) {
+    E.qcap = g.max_deg;
+    E.qi = qmem + (size_t)blockIdx.x * (2 * (size_t)g.max_deg + 1);
+    E.lc0 = E.qi + g.max_deg;
+  }
+  __syncthreads();
+  GridEng eng{&E};
+  C5Dense<C5Rec> loc;
+  loc.R = dense;
+  loc.L = dlist;
+  loc.nL = &cnt[2 * gi];
+  int32_t* J = dlist + g.n;
+  int* nJ = &cnt[2 * gi + 1];
+  C5Split sp;
+  sp.ns = ns;
+  sp.si = si;
+  const int32_t l = giants[gi];
+  long long t_prev = 0;
+  if (part == 0) {
+    c5_steps012(g, Tmid, Thigh, l, eng, loc, J, nJ, t_prev);
+  } else if (part == 1) {
+    c5_step3(g, l, eng, loc, J, *nJ, C5, sp);
+  } else if (part == 2) {
+    c5_steps456(g, Thigh, l, eng, loc, &tot[gi], C5, sp, t_prev);
+  } else {
+    c5_reset(eng, loc);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && tot[gi]) atomicAdd(&C5[l], tot[gi]);
   }
 }
 

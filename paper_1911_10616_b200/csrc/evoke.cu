@@ -231,6 +231,7 @@ struct Arena {
 struct Ctx {
   cudaStream_t st;
   int dev, num_sms;
+  double sm_mhz = 1965.0;  // (developer timers only)
   int launches = 0;
   int lib_launches = 0;
   cudaEvent_t ev[P_COUNT + 1];
@@ -442,6 +443,24 @@ __global__ void k_shard_sum_u32(const u32* __restrict__ skeys, int64_t n, int si
     if (all) atomicAdd(&sums[1], all);
   }
 }
+// the 5-cycle endpoints' work for the position split: giants (every shard takes 1/ns of their
+// step 3) are left out of it and counted here, W / ns for this shard
+__global__ void k_c5_giant_mask(const u64* __restrict__ W, int32_t n, u64 giant_w, int ns, u64* __restrict__ Wm,
+                                u64* __restrict__ sums) {
+  u64 own = 0, all = 0;
+  for (int32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
+    const u64 w = W[l];
+    const bool giant = w >= giant_w;
+    Wm[l] = giant ? 0 : w;
+    if (giant) { own += w / (u64)ns; all += w; }
+  }
+  own = warp_sum(own);
+  all = warp_sum(all);
+  if ((threadIdx.x & 31) == 0) {
+    if (own) atomicAdd(&sums[0], own);
+    if (all) atomicAdd(&sums[1], all);
+  }
+}
 // (k = d+(u))^3: the 4/5-clique unit's work estimate
 __global__ void k_clique_est(const int64_t* __restrict__ orow, int32_t n, u64* __restrict__ est) {
   for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
@@ -563,6 +582,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   Ctx C;
   C.dev = dev;
   CK(cudaDeviceGetAttribute(&C.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  if (getenv("EVOKE_DEBUG")) {
+    int khz = 0;
+    if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev) == cudaSuccess && khz > 0) C.sm_mhz = khz / 1e3;
+  }
   if (o.stream) {
     C.st = (cudaStream_t)o.stream;
   } else {
@@ -621,6 +644,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     const int prof = getenv("EVOKE_DEBUG") ? 1 : 0;  // developer step / phase timers
     CK(cudaMemcpyToSymbolAsync(g_c5_prof, &prof, sizeof(int), 0, cudaMemcpyHostToDevice, C.st));
     CK(cudaMemcpyToSymbolAsync(g_pair_prof, &prof, sizeof(int), 0, cudaMemcpyHostToDevice, C.st));
+    CK(cudaMemcpyToSymbolAsync(g_unit_prof, &prof, sizeof(int), 0, cudaMemcpyHostToDevice, C.st));
   }
   Arena A(C.st, dev);
   ZeroLease lease;  // destroyed before A (its buffer is not A's)
@@ -1339,26 +1363,36 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     k_c5_splus<<<grid_for(n, B, SM), B, 0, C.st>>>(g, splus);
     k_c5_work<<<warp_grid, B, 0, C.st>>>(g, splus, c5W, c5R);
     C.launches += 2;
-    const uint8_t* c5mine = shard_mask(A, C, c5W, n, si, ns, d_work + 4);
-    int32_t* c5lists = A.alloc<int32_t>((size_t)3 * n);  // light, mid, big
+    // giants (W(l) >= giant_w; W >= 2^32 always: their u64 records): the whole GPU per endpoint,
+    // on every shard (step 3 split by j-key), so they take no part in the position split
+    const u64 giant_w = env_cap("EVOKE_C5_GIANT_W", C5_GIANT_W);
+    const uint8_t* c5mine = nullptr;
+    if (ns > 1) {
+      u64* c5Wm = A.alloc<u64>(n);
+      k_c5_giant_mask<<<grid_for(n, B, SM), B, 0, C.st>>>(c5W, n, giant_w, ns, c5Wm, d_work + 4);
+      C.launches++;
+      c5mine = shard_mask(A, C, c5Wm, n, si, ns, d_work + 4);
+    }
+    int32_t* c5lists = A.alloc<int32_t>((size_t)4 * n);  // light, mid, big, giant
     u32* c5rb = A.alloc<u32>((size_t)2 * n);              // R(l) of the hashed tiers
     u64* c5bw = A.alloc<u64>(n);                          // W(l) of the big tier
-    int* c5c = A.alloc<int>(8, true);  // tier sizes [0..2], persistent-kernel counters [4..6]
+    int* c5c = A.alloc<int>(8, true);  // tier sizes [0..3], persistent-kernel counters [4..6]
     u64* C5out = Fp(F_C5);
     // tier limits (lower only: env for tests); mid work < 2^16 keeps the packed records exact
     const u64 rec_light = env_cap("EVOKE_C5_LIGHT_REC", C5_WARP_MAX), work_light = env_cap("EVOKE_C5_LIGHT_WORK", C5_WARP_WORK);
     const u64 rec_mid = env_cap("EVOKE_C5_MID_REC", C5_MID_MAX), work_mid = env_cap("EVOKE_C5_MID_WORK", C5_MID_WORK);
     k_c5_bin<<<grid_for(n, B, SM), B, 0, C.st>>>(g, c5W, c5R, c5mine, rec_light, work_light, rec_mid, work_mid,
-                                                 c5lists, c5rb, c5bw, c5c);
+                                                 giant_w, c5lists, c5rb, c5bw, c5c);
     C.launches++;
-    int hc5[3];
+    int hc5[4];
     CK(cudaMemcpyAsync(hc5, c5c, sizeof(hc5), cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     C.tick("c5_items+sync");
-    const int n5l = hc5[0], n5m = hc5[1], n5b = hc5[2];
+    const int n5l = hc5[0], n5m = hc5[1], n5b = hc5[2], n5g = hc5[3];
     int32_t* c5l = c5lists;
     u32* c5lr = c5rb;
-    if (getenv("EVOKE_DEBUG")) fprintf(stderr, "[evoke] c5 endpoints: light %d mid %d big %d\n", n5l, n5m, n5b);
+    if (getenv("EVOKE_DEBUG"))
+      fprintf(stderr, "[evoke] c5 endpoints: light %d mid %d big %d giant %d\n", n5l, n5m, n5b, n5g);
     if (getenv("EVOKE_C5_HIST")) {  // developer: W / R histogram of every endpoint
       std::vector<u64> hw(n), hr(n);
       CK(cudaMemcpyAsync(hw.data(), c5W, sizeof(u64) * n, cudaMemcpyDeviceToHost, C.st));
@@ -1417,6 +1451,25 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       C.lib_launches += 4;
       return d2h_scalar<u64>(bk, C.st);
     };
+    if (n5g > 0) {
+      // one giant at a time on every SM: steps 0-2, step 3, steps 4-6, reset (four kernels each)
+      const int32_t* gl = c5lists + (size_t)3 * n;
+      C5Rec* gdense = A.zalloc<C5Rec>((size_t)n);
+      int32_t* gdl = A.alloc<int32_t>((size_t)2 * n);
+      int* gcnt = A.alloc<int>((size_t)2 * n5g, true);
+      u64* gtot = A.alloc<u64>((size_t)n5g, true);
+      int bpg = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpg, k_c5_giant, C5_HBT, 0));
+      const int gg = std::max(1, bpg) * SM;
+      int32_t* gq = A.alloc<int32_t>((size_t)gg * (2 * (size_t)g.max_deg + 1));
+      c5chain.push_back([=, &C](cudaStream_t st) {
+        for (int q = 0; q < n5g; q++)
+          for (int part = 0; part < 4; part++) {
+            k_c5_giant<<<gg, C5_HBT, 0, st>>>(part, g, Tmid, Thigh, gl, q, gdense, gdl, gcnt, gtot, C5out, gq, ns, si);
+            C.launches++;
+          }
+      });
+    }
     const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: big-endpoint CTAs
     const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
     if (n5b > 0) {
@@ -1426,7 +1479,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const bool narrow = wmax < (1ull << 32) && !getenv("EVOKE_C5_WIDE");
       const size_t rec = narrow ? sizeof(C5RecT<u32>) : sizeof(C5Rec);
       const int64_t per = (int64_t)n * (int64_t)(rec + 8);
-      const int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, n5b), std::max<int64_t>(1, (int64_t)(freeb / 4) / per));
+      // (whole-GPU passes run alone: half the free estimate; concurrent: a quarter)
+      const int64_t budget = (int64_t)(whole_gpu_passes ? freeb / 2 : freeb / 4);
+      const int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, n5b), std::max<int64_t>(1, budget / per));
+      if (getenv("EVOKE_DEBUG"))
+        fprintf(stderr, "[evoke] c5 big: %d endpoints, W max %llu, %d CTAs (%s records, free estimate %.1f GB)\n",
+                n5b, (unsigned long long)wmax, hg, narrow ? "u32" : "u64", freeb / 1e9);
       char* dense = A.zalloc<char>((size_t)hg * n * rec);
       int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
       int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
@@ -1566,6 +1624,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     fprintf(stderr, "[evoke] c5 light records used %llu of %llu region slots\n", c5p[2][7], c5p[1][7]);
     unsigned long long z3[3][8] = {};
     CK(cudaMemcpyToSymbol(g_c5_phase, z3, sizeof(z3)));
+    unsigned long long umax[4], usum[4], uz[4] = {};
+    int uarg[4];
+    CK(cudaMemcpyFromSymbol(umax, g_unit_max, sizeof(umax)));
+    CK(cudaMemcpyFromSymbol(usum, g_unit_sum, sizeof(usum)));
+    CK(cudaMemcpyFromSymbol(uarg, g_unit_arg, sizeof(uarg)));
+    const char* un[3] = {"pair heavy", "hub heavy", "c5 big"};
+    for (int t = 0; t < 3; t++)
+      fprintf(stderr, "[evoke] %s units: longest %.3f ms (list index %d), sum %.3f ms (SM clock %.0f MHz)\n", un[t],
+              umax[t] / (C.sm_mhz * 1e3), uarg[t], usum[t] / (C.sm_mhz * 1e3), C.sm_mhz);
+    CK(cudaMemcpyToSymbol(g_unit_max, uz, sizeof(uz)));
+    CK(cudaMemcpyToSymbol(g_unit_sum, uz, sizeof(uz)));
   }
   C.njobs = (int)jobs.size();
   for (size_t i = 0; i < jobs.size(); i++) { C.job_pass[i] = jobs[i].pass; C.job_rank[i] = jobs[i].rank; }

@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(BT) k_hub_heavy(DGraph g, const int32_t* __res
     const u64 dv = (u64)g.deg[v];
     const u64 bound = min(dv - 1, (u64)heavy_est[idx]);  // distinct x of the item
     const bool c16 = g.foff[eva + 1] - g.foff[eva] < 65536;  // T(v,a) bounds every c(x)
+    const long long ut = unit_t0();
     if (c16 && bound <= (u64)min(hash_max, (int)(kSlots * 3 / 4))) {
       const u32 cap = (u32)min((u64)kSlots, bound + bound / 3 + 64);
       hub_item_cta<HUB_T_HASH, BT>(g, s, cap, hub_sh, S, gtab, glist, R68, R69, split);
@@ -565,6 +566,7 @@ __global__ void __launch_bounds__(BT) k_hub_heavy(DGraph g, const int32_t* __res
     } else {
       hub_item_cta<HUB_T_GLPOS, BT>(g, s, 0, hub_sh, S, gtab, glist, R68, R69, split);
     }
+    unit_t1(1, ut, idx);
   }
 }
 

@@ -1157,7 +1157,9 @@ __global__ void __launch_bounds__(PAIR_HBT) k_pairs_heavy(DGraph g, const u32* _
     const int idx = s_idx;
     __syncthreads();
     if (idx >= nsrc) break;
+    const long long ut = unit_t0();
     pair_source_cta<PAIR_HBT>(g, Te, srcs[idx], tab, E, red, o, 0u);
+    unit_t1(0, ut, idx);
     if (threadIdx.x == 0) s_ntouch = 0;
   }
 }

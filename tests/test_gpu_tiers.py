@@ -43,6 +43,8 @@ COMBOS = {
     "c5_big_hot": dict(C5_BIG, EVOKE_C5_HOT_MIN_W="0"),              # hot-vertex cache of every rank
     "c5_big_hot_partial": dict(C5_BIG, EVOKE_C5_HOT_MIN_W="0", EVOKE_C5_HOT="16"),  # of the top 16 ranks
     "c5_light_by_work": {"EVOKE_C5_LIGHT_WORK": "40", "EVOKE_C5_MID_WORK": "200"},
+    "c5_giant": {"EVOKE_C5_GIANT_W": "300"},                          # k_c5_giant (whole-GPU endpoints)
+    "c5_giant_all": {"EVOKE_C5_GIANT_W": "1"},                        # every endpoint a giant
     "all_heavy_sorted": dict(HEAVY_PAIR, **C5_BIG, EVOKE_PAIR_PACKED_LIM="0", EVOKE_HUB_WARP_MAX="0",
                              EVOKE_HUB_HASH_MAX="0", EVOKE_HUB_SH_DENSE="0", EVOKE_C5_WIDE="1", EVOKE_SORT_FULL_MIN="1"),
 }
@@ -122,3 +124,20 @@ def test_forced_tier_closed_forms(pkg, combo, monkeypatch):
         monkeypatch.setenv(k, v)
     for g in [graphgen.star(40), graphgen.complete_bipartite(3, 30), graphgen.complete(14)]:
         _eq(pkg.evoke_orbits_edges(g.n, g.edges), oracle.orbits(g.n, g.edges), f"{combo} {g.name}")
+
+
+@pytest.mark.parametrize("giant_w", ["1", "2000"])
+def test_giant_endpoints_split_over_shards(pkg, giant_w, monkeypatch):
+    """giant 5-cycle endpoints run on every shard with step 3 split by j-key and the constant
+    terms on shard 0: the shard partials still sum (mod 2^64) to the one-shard matrix, which
+    equals the oracle's"""
+    monkeypatch.setenv("EVOKE_C5_GIANT_W", giant_w)
+    monkeypatch.setenv("EVOKE_CHECK_ZERO", "1")
+    for g in [graphgen.erdos_renyi(60, 0.3, 77), graphgen.complete(12), _book(80, 0.04, 2)]:
+        ref = oracle.orbits(g.n, g.edges)
+        _eq(pkg.evoke_orbits_edges(g.n, g.edges), ref, f"giants {g.name}")
+        for ns in (2, 3, 8):
+            acc = np.zeros((g.n, 73), dtype=np.uint64)
+            for si in range(ns):
+                acc += np.asarray(pkg.evoke_orbits_edges(g.n, g.edges, shard_index=si, num_shards=ns)).view(np.uint64)
+            _eq(acc, ref, f"giants {g.name} shards={ns}")
