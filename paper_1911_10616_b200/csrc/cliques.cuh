@@ -39,7 +39,7 @@ __device__ __forceinline__ int row_rank(const u32* __restrict__ R, int W, int i,
 // sums (acc_u0, acc_u1; per lane, the caller reduces them).
 template <int MODE>
 __device__ __forceinline__ void clique_row(const DGraph& g, const u32* S, int W, int k, int64_t ou, int i,
-                                           int lane, bool do_k4, bool do_k5, const u32* __restrict__ Te,
+                                           int lane, bool do_k4, bool do_k5, bool rows66, const u32* __restrict__ Te,
                                            u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
                                            u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70,
                                            u64& acc_u0, u64& acc_u1) {
@@ -85,10 +85,11 @@ __device__ __forceinline__ void clique_row(const DGraph& g, const u32* S, int W,
         }
       }
     } else {
-      // theta66 / theta70 credits to L_i over the local edges (j,l) inside S_i
+      // theta66 / theta70 credits to L_i over the local edges (j,l) inside S_i (rows66; else
+      // credited per local edge by clique_edges66)
       const u64 te_uj = Te[ou + j];
       const int64_t qj0 = g.toff[ou + j];
-      for (int w = (j >> 5); w < W; w++) {
+      for (int w = (j >> 5); rows66 && w < W; w++) {
         const u32 x = Si[w] & Sj[w] & gt_mask(j, w);
         for_each_bit(x, w << 5, [&](int l) {
           const int64_t qjl = qj0 + row_rank(Sj, W, j, l);
@@ -135,9 +136,33 @@ __device__ __forceinline__ void clique_row(const DGraph& g, const u32* S, int W,
   }
 }
 
+// theta66 / theta70 credits of the local vertices, one local edge (j, l) at a time: the local
+// edge is the oriented triangle q = (u, L_j, L_l) of u's out-edges, and every local i adjacent
+// to both closes the 4-clique {u, L_i, L_j, L_l}; L_i gets T(u,L_j) + T(u,L_l) + T(L_j,L_l) for
+// theta66 and K4(q) - 1 for theta70.  The per-q values are read once, coalesced over q, and
+// the credits go to shared accumulators acc66/acc70 [k] (flushed by the caller) instead of a
+// per-(i, j, l) rank search and three dependent global loads.
+__device__ __forceinline__ void clique_edges66(const DGraph& g, const u32* S, int W, int64_t ou, int64_t q0,
+                                               int64_t q1, int t, int nt, const u32* __restrict__ Te,
+                                               const u32* __restrict__ K4t, u64* acc66, u64* acc70) {
+  for (int64_t q = q0 + t; q < q1; q += nt) {
+    const int32_t ej = g.tab[q], el = g.tac[q];
+    const u64 f66 = (u64)Te[ej] + (u64)Te[el] + (u64)Te[g.tbc[q]];
+    const u64 f70 = (u64)K4t[q] - 1ull;
+    const u32* Sj = S + (int64_t)(ej - ou) * W;
+    const u32* Sl = S + (int64_t)(el - ou) * W;
+    for (int w = 0; w < W; w++)
+      for_each_bit(Sj[w] & Sl[w], w << 5, [&](int i) {
+        atomicAdd(&acc66[i], f66);
+        if (f70) atomicAdd(&acc70[i], f70);
+      });
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cliques(
-    DGraph g, const int32_t* __restrict__ ulist, int nu, int smem_words, u32* __restrict__ gscratch,
+    DGraph g, const int32_t* __restrict__ ulist, int nu, int smem_words, int acc66_words, int acc_k,
+    u32* __restrict__ gscratch,
     int64_t gscratch_words, int do_k4, const uint8_t* __restrict__ mine,
     const u32* __restrict__ Te, u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
     u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70) {
@@ -145,6 +170,10 @@ __global__ void __launch_bounds__(256) k_cliques(
   __shared__ u64 red[1][2];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
   if (threadIdx.x == 0) { red[0][0] = 0; red[0][1] = 0; }
+  if (MODE == 1 && acc66_words > 0) {  // 2 x acc_k accumulators, kept zero between units by the flush
+    u64* acc = reinterpret_cast<u64*>(sh_bits + acc66_words);
+    for (int i = threadIdx.x; i < 2 * acc_k; i += blockDim.x) acc[i] = 0;
+  }
   __syncthreads();
   for (int idx = blockIdx.x; idx < nu; idx += gridDim.x) {
     const int32_t u = ulist[idx];
@@ -166,8 +195,25 @@ __global__ void __launch_bounds__(256) k_cliques(
     }
     __syncthreads();
     u64 acc_u0 = 0, acc_u1 = 0;  // u's own credits (MODE 0: 3*#K4 and 4*#K5; MODE 1: th66, th70)
+    // MODE 1, bitmap in shared memory: the local vertices' credits per local edge, into shared
+    // accumulators after the bitmap (the launch sizes them; k <= the bin's kmax)
+    const bool edges66 = MODE == 1 && S == sh_bits && acc66_words > 0;
+    if (edges66) {
+      u64* acc66 = reinterpret_cast<u64*>(sh_bits + acc66_words);
+      u64* acc70 = acc66 + k;
+      clique_edges66(g, S, W, ou, q0, q1, threadIdx.x, blockDim.x, Te, K4t, acc66, acc70);
+      __syncthreads();
+      for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const int32_t Li = g.ocol[ou + i];
+        if (acc66[i]) atomicAdd(&R66[Li], acc66[i]);
+        if (acc70[i]) atomicAdd(&R70[Li], acc70[i]);
+        acc66[i] = 0;
+        acc70[i] = 0;
+      }
+    }
     for (int i = wib; i < k; i += nwb)
-      clique_row<MODE>(g, S, W, k, ou, i, lane, do_k4, do_k5, Te, K4t, K4v, K4e, K5v, R66, R70, acc_u0, acc_u1);
+      clique_row<MODE>(g, S, W, k, ou, i, lane, do_k4, do_k5, !edges66, Te, K4t, K4v, K4e, K5v, R66, R70, acc_u0,
+                       acc_u1);
     // block reduction of u's credits
     acc_u0 = warp_sum(acc_u0);
     acc_u1 = warp_sum(acc_u1);
@@ -201,8 +247,12 @@ __global__ void __launch_bounds__(256) k_cliques_warp(
     const u32* __restrict__ Te, u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
     u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70) {
   __shared__ u32 sh_rows[8][32];
+  __shared__ u64 sh_acc[MODE == 1 ? 8 : 1][64];  // MODE 1: theta66 / theta70 accumulators per warp
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   u32* S = sh_rows[wib & 7];
+  u64* acc66 = sh_acc[MODE == 1 ? (wib & 7) : 0];
+  u64* acc70 = acc66 + 32;
+  if (MODE == 1) { acc66[lane] = 0; acc70[lane] = 0; }
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t idx = gw; idx < nu; idx += nw) {
@@ -223,8 +273,21 @@ __global__ void __launch_bounds__(256) k_cliques_warp(
     }
     __syncwarp();
     u64 acc_u0 = 0, acc_u1 = 0;
+    if (MODE == 1) {
+      clique_edges66(g, S, 1, ou, q0, q1, lane, 32, Te, K4t, acc66, acc70);
+      __syncwarp();
+      if (lane < k) {
+        const int32_t Li = g.ocol[ou + lane];
+        if (acc66[lane]) atomicAdd(&R66[Li], acc66[lane]);
+        if (acc70[lane]) atomicAdd(&R70[Li], acc70[lane]);
+        acc66[lane] = 0;
+        acc70[lane] = 0;
+      }
+      __syncwarp();
+    }
     for (int i = 0; i < k; i++)
-      clique_row<MODE>(g, S, 1, k, ou, i, lane, do_k4, do_k5, Te, K4t, K4v, K4e, K5v, R66, R70, acc_u0, acc_u1);
+      clique_row<MODE>(g, S, 1, k, ou, i, lane, do_k4, do_k5, MODE != 1, Te, K4t, K4v, K4e, K5v, R66, R70, acc_u0,
+                       acc_u1);
     acc_u0 = warp_sum(acc_u0);
     acc_u1 = warp_sum(acc_u1);
     if (lane == 0) {

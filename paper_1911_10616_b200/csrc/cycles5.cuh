@@ -550,8 +550,8 @@ __device__ __forceinline__ void c5_step3(const DGraph& g, int32_t l, const Eng& 
       const u64 q = rec_q(rj);
       const bool adjj = c5_flags(rj) & C5_ADJ;
       const u64 lj = (l > j && adjj) ? 1ull : 0ull;
-      const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-      const u64 c = q * (adjj ? 1ull : 0ull) * (dj - lj) + (rec_qt(rj) - q * lj);
+      u64 c = rec_qt(rj) - q * lj;
+      if (adjj) c += q * ((u64)(g.orow[j + 1] - g.orow[j]) - lj);
       if (c) atomicAdd(&C5[j], (u64)0 - c);
     }
 }
@@ -574,8 +574,9 @@ __device__ __forceinline__ void c5_steps456(const DGraph& g, const u32* __restri
         const auto* rj = loc.peek(j);
         const bool adjj = c5_flags(rj) & C5_ADJ;
         const u64 lj = (l > j && adjj) ? 1ull : 0ull;
-        const u64 dj = (u64)(g.orow[j + 1] - g.orow[j]);
-        return rec_s(rj) - (((adjj ? (dj - lj) : 0ull) + ((u64)Thigh[e] - lj)) & cm);
+        u64 c = (u64)Thigh[e] - lj;
+        if (adjj) c += (u64)(g.orow[j + 1] - g.orow[j]) - lj;  // d+(j): read for neighbours of l only
+        return rec_s(rj) - (c & cm);
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });
   C5_PHASE(4);
@@ -606,8 +607,11 @@ __device__ __forceinline__ void c5_steps456(const DGraph& g, const u32* __restri
         if (i == l) return 0;
         const int32_t w = g.ci[r0 + t];
         const auto* ri = loc.peek(i);
-        u64 corr = (w < i) ? (u64)g.tlows[r0 + t] : 0ull;
-        if (w < l && w < i) corr += (u64)g.tmids[s] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
+        u64 corr = 0;
+        if (w < i) {  // (the typed triangle counts are read only where they enter)
+          corr = (u64)g.tlows[r0 + t];
+          if (w < l) corr += (u64)g.tmids[s] - ((l < i && c5_adj(ri)) ? 1ull : 0ull);
+        }
         return rec_p(ri) - (corr & cm);
       },
       [&](int t, u64 s) { atomicAdd(&C5[g.ci[r0 + t]], s); });

@@ -1029,15 +1029,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       if (mode == 0) {
         if (smem > 48 * 1024)
           CK(cudaFuncSetAttribute(k_cliques<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_cliques<0><<<grid, block, smem, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
+        k_cliques<0><<<grid, block, smem, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, 0, 0, cscratch,
                                                  cscratch_words, 1, cmine, Te, K4t, Fp(F_K4), K4e, Fp(F_K5),
                                                  nullptr, nullptr);
       } else {
-        if (smem > 48 * 1024)
-          CK(cudaFuncSetAttribute(k_cliques<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_cliques<1><<<grid, block, smem, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, cscratch,
-                                                 cscratch_words, 0, cmine, Te, K4t, nullptr, nullptr, nullptr,
-                                                 Fp(F_R66), Fp(F_R70));
+        // theta66 / theta70 per local edge: 2 x kmax u64 accumulators after the bitmap (shared-memory bins)
+        const int accw = b < 4 ? (words + 1) & ~1 : 0;
+        const size_t smem1 = b < 4 ? (size_t)accw * sizeof(u32) + (size_t)2 * kmax * sizeof(u64) : smem;
+        if (smem1 > 48 * 1024)
+          CK(cudaFuncSetAttribute(k_cliques<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+        k_cliques<1><<<grid, block, smem1, lst>>>(g, cbins + (size_t)b * n, hcounts[b], words, accw, kmax, cscratch,
+                                                  cscratch_words, 0, cmine, Te, K4t, nullptr, nullptr, nullptr,
+                                                  Fp(F_R66), Fp(F_R70));
       }
       C.launches++;
     }
@@ -1081,6 +1084,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // passes overlap (the GPU analogue of the paper's concurrent orbit groups).
   struct Job { int pass; int rank; std::function<void(cudaStream_t)> fn; };
   std::vector<Job> jobs;  // rank: launch order / stream priority (long single-item tails first)
+  u64* pair_pa = nullptr;  // the pair pass's per-vertex credits (PairField order, interleaved)
   C.mark(P_PAIR);
   C.tick("start");
   if (n > 0 && m > 0) {
@@ -1142,8 +1146,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       k_hub_maps<<<std::min(nmaps, 4 * SM), 256, 0, C.st>>>(g, Te, hubs, nmaps, hpos);
     }
     C.launches += 2;
-    PairOut po{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R51), Fp(F_R63), Fp(F_R49), Fp(F_R62), Fp(F_R64), C4e, hstar,
-               hslot, hpos};
+    pair_pa = A.alloc<u64>((size_t)n * PO_STRIDE);
+    CK(cudaMemsetAsync(pair_pa, 0, sizeof(u64) * (size_t)n * PO_STRIDE, C.st));
+    PairOut po{pair_pa, C4e, hstar, hslot, hpos};
     const size_t freeb = avail_bytes(C.dev);
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
     const char* phg_env = getenv("EVOKE_PAIR_HG");  // developer knob: heavy-source CTAs
@@ -1582,6 +1587,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   // pair pass's (R8, C4e): they start on a stream of their own when the pair jobs end and run
   // beside the 5-cycle / hub-local / theta66-70 tails
   auto gathers23 = [&](cudaStream_t gs) {
+    if (pair_pa) {  // the pair pass's credits, interleaved by vertex, into their fields
+      const PairFields fl{{Fp(F_R8), Fp(F_R36), Fp(F_R50), Fp(F_R63), Fp(F_R51), Fp(F_R49), Fp(F_R62), Fp(F_R64)}};
+      k_pair_fields<<<grid_for((int64_t)n * PO_STRIDE, B, SM), B, 0, gs>>>(pair_pa, n, fl);
+      C.launches++;
+    }
     if (n > 0) {
       gather_on(gs, k_nbr<2>, k_nbr_heavy<2>, 1);
       if (!four) gather_on(gs, k_nbr<3>, k_nbr_heavy<3>, 2);

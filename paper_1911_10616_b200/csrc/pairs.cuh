@@ -39,13 +39,21 @@
 #include "common.cuh"
 #include "sched.cuh"
 
+// The pair pass's per-vertex credits, interleaved by vertex (PO_STRIDE u64 per vertex, the
+// four per-pair terms of a vertex in one 32-byte sector): the x-side credits of a pair are
+// scattered atomics, one sector each instead of one per field.  k_pair_fields copies them into
+// the per-field arrays F afterwards.
+enum PairField { PO_R8 = 0, PO_R36, PO_R50, PO_R63, PO_R51, PO_R49, PO_R62, PO_R64, PO_STRIDE };
 struct PairOut {
-  u64 *R8, *R36, *R50, *R51, *R63, *R49, *R62, *R64, *C4e;
+  u64* pa;  // [n][PO_STRIDE]
+  u64* C4e;
   const int32_t* hstar;     // per source: its heaviest neighbour h* (wedges through h* are not walked)
   const int32_t* hub_slot;  // per vertex: row of its position map, or -1
   const int32_t* hub_pos;   // [slot][x]: position of x in N(hub) if x ~ hub, else -1
 };
-__device__ __forceinline__ void xadd(u64* field, int32_t x, u64 v) { atomicAdd(&field[x], v); }
+__device__ __forceinline__ void xadd(const PairOut& o, int f, int32_t x, u64 v) {
+  atomicAdd(&o.pa[(size_t)x * PO_STRIDE + f], v);
+}
 __device__ __forceinline__ int64_t slot_of_lo_in_hi(const DGraph& g, int32_t e) { return g.eslot_hi[e]; }
 __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) {
   const int32_t a = g.esrc[e];
@@ -267,10 +275,10 @@ __device__ __forceinline__ void pair_c_terms(const DGraph& g, const PairOut& o, 
   a36 += c2 * (u64)(int64_t)(dg_deg(g, x) - 2);
   a50 += c3;
   a63 += t63;
-  xadd(o.R8, x, c2);
-  xadd(o.R36, x, c2 * (du - 2));  // du >= w >= 2
-  if (c3) xadd(o.R50, x, c3);
-  if (t63) xadd(o.R63, x, t63);
+  xadd(o, PO_R8, x, c2);
+  xadd(o, PO_R36, x, c2 * (du - 2));  // du >= w >= 2
+  if (c3) xadd(o, PO_R50, x, c3);
+  if (t63) xadd(o, PO_R63, x, t63);
 }
 
 // ---- per-element work (shared by the warp and CTA engines) --------------------------
@@ -311,9 +319,9 @@ struct PairAcc {
   __device__ __forceinline__ void zero() { c5 = c49 = c62 = c64 = 0; }
   __device__ __forceinline__ void flush(int32_t u, int32_t v, int32_t e, const PairOut& o) {
     if (u < v && c5) atomicAdd(&o.C4e[e], c5);
-    if (c49) atomicAdd(&o.R49[v], c49);
-    if (c62) atomicAdd(&o.R62[v], c62);
-    if (c64) atomicAdd(&o.R64[v], c64);
+    if (c49) xadd(o, PO_R49, v, c49);
+    if (c62) xadd(o, PO_R62, v, c62);
+    if (c64) xadd(o, PO_R64, v, c64);
     zero();
   }
 };
@@ -328,7 +336,7 @@ __device__ __forceinline__ void pass1_wedge(const DGraph& g, int64_t rb, int k, 
 __device__ __forceinline__ void wedge_x_side(const DGraph& g, const PairOut& o, int32_t x, int32_t v, int64_t t,
                                              int tuv, u64 w) {
   if (x < v) atomicAdd(&o.C4e[g.eid[t]], w - 1);
-  if (tuv) xadd(o.R51, x, (u64)tuv * (w - 1));
+  if (tuv) xadd(o, PO_R51, x, (u64)tuv * (w - 1));
 }
 
 // Chords and diamonds, flattened on two levels.  Every lane brings at most one chord
@@ -489,7 +497,7 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
     });
     __syncwarp();
     if (PASS == 2) {
-      if (have && acc[lane]) atomicAdd(&o.R64[it.v], acc[lane]);
+      if (have && acc[lane]) xadd(o, PO_R64, it.v, acc[lane]);
       acc[lane] = 0;
       __syncwarp();
     }
@@ -629,7 +637,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     });
     __syncwarp();
     if (PASS == 2) {
-      if (have && acc[lane]) atomicAdd(&o.R64[it.v], acc[lane]);
+      if (have && acc[lane]) xadd(o, PO_R64, it.v, acc[lane]);
       acc[lane] = 0;
       __syncwarp();
     }
@@ -719,7 +727,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       }
       if (PASS == 2) {
         A.c64 = warp_sum(A.c64);
-        if (lane == 0 && A.c64) atomicAdd(&o.R64[E.Q.qv[q]], A.c64);
+        if (lane == 0 && A.c64) xadd(o, PO_R64, E.Q.qv[q], A.c64);
       }
       continue;
     }
@@ -912,7 +920,7 @@ __device__ __forceinline__ void s51_adjacent(const DGraph& g, const PairOut& o, 
     const u64 w = tab.get_w_or0(x);
     if (w < 2) continue;
     s51 -= w * (w - 1);
-    xadd(o.R51, x, (u64)0 - w * (w - 1));
+    xadd(o, PO_R51, x, (u64)0 - w * (w - 1));
   }
 }
 
@@ -979,11 +987,11 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   __syncthreads();
   if (threadIdx.x == 0) {
     // atomics: the pairs' lower ends credit their upper ends concurrently
-    if (red[0]) atomicAdd(&o.R8[u], red[0]);
-    if (red[1]) atomicAdd(&o.R36[u], red[1]);
-    if (red[2]) atomicAdd(&o.R50[u], red[2]);
-    if (red[3]) atomicAdd(&o.R51[u], red[3]);
-    if (red[4]) atomicAdd(&o.R63[u], red[4]);
+    if (red[0]) xadd(o, PO_R8, u, red[0]);
+    if (red[1]) xadd(o, PO_R36, u, red[1]);
+    if (red[2]) xadd(o, PO_R50, u, red[2]);
+    if (red[3]) xadd(o, PO_R51, u, red[3]);
+    if (red[4]) xadd(o, PO_R63, u, red[4]);
     if (hs >= 0) {
       H.c5 = red[5]; H.c49 = red[6]; H.c62 = red[7]; H.c64 = 0;
       H.flush(u, hs, euh, o);
@@ -1024,11 +1032,11 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
   a8 = warp_sum(a8); a36 = warp_sum(a36); a50 = warp_sum(a50); a63 = warp_sum(a63); s51 = warp_sum(s51);
   H.c5 = warp_sum(H.c5); H.c49 = warp_sum(H.c49); H.c62 = warp_sum(H.c62);
   if (lane == 0) {
-    if (a8) atomicAdd(&o.R8[u], a8);
-    if (a36) atomicAdd(&o.R36[u], a36);
-    if (a50) atomicAdd(&o.R50[u], a50);
-    if (s51) atomicAdd(&o.R51[u], s51);
-    if (a63) atomicAdd(&o.R63[u], a63);
+    if (a8) xadd(o, PO_R8, u, a8);
+    if (a36) xadd(o, PO_R36, u, a36);
+    if (a50) xadd(o, PO_R50, u, a50);
+    if (s51) xadd(o, PO_R51, u, s51);
+    if (a63) xadd(o, PO_R63, u, a63);
     if (hs >= 0) H.flush(u, hs, euh, o);
   }
   __syncwarp();
@@ -1254,5 +1262,16 @@ __global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const i
       }
     }
     for (int t = 0; t < PT_COUNT; t++) warp_append(tier == t, u, lists + (size_t)t * g.n, counts + t);
+  }
+}
+
+// the interleaved pair credits into the per-field arrays (fields f0.. in PairField order)
+struct PairFields { u64* f[PO_STRIDE]; };
+__global__ void k_pair_fields(const u64* __restrict__ pa, int32_t n, PairFields fields) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)n * PO_STRIDE;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = (int32_t)(q / PO_STRIDE);
+    const int f = (int)(q % PO_STRIDE);
+    fields.f[f][u] = pa[q];
   }
 }
