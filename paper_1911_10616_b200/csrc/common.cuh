@@ -86,6 +86,8 @@ __device__ __forceinline__ u32 lt_mask(int j, int w) {
 // ---------------------------------------------------------------------------
 // Device graph view (relabelled ids = degeneracy rank).
 // ---------------------------------------------------------------------------
+#define OUT8 8
+#define OUT8_LONG (-2)
 struct DGraph {
   int32_t n;
   int64_t m;            // undirected edges
@@ -103,6 +105,11 @@ struct DGraph {
   const int32_t* esrc;  // [m] lower endpoint
   const int32_t* edst;  // [m] higher endpoint
   const int64_t* eslot_hi; // [m] slot of esrc inside edst's list
+  const int32_t* twin;  // [2m] for the slot of v in N(u): the slot of u in N(v)
+  // out-lists of at most OUT8 vertices in one 32-byte row each: out8[8 j + t] = N+(j)[t],
+  // -1 past the end; out8[8 j] = OUT8_LONG when d+(j) > OUT8 (then orow / ocol).  Built only
+  // when every out-list is that short (nullptr otherwise)
+  const int32_t* out8;
   // oriented triangle lists: edge e=(a->b): third vertices c > b, sorted
   const int64_t* toff;  // [m+1]
   const int32_t* tc;    // [ntri]

@@ -518,16 +518,26 @@ __device__ __forceinline__ void c5_step3(const DGraph& g, int32_t l, const Eng& 
                                          int nj, u64* __restrict__ C5, C5Split sp) {
   eng.lists(nj,
       [&](int t, int64_t& base, int& len) {
+        // N+(j) from j's out8 row (one sector) when it is short; base < 0 encodes the row
         const int32_t j = loc.id_of(J[t]);
-        base = g.orow[j];
-        len = sp.mine(j) ? (int)(g.orow[j + 1] - base) : 0;
+        if (g.out8) {  // (every out-list is short: max d+ <= OUT8)
+          const int4* r = reinterpret_cast<const int4*>(g.out8 + (size_t)OUT8 * j);
+          const int4 a = r[0];
+          const int4 b = r[1];
+          len = (a.x >= 0) + (a.y >= 0) + (a.z >= 0) + (a.w >= 0) + (b.x >= 0) + (b.y >= 0) + (b.z >= 0) + (b.w >= 0);
+          base = ~((int64_t)OUT8 * j);
+        } else {  // (a graph with longer out-lists: an extra load for every j was slower, config 3)
+          base = g.orow[j];
+          len = (int)(g.orow[j + 1] - base);
+        }
+        if (!sp.mine(j)) len = 0;
       },
       [&](int t, int64_t base, int k) -> u64 {
         // Only i with Wn[i] > 0 can close a 5-cycle: a path i <- j <- k -> l with Wn[i] = 0
         // has j !~ l and i !~ k (both would be wedges (i, w, l)), so its every term (P Wn,
         // A, the QM correction, its share of S[j]) is zero.  The lookup is read-only: no
         // record is created for such i (Wn is final after step 1).
-        const int32_t i = g.ocol[base + k];
+        const int32_t i = base >= 0 ? g.ocol[base + k] : g.out8[~base + k];
         if (i == l) return 0;
         const auto* rj = &loc.R[J[t]];
         u64 wn;
@@ -838,7 +848,11 @@ __global__ void __launch_bounds__(C5_HBT) k_c5_giant(int part, DGraph g, const u
 
 // Light endpoints: one warp each, 16-byte records in a per-warp open-addressing region whose
 // used part is sized per endpoint (2 x its record bound, so the records stay L2-resident).
-__global__ void __launch_bounds__(C5_BT) k_c5_light(DGraph g, const u32* __restrict__ Tlow,
+#ifndef C5_LIGHT_MINB
+#define C5_LIGHT_MINB 6  // resident CTAs per SM the register budget must allow (40 registers: config 4 light
+                         // endpoints 48.8 ms vs 50.4 at 48 registers / 5 CTAs, 49.7 at 32 registers / 8 CTAs)
+#endif
+__global__ void __launch_bounds__(C5_BT, C5_LIGHT_MINB) k_c5_light(DGraph g, const u32* __restrict__ Tlow,
                                                     const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                     const int32_t* __restrict__ light, const u32* __restrict__ lw,
                                                     int n_light, int* __restrict__ counter,

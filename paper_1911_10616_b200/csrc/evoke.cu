@@ -809,6 +809,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   int32_t* esrc = A.alloc<int32_t>(m + 1);
   int32_t* edst = A.alloc<int32_t>(m + 1);
   int64_t* eslot_hi = A.alloc<int64_t>(m + 1);
+  int32_t* twin = A.alloc<int32_t>(m2 + 1);
   int max_deg = 0, max_out = 0;
   if (n > 0) {
     int32_t* degc = A.alloc<int32_t>(n, true);
@@ -831,7 +832,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     C.launches += 4;
     if (m > 0) {
       k_edge_arrays<<<grid_for(m2, B, SM), B, 0, C.st>>>(dks, m2, rp, ci, dmv, orow, eid, ocol, esrc, edst,
-                                                         eslot_hi);
+                                                         eslot_hi, twin);
       C.launches++;
     }
     int* d_mx = A.alloc<int>(2, true);
@@ -854,7 +855,13 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   std::memset(&g, 0, sizeof(g));
   g.n = n; g.m = m; g.max_deg = std::max(max_deg, 1); g.max_out = max_out;
   g.rp = rp; g.ci = ci; g.dm = dmv; g.deg = degv; g.eid = eid; g.orow = orow; g.ocol = ocol; g.esrc = esrc;
-  g.edst = edst; g.eslot_hi = eslot_hi;
+  g.edst = edst; g.eslot_hi = eslot_hi; g.twin = twin;
+  if (n > 0 && max_out <= OUT8) {  // out8 rows only when every out-list fits one (no fallback loads)
+    int32_t* out8 = A.alloc<int32_t>((size_t)OUT8 * n);
+    k_out8<<<grid_for(n, B, SM), B, 0, C.st>>>(n, orow, ocol, reinterpret_cast<int4*>(out8));
+    C.launches++;
+    g.out8 = out8;
+  }
 
   // per-vertex fields and per-edge arrays
   u64* F = A.alloc<u64>((size_t)F_COUNT * std::max(n, 1), true);
@@ -978,6 +985,12 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   const bool whole_gpu_passes = m > concurrent_max_m;
   // per sharded pass (pair, hub-local, 5-cycle, cliques): this shard's and all work estimates
   u64* d_work = A.alloc<u64>(8, true);
+  // rows of the late gathers (k_pack_rows, k_trigather): allocated here, before the passes
+  // run (a pool allocation while the random-access passes run slowed them: TLB updates)
+  u64* V2rows = n > 0 ? A.alloc<u64>((size_t)n * V2_W) : nullptr;
+  u64* EVrows = n > 0 ? A.alloc<u64>((size_t)std::max<int64_t>(m, 1) * EV_W) : nullptr;
+  u64* TGrows = (ntri > 0 && !(o.flags & EVOKE_FLAG_FOUR) && 3 * ntri <= TG_ROWS_MAX_TPV * (int64_t)n)
+                    ? A.alloc<u64>((size_t)n * TG_W) : nullptr;
   // ------------------------------------------------------------------ a5/a9: cliques
   C.mark(P_CLIQ);
   const uint8_t* cmine = nullptr;
@@ -1592,13 +1605,31 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       k_pair_fields<<<grid_for((int64_t)n * PO_STRIDE, B, SM), B, 0, gs>>>(pair_pa, n, fl);
       C.launches++;
     }
+    if (n > 0) {  // rows of the values the late gathers read at random places
+      k_pack_rows<<<grid_for(std::max<int64_t>(n, m), B, SM), B, 0, gs>>>(g, ev, F, V2rows, EVrows);
+      C.launches++;
+      ev.V2 = V2rows;
+      ev.EV = EVrows;
+    }
     if (n > 0) {
       gather_on(gs, k_nbr<2>, k_nbr_heavy<2>, 1);
       if (!four) gather_on(gs, k_nbr<3>, k_nbr_heavy<3>, 2);
     }
   };
   auto trigather = [&](cudaStream_t gs) {
-    if (ntri > 0 && !four) { k_trigather<<<grid_for(ntri, B, SM), B, 0, gs>>>(g, ev, F); C.launches++; }
+    if (ntri > 0 && !four) {
+      // rows while the graph averages few triangles per vertex (config 4: 4.2 -> 2.5 ms);
+      // straight into the fields on triangle-heavy graphs (config 3: 48 ms vs 62 ms in rows)
+      if (3 * ntri <= TG_ROWS_MAX_TPV * (int64_t)n) {
+        CK(cudaMemsetAsync(TGrows, 0, sizeof(u64) * (size_t)n * TG_W, gs));
+        k_trigather<true><<<grid_for(ntri, B, SM), B, 0, gs>>>(g, ev, TGrows);
+        k_tg_fields<<<grid_for((int64_t)n * TG_W, B, SM), B, 0, gs>>>(TGrows, n, F);
+        C.launches += 2;
+      } else {
+        k_trigather<false><<<grid_for(ntri, B, SM), B, 0, gs>>>(g, ev, F);
+        C.launches++;
+      }
+    }
   };
   if (!serial && n > 0 && !getenv("EVOKE_NO_EARLY_GATHERS")) {
     C.gathers_early = true;
@@ -1786,7 +1817,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       // algorithmic bytes per pass = units x the bytes of graph data each unit must read
       // (DESIGN.md section 5.2); per-source / per-endpoint tables are on-chip or L2 scratch
       s->alg_bytes[P_TRI] = 8.0 * (double)hu.tri_stream + 16.0 * (double)ntri;
-      s->alg_bytes[P_PAIR] = 16.0 * (double)hu.pair_rwedge + 8.0 * (double)hu.pair_hwalk + 12.0 * (double)hu.sum_te2;
+      s->alg_bytes[P_PAIR] = 16.0 * (double)hu.pair_rwedge + 8.0 * (double)hu.pair_hwalk + 8.0 * (double)hu.sum_te2;
       s->alg_bytes[P_HUB] = 28.0 * (double)hu.hub;
       s->alg_bytes[P_C5] = 12.0 * (double)hu.c5_wedge + 12.0 * (double)hu.c5_q;
       s->alg_bytes[P_TRIG] = 16.0 * (double)ntri + 3.0 * 14.0 * 16.0 * (double)ntri;

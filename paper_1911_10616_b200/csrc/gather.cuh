@@ -29,7 +29,18 @@ struct EdgeVals {
   const u64* C4e;   // E5
   const u64* E7;
   const u32* K4t;
+  // packed rows for the late gathers (k_pack_rows): per vertex V2[v][V2_W], per edge EV[e][EV_W]
+  const u64* V2 = nullptr;
+  const u64* EV = nullptr;
 };
+
+// The late gathers (nbr2, the triangle gather) read, for every neighbour v / triangle corner,
+// about ten per-vertex fields and five per-edge values at random places: one 32-byte sector
+// per field in the field-major layout.  k_pack_rows copies them once (coalesced) into rows --
+// per vertex 96 bytes (the values of v the gathers read; the first sector holds what the
+// triangle gather needs), per edge 64 bytes -- so a random visit reads 1-3 sectors.
+enum { V2_D = 0, V2_DM1, V2_T, V2_DM5, V2_DM6, V2_DM10, V2_DM9, V2_DM13, V2_DM12, V2_K4, V2_R8, V2_W = 12 };
+enum { EV_E9F = 0, EV_E9B, EV_K4E, EV_C4E, EV_E7, EV_TE, EV_W = 8 };
 
 #define FLD(f, u) F[(size_t)(f) * (size_t)n + (u)]
 
@@ -82,31 +93,60 @@ __device__ __forceinline__ void nbr1_store(u64* __restrict__ F, int32_t n, int32
   FLD(F_S41, u) = a[8]; FLD(F_S55, u) = a[9];
 }
 
+__global__ void k_pack_rows(DGraph g, EdgeVals ev, const u64* __restrict__ F, u64* __restrict__ V2,
+                            u64* __restrict__ EV) {
+  const int32_t n = g.n;
+  const int64_t N = max((int64_t)n, g.m);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+    if (q < n) {
+      const int32_t v = (int32_t)q;
+      const u64 d = (u64)dg_deg(g, v), dm1 = FLD(F_DM1, v), t = FLD(F_T, v);
+      ulonglong2* r = reinterpret_cast<ulonglong2*>(V2 + (size_t)v * V2_W);
+      r[0] = make_ulonglong2(d, dm1);
+      r[1] = make_ulonglong2(t, dm1 * (d - 1) - 2 * t);  // DM5(v)
+      r[2] = make_ulonglong2(FLD(F_DM6, v), FLD(F_DM10, v));
+      r[3] = make_ulonglong2(FLD(F_DM9, v), FLD(F_DM13, v));
+      r[4] = make_ulonglong2(FLD(F_DM12, v), FLD(F_K4, v));
+      r[5] = make_ulonglong2(FLD(F_R8, v), 0ull);
+    }
+    if (q < g.m) {
+      ulonglong2* r = reinterpret_cast<ulonglong2*>(EV + (size_t)q * EV_W);
+      r[0] = make_ulonglong2(ev.E9f[q], ev.E9b[q]);
+      r[1] = make_ulonglong2(ev.K4e[q], ev.C4e[q]);
+      r[2] = make_ulonglong2(ev.E7[q], (u64)ev.Te[q]);
+    }
+  }
+}
+
 // ---- nbr2: needs DM1, DM6, DM9, DM10, DM12, DM13, K4, R8 of neighbours and E5/E9/E11
+// (from the packed rows)
 __device__ __forceinline__ void nbr2_acc(const DGraph& g, const EdgeVals& ev, const u64* __restrict__ F, int32_t n,
                                          int32_t u, int64_t start, int stride, u64 (&a)[14]) {
   for (int64_t s = g.rp[u] + start; s < g.rp[u + 1]; s += stride) {
     const int32_t v = g.ci[s];
     const int32_t e = g.eid[s];
-    const u64 dv = (u64)dg_deg(g, v);
-    const u64 dm1v = FLD(F_DM1, v);
-    const u64 te = ev.Te[e];
-    const u64 e9vu = (v < u) ? ev.E9f[e] : ev.E9b[e];  // E9<v,u>
-    const u64 k4e = ev.K4e[e];
-    a[0] += dm1v;
-    a[1] += FLD(F_DM6, v);
-    a[2] += dm1v * (dv - 1) - 2 * FLD(F_T, v);           // DM5(v)
-    a[3] += FLD(F_DM10, v);
-    a[4] += FLD(F_DM9, v);
-    a[5] += FLD(F_DM13, v);
+    const u64 te = g.tes[s];
+    const ulonglong2* r = reinterpret_cast<const ulonglong2*>(ev.V2 + (size_t)v * V2_W);
+    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(ev.EV + (size_t)e * EV_W);
+    const ulonglong2 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3], r4 = r[4], r5 = r[5];
+    const ulonglong2 q0 = q[0], q1 = q[1];
+    const u64 dv = r0.x;
+    const u64 e9vu = (v < u) ? q0.x : q0.y;  // E9<v,u>
+    const u64 k4e = q1.x;
+    a[0] += r0.y;            // DM1(v)
+    a[1] += r2.x;            // DM6(v)
+    a[2] += r1.y;            // DM5(v)
+    a[3] += r2.y;            // DM10(v)
+    a[4] += r3.x;            // DM9(v)
+    a[5] += r3.y;            // DM13(v)
     a[6] += e9vu * (dv - 3);
-    a[7] += FLD(F_DM12, v);
-    a[8] += FLD(F_K4, v);
+    a[7] += r4.x;            // DM12(v)
+    a[8] += r4.y;            // K4(v)
     a[9] += k4e * (dv - 3);
     a[10] += e9vu * (te - 1);
     a[11] += k4e * (te - 2);
-    a[12] += FLD(F_R8, v);
-    a[13] += ev.C4e[e] * (dv - 2);
+    a[12] += r5.x;           // R8(v)
+    a[13] += q1.y * (dv - 2);  // C4e
   }
 }
 __device__ __forceinline__ void nbr2_store(const DGraph& g, u64* __restrict__ F, int32_t n, int32_t u,
@@ -204,38 +244,79 @@ __global__ void __launch_bounds__(1024) k_nbr_heavy(DGraph g, EdgeVals ev, u64* 
 }
 
 // ---- triangle sums: thread per oriented triangle entry; each of the three vertices
-// gets the summand of every triangle-sum equation with itself as u.
-__device__ __forceinline__ void tri_credit(const DGraph& g, const EdgeVals& ev, u64* __restrict__ F,
-                                           int32_t n, int32_t u, int32_t v, int32_t x, int32_t euv,
-                                           int32_t eux, int32_t evx, u64 k4t) {
-  const u64 du = dg_deg(g, u), dv = dg_deg(g, v), dx = dg_deg(g, x);
-  const u64 tuv = ev.Te[euv], tux = ev.Te[eux], tvx = ev.Te[evx];
-  atomicAdd(&FLD(F_T25, u), (dv - 2) * (dx - 2));
-  atomicAdd(&FLD(F_T26, u), (du - 2) * ((dx - 2) + (dv - 2)));
-  atomicAdd(&FLD(F_T29, u), FLD(F_DM1, v) + FLD(F_DM1, x));
-  atomicAdd(&FLD(F_T32, u), binom2(dv - 2) + binom2(dx - 2));
-  atomicAdd(&FLD(F_T43, u), (FLD(F_T, v) - 1) + (FLD(F_T, x) - 1));
-  atomicAdd(&FLD(F_T46, u), ev.E7[evx]);
-  atomicAdd(&FLD(F_T48, u), (tuv - 1) * (dx - 2) + (tux - 1) * (dv - 2));
-  atomicAdd(&FLD(F_T54, u), binom2(tvx - 1));
-  atomicAdd(&FLD(F_T59, u), ev.E9f[evx] + ev.E9b[evx]);
-  atomicAdd(&FLD(F_T61, u), (tuv - 1) * (tux - 1));
-  atomicAdd(&FLD(F_T65, u), ev.K4e[evx]);
-  atomicAdd(&FLD(F_T71, u), binom2(k4t));
-  atomicAdd(&FLD(F_T52, u), ev.C4e[evx]);
-  atomicAdd(&FLD(F_T53, u), ev.C4e[euv] + ev.C4e[eux]);
+// gets the summand of every triangle-sum equation with itself as u, into per-vertex rows of
+// TG_W accumulators (one vertex's 14 sums in four sectors instead of 14 fields; k_tg_fields
+// copies them into F).  Corner and edge values from the packed rows.
+#define TG_ROWS_MAX_TPV 64  // triangle gather in rows while 3 #T <= this x n (triangle corners per vertex)
+enum { TG_T25 = 0, TG_T26, TG_T29, TG_T32, TG_T43, TG_T46, TG_T48, TG_T54, TG_T59, TG_T61, TG_T65, TG_T71,
+       TG_T52, TG_T53, TG_W = 16 };
+struct TriCorner {  // the first sector of a vertex row
+  u64 d, dm1, t;
+};
+__device__ __forceinline__ TriCorner tri_corner(const EdgeVals& ev, int32_t v) {
+  const ulonglong2* r = reinterpret_cast<const ulonglong2*>(ev.V2 + (size_t)v * V2_W);
+  const ulonglong2 a = r[0], b = r[1];
+  return TriCorner{a.x, a.y, b.x};
+}
+struct TriEdge {
+  u64 e9f, e9b, k4e, c4e, e7, te;
+};
+__device__ __forceinline__ TriEdge tri_edge(const EdgeVals& ev, int32_t e) {
+  const ulonglong2* r = reinterpret_cast<const ulonglong2*>(ev.EV + (size_t)e * EV_W);
+  const ulonglong2 a = r[0], b = r[1], c = r[2];
+  return TriEdge{a.x, a.y, b.x, b.y, c.x, c.y};
+}
+// corner u with the other corners v, x; edges uv, ux and the opposite edge vx.  ROWS: into
+// u's row of TG; else straight into the fields of F (triangle-heavy graphs: a hub's credits
+// spread over 14 lines instead of queueing on the 4 lines of its row)
+template <bool ROWS>
+__device__ __forceinline__ void tri_credit(u64* __restrict__ TG, int32_t n, int32_t u, const TriCorner& U,
+                                           const TriCorner& V, const TriCorner& X, const TriEdge& Euv,
+                                           const TriEdge& Eux, const TriEdge& Evx, u64 k4t) {
+  const u64 du = U.d, dv = V.d, dx = X.d;
+  const u64 tuv = Euv.te, tux = Eux.te, tvx = Evx.te;
+  u64* F = TG;
+  auto at = [&](int j, int fld) -> u64* { return ROWS ? &TG[(size_t)u * TG_W + j] : &FLD(fld, u); };
+  atomicAdd(at(TG_T25, F_T25), (dv - 2) * (dx - 2));
+  atomicAdd(at(TG_T26, F_T26), (du - 2) * ((dx - 2) + (dv - 2)));
+  atomicAdd(at(TG_T29, F_T29), V.dm1 + X.dm1);
+  atomicAdd(at(TG_T32, F_T32), binom2(dv - 2) + binom2(dx - 2));
+  atomicAdd(at(TG_T43, F_T43), (V.t - 1) + (X.t - 1));
+  atomicAdd(at(TG_T46, F_T46), Evx.e7);
+  atomicAdd(at(TG_T48, F_T48), (tuv - 1) * (dx - 2) + (tux - 1) * (dv - 2));
+  atomicAdd(at(TG_T54, F_T54), binom2(tvx - 1));
+  atomicAdd(at(TG_T59, F_T59), Evx.e9f + Evx.e9b);
+  atomicAdd(at(TG_T61, F_T61), (tuv - 1) * (tux - 1));
+  atomicAdd(at(TG_T65, F_T65), Evx.k4e);
+  atomicAdd(at(TG_T71, F_T71), binom2(k4t));
+  atomicAdd(at(TG_T52, F_T52), Evx.c4e);
+  atomicAdd(at(TG_T53, F_T53), Euv.c4e + Eux.c4e);
 }
 
-__global__ void k_trigather(DGraph g, EdgeVals ev, u64* __restrict__ F) {
-  const int32_t n = g.n;
+// ROWS: TG = the row accumulators (k_tg_fields copies them); else TG = F
+template <bool ROWS>
+__global__ void k_trigather(DGraph g, EdgeVals ev, u64* __restrict__ TG) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.ntri;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int32_t eab = g.tab[q], eac = g.tac[q], ebc = g.tbc[q];
     const int32_t a = g.esrc[eab], b = g.edst[eab], c = g.tc[q];
     const u64 k4t = ev.K4t[q];
-    tri_credit(g, ev, F, n, a, b, c, eab, eac, ebc, k4t);
-    tri_credit(g, ev, F, n, b, a, c, eab, ebc, eac, k4t);
-    tri_credit(g, ev, F, n, c, a, b, eac, ebc, eab, k4t);
+    const TriCorner A = tri_corner(ev, a), B = tri_corner(ev, b), C = tri_corner(ev, c);
+    const TriEdge Eab = tri_edge(ev, eab), Eac = tri_edge(ev, eac), Ebc = tri_edge(ev, ebc);
+    tri_credit<ROWS>(TG, g.n, a, A, B, C, Eab, Eac, Ebc, k4t);
+    tri_credit<ROWS>(TG, g.n, b, B, A, C, Eab, Ebc, Eac, k4t);
+    tri_credit<ROWS>(TG, g.n, c, C, A, B, Eac, Ebc, Eab, k4t);
+  }
+}
+
+// the triangle sums into their fields
+__global__ void k_tg_fields(const u64* __restrict__ TG, int32_t n, u64* __restrict__ F) {
+  const int fld[14] = {F_T25, F_T26, F_T29, F_T32, F_T43, F_T46, F_T48, F_T54, F_T59, F_T61, F_T65, F_T71,
+                       F_T52, F_T53};
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)n * TG_W;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(q % TG_W);
+    if (j < 14) F[(size_t)fld[j] * (size_t)n + (size_t)(q / TG_W)] = TG[q];
   }
 }
 

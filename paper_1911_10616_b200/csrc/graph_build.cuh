@@ -339,7 +339,8 @@ __global__ void k_edge_arrays(const u64* __restrict__ dk, int64_t m2, const int6
                               const int32_t* __restrict__ ci, const int32_t* __restrict__ dm,
                               const int64_t* __restrict__ orow, int32_t* __restrict__ eid,
                               int32_t* __restrict__ ocol, int32_t* __restrict__ esrc,
-                              int32_t* __restrict__ edst, int64_t* __restrict__ eslot_hi) {
+                              int32_t* __restrict__ edst, int64_t* __restrict__ eslot_hi,
+                              int32_t* __restrict__ twin) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
        s += (int64_t)gridDim.x * blockDim.x) {
     int32_t u = (int32_t)(dk[s] >> 32);
@@ -356,6 +357,23 @@ __global__ void k_edge_arrays(const u64* __restrict__ dk, int64_t m2, const int6
       int64_t e = orow[w] + (pos - lo);
       eid[s] = (int32_t)e;
       eslot_hi[e] = s;
+      twin[s] = (int32_t)pos;  // the two slots of the edge point at each other
+      twin[pos] = (int32_t)s;
     }
+  }
+}
+
+// out8 rows (DGraph::out8): one 32-byte row per vertex holding a short out-list
+__global__ void k_out8(int32_t n, const int64_t* __restrict__ orow, const int32_t* __restrict__ ocol,
+                       int4* __restrict__ out8) {
+  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int64_t b = orow[j];
+    const int d = (int)(orow[j + 1] - b);
+    int r[OUT8];
+#pragma unroll
+    for (int t = 0; t < OUT8; t++) r[t] = t < d ? ocol[b + t] : -1;
+    if (d > OUT8) r[0] = OUT8_LONG;
+    out8[2 * (size_t)j] = make_int4(r[0], r[1], r[2], r[3]);
+    out8[2 * (size_t)j + 1] = make_int4(r[4], r[5], r[6], r[7]);
   }
 }

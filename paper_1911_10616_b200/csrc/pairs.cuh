@@ -301,15 +301,17 @@ __device__ __forceinline__ int64_t slot_in_other(const DGraph& g, int32_t v, int
 // Item v of source u: its wedge part is the suffix of N(v) after u (x > u); the wedge part of
 // item h* is empty: W(u,x) gets the h* contribution from a membership test over the table
 // keys instead (see hstar_and_terms)
-__device__ __forceinline__ PairItem pair_item(const DGraph& g, int64_t s_uv, int32_t hs) {
+// (u: the source; the slot's twin, T(u,v) per slot and the rank order give the item with two
+// random loads, rp[v+1] and, for items with chords, foff[e])
+__device__ __forceinline__ PairItem pair_item(const DGraph& g, int32_t u, int64_t s_uv, int32_t hs) {
   PairItem it;
   it.v = g.ci[s_uv];
   it.e = g.eid[s_uv];
-  it.vlo = g.esrc[it.e] == it.v;
-  it.rb = slot_in_other(g, it.v, it.e, it.vlo) + 1;
+  it.vlo = it.v < u;  // ranks: the lower endpoint of e(u,v)
+  it.rb = (int64_t)g.twin[s_uv] + 1;
   it.dv = it.v == hs ? 0 : (int32_t)(g.rp[it.v + 1] - it.rb);
-  it.fo = g.foff[it.e];
-  it.tv = (int32_t)(g.foff[it.e + 1] - it.fo);
+  it.tv = (int32_t)g.tes[s_uv];
+  it.fo = it.tv ? g.foff[it.e] : 0;
   return it;
 }
 
@@ -340,21 +342,27 @@ __device__ __forceinline__ void wedge_x_side(const DGraph& g, const PairOut& o, 
 }
 
 // Chords and diamonds, flattened on two levels.  Every lane brings at most one chord
-// (v, w): the k-th third vertex of e(u,v) (PASS 1 keeps w > v only: D(u,x) counts each
-// chord once); the diamond lists tri(v,w) of the (up to 32) chords of the warp are then
-// flattened over the lanes with a second warp_flat.  PASS 2 adds W(u,x)-2 (x > u) into
-// acc[owner] (per-warp shared accumulators, one per item owner).  Warp-uniform call.
+// (v, w): the k-th third vertex of e(u,v), kept only for w > v -- each unordered chord once:
+// PASS 1 adds it to D(u,x) once, and PASS 2's theta64 sum over its diamond list,
+// sum_{x in tri(v,w), x > u} (W(u,x) - 2), is the same for both chord ends (tri(v,w) =
+// tri(w,v)), so it is computed once and credited to v (acc[owner], per-warp shared
+// accumulators, one per item owner) and to w (o->pa).  The diamond lists tri(v,w) of the (up
+// to 32) chords of the warp are flattened over the lanes with a second warp_flat.
+// Warp-uniform call.
 struct NoDefer {
   __device__ __forceinline__ bool operator()(int64_t, int32_t, bool) const { return false; }
 };
 template <int PASS, typename Tab, typename Defer = NoDefer>
 __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool valid, int32_t v, int64_t fo, bool vlo,
-                                            int k, int owner, Tab& tab, u64* acc, Defer defer = Defer()) {
+                                            int k, int owner, Tab& tab, u64* acc, const PairOut* o,
+                                            Defer defer = Defer()) {
   int64_t f0 = 0;
   int len2 = 0;
+  int32_t w = 0;
   if (valid) {
     const int64_t r = fo + k;
-    if (!(PASS == 1 && g.fx[r] <= v)) {
+    w = g.fx[r];
+    if (w > v) {
       const int32_t evw = vlo ? g.fe1[r] : g.fe2[r];
       f0 = g.foff[evw];
       len2 = (int)(g.foff[evw + 1] - f0);
@@ -367,25 +375,29 @@ __device__ __forceinline__ void chords_step(const DGraph& g, int32_t u, bool val
       if (len2 > PAIR_DIAM_DEFER && defer(r, v, vlo)) len2 = 0;
     }
   }
-  int cur = -1;
+  int cur = -1, cown = 0;
+  int32_t cw = 0;
   u64 c = 0;
   warp_flat(len2, [&](int j2, int k2, bool v2) {
     const int64_t f0j = __shfl_sync(FULL_MASK, f0, j2);
     const int own = __shfl_sync(FULL_MASK, owner, j2);
+    const int32_t wj = __shfl_sync(FULL_MASK, w, j2);
     if (!v2) return;
     const int32_t x = g.fx[f0j + k2];
     if (PASS == 1) {
       if (x > u) tab.add_d(x);
     } else {
-      if (own != cur) {
-        if (cur >= 0 && c) atomicAdd(&acc[cur], c);
-        cur = own;
+      if (j2 != cur) {
+        if (cur >= 0 && c) { atomicAdd(&acc[cown], c); xadd(*o, PO_R64, cw, c); }
+        cur = j2;
+        cown = own;
+        cw = wj;
         c = 0;
       }
       if (x > u) c += tab.get_w(x) - 2ull;
     }
   });
-  if (PASS == 2 && cur >= 0 && c) atomicAdd(&acc[cur], c);
+  if (PASS == 2 && cur >= 0 && c) { atomicAdd(&acc[cown], c); xadd(*o, PO_R64, cw, c); }
 }
 
 // Pass-2 wedge walk of up to 32 items (lane's item: list [rb, rb+len), vertex v, edge e),
@@ -467,7 +479,7 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
   for (int64_t o0 = r0; o0 < r1; o0 += 32) {
     PairItem it;
     const bool have = o0 + lane < r1;
-    if (have) it = pair_item(g, o0 + lane, hs);
+    if (have) it = pair_item(g, u, o0 + lane, hs);
     else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
     PairAcc A;
     A.zero();
@@ -493,7 +505,7 @@ __device__ __forceinline__ void warp_pass(const DGraph& g, const u32* __restrict
       const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
       const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
       const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc);
+      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc, &o);
     });
     __syncwarp();
     if (PASS == 2) {
@@ -569,14 +581,14 @@ struct CtaDefer {
     return true;
   }
 };
-__device__ __forceinline__ int part_len(const DGraph& g, const EngQueue& Q, int q, int32_t hs) {
+__device__ __forceinline__ int part_len(const DGraph& g, const EngQueue& Q, int q, int32_t u, int32_t hs) {
   const int kind = Q.qkind[q];
   if (kind == PK_DIAM) {
     const int64_t r = Q.qslot[q];
     const int32_t evw = Q.qvlo[q] ? g.fe1[r] : g.fe2[r];
     return (int)(g.foff[evw + 1] - g.foff[evw]);
   }
-  const PairItem it = pair_item(g, Q.qslot[q], hs);
+  const PairItem it = pair_item(g, u, Q.qslot[q], hs);
   return kind == PK_WEDGE ? it.dv : it.tv;
 }
 
@@ -599,7 +611,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     if (base >= nitems) break;
     PairItem it;
     const bool have = lane < grab && base + lane < nitems;
-    if (have) it = pair_item(g, r0 + base + lane, hs);
+    if (have) it = pair_item(g, u, r0 + base + lane, hs);
     else { it.v = 0; it.e = 0; it.rb = 0; it.fo = 0; it.dv = 0; it.tv = 0; it.vlo = false; }
     const int tuv = it.tv;  // T(u,v) for the wedges' x-side terms (it.tv is zeroed if the chords are queued)
     // defer long parts to the queue (if it has room)
@@ -633,7 +645,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       const int64_t foj = __shfl_sync(FULL_MASK, it.fo, j);
       const bool vloj = __shfl_sync(FULL_MASK, it.vlo, j);
       const int32_t vj = __shfl_sync(FULL_MASK, it.v, j);
-      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc, CtaDefer<ES>{&E});
+      chords_step<PASS>(g, u, valid, vj, foj, vloj, k, j, tab, acc, &o, CtaDefer<ES>{&E});
     });
     __syncwarp();
     if (PASS == 2) {
@@ -659,7 +671,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
     __syncthreads();
     for (int q0 = 0; q0 < nq; q0 += blockDim.x) {
       const int q = q0 + threadIdx.x;
-      const int nc = (q < nq) ? (part_len(g, E.Q, qb + q, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
+      const int nc = (q < nq) ? (part_len(g, E.Q, qb + q, u, hs) + PAIR_CHUNK - 1) / PAIR_CHUNK : 0;
       int ex = 0, tot = 0;
       if (blockDim.x == BT) {
         CScan(cscan).ExclusiveSum(nc, ex, tot);
@@ -725,13 +737,16 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
           if (x > u) A.c64 += tab.get_w(x) - 2ull;
         }
       }
-      if (PASS == 2) {
+      if (PASS == 2) {  // both chord ends: v (queued) and w = fx[r]
         A.c64 = warp_sum(A.c64);
-        if (lane == 0 && A.c64) xadd(o, PO_R64, E.Q.qv[q], A.c64);
+        if (lane == 0 && A.c64) {
+          xadd(o, PO_R64, E.Q.qv[q], A.c64);
+          xadd(o, PO_R64, g.fx[r], A.c64);
+        }
       }
       continue;
     }
-    const PairItem it = pair_item(g, E.Q.qslot[q], hs);
+    const PairItem it = pair_item(g, u, E.Q.qslot[q], hs);
     if (kind == PK_WEDGE) {
       // PAIR_CHUNK / 32 elements per lane, all loads issued before the table updates
       constexpr int U = PAIR_CHUNK / 32;
@@ -783,7 +798,7 @@ __device__ void cta_pass(const DGraph& g, const u32* __restrict__ Te, int32_t u,
       const int k1 = min(it.tv, k0 + PAIR_CHUNK);
       for (int i = 0; i < PAIR_CHUNK / 32; i++) {
         const int k = k0 + lane + 32 * i;
-        chords_step<PASS>(g, u, k < k1, it.v, it.fo, it.vlo, k, 0, tab, acc, CtaDefer<ES>{&E});
+        chords_step<PASS>(g, u, k < k1, it.v, it.fo, it.vlo, k, 0, tab, acc, &o, CtaDefer<ES>{&E});
       }
       __syncwarp();
       if (PASS == 2 && lane == 0) {
