@@ -426,6 +426,12 @@ def roofline(wm, pass_ms, peak_gbs, peak_src, l2_gbs, step_ms=None, config=None,
         base.update({"achieved": None, "frac": None})
         return base
     achieved = bytes_ / t / 1e9
+    if base["traffic"]:
+        # DRAM bytes the pass's kernels actually moved (ncu capture on this config) over the
+        # pass time: how close the random sector traffic runs to the HBM peak
+        base["traffic_gbs"] = base["traffic"] / t / 1e9
+        base["traffic_frac"] = base["traffic_gbs"] / peak_gbs
+        base["traffic_over_algorithmic"] = base["traffic"] / bytes_
     base.update({"achieved": achieved, "frac": achieved / peak_gbs, "algorithmic_bytes": bytes_,
                  "l2": {"peak": l2_gbs, "unit": "GB/s", "frac": achieved / l2_gbs,
                         "peak_source": "measured here: L2-resident copy (2 x 24 MiB buffers, read + write bytes)"}})

@@ -833,7 +833,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (m > 0) {
       k_edge_arrays<<<grid_for(m2, B, SM), B, 0, C.st>>>(dks, m2, rp, ci, dmv, orow, eid, ocol, esrc, edst,
                                                          eslot_hi, twin);
-      C.launches++;
+      k_twin_hi<<<grid_for(m2, B, SM), B, 0, C.st>>>(n, rp, dmv, orow, eslot_hi, eid, m2, dks, twin);
+      C.launches += 2;
     }
     int* d_mx = A.alloc<int>(2, true);
     k_max_diff_i64<<<grid_for(n, B, SM), B, 0, C.st>>>(rp, n, d_mx);
@@ -1129,6 +1130,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     ptiers.light_max = env_cap("EVOKE_PAIR_LIGHT_MAX", PAIR_WARP_MAX);
     ptiers.mids_max = env_cap("EVOKE_PAIR_MIDS_MAX", PAIR_MIDS_MAX);
     ptiers.mid_max = env_cap("EVOKE_PAIR_MID_MAX", PAIR_MID_MAX);
+    ptiers.tiny_max = env_cap("EVOKE_PAIR_TINY_MAX", PAIR_TINY_MAX);
     ptiers.sweep = getenv("EVOKE_PAIR_SWEEP") ? atoi(getenv("EVOKE_PAIR_SWEEP")) : -1;
     k_pair_classify<<<warp_grid, B, 0, C.st>>>(g, pk2, pv2, si, ns, ptiers, Fp(F_T), pwest, pest, plists, tiers);
     k_shard_sum_u32<<<grid_for(n, B, SM), B, 0, C.st>>>(pk2, n, si, ns, d_work + 0);
@@ -1140,8 +1142,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     C.tick("pair_classify+sync");
     auto plist = [&](int tier) { return plists + (size_t)tier * n; };
     if (getenv("EVOKE_DEBUG"))
-      fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d small-mid %d light %d\n", ht[PT_G64],
-              ht[PT_G32], ht[PT_G32S], ht[PT_MID], ht[PT_MIDS], ht[PT_LIGHT]);
+      fprintf(stderr, "[evoke] pair tiers: g64 %d g32 %d g32s %d mid %d small-mid %d light %d tiny %d\n", ht[PT_G64],
+              ht[PT_G32], ht[PT_G32S], ht[PT_MID], ht[PT_MIDS], ht[PT_LIGHT], ht[PT_TINY]);
     // adjacency maps of the hubs (h* membership and T(h*, x) in one load), within a memory budget
     int32_t* hslot = A.alloc<int32_t>(n);
     int* hcnt = A.alloc<int>(1, true);
@@ -1268,6 +1270,18 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       }});
     } else if (mids_fn) {
       jobs.push_back({P_PAIR, 3, mids_fn});
+    }
+    if (ht[PT_TINY] > 0) {
+      int bps = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_pairs_tiny<PAIR_TINY_CAP>, PAIR_BT, 0));
+      int* counter = A.alloc<int>(1, true);
+      const int32_t* pt = plist(PT_TINY);
+      const int nt = ht[PT_TINY];
+      const int grid = std::max(bps, 1) * SM;
+      jobs.push_back({P_PAIR, 3, [=, &C](cudaStream_t st) {
+        k_pairs_tiny<PAIR_TINY_CAP><<<grid, PAIR_BT, 0, st>>>(g, Te, pt, nt, pest, counter, po);
+        C.launches++;
+      }});
     }
   }
 

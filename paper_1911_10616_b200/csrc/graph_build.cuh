@@ -357,9 +357,19 @@ __global__ void k_edge_arrays(const u64* __restrict__ dk, int64_t m2, const int6
       int64_t e = orow[w] + (pos - lo);
       eid[s] = (int32_t)e;
       eslot_hi[e] = s;
-      twin[s] = (int32_t)pos;  // the two slots of the edge point at each other
-      twin[pos] = (int32_t)s;
+      twin[s] = (int32_t)pos;  // (the other slot's twin: k_twin_hi, once eslot_hi is complete)
     }
+  }
+}
+// twin of the slots of higher neighbours: the slot of u in N(w), w > u, is eslot_hi[e(u,w)]
+// (a gather along u's out-part, coalesced, instead of a scattered write above)
+__global__ void k_twin_hi(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ dm,
+                          const int64_t* __restrict__ orow, const int64_t* __restrict__ eslot_hi,
+                          const int32_t* __restrict__ eid, int64_t m2, const u64* __restrict__ dk,
+                          int32_t* __restrict__ twin) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2; s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = (int32_t)(dk[s] >> 32);
+    if (s >= rp[u] + dm[u]) twin[s] = (int32_t)eslot_hi[eid[s]];
   }
 }
 

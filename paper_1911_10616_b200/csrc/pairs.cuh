@@ -69,6 +69,11 @@ __device__ __forceinline__ int64_t slot_of_hi_in_lo(const DGraph& g, int32_t e) 
 #define PAIR_MIDS_MAX 2048       // small-mid tier: est <= this
 #define PAIR_WARP_CAP 1024       // light tier: per-warp packed hash entries (8 warps x 8 KB)
 #define PAIR_WARP_MAX 512        // light tier: est <= this
+#define PAIR_TINY_CAP 256        // tiny tier (k_pairs_tiny): per-warp packed hash entries ...
+#define PAIR_TINY_MAX 128        // ... for est <= this (load <= 0.5)
+#ifndef PAIR_TINY_MINB
+#define PAIR_TINY_MINB 4         // resident CTAs per SM the tiny kernel's register budget must allow
+#endif
 #define PAIR_HBT 1024            // heavy tier CTA
 #define PAIR_HOT_BYTES (192 << 10)  // heavy tier: shared table entries of the top ranks (hot x)
 
@@ -1061,7 +1066,10 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
 
 // Mid and light tiers: persistent CTAs take mid sources (one CTA each, packed shared
 // hash) from mid[0, n_mid), then each warp takes light sources from light[0, n_light).
-__global__ void __launch_bounds__(PAIR_BT, 3) k_pairs_main(DGraph g, const u32* __restrict__ Te,
+#ifndef PAIR_MAIN_MINB
+#define PAIR_MAIN_MINB 3  // resident CTAs per SM the register budget must allow (shared memory allows 3)
+#endif
+__global__ void __launch_bounds__(PAIR_BT, PAIR_MAIN_MINB) k_pairs_main(DGraph g, const u32* __restrict__ Te,
                                                         const int32_t* __restrict__ mid, int n_mid,
                                                         const int32_t* __restrict__ light, int n_light,
                                                         const u32* __restrict__ est, int* __restrict__ counters,
@@ -1108,6 +1116,40 @@ __global__ void __launch_bounds__(PAIR_BT, 3) k_pairs_main(DGraph g, const u32* 
     for (int q = idx; q < end; q++) {
       const int32_t u = light[q];
       const u32 cap = pow2_at_least(2u * est[u], 32u);
+      pair_source_warp(g, Te, u, cap, tab, o, acc);
+    }
+  }
+}
+
+// Tiny tier (est <= PAIR_TINY_MAX): the light tier's warp per source with a per-warp hash of
+// PAIR_TINY_CAP entries (2 KB instead of 8 KB) in a kernel of its own, so the shared memory
+// and a smaller register budget let PAIR_TINY_MINB CTAs share an SM (the main kernel's mid
+// tier holds it to three)
+template <int WCAP>
+__global__ void __launch_bounds__(PAIR_BT, PAIR_TINY_MINB) k_pairs_tiny(DGraph g, const u32* __restrict__ Te,
+                                                                       const int32_t* __restrict__ light, int n_light,
+                                                                       const u32* __restrict__ est,
+                                                                       int* __restrict__ counter, PairOut o_) {
+  __shared__ int32_t sh_tiny[PAIR_BT / 32][2 * WCAP];
+  __shared__ u64 sh_acc[PAIR_BT / 32][32];
+  const PairOut& o = o_;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  SharedPackedHash tab;
+  tab.keys = sh_tiny[wib];
+  tab.val = (u32*)(tab.keys + WCAP);
+  for (int h = lane; h < WCAP; h += 32) { tab.keys[h] = EMPTY_KEY; tab.val[h] = 0u; }
+  u64* acc = sh_acc[wib];
+  acc[lane] = 0;
+  __syncwarp();
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 2);
+    idx = __shfl_sync(FULL_MASK, idx, 0);
+    if (idx >= n_light) break;
+    const int end = min(idx + 2, n_light);
+    for (int q = idx; q < end; q++) {
+      const int32_t u = light[q];
+      const u32 cap = pow2_at_least(2u * est[u], 32u);  // <= WCAP (est <= PAIR_TINY_MAX)
       pair_source_warp(g, Te, u, cap, tab, o, acc);
     }
   }
@@ -1242,12 +1284,13 @@ __global__ void k_pair_est(DGraph g, const u64* __restrict__ dwork, u32* __restr
 
 // Shard filter of the est-sorted (descending) vertex list and tier classification.
 // Lists keep the descending order approximately (warp-aggregated appends in list order).
-enum { PT_G64 = 0, PT_G32, PT_G32S, PT_MID, PT_LIGHT, PT_MIDS, PT_COUNT };
+enum { PT_G64 = 0, PT_G32, PT_G32S, PT_MID, PT_LIGHT, PT_MIDS, PT_TINY, PT_COUNT };
 // tier limits: the defaults are the capacities of each tier's tables; tests lower them (env
 // EVOKE_PAIR_*) to force sources onto the heavier tiers' code paths on small graphs
 struct PairTiers {
   u64 packed_lim;  // d(u) and T(u) below this: packed 16-bit W | D (<= 65536)
   u64 light_max, mids_max, mid_max;  // <= PAIR_WARP_MAX, PAIR_MIDS_MAX, PAIR_MID_MAX
+  u64 tiny_max;                       // <= PAIR_TINY_MAX (light sources this small: the tiny tier)
   int sweep;       // -1: by size (2-hop set >= n/16), 0: never, 1: always sweep the table
 };
 __global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const int32_t* __restrict__ svals,
@@ -1269,6 +1312,7 @@ __global__ void k_pair_classify(DGraph g, const u32* __restrict__ skeys, const i
         const bool packed_ok = (u64)dg_deg(g, u) < pt.packed_lim && Tv[u] < pt.packed_lim;
         const bool sweep = pt.sweep < 0 ? ew * 16 >= (u64)g.n : pt.sweep > 0;
         tier = !packed_ok ? PT_G64
+             : (e <= pt.tiny_max && ew <= PAIR_TINY_MAX) ? PT_TINY
              : e <= pt.light_max ? PT_LIGHT
              : e <= pt.mids_max ? PT_MIDS
              : e <= pt.mid_max ? PT_MID

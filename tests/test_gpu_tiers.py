@@ -24,6 +24,7 @@ COMBOS = {
     "pair_dense_swept": dict(HEAVY_PAIR, EVOKE_PAIR_SWEEP="1"),        # k_pairs_heavy<u32, true>
     "pair_mid": {"EVOKE_PAIR_LIGHT_MAX": "0", "EVOKE_PAIR_MIDS_MAX": "0"},  # k_pairs_main CTA tier
     "pair_small_mid": {"EVOKE_PAIR_LIGHT_MAX": "0"},                  # k_pairs_mids
+    "pair_light_no_tiny": {"EVOKE_PAIR_TINY_MAX": "0"},                # light sources all in k_pairs_main
     "pair_dense_hot_partial": dict(HEAVY_PAIR, EVOKE_PAIR_HOT="16"),   # heavy tables, top 16 ranks shared
     "pair_dense_nohot": dict(HEAVY_PAIR, EVOKE_PAIR_HOT="0"),
     "hub_warp": {"EVOKE_HUB_MICRO_MAX": "0"},                         # hub_item_warp (no micro items)
