@@ -891,8 +891,14 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   const int tri_grid = grid_for((int64_t)n * 32, tri_block, SM);
   int32_t *tc = nullptr, *tab = nullptr, *tac = nullptr, *tbc = nullptr;
   if (m > 0) {
-    k_triangles<0><<<tri_grid, tri_block, tri_smem, C.st>>>(g, tri_smem_per_warp, Thigh, Tmid, Tlow, Te,
-                                                           Fp(F_T), E7, nullptr, nullptr, nullptr, nullptr);
+    // out-lists of at most 32: the (b, c) pairs of a vertex flattened over the lanes
+    const bool tri_flat = max_out <= 32 && !getenv("EVOKE_TRI_NO_FLAT");  // (env: tests / A/B)
+    if (tri_flat)
+      k_triangles_flat<0><<<tri_grid, tri_block, 0, C.st>>>(g, Thigh, Tmid, Tlow, Te, Fp(F_T), E7, nullptr, nullptr,
+                                                            nullptr, nullptr);
+    else
+      k_triangles<0><<<tri_grid, tri_block, tri_smem, C.st>>>(g, tri_smem_per_warp, Thigh, Tmid, Tlow, Te,
+                                                             Fp(F_T), E7, nullptr, nullptr, nullptr, nullptr);
     int64_t* th64 = A.alloc<int64_t>(m);
     k_u32_to_i64<<<grid_for(m, B, SM), B, 0, C.st>>>(Thigh, m, th64);
     k_set_i64<<<1, 1, 0, C.st>>>(toff, 0);
@@ -905,8 +911,11 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     tac = A.alloc<int32_t>(ntri + 1);
     tbc = A.alloc<int32_t>(ntri + 1);
     g.toff = toff; g.ntri = ntri; g.tc = tc; g.tab = tab; g.tac = tac; g.tbc = tbc;
-    k_triangles<1><<<tri_grid, tri_block, tri_smem, C.st>>>(g, tri_smem_per_warp, Thigh, Tmid, Tlow, Te,
-                                                           Fp(F_T), E7, tc, tab, tac, tbc);
+    if (tri_flat)
+      k_triangles_flat<1><<<tri_grid, tri_block, 0, C.st>>>(g, Thigh, Tmid, Tlow, Te, Fp(F_T), E7, tc, tab, tac, tbc);
+    else
+      k_triangles<1><<<tri_grid, tri_block, tri_smem, C.st>>>(g, tri_smem_per_warp, Thigh, Tmid, Tlow, Te,
+                                                             Fp(F_T), E7, tc, tab, tac, tbc);
     C.launches++;
   } else {
     CK(cudaMemsetAsync(toff, 0, sizeof(int64_t) * (m + 1), C.st));
@@ -1065,13 +1074,15 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   EdgeVals ev{Te, E9f, E9b, K4e, C4e, E7, K4t};
   const int warp_grid = grid_for((int64_t)n * 32, B, SM);
   int32_t* nbr_heavy = A.alloc<int32_t>(std::max(n, 1));
-  int* nbr_nh = A.alloc<int>(4, true);
-  auto gather_on = [&](cudaStream_t gs, auto kw, auto kh, int slot) {
-    kw<<<warp_grid, B, 0, gs>>>(g, ev, F, nbr_heavy + 0, nbr_nh + slot);
+  int32_t* nbr_mid = A.alloc<int32_t>(std::max(n, 1));
+  int* nbr_nh = A.alloc<int>(8, true);  // [slot] heavy, [4 + slot] mid counts of gather `slot`
+  const int group_grid = grid_for(((int64_t)n + 3) / 4 * 32, B, SM);
+  auto gather_on = [&](cudaStream_t gs, auto kw, auto km, auto kh, int slot) {
+    kw<<<group_grid, B, 0, gs>>>(g, ev, F, nbr_heavy, nbr_nh + slot, nbr_mid, nbr_nh + 4 + slot);
+    km<<<4 * SM, B, 0, gs>>>(g, ev, F, nbr_mid, nbr_nh + 4 + slot);
     kh<<<SM, 1024, 0, gs>>>(g, ev, F, nbr_heavy, nbr_nh + slot);
-    C.launches += 2;
+    C.launches += 3;
   };
-  auto gather = [&](auto kw, auto kh, int slot) { gather_on(C.st, kw, kh, slot); };
   const bool serial_flag = (o.flags & EVOKE_FLAG_SERIAL) != 0;
   cudaStream_t pre = C.st;
   if (!serial_flag && n > 0 && !getenv("EVOKE_NO_SIDE")) {  // (EVOKE_NO_SIDE: developer A/B)
@@ -1085,7 +1096,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   if (C.side_used) CK(cudaEventRecord(C.sev[1], pre));
   // ------------------------------------------------------------------ nbr gather 1
   C.mark(P_NBR1);
-  if (n > 0) gather_on(pre, k_nbr<1>, k_nbr_heavy<1>, 0);
+  if (n > 0) gather_on(pre, k_nbr<1>, k_nbr_mid<1>, k_nbr_heavy<1>, 0);
   if (C.side_used) {
     CK(cudaEventRecord(C.sev[2], pre));
     CK(cudaEventRecord(C.ev_side, pre));
@@ -1626,8 +1637,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       ev.EV = EVrows;
     }
     if (n > 0) {
-      gather_on(gs, k_nbr<2>, k_nbr_heavy<2>, 1);
-      if (!four) gather_on(gs, k_nbr<3>, k_nbr_heavy<3>, 2);
+      gather_on(gs, k_nbr<2>, k_nbr_mid<2>, k_nbr_heavy<2>, 1);
+      if (!four) gather_on(gs, k_nbr<3>, k_nbr_mid<3>, k_nbr_heavy<3>, 2);
     }
   };
   auto trigather = [&](cudaStream_t gs) {

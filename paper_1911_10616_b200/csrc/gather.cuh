@@ -199,21 +199,53 @@ struct NbrK<3> {
   }
 };
 
-// warp per vertex of degree <= NBR_HEAVY; heavier vertices go to `heavy` (count *nheavy)
+// Vertices of degree <= NBR_SMALL: eight lanes each (four vertices per warp; a warp per
+// vertex left half the lanes idle at mean degree 16 and spent 70 shuffles on its 14 sums);
+// degree <= NBR_HEAVY: appended to `mid` (a warp each, k_nbr_mid); heavier: to `heavy` (a CTA
+// each).  Counts *nmid, *nheavy.
+#define NBR_SMALL 64
 template <int K>
 __global__ void k_nbr(DGraph g, EdgeVals ev, u64* __restrict__ F, int32_t* __restrict__ heavy,
-                      int* __restrict__ nheavy) {
+                      int* __restrict__ nheavy, int32_t* __restrict__ mid, int* __restrict__ nmid) {
+  constexpr int NS = NbrK<K>::NS;
+  const int32_t n = g.n;
+  const int lane = threadIdx.x & 31, sub = lane & 7;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = gw * 4; base < n; base += nw * 4) {  // warp-uniform
+    const int64_t uq = base + (lane >> 3);
+    const int32_t u = (int32_t)min(uq, (int64_t)n - 1);
+    const int d = uq < n ? dg_deg(g, u) : 0;
+    u64 a[NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) a[i] = 0;
+    if (uq < n && d <= NBR_SMALL) NbrK<K>::acc(g, ev, F, n, u, sub, 8, a);
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+      a[i] += __shfl_xor_sync(FULL_MASK, a[i], 4);
+      a[i] += __shfl_xor_sync(FULL_MASK, a[i], 2);
+      a[i] += __shfl_xor_sync(FULL_MASK, a[i], 1);
+    }
+    if (uq < n && sub == 0) {
+      if (d <= NBR_SMALL) NbrK<K>::store(g, F, n, u, a);
+      else if (d <= NBR_HEAVY) mid[atomicAdd(nmid, 1)] = u;
+      else heavy[atomicAdd(nheavy, 1)] = u;
+    }
+  }
+}
+
+// a warp per vertex of the mid list
+template <int K>
+__global__ void k_nbr_mid(DGraph g, EdgeVals ev, u64* __restrict__ F, const int32_t* __restrict__ mid,
+                          const int* __restrict__ nmid) {
   constexpr int NS = NbrK<K>::NS;
   const int32_t n = g.n;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u64i = gw; u64i < n; u64i += nw) {
-    const int32_t u = (int32_t)u64i;
-    if (dg_deg(g, u) > NBR_HEAVY) {
-      if (lane == 0) heavy[atomicAdd(nheavy, 1)] = u;
-      continue;
-    }
+  const int cnt = *nmid;
+  for (int64_t q = gw; q < cnt; q += nw) {
+    const int32_t u = mid[q];
     u64 a[NS];
 #pragma unroll
     for (int i = 0; i < NS; i++) a[i] = 0;

@@ -163,18 +163,32 @@ __global__ void __launch_bounds__(PEEL_BT) k_peel(int32_t n, const int64_t* __re
     if (tid == 0) ctl->cnt[c2] = 0;
     const int32_t* L = lists(p);
     int32_t* Ln = lists(p ^ 1);
-    for (int i = warp; i < cur; i += nwarps) {
-      const int32_t v = L[i];
-      for (int64_t s = rp[v] + lane; s < rp[v + 1]; s += 32) {
-        // no stamp test first: a stamped vertex had degree <= k when stamped and k only
-        // grows, so its decrement can never return k + 1 (one dependent load less per round)
-        const int32_t w = adj[s];
-        const int old = atomicSub(&deg[w], 1);
-        if (old == k + 1) {
-          rnd[w] = round + 1;
-          Ln[atomicAdd(&ctl->cnt[c1], 1)] = w;
-        }
+    // `per` frontier vertices per warp step (up to 32, as many as keep every warp busy), their
+    // (vertex, neighbour) pairs flattened over the lanes: a warp per vertex left most lanes
+    // idle on the large degree-8 frontiers of config 4's first rounds, while a small frontier
+    // needs a warp per vertex to spread its lists
+    const int per = max(1, min(32, cur / nwarps));
+    for (int i0 = warp * per; i0 < cur; i0 += nwarps * per) {
+      int64_t b0 = 0;
+      int len = 0;
+      if (lane < per && i0 + lane < cur) {
+        const int32_t v = L[i0 + lane];
+        b0 = rp[v];
+        len = (int)(rp[v + 1] - b0);
       }
+      warp_flat(len, [&](int j, int kk, bool valid) {
+        const int64_t bj = __shfl_sync(FULL_MASK, b0, j);
+        bool hit = false;
+        int32_t w = 0;
+        if (valid) {
+          // no stamp test first: a stamped vertex had degree <= k when stamped and k only
+          // grows, so its decrement can never return k + 1 (one dependent load less per round)
+          w = adj[bj + kk];
+          hit = atomicSub(&deg[w], 1) == k + 1;
+          if (hit) rnd[w] = round + 1;
+        }
+        warp_append(hit, w, Ln, &ctl->cnt[c1]);
+      });
     }
     removed += cur;
     round++;

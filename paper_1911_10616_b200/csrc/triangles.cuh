@@ -91,6 +91,98 @@ __global__ void __launch_bounds__(256) k_triangles(
   }
 }
 
+// Graphs whose out-lists are all short (max d+ <= 32): the same pass with the (b, c) pairs
+// of a vertex flattened over the lanes (warp_flat over the items b in N+(a)), so a warp does
+// not walk N+(a) one b at a time with most lanes idle (config 4: d+ <= 8).  The lanes of one
+// item are consecutive, so a found c's rank inside its list is the item's count so far
+// (per-warp shared) plus the found lanes below it among the item's lanes (match_any mask);
+// the lists stay sorted by c.
+template <int PASS>
+__global__ void __launch_bounds__(256) k_triangles_flat(
+    DGraph g, u32* __restrict__ Thigh, u32* __restrict__ Tmid, u32* __restrict__ Tlow, u32* __restrict__ Te,
+    u64* __restrict__ Tv, u64* __restrict__ E7, int32_t* __restrict__ tc, int32_t* __restrict__ tab,
+    int32_t* __restrict__ tac, int32_t* __restrict__ tbc) {
+  __shared__ int32_t sh_L[8][32];
+  __shared__ u32 sh_cnt[8][32];
+  __shared__ u64 sh_e7[8][32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int32_t* La = sh_L[wib];
+  u32* cnt = sh_cnt[wib];
+  u64* e7 = sh_e7[wib];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a64 = gw; a64 < g.n; a64 += nw) {
+    const int32_t a = (int32_t)a64;
+    const int64_t oa = g.orow[a];
+    const int32_t da = (int32_t)(g.orow[a + 1] - oa);  // <= 32
+    if (da < 2) continue;
+    const int32_t dga = dg_deg(g, a);
+    // item lane i < da - 1: b = N+(a)[i], its out-list
+    int32_t b = 0, db = 0, dgb = 0;
+    int64_t ob = 0, base = 0;
+    if (lane < da) {
+      b = g.ocol[oa + lane];
+      La[lane] = b;
+    }
+    if (lane < da - 1) {
+      ob = g.orow[b];
+      db = (int32_t)(g.orow[b + 1] - ob);
+      dgb = dg_deg(g, b);
+      if (PASS == 1) base = g.toff[oa + lane];
+    }
+    cnt[lane] = 0u;
+    if (PASS == 1) e7[lane] = 0ull;
+    __syncwarp();
+    warp_flat(db, [&](int j, int k, bool valid) {
+      const int64_t obj = __shfl_sync(FULL_MASK, ob, j);
+      const int64_t basej = __shfl_sync(FULL_MASK, base, j);
+      const int32_t dgbj = __shfl_sync(FULL_MASK, dgb, j);
+      bool found = false;
+      int32_t c = 0;
+      int64_t pos = 0;
+      if (valid) {
+        c = g.ocol[obj + k];
+        pos = lower_bound_dev<int32_t>(La, j + 1, da, c);
+        found = pos < da && La[pos] == c;
+      }
+      const unsigned same = __match_any_sync(FULL_MASK, valid ? j : -1);
+      const unsigned bal = __ballot_sync(FULL_MASK, found) & same;
+      const u32 before = cnt[j];  // (every lane of the group reads it before the leader adds)
+      __syncwarp();
+      if (valid && lane == __ffs(same) - 1) cnt[j] = before + __popc(bal);
+      if (PASS == 1 && found) {
+        const int64_t q = basej + before + __popc(bal & ((1u << lane) - 1u));
+        const int32_t eac = (int32_t)(oa + pos), ebc = (int32_t)(obj + k);
+        tc[q] = c; tab[q] = (int32_t)(oa + j); tac[q] = eac; tbc[q] = ebc;
+        atomicAdd(&Tv[c], 1ull);
+        atomicAdd(&Te[eac], 1u);
+        atomicAdd(&Te[ebc], 1u);
+        atomicAdd(&Tmid[eac], 1u);
+        atomicAdd(&Tlow[ebc], 1u);
+        atomicAdd(&e7[j], (u64)(dg_deg(g, c) - 2));
+        atomicAdd(&E7[eac], (u64)(dgbj - 2));
+        atomicAdd(&E7[ebc], (u64)(dga - 2));
+      }
+      __syncwarp();
+    });
+    __syncwarp();
+    const u32 cb = lane < da - 1 ? cnt[lane] : 0u;
+    if (PASS == 0) {
+      if (lane < da - 1) Thigh[oa + lane] = cb;
+    } else {
+      if (cb) {
+        atomicAdd(&Te[oa + lane], cb);
+        atomicAdd(&Tv[b], (u64)cb);
+        atomicAdd(&E7[oa + lane], e7[lane]);
+      }
+      const u64 ta = warp_sum((u64)cb);
+      if (lane == 0 && ta) atomicAdd(&Tv[a], ta);
+    }
+    __syncwarp();
+  }
+}
+
 // Thread per oriented triangle entry q (a<b<c): E9 for the six ordered edges
 // (E9<x,y> = sum over triangles (x,y,z) of E1(x,z)-1), DM12 for the three
 // vertices (sum over triangles (u,v,x) of T(v,x)-1), and the full per-edge

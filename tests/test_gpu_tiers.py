@@ -44,6 +44,7 @@ COMBOS = {
     "c5_big_hot": dict(C5_BIG, EVOKE_C5_HOT_MIN_W="0"),              # hot-vertex cache of every rank
     "c5_big_hot_partial": dict(C5_BIG, EVOKE_C5_HOT_MIN_W="0", EVOKE_C5_HOT="16"),  # of the top 16 ranks
     "c5_light_by_work": {"EVOKE_C5_LIGHT_WORK": "40", "EVOKE_C5_MID_WORK": "200"},
+    "tri_not_flat": {"EVOKE_TRI_NO_FLAT": "1"},                       # k_triangles (warp walks N+(a) item by item)
     "c5_giant": {"EVOKE_C5_GIANT_W": "300"},                          # k_c5_giant (whole-GPU endpoints)
     "c5_giant_all": {"EVOKE_C5_GIANT_W": "1"},                        # every endpoint a giant
     "all_heavy_sorted": dict(HEAVY_PAIR, **C5_BIG, EVOKE_PAIR_PACKED_LIM="0", EVOKE_HUB_WARP_MAX="0",
