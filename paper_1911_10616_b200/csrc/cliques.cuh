@@ -237,6 +237,80 @@ __global__ void __launch_bounds__(256) k_cliques(
   }
 }
 
+// The rows of a one-word bitmap (k <= 32) with the (i, j) pairs, j in S_i, flattened over the
+// lanes (warp_flat over the rows; __fns finds the pair's column): the same per-pair work as
+// clique_row, but a warp no longer walks the k rows one after the other with only the k
+// lanes of a row busy (config 4: k <= 8).  Per-row sums go to the warp's shared acc0/acc1
+// [32] (MODE 0; flushed here), u's own sums to acc_u0/acc_u1 (per lane).
+template <int MODE>
+__device__ __forceinline__ void clique_pairs_w1(const DGraph& g, const u32* S, int k, int64_t ou, int lane,
+                                                bool do_k4, bool do_k5, const u32* __restrict__ Te,
+                                                u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
+                                                u64* __restrict__ K5v, u64* acc0, u64* acc1, u64& acc_u0,
+                                                u64& acc_u1) {
+  const u32 Sl_own = lane < k ? S[lane] : 0u;
+  const int len = __popc(Sl_own);
+  const int64_t qi0_own = lane < k ? g.toff[ou + lane] : 0;
+  if (MODE == 0) { acc0[lane] = 0; acc1[lane] = 0; }
+  __syncwarp();
+  warp_flat(len, [&](int i, int kk, bool valid) {
+    const u32 Si = __shfl_sync(FULL_MASK, Sl_own, i);
+    const int64_t qi0 = __shfl_sync(FULL_MASK, qi0_own, i);
+    if (!valid) return;
+    const int j = __fns(Si, 0, kk + 1);  // the kk-th column of row i
+    const u32 Sj = S[j];
+    const u32 gtj = j == 31 ? 0u : (FULL_MASK << (j + 1));
+    const u32 x = Si & Sj & gtj;  // local triangles (i, j, l), l > j
+    if (MODE == 0) {
+      if (do_k4 && x) atomicAdd(&acc0[i], (u64)__popc(x));
+      if (do_k5) {
+        u64 c5 = 0;
+        for_each_bit(x, 0, [&](int l) {
+          const u32 gtl = l == 31 ? 0u : (FULL_MASK << (l + 1));
+          c5 += __popc(Si & Sj & S[l] & gtl);
+        });
+        if (c5) atomicAdd(&acc1[i], c5);
+      }
+    }
+    if (j > i && (MODE == 1 || do_k4)) {
+      const u32 c = __popc(Si & Sj);
+      const u32 gti = i == 31 ? 0u : (FULL_MASK << (i + 1));
+      const int64_t qij = qi0 + __popc(Si & gti & ((1u << j) - 1u));
+      const int32_t eij = g.tbc[qij];
+      if (MODE == 0) {
+        if (c) {
+          atomicAdd(&K4e[eij], (u64)c);
+          atomicAdd(&K4t[qij], c);
+        }
+      } else {
+        acc_u0 += (u64)Te[eij] * (u64)c;
+      }
+      int64_t lo = g.toff[eij];
+      const int64_t hi = g.toff[eij + 1];
+      for_each_bit(x, 0, [&](int l) {
+        const int32_t Ll = g.ocol[ou + l];
+        const int64_t pos = lower_bound_dev<int32_t>(g.tc, lo, hi, Ll);
+        if (MODE == 0) atomicAdd(&K4t[pos], 1u);
+        else acc_u1 += (u64)K4t[pos] - 1ull;
+        lo = pos + 1;
+      });
+    }
+  });
+  __syncwarp();
+  if (MODE == 0 && lane < k) {
+    const u64 a0 = acc0[lane], a1 = acc1[lane];
+    const int32_t Li = g.ocol[ou + lane];
+    if (do_k4 && a0) {
+      atomicAdd(&K4v[Li], a0);
+      atomicAdd(&K4e[ou + lane], a0);
+    }
+    if (do_k5 && a1) atomicAdd(&K5v[Li], a1);
+    acc_u0 += a0;
+    acc_u1 += a1;
+  }
+  __syncwarp();
+}
+
 // Units with k = d+(u) <= 32 (one bitmap word per row): one WARP per unit instead of a CTA,
 // the rows in a per-warp 32-word slice of shared memory (most units of a sparse graph:
 // config 4 has degeneracy 8, so every unit is this small and a CTA per unit spent its time
@@ -247,10 +321,10 @@ __global__ void __launch_bounds__(256) k_cliques_warp(
     const u32* __restrict__ Te, u32* __restrict__ K4t, u64* __restrict__ K4v, u64* __restrict__ K4e,
     u64* __restrict__ K5v, u64* __restrict__ R66, u64* __restrict__ R70) {
   __shared__ u32 sh_rows[8][32];
-  __shared__ u64 sh_acc[MODE == 1 ? 8 : 1][64];  // MODE 1: theta66 / theta70 accumulators per warp
+  __shared__ u64 sh_acc[8][64];  // per warp: theta66 / theta70 (MODE 1) or per-row K4 / K5 sums (MODE 0)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   u32* S = sh_rows[wib & 7];
-  u64* acc66 = sh_acc[MODE == 1 ? (wib & 7) : 0];
+  u64* acc66 = sh_acc[wib & 7];
   u64* acc70 = acc66 + 32;
   if (MODE == 1) { acc66[lane] = 0; acc70[lane] = 0; }
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -285,9 +359,7 @@ __global__ void __launch_bounds__(256) k_cliques_warp(
       }
       __syncwarp();
     }
-    for (int i = 0; i < k; i++)
-      clique_row<MODE>(g, S, 1, k, ou, i, lane, do_k4, do_k5, MODE != 1, Te, K4t, K4v, K4e, K5v, R66, R70, acc_u0,
-                       acc_u1);
+    clique_pairs_w1<MODE>(g, S, k, ou, lane, do_k4, do_k5, Te, K4t, K4v, K4e, K5v, acc66, acc70, acc_u0, acc_u1);
     acc_u0 = warp_sum(acc_u0);
     acc_u1 = warp_sum(acc_u1);
     if (lane == 0) {

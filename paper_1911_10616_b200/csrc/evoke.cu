@@ -1717,8 +1717,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   u64* dout = nullptr;
   if (n > 0) {
     dout = A.alloc<u64>((size_t)n * 73);  // staged: `out` is written only after every check passed
-    k_combine<<<grid_for(n, 128, SM), 128, 0, C.st>>>(g, F, perm, o.induced, si == 0 ? 1 : 0, four ? 15 : 73,
-                                                       dout);
+    const size_t csm = (size_t)COMBINE_BT * EVOKE_NUM_ORBITS_DEV * sizeof(u64);
+    CK(cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    k_combine<<<grid_for(n, COMBINE_BT, SM), COMBINE_BT, csm, C.st>>>(g, F, perm, o.induced, si == 0 ? 1 : 0,
+                                                                      four ? 15 : 73, dout);
     C.launches++;
   }
   // every check before `out` is touched: kernel faults (sync), and in the developer mode

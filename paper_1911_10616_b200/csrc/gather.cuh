@@ -444,29 +444,48 @@ __device__ void compute_dm(const DGraph& g, const u64* __restrict__ F, int32_t n
 }
 
 // ncols = 73, or 15 for the 4-vertex orbits only (the 5-vertex columns are written as 0;
-// A is block diagonal by pattern size, so DIM 0..14 needs DM 0..14 only)
-__global__ void k_combine(DGraph g, const u64* __restrict__ F, const int32_t* __restrict__ perm,
-                          int induced, int primary, int ncols, u64* __restrict__ out) {
+// A is block diagonal by pattern size, so DIM 0..14 needs DM 0..14 only).  Each thread's DM
+// row lives in shared memory (a local array indexed by the A^-1 column list spilled to local
+// memory), the transform runs in place (A^-1 is unit upper triangular: DIM_i reads DM_j, j >=
+// i, so row i may overwrite DM_i once computed), and the warp then writes its 32 output rows
+// (scattered by perm) one row at a time, consecutive lanes on consecutive words.
+#define COMBINE_BT 128
+__global__ void __launch_bounds__(COMBINE_BT) k_combine(DGraph g, const u64* __restrict__ F,
+                                                        const int32_t* __restrict__ perm, int induced, int primary,
+                                                        int ncols, u64* __restrict__ out) {
+  extern __shared__ u64 comb_sh[];  // [COMBINE_BT][73]
   const int32_t n = g.n;
-  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    u64 DM[EVOKE_NUM_ORBITS_DEV];
-    compute_dm(g, F, n, u, false, DM);
-    if (!primary) {
-      u64 DM0[EVOKE_NUM_ORBITS_DEV];
-      compute_dm(g, F, n, u, true, DM0);
-      for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) DM[i] -= DM0[i];
-    }
-    u64* row = out + (size_t)perm[u] * EVOKE_NUM_ORBITS_DEV;
-    if (!induced) {
-      for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) row[i] = i < ncols ? DM[i] : 0ull;
-    } else {
-      for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) {
-        u64 acc = 0;
-        if (i < ncols)
-          for (int p = c_ainv_rp[i]; p < c_ainv_rp[i + 1]; p++)
-            acc += (u64)c_ainv_val[p] * DM[c_ainv_col[p]];
-        row[i] = acc;
+  const int lane = threadIdx.x & 31;
+  u64* tile = comb_sh + (size_t)(threadIdx.x & ~31) * EVOKE_NUM_ORBITS_DEV;  // this warp's 32 rows
+  u64* DM = tile + (size_t)lane * EVOKE_NUM_ORBITS_DEV;
+  for (int32_t base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < n; base += gridDim.x * blockDim.x) {
+    const int32_t u = base + lane;
+    if (u < n) {
+      compute_dm(g, F, n, u, false, DM);
+      if (!primary) {
+        u64 DM0[EVOKE_NUM_ORBITS_DEV];
+        compute_dm(g, F, n, u, true, DM0);
+        for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) DM[i] -= DM0[i];
+      }
+      if (!induced) {
+        for (int i = ncols; i < EVOKE_NUM_ORBITS_DEV; i++) DM[i] = 0ull;
+      } else {
+        for (int i = 0; i < EVOKE_NUM_ORBITS_DEV; i++) {
+          u64 acc = 0;
+          if (i < ncols)
+            for (int p = c_ainv_rp[i]; p < c_ainv_rp[i + 1]; p++)
+              acc += (u64)c_ainv_val[p] * DM[c_ainv_col[p]];
+          DM[i] = acc;  // in place: rows > i read only DM_j, j > i
+        }
       }
     }
+    __syncwarp();
+    const int rows = min(32, n - base);
+    for (int r = 0; r < rows; r++) {
+      u64* dst = out + (size_t)perm[base + r] * EVOKE_NUM_ORBITS_DEV;
+      const u64* src = tile + (size_t)r * EVOKE_NUM_ORBITS_DEV;
+      for (int i = lane; i < EVOKE_NUM_ORBITS_DEV; i += 32) dst[i] = src[i];
+    }
+    __syncwarp();
   }
 }
