@@ -697,7 +697,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   u64* ukeys = A.alloc<u64>(mraw + 1);
   if (mraw > 0) {
     u64* sk = A.alloc<u64>(mraw);
-    sort_keys_u64(A, C, keys, sk, mraw, 64);
+    // keys (min << 32) | max < 2^(32 + bits(n)); the self-loop sentinel ~0 is still above every
+    // key in those bits, so it sorts last
+    sort_keys_u64(A, C, keys, sk, mraw, std::min(64, 32 + bits_for(n)));
     int64_t* d_nsel = A.alloc<int64_t>(1);
     size_t tb = 0;
     CK(cub::DeviceSelect::Unique(nullptr, tb, sk, ukeys, d_nsel, mraw, C.st));
@@ -948,7 +950,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     const size_t freeb = avail_bytes(C.dev);
     const char* sort_env = getenv("EVOKE_SORT_FULL_MIN");  // test hook: force / disable the sort
     const int64_t sort_min = sort_env ? atoll(sort_env) : EVOKE_SORT_FULL_MIN;
-    if (N3 >= sort_min && (size_t)N3 * 40 < freeb / 2) {
+    // (and only when the lists are long on average: 3 #T >= 8 m; config 4's 1.4 entries per
+    // list gained nothing from the 1.6 ms sort)
+    if (N3 >= sort_min && (sort_env || N3 >= 8 * m) && (size_t)N3 * 40 < freeb / 2) {
       u64* k0 = A.alloc<u64>(N3);
       u64* k1 = A.alloc<u64>(N3);
       int32_t* i0 = A.alloc<int32_t>(N3);
