@@ -774,7 +774,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     if (!launched) {
       int bps = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel<false>, PEEL_BT, peel_smem));
-      const int pgrid = n <= peel_switch ? 1 : std::max(1, std::min(std::min(bps, 1) * SM, PEEL_GRID));
+      const char* pg_env = getenv("EVOKE_PEEL_GRID");  // developer knob: CTAs of the grid-wide phase
+      const int pg_want = pg_env ? std::max(1, atoi(pg_env)) : PEEL_GRID;
+      const int pgrid = n <= peel_switch ? 1 : std::max(1, std::min(std::max(bps, 1) * SM, pg_want));
       CK(cudaLaunchCooperativeKernel((void*)k_peel<false>, pgrid, PEEL_BT, args, peel_smem, C.st));
     }
     C.launches++;
@@ -1518,7 +1520,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       });
     }
     const char* hg_env = getenv("EVOKE_C5_HG");  // developer knob: big-endpoint CTAs
-    const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : SM;
+    // (passes running alone: two big-endpoint CTAs per SM when registers and shared memory
+    // allow -- 64 warps hide more of the records' L2/DRAM round trips: config 4 47.9 -> 46.2 ms)
+    const int64_t hg_want = hg_env ? std::max(1, atoi(hg_env)) : (whole_gpu_passes ? 2 * SM : SM);
     if (n5b > 0) {
       int32_t* bs = nullptr;
       const u64 wmax = sort_big(n5b, bs);
@@ -1528,13 +1532,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       const int64_t per = (int64_t)n * (int64_t)(rec + 8);
       // (whole-GPU passes run alone: half the free estimate; concurrent: a quarter)
       const int64_t budget = (int64_t)(whole_gpu_passes ? freeb / 2 : freeb / 4);
-      const int hg = (int)std::min<int64_t>(std::min<int64_t>(hg_want, n5b), std::max<int64_t>(1, budget / per));
-      if (getenv("EVOKE_DEBUG"))
-        fprintf(stderr, "[evoke] c5 big: %d endpoints, W max %llu, %d CTAs (%s records, free estimate %.1f GB)\n",
-                n5b, (unsigned long long)wmax, hg, narrow ? "u32" : "u64", freeb / 1e9);
-      char* dense = A.zalloc<char>((size_t)hg * n * rec);
-      int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
-      int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
+      const int hg0 = (int)std::min<int64_t>(std::min<int64_t>(hg_want, n5b), std::max<int64_t>(1, budget / per));
       // first-touch bitmaps (present, j-key) in shared memory when they fit
       const size_t bits_smem = (size_t)2 * ((n + 31) / 32) * sizeof(u32);
       const int use_bits = bits_smem <= C5_BITS_SMEM_MAX && !getenv("EVOKE_C5_NO_BITS") ? 1 : 0;
@@ -1549,6 +1547,16 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
         CK(cudaFuncSetAttribute(k_c5_heavy<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
         CK(cudaFuncSetAttribute(k_c5_heavy<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
       }
+      int hbps = 0;  // resident big-endpoint CTAs per SM: the grid never exceeds what is co-resident
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hbps, narrow ? (const void*)k_c5_heavy<u32>
+                                                                     : (const void*)k_c5_heavy<u64>, C5_HBT, bsm));
+      const int hg = std::min(hg0, std::max(1, hbps) * SM);
+      if (getenv("EVOKE_DEBUG"))
+        fprintf(stderr, "[evoke] c5 big: %d endpoints, W max %llu, %d CTAs (%s records, free estimate %.1f GB)\n",
+                n5b, (unsigned long long)wmax, hg, narrow ? "u32" : "u64", freeb / 1e9);
+      char* dense = A.zalloc<char>((size_t)hg * n * rec);
+      int32_t* dl = A.alloc<int32_t>((size_t)hg * 2 * n);
+      int32_t* lq = A.alloc<int32_t>((size_t)hg * (2 * (size_t)g.max_deg + 1));
       c5chain.push_back([=, &C](cudaStream_t st) {
         if (narrow)
           k_c5_heavy<u32><<<hg, C5_HBT, bsm, st>>>(g, Tlow, Tmid, Thigh, bs, n5b, c5c + 6,
