@@ -751,7 +751,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
                     (void*)&l1, (void*)&lidmap, (void*)&loc, (void*)&lcnt, (void*)&ladj, (void*)&ctl,
                     (void*)&peel_switch};
     // graphs up to PEEL_CLUSTER_MAXN vertices: one 16-CTA cluster with hardware cluster
-    // barriers between rounds; larger: a cooperative grid (PEEL_GRID CTAs)
+    // barriers between rounds; larger: a cooperative grid (one CTA per SM)
     bool launched = false;
     if (n <= PEEL_CLUSTER_MAXN && n > peel_switch) {
       if (cudaFuncSetAttribute(k_peel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
@@ -775,7 +775,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       int bps = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_peel<false>, PEEL_BT, peel_smem));
       const char* pg_env = getenv("EVOKE_PEEL_GRID");  // developer knob: CTAs of the grid-wide phase
-      const int pg_want = pg_env ? std::max(1, atoi(pg_env)) : PEEL_GRID;
+      // (every SM: config 4's first rounds are large -- 3.53 ms at 64 CTAs, 3.17 ms at 148; the
+      // grid barrier of the small rounds costs no more at 148: config 3 6.26 vs 6.25 ms)
+      const int pg_want = pg_env ? std::max(1, atoi(pg_env)) : SM;
       const int pgrid = n <= peel_switch ? 1 : std::max(1, std::min(std::max(bps, 1) * SM, pg_want));
       CK(cudaLaunchCooperativeKernel((void*)k_peel<false>, pgrid, PEEL_BT, args, peel_smem, C.st));
     }
@@ -938,7 +940,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     inclusive_sum(A, C, te64, foff + 1, m);
     A.release(te64);
     int64_t* fcur = A.alloc<int64_t>(m + 1);
-    CK(cudaMemcpyAsync(fcur, foff, sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, C.st));
+    k_fcur_init<<<grid_for(m, B, SM), B, 0, C.st>>>(m, foff, Thigh, fcur);
     fx = A.alloc<int32_t>(3 * ntri);
     fe1 = A.alloc<int32_t>(3 * ntri);
     fe2 = A.alloc<int32_t>(3 * ntri);

@@ -83,7 +83,6 @@ struct PeelCtl {
 
 #define PEEL_BT 1024           // threads per CTA
 #define PEEL_SWITCH 8192       // vertices left at or below which one CTA finishes the peel locally
-#define PEEL_GRID 64           // CTAs of the grid-wide phase (cheaper grid barriers; rounds are small)
 #define PEEL_CLUSTER 16        // CTAs of the cluster variant (non-portable cluster size)
 #define PEEL_CLUSTER_MAXN (1 << 18)  // graphs up to this many vertices use the cluster variant
 // shared bytes per local vertex of phase 2: ldeg, lrnd (int32), lbeg (u32), lcnt, two frontier

@@ -85,10 +85,7 @@ __global__ void k_hub_bin(DGraph g, const u32* __restrict__ Te, const u64* __res
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = base + lane;
     u64 e = 0;
-    if (s < m2) {
-      const int32_t eva = g.eid[s];
-      if (Te[eva] >= 2 && (!mine || mine[s])) e = est[s];
-    }
+    if (s < m2 && g.tes[s] >= 2 && (!mine || mine[s])) e = est[s];  // (T(v,a) per slot: no edge-id load)
     warp_append(e > 0 && e <= micro_max, (int32_t)s, micro, n_micro);
     warp_append(e > micro_max && e <= warp_max, (int32_t)s, light, n_light);
     const bool is_heavy = e > warp_max;

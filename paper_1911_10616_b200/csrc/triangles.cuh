@@ -183,6 +183,12 @@ __global__ void __launch_bounds__(256) k_triangles_flat(
   }
 }
 
+__global__ void k_fcur_init(int64_t m, const int64_t* __restrict__ foff, const u32* __restrict__ Thigh,
+                            int64_t* __restrict__ fcur) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+    fcur[e] = foff[e] + Thigh[e];
+}
+
 // Thread per oriented triangle entry q (a<b<c): E9 for the six ordered edges
 // (E9<x,y> = sum over triangles (x,y,z) of E1(x,z)-1), DM12 for the three
 // vertices (sum over triangles (u,v,x) of T(v,x)-1), and the full per-edge
@@ -206,7 +212,9 @@ __global__ void k_tri_sweep1(DGraph g, const u32* __restrict__ Te, u64* __restri
     atomicAdd(&DM12[b], tac_ - 1);
     atomicAdd(&DM12[c], tab_ - 1);
     int64_t r;
-    r = (int64_t)atomicAdd((unsigned long long*)&fcur[eab], 1ull);
+    // the owner edge's entries come first, in oriented-list order (no atomic); the two other
+    // roles append after them (fcur starts at foff + Thigh)
+    r = g.foff[eab] + (q - g.toff[eab]);
     fx[r] = c; fe1[r] = eac; fe2[r] = ebc;
     r = (int64_t)atomicAdd((unsigned long long*)&fcur[eac], 1ull);
     fx[r] = b; fe1[r] = eab; fe2[r] = ebc;
