@@ -1159,7 +1159,11 @@ __global__ void __launch_bounds__(PAIR_BT, PAIR_TINY_MINB) k_pairs_tiny(DGraph g
 // shared hash of PAIR_MIDS_CAP entries).  Smaller CTAs than the mid tier: a source's phases
 // are latency-bound and separated by CTA barriers, so more sources in flight per SM (five
 // instead of three) hide more of the latency than more threads per source would.
-__global__ void __launch_bounds__(PAIR_MIDS_BT) k_pairs_mids(DGraph g, const u32* __restrict__ Te,
+#ifndef PAIR_MIDS_MINB
+#define PAIR_MIDS_MINB 5  // resident small-mid CTAs per SM the register budget must allow (96 registers: config 4
+                          // pair pass 40.9 -> 38.7 ms against 126 registers / 4 CTAs; 6 CTAs: 39.0 ms)
+#endif
+__global__ void __launch_bounds__(PAIR_MIDS_BT, PAIR_MIDS_MINB) k_pairs_mids(DGraph g, const u32* __restrict__ Te,
                                                              const int32_t* __restrict__ mids, int n_mids,
                                                              const u32* __restrict__ est, int* __restrict__ counter,
                                                              PairOut o_, char* __restrict__ qmem, int qcap) {
