@@ -918,7 +918,11 @@ __global__ void __launch_bounds__(C5_BT, C5_LIGHT_MINB) k_c5_light(DGraph g, con
 // 2 x R(l) slots in global memory (the region is reused endpoint after endpoint, so it stays
 // in L2).  A 1024-thread CTA per such endpoint would spend its time in barriers and dependent
 // round trips with most warps idle.
-__global__ void __launch_bounds__(C5_MBT) k_c5_mid(DGraph g, const u32* __restrict__ Tlow,
+#ifndef C5_MID_MINB
+#define C5_MID_MINB 16  // resident mid-endpoint CTAs per SM the register budget must allow (32 registers:
+                        // config 4 5-cycle pass 47.9 -> 46.2 ms against 40 registers / 12 CTAs)
+#endif
+__global__ void __launch_bounds__(C5_MBT, C5_MID_MINB) k_c5_mid(DGraph g, const u32* __restrict__ Tlow,
                                                    const u32* __restrict__ Tmid, const u32* __restrict__ Thigh,
                                                    const int32_t* __restrict__ list, const u32* __restrict__ rb,
                                                    int n_mid, int* __restrict__ counter, C5RecP* __restrict__ regions,

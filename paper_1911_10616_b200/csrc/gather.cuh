@@ -204,8 +204,12 @@ struct NbrK<3> {
 // degree <= NBR_HEAVY: appended to `mid` (a warp each, k_nbr_mid); heavier: to `heavy` (a CTA
 // each).  Counts *nmid, *nheavy.
 #define NBR_SMALL 64
+#ifndef NBR_MINB
+#define NBR_MINB 4  // resident 256-thread CTAs per SM the register budget must allow (config 4: gather 1
+                    // 1.00 -> 0.95 ms, gather 2 2.87 -> 2.78 ms; the triangle gather at 4 was slower, 2.70 vs 2.50)
+#endif
 template <int K>
-__global__ void k_nbr(DGraph g, EdgeVals ev, u64* __restrict__ F, int32_t* __restrict__ heavy,
+__global__ void __launch_bounds__(256, NBR_MINB) k_nbr(DGraph g, EdgeVals ev, u64* __restrict__ F, int32_t* __restrict__ heavy,
                       int* __restrict__ nheavy, int32_t* __restrict__ mid, int* __restrict__ nmid) {
   constexpr int NS = NbrK<K>::NS;
   const int32_t n = g.n;
@@ -326,8 +330,11 @@ __device__ __forceinline__ void tri_credit(u64* __restrict__ TG, int32_t n, int3
 }
 
 // ROWS: TG = the row accumulators (k_tg_fields copies them); else TG = F
+#ifndef TRIG_MINB
+#define TRIG_MINB 1  // (developer variant: resident 256-thread CTAs per SM for the register budget)
+#endif
 template <bool ROWS>
-__global__ void k_trigather(DGraph g, EdgeVals ev, u64* __restrict__ TG) {
+__global__ void __launch_bounds__(256, TRIG_MINB) k_trigather(DGraph g, EdgeVals ev, u64* __restrict__ TG) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.ntri;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int32_t eab = g.tab[q], eac = g.tac[q], ebc = g.tbc[q];
