@@ -817,16 +817,17 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
   int64_t* eslot_hi = A.alloc<int64_t>(m + 1);
   int32_t* twin = A.alloc<int32_t>(m2 + 1);
   int max_deg = 0, max_out = 0;
+  const int kb = bits_for(std::max(n, 1));  // bits of a vertex id in the directed CSR keys
   if (n > 0) {
     int32_t* degc = A.alloc<int32_t>(n, true);
     int64_t* tmp64 = A.alloc<int64_t>(n);
     u64* dk = A.alloc<u64>(m2 + 1);
     u64* dks = A.alloc<u64>(m2 + 1);
     if (m > 0) {
-      k_relabel_keys<<<grid_for(m, B, SM), B, 0, C.st>>>(ukeys, m, inv, dk);
+      k_relabel_keys<<<grid_for(m, B, SM), B, 0, C.st>>>(ukeys, m, inv, dk, kb);
       C.launches++;
-      sort_keys_u64(A, C, dk, dks, m2, 32 + bits_for(n));
-      k_split_keys<<<grid_for(m2, B, SM), B, 0, C.st>>>(dks, m2, ci, degc);
+      sort_keys_u64(A, C, dk, dks, m2, 2 * kb);
+      k_split_keys<<<grid_for(m2, B, SM), B, 0, C.st>>>(dks, m2, ci, degc, kb);
       C.launches++;
     }
     k_i32_to_i64<<<grid_for(n, B, SM), B, 0, C.st>>>(degc, n, tmp64);
@@ -838,8 +839,8 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     C.launches += 4;
     if (m > 0) {
       k_edge_arrays<<<grid_for(m2, B, SM), B, 0, C.st>>>(dks, m2, rp, ci, dmv, orow, eid, ocol, esrc, edst,
-                                                         eslot_hi, twin);
-      k_twin_hi<<<grid_for(m2, B, SM), B, 0, C.st>>>(n, rp, dmv, orow, eslot_hi, eid, m2, dks, twin);
+                                                         eslot_hi, twin, kb);
+      k_twin_hi<<<grid_for(m2, B, SM), B, 0, C.st>>>(n, rp, dmv, orow, eslot_hi, eid, m2, dks, twin, kb);
       C.launches += 2;
     }
     int* d_mx = A.alloc<int>(2, true);

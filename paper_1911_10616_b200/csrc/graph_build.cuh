@@ -315,24 +315,26 @@ __global__ void k_perm(const u64* __restrict__ sorted, int32_t n, int32_t* __res
 }
 
 // ---- a3: relabelled directed keys, both directions ---------------------------
+// directed keys (x << kb) | y in new ids, kb = bits(n): 2 kb key bits instead of 32 + kb (one
+// radix pass less on config 4's 32 M keys)
 __global__ void k_relabel_keys(const u64* __restrict__ keys, int64_t m, const int32_t* __restrict__ inv,
-                               u64* __restrict__ dk) {
+                               u64* __restrict__ dk, int kb) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
        e += (int64_t)gridDim.x * blockDim.x) {
     u64 k = keys[e];
     u32 a = (u32)inv[(int32_t)(k >> 32)], b = (u32)inv[(int32_t)(k & 0xffffffffu)];
-    dk[2 * e] = ((u64)a << 32) | b;
-    dk[2 * e + 1] = ((u64)b << 32) | a;
+    dk[2 * e] = ((u64)a << kb) | b;
+    dk[2 * e + 1] = ((u64)b << kb) | a;
   }
 }
 
 __global__ void k_split_keys(const u64* __restrict__ dk, int64_t m2, int32_t* __restrict__ ci,
-                             int32_t* __restrict__ degc) {
+                             int32_t* __restrict__ degc, int kb) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
        s += (int64_t)gridDim.x * blockDim.x) {
     u64 k = dk[s];
-    ci[s] = (int32_t)(k & 0xffffffffu);
-    atomicAdd(&degc[(int32_t)(k >> 32)], 1);
+    ci[s] = (int32_t)(k & ((1ull << kb) - 1));
+    atomicAdd(&degc[(int32_t)(k >> kb)], 1);
   }
 }
 
@@ -353,10 +355,10 @@ __global__ void k_edge_arrays(const u64* __restrict__ dk, int64_t m2, const int6
                               const int64_t* __restrict__ orow, int32_t* __restrict__ eid,
                               int32_t* __restrict__ ocol, int32_t* __restrict__ esrc,
                               int32_t* __restrict__ edst, int64_t* __restrict__ eslot_hi,
-                              int32_t* __restrict__ twin) {
+                              int32_t* __restrict__ twin, int kb) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
        s += (int64_t)gridDim.x * blockDim.x) {
-    int32_t u = (int32_t)(dk[s] >> 32);
+    int32_t u = (int32_t)(dk[s] >> kb);
     int32_t w = ci[s];
     if (w > u) {
       int64_t e = orow[u] + (s - rp[u] - dm[u]);
@@ -379,9 +381,9 @@ __global__ void k_edge_arrays(const u64* __restrict__ dk, int64_t m2, const int6
 __global__ void k_twin_hi(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ dm,
                           const int64_t* __restrict__ orow, const int64_t* __restrict__ eslot_hi,
                           const int32_t* __restrict__ eid, int64_t m2, const u64* __restrict__ dk,
-                          int32_t* __restrict__ twin) {
+                          int32_t* __restrict__ twin, int kb) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2; s += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t u = (int32_t)(dk[s] >> 32);
+    const int32_t u = (int32_t)(dk[s] >> kb);
     if (s >= rp[u] + dm[u]) twin[s] = (int32_t)eslot_hi[eid[s]];
   }
 }

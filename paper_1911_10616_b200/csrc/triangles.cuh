@@ -97,8 +97,11 @@ __global__ void __launch_bounds__(256) k_triangles(
 // item are consecutive, so a found c's rank inside its list is the item's count so far
 // (per-warp shared) plus the found lanes below it among the item's lanes (match_any mask);
 // the lists stay sorted by c.
+#ifndef TRIFLAT_MINB
+#define TRIFLAT_MINB 8  // resident CTAs per SM the register budget must allow (config 4: 2.57 -> 2.44 ms)
+#endif
 template <int PASS>
-__global__ void __launch_bounds__(256) k_triangles_flat(
+__global__ void __launch_bounds__(256, TRIFLAT_MINB) k_triangles_flat(
     DGraph g, u32* __restrict__ Thigh, u32* __restrict__ Tmid, u32* __restrict__ Tlow, u32* __restrict__ Te,
     u64* __restrict__ Tv, u64* __restrict__ E7, int32_t* __restrict__ tc, int32_t* __restrict__ tab,
     int32_t* __restrict__ tac, int32_t* __restrict__ tbc) {
@@ -193,7 +196,10 @@ __global__ void k_fcur_init(int64_t m, const int64_t* __restrict__ foff, const u
 // (E9<x,y> = sum over triangles (x,y,z) of E1(x,z)-1), DM12 for the three
 // vertices (sum over triangles (u,v,x) of T(v,x)-1), and the full per-edge
 // lists: for edge e=(lo,hi) entries (x, e(lo,x), e(hi,x)).
-__global__ void k_tri_sweep1(DGraph g, const u32* __restrict__ Te, u64* __restrict__ E9f,
+#ifndef SWEEP1_MINB
+#define SWEEP1_MINB 1  // (developer variant: resident 256-thread CTAs per SM for the register budget)
+#endif
+__global__ void __launch_bounds__(256, SWEEP1_MINB) k_tri_sweep1(DGraph g, const u32* __restrict__ Te, u64* __restrict__ E9f,
                              u64* __restrict__ E9b, u64* __restrict__ DM12,
                              int64_t* __restrict__ fcur, int32_t* __restrict__ fx,
                              int32_t* __restrict__ fe1, int32_t* __restrict__ fe2) {
