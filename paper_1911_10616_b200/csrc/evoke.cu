@@ -212,11 +212,17 @@ struct Arena {
   // zeroed allocation
   template <typename T>
   T* zalloc(size_t count) {
+    T* p = try_zalloc<T>(count);
+    if (!p) throw EvokeError{EVOKE_ENOMEM};
+    return p;
+  }
+  template <typename T>
+  T* try_zalloc(size_t count) {
     const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
     if (lease) {
       if (void* q = lease->take(bytes)) return (T*)q;
     }
-    return alloc<T>(count, true);
+    return try_alloc<T>(count, true);
   }
   void release(void* p) {
     for (auto& q : ptrs)
@@ -1131,6 +1137,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     int32_t* plists = A.alloc<int32_t>((size_t)PT_COUNT * n);
     int* tiers = A.alloc<int>(8, true);
     int32_t* hstar = A.alloc<int32_t>(n);
+    int32_t* hstar_s = A.alloc<int32_t>(n);
     u32* pwest = A.alloc<u32>(n);
     u64* dwork = nullptr;
     if (ntri > 0 && !getenv("EVOKE_PAIR_NO_DWORK")) {  // (env: developer A/B)
@@ -1138,7 +1145,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       k_pair_dwork<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, Te, dwork);
       C.launches++;
     }
-    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, dwork, pk, pv, pwest, hstar);
+    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, dwork, pk, pv, pwest, hstar, hstar_s);
     C.tick("pair_est");
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 32, C.st));
@@ -1183,7 +1190,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     C.launches += 2;
     pair_pa = A.alloc<u64>((size_t)n * PO_STRIDE);
     CK(cudaMemsetAsync(pair_pa, 0, sizeof(u64) * (size_t)n * PO_STRIDE, C.st));
-    PairOut po{pair_pa, C4e, hstar, hslot, hpos};
+    PairOut po{pair_pa, C4e, hstar, hstar_s, hslot, hpos};
     const size_t freeb = avail_bytes(C.dev);
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
     const char* phg_env = getenv("EVOKE_PAIR_HG");  // developer knob: heavy-source CTAs
@@ -1212,16 +1219,33 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       return (int)std::min<int64_t>({(int64_t)env_cap("EVOKE_PAIR_HOT", PAIR_HOT_BYTES / word), (int64_t)n,
                                      (int64_t)(PAIR_HOT_BYTES / word)});
     };
+    // the tables, touched lists and queues of pg heavy CTAs; on an allocation failure (the
+    // free estimate is a reading from earlier in the process) half as many CTAs, down to one
+    auto heavy_alloc = [&](int& pg, size_t word, bool with_list, void*& tabs, int32_t*& lists, char*& qmem) {
+      for (;;) {
+        const size_t per = (size_t)((n + 3) / 4 * 4) * word;
+        tabs = A.try_zalloc<char>((size_t)pg * per);
+        lists = (tabs && with_list) ? A.try_alloc<int32_t>((size_t)pg * n) : nullptr;
+        qmem = (tabs && (lists || !with_list)) ? A.try_alloc<char>((size_t)pg * eng_queue_bytes(heavy_qcap)) : nullptr;
+        if (qmem) return;
+        if (tabs) A.release(tabs);
+        if (lists) A.release(lists);
+        if (pg == 1) throw EvokeError{EVOKE_ENOMEM};
+        pg = std::max(1, pg / 2);
+      }
+    };
     if (ht[PT_G64] > 0) {
       // sources beyond the packed 16-bit counters (d(u) or T(u) >= 2^16): u64 tables
-      const int pg = heavy_grid(ht[PT_G64], 8, SM);
-      u64* tabs = A.zalloc<u64>((size_t)pg * (size_t)((n + 1) / 2 * 2));
-      int32_t* lists = A.alloc<int32_t>((size_t)pg * n);
+      int pg = heavy_grid(ht[PT_G64], 8, SM);
+      void* tabs_v;
+      int32_t* lists;
+      char* qmem;
+      heavy_alloc(pg, 8, true, tabs_v, lists, qmem);
+      u64* tabs = (u64*)tabs_v;
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(PT_G64);
       const int cnt = ht[PT_G64];
       const int qcap = heavy_qcap;
-      char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
       const int hk = pair_hot_k(8);
       CK(cudaFuncSetAttribute(k_pairs_heavy<u64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hk * 8));
       jobs.push_back({P_PAIR, 1, [=, &C](cudaStream_t st) {
@@ -1232,14 +1256,16 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     }
     for (int tier : {PT_G32S, PT_G32}) {
       if (ht[tier] == 0) continue;
-      const int pg = heavy_grid(ht[tier], 4, SM);
-      u32* tabs = A.zalloc<u32>((size_t)pg * (size_t)((n + 3) / 4 * 4));
-      int32_t* lists = tier == PT_G32 ? A.alloc<int32_t>((size_t)pg * n) : nullptr;
+      int pg = heavy_grid(ht[tier], 4, SM);
+      void* tabs_v;
+      int32_t* lists;
+      char* qmem;
+      heavy_alloc(pg, 4, tier == PT_G32, tabs_v, lists, qmem);
+      u32* tabs = (u32*)tabs_v;
       int* counter = A.alloc<int>(1, true);
       const int32_t* pl = plist(tier);
       const int cnt = ht[tier];
       const int qcap = heavy_qcap;
-      char* qmem = A.alloc<char>((size_t)pg * eng_queue_bytes(qcap));
       const int hk = pair_hot_k(4);
       CK(cudaFuncSetAttribute(k_pairs_heavy<u32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hk * 4));
       CK(cudaFuncSetAttribute(k_pairs_heavy<u32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hk * 4));

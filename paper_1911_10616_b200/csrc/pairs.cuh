@@ -48,6 +48,7 @@ struct PairOut {
   u64* pa;  // [n][PO_STRIDE]
   u64* C4e;
   const int32_t* hstar;     // per source: its heaviest neighbour h* (wedges through h* are not walked)
+  const int32_t* hstar_s;   // per source: the slot of h* in N(u)
   const int32_t* hub_slot;  // per vertex: row of its position map, or -1
   const int32_t* hub_pos;   // [slot][x]: position of x in N(hub) if x ~ hub, else -1
 };
@@ -945,14 +946,14 @@ __device__ __forceinline__ void s51_adjacent(const DGraph& g, const PairOut& o, 
 }
 
 // h* of u: the first slot of N(h*) above u, and T(u, h*)
-__device__ __forceinline__ void hstar_info(const DGraph& g, int32_t u, int32_t hs, int64_t& hfrom, int& tuh,
+// (p: the slot of h* in N(u), from k_pair_est; its twin is u's slot in N(h*))
+__device__ __forceinline__ void hstar_info(const DGraph& g, int32_t hs, int32_t p, int64_t& hfrom, int& tuh,
                                            int32_t& euh) {
   hfrom = 0; tuh = 0; euh = -1;
   if (hs < 0) return;
-  const int64_t p = lower_bound_dev<int32_t>(g.ci, g.rp[u], g.rp[u + 1], hs);
   euh = g.eid[p];
   tuh = (int)g.tes[p];
-  hfrom = slot_in_other(g, hs, euh, g.esrc[euh] == hs) + 1;
+  hfrom = (int64_t)g.twin[p] + 1;
 }
 
 // slot of h* in N(u) -> edge id e(u, h*)
@@ -970,7 +971,7 @@ __device__ void pair_source_cta(const DGraph& g, const u32* __restrict__ Te, int
   int64_t hfrom;
   int tuh;
   int32_t euh;
-  hstar_info(g, u, hs, hfrom, tuh, euh);
+  hstar_info(g, hs, hs >= 0 ? o.hstar_s[u] : 0, hfrom, tuh, euh);
   u64 s51 = 0;
   long long t_prev = clock64();
   cta_pass<1, BT>(g, Te, u, hs, r0, r1, tab, E, s51, o);
@@ -1032,7 +1033,7 @@ __device__ void pair_source_warp(const DGraph& g, const u32* __restrict__ Te, in
   int64_t hfrom;
   int tuh;
   int32_t euh;
-  hstar_info(g, u, hs, hfrom, tuh, euh);
+  hstar_info(g, hs, hs >= 0 ? o.hstar_s[u] : 0, hfrom, tuh, euh);
   tab.mask = cap - 1;
   u64 s51 = 0;
   warp_pass<1>(g, Te, u, hs, r0, r1, tab, s51, o, acc);
@@ -1252,27 +1253,28 @@ __global__ void k_pair_dwork(DGraph g, const u32* __restrict__ Te, u64* __restri
 // few wedges can own long diamond lists).  h*(u) = the neighbour with the longest such suffix
 // (ties: lower id).
 __global__ void k_pair_est(DGraph g, const u64* __restrict__ dwork, u32* __restrict__ keys,
-                           int32_t* __restrict__ vals, u32* __restrict__ west, int32_t* __restrict__ hstar) {
+                           int32_t* __restrict__ vals, u32* __restrict__ west, int32_t* __restrict__ hstar,
+                           int32_t* __restrict__ hstar_s) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t ui = gw; ui < g.n; ui += nw) {
     const int32_t u = (int32_t)ui;
     u64 s = 0;
-    int32_t best = -1, bestl = -1;
+    int32_t best = -1, bestl = -1, bests = 0;
     for (int64_t t = g.rp[u] + lane; t < g.rp[u + 1]; t += 32) {
       const int32_t v = g.ci[t];
-      const int32_t e = g.eid[t];
-      const int32_t len = (int32_t)(g.rp[v + 1] - slot_in_other(g, v, e, g.esrc[e] == v) - 1);
+      const int32_t len = (int32_t)(g.rp[v + 1] - g.twin[t] - 1);  // N(v) above u
       s += (u64)len;
-      if (len > bestl || (len == bestl && v < best)) { bestl = len; best = v; }
+      if (len > bestl || (len == bestl && v < best)) { bestl = len; best = v; bests = (int32_t)t; }
     }
     s = warp_sum(s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const int32_t ol = __shfl_xor_sync(FULL_MASK, bestl, o);
       const int32_t ob = __shfl_xor_sync(FULL_MASK, best, o);
-      if (ol > bestl || (ol == bestl && ob < best)) { bestl = ol; best = ob; }
+      const int32_t os = __shfl_xor_sync(FULL_MASK, bests, o);
+      if (ol > bestl || (ol == bestl && ob < best)) { bestl = ol; best = ob; bests = os; }
     }
     if (lane == 0) {
       const u64 est = best >= 0 ? s - (u64)bestl : 0;
@@ -1281,6 +1283,7 @@ __global__ void k_pair_est(DGraph g, const u64* __restrict__ dwork, u32* __restr
       vals[u] = u;
       west[u] = (u32)min(est, (u64)0xffffffffu);
       hstar[u] = best;
+      hstar_s[u] = bests;
     }
   }
 }
