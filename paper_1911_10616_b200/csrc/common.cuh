@@ -110,6 +110,11 @@ struct DGraph {
   // -1 past the end; out8[8 j] = OUT8_LONG when d+(j) > OUT8 (then orow / ocol).  Built only
   // when every out-list is that short (nullptr otherwise)
   const int32_t* out8;
+  // pair pass: for the slot of v in N(u), |N(v) above u| (written by k_pair_est)
+  const int32_t* plen;
+  // 5-cycle pass: for the slot of w in N(l), {start, length} of w's wedge list Nsel(w) (N(w) if
+  // w < l, N+(w) if w > l) and, for w < l, of w's out-list in edge ids (k_c5_slots)
+  const int4* c5s;
   // oriented triangle lists: edge e=(a->b): third vertices c > b, sorted
   const int64_t* toff;  // [m+1]
   const int32_t* tc;    // [ntri]

@@ -454,15 +454,16 @@ struct C5Split {
   __device__ __forceinline__ bool consts() const { return si == 0; }
 };
 
-// wedge lists of steps 1/6: w = N(l)[t], i in N(w) (w < l) or N+(w) (w > l)
+// wedge lists of steps 1/6: w = N(l)[t], i in N(w) (w < l) or N+(w) (w > l); from the slot's
+// precomputed row (coalesced along N(l), no dependent load through w)
 struct C5WInfo {
   const DGraph& g;
   int64_t r0;
   int32_t l;
   __device__ __forceinline__ void operator()(int t, int64_t& base, int& len) const {
-    const int32_t w = g.ci[r0 + t];
-    base = (w < l) ? g.rp[w] : g.rp[w] + g.dm[w];
-    len = (int)(g.rp[w + 1] - base);
+    const int4 si = g.c5s[r0 + t];
+    base = si.x;
+    len = si.y;
   }
 };
 // out-out lists of steps 2/4: k = N-(l)[t], j in N+(k) (edge ids orow[k] + .)
@@ -470,11 +471,34 @@ struct C5KInfo {
   const DGraph& g;
   int64_t r0;
   __device__ __forceinline__ void operator()(int t, int64_t& base, int& len) const {
-    const int32_t k = g.ci[r0 + t];
-    base = g.orow[k];
-    len = (int)(g.orow[k + 1] - base);
+    const int4 si = g.c5s[r0 + t];
+    base = si.z;
+    len = si.w;
   }
 };
+
+// the slot rows of C5WInfo / C5KInfo, one warp per vertex l
+__global__ void k_c5_slots(DGraph g, int4* __restrict__ c5s) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = gw; q < g.n; q += nw) {
+    const int32_t l = (int32_t)q;
+    for (int64_t s = g.rp[l] + lane; s < g.rp[l + 1]; s += 32) {
+      const int32_t w = g.ci[s];
+      const int64_t rw = g.rp[w];
+      const int dw = g.deg[w], dmw = g.dm[w];
+      int4 r;
+      if (w < l) {
+        const int64_t ow = g.orow[w];
+        r = make_int4((int)rw, dw, (int)ow, dw - dmw);  // d+(w) = d(w) - d-(w)
+      } else {
+        r = make_int4((int)(rw + dmw), dw - dmw, 0, 0);
+      }
+      c5s[s] = r;
+    }
+  }
+}
 
 // steps 0-2: ADJ flags, Wn, Q/QT/QM and the j-key list
 template <typename Eng, typename Loc>

@@ -1145,7 +1145,9 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
       k_pair_dwork<<<grid_for(ntri, B, SM), B, 0, C.st>>>(g, Te, dwork);
       C.launches++;
     }
-    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, dwork, pk, pv, pwest, hstar, hstar_s);
+    int32_t* plen = A.alloc<int32_t>(m2 + 1);
+    k_pair_est<<<warp_grid, B, 0, C.st>>>(g, dwork, pk, pv, pwest, hstar, hstar_s, plen);
+    g.plen = plen;  // (the pair jobs capture g after this)
     C.tick("pair_est");
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pk2, pv, pv2, (int64_t)n, 0, 32, C.st));
@@ -1438,6 +1440,10 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     u32* splus = A.alloc<u32>(n);
     u64* c5W = A.alloc<u64>(n);
     u64* c5R = A.alloc<u64>(n);
+    int4* c5s = A.alloc<int4>(m2 + 1);
+    k_c5_slots<<<warp_grid, B, 0, C.st>>>(g, c5s);
+    g.c5s = c5s;  // (the 5-cycle jobs capture g after this)
+    C.launches++;
     k_c5_splus<<<grid_for(n, B, SM), B, 0, C.st>>>(g, splus);
     k_c5_work<<<warp_grid, B, 0, C.st>>>(g, splus, c5W, c5R);
     C.launches += 2;

@@ -315,7 +315,7 @@ __device__ __forceinline__ PairItem pair_item(const DGraph& g, int32_t u, int64_
   it.e = g.eid[s_uv];
   it.vlo = it.v < u;  // ranks: the lower endpoint of e(u,v)
   it.rb = (int64_t)g.twin[s_uv] + 1;
-  it.dv = it.v == hs ? 0 : (int32_t)(g.rp[it.v + 1] - it.rb);
+  it.dv = it.v == hs ? 0 : g.plen[s_uv];  // (= rp[v+1] - rb, from the estimates)
   it.tv = (int32_t)g.tes[s_uv];
   it.fo = it.tv ? g.foff[it.e] : 0;
   return it;
@@ -1254,7 +1254,7 @@ __global__ void k_pair_dwork(DGraph g, const u32* __restrict__ Te, u64* __restri
 // (ties: lower id).
 __global__ void k_pair_est(DGraph g, const u64* __restrict__ dwork, u32* __restrict__ keys,
                            int32_t* __restrict__ vals, u32* __restrict__ west, int32_t* __restrict__ hstar,
-                           int32_t* __restrict__ hstar_s) {
+                           int32_t* __restrict__ hstar_s, int32_t* __restrict__ plen) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1265,6 +1265,7 @@ __global__ void k_pair_est(DGraph g, const u64* __restrict__ dwork, u32* __restr
     for (int64_t t = g.rp[u] + lane; t < g.rp[u + 1]; t += 32) {
       const int32_t v = g.ci[t];
       const int32_t len = (int32_t)(g.rp[v + 1] - g.twin[t] - 1);  // N(v) above u
+      plen[t] = len;
       s += (u64)len;
       if (len > bestl || (len == bestl && v < best)) { bestl = len; best = v; bests = (int32_t)t; }
     }
