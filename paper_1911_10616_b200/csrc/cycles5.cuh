@@ -710,13 +710,13 @@ __global__ void k_c5_work(DGraph g, const u32* __restrict__ splus, u64* __restri
     const int64_t r0 = g.rp[l], r1 = g.rp[l + 1], rm = r0 + g.dm[l];
     u64 w = 0, r = 0;
     for (int64_t s = r0 + lane; s < r1; s += 32) {
-      const int32_t x = g.ci[s];
-      const u64 sel = (u64)((x < l) ? g.deg[x] : (g.deg[x] - g.dm[x]));
+      const int4 si = g.c5s[s];  // the slot's |Nsel(x)| and, for x < l, d+(x)
+      const u64 sel = (u64)si.y;
       w += sel;
       r += sel;
       if (s < rm) {
-        const u64 dpx = (u64)(g.orow[x + 1] - g.orow[x]);
-        w += dpx + (u64)splus[x];
+        const u64 dpx = (u64)si.w;
+        w += dpx + (u64)splus[g.ci[s]];
         r += dpx;
       }
     }

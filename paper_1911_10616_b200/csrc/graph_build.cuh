@@ -328,13 +328,29 @@ __global__ void k_relabel_keys(const u64* __restrict__ keys, int64_t m, const in
   }
 }
 
+// (degrees from the sorted keys: the slot that ends a run of equal rows writes its length,
+// found by a search back to the run's start -- no atomics on the rows' counters)
 __global__ void k_split_keys(const u64* __restrict__ dk, int64_t m2, int32_t* __restrict__ ci,
                              int32_t* __restrict__ degc, int kb) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
        s += (int64_t)gridDim.x * blockDim.x) {
-    u64 k = dk[s];
+    const u64 k = dk[s];
     ci[s] = (int32_t)(k & ((1ull << kb) - 1));
-    atomicAdd(&degc[(int32_t)(k >> kb)], 1);
+    const u64 row = k >> kb;
+    if (s + 1 == m2 || (dk[s + 1] >> kb) != row) {  // last slot of its row
+      // first slot of the row: gallop back from s, then bisect (O(log d) loads)
+      int64_t hi = s, step = 1, lo = s - 1;
+      while (lo >= 0 && (dk[lo] >> kb) == row) {
+        hi = lo;
+        lo = s - (step <<= 1);
+      }
+      lo = lo < 0 ? 0 : lo + 1;  // dk[lo - 1] (if any) belongs to an earlier row; dk[hi] to this one
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((dk[mid] >> kb) < row) lo = mid + 1; else hi = mid;
+      }
+      degc[(int32_t)row] = (int32_t)(s - lo + 1);
+    }
   }
 }
 
