@@ -49,6 +49,7 @@ def _load():
             lib.oracle_orbits_bruteforce.argtypes = [i64, i64, i32p, u64p]
             lib.oracle_noninduced_bruteforce.argtypes = [i64, i64, i32p, u64p]
             lib.oracle_clique_totals.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
+            lib.oracle_clique_totals_bits.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_pattern.argtypes = [ctypes.c_int, ip, ip, ip, ip]
             lib.oracle_automorphism_classes.argtypes = [ctypes.c_int, ip, ip]
             lib.oracle_classify.argtypes = [ctypes.c_int, ctypes.c_int, ip]
@@ -123,6 +124,19 @@ def clique_totals(n: int, edges, threads: int = 0, kmax: int = 5):
     if lib.oracle_clique_totals(n, e.shape[0], _ptr(e, ctypes.c_int32), _ptr(c, ctypes.c_uint64), threads,
                                 int(kmax)):
         raise RuntimeError("oracle_clique_totals failed")
+    return int(c[0]), (int(c[1]) if kmax >= 4 else None), (int(c[2]) if kmax >= 5 else None)
+
+
+def clique_totals_bits(n: int, edges, threads: int = 0, kmax: int = 5):
+    """The same totals as ``clique_totals`` (same definition, same counting vertex), with
+    the membership tests on a local adjacency bitmap of N>(a): fast enough for config 3's
+    5-cliques and config 5's 4- and 5-cliques."""
+    lib = _load()
+    e = _edges(edges)
+    c = np.zeros(3, dtype=np.uint64)
+    if lib.oracle_clique_totals_bits(n, e.shape[0], _ptr(e, ctypes.c_int32), _ptr(c, ctypes.c_uint64), threads,
+                                     int(kmax)):
+        raise RuntimeError("oracle_clique_totals_bits failed")
     return int(c[0]), (int(c[1]) if kmax >= 4 else None), (int(c[2]) if kmax >= 5 else None)
 
 

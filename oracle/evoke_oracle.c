@@ -613,3 +613,102 @@ int oracle_clique_totals(int64_t n, int64_t m, const int32_t *edges, uint64_t *c
   graph_free(&g);
   return 0;
 }
+
+/* The same clique totals (cliques = P:702 / P:861-864, each counted once at its first
+ * vertex in the degree order of P:432-437) with the inner membership tests done on a
+ * local adjacency bitmap, for the graphs where the plain loop nest above is too slow
+ * (config 3's 5-cliques, config 5's 4- and 5-cliques).  For every vertex a:
+ *   L = N>(a) listed in degree order; row i of the bitmap holds bit j (j > i) iff
+ *   L[i] ~ L[j].  A clique {a} + S, S a pairwise-adjacent subset of L, is found once, from
+ *   its member of least position: triangles = sum_i |row i|, 4-cliques = sum over bits j of
+ *   row i of |row i & row j|, 5-cliques = sum over bits l of (row i & row j) of
+ *   |row i & row j & row l|.
+ * Pinned against oracle_clique_totals (itself pinned against all-subsets brute force) in
+ * tests/test_oracle_pins.py; kmax as there. */
+static int64_t *g_ord_rank;  /* rank of each vertex in degree order (read-only in the loop) */
+static int cmp_by_rank(const void *x, const void *y) {
+  int64_t a = g_ord_rank[*(const int32_t *)x], b = g_ord_rank[*(const int32_t *)y];
+  return (a > b) - (a < b);
+}
+
+int oracle_clique_totals_bits(int64_t n, int64_t m, const int32_t *edges, uint64_t *counts, int threads,
+                              int kmax) {
+  graph_t g;
+  if (graph_build(&g, n, m, edges)) return -1;
+  /* degree order (ties by id) as a rank: sort ids by (degree, id) */
+  int64_t *key = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t *rank = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t *orp = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  int32_t *oadj = (int32_t *)malloc(sizeof(int32_t) * (size_t)(g.rp[n] / 2 + 1));
+  if (!key || !rank || !orp || !oadj) { free(key); free(rank); free(orp); free(oadj); graph_free(&g); return -1; }
+  for (int64_t v = 0; v < n; v++) key[v] = ((g.rp[v + 1] - g.rp[v]) << 32) | v;  /* degree < 2^31 */
+  qsort(key, (size_t)n, sizeof(int64_t), cmp_u64);  /* non-negative keys: unsigned order = signed order */
+  for (int64_t r = 0; r < n; r++) rank[key[r] & 0xffffffffLL] = r;
+  free(key);
+  /* N>(a): the later neighbours of a, listed in degree order */
+  int64_t kmax_list = 0;
+  for (int64_t a = 0; a < n; a++) {
+    orp[a + 1] = orp[a];
+    for (int64_t p = g.rp[a]; p < g.rp[a + 1]; p++)
+      if (rank[g.adj[p]] > rank[a]) oadj[orp[a + 1]++] = g.adj[p];
+    if (orp[a + 1] - orp[a] > kmax_list) kmax_list = orp[a + 1] - orp[a];
+  }
+  g_ord_rank = rank;
+  for (int64_t a = 0; a < n; a++) qsort(oadj + orp[a], (size_t)(orp[a + 1] - orp[a]), sizeof(int32_t), cmp_by_rank);
+  uint64_t t3 = 0, t4 = 0, t5 = 0;
+  int fail = 0;
+  const int64_t W = (kmax_list + 63) / 64;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+#pragma omp parallel reduction(+:t3, t4, t5) reduction(|:fail)
+  {
+    int32_t *pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));  /* position in L, or -1 */
+    uint64_t *row = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(kmax_list * W + 1));
+    uint64_t *c2 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(W + 1));
+    const int ok = pos && row && c2;
+    if (ok) for (int64_t v = 0; v < n; v++) pos[v] = -1;
+    {
+#pragma omp for schedule(dynamic, 16)
+      for (int64_t a = 0; a < n; a++) {
+        if (!ok) { fail = 1; continue; }  /* every thread still reaches the worksharing loop */
+        const int32_t *L = oadj + orp[a];
+        const int64_t k = orp[a + 1] - orp[a], w = (k + 63) / 64;
+        if (k < 2) continue;
+        for (int64_t i = 0; i < k; i++) pos[L[i]] = (int32_t)i;
+        memset(row, 0, sizeof(uint64_t) * (size_t)(k * w));
+        /* L[i] ~ L[j] with j > i  <=>  L[j] in N>(L[i]) and in L */
+        for (int64_t i = 0; i < k; i++)
+          for (int64_t p = orp[L[i]]; p < orp[L[i] + 1]; p++) {
+            int32_t j = pos[oadj[p]];
+            if (j >= 0) row[i * w + j / 64] |= 1ULL << (j % 64);
+          }
+        for (int64_t i = 0; i < k; i++) {
+          const uint64_t *ri = row + i * w;
+          for (int64_t q = 0; q < w; q++) t3 += (uint64_t)__builtin_popcountll(ri[q]);
+          if (kmax < 4) continue;
+          for (int64_t q = 0; q < w; q++)
+            for (uint64_t bits = ri[q]; bits; bits &= bits - 1) {
+              int64_t j = q * 64 + __builtin_ctzll(bits);
+              const uint64_t *rj = row + j * w;
+              for (int64_t s = 0; s < w; s++) { c2[s] = ri[s] & rj[s]; t4 += (uint64_t)__builtin_popcountll(c2[s]); }
+              if (kmax < 5) continue;
+              for (int64_t s = 0; s < w; s++)
+                for (uint64_t b2 = c2[s]; b2; b2 &= b2 - 1) {
+                  const uint64_t *rl = row + (s * 64 + __builtin_ctzll(b2)) * w;
+                  for (int64_t u = 0; u < w; u++) t5 += (uint64_t)__builtin_popcountll(c2[u] & rl[u]);
+                }
+            }
+        }
+        for (int64_t i = 0; i < k; i++) pos[L[i]] = -1;
+      }
+    }
+    free(pos); free(row); free(c2);
+  }
+  counts[0] = t3; counts[1] = t4; counts[2] = t5;
+  free(rank); free(orp); free(oadj);
+  graph_free(&g);
+  return fail ? -1 : 0;
+}

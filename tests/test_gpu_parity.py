@@ -293,12 +293,18 @@ def test_config2_low_degree_core_full_matrix(pkg):
     deg = np.bincount(e.ravel(), minlength=g.n)
     keep = deg <= 12
     e = e[keep[e[:, 0]] & keep[e[:, 1]]].astype(np.int32)
-    _assert_equal(pkg.evoke_orbits_edges(g.n, e), oracle.orbits(g.n, e), "config2 core")
+    ref = oracle.orbits(g.n, e)
+    _assert_equal(pkg.evoke_orbits_edges(g.n, e), ref, "config2 core")
+    # EVOKE-4 and the serial schedule against the oracle at this size too
+    got4 = pkg.evoke_orbits_edges(g.n, e, four_only=True)
+    _assert_equal(got4[:, :15], ref[:, :15], "config2 core four")
+    assert (got4[:, 15:] == 0).all()
+    _assert_equal(pkg.evoke_orbits_edges(g.n, e, serial=True), ref, "config2 core serial")
 
 
 def test_config3_rows_and_invariants(pkg):
-    """R-MAT 18 (BASELINE configs[2]): invariants incl. Sigma DIM3 = 3 #K3 and Sigma DIM14 =
-    4 #K4 (golden totals from the oracle), sampled rooted rows (cheapest roots plus a few
+    """R-MAT 18 (BASELINE configs[2]): invariants incl. Sigma DIM3 = 3 #K3, Sigma DIM14 =
+    4 #K4 and Sigma DIM72 = 5 #K5 (golden totals from the oracle), sampled rooted rows (cheapest roots plus a few
     drawn uniformly, each kept when the rooted oracle finishes within its cap); the hub rows
     are covered by test_noninduced_degree_forms_every_vertex and the invariants"""
     g = graphgen.config(3)
@@ -357,8 +363,11 @@ def test_ccd_matches_definition(pkg):
         vals, cnts = pkg.evoke_ccd(out, orbit)
         uv = np.unique(col)
         assert np.array_equal(vals, uv), orbit
-        exp = np.array([(col >= x).sum() for x in uv[:50]], dtype=np.uint64)
-        assert np.array_equal(cnts[:50], exp), orbit
+        # every distinct value: #{v : col[v] >= x} = n - #{v : col[v] < x}
+        exp = (g.n - np.searchsorted(np.sort(col), uv, side="left")).astype(np.uint64)
+        assert np.array_equal(cnts, exp), orbit
+        for x in uv[:: max(1, uv.size // 40)]:  # the definition written out on a spread of values
+            assert int(cnts[np.searchsorted(uv, x)]) == int((col >= x).sum()), (orbit, x)
         assert int(cnts[0]) == g.n
 
 
@@ -476,8 +485,9 @@ def test_release_scratch_returns_memory(pkg):
 # ------------------------------------------------------------ config 5 (last: longest) ---
 def test_config5_invariants(pkg):
     """R-MAT 23 (BASELINE configs[4], ~65M edges, the 8-GPU config) on one B200: orbit 0 =
-    degree, per-pattern consistency mod 2^64, Sigma DIM3 = 3 #K3 (golden, from the oracle),
-    and the rooted oracle's rows for sampled cheap roots"""
+    degree, per-pattern consistency mod 2^64, Sigma DIM3 = 3 #K3,
+    Sigma DIM14 = 4 #K4 and Sigma DIM72 = 5 #K5 (golden totals from the oracle's bitmap
+    clique counter), and the rooted oracle's rows for sampled cheap roots"""
     g = graphgen.config(5)
     out = pkg.evoke_orbits_edges(g.n, g.edges)
     _invariants(g, out, cliques=_golden_cliques(5, g))

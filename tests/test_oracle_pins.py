@@ -401,6 +401,35 @@ def test_clique_totals_kmax():
         assert oracle.clique_totals(n, e, kmax=4) == (t3, t4, None)
 
 
+# oracle.clique_totals_bits: the same totals with the membership tests on a bitmap of N>(a)
+# (what the golden totals of configs 3 and 5 need); pinned by the same brute force and
+# closed forms, with lists longer than one 64-bit word
+def test_clique_totals_bits_vs_all_subsets_and_plain():
+    rng = random.Random(75)
+    for _ in range(60):
+        n, e = rand_graph(rng, 3, 14, 0.2, 0.95)
+        assert oracle.clique_totals_bits(n, e) == _cliques_by_subsets(n, e), (n, e)
+    for t in range(6):  # rows of 2-4 words: N>(a) up to ~200 vertices
+        g = graphgen.erdos_renyi(int(rng.randint(90, 220)), rng.uniform(0.3, 0.6), 700 + t)
+        assert oracle.clique_totals_bits(g.n, g.edges) == oracle.clique_totals(g.n, g.edges), g.name
+
+
+@pytest.mark.parametrize("n", [3, 5, 17, 64, 65, 66, 130])
+def test_clique_totals_bits_complete_graph(n):
+    assert oracle.clique_totals_bits(n, graphgen.complete(n).edges) == (C(n, 3), C(n, 4), C(n, 5))
+
+
+def test_clique_totals_bits_complete_multipartite_and_kmax():
+    for parts in [(2, 3, 4), (1, 1, 5, 2), (3, 3, 3, 3, 3), (4, 1, 2, 6, 3), (20, 30, 25, 1, 9)]:
+        offs = np.cumsum((0,) + parts)
+        e = [(a, b) for i in range(len(parts)) for j in range(i + 1, len(parts))
+             for a in range(offs[i], offs[i + 1]) for b in range(offs[j], offs[j + 1])]
+        ek = [sum(int(np.prod(c)) for c in itertools.combinations(parts, k)) for k in (3, 4, 5)]
+        assert oracle.clique_totals_bits(int(offs[-1]), e) == tuple(ek), parts
+        assert oracle.clique_totals_bits(int(offs[-1]), e, kmax=3) == (ek[0], None, None)
+        assert oracle.clique_totals_bits(int(offs[-1]), e, kmax=4) == (ek[0], ek[1], None)
+
+
 def test_degree_forms_vs_noninduced_bruteforce():
     """the degree-only closed forms the GPU tests apply to every vertex of configs 2-4
     (tests/degree_forms.py) equal the non-induced brute force on random graphs"""
