@@ -132,6 +132,32 @@ int evoke_orbits_csr(int64_t n, const int64_t* rowptr, const int32_t* col, uint6
                      const evoke_options* opt);
 
 /*
+ * evoke_orbits_edges_multi -- the same result computed on several GPUs of one process
+ * (SURVEY 8(b)'s num_gpus; the north star's data-parallel layout: the graph replicated on
+ * every GPU, the work units of the sharded passes split by balanced work estimate,
+ * DESIGN.md section 7; the paper's parallel orbit groups).
+ *   devices      int[num_devices], CUDA ordinals; shard d of num_devices runs on devices[d]
+ *                (one host thread per distinct device; shards naming the same device run
+ *                one after the other on it, which tests the decomposition on one GPU)
+ *   num_devices  1..64
+ *   opt          as for evoke_orbits_edges, except: opt->device and opt->stream are
+ *                ignored (each shard runs on its device's library stream); with
+ *                device_pointers=1, edges and out live on devices[0] (the other devices
+ *                copy the edge list over peer memory); opt->num_shards / shard_index compose
+ *                (this call computes shards shard_index*num_devices + d of
+ *                num_shards*num_devices, so several processes or nodes can split further);
+ *                opt->stats, if set, receives shard 0's statistics.
+ * Each device computes its shard's partial n x 73 matrix (exact modulo 2^64); devices[0]
+ * sums them element-wise modulo 2^64, reading peer partials directly over NVLink when peer
+ * access is available (staged copies otherwise).  Memory: every device holds the edge list,
+ * its call's scratch and one n x 73 uint64 partial.  Returns EVOKE_OK or the first failing
+ * shard's code (message via evoke_last_error(), naming the shard and device); out is written
+ * only on success.
+ */
+int evoke_orbits_edges_multi(int64_t n, int64_t m, const int32_t* edges, uint64_t* out,
+                             const int* devices, int num_devices, const evoke_options* opt);
+
+/*
  * evoke_ccd -- complementary cumulative distribution of one orbit (the paper's VOC
  * distributions: "for x, ... the fraction of vertices whose orbit count is at
  * least x").

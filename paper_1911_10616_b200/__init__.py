@@ -61,7 +61,8 @@ _lock = threading.Lock()
 _lib = None
 
 EXPORTED_SYMBOLS = ("evoke_default_options", "evoke_orbits_edges", "evoke_orbits_csr", "evoke_pass_name",
-                    "evoke_strerror", "evoke_last_error", "evoke_version", "evoke_ccd", "evoke_release_scratch")
+                    "evoke_strerror", "evoke_last_error", "evoke_version", "evoke_ccd", "evoke_release_scratch",
+                    "evoke_orbits_edges_multi")
 
 
 def lib():
@@ -80,6 +81,10 @@ def lib():
             L.evoke_orbits_csr.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.POINTER(_Options)]
             L.evoke_orbits_csr.restype = ctypes.c_int
+            L.evoke_orbits_edges_multi.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                                   ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                                   ctypes.POINTER(_Options)]
+            L.evoke_orbits_edges_multi.restype = ctypes.c_int
             L.evoke_ccd.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_Options)]
             L.evoke_ccd.restype = ctypes.c_int
@@ -188,6 +193,42 @@ def evoke_orbits_edges(n: int, edges, out=None, induced: bool = True, shard_inde
         rc = lib().evoke_orbits_edges(n, m, e.ctypes.data if m else None, out.ctypes.data, ctypes.byref(o))
     _check(rc)
     if return_stats or workmodel:
+        return out, _stats_dict(st)
+    return out
+
+
+def evoke_orbits_edges_multi(n: int, edges, devices, out=None, induced: bool = True, shard_index: int = 0,
+                             num_shards: int = 1, return_stats: bool = False, four_only: bool = False):
+    """The same matrix computed on several GPUs of this process (C ABI
+    ``evoke_orbits_edges_multi``): shard d of len(devices) runs on devices[d], devices[0]
+    sums the partials over peer memory.  ``edges``: numpy int32 [m, 2] (host) or a CUDA torch
+    tensor on devices[0]; ``out`` as for ``evoke_orbits_edges``."""
+    st = _Stats() if return_stats else None
+    fl = FLAG_FOUR if four_only else 0
+    devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+    if _is_torch(edges):
+        import torch
+        assert edges.is_cuda and edges.dtype == torch.int32, "device edges must be CUDA int32"
+        assert edges.device.index == int(devices[0]), "device edges must live on devices[0]"
+        e = edges.contiguous()
+        m = e.numel() // 2
+        if out is None:
+            out = torch.empty((n, NUM_ORBITS), dtype=torch.int64, device=e.device)
+        assert out.is_cuda and out.device == e.device and out.is_contiguous() and out.numel() == n * NUM_ORBITS
+        torch.cuda.synchronize(e.device)  # the library's per-device streams do not see torch's
+        o = _make_options(induced, True, shard_index, num_shards, None, None, st, fl)
+        rc = lib().evoke_orbits_edges_multi(n, m, e.data_ptr(), out.data_ptr(), devs, len(devices), ctypes.byref(o))
+    else:
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+        m = e.shape[0]
+        if out is None:
+            out = np.zeros((n, NUM_ORBITS), dtype=np.uint64)
+        assert out.dtype == np.uint64 and out.flags.c_contiguous and out.size == n * NUM_ORBITS
+        o = _make_options(induced, False, shard_index, num_shards, None, None, st, fl)
+        rc = lib().evoke_orbits_edges_multi(n, m, e.ctypes.data if m else None, out.ctypes.data, devs, len(devices),
+                                            ctypes.byref(o))
+    _check(rc)
+    if return_stats:
         return out, _stats_dict(st)
     return out
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/evoke.h"
@@ -1943,6 +1944,173 @@ int guarded(const Input& in, uint64_t* out, const evoke_options* opt) {
   return EVOKE_OK;
 }
 
+// ---- several GPUs from one process (SURVEY 8(b) num_gpus) ----------
+// acc[i] += src[i] modulo 2^64.  src is a partial matrix on this device or on a peer device
+// (then every load crosses NVLink: the reduction reads the peer's memory directly, there is
+// no staging copy).  Buffers from cudaMalloc, so 16-byte aligned.
+__global__ void k_add_partial(u64* __restrict__ acc, const u64* __restrict__ src, int64_t cnt) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  ulonglong2* a2 = reinterpret_cast<ulonglong2*>(acc);
+  const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src);
+  for (int64_t i = t0; i < cnt / 2; i += nt) {
+    ulonglong2 a = a2[i];
+    const ulonglong2 b = s2[i];
+    a.x += b.x;
+    a.y += b.y;
+    a2[i] = a;
+  }
+  if (t0 == 0 && (cnt & 1)) acc[cnt - 1] += src[cnt - 1];
+}
+
+// Shard d of num_devices runs on devices[d] (one host thread per distinct device; shards
+// that name the same device run one after the other on it), every device with its own copy
+// of the edge list (the graph is replicated), each shard's partial n x 73
+// matrix in that device's memory.  devices[0] then sums the partials (k_add_partial over
+// peer memory, or staged chunks when peer access is unavailable) and the sum is copied to
+// out only after every shard and the reduction succeeded.
+int multi_edges(int64_t n, int64_t m, const int32_t* edges, uint64_t* out, const int* devices, int nd,
+                const evoke_options* opt) {
+  g_last_error.clear();
+  evoke_options o;
+  evoke_default_options(&o);
+  if (opt) {
+    if (opt->struct_size != 0 && opt->struct_size < sizeof(evoke_options)) std::memcpy(&o, opt, opt->struct_size);
+    else o = *opt;
+  }
+  if (!devices || nd < 1 || nd > 64) { set_error("need 1..64 devices, got %d", nd); return EVOKE_EINVAL; }
+  if (o.num_shards < 1 || o.shard_index < 0 || o.shard_index >= o.num_shards ||
+      (int64_t)o.num_shards * nd > (int64_t)INT32_MAX) {
+    set_error("bad shard %d of %d (x %d devices)", o.shard_index, o.num_shards, nd);
+    return EVOKE_EINVAL;
+  }
+  if (n < 0 || n >= (1ll << 31) - 1) { set_error("bad n = %lld", (long long)n); return EVOKE_EINVAL; }
+  if (m < 0 || (m > 0 && !edges)) { set_error("bad m or NULL edges"); return EVOKE_EINVAL; }
+  if (n > 0 && !out) { set_error("out is NULL"); return EVOKE_EINVAL; }
+  if (n == 0) {
+    if (o.stats) { std::memset(o.stats, 0, sizeof(*o.stats)); o.stats->num_passes = P_COUNT; }
+    return EVOKE_OK;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+    set_error("cudaGetDeviceCount: %s", cudaGetErrorString(cudaGetLastError()));
+    return EVOKE_ECUDA;
+  }
+  for (int d = 0; d < nd; d++)
+    if (devices[d] < 0 || devices[d] >= ndev) { set_error("device %d not in [0, %d)", devices[d], ndev); return EVOKE_EINVAL; }
+  int cur = 0;
+  (void)cudaGetDevice(&cur);
+  const int dev0 = devices[0];
+  std::vector<int> uniq;
+  std::vector<std::vector<int>> shards_of;
+  for (int d = 0; d < nd; d++) {
+    const size_t u = std::find(uniq.begin(), uniq.end(), devices[d]) - uniq.begin();
+    if (u == uniq.size()) { uniq.push_back(devices[d]); shards_of.emplace_back(); }
+    shards_of[u].push_back(d);
+  }
+  const size_t cells = (size_t)n * EVOKE_NUM_ORBITS, ebytes = sizeof(int32_t) * 2 * (size_t)m;
+  std::vector<u64*> part(nd, nullptr);
+  std::vector<int> rc(uniq.size(), EVOKE_OK);
+  std::vector<std::string> msg(uniq.size());
+  auto worker = [&](size_t ui) {
+    const int dev = uniq[ui];
+    int32_t* dedges = nullptr;
+    bool own_edges = false;
+    auto fail = [&](int code, const std::string& what) { rc[ui] = code; msg[ui] = what; };
+    auto cuda_ok = [&](cudaError_t e, const char* what) {
+      if (e == cudaSuccess) return true;
+      (void)cudaGetLastError();
+      fail(e == cudaErrorMemoryAllocation ? EVOKE_ENOMEM : EVOKE_ECUDA,
+           std::string(what) + ": " + cudaGetErrorString(e) + " (device " + std::to_string(dev) + ")");
+      return false;
+    };
+    if (!cuda_ok(cudaSetDevice(dev), "cudaSetDevice")) return;
+    if (m > 0) {
+      if (o.device_pointers && dev == dev0) {
+        dedges = const_cast<int32_t*>(edges);  // the caller's copy, on devices[0]
+      } else if (cuda_ok(cudaMalloc(&dedges, ebytes), "edge list copy")) {
+        own_edges = true;
+        if (o.device_pointers) cuda_ok(cudaMemcpyPeer(dedges, dev, edges, dev0, ebytes), "edge list peer copy");
+        else cuda_ok(cudaMemcpy(dedges, edges, ebytes, cudaMemcpyHostToDevice), "edge list H2D");
+      }
+    }
+    for (int d : shards_of[ui]) {
+      if (rc[ui] != EVOKE_OK) break;
+      if (!cuda_ok(cudaMalloc(&part[d], sizeof(u64) * cells), "partial matrix")) break;
+      evoke_options od = o;
+      od.device = dev;
+      od.device_pointers = 1;
+      od.stream = nullptr;
+      od.num_shards = o.num_shards * nd;
+      od.shard_index = o.shard_index * nd + d;
+      od.stats = d == 0 ? o.stats : nullptr;
+      const int r = evoke_orbits_edges(n, m, dedges, reinterpret_cast<uint64_t*>(part[d]), &od);
+      if (r != EVOKE_OK) fail(r, std::string("shard ") + std::to_string(d) + ": " + evoke_last_error());
+      else cuda_ok(cudaDeviceSynchronize(), "shard synchronise");
+    }
+    if (own_edges) (void)cudaFree(dedges);
+  };
+  std::vector<std::thread> th;
+  for (size_t ui = 1; ui < uniq.size(); ui++) th.emplace_back(worker, ui);
+  worker(0);
+  for (auto& t : th) t.join();
+  int code = EVOKE_OK;
+  std::string why;
+  for (size_t ui = 0; ui < uniq.size(); ui++)
+    if (rc[ui] != EVOKE_OK && code == EVOKE_OK) { code = rc[ui]; why = msg[ui]; }
+  // the reduction on devices[0]: acc = partial of shard 0 (which runs there)
+  u64* stage = nullptr;
+  if (code == EVOKE_OK) {
+    auto step = [&](cudaError_t e, const char* what) {
+      if (e == cudaSuccess || code != EVOKE_OK) return code == EVOKE_OK;
+      (void)cudaGetLastError();
+      code = e == cudaErrorMemoryAllocation ? EVOKE_ENOMEM : EVOKE_ECUDA;
+      why = std::string(what) + ": " + cudaGetErrorString(e);
+      return false;
+    };
+    step(cudaSetDevice(dev0), "cudaSetDevice");
+    int SM = 148;
+    step(cudaDeviceGetAttribute(&SM, cudaDevAttrMultiProcessorCount, dev0), "SM count");
+    u64* acc = part[0];
+    const size_t chunk = std::min<size_t>(cells, (size_t)1 << 25);  // 256 MB staging chunks
+    for (int d = 1; d < nd && code == EVOKE_OK; d++) {
+      int peer = devices[d] == dev0;
+      if (!peer) {
+        (void)cudaDeviceCanAccessPeer(&peer, dev0, devices[d]);
+        if (peer) {
+          const cudaError_t e = cudaDeviceEnablePeerAccess(devices[d], 0);
+          if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            if (e != cudaErrorPeerAccessAlreadyEnabled) peer = 0;
+          }
+        }
+      }
+      if (peer) {
+        k_add_partial<<<SM * 4, 256>>>(acc, part[d], (int64_t)cells);
+        step(cudaGetLastError(), "k_add_partial");
+      } else {
+        if (!stage && !step(cudaMalloc(&stage, sizeof(u64) * chunk), "staging buffer")) break;
+        for (size_t off = 0; off < cells && code == EVOKE_OK; off += chunk) {
+          const size_t c = std::min(chunk, cells - off);
+          if (!step(cudaMemcpyPeer(stage, dev0, part[d] + off, devices[d], sizeof(u64) * c), "partial peer copy")) break;
+          k_add_partial<<<SM * 4, 256>>>(acc + off, stage, (int64_t)c);
+          step(cudaGetLastError(), "k_add_partial");
+        }
+      }
+    }
+    step(cudaDeviceSynchronize(), "reduction");
+    if (code == EVOKE_OK)  // out is written only now, after every shard and the sum succeeded
+      step(cudaMemcpy(out, acc, sizeof(u64) * cells, o.device_pointers ? cudaMemcpyDeviceToDevice
+                                                                        : cudaMemcpyDeviceToHost), "result copy");
+  }
+  for (int d = 0; d < nd; d++)
+    if (part[d]) { (void)cudaSetDevice(devices[d]); (void)cudaFree(part[d]); }
+  if (stage) { (void)cudaSetDevice(dev0); (void)cudaFree(stage); }
+  (void)cudaGetLastError();
+  (void)cudaSetDevice(cur);
+  if (code != EVOKE_OK) set_error("%s", why.c_str());
+  return code;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1970,6 +2138,16 @@ int evoke_orbits_csr(int64_t n, const int64_t* rowptr, const int32_t* col, uint6
                      const evoke_options* opt) {
   Input in{1, n, 0, nullptr, rowptr, col};
   return guarded(in, out, opt);
+}
+
+int evoke_orbits_edges_multi(int64_t n, int64_t m, const int32_t* edges, uint64_t* out, const int* devices,
+                             int num_devices, const evoke_options* opt) {
+  try {
+    return multi_edges(n, m, edges, out, devices, num_devices, opt);
+  } catch (const std::exception& e) {
+    set_error("%s", e.what());
+    return EVOKE_EINTERNAL;
+  }
 }
 
 int evoke_ccd(int64_t n, const uint64_t* dim, int orbit, uint64_t* values, uint64_t* counts, int64_t* nvals,

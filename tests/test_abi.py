@@ -31,7 +31,8 @@ def _declared_functions():
 
 def test_header_declares_the_boundary():
     names = _declared_functions()
-    assert {"evoke_orbits_edges", "evoke_orbits_csr", "evoke_default_options", "evoke_strerror",
+    assert {"evoke_orbits_edges", "evoke_orbits_csr", "evoke_orbits_edges_multi", "evoke_default_options",
+            "evoke_strerror",
             "evoke_last_error", "evoke_version", "evoke_pass_name"} <= set(names)
     assert "#define EVOKE_NUM_ORBITS 73" in open(HEADER).read()
 
@@ -89,6 +90,17 @@ def test_argument_validation_without_gpu(pkg):
                               ctypes.byref(o)) == pkg.EVOKE_EINVAL
     with pytest.raises(pkg.EvokeError):
         pkg.evoke_orbits_edges(4, e, num_shards=0)
+    # several GPUs in one process: the device list and the shard arguments are checked first
+    devs = (ctypes.c_int * 2)(0, 0)
+    M = L.evoke_orbits_edges_multi
+    assert M(4, 1, e.ctypes.data, out.ctypes.data, None, 2, ctypes.byref(o)) == pkg.EVOKE_EINVAL
+    assert M(4, 1, e.ctypes.data, out.ctypes.data, devs, 0, ctypes.byref(o)) == pkg.EVOKE_EINVAL
+    assert M(4, 1, e.ctypes.data, out.ctypes.data, devs, 65, ctypes.byref(o)) == pkg.EVOKE_EINVAL
+    assert M(4, 1, e.ctypes.data, out.ctypes.data, devs, 2, ctypes.byref(o2)) == pkg.EVOKE_EINVAL
+    assert M(-1, 1, e.ctypes.data, out.ctypes.data, devs, 2, ctypes.byref(o)) == pkg.EVOKE_EINVAL
+    assert M(4, 1, None, out.ctypes.data, devs, 2, ctypes.byref(o)) == pkg.EVOKE_EINVAL
+    assert M(4, 1, e.ctypes.data, None, devs, 2, ctypes.byref(o)) == pkg.EVOKE_EINVAL
+    assert M(0, 0, None, None, devs, 2, ctypes.byref(o)) == pkg.EVOKE_OK
     # the kept scratch: bad ordinal rejected; releasing when nothing is kept is a no-op
     assert L.evoke_release_scratch(64) == pkg.EVOKE_EINVAL
     assert L.evoke_release_scratch(-2) == pkg.EVOKE_EINVAL

@@ -135,6 +135,34 @@ def test_csr_and_device_pointer_paths(pkg):
     _assert_equal(out.cpu().numpy(), ref, "csr device")
 
 
+def test_multi_device_call(pkg):
+    """evoke_orbits_edges_multi (the C ABI's several-GPUs-in-one-process call): the shards on
+    a device list -- here the one GPU named 2, 3 and 4 times, so the decomposition, the
+    per-device workers, the sum modulo 2^64 and the staged result all run; the peer-memory
+    read of another GPU's partial needs a second GPU -- equal the oracle / the one-call
+    matrix bit for bit; shard arguments compose; a failing shard leaves out untouched"""
+    import torch
+    rng = np.random.default_rng(11)
+    for t in range(20):
+        g = graphgen.erdos_renyi(int(rng.integers(5, 14)), float(rng.uniform(0.2, 0.8)), 4000 + t)
+        ref = oracle.orbits(g.n, g.edges)
+        _assert_equal(pkg.evoke_orbits_edges_multi(g.n, g.edges, [0, 0]), ref, g.name + " multi2")
+        _assert_equal(pkg.evoke_orbits_edges_multi(g.n, g.edges, [0, 0, 0]), ref, g.name + " multi3")
+    g = graphgen.config(2)
+    full = pkg.evoke_orbits_edges(g.n, g.edges)
+    _assert_equal(pkg.evoke_orbits_edges_multi(g.n, g.edges, [0, 0, 0, 0]), full, "config2 multi4")
+    ed = torch.from_numpy(g.edges).to("cuda:0")
+    parts = [pkg.evoke_orbits_edges_multi(g.n, ed, [0, 0], shard_index=r, num_shards=2) for r in range(2)]
+    tot = (parts[0] + parts[1]).cpu().numpy()  # int64 addition wraps like uint64
+    _assert_equal(tot, full, "config2 2 x 2 shards")
+    out = np.full((4, 73), 7, np.uint64)
+    with pytest.raises(pkg.EvokeError) as ei:
+        pkg.evoke_orbits_edges_multi(4, np.array([[0, 1], [1, 7]], np.int32), [0, 0], out=out)
+    assert ei.value.code == pkg.EVOKE_EINVAL and (out == 7).all()
+    with pytest.raises(pkg.EvokeError):
+        pkg.evoke_orbits_edges_multi(4, np.array([[0, 1]], np.int32), [0, 99])
+
+
 def test_sharded_partials_sum_to_full(pkg):
     """multi-GPU decomposition on one device: partials of every shard sum (mod 2^64) to
     the full matrix bit for bit"""
