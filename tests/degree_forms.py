@@ -26,23 +26,24 @@ def _binom_mod(x: np.ndarray, k: int) -> np.ndarray:
 
 def degree_forms(n: int, edges) -> dict:
     """{orbit: uint64[n]} for the columns in COLUMNS."""
-    e = np.unique(np.sort(np.asarray(edges, dtype=np.int64).reshape(-1, 2), axis=1), axis=0)
+    e = np.sort(np.asarray(edges, dtype=np.int64).reshape(-1, 2), axis=1)
     e = e[e[:, 0] != e[:, 1]]
-    a = np.concatenate([e[:, 0], e[:, 1]])
-    b = np.concatenate([e[:, 1], e[:, 0]])
-    order = np.argsort(a, kind="stable")
-    a, b = a[order], b[order]
+    key = np.sort(e[:, 0] * max(n, 1) + e[:, 1])
+    key = key[np.concatenate([[True], key[1:] != key[:-1]])] if key.size else key  # each edge once
+    lo, hi = key // max(n, 1), key % max(n, 1)
+    a = np.concatenate([lo, hi])
+    b = np.concatenate([hi, lo])
     deg = np.bincount(a, minlength=n).astype(np.int64)
-    starts = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(deg, out=starts[1:])
 
     def nbr_sum(f: np.ndarray) -> np.ndarray:  # sum_{u in N(v)} f(u), wrapping uint64
+        # in three 22-bit limbs: each limb's sum over a neighbourhood stays below 2^53, so the
+        # float64 bincount is exact; the limbs are recombined modulo 2^64
         out = np.zeros(n, dtype=np.uint64)
-        if a.size == 0:
-            return out
-        vals = f[b]
-        has = deg > 0
-        out[has] = np.add.reduceat(vals, starts[:-1][has])
+        vals = f[b].astype(np.uint64)
+        for sh in (0, 22, 44):
+            limb = ((vals >> np.uint64(sh)) & np.uint64((1 << 22) - 1)).astype(np.float64)
+            s = np.bincount(a, weights=limb, minlength=n).astype(np.uint64)
+            out += s << np.uint64(sh)
         return out
 
     dm1 = np.maximum(deg - 1, 0)

@@ -40,6 +40,17 @@ def _rand(rng, nmin, nmax, pmin, pmax, seed):
     return graphgen.erdos_renyi(n, p, seed)
 
 
+def _unique_edges(n, edges):
+    """the distinct unordered pairs of an edge list as sorted (lo, hi) rows (what
+    np.unique(np.sort(edges, axis=1), axis=0) returns, by one key sort: np.unique with
+    axis=0 takes minutes on config 5's 67M pairs)"""
+    e = np.sort(np.asarray(edges, dtype=np.int64).reshape(-1, 2), axis=1)
+    key = np.sort(e[:, 0] * max(n, 1) + e[:, 1])
+    if key.size:
+        key = key[np.concatenate([[True], key[1:] != key[:-1]])]
+    return np.stack([key // max(n, 1), key % max(n, 1)], axis=1)
+
+
 def _assert_equal(got, exp, what=""):
     got = np.asarray(got)
     if got.dtype != np.uint64:
@@ -254,7 +265,7 @@ def _golden_cliques(cfg, g):
 
 
 def _invariants(g, out, check_cliques=True, cliques=None):
-    e = np.unique(np.sort(g.edges.astype(np.int64), axis=1), axis=0)
+    e = _unique_edges(g.n, g.edges)
     e = e[e[:, 0] != e[:, 1]]
     deg = np.bincount(e.ravel(), minlength=g.n).astype(np.uint64)
     assert (out[:, 0] == deg).all(), "orbit 0 = degree"
@@ -278,7 +289,7 @@ def _invariants(g, out, check_cliques=True, cliques=None):
 def _cheap_roots(g, k, seed, pool=4000):
     """roots whose rooted enumeration is small: lowest 3-hop path count sum_w s2(w),
     s2(w) = sum_{x in N(w)} d(x), plus a few uniformly random roots"""
-    e = np.unique(np.sort(g.edges.astype(np.int64), axis=1), axis=0)
+    e = _unique_edges(g.n, g.edges)
     e = e[e[:, 0] != e[:, 1]]
     a = np.concatenate([e[:, 0], e[:, 1]])
     b = np.concatenate([e[:, 1], e[:, 0]])
@@ -316,7 +327,7 @@ def test_config2_low_degree_core_full_matrix(pkg):
     """the config-2 subgraph induced by its vertices of degree <= 12: same generator and
     degree tail cut, small enough for the full ESU oracle at n = 1e5"""
     g = graphgen.config(2)
-    e = np.unique(np.sort(g.edges.astype(np.int64), axis=1), axis=0)
+    e = _unique_edges(g.n, g.edges)
     e = e[e[:, 0] != e[:, 1]]
     deg = np.bincount(e.ravel(), minlength=g.n)
     keep = deg <= 12
@@ -353,7 +364,7 @@ def test_config4_invariants_and_low_degree_core(pkg):
     out = pkg.evoke_orbits_edges(g.n, g.edges)
     _invariants(g, out, cliques=_golden_cliques(4, g))
     del out
-    e = np.unique(np.sort(g.edges.astype(np.int64), axis=1), axis=0)
+    e = _unique_edges(g.n, g.edges)
     e = e[e[:, 0] != e[:, 1]]
     deg = np.bincount(e.ravel(), minlength=g.n)
     keep = deg <= 11
@@ -515,9 +526,18 @@ def test_config5_invariants(pkg):
     """R-MAT 23 (BASELINE configs[4], ~65M edges, the 8-GPU config) on one B200: orbit 0 =
     degree, per-pattern consistency mod 2^64, Sigma DIM3 = 3 #K3,
     Sigma DIM14 = 4 #K4 and Sigma DIM72 = 5 #K5 (golden totals from the oracle's bitmap
-    clique counter), and the rooted oracle's rows for sampled cheap roots"""
+    clique counter), the rooted oracle's rows for sampled cheap roots, and in non-induced
+    mode the degree-only closed forms on every vertex"""
     g = graphgen.config(5)
     out = pkg.evoke_orbits_edges(g.n, g.edges)
     _invariants(g, out, cliques=_golden_cliques(5, g))
     done = _sampled_rows(g, out, 40, 5, cap=5_000_000)
     assert done >= 3, done
+    del out
+    # non-induced mode: the degree-only closed forms on every vertex, the hubs included
+    # (as test_noninduced_degree_forms_every_vertex does for configs 2-4)
+    out = pkg.evoke_orbits_edges(g.n, g.edges, induced=False)
+    f = degree_forms(g.n, g.edges)
+    for c in DEGREE_FORM_COLUMNS:
+        bad = np.flatnonzero(out[:, c] != f[c])
+        assert bad.size == 0, f"config 5 theta{c}: {bad.size} rows differ, first {bad[:5].tolist()}"
