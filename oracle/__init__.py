@@ -50,6 +50,7 @@ def _load():
             lib.oracle_noninduced_bruteforce.argtypes = [i64, i64, i32p, u64p]
             lib.oracle_clique_totals.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_clique_totals_bits.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
+            lib.oracle_clique_counts_vertex.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_pattern.argtypes = [ctypes.c_int, ip, ip, ip, ip]
             lib.oracle_automorphism_classes.argtypes = [ctypes.c_int, ip, ip]
             lib.oracle_classify.argtypes = [ctypes.c_int, ctypes.c_int, ip]
@@ -138,6 +139,19 @@ def clique_totals_bits(n: int, edges, threads: int = 0, kmax: int = 5):
                                      int(kmax)):
         raise RuntimeError("oracle_clique_totals_bits failed")
     return int(c[0]), (int(c[1]) if kmax >= 4 else None), (int(c[2]) if kmax >= 5 else None)
+
+
+
+def clique_counts_vertex(n: int, edges, threads: int = 0, kmax: int = 5) -> np.ndarray:
+    """uint64[n, 3]: the triangles / 4-cliques / 5-cliques containing each vertex (= columns
+    3 / 14 / 72 of the orbit matrix, induced or not); columns beyond ``kmax`` stay 0."""
+    lib = _load()
+    e = _edges(edges)
+    out = np.zeros((n, 3), dtype=np.uint64)
+    if lib.oracle_clique_counts_vertex(n, e.shape[0], _ptr(e, ctypes.c_int32), _ptr(out, ctypes.c_uint64),
+                                       threads, int(kmax)):
+        raise RuntimeError("oracle_clique_counts_vertex failed")
+    return out
 
 
 def catalog():

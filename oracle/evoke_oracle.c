@@ -712,3 +712,121 @@ int oracle_clique_totals_bits(int64_t n, int64_t m, const int32_t *edges, uint64
   graph_free(&g);
   return fail ? -1 : 0;
 }
+
+/* Per-vertex clique counts: out[v*3 + 0] = #triangles, + 1 = #4-cliques, + 2 = #5-cliques
+ * that contain v (cliques = P:702 / P:861-864).  A clique is an induced copy of itself and
+ * all its vertices are one orbit, so these are three columns of the orbit matrix by their
+ * definition: DIM(v, theta3) = DM(v, theta3) = T(v), DIM(v, theta14) = K4(v),
+ * DIM(v, theta72) = K5(v) -- exact on every vertex, hubs included, at sizes the ESU cannot
+ * reach (used by the GPU tests on the full configs).
+ * Enumeration exactly as in oracle_clique_totals_bits (each clique found once, from its
+ * first vertex a in the degree order of P:432-437 and its members of increasing position
+ * in L = N>(a), membership on the local bitmap); here every clique found adds 1 to each of
+ * its members instead of 1 to a total.  Members shared by all the cliques of an inner loop
+ * get that loop's count in one addition; the last member is credited bit by bit.
+ * Counts wrap modulo 2^64 (reading R20).  kmax as above (columns beyond kmax stay 0).
+ * Pinned in tests/test_oracle_pins.py against the ESU columns 3/14/72, the all-subsets
+ * brute force, K_n and the totals (sum_v = k * #K_k). */
+int oracle_clique_counts_vertex(int64_t n, int64_t m, const int32_t *edges, uint64_t *out, int threads,
+                                int kmax) {
+  graph_t g;
+  if (graph_build(&g, n, m, edges)) return -1;
+  int64_t *key = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t *rank = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t *orp = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  int32_t *oadj = (int32_t *)malloc(sizeof(int32_t) * (size_t)(g.rp[n] / 2 + 1));
+  if (!key || !rank || !orp || !oadj) { free(key); free(rank); free(orp); free(oadj); graph_free(&g); return -1; }
+  for (int64_t v = 0; v < n; v++) key[v] = ((g.rp[v + 1] - g.rp[v]) << 32) | v;
+  qsort(key, (size_t)n, sizeof(int64_t), cmp_u64);
+  for (int64_t r = 0; r < n; r++) rank[key[r] & 0xffffffffLL] = r;
+  free(key);
+  int64_t kmax_list = 0;
+  for (int64_t a = 0; a < n; a++) {
+    orp[a + 1] = orp[a];
+    for (int64_t p = g.rp[a]; p < g.rp[a + 1]; p++)
+      if (rank[g.adj[p]] > rank[a]) oadj[orp[a + 1]++] = g.adj[p];
+    if (orp[a + 1] - orp[a] > kmax_list) kmax_list = orp[a + 1] - orp[a];
+  }
+  g_ord_rank = rank;
+  for (int64_t a = 0; a < n; a++) qsort(oadj + orp[a], (size_t)(orp[a + 1] - orp[a]), sizeof(int32_t), cmp_by_rank);
+  memset(out, 0, sizeof(uint64_t) * (size_t)n * 3);
+  int fail = 0;
+  const int64_t W = (kmax_list + 63) / 64;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+#pragma omp parallel reduction(|:fail)
+  {
+    int32_t *pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    uint64_t *row = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(kmax_list * W + 1));
+    uint64_t *c2 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(W + 1));
+    uint64_t *loc = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(kmax_list * 3 + 3));  /* credits of L[i] */
+    const int ok = pos && row && c2 && loc;
+    if (ok) for (int64_t v = 0; v < n; v++) pos[v] = -1;
+    {
+#pragma omp for schedule(dynamic, 16)
+      for (int64_t a = 0; a < n; a++) {
+        if (!ok) { fail = 1; continue; }
+        const int32_t *L = oadj + orp[a];
+        const int64_t k = orp[a + 1] - orp[a], w = (k + 63) / 64;
+        if (k < 2) continue;
+        for (int64_t i = 0; i < k; i++) pos[L[i]] = (int32_t)i;
+        memset(row, 0, sizeof(uint64_t) * (size_t)(k * w));
+        memset(loc, 0, sizeof(uint64_t) * (size_t)(k * 3));
+        for (int64_t i = 0; i < k; i++)
+          for (int64_t p = orp[L[i]]; p < orp[L[i] + 1]; p++) {
+            int32_t j = pos[oadj[p]];
+            if (j >= 0) row[i * w + j / 64] |= 1ULL << (j % 64);
+          }
+        uint64_t a3 = 0, a4 = 0, a5 = 0;  /* cliques found at a: a is a member of each */
+        for (int64_t i = 0; i < k; i++) {
+          const uint64_t *ri = row + i * w;
+          for (int64_t q = 0; q < w; q++)
+            for (uint64_t bits = ri[q]; bits; bits &= bits - 1) {
+              const int64_t j = q * 64 + __builtin_ctzll(bits);
+              /* triangle {a, L[i], L[j]} */
+              a3++; loc[i * 3]++; loc[j * 3]++;
+              if (kmax < 4) continue;
+              const uint64_t *rj = row + j * w;
+              for (int64_t s = 0; s < w; s++) c2[s] = ri[s] & rj[s];
+              for (int64_t s = 0; s < w; s++)
+                for (uint64_t b2 = c2[s]; b2; b2 &= b2 - 1) {
+                  const int64_t l = s * 64 + __builtin_ctzll(b2);
+                  /* 4-clique {a, L[i], L[j], L[l]} */
+                  a4++; loc[i * 3 + 1]++; loc[j * 3 + 1]++; loc[l * 3 + 1]++;
+                  if (kmax < 5) continue;
+                  const uint64_t *rl = row + l * w;
+                  for (int64_t u = 0; u < w; u++)
+                    for (uint64_t b3 = c2[u] & rl[u]; b3; b3 &= b3 - 1) {
+                      const int64_t p5 = u * 64 + __builtin_ctzll(b3);
+                      /* 5-clique {a, L[i], L[j], L[l], L[p5]} */
+                      a5++; loc[i * 3 + 2]++; loc[j * 3 + 2]++; loc[l * 3 + 2]++; loc[p5 * 3 + 2]++;
+                    }
+                }
+            }
+        }
+        for (int c = 0; c < 3; c++) {
+          const uint64_t av = c == 0 ? a3 : c == 1 ? a4 : a5;
+          if (av) {
+#pragma omp atomic
+            out[a * 3 + c] += av;
+          }
+        }
+        for (int64_t i = 0; i < k; i++) {
+          for (int c = 0; c < 3; c++)
+            if (loc[i * 3 + c]) {
+#pragma omp atomic
+              out[(int64_t)L[i] * 3 + c] += loc[i * 3 + c];
+            }
+          pos[L[i]] = -1;
+        }
+      }
+    }
+    free(pos); free(row); free(c2); free(loc);
+  }
+  free(rank); free(orp); free(oadj);
+  graph_free(&g);
+  return fail ? -1 : 0;
+}

@@ -456,6 +456,26 @@ def test_noninduced_degree_forms_every_vertex(pkg, cfg):
         assert bad.size == 0, f"config {cfg} theta{c}: {bad.size} rows differ, first {bad[:5].tolist()}"
 
 
+# ------------------------------------------------ clique columns on every vertex ---
+def _clique_columns(cfg, g, out, kmax):
+    """columns 3 / 14 / 72 of the induced matrix against the oracle's per-vertex clique counts
+    (oracle.clique_counts_vertex: a clique is an induced copy of itself, so DIM(v, theta3) =
+    T(v), DIM(v, theta14) = K4(v), DIM(v, theta72) = K5(v); P:139-142, P:702, P:861-864)"""
+    ref = oracle.clique_counts_vertex(g.n, g.edges, kmax=kmax)
+    for j, c in enumerate((3, 14, 72)[:kmax - 2]):
+        bad = np.flatnonzero(out[:, c] != ref[:, j])
+        assert bad.size == 0, f"config {cfg} theta{c}: {bad.size} rows differ, first {bad[:5].tolist()}"
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_clique_columns_every_vertex(pkg, cfg):
+    """induced mode: the triangle, 4-clique and 5-clique orbits (theta3, theta14, theta72)
+    bit-exact on EVERY vertex of the config, hub rows included, against an enumeration that
+    shares nothing with the CUDA path (pinned in tests/test_oracle_pins.py)"""
+    g = graphgen.config(cfg)
+    _clique_columns(cfg, g, pkg.evoke_orbits_edges(g.n, g.edges), 5)
+
+
 # ------------------------------------------------------- work-balanced sharding ---
 @pytest.mark.parametrize("cfg", [2, 3])
 def test_eight_shards_sum_to_full_and_balance(pkg, cfg):
@@ -533,6 +553,8 @@ def test_config5_invariants(pkg):
     _invariants(g, out, cliques=_golden_cliques(5, g))
     done = _sampled_rows(g, out, 40, 5, cap=5_000_000)
     assert done >= 3, done
+    # theta3 and theta14 on every vertex (the 1.1e12 5-cliques are left to the total above)
+    _clique_columns(5, g, out, 4)
     del out
     # non-induced mode: the degree-only closed forms on every vertex, the hubs included
     # (as test_noninduced_degree_forms_every_vertex does for configs 2-4)

@@ -430,6 +430,75 @@ def test_clique_totals_bits_complete_multipartite_and_kmax():
         assert oracle.clique_totals_bits(int(offs[-1]), e, kmax=4) == (ek[0], ek[1], None)
 
 
+# oracle.clique_counts_vertex: T(v), K4(v), K5(v) on every vertex = columns 3 / 14 / 72 of the
+# orbit matrix (a clique is an induced copy of itself), the
+# per-vertex check the GPU tests apply to the hub rows of the full configs
+def _cliques_per_vertex_by_subsets(n, edges):
+    adj = [set() for _ in range(n)]
+    for a, b in edges:
+        if a != b:
+            adj[a].add(b)
+            adj[b].add(a)
+    out = np.zeros((n, 3), dtype=np.uint64)
+    for c, k in enumerate((3, 4, 5)):
+        for S in itertools.combinations(range(n), k):
+            if all(y in adj[x] for x, y in itertools.combinations(S, 2)):
+                for v in S:
+                    out[v, c] += np.uint64(1)
+    return out
+
+
+def test_clique_counts_vertex_vs_all_subsets():
+    rng = random.Random(76)
+    for _ in range(60):
+        n, e = rand_graph(rng, 3, 14, 0.2, 0.95)
+        assert (oracle.clique_counts_vertex(n, e) == _cliques_per_vertex_by_subsets(n, e)).all(), (n, e)
+
+
+def test_clique_counts_vertex_vs_esu_columns():
+    """columns 3 / 14 / 72 of the ESU matrix (pinned to brute force above) on dense graphs and
+    on graphs whose N>(a) bitmaps have rows of several words; sums = k * totals"""
+    rng = random.Random(77)
+    graphs = [rand_graph(rng, 15, 32, 0.45, 0.92) for _ in range(20)]
+    graphs += [(g.n, g.edges) for g in (graphgen.erdos_renyi(100, 0.45, 801), graphgen.erdos_renyi(70, 0.8, 802),
+                                        graphgen.config(1))]
+    for n, e in graphs:
+        dim = oracle.orbits(n, e)
+        got = oracle.clique_counts_vertex(n, e)
+        assert (got[:, 0] == dim[:, 3]).all() and (got[:, 1] == dim[:, 14]).all() and (got[:, 2] == dim[:, 72]).all()
+        t3, t4, t5 = oracle.clique_totals(n, e)
+        assert [int(x) for x in got.astype(object).sum(axis=0)] == [3 * t3, 4 * t4, 5 * t5]
+
+
+@pytest.mark.parametrize("n", [3, 5, 17, 64, 65, 66, 130])
+def test_clique_counts_vertex_complete_graph_and_kmax(n):
+    e = graphgen.complete(n).edges
+    exp = np.array([C(n - 1, 2), C(n - 1, 3), C(n - 1, 4)], dtype=np.uint64)  # P: every vertex of K_n
+    assert (oracle.clique_counts_vertex(n, e) == exp).all()
+    got = oracle.clique_counts_vertex(n, e, kmax=4)
+    assert (got[:, :2] == exp[:2]).all() and (got[:, 2] == 0).all()
+    got = oracle.clique_counts_vertex(n, e, kmax=3)
+    assert (got[:, 0] == exp[0]).all() and (got[:, 1:] == 0).all()
+
+
+def test_clique_counts_vertex_star_of_cliques():
+    """a hub joined to every vertex of several disjoint cliques K_s: the hub is in sum C(s,k-1)
+    k-cliques, a clique vertex in C(s-1,k-1) + C(s-1,k-2) (asymmetric roles, so a credit given
+    to the wrong member shows)"""
+    sizes = (3, 4, 6, 9)
+    e, off = [], 1
+    for s in sizes:
+        e += [(off + i, off + j) for i in range(s) for j in range(i + 1, s)] + [(0, off + i) for i in range(s)]
+        off += s
+    got = oracle.clique_counts_vertex(off, e)
+    assert got[0].tolist() == [sum(C(s, k - 1) for s in sizes) for k in (3, 4, 5)]
+    off = 1
+    for s in sizes:
+        for i in range(s):
+            assert got[off + i].tolist() == [C(s - 1, k - 1) + C(s - 1, k - 2) for k in (3, 4, 5)], (s, i)
+        off += s
+
+
 def test_degree_forms_vs_noninduced_bruteforce():
     """the degree-only closed forms the GPU tests apply to every vertex of configs 2-4
     (tests/degree_forms.py) equal the non-induced brute force on random graphs"""
