@@ -51,6 +51,7 @@ def _load():
             lib.oracle_clique_totals.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_clique_totals_bits.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_clique_counts_vertex.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
+            lib.oracle_dm4_vertex.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_pattern.argtypes = [ctypes.c_int, ip, ip, ip, ip]
             lib.oracle_automorphism_classes.argtypes = [ctypes.c_int, ip, ip]
             lib.oracle_classify.argtypes = [ctypes.c_int, ctypes.c_int, ip]
@@ -151,6 +152,23 @@ def clique_counts_vertex(n: int, edges, threads: int = 0, kmax: int = 5) -> np.n
     if lib.oracle_clique_counts_vertex(n, e.shape[0], _ptr(e, ctypes.c_int32), _ptr(out, ctypes.c_uint64),
                                        threads, int(kmax)):
         raise RuntimeError("oracle_clique_counts_vertex failed")
+    return out
+
+
+
+def dm4_vertex(n: int, edges, threads: int = 0, with_c4: bool = True, with_k4: bool = True) -> np.ndarray:
+    """uint64[n, 15]: the NON-induced counts DM(v, theta_0..14) of the orbits with at most 4
+    vertices on every vertex, by Lemma 4vertexorbit from plain definitions of its
+    inputs; theta_14 = K4(v) from ``clique_counts_vertex``.  Columns skipped by the flags
+    (theta_8 / theta_14) stay 0."""
+    lib = _load()
+    e = _edges(edges)
+    out = np.zeros((n, 15), dtype=np.uint64)
+    if lib.oracle_dm4_vertex(n, e.shape[0], _ptr(e, ctypes.c_int32), _ptr(out, ctypes.c_uint64), threads,
+                             int(bool(with_c4))):
+        raise RuntimeError("oracle_dm4_vertex failed")
+    if with_k4:
+        out[:, 14] = clique_counts_vertex(n, e, threads=threads, kmax=4)[:, 1]
     return out
 
 

@@ -830,3 +830,121 @@ int oracle_clique_counts_vertex(int64_t n, int64_t m, const int32_t *edges, uint
   graph_free(&g);
   return fail ? -1 : 0;
 }
+
+/* Non-induced counts DM(u, theta_0..13) of the orbits with at most 4 vertices on EVERY
+ * vertex, by Lemma "4vertexorbit" read line by line, from the plain
+ * definitions of its inputs: d(u); T(u,v) = |N(u) & N(v)| for every edge (a merge
+ * of the two sorted lists); T(u) = (1/2) sum_{v in N(u)} T(u,v); C4(u) = sum_{x != u}
+ * C(c(u,x), 2), c(u,x) = #common neighbours = #wedges u-w-x (a 4-cycle through u is its
+ * opposite vertex x and two of their common neighbours).  K4(u) (theta_14) is
+ * oracle_clique_counts_vertex's column 1 and is not computed here.
+ * out[u*15 + i] = DM(u, theta_i), i = 0..13 (slot 14 left 0), wrapping modulo 2^64
+ * (reading R20).  with_c4 = 0 skips theta_8 (left 0): its wedge walk is O(sum d^2).
+ * These are the NON-induced counts of Def. "unlabeled-match": the GPU tests
+ * compare them with the non-induced mode of the product on every vertex of the
+ * full configs, hub rows included.  Pinned against oracle_noninduced_bruteforce on random
+ * graphs and against K_n / K_{a,b} closed forms in tests/test_oracle_pins.py. */
+static uint64_t binom_u64(uint64_t x, int k) {  /* C(x, k) mod 2^64, k <= 3, via 128-bit products */
+  if (x < (uint64_t)k) return 0;
+  unsigned __int128 r = 1;
+  for (int i = 0; i < k; i++) r *= (unsigned __int128)(x - (uint64_t)i);
+  for (int i = 2; i <= k; i++) r /= (unsigned)i;  /* x < 2^40: the product is exact in 128 bits */
+  return (uint64_t)r;
+}
+
+int oracle_dm4_vertex(int64_t n, int64_t m, const int32_t *edges, uint64_t *out, int threads, int with_c4) {
+  graph_t g;
+  if (graph_build(&g, n, m, edges)) return -1;
+  const int64_t M2 = g.rp[n];
+  uint32_t *te = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(M2 + 1));  /* T(u,v) per list slot */
+  uint64_t *T = (uint64_t *)calloc((size_t)n + 1, sizeof(uint64_t));
+  uint64_t *dm1 = (uint64_t *)calloc((size_t)n + 1, sizeof(uint64_t));
+  if (!te || !T || !dm1) { free(te); free(T); free(dm1); graph_free(&g); return -1; }
+  memset(out, 0, sizeof(uint64_t) * (size_t)n * 15);
+  int fail = 0;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+  /* T(u,v) for every edge, both directions; T(u); DM(u, theta_1) */
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t u = 0; u < n; u++) {
+    uint64_t tu = 0, s1 = 0;
+    for (int64_t p = g.rp[u]; p < g.rp[u + 1]; p++) {
+      const int v = g.adj[p];
+      int64_t a = g.rp[u], b = g.rp[v];
+      uint32_t c = 0;
+      while (a < g.rp[u + 1] && b < g.rp[v + 1]) {
+        if (g.adj[a] < g.adj[b]) a++;
+        else if (g.adj[a] > g.adj[b]) b++;
+        else { c++; a++; b++; }
+      }
+      te[p] = c;
+      tu += c;
+      s1 += (uint64_t)(g.rp[v + 1] - g.rp[v]) - 1;
+    }
+    T[u] = tu / 2;
+    dm1[u] = s1;
+  }
+#pragma omp parallel reduction(|:fail)
+  {
+    uint32_t *cnt = with_c4 ? (uint32_t *)calloc((size_t)n + 1, sizeof(uint32_t)) : NULL;
+    int32_t *touched = with_c4 ? (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1)) : NULL;
+    const int ok = !with_c4 || (cnt && touched);
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t u = 0; u < n; u++) {
+      if (!ok) { fail = 1; continue; }
+      uint64_t *o = out + u * 15;
+      const uint64_t d = (uint64_t)(g.rp[u + 1] - g.rp[u]);
+      uint64_t s4 = 0, s6 = 0, s9 = 0, s10 = 0, s12 = 0, s13 = 0;
+      for (int64_t p = g.rp[u]; p < g.rp[u + 1]; p++) {
+        const int v = g.adj[p];
+        const uint64_t dv = (uint64_t)(g.rp[v + 1] - g.rp[v]), tuv = te[p];
+        s4 += dm1[v];
+        s6 += binom_u64(dv - 1, 2);
+        s9 += T[v] - tuv;
+        s10 += tuv * (dv - 2);
+        s13 += binom_u64(tuv, 2);
+        /* triangles t = (u, v, x) with v < x: x in N(u) & N(v); add T(v,x) - 1 */
+        int64_t a = g.rp[u], b = g.rp[v];
+        while (a < g.rp[u + 1] && b < g.rp[v + 1]) {
+          if (g.adj[a] < g.adj[b]) a++;
+          else if (g.adj[a] > g.adj[b]) b++;
+          else { if (g.adj[b] > v) s12 += (uint64_t)te[b] - 1; a++; b++; }  /* slot b = x in N(v) */
+        }
+      }
+      o[0] = d;
+      o[1] = dm1[u];
+      o[2] = binom_u64(d, 2);
+      o[3] = T[u];
+      o[4] = s4 - 2 * o[2] - 2 * o[3];
+      o[5] = o[1] * (d - 1) - 2 * o[3];
+      o[6] = s6;
+      o[7] = binom_u64(d, 3);
+      o[9] = s9;
+      o[10] = s10;
+      o[11] = o[3] * (d - 2);
+      o[12] = s12;
+      o[13] = s13;
+      if (with_c4) {
+        int64_t nt = 0;
+        for (int64_t p = g.rp[u]; p < g.rp[u + 1]; p++) {
+          const int w = g.adj[p];
+          for (int64_t q = g.rp[w]; q < g.rp[w + 1]; q++) {
+            const int x = g.adj[q];
+            if (x == u) continue;
+            if (cnt[x]++ == 0) touched[nt++] = x;
+          }
+        }
+        uint64_t c4 = 0;
+        for (int64_t i = 0; i < nt; i++) { c4 += binom_u64(cnt[touched[i]], 2); cnt[touched[i]] = 0; }
+        o[8] = c4;
+      }
+    }
+    free(cnt); free(touched);
+  }
+  free(te); free(T); free(dm1);
+  graph_free(&g);
+  return fail ? -1 : 0;
+}

@@ -456,6 +456,21 @@ def test_noninduced_degree_forms_every_vertex(pkg, cfg):
         assert bad.size == 0, f"config {cfg} theta{c}: {bad.size} rows differ, first {bad[:5].tolist()}"
 
 
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_noninduced_four_vertex_orbits_every_vertex(pkg, cfg):
+    """non-induced mode: ALL fifteen orbits with at most 4 vertices
+    (theta0..theta14: wedges, triangles, 3-paths, 4-cycles, tailed triangles, diamonds,
+    4-cliques) bit-exact on EVERY vertex of the config, hub rows included, against the
+    oracle's Lemma-4vertexorbit counter (oracle.dm4_vertex: the paper's equations
+    on plain definitions of T(u,v) and C4(u), pinned against the non-induced brute force)"""
+    g = graphgen.config(cfg)
+    out = pkg.evoke_orbits_edges(g.n, g.edges, induced=False)
+    ref = oracle.dm4_vertex(g.n, g.edges)
+    for c in range(15):
+        bad = np.flatnonzero(out[:, c] != ref[:, c])
+        assert bad.size == 0, f"config {cfg} theta{c}: {bad.size} rows differ, first {bad[:5].tolist()}"
+
+
 # ------------------------------------------------ clique columns on every vertex ---
 def _clique_columns(cfg, g, out, kmax):
     """columns 3 / 14 / 72 of the induced matrix against the oracle's per-vertex clique counts

@@ -499,6 +499,50 @@ def test_clique_counts_vertex_star_of_cliques():
         off += s
 
 
+# oracle.dm4_vertex: Lemma 4vertexorbit on every vertex from plain definitions of
+# d, T(u,v), T(u), C4(u) -- the non-induced columns 0..14 the GPU tests check on the hub rows
+def test_dm4_vertex_vs_noninduced_bruteforce():
+    rng = random.Random(78)
+    for _ in range(80):
+        n, e = rand_graph(rng, 2, 10, 0.15, 0.95)
+        assert (oracle.dm4_vertex(n, e) == oracle.noninduced_bruteforce(n, e)[:, :15]).all(), (n, e)
+
+
+def test_dm4_vertex_is_transform_of_esu_on_larger_graphs():
+    """DM = A . DIM restricted to the 4-vertex orbits, A = the brute-force
+    transform pinned to Fig. 11: on graphs past brute-force size the lemma's columns must equal
+    the ESU's induced counts pushed through A"""
+    mats = [(lo, hi, _A_block(lo, hi).astype(object)) for lo, hi in [(0, 0), (1, 3), (4, 14)]]
+    for g in (graphgen.erdos_renyi(60, 0.3, 811), graphgen.erdos_renyi(200, 0.06, 812), graphgen.config(1)):
+        dim = oracle.orbits(g.n, g.edges).astype(object)
+        got = oracle.dm4_vertex(g.n, g.edges).astype(object)
+        for lo, hi, A in mats:
+            assert (A.dot(dim[:, lo:hi + 1].T).T == got[:, lo:hi + 1]).all(), (g.name, lo)
+
+
+@pytest.mark.parametrize("n", [4, 5, 9, 40])
+def test_dm4_vertex_complete_graph(n):
+    d = n - 1
+    exp = [d, d * (d - 1), C(d, 2), C(d, 2), d * (d - 1) * (d - 2), d * (d - 1) * (d - 2), d * C(d - 1, 2), C(d, 3),
+           3 * C(d, 3), d * (d - 1) * (d - 2) // 2, d * (d - 1) * (d - 2), C(d, 2) * (d - 2), C(d, 2) * (n - 3),
+           d * C(n - 2, 2), C(d, 3)]
+    got = oracle.dm4_vertex(n, graphgen.complete(n).edges)
+    assert (got == np.array(exp, dtype=np.uint64)).all(), (got[0].tolist(), exp)
+
+
+def test_dm4_vertex_complete_bipartite_and_flags():
+    a, b = 9, 700
+    e = [(i, a + j) for i in range(a) for j in range(b)]
+    got = oracle.dm4_vertex(a + b, e)
+    # no triangles; a 4-cycle through v = another vertex of its side and two of the other side
+    assert (got[:, [3, 9, 10, 11, 12, 13, 14]] == 0).all()
+    assert (got[:a, 8] == (a - 1) * C(b, 2)).all() and (got[a:, 8] == (b - 1) * C(a, 2)).all()
+    assert (got[:a, 0] == b).all() and (got[:a, 1] == b * (a - 1)).all() and (got[:a, 7] == C(b, 3)).all()
+    assert (got[:a, 4] == b * (a - 1) * (b - 1)).all() and (got[:a, 5] == b * (a - 1) * (b - 1)).all()
+    off = oracle.dm4_vertex(a + b, e, with_c4=False, with_k4=False)
+    assert (off[:, 8] == 0).all() and (np.delete(off, 8, axis=1) == np.delete(got, 8, axis=1)).all()
+
+
 def test_degree_forms_vs_noninduced_bruteforce():
     """the degree-only closed forms the GPU tests apply to every vertex of configs 2-4
     (tests/degree_forms.py) equal the non-induced brute force on random graphs"""
