@@ -52,6 +52,8 @@ def _load():
             lib.oracle_clique_totals_bits.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_clique_counts_vertex.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
             lib.oracle_dm4_vertex.argtypes = [i64, i64, i32p, u64p, ctypes.c_int, ctypes.c_int]
+            lib.oracle_c5_rows.argtypes = [i64, i64, i32p, i64, ctypes.POINTER(ctypes.c_int64), u64p, ip,
+                                           ctypes.c_uint64, ctypes.c_int]
             lib.oracle_pattern.argtypes = [ctypes.c_int, ip, ip, ip, ip]
             lib.oracle_automorphism_classes.argtypes = [ctypes.c_int, ip, ip]
             lib.oracle_classify.argtypes = [ctypes.c_int, ctypes.c_int, ip]
@@ -170,6 +172,22 @@ def dm4_vertex(n: int, edges, threads: int = 0, with_c4: bool = True, with_k4: b
     if with_k4:
         out[:, 14] = clique_counts_vertex(n, e, threads=threads, kmax=4)[:, 1]
     return out
+
+
+
+def c5_rows(n: int, edges, roots, cap: int = 0, threads: int = 0):
+    """(counts uint64[len(roots)], status int32[len(roots)]): the number of (non-induced)
+    5-cycles through each root = DM(root, theta_34), from the definition; status 1 = abandoned
+    after ``cap`` innermost steps."""
+    lib = _load()
+    e = _edges(edges)
+    r = np.ascontiguousarray(np.asarray(roots, dtype=np.int64).reshape(-1))
+    out = np.zeros(r.size, dtype=np.uint64)
+    st = np.zeros(r.size, dtype=np.int32)
+    if lib.oracle_c5_rows(n, e.shape[0], _ptr(e, ctypes.c_int32), r.size, _ptr(r, ctypes.c_int64),
+                          _ptr(out, ctypes.c_uint64), _ptr(st, ctypes.c_int), int(cap), threads):
+        raise RuntimeError("oracle_c5_rows failed")
+    return out, st
 
 
 def catalog():

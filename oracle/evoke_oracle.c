@@ -948,3 +948,57 @@ int oracle_dm4_vertex(int64_t n, int64_t m, const int32_t *edges, uint64_t *out,
   graph_free(&g);
   return fail ? -1 : 0;
 }
+
+/* Non-induced 5-cycle count of chosen vertices: out[r] = DM(roots[r], theta_34) = the number
+ * of 5-cycles of G through v = roots[r] (the 5-cycle pattern has one orbit, theta_34: "each
+ * vertex of the Petersen graph is in 6 five-cycles"; Def. "unlabeled-match" P:419-422),
+ * straight from the definition: a 5-cycle through v is v-a-x-y-b-v with five distinct
+ * vertices and the five edges present; each is met twice (once per direction), so the
+ * number of such (a, x, y, b) is halved.  The walk is O(#4-paths from v) -- cheap for a hub
+ * of a sparse graph, where the rooted ESU (all connected 5-sets around the hub) is not.
+ * status[r] = 0 done, 1 abandoned after `cap` innermost steps (cap = 0: no cap).
+ * Pinned against oracle_noninduced_bruteforce column 34 and K_n / C_5 / Petersen closed
+ * forms in tests/test_oracle_pins.py. */
+int oracle_c5_rows(int64_t n, int64_t m, const int32_t *edges, int64_t nroots, const int64_t *roots,
+                   uint64_t *out, int *status, uint64_t cap, int threads) {
+  graph_t g;
+  if (graph_build(&g, n, m, edges)) return -1;
+  unsigned char *nv = (unsigned char *)calloc((size_t)n + 1, 1);  /* nv[b] = 1 iff b ~ v */
+  if (!nv) { graph_free(&g); return -1; }
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+  for (int64_t r = 0; r < nroots; r++) {
+    const int64_t v = roots[r];
+    if (v < 0 || v >= n) { free(nv); graph_free(&g); return -1; }
+    for (int64_t p = g.rp[v]; p < g.rp[v + 1]; p++) nv[g.adj[p]] = 1;
+    uint64_t cnt = 0, steps = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+:cnt, steps)
+    for (int64_t pa = g.rp[v]; pa < g.rp[v + 1]; pa++) {
+      const int a = g.adj[pa];
+      for (int64_t px = g.rp[a]; px < g.rp[a + 1]; px++) {
+        const int x = g.adj[px];
+        if (x == v) continue;
+        if (cap && steps > cap) break;  /* this thread's share alone is past the cap */
+        for (int64_t py = g.rp[x]; py < g.rp[x + 1]; py++) {
+          const int y = g.adj[py];
+          if (y == v || y == a) continue;
+          steps += (uint64_t)(g.rp[y + 1] - g.rp[y]);
+          for (int64_t pb = g.rp[y]; pb < g.rp[y + 1]; pb++) {
+            const int b = g.adj[pb];
+            if (b == v || b == a || b == x) continue;
+            cnt += nv[b];
+          }
+        }
+      }
+    }
+    for (int64_t p = g.rp[v]; p < g.rp[v + 1]; p++) nv[g.adj[p]] = 0;
+    status[r] = (cap && steps > cap) ? 1 : 0;
+    out[r] = status[r] ? 0 : cnt / 2;
+  }
+  free(nv);
+  graph_free(&g);
+  return 0;
+}

@@ -471,6 +471,25 @@ def test_noninduced_four_vertex_orbits_every_vertex(pkg, cfg):
         assert bad.size == 0, f"config {cfg} theta{c}: {bad.size} rows differ, first {bad[:5].tolist()}"
 
 
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_noninduced_five_cycles_at_the_hubs(pkg, cfg):
+    """non-induced theta34 (the 5-cycles through a vertex, the 5-cycle pass's own output) on
+    the 12 highest-degree vertices of the config and 40 drawn uniformly, against the oracle's
+    definition walk (oracle.c5_rows: O(#4-paths from v), feasible at hubs of these sparse
+    graphs where the rooted ESU is not; on the R-MAT configs every 4-path walk runs through
+    the 6e4-degree hub and none finishes)"""
+    g = graphgen.config(cfg)
+    out = pkg.evoke_orbits_edges(g.n, g.edges, induced=False)
+    deg = np.bincount(g.edges.ravel(), minlength=g.n)
+    rng = np.random.default_rng(40 + cfg)
+    roots = np.unique(np.concatenate([np.argsort(-deg, kind="stable")[:12], rng.choice(g.n, 40, replace=False)]))
+    ref, st = oracle.c5_rows(g.n, g.edges, roots, cap=50_000_000_000)
+    assert (st == 0).sum() >= 40, st.tolist()
+    for r, c, s_ in zip(roots, ref, st):
+        if s_ == 0:
+            assert out[r, 34] == c, f"config {cfg} vertex {r} (degree {deg[r]}): got {out[r, 34]} exp {c}"
+
+
 # ------------------------------------------------ clique columns on every vertex ---
 def _clique_columns(cfg, g, out, kmax):
     """columns 3 / 14 / 72 of the induced matrix against the oracle's per-vertex clique counts

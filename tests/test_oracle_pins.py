@@ -543,6 +543,39 @@ def test_dm4_vertex_complete_bipartite_and_flags():
     assert (off[:, 8] == 0).all() and (np.delete(off, 8, axis=1) == np.delete(got, 8, axis=1)).all()
 
 
+# oracle.c5_rows: the 5-cycles through chosen vertices (non-induced theta34) from the
+# definition -- what the GPU tests compare the hub rows of configs 2 and 4 with
+def test_c5_rows_vs_noninduced_bruteforce_and_closed_forms():
+    rng = random.Random(79)
+    for _ in range(60):
+        n, e = rand_graph(rng, 3, 10, 0.2, 0.95)
+        got, st = oracle.c5_rows(n, e, range(n))
+        assert (st == 0).all() and (got == oracle.noninduced_bruteforce(n, e)[:, 34]).all(), (n, e)
+    for n in (5, 6, 9, 30):  # K_n: choose the 4 others, 4!/2 cyclic orders
+        got, _ = oracle.c5_rows(n, graphgen.complete(n).edges, range(n))
+        assert (got == C(n - 1, 4) * 12).all()
+    got, _ = oracle.c5_rows(10, graphgen.petersen().edges, range(10))
+    assert (got == 6).all()  # P: each vertex of the Petersen graph is in 6 five-cycles (theta34 = 6)
+    got, _ = oracle.c5_rows(12, graphgen.cycle(12).edges, range(12))
+    assert (got == 0).all()
+    got, _ = oracle.c5_rows(5, graphgen.cycle(5).edges, range(5))
+    assert (got == 1).all()
+
+
+def test_c5_rows_cap_and_larger_graph():
+    """past brute-force size: non-induced theta34 = (A . DIM)[34] of the ESU matrix, A's row
+    from the brute-force transform on the 5-vertex patterns; a tiny cap abandons the root"""
+    A = _A_block(15, 72).astype(object)
+    for g in (graphgen.erdos_renyi(45, 0.3, 821), graphgen.config(1)):
+        dim = oracle.orbits(g.n, g.edges)[:, 15:].astype(object)
+        exp = dim.dot(A[34 - 15])
+        got, st = oracle.c5_rows(g.n, g.edges, range(g.n))
+        assert (st == 0).all() and (got.astype(object) == exp).all(), g.name
+    g = graphgen.complete(30)
+    got, st = oracle.c5_rows(g.n, g.edges, [0, 1], cap=10)
+    assert (st == 1).all() and (got == 0).all()
+
+
 def test_degree_forms_vs_noninduced_bruteforce():
     """the degree-only closed forms the GPU tests apply to every vertex of configs 2-4
     (tests/degree_forms.py) equal the non-induced brute force on random graphs"""
