@@ -582,18 +582,33 @@ def test_config5_invariants(pkg):
     Sigma DIM14 = 4 #K4 and Sigma DIM72 = 5 #K5 (golden totals from the oracle's bitmap
     clique counter), the rooted oracle's rows for sampled cheap roots, and in non-induced
     mode the degree-only closed forms on every vertex"""
+    import time
+    t0 = time.time()
+
+    def lap(what):  # shown with pytest -s / on failure: where the minutes of this test go
+        nonlocal t0
+        print(f"[config5] {what}: {time.time() - t0:.1f} s", flush=True)
+        t0 = time.time()
+
     g = graphgen.config(5)
+    lap("generate")
     out = pkg.evoke_orbits_edges(g.n, g.edges)
+    lap("GPU call, induced")
     _invariants(g, out, cliques=_golden_cliques(5, g))
+    lap("invariants")
     done = _sampled_rows(g, out, 40, 5, cap=5_000_000)
     assert done >= 3, done
+    lap("sampled rows")
     # theta3 and theta14 on every vertex (the 1.1e12 5-cliques are left to the total above)
     _clique_columns(5, g, out, 4)
+    lap("clique columns")
     del out
     # non-induced mode: the degree-only closed forms on every vertex, the hubs included
     # (as test_noninduced_degree_forms_every_vertex does for configs 2-4)
     out = pkg.evoke_orbits_edges(g.n, g.edges, induced=False)
+    lap("GPU call, non-induced")
     f = degree_forms(g.n, g.edges)
+    lap("degree forms")
     for c in DEGREE_FORM_COLUMNS:
         bad = np.flatnonzero(out[:, c] != f[c])
         assert bad.size == 0, f"config 5 theta{c}: {bad.size} rows differ, first {bad[:5].tolist()}"
