@@ -590,10 +590,18 @@ def test_config5_invariants(pkg):
         print(f"[config5] {what}: {time.time() - t0:.1f} s", flush=True)
         t0 = time.time()
 
+    def gpu_state(st):
+        import torch
+        free, total = torch.cuda.mem_get_info()
+        top = sorted(st["ms_pass"].items(), key=lambda kv: -kv[1])[:4]
+        return (f"{st['ms_total'] / 1e3:.1f} s on the GPU ({', '.join(f'{k} {v / 1e3:.1f}' for k, v in top)}); "
+                f"device free {free / 2**30:.1f} of {total / 2**30:.1f} GiB, torch reserved "
+                f"{torch.cuda.memory_reserved() / 2**30:.2f} GiB")
+
     g = graphgen.config(5)
     lap("generate")
-    out = pkg.evoke_orbits_edges(g.n, g.edges)
-    lap("GPU call, induced")
+    out, st = pkg.evoke_orbits_edges(g.n, g.edges, return_stats=True)
+    lap("GPU call, induced: " + gpu_state(st))
     _invariants(g, out, cliques=_golden_cliques(5, g))
     lap("invariants")
     done = _sampled_rows(g, out, 40, 5, cap=5_000_000)
@@ -605,8 +613,8 @@ def test_config5_invariants(pkg):
     del out
     # non-induced mode: the degree-only closed forms on every vertex, the hubs included
     # (as test_noninduced_degree_forms_every_vertex does for configs 2-4)
-    out = pkg.evoke_orbits_edges(g.n, g.edges, induced=False)
-    lap("GPU call, non-induced")
+    out, st = pkg.evoke_orbits_edges(g.n, g.edges, induced=False, return_stats=True)
+    lap("GPU call, non-induced: " + gpu_state(st))
     f = degree_forms(g.n, g.edges)
     lap("degree forms")
     for c in DEGREE_FORM_COLUMNS:
