@@ -120,6 +120,31 @@ cudaMemPool_t evoke_pool_if_any(int dev) {  // the pool if one was created (neve
 // the memsets (≈ 0.9 GB at config 2).  A call that fails leaves the buffer marked dirty and
 // the next lease zeroes it again; a call that needed more than the buffer holds got fresh
 // allocations for the rest, and the next lease grows the buffer to that size.
+// The kept buffer is worth its memory where the memsets it saves are a visible part of the
+// call (0.9 GB of a 9 ms call at config 2, ~25 GB of a 109 ms call at config 4); at config 5 a
+// call's tables pass 100 GB, zeroing them is 0.05 % of the call, and a kept buffer of that size
+// starved the next call's budgets (avail_bytes counts it as used) and had to be re-carved out
+// of a fragmented pool: the test suite's second config-5 call ran its heavy pair tier on a
+// handful of CTAs, 760 s instead of 28 s.  So the buffer never grows past a quarter of the
+// device; tables that do not fit get fresh zeroed allocations, as without a lease.
+size_t zero_pool_cap(int dev) {
+  static std::mutex mu;
+  static size_t cap[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return 0;
+  if (!cap[dev]) {
+    int cur = 0;
+    size_t freeb = 0, totalb = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess &&
+        cudaMemGetInfo(&freeb, &totalb) == cudaSuccess)
+      cap[dev] = totalb / 4;
+    else
+      cap[dev] = (size_t)16 << 30;
+    (void)cudaGetLastError();
+    (void)cudaSetDevice(cur);
+  }
+  return cap[dev];
+}
 struct ZeroPool {
   std::mutex mu;
   char* p = nullptr;
@@ -134,12 +159,13 @@ ZeroPool& zero_pool(int dev) {
 }
 struct ZeroLease {
   ZeroPool* zp = nullptr;
-  size_t used = 0, need = 0;
+  size_t used = 0, need = 0, cap = 0;
   bool ok = false;  // set when the call completed (the tables are zero again)
   void acquire(int dev, cudaStream_t st) {
     ZeroPool& z = zero_pool(dev);
     if (std::getenv("EVOKE_NO_ZERO_POOL") || !z.mu.try_lock()) return;
     zp = &z;
+    cap = zero_pool_cap(dev);
     if (z.target > z.bytes) {
       if (z.p) CK(cudaFreeAsync(z.p, st));
       z.p = nullptr;
@@ -159,6 +185,9 @@ struct ZeroLease {
       z.dirty = false;
     }
   }
+  // what is left of the leased buffer: the pool counts the whole buffer as used, but this
+  // much of it is still there for the call's tables (added to avail_bytes by the budgets)
+  size_t room() const { return (zp && zp->p && zp->bytes > used) ? zp->bytes - used : 0; }
   // zeroed region of `bytes` from the lease, or nullptr (the caller allocates)
   void* take(size_t bytes) {
     bytes = (bytes + 255) & ~(size_t)255;
@@ -176,7 +205,7 @@ struct ZeroLease {
       (void)cudaGetLastError();
       zp->dirty = true;
     }
-    if (need > zp->target) zp->target = need;
+    if (std::min(need, cap) > zp->target) zp->target = std::min(need, cap);
     zp->mu.unlock();
   }
 };
@@ -199,6 +228,14 @@ struct Arena {
     void* p = nullptr;
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
     cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, st);
+    if (e == cudaErrorMemoryAllocation) {
+      // the pool keeps every block this process ever freed (release threshold = never): hand
+      // the unused ones back to the device so that the request can be met with fresh memory
+      // whatever the cached blocks' sizes, and try once more
+      (void)cudaGetLastError();
+      if (cudaStreamSynchronize(st) == cudaSuccess && cudaMemPoolTrimTo(pool, 0) == cudaSuccess)
+        e = cudaMallocFromPoolAsync(&p, bytes, pool, st);
+    }
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       set_error("cudaMallocFromPoolAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
@@ -959,7 +996,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     // triangle-heavy graphs: sort every full list by third vertex, so the passes that need
     // only x < a (hub-local) or x > u (pair pass 2) read a prefix / suffix instead of filtering
     const int64_t N3 = 3 * ntri;
-    const size_t freeb = avail_bytes(C.dev);
+    const size_t freeb = avail_bytes(C.dev) + lease.room();
     const char* sort_env = getenv("EVOKE_SORT_FULL_MIN");  // test hook: force / disable the sort
     const int64_t sort_min = sort_env ? atoll(sort_env) : EVOKE_SORT_FULL_MIN;
     // (and only when the lists are long on average: 3 #T >= 8 m; config 4's 1.4 entries per
@@ -1194,7 +1231,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
     pair_pa = A.alloc<u64>((size_t)n * PO_STRIDE);
     CK(cudaMemsetAsync(pair_pa, 0, sizeof(u64) * (size_t)n * PO_STRIDE, C.st));
     PairOut po{pair_pa, C4e, hstar, hstar_s, hslot, hpos};
-    const size_t freeb = avail_bytes(C.dev);
+    const size_t freeb = avail_bytes(C.dev) + lease.room();
     // heavy tiers: dense per-CTA tables, as many CTAs as keep the tables L2-resident
     const char* phg_env = getenv("EVOKE_PAIR_HG");  // developer knob: heavy-source CTAs
     // heavy tiers: one CTA (a whole SM: 1024 threads x 64 registers) per source at a time.
@@ -1497,7 +1534,7 @@ void run(const Input& in, uint64_t* out, const evoke_options& o) {
                 (unsigned long long)edges_[b2], (unsigned long long)cw[b2], (unsigned long long)sw[b2],
                 (unsigned long long)cr[b2]);
     }
-    const size_t freeb = avail_bytes(C.dev);
+    const size_t freeb = avail_bytes(C.dev) + lease.room();
     // W-descending order of a hashed tier's list (heaviest endpoints first)
     auto sort_tier = [&](int t, int cnt, int32_t*& ls, u32*& rs) {
       ls = c5lists + (size_t)t * n;
