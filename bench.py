@@ -117,7 +117,7 @@ def run_cpu_oracle(cfg_graph, sub, desc, steps=1):
         oracle.orbits(cfg_graph.n, sub, threads=threads)
         times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
-    return {"value": sub.shape[0] / t, "unit": UNIT, "cores": threads, "kind": "oracle",
+    return {"value": sub.shape[0] / t, "unit": UNIT, "cores": threads, "kind": "oracle", "ms": t * 1e3,
             "sample": desc + f"; {t:.2f} s per run (plain ESU over all roots, OpenMP {threads} threads)"}
 
 
@@ -131,9 +131,10 @@ def bench_reference(args):
     sub, desc = cpu_sample(g, args.cpu_deg or CPU_DEG[args.config])
     cb = run_cpu_oracle(g, sub, desc, steps=max(1, min(args.steps, 3)))
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": f"config{args.config} CPU-oracle sample", "graph": g.name},
+            "config": {"workload": f"BASELINE configs[{args.config - 1}]: {graphgen.CONFIG_NAMES[args.config]}",
+                       "graph": g.name, "sample": desc, "timed_runs": max(1, min(args.steps, 3))},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
